@@ -1,0 +1,197 @@
+/* dpro_cuda.h -- C ABI of the B200 Replayer (libdpro_cuda.so).
+ *
+ * Drop-in boundary for the reference's replay operator API,
+ * proj/include/dpro/replay.hpp:48-91. The reference keeps its C++ signatures
+ * (replay / execution_graph / critical_path / sync_makespan / partial_replay);
+ * a thin adapter marshals GlobalDFG into the index-ordered
+ * CSR below and calls these entry points. Plain C: no exceptions, no torch or
+ * STL types, caller-owned buffers, status codes instead of throws.
+ *
+ * Index order is the reference op index (byte-lexicographic op id order,
+ * proj/src/graph.cpp:278-297); succ lists ascending (graph.cpp:290-295);
+ * dense device ids in DeviceId order (graph.hpp:57-72). Times are integers in
+ * the caller's unit (the reference's microseconds, or ns): replay only adds
+ * and compares durations, so any integer unit is exact.
+ *
+ * Status codes map onto the reference exceptions:
+ *   DPRO_MISSING_PROFILE  MissingProfileError  (replay.cpp:39-44)
+ *                         err = index of the first non-virtual op with dur<0
+ *   DPRO_CYCLE            CycleError           (replay.cpp:108-117)
+ *                         err = number of ops never scheduled
+ *   DPRO_EINVAL           dpro::Error          (e.g. sync_makespan k<1,
+ *                         replay.cpp:229-232) or a malformed CSR
+ */
+#ifndef DPRO_CUDA_H_
+#define DPRO_CUDA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DPRO_ABI_VERSION 1
+
+enum dpro_status {
+  DPRO_OK = 0,
+  DPRO_MISSING_PROFILE = 1,
+  DPRO_CYCLE = 2,
+  DPRO_EINVAL = 3,
+  DPRO_ECUDA = 4,
+  DPRO_ENOMEM = 5,
+  DPRO_EUNSUPPORTED = 6
+};
+
+enum dpro_memspace { DPRO_HOST = 0, DPRO_DEVICE = 1 };
+
+/* op flag bits (dpro::OpKind, proj/include/dpro/graph.hpp:30-50) */
+#define DPRO_FLAG_VIRTUAL 0x1u /* kVirtualIn / kVirtualOut          */
+#define DPRO_FLAG_COMM 0x2u    /* kSend / kRecv (is_communication) */
+
+/* One candidate data flow graph (GlobalDFG, graph.hpp:110-160) as CSR. */
+typedef struct dpro_csr {
+  uint32_t n_ops;
+  uint32_t n_edges;
+  uint32_t n_devices;         /* dense device ids are < n_devices         */
+  int32_t dur_bits;           /* 64: int64_t dur (dpro::Us), 32: int32_t  */
+  const void* dur;            /* [n_ops] op duration (virtual: ignored)   */
+  const uint16_t* dev;        /* [n_ops] dense device id                  */
+  const uint8_t* flags;       /* [n_ops] DPRO_FLAG_*                      */
+  const uint32_t* succ_off;   /* [n_ops+1]                                */
+  const uint32_t* succ;       /* [n_edges] ascending within each op       */
+  const uint32_t* indeg;      /* [n_ops] |preds|, or NULL (computed)      */
+} dpro_csr;
+
+/* ClusterSpec (proj/include/dpro/cluster.hpp:43-65). */
+typedef struct dpro_cluster_desc {
+  int32_t scheme;                /* 0 ring all-reduce, 1 parameter server */
+  int32_t n_nodes;
+  const char* const* node_ids;   /* [n_nodes]                             */
+  const int32_t* node_role;      /* [n_nodes] 0 worker, 1 ps              */
+  int32_t n_links;
+  const int32_t* link_src;       /* [n_links] node index                  */
+  const int32_t* link_dst;
+  const double* link_bw;         /* bytes per time unit                   */
+  const double* link_lat;        /* time units                            */
+  int32_t n_ring;                /* 0: workers in byte-lexicographic order */
+  const int32_t* ring_order;     /* [n_ring] node indices                 */
+  int32_t chunks_per_tensor;     /* 0: ring size                          */
+} dpro_cluster_desc;
+
+/* ------------------------------------------------------------------------
+ * Engine context: one per GPU; used by one host thread at a time.
+ * --------------------------------------------------------------------- */
+typedef struct dpro_ctx dpro_ctx;
+typedef struct dpro_batch dpro_batch;
+
+int dpro_cuda_abi_version(void);
+dpro_ctx* dpro_cuda_create(int device);
+void dpro_cuda_destroy(dpro_ctx* ctx);
+/* cudaStream_t the engine launches on (NULL: the legacy default stream). */
+int dpro_cuda_set_stream(dpro_ctx* ctx, void* stream);
+const char* dpro_cuda_last_error(dpro_ctx* ctx);
+
+/* ------------------------------------------------------------------------
+ * Batched replay (replaces dpro::replay, replay.cpp:37-134, for B graphs).
+ * --------------------------------------------------------------------- */
+
+/* Registers a batch. memspace DPRO_HOST: the CSR arrays are uploaded into
+ * one engine-owned device arena (dur packed to int32 when it fits).
+ * DPRO_DEVICE: the arrays are used in place (must stay alive). */
+dpro_batch* dpro_cuda_batch_create(dpro_ctx* ctx, const dpro_csr* cands,
+                                   int32_t n_cands, int32_t memspace);
+void dpro_cuda_batch_destroy(dpro_ctx* ctx, dpro_batch* b);
+/* Replays every candidate on the GPU (stream-ordered, asynchronous).
+ * want_schedule=0 skips the per-op start/end writes (makespan only). */
+int dpro_cuda_batch_replay(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule);
+/* Device pointers of the batch results (valid until the next replay):
+ * makespan/err [n_cands] int64, status [n_cands] int32, start/end
+ * concatenated per candidate in batch order ([sum n_ops] int64). */
+int dpro_cuda_batch_device_results(dpro_batch* b, int64_t** makespan,
+                                   int32_t** status, int64_t** err,
+                                   int64_t** start, int64_t** end);
+/* Copies results to host buffers (any may be NULL); synchronizes. */
+int dpro_cuda_batch_results(dpro_ctx* ctx, dpro_batch* b, int64_t* makespan,
+                            int32_t* status, int64_t* err, int64_t* start,
+                            int64_t* end);
+/* Per-device dispatch order of candidate `cand` after a replay
+ * (ReplayResult::device_timelines): order[dev_off[d]..dev_off[d+1]) are the
+ * op indices device d ran, in order; busy[d] = summed dur (utilization
+ * numerator, replay.cpp:124-132). Host buffers: order [n_ops],
+ * dev_off [n_devices+1], busy [n_devices]; any may be NULL. */
+int dpro_cuda_batch_timelines(dpro_ctx* ctx, dpro_batch* b, int32_t cand,
+                              uint32_t* order, uint32_t* dev_off,
+                              int64_t* busy);
+/* scheduled[i] = 1 for ops the replay scheduled (host buffer [n_ops]); the
+ * ids with 0 form CycleError::cycle (replay.cpp:108-117). */
+int dpro_cuda_batch_scheduled(dpro_ctx* ctx, dpro_batch* b, int32_t cand,
+                              uint8_t* scheduled);
+/* critical_path(execution_graph(g, r), r) (replay.cpp:136-226) for every
+ * candidate of the last replay. paths: concatenated per candidate with
+ * capacity n_ops each (same offsets as start/end); path_len [n_cands].
+ * Host buffers. */
+int dpro_cuda_batch_critical_paths(dpro_ctx* ctx, dpro_batch* b,
+                                   uint32_t* paths, int64_t* path_len);
+
+/* One-shot convenience with the reference-style signature: create, replay,
+ * copy back (host outputs), destroy. start/end may be NULL. */
+int dpro_cuda_replay_batch(dpro_ctx* ctx, const dpro_csr* cands,
+                           int32_t n_cands, int32_t memspace,
+                           int64_t* makespan, int64_t* start, int64_t* end,
+                           int32_t* status, int64_t* err);
+
+/* ------------------------------------------------------------------------
+ * t_sync grid (replaces sync_makespan, replay.cpp:228-246, and the memoized
+ * SearchCtx::sync grid of optimize.cpp:562-576,1170-1194): out[i] =
+ * makespan of syncing bytes[i] as k[i] balanced partitions under the
+ * cluster's scheme. status[i] = DPRO_EINVAL when k[i] < 1.
+ * --------------------------------------------------------------------- */
+int dpro_cuda_tsync_grid(dpro_ctx* ctx, const dpro_cluster_desc* cluster,
+                         const int64_t* bytes, const int32_t* k, int32_t n,
+                         int64_t* out, int32_t* status);
+
+/* ------------------------------------------------------------------------
+ * Host-side CSR graph construction (candidate generation; no GPU needed).
+ * Builds the same graph the reference ingest/rewrite path builds
+ * (ingest.cpp:187-454, optimize.cpp:459-492) directly in index order.
+ * --------------------------------------------------------------------- */
+typedef struct dpro_graph dpro_graph;
+
+/* Layered data-parallel model of proj/src/synth.cpp:200-217: FW chain,
+ * mirrored BW chain producing tensor g<i> per layer, UPDATE.l<i> gated on
+ * OUT(g<i>). */
+typedef struct dpro_layered_model {
+  int32_t layers;
+  const int64_t* fw_dur;        /* [layers] */
+  const int64_t* bw_dur;        /* [layers] */
+  const int64_t* tensor_bytes;  /* [layers] */
+  int64_t update_dur;
+} dpro_layered_model;
+
+/* part_k: [layers] partition count per tensor (NULL: all 1), as applied by
+ * apply_tensor_partition (optimize.cpp:459-492). */
+dpro_graph* dpro_graph_layered(const dpro_layered_model* model,
+                               const dpro_cluster_desc* cluster,
+                               const int32_t* part_k, int32_t* status);
+/* n graphs with part_k[n*layers], built on `threads` host threads. */
+int dpro_graph_layered_batch(const dpro_layered_model* model,
+                             const dpro_cluster_desc* cluster,
+                             const int32_t* part_k, int32_t n,
+                             int32_t threads, dpro_graph** out);
+/* Comm-only graph of sync_makespan(cluster, bytes, k). */
+dpro_graph* dpro_graph_tsync(const dpro_cluster_desc* cluster, int64_t bytes,
+                             int32_t k, int32_t* status);
+/* Host CSR view (pointers owned by the graph; dur_bits = 64). */
+int dpro_graph_csr(const dpro_graph* g, dpro_csr* out);
+const char* dpro_graph_op_id(const dpro_graph* g, uint32_t i);
+int32_t dpro_graph_op_kind(const dpro_graph* g, uint32_t i);
+const char* dpro_graph_device_str(const dpro_graph* g, uint32_t d);
+void dpro_graph_free(dpro_graph* g);
+const char* dpro_graph_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DPRO_CUDA_H_ */

@@ -1,0 +1,23 @@
+"""B200-native dPRO Replayer (arxiv 2205.02473): batched exact replay of
+candidate data-flow graphs on sm_100a, behind the reference's replay API.
+
+Product path: libdpro_cuda.so (csrc/, C ABI include/dpro_cuda.h). There is
+no CPU fallback -- importing this package fails if the library is missing.
+"""
+from . import _native  # noqa: F401  (fails loudly without libdpro_cuda.so)
+from .engine import Batch, Csr, Engine, default_engine
+from .errors import CycleError, EngineError, Error, LookupError_, MissingProfileError
+from .graph import (ClusterSpec, DeviceId, DeviceKind, GlobalDFG, GraphBuilder, LinkSpec,
+                    NodeSpec, Op, OpKind, TensorUnit, comp, round_us, synth_cluster)
+from .replay import (CriticalPath, PathEntry, PathRun, ReplayResult, ScheduleEntry,
+                     critical_path, execution_graph, partial_replay, replay, replay_many,
+                     sync_makespan, sync_makespan_grid)
+
+__all__ = [
+    "Batch", "Csr", "Engine", "default_engine", "CycleError", "EngineError", "Error",
+    "LookupError_", "MissingProfileError", "ClusterSpec", "DeviceId", "DeviceKind",
+    "GlobalDFG", "GraphBuilder", "LinkSpec", "NodeSpec", "Op", "OpKind", "TensorUnit",
+    "comp", "round_us", "synth_cluster", "CriticalPath", "PathEntry", "PathRun",
+    "ReplayResult", "ScheduleEntry", "critical_path", "execution_graph", "partial_replay",
+    "replay", "replay_many", "sync_makespan", "sync_makespan_grid",
+]

@@ -1,0 +1,447 @@
+// Host-side candidate-graph construction straight into index-ordered CSR.
+//
+// Builds the graphs the reference builds through string-keyed GraphBuilder
+// copies (proj/src/graph.cpp:199-297), without the per-rewrite map copies:
+//   * the layered data-parallel model of proj/src/synth.cpp:200-245 as
+//     ingested by proj/src/ingest.cpp:187-266,386-454 (local DFGs + splice);
+//   * ring all-reduce / PS expansion, proj/src/ingest.cpp:37-67,268-384;
+//   * tensor partition re-expansion, proj/src/optimize.cpp:459-492;
+//   * the comm-only t_sync graph of proj/src/replay.cpp:228-246.
+// Op ids are generated with the reference naming so the byte-lexicographic
+// sort reproduces the reference op index (the replay tie-break order).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <utility>
+#include <vector>
+
+#include "dpro_cuda.h"
+
+namespace {
+
+thread_local std::string g_gen_err;
+
+// Reference OpKind enumerator order (graph.hpp:30-38).
+enum Kind : int32_t { kFw = 0, kBw, kUpdate, kSend, kRecv, kVin, kVout };
+
+// round half to even, proj/include/dpro/time_util.hpp:28-35.
+int64_t round_half_even(double value) {
+  const double f = std::floor(value);
+  const double frac = value - f;
+  const int64_t lo = static_cast<int64_t>(f);
+  if (frac > 0.5) return lo + 1;
+  if (frac < 0.5) return lo;
+  return (lo % 2 == 0) ? lo : lo + 1;
+}
+
+// FNV-1a, proj/src/graph.cpp:57-64 (PS placement hash).
+uint64_t fnv1a(const std::string& s) {
+  uint64_t h = 1469598103934665603ULL;
+  for (unsigned char c : s) {
+    h ^= c;
+    h *= 1099511628211ULL;
+  }
+  return h;
+}
+
+struct Cluster {
+  int scheme = 0;
+  std::vector<std::string> nodes;
+  std::vector<int> role;
+  std::map<std::pair<int, int>, std::pair<double, double>> link;  // first wins
+  std::vector<int> ring;  // node indices
+  std::vector<int> sorted_workers;
+  std::vector<int> sorted_ps;
+  int chunks = 0;
+
+  explicit Cluster(const dpro_cluster_desc& d) {
+    scheme = d.scheme;
+    for (int i = 0; i < d.n_nodes; ++i) {
+      nodes.emplace_back(d.node_ids[i]);
+      role.push_back(d.node_role[i]);
+    }
+    for (int l = 0; l < d.n_links; ++l)
+      link.emplace(std::make_pair(d.link_src[l], d.link_dst[l]),
+                   std::make_pair(d.link_bw[l], d.link_lat[l]));
+    for (int i = 0; i < d.n_nodes; ++i) {
+      if (role[i] == 0) sorted_workers.push_back(i);
+      if (role[i] == 1) sorted_ps.push_back(i);
+    }
+    auto by_name = [&](int a, int b) { return nodes[a] < nodes[b]; };
+    std::sort(sorted_workers.begin(), sorted_workers.end(), by_name);
+    std::sort(sorted_ps.begin(), sorted_ps.end(), by_name);
+    if (d.n_ring > 0)
+      ring.assign(d.ring_order, d.ring_order + d.n_ring);
+    else
+      ring = sorted_workers;  // ingest.cpp:63-67,271-272
+    chunks = d.chunks_per_tensor;
+  }
+
+  // hop_dur, ingest.cpp:37-48
+  int64_t hop(int64_t bytes, int src, int dst) const {
+    double bw = 1.0, lat = 0.0;
+    auto it = link.find({src, dst});
+    if (it != link.end()) {
+      bw = it->second.first;
+      lat = it->second.second;
+    }
+    return round_half_even(static_cast<double>(bytes) / bw + lat);
+  }
+};
+
+struct Gen {
+  struct Op {
+    std::string id;
+    int32_t kind;
+    uint32_t devkey;
+    int64_t dur;
+  };
+  std::vector<Op> ops;
+  std::vector<std::pair<uint32_t, uint32_t>> edges;  // creation indices
+  std::map<std::pair<int, std::string>, uint32_t> devkeys;  // (kind, str)
+
+  uint32_t device(int dkind, const std::string& node, const std::string& peer) {
+    // DeviceId order: kind (compute < link), node, peer (graph.hpp:57-72).
+    // Encode as (kind, node + '\0' + peer) which sorts identically.
+    std::string key = node;
+    key.push_back('\0');
+    key += peer;
+    auto it = devkeys.emplace(std::make_pair(dkind, key),
+                              static_cast<uint32_t>(devkeys.size()));
+    return it.first->second;
+  }
+  uint32_t add(std::string id, int32_t kind, uint32_t dev, int64_t dur) {
+    ops.push_back({std::move(id), kind, dev, dur});
+    return static_cast<uint32_t>(ops.size() - 1);
+  }
+  void edge(uint32_t a, uint32_t b) { edges.emplace_back(a, b); }
+};
+
+// One tensor unit's comm topology spliced onto per-node IN/OUT ops
+// (ingest.cpp:268-384 expansion + assemble_global_dfg 404-441 splice).
+// in_op/out_op: node index -> creation index (UINT32_MAX when absent).
+void expand_unit(Gen& g, const Cluster& c, const std::string& unit,
+                 int64_t bytes, const std::vector<uint32_t>* in_op,
+                 const std::vector<uint32_t>* out_op) {
+  auto link_dev = [&](int s, int d) {
+    return g.device(1, c.nodes[s], c.nodes[d]);
+  };
+  auto need = [&](const std::vector<uint32_t>* v, int node) -> uint32_t {
+    if (!v) return UINT32_MAX;
+    uint32_t x = (*v)[node];
+    if (x == UINT32_MAX)
+      throw std::runtime_error("tensor " + unit + " attaches to node " +
+                               c.nodes[node] + " which has no IN/OUT op");
+    return x;
+  };
+  if (c.scheme == 0) {
+    const int n = static_cast<int>(c.ring.size());
+    if (n < 2)
+      throw std::runtime_error("degenerate ring: allreduce needs at least 2 workers");
+    const int chunks = c.chunks > 0 ? c.chunks : n;
+    const int steps = 2 * (n - 1);
+    const int64_t base = bytes / chunks, rem = bytes % chunks;
+    for (int ch = 0; ch < chunks; ++ch) {
+      const int64_t cb = base + (ch < rem ? 1 : 0);
+      uint32_t prev_recv = UINT32_MAX;
+      for (int s = 0; s < steps; ++s) {
+        const int src = c.ring[(ch + s) % n];
+        const int dst = c.ring[(ch + s + 1) % n];
+        const std::string txn = unit + "#c" + std::to_string(ch) + "#s" +
+                                std::to_string(s) + "#" + c.nodes[src] + "#" +
+                                c.nodes[dst];
+        const uint32_t dv = link_dev(src, dst);
+        const uint32_t snd = g.add("SEND." + txn, kSend, dv, 0);
+        const uint32_t rcv = g.add("RECV." + txn, kRecv, dv, c.hop(cb, src, dst));
+        g.edge(snd, rcv);
+        if (s == 0) {
+          const uint32_t in = need(in_op, src);
+          if (in != UINT32_MAX) g.edge(in, snd);
+        } else {
+          g.edge(prev_recv, snd);
+        }
+        if (s >= n - 2) {
+          const uint32_t out = need(out_op, dst);
+          if (out != UINT32_MAX) g.edge(rcv, out);
+        }
+        prev_recv = rcv;
+      }
+    }
+  } else {
+    if (c.sorted_ps.empty())
+      throw std::runtime_error("parameter-server scheme requires at least one ps node");
+    if (c.sorted_workers.empty())
+      throw std::runtime_error("parameter-server scheme requires at least one worker");
+    const int server = c.sorted_ps[fnv1a(unit) % c.sorted_ps.size()];
+    std::vector<uint32_t> push_recvs, pull_sends;
+    for (int w : c.sorted_workers) {
+      const std::string push = unit + "#push#" + c.nodes[w] + "#" + c.nodes[server];
+      const uint32_t dpush = link_dev(w, server);
+      const uint32_t ps = g.add("SEND." + push, kSend, dpush, 0);
+      const uint32_t pr = g.add("RECV." + push, kRecv, dpush, c.hop(bytes, w, server));
+      g.edge(ps, pr);
+      const uint32_t in = need(in_op, w);
+      if (in != UINT32_MAX) g.edge(in, ps);
+      push_recvs.push_back(pr);
+      const std::string pull = unit + "#pull#" + c.nodes[server] + "#" + c.nodes[w];
+      const uint32_t dpull = link_dev(server, w);
+      const uint32_t ls = g.add("SEND." + pull, kSend, dpull, 0);
+      const uint32_t lr = g.add("RECV." + pull, kRecv, dpull, c.hop(bytes, server, w));
+      g.edge(ls, lr);
+      const uint32_t out = need(out_op, w);
+      if (out != UINT32_MAX) g.edge(lr, out);
+      pull_sends.push_back(ls);
+    }
+    for (uint32_t pull : pull_sends)
+      for (uint32_t push : push_recvs) g.edge(push, pull);
+  }
+}
+
+}  // namespace
+
+struct dpro_graph {
+  std::vector<std::string> ids;
+  std::vector<int32_t> kind;
+  std::vector<int64_t> dur;
+  std::vector<uint16_t> dev;
+  std::vector<uint8_t> flags;
+  std::vector<uint32_t> succ_off, succ, indeg;
+  std::vector<std::string> device_strs;
+};
+
+namespace {
+
+// Sort ops by id (std::map order in GraphBuilder::build), dense device ids in
+// DeviceId order, ascending deduplicated succ lists (std::set of edges).
+dpro_graph* finalize(Gen& g) {
+  const uint32_t n = static_cast<uint32_t>(g.ops.size());
+  std::vector<uint32_t> order(n);
+  std::iota(order.begin(), order.end(), 0u);
+  std::sort(order.begin(), order.end(),
+            [&](uint32_t a, uint32_t b) { return g.ops[a].id < g.ops[b].id; });
+  for (uint32_t i = 1; i < n; ++i)
+    if (g.ops[order[i]].id == g.ops[order[i - 1]].id)
+      throw std::runtime_error("duplicate op id '" + g.ops[order[i]].id + "'");
+  std::vector<uint32_t> rank(n);
+  for (uint32_t i = 0; i < n; ++i) rank[order[i]] = i;
+
+  std::vector<uint32_t> dev_rank(g.devkeys.size());
+  auto* out = new dpro_graph;
+  {
+    uint32_t k = 0;
+    for (const auto& [key, id] : g.devkeys) {  // map order == DeviceId order
+      dev_rank[id] = k++;
+      const std::string& s = key.second;
+      const auto z = s.find('\0');
+      out->device_strs.push_back(key.first == 0 ? s.substr(0, z)
+                                                : s.substr(0, z) + ">" + s.substr(z + 1));
+    }
+  }
+  if (g.devkeys.size() > 65535) {
+    delete out;
+    throw std::runtime_error("more than 65535 devices");
+  }
+  out->ids.resize(n);
+  out->kind.resize(n);
+  out->dur.resize(n);
+  out->dev.resize(n);
+  out->flags.resize(n);
+  for (uint32_t i = 0; i < n; ++i) {
+    auto& op = g.ops[order[i]];
+    out->ids[i] = std::move(op.id);
+    out->kind[i] = op.kind;
+    out->dur[i] = op.dur;
+    out->dev[i] = static_cast<uint16_t>(dev_rank[op.devkey]);
+    out->flags[i] = static_cast<uint8_t>(
+        (op.kind == kVin || op.kind == kVout ? DPRO_FLAG_VIRTUAL : 0u) |
+        (op.kind == kSend || op.kind == kRecv ? DPRO_FLAG_COMM : 0u));
+  }
+  for (auto& e : g.edges) e = {rank[e.first], rank[e.second]};
+  std::sort(g.edges.begin(), g.edges.end());
+  g.edges.erase(std::unique(g.edges.begin(), g.edges.end()), g.edges.end());
+  out->succ_off.assign(n + 1, 0);
+  out->indeg.assign(n, 0);
+  out->succ.resize(g.edges.size());
+  for (size_t e = 0; e < g.edges.size(); ++e) {
+    out->succ_off[g.edges[e].first + 1]++;
+    out->indeg[g.edges[e].second]++;
+    out->succ[e] = g.edges[e].second;
+  }
+  for (uint32_t i = 0; i < n; ++i) out->succ_off[i + 1] += out->succ_off[i];
+  return out;
+}
+
+dpro_graph* build_layered(const dpro_layered_model& m, const Cluster& c,
+                          const int32_t* part_k) {
+  Gen g;
+  const int L = m.layers;
+  if (L < 1) throw std::runtime_error("synthetic model needs at least one layer");
+  const int N = static_cast<int>(c.nodes.size());
+  std::vector<int> workers;
+  for (int i = 0; i < N; ++i)
+    if (c.role[i] == 0) workers.push_back(i);
+  // per tensor layer i: IN/OUT creation index per node
+  std::vector<std::vector<uint32_t>> in_op(L, std::vector<uint32_t>(N, UINT32_MAX));
+  std::vector<std::vector<uint32_t>> out_op(L, std::vector<uint32_t>(N, UINT32_MAX));
+  for (int w : workers) {
+    const std::string& node = c.nodes[w];
+    const uint32_t dv = g.device(0, node, "");
+    std::vector<uint32_t> fw(L), bw(L), up(L);
+    for (int i = 0; i < L; ++i) {
+      const std::string li = std::to_string(i);
+      fw[i] = g.add(node + "->FW.l" + li, kFw, dv, m.fw_dur[i]);
+      bw[i] = g.add(node + "->BW.l" + li, kBw, dv, m.bw_dur[i]);
+      up[i] = g.add(node + "->UPDATE.l" + li, kUpdate, dv, m.update_dur);
+      in_op[i][w] = g.add(node + "->IN.g" + li, kVin, dv, 0);
+      out_op[i][w] = g.add(node + "->OUT.g" + li, kVout, dv, 0);
+    }
+    // synth.cpp:200-212 deps, resolved by build_local_dfg (ingest.cpp:243-265)
+    for (int i = 0; i < L; ++i) {
+      if (i > 0) g.edge(fw[i - 1], fw[i]);
+      if (i + 1 < L) g.edge(bw[i + 1], bw[i]);
+      g.edge(fw[i], bw[i]);
+      g.edge(bw[i], in_op[i][w]);   // producer feeds IN (ingest.cpp:242)
+      g.edge(out_op[i][w], up[i]);  // OUT(g_i) -> UPDATE.l_i
+    }
+  }
+  for (int i = 0; i < L; ++i) {
+    const std::string t = "g" + std::to_string(i);
+    const int64_t bytes = m.tensor_bytes[i];
+    const int k = part_k ? part_k[i] : 1;
+    if (k < 1)
+      throw std::runtime_error("partition count must be >= 1, got " + std::to_string(k));
+    if (k > bytes)
+      throw std::runtime_error("cannot split " + std::to_string(bytes) +
+                               " bytes of " + t + " into " + std::to_string(k) +
+                               " partitions");
+    const int64_t base = bytes / k, rem = bytes % k;
+    for (int p = 0; p < k; ++p) {
+      const std::string unit = k == 1 ? t : t + "#p" + std::to_string(p);
+      expand_unit(g, c, unit, base + (p < rem ? 1 : 0), &in_op[i], &out_op[i]);
+    }
+  }
+  return finalize(g);
+}
+
+dpro_graph* build_tsync(const Cluster& c, int64_t bytes, int k) {
+  if (k < 1)
+    throw std::invalid_argument("sync_makespan: partition count must be >= 1, got " +
+                                std::to_string(k));
+  Gen g;
+  const int64_t base = bytes / k, rem = bytes % k;
+  for (int i = 0; i < k; ++i) {
+    const std::string unit = k == 1 ? "tsync" : "tsync#p" + std::to_string(i);
+    expand_unit(g, c, unit, base + (i < rem ? 1 : 0), nullptr, nullptr);
+  }
+  return finalize(g);
+}
+
+template <typename F>
+dpro_graph* guarded(F&& f, int32_t* status) {
+  try {
+    dpro_graph* g = f();
+    if (status) *status = DPRO_OK;
+    return g;
+  } catch (const std::bad_alloc&) {
+    g_gen_err = "out of host memory";
+    if (status) *status = DPRO_ENOMEM;
+  } catch (const std::exception& e) {
+    g_gen_err = e.what();
+    if (status) *status = DPRO_EINVAL;
+  }
+  return nullptr;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* dpro_graph_last_error(void) { return g_gen_err.c_str(); }
+
+dpro_graph* dpro_graph_layered(const dpro_layered_model* model,
+                               const dpro_cluster_desc* cluster,
+                               const int32_t* part_k, int32_t* status) {
+  return guarded([&] { return build_layered(*model, Cluster(*cluster), part_k); },
+                 status);
+}
+
+int dpro_graph_layered_batch(const dpro_layered_model* model,
+                             const dpro_cluster_desc* cluster,
+                             const int32_t* part_k, int32_t n, int32_t threads,
+                             dpro_graph** out) {
+  const Cluster c(*cluster);
+  if (threads < 1) threads = 1;
+  std::vector<int32_t> st(n, DPRO_OK);
+  std::vector<std::string> errs(threads);
+  auto work = [&](int tid) {
+    for (int i = tid; i < n; i += threads) {
+      try {
+        out[i] = build_layered(*model, c, part_k ? part_k + (size_t)i * model->layers : nullptr);
+      } catch (const std::exception& e) {
+        out[i] = nullptr;
+        st[i] = DPRO_EINVAL;
+        errs[tid] = e.what();
+      }
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < threads; ++t) pool.emplace_back(work, t);
+  work(0);
+  for (auto& th : pool) th.join();
+  for (int i = 0; i < n; ++i)
+    if (st[i] != DPRO_OK) {
+      for (auto& e : errs)
+        if (!e.empty()) g_gen_err = e;
+      return st[i];
+    }
+  return DPRO_OK;
+}
+
+dpro_graph* dpro_graph_tsync(const dpro_cluster_desc* cluster, int64_t bytes,
+                             int32_t k, int32_t* status) {
+  return guarded([&] { return build_tsync(Cluster(*cluster), bytes, k); }, status);
+}
+
+int dpro_graph_csr(const dpro_graph* g, dpro_csr* out) {
+  if (!g || !out) return DPRO_EINVAL;
+  out->n_ops = static_cast<uint32_t>(g->ids.size());
+  out->n_edges = static_cast<uint32_t>(g->succ.size());
+  out->n_devices = static_cast<uint32_t>(g->device_strs.size());
+  out->dur_bits = 64;
+  out->dur = g->dur.data();
+  out->dev = g->dev.data();
+  out->flags = g->flags.data();
+  out->succ_off = g->succ_off.data();
+  out->succ = g->succ.data();
+  out->indeg = g->indeg.data();
+  return DPRO_OK;
+}
+
+const char* dpro_graph_op_id(const dpro_graph* g, uint32_t i) {
+  return g->ids.at(i).c_str();
+}
+int32_t dpro_graph_op_kind(const dpro_graph* g, uint32_t i) { return g->kind.at(i); }
+const char* dpro_graph_device_str(const dpro_graph* g, uint32_t d) {
+  return g->device_strs.at(d).c_str();
+}
+void dpro_graph_free(dpro_graph* g) { delete g; }
+
+}  // extern "C"
+
+// Internal entry for the engine's t_sync grid (engine.cu).
+dpro_graph* dpro_internal_tsync_graph(const dpro_cluster_desc* cluster,
+                                      int64_t bytes, int32_t k,
+                                      std::string* err) {
+  try {
+    return build_tsync(Cluster(*cluster), bytes, k);
+  } catch (const std::exception& e) {
+    if (err) *err = e.what();
+    return nullptr;
+  }
+}

@@ -1,0 +1,540 @@
+// libdpro_cuda.so: engine context, batch arenas, launches and the C ABI of
+// include/dpro_cuda.h. Host code is plain C++ over the CUDA runtime; the
+// kernels live in replay_kernel.cuh (K1) and critical_path_kernel.cuh (K3).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "critical_path_kernel.cuh"
+#include "dpro_cuda.h"
+#include "replay_kernel.cuh"
+
+struct dpro_graph;
+dpro_graph* dpro_internal_tsync_graph(const dpro_cluster_desc* cluster,
+                                      int64_t bytes, int32_t k,
+                                      std::string* err);
+
+namespace {
+
+using dpro_k::Cand;
+using dpro_k::CpScratch;
+using dpro_k::DevSt;
+using dpro_k::Outs;
+using dpro_k::Scratch;
+
+constexpr int kWarpsPerBlock = 4;
+constexpr size_t kSmemHeader = 16 * 8;
+
+size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    cudaError_t e = cudaMalloc(&p, std::max<size_t>(bytes, 256));
+    if (e == cudaSuccess) cap = std::max<size_t>(bytes, 256);
+    return e;
+  }
+  template <typename T>
+  T* as(size_t byte_off = 0) const {
+    return reinterpret_cast<T*>(static_cast<char*>(p) + byte_off);
+  }
+};
+
+struct HostPinned {
+  void* p = nullptr;
+  size_t cap = 0;
+  ~HostPinned() {
+    if (p) cudaFreeHost(p);
+  }
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+    cudaError_t e = cudaMallocHost(&p, bytes);
+    if (e == cudaSuccess) cap = bytes;
+    return e;
+  }
+};
+
+}  // namespace
+
+struct dpro_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int sm_count = 148;
+  size_t smem_optin = 0;
+  std::string err;
+  HostPinned staging;
+};
+
+struct dpro_batch {
+  int32_t n = 0;
+  int32_t memspace = DPRO_HOST;
+  std::vector<Cand> hc;              // host copy of descriptors
+  std::vector<uint32_t> n_ops, n_dev, n_edges;
+  unsigned long long sum_n = 0, sum_d = 0, sum_dof = 0, sum_e = 0;
+  uint32_t max_d = 0;
+  DevBuf arena;   // uploaded CSR (host memspace)
+  DevBuf desc;    // Cand[n]
+  DevBuf scratch; // op / device scratch
+  DevBuf outs;    // results
+  DevBuf work;    // work counter
+  DevBuf cp;      // critical-path scratch
+  Scratch S{};
+  Outs O{};
+  bool replayed = false;
+  bool with_schedule = false;
+};
+
+namespace {
+
+int set_err(dpro_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  return code;
+}
+
+#define CU(call)                                                          \
+  do {                                                                    \
+    cudaError_t e_ = (call);                                              \
+    if (e_ != cudaSuccess)                                                \
+      return set_err(ctx, e_ == cudaErrorMemoryAllocation ? DPRO_ENOMEM   \
+                                                          : DPRO_ECUDA,   \
+                     std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+bool fits_i32(const int64_t* d, uint32_t n) {
+  for (uint32_t i = 0; i < n; ++i)
+    if (d[i] > INT32_MAX || d[i] < INT32_MIN) return false;
+  return true;
+}
+
+// Uploads host CSR arrays into one device arena via a pinned staging buffer
+// (packed on `threads` host threads, one H2D copy). dur -> int32 when exact.
+int upload_host(dpro_ctx* ctx, dpro_batch* b, const dpro_csr* cands) {
+  const int32_t n = b->n;
+  std::vector<size_t> off(n + 1, 0);
+  std::vector<uint8_t> d32(n, 0);
+  for (int32_t i = 0; i < n; ++i) {
+    const dpro_csr& c = cands[i];
+    const bool narrow = c.dur_bits == 32 || c.n_ops == 0 ||
+                        fits_i32(static_cast<const int64_t*>(c.dur), c.n_ops);
+    d32[i] = narrow;
+    size_t s = align16(size_t(c.n_ops) * (narrow ? 4 : 8));
+    s += align16(size_t(c.n_ops) * 2);
+    s += align16(size_t(c.n_ops));
+    s += align16(size_t(c.n_ops + 1) * 4);
+    s += align16(size_t(c.n_edges) * 4);
+    s += align16(size_t(c.n_ops) * 4);
+    off[i + 1] = off[i] + s;
+  }
+  const size_t total = off[n];
+  // the staging buffer may still feed an earlier in-flight upload
+  CU(cudaStreamSynchronize(ctx->stream));
+  CU(b->arena.ensure(total));
+  CU(ctx->staging.ensure(total));
+  char* stage = static_cast<char*>(ctx->staging.p);
+  auto pack = [&](int tid, int nt) {
+    for (int32_t i = tid; i < n; i += nt) {
+      const dpro_csr& c = cands[i];
+      char* p = stage + off[i];
+      size_t o = 0;
+      Cand& hc = b->hc[i];
+      const size_t base = off[i];
+      if (d32[i]) {
+        int32_t* dd = reinterpret_cast<int32_t*>(p + o);
+        if (c.n_ops == 0) {
+        } else if (c.dur_bits == 32)
+          std::memcpy(dd, c.dur, size_t(c.n_ops) * 4);
+        else
+          for (uint32_t k = 0; k < c.n_ops; ++k)
+            dd[k] = static_cast<int32_t>(static_cast<const int64_t*>(c.dur)[k]);
+        hc.dur64 = 0;
+      } else {
+        std::memcpy(p + o, c.dur, size_t(c.n_ops) * 8);
+        hc.dur64 = 1;
+      }
+      hc.dur = b->arena.as<void>(base + o);
+      o += align16(size_t(c.n_ops) * (d32[i] ? 4 : 8));
+      if (c.n_ops) std::memcpy(p + o, c.dev, size_t(c.n_ops) * 2);
+      hc.dev = b->arena.as<uint16_t>(base + o);
+      o += align16(size_t(c.n_ops) * 2);
+      if (c.n_ops) std::memcpy(p + o, c.flags, c.n_ops);
+      hc.flags = b->arena.as<uint8_t>(base + o);
+      o += align16(c.n_ops);
+      if (c.succ_off)
+        std::memcpy(p + o, c.succ_off, size_t(c.n_ops + 1) * 4);
+      else
+        std::memset(p + o, 0, 4);
+      hc.succ_off = b->arena.as<uint32_t>(base + o);
+      o += align16(size_t(c.n_ops + 1) * 4);
+      if (c.n_edges) std::memcpy(p + o, c.succ, size_t(c.n_edges) * 4);
+      hc.succ = b->arena.as<uint32_t>(base + o);
+      o += align16(size_t(c.n_edges) * 4);
+      uint32_t* ind = reinterpret_cast<uint32_t*>(p + o);
+      if (c.indeg) {
+        if (c.n_ops) std::memcpy(ind, c.indeg, size_t(c.n_ops) * 4);
+      } else {
+        std::memset(ind, 0, size_t(c.n_ops) * 4);
+        for (uint32_t e = 0; e < c.n_edges; ++e) ind[c.succ[e]]++;
+      }
+      hc.indeg = b->arena.as<uint32_t>(base + o);
+    }
+  };
+  const int nt = std::max(1, std::min<int>(n, (int)std::thread::hardware_concurrency()));
+  if (total > (size_t(8) << 20) && nt > 1) {
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t) pool.emplace_back(pack, t, nt);
+    pack(0, nt);
+    for (auto& th : pool) th.join();
+  } else {
+    pack(0, 1);
+  }
+  CU(cudaMemcpyAsync(b->arena.p, stage, total, cudaMemcpyHostToDevice, ctx->stream));
+  return DPRO_OK;
+}
+
+int build_batch(dpro_ctx* ctx, dpro_batch* b, const dpro_csr* cands) {
+  const int32_t n = b->n;
+  b->hc.resize(n);
+  b->n_ops.resize(n);
+  b->n_dev.resize(n);
+  b->n_edges.resize(n);
+  unsigned long long so = 0, sd = 0, sdo = 0, se = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    const dpro_csr& c = cands[i];
+    if (c.n_ops > 0 && (!c.dur || !c.dev || !c.flags || !c.succ_off))
+      return set_err(ctx, DPRO_EINVAL, "candidate " + std::to_string(i) + ": null CSR array");
+    if (c.n_edges > 0 && !c.succ)
+      return set_err(ctx, DPRO_EINVAL, "candidate " + std::to_string(i) + ": null succ");
+    if (c.dur_bits != 32 && c.dur_bits != 64)
+      return set_err(ctx, DPRO_EINVAL, "dur_bits must be 32 or 64");
+    Cand& h = b->hc[i];
+    std::memset(&h, 0, sizeof h);
+    h.n = c.n_ops;
+    h.e = c.n_edges;
+    h.d = c.n_devices;
+    h.op_off = so;
+    h.dev_off = sd;
+    h.dof_off = sdo;
+    b->n_ops[i] = c.n_ops;
+    b->n_dev[i] = c.n_devices;
+    b->n_edges[i] = c.n_edges;
+    b->max_d = std::max(b->max_d, c.n_devices);
+    so += c.n_ops;
+    sd += c.n_devices;
+    sdo += c.n_devices + 1;
+    se += c.n_edges;
+    if (b->memspace == DPRO_DEVICE) {
+      h.dur = c.dur;
+      h.dur64 = c.dur_bits == 64;
+      h.dev = c.dev;
+      h.flags = c.flags;
+      h.succ_off = c.succ_off;
+      h.succ = c.succ;
+      h.indeg = c.indeg;
+    }
+  }
+  b->sum_n = so;
+  b->sum_d = sd;
+  b->sum_dof = sdo;
+  b->sum_e = se;
+  if (b->memspace == DPRO_HOST) {
+    int st = upload_host(ctx, b, cands);
+    if (st != DPRO_OK) return st;
+  }
+  // scratch: indeg, qbuf, qpos, vstack (u32), sched (u8), devoff, dstate, busy
+  const size_t s_u32 = align16(so * 4 + 4);
+  const size_t s_u8 = align16(so + 1);
+  const size_t s_dof = align16(sdo * 4 + 4);
+  const size_t s_dst = align16(sd * sizeof(DevSt) + 16);
+  const size_t s_busy = align16(sd * 8 + 8);
+  CU(b->scratch.ensure(4 * s_u32 + s_u8 + s_dof + s_dst + s_busy));
+  size_t o = 0;
+  b->S.indeg = b->scratch.as<uint32_t>(o); o += s_u32;
+  b->S.qbuf = b->scratch.as<uint32_t>(o); o += s_u32;
+  b->S.qpos = b->scratch.as<uint32_t>(o); o += s_u32;
+  b->S.vstack = b->scratch.as<uint32_t>(o); o += s_u32;
+  b->S.sched = b->scratch.as<uint8_t>(o); o += s_u8;
+  b->S.devoff = b->scratch.as<uint32_t>(o); o += s_dof;
+  b->S.dstate = b->scratch.as<DevSt>(o); o += s_dst;
+  b->S.busy = b->scratch.as<long long>(o); o += s_busy;
+  // outputs: makespan, err (i64), status (i32), start, end (i64 [sum n])
+  const size_t o_b64 = align16(size_t(n) * 8 + 8);
+  const size_t o_b32 = align16(size_t(n) * 4 + 4);
+  const size_t o_op = align16(so * 8 + 8);
+  CU(b->outs.ensure(2 * o_b64 + o_b32 + 2 * o_op));
+  o = 0;
+  b->O.makespan = b->outs.as<long long>(o); o += o_b64;
+  b->O.err = b->outs.as<long long>(o); o += o_b64;
+  b->O.status = b->outs.as<int>(o); o += o_b32;
+  b->O.start = b->outs.as<long long>(o); o += o_op;
+  b->O.end = b->outs.as<long long>(o); o += o_op;
+  CU(b->desc.ensure(sizeof(Cand) * std::max(n, 1)));
+  CU(cudaMemcpyAsync(b->desc.p, b->hc.data(), sizeof(Cand) * n,
+                     cudaMemcpyHostToDevice, ctx->stream));
+  CU(b->work.ensure(16));
+  return DPRO_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dpro_cuda_abi_version(void) { return DPRO_ABI_VERSION; }
+
+dpro_ctx* dpro_cuda_create(int device) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || device < 0 || device >= count)
+    return nullptr;
+  if (cudaSetDevice(device) != cudaSuccess) return nullptr;
+  auto* ctx = new dpro_ctx;
+  ctx->device = device;
+  cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
+  int optin = 0;
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  ctx->smem_optin = static_cast<size_t>(optin);
+  cudaFuncSetAttribute(dpro_k::replay_batch_kernel,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+  return ctx;
+}
+
+void dpro_cuda_destroy(dpro_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  delete ctx;
+}
+
+int dpro_cuda_set_stream(dpro_ctx* ctx, void* stream) {
+  if (!ctx) return DPRO_EINVAL;
+  ctx->stream = static_cast<cudaStream_t>(stream);
+  return DPRO_OK;
+}
+
+const char* dpro_cuda_last_error(dpro_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : "null context";
+}
+
+dpro_batch* dpro_cuda_batch_create(dpro_ctx* ctx, const dpro_csr* cands,
+                                   int32_t n_cands, int32_t memspace) {
+  if (!ctx || (n_cands > 0 && !cands) || n_cands < 0 ||
+      (memspace != DPRO_HOST && memspace != DPRO_DEVICE)) {
+    if (ctx) ctx->err = "bad batch arguments";
+    return nullptr;
+  }
+  cudaSetDevice(ctx->device);
+  auto* b = new dpro_batch;
+  b->n = n_cands;
+  b->memspace = memspace;
+  if (build_batch(ctx, b, cands) != DPRO_OK) {
+    delete b;
+    return nullptr;
+  }
+  return b;
+}
+
+void dpro_cuda_batch_destroy(dpro_ctx* ctx, dpro_batch* b) {
+  if (ctx) cudaStreamSynchronize(ctx->stream);
+  delete b;
+}
+
+int dpro_cuda_batch_replay(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
+  if (!ctx || !b) return DPRO_EINVAL;
+  if (b->n == 0) return DPRO_OK;
+  CU(cudaSetDevice(ctx->device));
+  // shared memory: per warp, device state for up to dcap devices
+  size_t budget = std::min<size_t>(ctx->smem_optin, 200 * 1024);
+  uint32_t dcap = static_cast<uint32_t>((budget - kSmemHeader) / (kWarpsPerBlock * sizeof(DevSt)));
+  dcap = std::min<uint32_t>(dcap, std::max<uint32_t>(b->max_d, 1));
+  const size_t smem = kSmemHeader + size_t(kWarpsPerBlock) * dcap * sizeof(DevSt);
+  int blocks_per_sm = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &blocks_per_sm, dpro_k::replay_batch_kernel, 32 * kWarpsPerBlock, smem));
+  blocks_per_sm = std::max(blocks_per_sm, 1);
+  const int need = (b->n + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const int grid = std::max(1, std::min(need, ctx->sm_count * blocks_per_sm));
+  CU(cudaMemsetAsync(b->work.p, 0, 4, ctx->stream));
+  dpro_k::replay_batch_kernel<<<grid, 32 * kWarpsPerBlock, smem, ctx->stream>>>(
+      b->desc.as<Cand>(), b->n, b->S, b->O, want_schedule ? 1 : 0,
+      b->work.as<unsigned>(), dcap);
+  CU(cudaGetLastError());
+  b->replayed = true;
+  b->with_schedule = want_schedule != 0;
+  return DPRO_OK;
+}
+
+int dpro_cuda_batch_device_results(dpro_batch* b, int64_t** makespan,
+                                   int32_t** status, int64_t** err,
+                                   int64_t** start, int64_t** end) {
+  if (!b) return DPRO_EINVAL;
+  if (makespan) *makespan = reinterpret_cast<int64_t*>(b->O.makespan);
+  if (status) *status = b->O.status;
+  if (err) *err = reinterpret_cast<int64_t*>(b->O.err);
+  if (start) *start = reinterpret_cast<int64_t*>(b->O.start);
+  if (end) *end = reinterpret_cast<int64_t*>(b->O.end);
+  return DPRO_OK;
+}
+
+int dpro_cuda_batch_results(dpro_ctx* ctx, dpro_batch* b, int64_t* makespan,
+                            int32_t* status, int64_t* err, int64_t* start,
+                            int64_t* end) {
+  if (!ctx || !b) return DPRO_EINVAL;
+  if (!b->replayed) return set_err(ctx, DPRO_EINVAL, "batch not replayed");
+  CU(cudaSetDevice(ctx->device));
+  const size_t n = b->n;
+  if (makespan) CU(cudaMemcpyAsync(makespan, b->O.makespan, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  if (status) CU(cudaMemcpyAsync(status, b->O.status, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  if (err) CU(cudaMemcpyAsync(err, b->O.err, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  if ((start || end) && !b->with_schedule)
+    return set_err(ctx, DPRO_EINVAL, "replay ran without want_schedule");
+  if (start) CU(cudaMemcpyAsync(start, b->O.start, b->sum_n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  if (end) CU(cudaMemcpyAsync(end, b->O.end, b->sum_n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return DPRO_OK;
+}
+
+int dpro_cuda_batch_timelines(dpro_ctx* ctx, dpro_batch* b, int32_t cand,
+                              uint32_t* order, uint32_t* dev_off,
+                              int64_t* busy) {
+  if (!ctx || !b || cand < 0 || cand >= b->n) return DPRO_EINVAL;
+  if (!b->replayed) return set_err(ctx, DPRO_EINVAL, "batch not replayed");
+  CU(cudaSetDevice(ctx->device));
+  const Cand& h = b->hc[cand];
+  if (order) CU(cudaMemcpyAsync(order, b->S.qbuf + h.op_off, size_t(h.n) * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  if (dev_off) CU(cudaMemcpyAsync(dev_off, b->S.devoff + h.dof_off, size_t(h.d + 1) * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  if (busy) CU(cudaMemcpyAsync(busy, b->S.busy + h.dev_off, size_t(h.d) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return DPRO_OK;
+}
+
+int dpro_cuda_batch_scheduled(dpro_ctx* ctx, dpro_batch* b, int32_t cand,
+                              uint8_t* scheduled) {
+  if (!ctx || !b || cand < 0 || cand >= b->n || !scheduled) return DPRO_EINVAL;
+  if (!b->replayed) return set_err(ctx, DPRO_EINVAL, "batch not replayed");
+  CU(cudaSetDevice(ctx->device));
+  const Cand& h = b->hc[cand];
+  CU(cudaMemcpyAsync(scheduled, b->S.sched + h.op_off, h.n, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return DPRO_OK;
+}
+
+int dpro_cuda_batch_critical_paths(dpro_ctx* ctx, dpro_batch* b,
+                                   uint32_t* paths, int64_t* path_len) {
+  if (!ctx || !b) return DPRO_EINVAL;
+  if (!b->replayed || !b->with_schedule)
+    return set_err(ctx, DPRO_EINVAL, "critical path needs a replay with want_schedule");
+  CU(cudaSetDevice(ctx->device));
+  const size_t n = b->n;
+  std::vector<unsigned long long> e_off(n), po_off(n);
+  unsigned long long eo = 0, po = 0;
+  for (size_t i = 0; i < n; ++i) {
+    e_off[i] = eo;
+    po_off[i] = po;
+    eo += b->n_edges[i];
+    po += b->n_ops[i] + 1;
+  }
+  const size_t s_po = align16(po * 4 + 4), s_e = align16(eo * 4 + 4),
+               s_n = align16(b->sum_n * 4 + 4), s_off = align16(n * 8 + 8);
+  const size_t s_paths = align16(b->sum_n * 4 + 4), s_len = align16(n * 8 + 8);
+  CU(b->cp.ensure(s_po + s_e + 2 * s_n + 2 * s_off + s_paths + s_len));
+  CpScratch P;
+  size_t o = 0;
+  P.pred_off = b->cp.as<uint32_t>(o); o += s_po;
+  P.pred = b->cp.as<uint32_t>(o); o += s_e;
+  P.good = b->cp.as<uint32_t>(o); o += s_n;
+  P.stack = b->cp.as<uint32_t>(o); o += s_n;
+  P.e_off = b->cp.as<unsigned long long>(o); o += s_off;
+  P.po_off = b->cp.as<unsigned long long>(o); o += s_off;
+  uint32_t* d_paths = b->cp.as<uint32_t>(o); o += s_paths;
+  long long* d_len = b->cp.as<long long>(o); o += s_len;
+  CU(cudaMemcpyAsync(P.e_off, e_off.data(), n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaMemcpyAsync(P.po_off, po_off.data(), n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  const int threads = 128;
+  const int grid = std::max<int>(1, std::min<int>((n * 32 + threads - 1) / threads, ctx->sm_count * 8));
+  dpro_k::critical_path_kernel<<<grid, threads, 0, ctx->stream>>>(
+      b->desc.as<Cand>(), b->n, b->S, b->O, P, d_paths, d_len);
+  CU(cudaGetLastError());
+  if (paths) CU(cudaMemcpyAsync(paths, d_paths, b->sum_n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  if (path_len) CU(cudaMemcpyAsync(path_len, d_len, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return DPRO_OK;
+}
+
+int dpro_cuda_replay_batch(dpro_ctx* ctx, const dpro_csr* cands,
+                           int32_t n_cands, int32_t memspace,
+                           int64_t* makespan, int64_t* start, int64_t* end,
+                           int32_t* status, int64_t* err) {
+  if (!ctx) return DPRO_EINVAL;
+  dpro_batch* b = dpro_cuda_batch_create(ctx, cands, n_cands, memspace);
+  if (!b) return DPRO_EINVAL;
+  int st = dpro_cuda_batch_replay(ctx, b, (start || end) ? 1 : 0);
+  if (st == DPRO_OK)
+    st = dpro_cuda_batch_results(ctx, b, makespan, status, err, start, end);
+  dpro_cuda_batch_destroy(ctx, b);
+  return st;
+}
+
+int dpro_cuda_tsync_grid(dpro_ctx* ctx, const dpro_cluster_desc* cluster,
+                         const int64_t* bytes, const int32_t* k, int32_t n,
+                         int64_t* out, int32_t* status) {
+  if (!ctx || !cluster || n < 0) return DPRO_EINVAL;
+  std::vector<dpro_graph*> graphs(n, nullptr);
+  std::vector<std::string> errs(n);
+  std::vector<int> idx;
+  const int nt = std::max(1, std::min<int>(n, (int)std::thread::hardware_concurrency()));
+  auto work = [&](int tid) {
+    for (int i = tid; i < n; i += nt)
+      if (k[i] >= 1) graphs[i] = dpro_internal_tsync_graph(cluster, bytes[i], k[i], &errs[i]);
+      else errs[i] = "sync_makespan: partition count must be >= 1, got " + std::to_string(k[i]);
+  };
+  {
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t) pool.emplace_back(work, t);
+    work(0);
+    for (auto& th : pool) th.join();
+  }
+  std::vector<dpro_csr> csrs;
+  for (int i = 0; i < n; ++i) {
+    if (!graphs[i]) {
+      if (status) status[i] = DPRO_EINVAL;
+      out[i] = 0;
+      ctx->err = errs[i];
+      continue;
+    }
+    dpro_csr c;
+    dpro_graph_csr(graphs[i], &c);
+    csrs.push_back(c);
+    idx.push_back(i);
+  }
+  int st = DPRO_OK;
+  if (!csrs.empty()) {
+    std::vector<int64_t> ms(csrs.size()), er(csrs.size());
+    std::vector<int32_t> ss(csrs.size());
+    st = dpro_cuda_replay_batch(ctx, csrs.data(), (int32_t)csrs.size(), DPRO_HOST,
+                                ms.data(), nullptr, nullptr, ss.data(), er.data());
+    for (size_t j = 0; j < idx.size(); ++j) {
+      out[idx[j]] = ms[j];
+      if (status) status[idx[j]] = st == DPRO_OK ? ss[j] : st;
+    }
+  }
+  for (auto* g : graphs)
+    if (g) dpro_graph_free(g);
+  return st;
+}
+
+}  // extern "C"

@@ -1,0 +1,201 @@
+"""Batched replay engine: the host side over the C ABI (include/dpro_cuda.h).
+
+`Engine` owns one dpro_ctx (one GPU). `Batch` is a registered set of
+candidate CSR graphs (host arrays uploaded once, or device arrays used in
+place) that can be replayed repeatedly; results stay on the device until
+asked for. This is the interface the search loop drives in bulk; the
+reference-shaped single-graph API lives in replay.py.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+
+from . import _native as N
+from .errors import EngineError
+
+
+@dataclass
+class Csr:
+    """Index-ordered CSR of one DFG (numpy, host)."""
+    dur: np.ndarray        # int64 [n]
+    dev: np.ndarray        # uint16 [n]
+    flags: np.ndarray      # uint8 [n]
+    succ_off: np.ndarray   # uint32 [n+1]
+    succ: np.ndarray       # uint32 [e]
+    indeg: np.ndarray | None
+    n_devices: int
+
+    @property
+    def n_ops(self) -> int:
+        return int(self.dur.shape[0])
+
+    @property
+    def n_edges(self) -> int:
+        return int(self.succ.shape[0])
+
+    @staticmethod
+    def from_dict(d: dict) -> "Csr":
+        return Csr(d["dur"], d["dev"], d["flags"], d["succ_off"], d["succ"],
+                   d.get("indeg"), int(d["n_devices"]))
+
+    def algorithmic_bytes(self) -> int:
+        """B = 32 V + 4 E per replay."""
+        return 32 * self.n_ops + 4 * self.n_edges
+
+    def as_struct(self) -> N.DproCsr:
+        for a, dt in ((self.dur, np.int64), (self.dev, np.uint16), (self.flags, np.uint8),
+                      (self.succ_off, np.uint32), (self.succ, np.uint32)):
+            if a.dtype != dt or not a.flags["C_CONTIGUOUS"]:
+                raise ValueError(f"CSR array must be contiguous {np.dtype(dt)}")
+        return N.DproCsr(self.n_ops, self.n_edges, self.n_devices, 64,
+                         N.ptr(self.dur), N.ptr(self.dev), N.ptr(self.flags),
+                         N.ptr(self.succ_off), N.ptr(self.succ),
+                         N.ptr(self.indeg) if self.indeg is not None else None)
+
+
+def _check(ctx, rc: int, what: str) -> None:
+    if rc != N.DPRO_OK:
+        msg = N.lib.dpro_cuda_last_error(ctx).decode(errors="replace")
+        raise EngineError(f"{what} failed ({rc}): {msg}")
+
+
+class Engine:
+    """One dpro_ctx on one CUDA device."""
+
+    def __init__(self, device: int = 0):
+        self.device = device
+        self.ctx = N.lib.dpro_cuda_create(device)
+        if not self.ctx:
+            raise EngineError(f"dpro_cuda_create({device}) failed: no usable CUDA device")
+
+    def close(self) -> None:
+        if self.ctx:
+            N.lib.dpro_cuda_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream_handle: int | None) -> None:
+        _check(self.ctx, N.lib.dpro_cuda_set_stream(self.ctx, stream_handle), "set_stream")
+
+    def batch(self, cands: Sequence[Csr] | Sequence[N.DproCsr],
+              memspace: int = N.DPRO_HOST) -> "Batch":
+        return Batch(self, cands, memspace)
+
+    def tsync_grid(self, cluster, bytes_: Sequence[int], ks: Sequence[int]):
+        """dpro_cuda_tsync_grid: (makespans, statuses)."""
+        holder = N.ClusterDescHolder(cluster)
+        b = np.ascontiguousarray(bytes_, dtype=np.int64)
+        k = np.ascontiguousarray(ks, dtype=np.int32)
+        out = np.zeros(len(b), np.int64)
+        st = np.zeros(len(b), np.int32)
+        rc = N.lib.dpro_cuda_tsync_grid(self.ctx, C.byref(holder.desc), N.ptr(b), N.ptr(k),
+                                        len(b), N.ptr(out), N.ptr(st))
+        if rc not in (N.DPRO_OK, N.DPRO_EINVAL):
+            _check(self.ctx, rc, "tsync_grid")
+        return out, st
+
+
+class Batch:
+    def __init__(self, engine: Engine, cands, memspace: int):
+        self.engine = engine
+        self._keep = list(cands)
+        structs = [c.as_struct() if isinstance(c, Csr) else c for c in cands]
+        self.n = len(structs)
+        self.n_ops = np.array([s.n_ops for s in structs], np.int64)
+        self.n_edges = np.array([s.n_edges for s in structs], np.int64)
+        self.n_devices = np.array([s.n_devices for s in structs], np.int64)
+        self.op_off = np.zeros(self.n + 1, np.int64)
+        self.op_off[1:] = np.cumsum(self.n_ops)
+        arr = (N.DproCsr * max(1, self.n))(*structs)
+        self.handle = N.lib.dpro_cuda_batch_create(engine.ctx, arr, self.n, memspace)
+        if not self.handle:
+            _check(engine.ctx, N.DPRO_EINVAL, "batch_create")
+        self.with_schedule = False
+
+    def close(self) -> None:
+        if self.handle:
+            N.lib.dpro_cuda_batch_destroy(self.engine.ctx, self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def algorithmic_bytes(self) -> int:
+        return int(32 * self.n_ops.sum() + 4 * self.n_edges.sum())
+
+    def replay(self, want_schedule: bool = True) -> None:
+        """Asynchronous on the engine's stream."""
+        _check(self.engine.ctx,
+               N.lib.dpro_cuda_batch_replay(self.engine.ctx, self.handle, int(want_schedule)),
+               "batch_replay")
+        self.with_schedule = want_schedule
+
+    def device_results(self) -> dict:
+        ps = [C.c_void_p() for _ in range(5)]
+        N.lib.dpro_cuda_batch_device_results(self.handle, *[C.byref(p) for p in ps])
+        return dict(zip(("makespan", "status", "err", "start", "end"),
+                        [p.value for p in ps]))
+
+    def results(self, schedule: bool = False):
+        ms = np.zeros(self.n, np.int64)
+        st = np.zeros(self.n, np.int32)
+        er = np.zeros(self.n, np.int64)
+        start = end = None
+        if schedule:
+            start = np.zeros(int(self.op_off[-1]), np.int64)
+            end = np.zeros(int(self.op_off[-1]), np.int64)
+        _check(self.engine.ctx,
+               N.lib.dpro_cuda_batch_results(self.engine.ctx, self.handle, N.ptr(ms), N.ptr(st),
+                                             N.ptr(er), N.ptr(start), N.ptr(end)),
+               "batch_results")
+        return ms, st, er, start, end
+
+    def timelines(self, cand: int):
+        n, d = int(self.n_ops[cand]), int(self.n_devices[cand])
+        order = np.zeros(max(n, 1), np.uint32)
+        dev_off = np.zeros(d + 1, np.uint32)
+        busy = np.zeros(max(d, 1), np.int64)
+        _check(self.engine.ctx,
+               N.lib.dpro_cuda_batch_timelines(self.engine.ctx, self.handle, cand, N.ptr(order),
+                                               N.ptr(dev_off), N.ptr(busy)),
+               "batch_timelines")
+        return order, dev_off, busy[:d]
+
+    def scheduled(self, cand: int) -> np.ndarray:
+        m = np.zeros(max(1, int(self.n_ops[cand])), np.uint8)
+        _check(self.engine.ctx,
+               N.lib.dpro_cuda_batch_scheduled(self.engine.ctx, self.handle, cand, N.ptr(m)),
+               "batch_scheduled")
+        return m[: int(self.n_ops[cand])]
+
+    def critical_paths(self):
+        """List of per-candidate path index arrays (empty on error status)."""
+        paths = np.zeros(max(1, int(self.op_off[-1])), np.uint32)
+        lens = np.zeros(self.n, np.int64)
+        _check(self.engine.ctx,
+               N.lib.dpro_cuda_batch_critical_paths(self.engine.ctx, self.handle, N.ptr(paths),
+                                                    N.ptr(lens)),
+               "batch_critical_paths")
+        return [paths[self.op_off[i]: self.op_off[i] + lens[i]].copy() for i in range(self.n)]
+
+
+_default: Engine | None = None
+
+
+def default_engine() -> Engine:
+    global _default
+    if _default is None:
+        _default = Engine(0)
+    return _default

@@ -1,0 +1,271 @@
+"""Comm-topology expansion and layered-model graphs.
+
+* `expand_*` mirror proj/src/ingest.cpp:268-384 on the Python graph model
+  (small graphs: fixtures, partial_replay tensors).
+* `NativeGraph` wraps the C++ CSR generator of libdpro_cuda.so
+  (csrc/dfg_gen.cpp) that builds the ingest/partition graphs of
+  proj/src/ingest.cpp:187-454 and proj/src/optimize.cpp:459-492 straight in
+  index order -- used for the large synthetic workloads.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import numpy as np
+
+from . import _native as N
+from .engine import Csr
+from .errors import Error, TopologyError
+from .graph import (ClusterSpec, DeviceId, GlobalDFG, GraphBuilder, Op, OpKind,
+                    TensorUnit, base_of_unit_name, fnv1a, round_us)
+
+
+@dataclass
+class CommTopology:
+    unit: str
+    bytes: int = 0
+    part_index: int = 0
+    part_count: int = 1
+    ps_node: str = ""
+    ops: list[Op] = field(default_factory=list)
+    edges: list[tuple[str, str]] = field(default_factory=list)
+    entry: dict[str, list[str]] = field(default_factory=dict)
+    exit: dict[str, list[str]] = field(default_factory=dict)
+
+
+def _hop_dur(bytes_: int, cluster: ClusterSpec, src: str, dst: str) -> int:
+    l = cluster.find_link(src, dst)  # ingest.cpp:37-48
+    bw, lat = (l.bandwidth_bytes_per_us, l.latency_us) if l else (1.0, 0.0)
+    return round_us(float(bytes_) / bw + lat)
+
+
+def _comm_op(kind: OpKind, src: str, dst: str, tensor: str, bytes_: int, txn: str,
+             dur: int) -> Op:
+    return Op(id=f"{kind.name}.{txn}", kind=kind, node=src if kind == OpKind.SEND else dst,
+              device=DeviceId.link(src, dst), dur=dur, tensor=tensor, bytes=bytes_,
+              transaction=txn)
+
+
+def expand_ring_allreduce(tensor: str, bytes_: int, cluster: ClusterSpec) -> CommTopology:
+    """ingest.cpp:268-315."""
+    order = list(cluster.ring_order) or sorted(cluster.workers())
+    n = len(order)
+    if n < 2:
+        raise TopologyError(
+            f"degenerate ring: allreduce needs at least 2 workers, got {n}")
+    chunks = cluster.chunks_per_tensor if cluster.chunks_per_tensor > 0 else n
+    steps = 2 * (n - 1)
+    base, rem = divmod(bytes_, chunks) if bytes_ >= 0 else (int(bytes_ / chunks), 0)
+    topo = CommTopology(tensor, bytes_)
+    for c in range(chunks):
+        cb = base + (1 if c < rem else 0)
+        prev = None
+        for s in range(steps):
+            src, dst = order[(c + s) % n], order[(c + s + 1) % n]
+            txn = f"{tensor}#c{c}#s{s}#{src}#{dst}"
+            snd = _comm_op(OpKind.SEND, src, dst, tensor, cb, txn, 0)
+            rcv = _comm_op(OpKind.RECV, src, dst, tensor, cb, txn,
+                           _hop_dur(cb, cluster, src, dst))
+            topo.edges.append((snd.id, rcv.id))
+            if s == 0:
+                topo.entry.setdefault(src, []).append(snd.id)
+            else:
+                topo.edges.append((prev, snd.id))
+            if s >= n - 2:
+                topo.exit.setdefault(dst, []).append(rcv.id)
+            prev = rcv.id
+            topo.ops += [snd, rcv]
+    for ids in topo.exit.values():
+        ids.sort()
+    return topo
+
+
+def ps_node_for(tensor: str, cluster: ClusterSpec) -> str:
+    servers = sorted(cluster.ps_nodes())  # ingest.cpp:317-325
+    if not servers:
+        raise TopologyError("parameter-server scheme requires at least one ps node")
+    return servers[fnv1a(tensor) % len(servers)]
+
+
+def expand_ps(tensor: str, bytes_: int, cluster: ClusterSpec) -> CommTopology:
+    """ingest.cpp:327-373."""
+    server = ps_node_for(tensor, cluster)
+    workers = sorted(cluster.workers())
+    if not workers:
+        raise TopologyError("parameter-server scheme requires at least one worker")
+    topo = CommTopology(tensor, bytes_, ps_node=server)
+    push_recvs, pull_sends = [], []
+    for w in workers:
+        push = f"{tensor}#push#{w}#{server}"
+        ps = _comm_op(OpKind.SEND, w, server, tensor, bytes_, push, 0)
+        pr = _comm_op(OpKind.RECV, w, server, tensor, bytes_, push,
+                      _hop_dur(bytes_, cluster, w, server))
+        topo.edges.append((ps.id, pr.id))
+        topo.entry.setdefault(w, []).append(ps.id)
+        push_recvs.append(pr.id)
+        pull = f"{tensor}#pull#{server}#{w}"
+        ls = _comm_op(OpKind.SEND, server, w, tensor, bytes_, pull, 0)
+        lr = _comm_op(OpKind.RECV, server, w, tensor, bytes_, pull,
+                      _hop_dur(bytes_, cluster, server, w))
+        topo.edges.append((ls.id, lr.id))
+        topo.exit.setdefault(w, []).append(lr.id)
+        pull_sends.append(ls.id)
+        topo.ops += [ps, pr, ls, lr]
+    for pull in pull_sends:
+        for push in push_recvs:
+            topo.edges.append((push, pull))
+    return topo
+
+
+def expand_tensor(tensor: str, bytes_: int, cluster: ClusterSpec) -> CommTopology:
+    if cluster.scheme == "ring":
+        return expand_ring_allreduce(tensor, bytes_, cluster)
+    return expand_ps(tensor, bytes_, cluster)
+
+
+def splice(b: GraphBuilder, topo: CommTopology, base: str | None = None) -> None:
+    """Adds a topology and hooks it onto <node>->IN./OUT.<base> when those
+    ops exist (assemble_global_dfg, ingest.cpp:404-441)."""
+    base = base or base_of_unit_name(topo.unit)
+    for op in topo.ops:
+        b.add_op(op)
+    for x, y in topo.edges:
+        b.add_edge(x, y)
+    unit = TensorUnit(topo.unit, base, topo.bytes, topo.part_index, topo.part_count,
+                      topo.ps_node, sorted(op.id for op in topo.ops))
+    for node, ids in topo.entry.items():
+        vin = f"{node}->IN.{base}"
+        if b.has_op(vin):
+            for i in ids:
+                b.add_edge(vin, i)
+            unit.vin[node] = vin
+    for node, ids in topo.exit.items():
+        vout = f"{node}->OUT.{base}"
+        if b.has_op(vout):
+            for i in ids:
+                b.add_edge(i, vout)
+            unit.vout[node] = vout
+    b.add_tensor_unit(unit)
+
+
+# --------------------------------------------------------------------------
+# native generator
+# --------------------------------------------------------------------------
+class NativeGraph:
+    """Owning handle of a dpro_graph (host CSR built by csrc/dfg_gen.cpp)."""
+
+    def __init__(self, handle: int):
+        if not handle:
+            raise Error(N.lib.dpro_graph_last_error().decode())
+        self.handle = handle
+        s = N.DproCsr()
+        N.lib.dpro_graph_csr(handle, C.byref(s))
+        self.struct = s
+        n, e = s.n_ops, s.n_edges
+
+        def view(p, dt, cnt):
+            if cnt == 0:
+                return np.zeros(0, dt)
+            return np.ctypeslib.as_array(
+                C.cast(p, C.POINTER(np.ctypeslib.as_ctypes_type(dt))), (cnt,))
+
+        self.csr = Csr(view(s.dur, np.int64, n), view(s.dev, np.uint16, n),
+                       view(s.flags, np.uint8, n), view(s.succ_off, np.uint32, n + 1),
+                       view(s.succ, np.uint32, e), view(s.indeg, np.uint32, n),
+                       int(s.n_devices))
+
+    def __del__(self):  # pragma: no cover
+        if getattr(self, "handle", None):
+            N.lib.dpro_graph_free(self.handle)
+            self.handle = None
+
+    @property
+    def n_ops(self) -> int:
+        return self.struct.n_ops
+
+    @property
+    def n_edges(self) -> int:
+        return self.struct.n_edges
+
+    def op_id(self, i: int) -> str:
+        return N.lib.dpro_graph_op_id(self.handle, i).decode()
+
+    def op_kind(self, i: int) -> int:
+        return N.lib.dpro_graph_op_kind(self.handle, i)
+
+    def op_ids(self) -> list[str]:
+        return [self.op_id(i) for i in range(self.n_ops)]
+
+    def device_strs(self) -> list[str]:
+        return [N.lib.dpro_graph_device_str(self.handle, d).decode()
+                for d in range(self.csr.n_devices)]
+
+    def to_global_dfg(self, cluster: ClusterSpec | None = None) -> GlobalDFG:
+        """Python graph object (small graphs: tests / reference-shaped API)."""
+        devs = self.device_strs()
+        ids = self.op_ids()
+        ops = []
+        for i, id_ in enumerate(ids):
+            ds = devs[int(self.csr.dev[i])]
+            dev = DeviceId.link(*ds.split(">", 1)) if ">" in ds else DeviceId.compute(ds)
+            ops.append(Op(id=id_, kind=OpKind(self.op_kind(i)), node=dev.node, device=dev,
+                          dur=int(self.csr.dur[i])))
+        so, su = self.csr.succ_off, self.csr.succ
+        succs = [su[so[i]:so[i + 1]].tolist() for i in range(len(ids))]
+        return GlobalDFG(ops, succs, {}, cluster or ClusterSpec())
+
+
+@dataclass
+class LayeredModel:
+    """SynthSpec's layered model (proj/include/dpro/synth.hpp:32-44)."""
+    fw_dur: Sequence[int]
+    bw_dur: Sequence[int]
+    tensor_bytes: Sequence[int]
+    update_dur: int = 5
+
+    @property
+    def layers(self) -> int:
+        return len(self.fw_dur)
+
+    def struct(self):
+        self._fw = np.ascontiguousarray(self.fw_dur, np.int64)
+        self._bw = np.ascontiguousarray(self.bw_dur, np.int64)
+        self._tb = np.ascontiguousarray(self.tensor_bytes, np.int64)
+        P = C.POINTER(C.c_int64)
+        return N.DproLayeredModel(self.layers, self._fw.ctypes.data_as(P),
+                                  self._bw.ctypes.data_as(P), self._tb.ctypes.data_as(P),
+                                  int(self.update_dur))
+
+
+def layered_graph(model: LayeredModel, cluster: ClusterSpec,
+                  part_k: Sequence[int] | None = None) -> NativeGraph:
+    m = model.struct()
+    holder = N.ClusterDescHolder(cluster)
+    pk = None if part_k is None else np.ascontiguousarray(part_k, np.int32)
+    st = C.c_int32(0)
+    h = N.lib.dpro_graph_layered(C.byref(m), C.byref(holder.desc), N.ptr(pk), C.byref(st))
+    return NativeGraph(h)
+
+
+def layered_graphs(model: LayeredModel, cluster: ClusterSpec, part_k: np.ndarray,
+                   threads: int = 8) -> list[NativeGraph]:
+    """Candidate batch: one graph per row of part_k [n, layers]."""
+    m = model.struct()
+    holder = N.ClusterDescHolder(cluster)
+    pk = np.ascontiguousarray(part_k, np.int32)
+    n = pk.shape[0]
+    out = (C.c_void_p * n)()
+    rc = N.lib.dpro_graph_layered_batch(C.byref(m), C.byref(holder.desc), N.ptr(pk), n,
+                                        threads, out)
+    if rc != N.DPRO_OK:
+        raise Error(N.lib.dpro_graph_last_error().decode())
+    return [NativeGraph(out[i]) for i in range(n)]
+
+
+def tsync_graph(cluster: ClusterSpec, bytes_: int, k: int) -> NativeGraph:
+    holder = N.ClusterDescHolder(cluster)
+    st = C.c_int32(0)
+    return NativeGraph(N.lib.dpro_graph_tsync(C.byref(holder.desc), int(bytes_), int(k),
+                                              C.byref(st)))

@@ -1,0 +1,98 @@
+"""Random-graph families for parity tests (test infrastructure).
+
+* `random_dag_ref`   -- proj/tests/test_replay.cpp:214-238 (2-12 ops, 1-3
+  devices, durations 1..6, edge p=0.22, shuffled wiring).
+* `acceptance_dag`   -- proj/tests/acceptance_main.cpp:293-320 (durations
+  1..50, edge p=0.3, ids "<node>->opNN").
+* `fuzz_dag`         -- beyond the reference's oracles: zero
+  durations, virtual ops (each with >= 1 predecessor), link devices,
+  shuffled multi-digit names (w10 < w2 byte order), wider graphs.
+numpy RNGs replace std::mt19937, so the draws differ from the reference's
+sequences; the families (shape, sizes, distributions) are the same.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from paper_2205_02473_b200.graph import DeviceId, GraphBuilder, Op, OpKind, comp
+
+
+def random_dag_ref(rng: np.random.Generator):
+    n = int(rng.integers(2, 13))
+    devs = int(rng.integers(1, 4))
+    b = GraphBuilder()
+    names = []
+    for i in range(n):
+        name = chr(ord("a") + i)
+        dev = chr(ord("A") + int(rng.integers(0, devs)))
+        names.append(name)
+        b.add_op(comp(name, dev, int(rng.integers(1, 7))))
+    rng.shuffle(names)
+    for i in range(n):
+        for j in range(i + 1, n):
+            if rng.random() < 0.22:
+                b.add_edge(names[i], names[j])
+    return b.build()
+
+
+def acceptance_dag(rng: np.random.Generator):
+    n = int(rng.integers(2, 13))
+    devices = int(rng.integers(1, 4))
+    b = GraphBuilder()
+    ids = []
+    for i in range(n):
+        node = f"n{int(rng.integers(0, devices))}"
+        name = f"{node}->op{i:02d}"
+        ids.append(name)
+        b.add_op(comp(name, node, int(rng.integers(1, 51))))
+    for i in range(n):
+        for j in range(i + 1, n):
+            if rng.random() < 0.3:
+                b.add_edge(ids[i], ids[j])
+    return b.build()
+
+
+def fuzz_dag(rng: np.random.Generator, max_ops: int = 40, zero_p: float = 0.3,
+             virt_p: float = 0.15, edge_p: float | None = None, max_dur: int = 9):
+    n = int(rng.integers(2, max_ops + 1))
+    nodes = [f"w{i}" for i in range(int(rng.integers(1, 13)))]
+    b = GraphBuilder()
+    names = []
+    ep = edge_p if edge_p is not None else float(rng.uniform(0.05, 0.35))
+    order = rng.permutation(n)  # wiring order independent of names
+    kinds = {}
+    for i in range(n):
+        name = f"op{int(rng.integers(0, 10**6))}_{i}"
+        names.append(name)
+    for pos, i in enumerate(order):
+        name = names[i]
+        # an op may be virtual only if it can get a predecessor
+        virtual = pos > 0 and rng.random() < virt_p
+        if virtual:
+            node = nodes[int(rng.integers(0, len(nodes)))]
+            kind = OpKind.VIRTUAL_IN if rng.random() < 0.5 else OpKind.VIRTUAL_OUT
+            b.add_op(Op(id=name, kind=kind, node=node, device=DeviceId.compute(node), dur=0))
+        else:
+            src = nodes[int(rng.integers(0, len(nodes)))]
+            if rng.random() < 0.4 and len(nodes) > 1:
+                dst = nodes[int(rng.integers(0, len(nodes)))]
+                while dst == src:
+                    dst = nodes[int(rng.integers(0, len(nodes)))]
+                dev = DeviceId.link(src, dst)
+                kind = OpKind.RECV if rng.random() < 0.5 else OpKind.SEND
+            else:
+                dev = DeviceId.compute(src)
+                kind = OpKind.FW
+            dur = 0 if rng.random() < zero_p else int(rng.integers(1, max_dur + 1))
+            b.add_op(Op(id=name, kind=kind, node=src, device=dev, dur=dur))
+        kinds[name] = virtual
+    for a in range(n):
+        for c in range(a + 1, n):
+            if rng.random() < ep:
+                b.add_edge(names[order[a]], names[order[c]])
+    # every virtual op gets >= 1 predecessor (else the init quirk may fire)
+    for pos in range(1, n):
+        nm = names[order[pos]]
+        if kinds[nm] and not any(b.has_edge(names[order[a]], nm) for a in range(pos)):
+            b.add_edge(names[order[int(rng.integers(0, pos))]], nm)
+    return b.build()

@@ -1,0 +1,192 @@
+"""K1 (replay) and K3 (critical path) on the GPU, bit-exact against the
+reference's golden vectors and the C oracle. Mirrors proj/tests/test_replay.cpp."""
+import numpy as np
+import pytest
+
+from dags import acceptance_dag, fuzz_dag, random_dag_ref
+from golden_io import graph_from_json, replay_vectors, tl_pos_from
+from paper_2205_02473_b200 import (CycleError, DeviceId, GraphBuilder, MissingProfileError, Op,
+                                   OpKind, comp, critical_path, execution_graph, replay,
+                                   replay_many)
+from paper_2205_02473_b200.engine import Csr
+
+pytestmark = pytest.mark.gpu
+
+
+def _batch_check(engine, graphs, expects, label):
+    """Replays all graphs in one batch and compares every output."""
+    batch = engine.batch([Csr.from_dict(g.to_csr()) for g in graphs])
+    batch.replay(want_schedule=True)
+    ms, st, er, start, end = batch.results(schedule=True)
+    paths = batch.critical_paths()
+    for i, (g, exp) in enumerate(zip(graphs, expects)):
+        name = f"{label}[{i}]"
+        a, b = int(batch.op_off[i]), int(batch.op_off[i + 1])
+        if exp["status"] != 0:
+            assert st[i] == exp["status"], name
+            if exp["status"] == 1:
+                assert exp["message"] == f"op {g.op_at(int(er[i])).id} has no duration", name
+            else:
+                stuck = [g.op_at(j).id for j in np.flatnonzero(batch.scheduled(i) == 0)]
+                assert stuck == exp["cycle"], name
+                assert f"; {int(er[i])} ops never became ready" in exp["message"], name
+            continue
+        assert st[i] == 0, (name, st[i], er[i])
+        assert ms[i] == exp["T"], name
+        assert start[a:b].tolist() == exp["start"], name
+        assert end[a:b].tolist() == exp["end"], name
+        order, dev_off, busy = batch.timelines(i)
+        assert tl_pos_from(order, dev_off, g.size()).tolist() == exp["tl_pos"], name
+        assert paths[i].tolist() == exp["path"], name
+        if "util" in exp:
+            T = exp["T"]
+            for d, u in enumerate(exp["util"]):
+                if u >= 0:
+                    assert (busy[d] / T if T > 0 else 0.0) == pytest.approx(u, abs=0), name
+
+
+def test_reference_golden_vectors_bit_exact(engine):
+    vecs = replay_vectors()
+    graphs = [graph_from_json(v["graph"]) for v in vecs]
+    _batch_check(engine, graphs, [v["expect"] for v in vecs], "golden")
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_fuzz_against_c_oracle(engine, port, seed):
+    rng = np.random.default_rng(1000 + seed)
+    graphs = []
+    for t in range(1500):
+        kind = t % 5
+        if kind == 0:
+            graphs.append(random_dag_ref(rng))
+        elif kind == 1:
+            graphs.append(acceptance_dag(rng))
+        elif kind == 2:
+            graphs.append(fuzz_dag(rng, max_ops=80, zero_p=0.5, virt_p=0.2))
+        elif kind == 3:
+            graphs.append(fuzz_dag(rng, max_ops=200, zero_p=0.2, virt_p=0.1, edge_p=0.03,
+                                   max_dur=3))
+        else:
+            graphs.append(fuzz_dag(rng, max_ops=30, zero_p=0.8, virt_p=0.3))
+    expects = []
+    for g in graphs:
+        o = port.port_replay(g.to_csr())
+        if o["status"] == 0:
+            expects.append({"status": 0, "T": o["T"], "start": o["start"].tolist(),
+                            "end": o["end"].tolist(), "tl_pos": o["tl_pos"].tolist(),
+                            "path": o["path"].tolist()})
+        elif o["status"] == 1:
+            expects.append({"status": 1,
+                            "message": f"op {g.op_at(int(o['err'])).id} has no duration"})
+        else:
+            stuck = [g.op_at(j).id for j in np.flatnonzero(o["scheduled"] == 0)]
+            expects.append({"status": 2, "cycle": stuck,
+                            "message": f"replay requires an acyclic graph; {o['err']} ops never became ready"})
+    _batch_check(engine, graphs, expects, f"fuzz{seed}")
+
+
+# ---- proj/tests/test_replay.cpp, through the reference-shaped API ----------
+def test_two_device_chain():
+    b = GraphBuilder()
+    b.add_op(comp("x", "A", 10)); b.add_op(comp("y", "B", 5)); b.add_edge("x", "y")
+    r = replay(b.build())
+    assert r.iteration_time_us == 15
+    assert r.schedule["x"].start == 0 and r.schedule["y"].start == 10
+    assert r.schedule["y"].end == 15
+
+
+def test_independent_ops_serialize():
+    b = GraphBuilder()
+    b.add_op(comp("p", "A", 10)); b.add_op(comp("q", "A", 5))
+    r = replay(b.build())
+    assert r.iteration_time_us == 15
+    assert r.schedule["p"].start == 0 and r.schedule["q"].start == 10
+    assert r.utilization[DeviceId.compute("A")] == pytest.approx(1.0)
+
+
+def test_diamond_execution_graph_critical_path():
+    b = GraphBuilder()
+    for n, d, t in [("a", "d1", 2), ("b", "d1", 3), ("c", "d2", 5), ("d", "d1", 1)]:
+        b.add_op(comp(n, d, t))
+    for x, y in [("a", "b"), ("a", "c"), ("c", "d")]:
+        b.add_edge(x, y)
+    g = b.build()
+    r = replay(g)
+    assert (r.schedule["a"].end, r.schedule["b"].start, r.schedule["b"].end) == (2, 2, 5)
+    assert (r.schedule["c"].start, r.schedule["c"].end, r.schedule["d"].start) == (2, 7, 7)
+    assert r.iteration_time_us == 8
+    ex = execution_graph(g, r)
+    assert ex.has_edge("b", "d") and ex.edge_count() == 4
+    p = critical_path(ex, r)
+    assert [e.op for e in p.ops] == ["a", "c", "d"]
+    assert p.total_us == 8 and p.conforming
+
+
+def test_equal_branches_lexicographic_path():
+    b = GraphBuilder()
+    for n, d, t in [("a", "A", 2), ("b", "B", 4), ("c", "C", 4), ("d", "A", 1)]:
+        b.add_op(comp(n, d, t))
+    for x, y in [("a", "b"), ("a", "c"), ("b", "d"), ("c", "d")]:
+        b.add_edge(x, y)
+    g = b.build()
+    r = replay(g)
+    p = critical_path(execution_graph(g, r), r)
+    assert [e.op for e in p.ops] == ["a", "b", "d"]
+
+
+def test_earlier_ready_beats_smaller_name():
+    b = GraphBuilder()
+    for n, d, t in [("m", "D", 10), ("pa", "E", 2), ("pb", "F", 4), ("z", "D", 3), ("a", "D", 3)]:
+        b.add_op(comp(n, d, t))
+    b.add_edge("pa", "z"); b.add_edge("pb", "a")
+    r = replay(b.build())
+    assert r.schedule["z"].start == 10 and r.schedule["a"].start == 13
+
+
+def test_virtual_ops_occupy_no_device():
+    b = GraphBuilder()
+    b.add_op(comp("a", "w0", 5))
+    b.add_op(Op("v", OpKind.VIRTUAL_IN, "w0", DeviceId.compute("w0"), 0))
+    b.add_op(comp("b", "w0", 3))
+    b.add_edge("a", "v"); b.add_edge("v", "b")
+    r = replay(b.build())
+    assert (r.schedule["v"].start, r.schedule["v"].end, r.schedule["b"].start) == (5, 5, 5)
+    assert r.iteration_time_us == 8
+    assert r.device_timelines[DeviceId.compute("w0")] == ["a", "b"]
+
+
+def test_cycles_and_unset_durations_raise():
+    b = GraphBuilder()
+    b.add_op(comp("a", "A", 1)); b.add_op(comp("b", "A", 1))
+    b.add_edge("a", "b"); b.add_edge("b", "a")
+    with pytest.raises(CycleError) as e:
+        replay(b.build())
+    assert e.value.cycle == ["a", "b"]
+    b = GraphBuilder()
+    b.add_op(comp("a", "A", -1))
+    with pytest.raises(MissingProfileError, match="op a has no duration"):
+        replay(b.build())
+
+
+def test_deterministic_and_critical_path_sums_to_T():
+    rng = np.random.default_rng(1234)
+    graphs = [random_dag_ref(rng) for _ in range(100)]
+    r1 = replay_many(graphs)
+    r2 = replay_many(graphs)
+    for g, a, b in zip(graphs, r1, r2):
+        assert a.schedule == b.schedule and a.device_timelines == b.device_timelines
+        p = critical_path(execution_graph(g, a), a)
+        assert sum(e.dur for e in p.ops) == a.iteration_time_us == p.total_us
+
+
+def test_longer_ops_never_shrink_pinned_order_makespan():
+    """test_replay.cpp:439-450."""
+    rng = np.random.default_rng(99)
+    for _ in range(60):
+        g = random_dag_ref(rng)
+        r = replay(g)
+        ex = execution_graph(g, r)
+        victim = int(rng.integers(0, ex.size()))
+        b = GraphBuilder(ex)
+        b.op(ex.op_at(victim).id).dur += 1 + int(rng.integers(0, 5))
+        assert replay(b.build()).iteration_time_us >= r.iteration_time_us

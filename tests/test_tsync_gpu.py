@@ -1,0 +1,79 @@
+"""t_sync grid (sync_makespan / partial_replay) on the GPU vs the reference's
+values (golden vectors from the compiled reference; test_optimize.cpp:265-291
+and SURVEY Appendix A Z5/Z6 are among them)."""
+import hashlib
+
+import numpy as np
+import pytest
+
+from golden_io import synth_vectors, tsync_vectors
+from paper_2205_02473_b200 import (Error, GraphBuilder, LookupError_, TensorUnit, partial_replay,
+                                   replay, sync_makespan, sync_makespan_grid)
+from paper_2205_02473_b200.engine import Csr
+from paper_2205_02473_b200.graph import DeviceId, Op, OpKind, synth_cluster
+from paper_2205_02473_b200.ingest import LayeredModel, expand_ps, layered_graph, splice
+
+pytestmark = pytest.mark.gpu
+
+
+def test_tsync_golden_grid():
+    clusters, cases = tsync_vectors()
+    by_cluster = {}
+    for c in cases:
+        by_cluster.setdefault(c["cluster"], []).append(c)
+    for name, cs in by_cluster.items():
+        got = sync_makespan_grid(clusters[name], [c["bytes"] for c in cs], [c["k"] for c in cs])
+        assert got == [c["expect"] for c in cs], name
+
+
+def test_partition_grid_pipeline_schedule():
+    c = synth_cluster("ps", 1, 1, 1.0, 0.0)
+    assert [sync_makespan(c, 100, k) for k in (1, 2, 3, 4)] == [200, 150, 134, 125]
+    with pytest.raises(Error, match="partition count must be >= 1"):
+        sync_makespan(c, 100, 0)
+
+
+def _ps_fixture():
+    """test_replay.cpp:472-490: one worker, one server, 1 B/us, 100 B tensor."""
+    c = synth_cluster("ps", 1, 1, 1.0, 0.0)
+    b = GraphBuilder()
+    b.set_cluster(c)
+    b.add_op(Op("w0->BW.a", OpKind.BW, "w0", DeviceId.compute("w0"), 10))
+    b.add_op(Op("w0->IN.g0", OpKind.VIRTUAL_IN, "w0", DeviceId.compute("w0"), 0))
+    b.add_op(Op("w0->OUT.g0", OpKind.VIRTUAL_OUT, "w0", DeviceId.compute("w0"), 0))
+    b.add_edge("w0->BW.a", "w0->IN.g0")
+    splice(b, expand_ps("g0", 100, c))
+    return b.build()
+
+
+def test_partial_replay_of_ps_tensor():
+    g = _ps_fixture()
+    assert partial_replay(g, "g0", 1) == 200
+    assert partial_replay(g, "g0", 2) == 150
+    with pytest.raises(LookupError_):
+        partial_replay(g, "nope", 1)
+    with pytest.raises(Error):
+        partial_replay(g, "g0", 0)
+    assert replay(g).iteration_time_us == 210
+
+
+def test_ingest_built_graphs_on_gpu(engine):
+    vs = synth_vectors()
+    graphs = []
+    for v in vs:
+        s = v["spec"]
+        c = synth_cluster(s["scheme"], s["workers"], s["ps_count"], s["bandwidth_bytes_per_us"],
+                          s["latency_us"])
+        graphs.append(layered_graph(LayeredModel(s["fw_dur_us"], s["bw_dur_us"],
+                                                 s["tensor_bytes"], s["update_dur_us"]), c,
+                                    v["part_k"]))
+    batch = engine.batch([g.csr for g in graphs])
+    batch.replay(True)
+    ms, st, er, start, end = batch.results(schedule=True)
+    paths = batch.critical_paths()
+    for i, v in enumerate(vs):
+        a, b = int(batch.op_off[i]), int(batch.op_off[i + 1])
+        assert st[i] == 0 and ms[i] == v["T"]
+        d = hashlib.sha256(np.concatenate([start[a:b], end[a:b]]).astype("<i8").tobytes())
+        assert d.hexdigest() == v["schedule_sha256"]
+        assert paths[i].tolist() == v["path"]
