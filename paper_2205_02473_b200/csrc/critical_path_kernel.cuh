@@ -36,11 +36,11 @@ __device__ __forceinline__ uint32_t tl_prev(uint32_t v, const Cand& c,
 __device__ __forceinline__ uint32_t tl_next(uint32_t v, const Cand& c,
                                             const uint32_t* qbuf,
                                             const uint32_t* qpos,
-                                            const uint32_t* devoff) {
+                                            const uint32_t* dhead) {
   if (c.flags[v] & 1u) return kNone;
   const uint32_t q = qpos[v];
   if (q == kNone) return kNone;
-  return q + 1 < devoff[c.dev[v] + 1] ? qbuf[q + 1] : kNone;
+  return q + 1 < dhead[c.dev[v]] ? qbuf[q + 1] : kNone;
 }
 
 __global__ void __launch_bounds__(128) critical_path_kernel(
@@ -63,6 +63,7 @@ __global__ void __launch_bounds__(128) critical_path_kernel(
     const uint32_t* qbuf = S.qbuf + oo;
     const uint32_t* qpos = S.qpos + oo;
     const uint32_t* devoff = S.devoff + c.dof_off;
+    const uint32_t* dhead = S.dhead + c.dev_off;
     uint32_t* poff = P.pred_off + P.po_off[cid];
     uint32_t* pred = P.pred + P.e_off[cid];
     uint32_t* good = P.good + oo;
@@ -152,7 +153,7 @@ __global__ void __launch_bounds__(128) critical_path_kernel(
         if (e < se)
           s = c.succ[e];
         else if (e == se)
-          s = tl_next(cur, c, qbuf, qpos, devoff);
+          s = tl_next(cur, c, qbuf, qpos, dhead);
         if (s != kNone && __ldcg(&good[s]) && st[s] == ec) best = min(best, s);
         if (e >= se) break;
       }

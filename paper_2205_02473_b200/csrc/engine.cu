@@ -263,7 +263,8 @@ int build_batch(dpro_ctx* ctx, dpro_batch* b, const dpro_csr* cands) {
   const size_t s_dof = align16(sdo * 4 + 4);
   const size_t s_dst = align16(sd * sizeof(DevSt) + 16);
   const size_t s_busy = align16(sd * 8 + 8);
-  CU(b->scratch.ensure(4 * s_u32 + s_u8 + s_dof + s_dst + s_busy));
+  const size_t s_dh = align16(sd * 4 + 4);
+  CU(b->scratch.ensure(4 * s_u32 + s_u8 + s_dof + s_dst + s_busy + s_dh));
   size_t o = 0;
   b->S.indeg = b->scratch.as<uint32_t>(o); o += s_u32;
   b->S.qbuf = b->scratch.as<uint32_t>(o); o += s_u32;
@@ -273,6 +274,7 @@ int build_batch(dpro_ctx* ctx, dpro_batch* b, const dpro_csr* cands) {
   b->S.devoff = b->scratch.as<uint32_t>(o); o += s_dof;
   b->S.dstate = b->scratch.as<DevSt>(o); o += s_dst;
   b->S.busy = b->scratch.as<long long>(o); o += s_busy;
+  b->S.dhead = b->scratch.as<uint32_t>(o); o += s_dh;
   // outputs: makespan, err (i64), status (i32), start, end (i64 [sum n])
   const size_t o_b64 = align16(size_t(n) * 8 + 8);
   const size_t o_b32 = align16(size_t(n) * 4 + 4);
@@ -415,10 +417,21 @@ int dpro_cuda_batch_timelines(dpro_ctx* ctx, dpro_batch* b, int32_t cand,
   if (!b->replayed) return set_err(ctx, DPRO_EINVAL, "batch not replayed");
   CU(cudaSetDevice(ctx->device));
   const Cand& h = b->hc[cand];
-  if (order) CU(cudaMemcpyAsync(order, b->S.qbuf + h.op_off, size_t(h.n) * 4, cudaMemcpyDeviceToHost, ctx->stream));
-  if (dev_off) CU(cudaMemcpyAsync(dev_off, b->S.devoff + h.dof_off, size_t(h.d + 1) * 4, cudaMemcpyDeviceToHost, ctx->stream));
-  if (busy) CU(cudaMemcpyAsync(busy, b->S.busy + h.dev_off, size_t(h.d) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  // queue regions hold only the dispatched prefix [devoff[d], dhead[d]);
+  // ops never scheduled (cycles / init quirk) leave holes: compact them out
+  std::vector<uint32_t> q(h.n), doff(h.d + 1), dh(h.d);
+  if (h.n) CU(cudaMemcpyAsync(q.data(), b->S.qbuf + h.op_off, size_t(h.n) * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaMemcpyAsync(doff.data(), b->S.devoff + h.dof_off, size_t(h.d + 1) * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  if (h.d) CU(cudaMemcpyAsync(dh.data(), b->S.dhead + h.dev_off, size_t(h.d) * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  if (busy && h.d) CU(cudaMemcpyAsync(busy, b->S.busy + h.dev_off, size_t(h.d) * 8, cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
+  uint32_t k = 0;
+  for (uint32_t d = 0; d < h.d; ++d) {
+    if (dev_off) dev_off[d] = k;
+    for (uint32_t p = doff[d]; p < dh[d]; ++p, ++k)
+      if (order) order[k] = q[p];
+  }
+  if (dev_off) dev_off[h.d] = k;
   return DPRO_OK;
 }
 

@@ -61,6 +61,7 @@ struct Scratch {
   uint32_t* devoff;  // [sum (d+1)]
   DevSt* dstate;     // [sum d]  global fallback for device state
   long long* busy;   // [sum d]
+  uint32_t* dhead;   // [sum d]  end of the dispatched prefix of each region
 };
 
 struct Outs {
@@ -449,7 +450,10 @@ __device__ void replay_candidate(const Cand& c, int cid, DevSt* ds,
   const unsigned long long vc = warp_sum64(R.vcount);
   const unsigned long long dc = warp_sum64(R.dcount);
   const long long T = warp_max64(R.tmax);
-  for (uint32_t d = lane; d < D; d += 32) S.busy[c.dev_off + d] = ds[d].busy;
+  for (uint32_t d = lane; d < D; d += 32) {
+    S.busy[c.dev_off + d] = ds[d].busy;
+    S.dhead[c.dev_off + d] = ds[d].head;
+  }
   const uint32_t remaining = n - static_cast<uint32_t>(vc + dc);  // uint32 wrap
   if (remaining != 0u) {
     unsigned long long stuck = 0;
