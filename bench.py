@@ -161,8 +161,9 @@ def run_reference(args) -> None:
     w, graphs = build_candidates(args.config, min(args.batch, 4 * threads), 0, threads)
     vals = []
     cpu = None
+    per_step = min(args.ref_seconds, 150.0 / max(1, args.warmup + args.steps))
     for step in range(args.warmup + args.steps):
-        cpu = cpu_reference_time(graphs, budget_s=args.ref_seconds, threads=threads)
+        cpu = cpu_reference_time(graphs, budget_s=per_step, threads=threads)
         if step >= args.warmup:
             vals.append(cpu["value"])
     value = float(np.mean(vals))
