@@ -90,6 +90,10 @@ dpro_ctx* dpro_cuda_create(int device);
 void dpro_cuda_destroy(dpro_ctx* ctx);
 /* cudaStream_t the engine launches on (NULL: the legacy default stream). */
 int dpro_cuda_set_stream(dpro_ctx* ctx, void* stream);
+/* Engine options: "fast" (1: on-chip fast path with exact fallback, 0: the
+ * general kernel only), "ring" (fast-path queue capacity per device, power
+ * of two). Returns DPRO_EINVAL for unknown keys or values. */
+int dpro_cuda_set_option(dpro_ctx* ctx, const char* key, int64_t value);
 const char* dpro_cuda_last_error(dpro_ctx* ctx);
 
 /* ------------------------------------------------------------------------
@@ -123,6 +127,10 @@ int dpro_cuda_batch_results(dpro_ctx* ctx, dpro_batch* b, int64_t* makespan,
 int dpro_cuda_batch_timelines(dpro_ctx* ctx, dpro_batch* b, int32_t cand,
                               uint32_t* order, uint32_t* dev_off,
                               int64_t* busy);
+/* Counters of the last replay: stats[0] = candidates that took the general
+ * (fallback) path, stats[1] = fast-path shared memory bytes per candidate,
+ * stats[2] = fast-path candidates resident per SM. */
+int dpro_cuda_batch_stats(dpro_ctx* ctx, dpro_batch* b, int64_t* stats);
 /* scheduled[i] = 1 for ops the replay scheduled (host buffer [n_ops]); the
  * ids with 0 form CycleError::cycle (replay.cpp:108-117). */
 int dpro_cuda_batch_scheduled(dpro_ctx* ctx, dpro_batch* b, int32_t cand,

@@ -13,6 +13,8 @@
 
 #include "critical_path_kernel.cuh"
 #include "dpro_cuda.h"
+#include "pack_kernel.cuh"
+#include "replay_fast.cuh"
 #include "replay_kernel.cuh"
 
 struct dpro_graph;
@@ -25,7 +27,9 @@ namespace {
 using dpro_k::Cand;
 using dpro_k::CpScratch;
 using dpro_k::DevSt;
+using dpro_k::FastCfg;
 using dpro_k::Outs;
+using dpro_k::PackOut;
 using dpro_k::Scratch;
 
 constexpr int kWarpsPerBlock = 4;
@@ -80,6 +84,8 @@ struct dpro_ctx {
   size_t smem_optin = 0;
   std::string err;
   HostPinned staging;
+  int fast = 1;       // option "fast"
+  uint32_t ring = 4;  // option "ring"
 };
 
 struct dpro_batch {
@@ -95,8 +101,13 @@ struct dpro_batch {
   DevBuf outs;    // results
   DevBuf work;    // work counter
   DevBuf cp;      // critical-path scratch
+  DevBuf pack;    // packed replay layout (rec, erec, cnt0, offsets, info)
   Scratch S{};
   Outs O{};
+  PackOut P{};
+  FastCfg F{};
+  int blocks_per_sm_fast = 0;
+  unsigned last_fallbacks = 0;
   bool replayed = false;
   bool with_schedule = false;
 };
@@ -290,6 +301,40 @@ int build_batch(dpro_ctx* ctx, dpro_batch* b, const dpro_csr* cands) {
   CU(cudaMemcpyAsync(b->desc.p, b->hc.data(), sizeof(Cand) * n,
                      cudaMemcpyHostToDevice, ctx->stream));
   CU(b->work.ensure(16));
+  // packed replay layout (pack_kernel.cuh)
+  {
+    std::vector<unsigned long long> e_off(n), c_off(n);
+    unsigned long long eo = 0, co = 0;
+    for (int32_t i = 0; i < n; ++i) {
+      e_off[i] = eo;
+      c_off[i] = co;
+      eo += b->n_edges[i];
+      co += (b->n_ops[i] + 15) & ~15u;
+    }
+    const size_t s_rec = align16(so * 16 + 16), s_erec = align16(eo * 16 + 16),
+                 s_cnt = align16(co + 16), s_off = align16(size_t(n) * 8 + 8),
+                 s_info = align16(size_t(n) * sizeof(dpro_k::PackInfo) + 16);
+    CU(b->pack.ensure(s_rec + s_erec + s_cnt + 2 * s_off + s_info));
+    size_t po = 0;
+    b->P.rec = b->pack.as<uint4>(po); po += s_rec;
+    b->P.erec = b->pack.as<uint4>(po); po += s_erec;
+    b->P.cnt0 = b->pack.as<uint8_t>(po); po += s_cnt;
+    b->P.e_off = b->pack.as<unsigned long long>(po); po += s_off;
+    b->P.c_off = b->pack.as<unsigned long long>(po); po += s_off;
+    b->P.info = b->pack.as<dpro_k::PackInfo>(po); po += s_info;
+    CU(cudaMemcpyAsync(b->P.e_off, e_off.data(), size_t(n) * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaMemcpyAsync(b->P.c_off, c_off.data(), size_t(n) * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaMemsetAsync(b->P.cnt0, 0, s_cnt, ctx->stream));
+    if (n > 0) {
+      const int grid = std::min<int>(n, ctx->sm_count * 8);
+      bool need_indeg = false;
+      for (int32_t i = 0; i < n; ++i) need_indeg |= (b->hc[i].indeg == nullptr);
+      if (need_indeg)
+        dpro_k::count_indeg_kernel<<<grid, 256, 0, ctx->stream>>>(b->desc.as<Cand>(), n, b->S);
+      dpro_k::pack_kernel<<<grid, 256, 0, ctx->stream>>>(b->desc.as<Cand>(), n, b->S, b->P);
+      CU(cudaGetLastError());
+    }
+  }
   return DPRO_OK;
 }
 
@@ -355,11 +400,23 @@ void dpro_cuda_batch_destroy(dpro_ctx* ctx, dpro_batch* b) {
   delete b;
 }
 
-int dpro_cuda_batch_replay(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
-  if (!ctx || !b) return DPRO_EINVAL;
-  if (b->n == 0) return DPRO_OK;
-  CU(cudaSetDevice(ctx->device));
-  // shared memory: per warp, device state for up to dcap devices
+int dpro_cuda_set_option(dpro_ctx* ctx, const char* key, int64_t value) {
+  if (!ctx || !key) return DPRO_EINVAL;
+  const std::string k(key);
+  if (k == "fast" && (value == 0 || value == 1)) {
+    ctx->fast = static_cast<int>(value);
+    return DPRO_OK;
+  }
+  if (k == "ring" && value >= 2 && value <= 64 && (value & (value - 1)) == 0) {
+    ctx->ring = static_cast<uint32_t>(value);
+    return DPRO_OK;
+  }
+  return set_err(ctx, DPRO_EINVAL, "unknown option or value: " + k);
+}
+
+namespace {
+
+int launch_general(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
   size_t budget = std::min<size_t>(ctx->smem_optin, 200 * 1024);
   uint32_t dcap = static_cast<uint32_t>((budget - kSmemHeader) / (kWarpsPerBlock * sizeof(DevSt)));
   dcap = std::min<uint32_t>(dcap, std::max<uint32_t>(b->max_d, 1));
@@ -375,8 +432,69 @@ int dpro_cuda_batch_replay(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) 
       b->desc.as<Cand>(), b->n, b->S, b->O, want_schedule ? 1 : 0,
       b->work.as<unsigned>(), dcap);
   CU(cudaGetLastError());
+  return DPRO_OK;
+}
+
+// Fast-path shared memory per candidate (one warp per block):
+// devices x (DevF + ring) + virtual worklist + misc + u8 counters.
+size_t fast_bytes(uint32_t dcap, uint32_t qc, uint32_t vs, uint32_t vcap) {
+  return size_t(dcap) * (sizeof(dpro_k::DevF) + 16 * qc) + 16 * vs + 16 + vcap;
+}
+
+int launch_fast(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
+  FastCfg F;
+  F.qc = ctx->ring;
+  F.vs = 64;
+  F.dcap = std::max<uint32_t>(1, std::min<uint32_t>(b->max_d, 2048));
+  uint32_t max_n = 16;
+  for (auto v : b->n_ops) max_n = std::max(max_n, v);
+  F.vcap = (max_n + 15) & ~15u;
+  const size_t limit = ctx->smem_optin;
+  while (fast_bytes(F.dcap, F.qc, F.vs, F.vcap) > limit && F.vcap > 16)
+    F.vcap = std::max<uint32_t>(16, (F.vcap / 2 + 15) & ~15u);
+  while (fast_bytes(F.dcap, F.qc, F.vs, F.vcap) > limit && F.dcap > 1) F.dcap /= 2;
+  const size_t smem = fast_bytes(F.dcap, F.qc, F.vs, F.vcap);
+  F.warp_bytes = static_cast<uint32_t>(smem);
+  CU(cudaFuncSetAttribute(dpro_k::replay_fast_kernel,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int blocks_per_sm = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, dpro_k::replay_fast_kernel,
+                                                   32, smem));
+  blocks_per_sm = std::max(blocks_per_sm, 1);
+  b->blocks_per_sm_fast = blocks_per_sm;
+  const int grid = std::max(1, std::min(b->n, ctx->sm_count * blocks_per_sm));
+  CU(cudaMemsetAsync(b->work.p, 0, 8, ctx->stream));
+  b->F = F;
+  dpro_k::replay_fast_kernel<<<grid, 32, smem, ctx->stream>>>(
+      b->desc.as<Cand>(), b->n, b->S, b->O, b->P, F, want_schedule ? 1 : 0,
+      b->work.as<unsigned>(), b->work.as<unsigned>() + 1);
+  CU(cudaGetLastError());
+  return DPRO_OK;
+}
+
+}  // namespace
+
+int dpro_cuda_batch_replay(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
+  if (!ctx || !b) return DPRO_EINVAL;
+  if (b->n == 0) return DPRO_OK;
+  CU(cudaSetDevice(ctx->device));
+  const int st = ctx->fast ? launch_fast(ctx, b, want_schedule)
+                           : launch_general(ctx, b, want_schedule);
+  if (st != DPRO_OK) return st;
   b->replayed = true;
   b->with_schedule = want_schedule != 0;
+  return DPRO_OK;
+}
+
+int dpro_cuda_batch_stats(dpro_ctx* ctx, dpro_batch* b, int64_t* stats) {
+  if (!ctx || !b || !stats) return DPRO_EINVAL;
+  CU(cudaSetDevice(ctx->device));
+  unsigned w[2] = {0, 0};
+  CU(cudaMemcpyAsync(w, b->work.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  stats[0] = ctx->fast ? w[1] : b->n;
+  stats[1] = b->F.warp_bytes;
+  stats[2] = b->blocks_per_sm_fast;
   return DPRO_OK;
 }
 
