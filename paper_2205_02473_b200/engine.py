@@ -86,6 +86,12 @@ class Engine:
     def set_stream(self, stream_handle: int | None) -> None:
         _check(self.ctx, N.lib.dpro_cuda_set_stream(self.ctx, stream_handle), "set_stream")
 
+    def set_option(self, key: str, value: int) -> None:
+        """'fast' (1 on-chip fast path + exact fallback, 0 general kernel),
+        'ring' (fast-path queue capacity per device)."""
+        _check(self.ctx, N.lib.dpro_cuda_set_option(self.ctx, key.encode(), int(value)),
+               f"set_option({key})")
+
     def batch(self, cands: Sequence[Csr] | Sequence[N.DproCsr],
               memspace: int = N.DPRO_HOST) -> "Batch":
         return Batch(self, cands, memspace)
@@ -141,6 +147,13 @@ class Batch:
                N.lib.dpro_cuda_batch_replay(self.engine.ctx, self.handle, int(want_schedule)),
                "batch_replay")
         self.with_schedule = want_schedule
+
+    def stats(self) -> dict:
+        st = np.zeros(3, np.int64)
+        _check(self.engine.ctx, N.lib.dpro_cuda_batch_stats(self.engine.ctx, self.handle,
+                                                            N.ptr(st)), "batch_stats")
+        return {"fallbacks": int(st[0]), "fast_smem_bytes": int(st[1]),
+                "fast_blocks_per_sm": int(st[2])}
 
     def device_results(self) -> dict:
         ps = [C.c_void_p() for _ in range(5)]

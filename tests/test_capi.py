@@ -32,3 +32,7 @@ def test_product_package_never_imports_oracle():
     pkg = pathlib.Path(N.__file__).parent
     for f in pkg.rglob("*.py"):
         assert "oracle" not in f.read_text().replace("# oracle", ""), f
+
+
+def test_options_rejected_without_context():
+    assert N.lib.dpro_cuda_set_option(None, b"fast", 1) == N.DPRO_EINVAL

@@ -45,14 +45,26 @@ def _batch_check(engine, graphs, expects, label):
                     assert (busy[d] / T if T > 0 else 0.0) == pytest.approx(u, abs=0), name
 
 
-def test_reference_golden_vectors_bit_exact(engine):
+@pytest.fixture(params=["fast", "general", "fast_ring2"])
+def mode_engine(engine, request):
+    """Both kernels: the on-chip fast path (with exact fallback) and the
+    general global-memory kernel; ring=2 forces frequent fast-path bail-outs."""
+    engine.set_option("fast", 0 if request.param == "general" else 1)
+    engine.set_option("ring", 2 if request.param == "fast_ring2" else 4)
+    yield engine
+    engine.set_option("fast", 1)
+    engine.set_option("ring", 4)
+
+
+def test_reference_golden_vectors_bit_exact(mode_engine):
     vecs = replay_vectors()
     graphs = [graph_from_json(v["graph"]) for v in vecs]
-    _batch_check(engine, graphs, [v["expect"] for v in vecs], "golden")
+    _batch_check(mode_engine, graphs, [v["expect"] for v in vecs], "golden")
 
 
 @pytest.mark.parametrize("seed", range(4))
-def test_fuzz_against_c_oracle(engine, port, seed):
+def test_fuzz_against_c_oracle(mode_engine, port, seed):
+    engine = mode_engine
     rng = np.random.default_rng(1000 + seed)
     graphs = []
     for t in range(1500):

@@ -57,7 +57,9 @@ def test_partial_replay_of_ps_tensor():
     assert replay(g).iteration_time_us == 210
 
 
-def test_ingest_built_graphs_on_gpu(engine):
+@pytest.mark.parametrize("fast", [1, 0])
+def test_ingest_built_graphs_on_gpu(engine, fast):
+    engine.set_option("fast", fast)
     vs = synth_vectors()
     graphs = []
     for v in vs:
@@ -77,3 +79,6 @@ def test_ingest_built_graphs_on_gpu(engine):
         d = hashlib.sha256(np.concatenate([start[a:b], end[a:b]]).astype("<i8").tobytes())
         assert d.hexdigest() == v["schedule_sha256"]
         assert paths[i].tolist() == v["path"]
+    if fast:
+        assert batch.stats()["fallbacks"] == 0
+    engine.set_option("fast", 1)
