@@ -248,6 +248,7 @@ def run_ours(args) -> None:
         total_ms = float(t.item())
     ms, st, er, _, _ = batch.results()
     ok = int((st == 0).sum())
+    kstats = batch.stats()
 
     # e2e: the C-ABI one-shot call with HOST buffers (H2D upload of every
     # candidate + D2H of makespans/status/err inside the timed region)
@@ -302,7 +303,10 @@ def run_ours(args) -> None:
                    "parallelism": f"candidates sharded over {world} GPU(s)",
                    "l2": "inputs (%.2f GB CSR) larger than L2; no flush" % (algo_bytes / 1e9),
                    "node_updates_per_s": value * float(batch.n_ops.mean()),
-                   "build_s": round(t_build, 2), "status_ok": ok},
+                   "build_s": round(t_build, 2), "status_ok": ok,
+                   "kernel": "replay_fast_kernel (general-path fallbacks: %d)" % kstats["fallbacks"],
+                   "fast_smem_bytes_per_candidate": kstats["fast_smem_bytes"],
+                   "fast_candidates_per_sm": kstats["fast_blocks_per_sm"]},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": _ncu_traffic(),
                      "algorithmic_bytes_per_launch": algo_bytes, "peak_source": peak_src,
