@@ -107,7 +107,7 @@ struct dpro_batch {
   PackOut P{};
   FastCfg F{};
   int blocks_per_sm_fast = 0;
-  unsigned last_fallbacks = 0;
+  std::vector<dpro_k::PackInfo> info;  // host copy (read once after pack)
   bool replayed = false;
   bool with_schedule = false;
 };
@@ -311,20 +311,24 @@ int build_batch(dpro_ctx* ctx, dpro_batch* b, const dpro_csr* cands) {
       eo += b->n_edges[i];
       co += (b->n_ops[i] + 15) & ~15u;
     }
-    const size_t s_rec = align16(so * 16 + 16), s_erec = align16(eo * 16 + 16),
-                 s_cnt = align16(co + 16), s_off = align16(size_t(n) * 8 + 8),
+    const size_t s_rec = align16(so * 32 + 32), s_erec = align16(eo * 32 + 32),
+                 s_cnt = align16(co + 16), s_u32 = align16(so * 4 + 4),
+                 s_off = align16(size_t(n) * 8 + 8),
                  s_info = align16(size_t(n) * sizeof(dpro_k::PackInfo) + 16);
-    CU(b->pack.ensure(s_rec + s_erec + s_cnt + 2 * s_off + s_info));
+    CU(b->pack.ensure(s_rec + s_erec + s_cnt + 2 * s_u32 + 2 * s_off + s_info));
     size_t po = 0;
     b->P.rec = b->pack.as<uint4>(po); po += s_rec;
     b->P.erec = b->pack.as<uint4>(po); po += s_erec;
     b->P.cnt0 = b->pack.as<uint8_t>(po); po += s_cnt;
+    b->P.srcs = b->pack.as<uint32_t>(po); po += s_u32;
+    b->P.cidx = b->pack.as<uint32_t>(po); po += s_u32;
     b->P.e_off = b->pack.as<unsigned long long>(po); po += s_off;
     b->P.c_off = b->pack.as<unsigned long long>(po); po += s_off;
     b->P.info = b->pack.as<dpro_k::PackInfo>(po); po += s_info;
     CU(cudaMemcpyAsync(b->P.e_off, e_off.data(), size_t(n) * 8, cudaMemcpyHostToDevice, ctx->stream));
     CU(cudaMemcpyAsync(b->P.c_off, c_off.data(), size_t(n) * 8, cudaMemcpyHostToDevice, ctx->stream));
     CU(cudaMemsetAsync(b->P.cnt0, 0, s_cnt, ctx->stream));
+    b->info.assign(n, dpro_k::PackInfo{});
     if (n > 0) {
       const int grid = std::min<int>(n, ctx->sm_count * 8);
       bool need_indeg = false;
@@ -333,6 +337,9 @@ int build_batch(dpro_ctx* ctx, dpro_batch* b, const dpro_csr* cands) {
         dpro_k::count_indeg_kernel<<<grid, 256, 0, ctx->stream>>>(b->desc.as<Cand>(), n, b->S);
       dpro_k::pack_kernel<<<grid, 256, 0, ctx->stream>>>(b->desc.as<Cand>(), n, b->S, b->P);
       CU(cudaGetLastError());
+      CU(cudaMemcpyAsync(b->info.data(), b->P.info, size_t(n) * sizeof(dpro_k::PackInfo),
+                         cudaMemcpyDeviceToHost, ctx->stream));
+      CU(cudaStreamSynchronize(ctx->stream));
     }
   }
   return DPRO_OK;
@@ -414,6 +421,8 @@ int dpro_cuda_set_option(dpro_ctx* ctx, const char* key, int64_t value) {
   return set_err(ctx, DPRO_EINVAL, "unknown option or value: " + k);
 }
 
+}  // extern "C"
+
 namespace {
 
 int launch_general(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
@@ -436,43 +445,65 @@ int launch_general(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
 }
 
 // Fast-path shared memory per candidate (one warp per block):
-// devices x (DevF + ring) + virtual worklist + misc + u8 counters.
-size_t fast_bytes(uint32_t dcap, uint32_t qc, uint32_t vs, uint32_t vcap) {
-  return size_t(dcap) * (sizeof(dpro_k::DevF) + 16 * qc) + 16 * vs + 16 + vcap;
+// devices x (DevF + ring) + virtual worklist + misc words + u8 counters.
+size_t fast_bytes(uint32_t dcap, uint32_t qc, uint32_t vs, uint32_t ccap) {
+  return size_t(dcap) * (sizeof(dpro_k::DevF) + 16 * qc) + 16 * vs +
+         4 * dpro_k::fast_misc_words() + ccap;
 }
 
-int launch_fast(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
-  FastCfg F;
-  F.qc = ctx->ring;
-  F.vs = 64;
-  F.dcap = std::max<uint32_t>(1, std::min<uint32_t>(b->max_d, 2048));
-  uint32_t max_n = 16;
-  for (auto v : b->n_ops) max_n = std::max(max_n, v);
-  F.vcap = (max_n + 15) & ~15u;
-  const size_t limit = ctx->smem_optin;
-  while (fast_bytes(F.dcap, F.qc, F.vs, F.vcap) > limit && F.vcap > 16)
-    F.vcap = std::max<uint32_t>(16, (F.vcap / 2 + 15) & ~15u);
-  while (fast_bytes(F.dcap, F.qc, F.vs, F.vcap) > limit && F.dcap > 1) F.dcap /= 2;
-  const size_t smem = fast_bytes(F.dcap, F.qc, F.vs, F.vcap);
-  F.warp_bytes = static_cast<uint32_t>(smem);
-  CU(cudaFuncSetAttribute(dpro_k::replay_fast_kernel,
+template <int KD>
+int launch_fast_kd(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule, FastCfg F) {
+  const size_t smem = F.warp_bytes;
+  CU(cudaFuncSetAttribute(dpro_k::replay_fast_kernel<KD>,
                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int blocks_per_sm = 0;
-  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, dpro_k::replay_fast_kernel,
-                                                   32, smem));
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm,
+                                                   dpro_k::replay_fast_kernel<KD>, 32, smem));
   blocks_per_sm = std::max(blocks_per_sm, 1);
   b->blocks_per_sm_fast = blocks_per_sm;
   const int grid = std::max(1, std::min(b->n, ctx->sm_count * blocks_per_sm));
   CU(cudaMemsetAsync(b->work.p, 0, 8, ctx->stream));
   b->F = F;
-  dpro_k::replay_fast_kernel<<<grid, 32, smem, ctx->stream>>>(
+  dpro_k::replay_fast_kernel<KD><<<grid, 32, smem, ctx->stream>>>(
       b->desc.as<Cand>(), b->n, b->S, b->O, b->P, F, want_schedule ? 1 : 0,
       b->work.as<unsigned>(), b->work.as<unsigned>() + 1);
   CU(cudaGetLastError());
   return DPRO_OK;
 }
 
+int launch_fast(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
+  FastCfg F;
+  F.qc = ctx->ring;
+  F.vs = 64;
+  uint32_t max_cnt = 16;
+  for (const auto& inf : b->info) max_cnt = std::max(max_cnt, inf.n_cnt);
+  uint32_t kd = std::max<uint32_t>(1, (b->max_d + 31) / 32);
+  if (kd > 8) kd = kd <= 12 ? 12 : 16;
+  F.kd = kd;
+  F.dcap = std::max<uint32_t>(1, std::min<uint32_t>(b->max_d, 32 * kd));
+  F.ccap = (max_cnt + 15) & ~15u;
+  const size_t limit = ctx->smem_optin;
+  while (fast_bytes(F.dcap, F.qc, F.vs, F.ccap) > limit && F.ccap > 16)
+    F.ccap = std::max<uint32_t>(16, (F.ccap / 2 + 15) & ~15u);
+  while (fast_bytes(F.dcap, F.qc, F.vs, F.ccap) > limit && F.dcap > 1) F.dcap /= 2;
+  F.warp_bytes = static_cast<uint32_t>(fast_bytes(F.dcap, F.qc, F.vs, F.ccap));
+  switch (kd) {
+    case 1: return launch_fast_kd<1>(ctx, b, want_schedule, F);
+    case 2: return launch_fast_kd<2>(ctx, b, want_schedule, F);
+    case 3: return launch_fast_kd<3>(ctx, b, want_schedule, F);
+    case 4: return launch_fast_kd<4>(ctx, b, want_schedule, F);
+    case 5: return launch_fast_kd<5>(ctx, b, want_schedule, F);
+    case 6: return launch_fast_kd<6>(ctx, b, want_schedule, F);
+    case 7: return launch_fast_kd<7>(ctx, b, want_schedule, F);
+    case 8: return launch_fast_kd<8>(ctx, b, want_schedule, F);
+    case 12: return launch_fast_kd<12>(ctx, b, want_schedule, F);
+    default: return launch_fast_kd<16>(ctx, b, want_schedule, F);
+  }
+}
+
 }  // namespace
+
+extern "C" {
 
 int dpro_cuda_batch_replay(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
   if (!ctx || !b) return DPRO_EINVAL;

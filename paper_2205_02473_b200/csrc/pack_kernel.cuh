@@ -1,16 +1,16 @@
 // Pack: caller CSR (SoA, index order) -> the engine's replay layout.
 //
 // Runs once when a batch is registered (engine.cu). Per candidate:
-//   rec[i]  = {dur_i, devflags_i, succ_beg_i, succ_end_i}         (uint4)
-//   erec[k] = {s, dur_s, devflags_s, succ_beg_s} for edge k: i->s  (uint4)
-//   cnt0[i] = min(indeg_i, 255)                                    (u8)
+//   rec[i]  = 32-byte record of op i     {i, dur, devflags, sb | se, cidx}
+//   erec[k] = the record of s for edge k: i -> s (same 32-byte format)
+//   cnt0[c] = indeg of the c-th multi-predecessor op (compact u8 counters)
+//   srcs    = ops with no predecessor (unordered; the replay sorts them)
 //   devoff  = exclusive scan of non-virtual ops per device (timeline regions)
-//   info    = first op without duration, eligibility for the fast path.
-// The per-edge record carries everything the replay needs when the edge's
-// completion makes s ready (its device, virtual flag, duration and successor
-// range), so an event round touches one 16-byte record per edge instead of
-// five dependent SoA loads (proj/src/replay.cpp:60-72,80-87 read kind,
-// device, dur and succ of s at exactly that moment).
+//   info    = first op without duration, fast-path eligibility, sizes.
+// The per-edge record carries everything the replay needs at the moment the
+// edge's completion makes s ready (device, virtual flag, duration, successor
+// range, counter slot) -- exactly what proj/src/replay.cpp:60-72,80-87 reads
+// about s then -- so an event round touches one record per edge.
 #pragma once
 
 #include "replay_kernel.cuh"
@@ -19,88 +19,107 @@ namespace dpro_k {
 
 constexpr uint32_t kDevMask = 0xFFFFu;
 constexpr uint32_t kFVirt = 1u << 16;
-constexpr uint32_t kFComm = 1u << 17;
-constexpr uint32_t kFMulti = 1u << 18;   // indeg >= 2: counted in smem
-constexpr uint32_t kCntShift = 20;       // successor count; kCntMax: see rec
-constexpr uint32_t kCntMax = 4095u;
+constexpr uint32_t kFMulti = 1u << 17;  // >= 2 predecessors: has a counter
+
+// not_fast bits
+constexpr uint32_t kNfDur = 1u;       // |dur| >= 2^31 or sum of dur >= 2^31
+constexpr uint32_t kNfIndeg = 2u;     // some indeg >= 255
+constexpr uint32_t kNfVsrc = 4u;      // virtual op without predecessors
+constexpr uint32_t kNfDev = 8u;       // device id out of range
 
 struct PackInfo {
   uint32_t first_missing;  // kNone: every non-virtual op has dur >= 0
-  uint32_t not_fast;       // bit0 dur>int32, bit1 indeg>=255, bit2 virtual
-                           // source, bit3 bad device id
-  uint32_t max_indeg;
-  uint32_t pad;
+  uint32_t not_fast;
+  uint32_t n_cnt;          // multi-predecessor ops (compact counters)
+  uint32_t n_src;          // ops without predecessors
+  unsigned long long dur_sum;
 };
 
 struct PackOut {
-  uint4* rec;                  // [sum n]
-  uint4* erec;                 // [sum e]
-  uint8_t* cnt0;               // [sum n16] (each candidate 16-byte aligned)
-  unsigned long long* e_off;   // per candidate offset into erec
-  unsigned long long* c_off;   // per candidate offset into cnt0
+  uint4* rec;                  // [2 * sum n]
+  uint4* erec;                 // [2 * sum e]
+  uint8_t* cnt0;               // [sum n16]
+  uint32_t* srcs;              // [sum n]
+  uint32_t* cidx;              // [sum n] scratch: counter slot per op
+  unsigned long long* e_off;   // per candidate offset into erec (in edges)
+  unsigned long long* c_off;   // per candidate byte offset into cnt0
   PackInfo* info;              // [B]
 };
 
-__device__ __forceinline__ uint32_t devflags_of(const Cand& c, uint32_t i,
-                                                uint32_t indeg) {
-  const uint32_t f = c.flags[i];
-  const uint32_t cnt = c.succ_off[i + 1] - c.succ_off[i];
-  return (uint32_t(c.dev[i]) & kDevMask) | ((f & 1u) ? kFVirt : 0u) |
-         ((f & 2u) ? kFComm : 0u) | (indeg >= 2 ? kFMulti : 0u) |
-         (min(cnt, kCntMax) << kCntShift);
+__device__ __forceinline__ void put_rec(uint4* dst, uint32_t s, const Cand& c,
+                                        const uint32_t* indeg, const uint32_t* cidx) {
+  const uint32_t f = c.flags[s];
+  const uint32_t ind = indeg[s];
+  const uint32_t df = (uint32_t(c.dev[s]) & kDevMask) | ((f & 1u) ? kFVirt : 0u) |
+                      (ind >= 2 ? kFMulti : 0u);
+  const long long du = ld_dur(c, s);
+  dst[0] = make_uint4(s, static_cast<uint32_t>(static_cast<int>(du)), df, c.succ_off[s]);
+  dst[1] = make_uint4(c.succ_off[s + 1], ind >= 2 ? cidx[s] : 0u, 0u, 0u);
 }
 
-// One block per candidate (grid-stride). indeg must be present (the host
-// upload computes it when the caller passes NULL; device batches without
-// indeg are counted into S.indeg first by count_indeg_kernel).
+// One block per candidate (grid-stride). indeg must be present (host upload
+// computes it; device batches without it go through count_indeg_kernel).
 __global__ void __launch_bounds__(256) pack_kernel(const Cand* __restrict__ cands,
                                                    int n_cands, Scratch S,
                                                    PackOut P) {
-  __shared__ uint32_t s_first, s_flags, s_max;
+  __shared__ uint32_t s_first, s_flags, s_ncnt, s_nsrc;
+  __shared__ unsigned long long s_sum;
   for (int cid = blockIdx.x; cid < n_cands; cid += gridDim.x) {
     const Cand c = cands[cid];
     const uint32_t n = c.n;
     const uint32_t* indeg = c.indeg ? c.indeg : S.indeg + c.op_off;
-    uint4* rec = P.rec + c.op_off;
-    uint4* erec = P.erec + P.e_off[cid];
+    uint4* rec = P.rec + 2 * c.op_off;
+    uint4* erec = P.erec + 2 * P.e_off[cid];
     uint8_t* cnt0 = P.cnt0 + P.c_off[cid];
+    uint32_t* srcs = P.srcs + c.op_off;
+    uint32_t* cidx = P.cidx + c.op_off;
     if (threadIdx.x == 0) {
       s_first = kNone;
       s_flags = 0;
-      s_max = 0;
+      s_ncnt = 0;
+      s_nsrc = 0;
+      s_sum = 0;
     }
     __syncthreads();
-    uint32_t flags = 0, mx = 0, first = kNone;
+    uint32_t flags = 0, first = kNone;
+    unsigned long long sum = 0;
+    // pass 1: counter slots, sources, checks
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
       const long long du = ld_dur(c, i);
-      const uint32_t f = c.flags[i];
+      const bool virt = c.flags[i] & 1u;
       const uint32_t ind = indeg[i];
-      const bool virt = f & 1u;
       if (!virt && du < 0) first = min(first, i);
-      if (du > 0x7FFFFFFFLL || du < -0x80000000LL) flags |= 1u;
-      if (ind >= 255u) flags |= 2u;
-      if (virt && ind == 0u) flags |= 4u;
-      if (!virt && c.dev[i] >= c.d) flags |= 8u;
-      mx = max(mx, ind);
-      const uint32_t df = devflags_of(c, i, ind);
-      rec[i] = make_uint4(static_cast<uint32_t>(static_cast<int>(du)), df,
-                          c.succ_off[i], c.succ_off[i + 1]);
-      cnt0[i] = static_cast<uint8_t>(min(ind, 255u));
-      for (uint32_t k = c.succ_off[i]; k < c.succ_off[i + 1]; ++k) {
-        const uint32_t s = c.succ[k];
-        erec[k] = make_uint4(s, static_cast<uint32_t>(static_cast<int>(ld_dur(c, s))),
-                             devflags_of(c, s, indeg[s]), c.succ_off[s]);
+      if (du > 0x7FFFFFFFLL || du < -0x80000000LL) flags |= kNfDur;
+      if (!virt && du > 0) sum += static_cast<unsigned long long>(du);
+      if (ind >= 255u) flags |= kNfIndeg;
+      if (virt && ind == 0u) flags |= kNfVsrc;
+      if (!virt && c.dev[i] >= c.d) flags |= kNfDev;
+      if (ind >= 2u) {
+        const uint32_t slot = atomicAdd(&s_ncnt, 1u);
+        cidx[i] = slot;
+        cnt0[slot] = static_cast<uint8_t>(min(ind, 255u));
+      } else if (ind == 0u) {
+        srcs[atomicAdd(&s_nsrc, 1u)] = i;
       }
     }
     if (first != kNone) atomicMin(&s_first, first);
     if (flags) atomicOr(&s_flags, flags);
-    if (mx) atomicMax(&s_max, mx);
+    if (sum) atomicAdd(&s_sum, sum);
     __syncthreads();
+    // pass 2: records
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+      put_rec(rec + 2 * i, i, c, indeg, cidx);
+      for (uint32_t k = c.succ_off[i]; k < c.succ_off[i + 1]; ++k)
+        put_rec(erec + 2 * k, c.succ[k], c, indeg, cidx);
+    }
     if (threadIdx.x == 0) {
-      P.info[cid].first_missing = s_first;
-      P.info[cid].not_fast = s_flags;
-      P.info[cid].max_indeg = s_max;
-      P.info[cid].pad = 0;
+      PackInfo inf;
+      inf.first_missing = s_first;
+      inf.not_fast = s_flags | (s_sum >= 0x7FFFFFFFull ? kNfDur : 0u);
+      inf.n_cnt = s_ncnt;
+      inf.n_src = s_nsrc;
+      inf.dur_sum = s_sum;
+      P.info[cid] = inf;
     }
     // timeline regions: per-device non-virtual op counts, exclusive scan
     uint32_t* devoff = S.devoff + c.dof_off;

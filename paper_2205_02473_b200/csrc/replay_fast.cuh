@@ -1,21 +1,24 @@
 // K1 fast path: exact batched replay with all mutable state on chip.
 //
-// Same round semantics as replay_kernel.cuh (and proj/src/replay.cpp:37-134);
-// what changes is where the state lives and what an event round touches:
-//   * per-candidate in-degree countdowns: u8 in shared memory (4 per 32-bit
-//     word, decremented with word atomics); ops with a single predecessor
-//     skip the counter entirely (devflags kFMulti);
-//   * per-device queues: shared-memory rings of QC 16-byte records (the
-//     packed successor record of pack_kernel.cuh), so dispatch reads the
-//     duration and the successor range from the queue entry itself;
-//   * device state: shared memory, lane-owned (device d -> lane d % 32);
-//   * the one global read left in a round is the completing op's edge
-//     records, prefetched to L2 when the op is enqueued and dispatched.
-// Anything the fast path cannot represent (a ring overflow, a virtual source
-// -> init quirk, indeg >= 255, int64 durations, more devices or ops than the
-// shared-memory budget, a cycle) falls back, inside the same launch, to the
-// general kernel (replay_candidate, global-memory state), so every
-// candidate's result is exact.
+// Same round semantics as replay_kernel.cuh (proj/src/replay.cpp:37-134);
+// what changes is where the state lives and what an event round touches.
+//   * one warp per candidate; lane l owns devices d = l + 32 j (j < KD); the
+//     in-flight end time of each owned device lives in a lane register, so
+//     the next event time is one REDUX.MIN over the warp (32-bit times: the
+//     pack pass proves sum(dur) < 2^31, hence every time fits);
+//   * a round only visits devices that completed or received arrivals
+//     (per-lane dirty bitmask in shared memory, set by producers);
+//   * per-device FIFOs are shared-memory rings of 16-byte entries
+//     {op, dur, succ_beg, succ_end}, sorted by (ready, index) on arrival;
+//   * in-degree countdowns exist only for ops with >= 2 predecessors, as
+//     compact u8 counters in shared memory (4 per word, word atomics);
+//   * the only global read in a round is the completing op's 32-byte edge
+//     records (pack_kernel.cuh), prefetched to L2 when the op is enqueued.
+// Whatever the fast path cannot represent (ring or worklist overflow, a
+// virtual source -> init quirk, indeg >= 255, durations that need 64-bit
+// times, too many devices / counters, a cycle) falls back inside the same
+// launch to the general kernel (replay_candidate, global state): every
+// candidate's result is exact either way.
 #pragma once
 
 #include "pack_kernel.cuh"
@@ -23,35 +26,38 @@
 
 namespace dpro_k {
 
+constexpr uint32_t kT32Inf = 0xFFFFFFFFu;
+
 struct __align__(16) DevF {
   uint32_t head, tail, tsort, segbeg;
-  uint32_t zlo, zhi, iop, pad;
-  long long iend, segt, busy, pad2;
-  uint4 ient;
+  uint32_t zlo, zhi, segt, busy;
+  uint4 ient;  // in-flight positive-duration op {op, dur, sb, se}
 };
-static_assert(sizeof(DevF) == 80, "DevF layout");
+static_assert(sizeof(DevF) == 48, "DevF layout");
 
 struct FastCfg {
-  uint32_t dcap;     // devices per warp
-  uint32_t vcap;     // ops per warp (u8 counters), multiple of 16
-  uint32_t qc;       // ring capacity per device (power of two)
-  uint32_t vs;       // virtual worklist capacity
+  uint32_t dcap;   // devices per warp (multiple of 32)
+  uint32_t ccap;   // compact counters per warp (bytes, multiple of 16)
+  uint32_t qc;     // ring capacity per device (power of two)
+  uint32_t vs;     // virtual worklist capacity
   uint32_t warp_bytes;
+  uint32_t kd;     // devices per lane (template parameter)
 };
 
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
+__host__ __device__ constexpr size_t fast_misc_words() { return 4 + 32; }
+
+template <int KD>
 struct FastWarp {
-  const Cand& c;
-  const uint4* __restrict__ rec;
-  const uint4* __restrict__ erec;
+  const uint4* __restrict__ erec;  // 2 x uint4 per edge
   DevF* dv;
-  uint4* q;            // [dcap][qc]
-  uint4* vstk;         // [vs]
-  uint32_t* cnt32;     // u8 counters packed in words
-  volatile uint32_t* misc;  // [0] vtop, [1] overflow
+  uint4* q;                 // [dcap][qc]
+  uint4* vstk;              // [vs]
+  volatile uint32_t* misc;  // [0] vtop [1] overflow [4..35] dirty masks
+  uint32_t* cw;             // compact counters (u8 in words)
   uint32_t qc, vs;
   uint32_t* qbuf;
   uint32_t* qpos;
@@ -59,55 +65,57 @@ struct FastWarp {
   long long* start;
   long long* end;
   bool want;
-  unsigned long long vcount = 0, dcount = 0;
-  long long tmax = 0;
+  uint32_t vcount = 0, dcount = 0, tmax = 0;
 
   __device__ __forceinline__ uint4* ring(uint32_t d) { return q + (size_t)d * qc; }
 
-  __device__ __forceinline__ void ready(const uint4& x, long long t) {
-    prefetch_l2(erec + x.w);  // its completion reads these edge records
-    if (x.z & kFVirt) {
+  // ready(s, t) of replay.cpp:60-72 for s reached through an edge record.
+  __device__ __forceinline__ void ready(const uint4& a, const uint4& b, uint32_t t) {
+    const uint4 e = make_uint4(a.x, a.y, a.w, b.x);  // {op, dur, sb, se}
+    if (a.z & kFVirt) {
       if (want) {
-        start[x.x] = t;
-        end[x.x] = t;
+        start[a.x] = t;
+        end[a.x] = t;
       }
       ++vcount;
       tmax = max(tmax, t);
       const uint32_t p = atomicAdd(const_cast<uint32_t*>(&misc[0]), 1u);
       if (p < vs)
-        vstk[p] = x;
+        vstk[p] = e;
       else
         misc[1] = 1u;
     } else {
-      const uint32_t d = x.z & kDevMask;
+      const uint32_t d = a.z & kDevMask;
       DevF& s = dv[d];
       const uint32_t pos = atomicAdd(&s.tail, 1u);
       const uint32_t zl = *reinterpret_cast<volatile uint32_t*>(&s.zlo);
       const uint32_t zh = *reinterpret_cast<volatile uint32_t*>(&s.zhi);
-      const uint32_t low = zl < zh ? zl : s.head;
-      if (pos - low >= qc)
+      const uint32_t low = zl < zh ? zl : *reinterpret_cast<volatile uint32_t*>(&s.head);
+      if (pos - low >= qc) {
         misc[1] = 1u;
-      else
-        ring(d)[pos & (qc - 1)] = x;
+      } else {
+        ring(d)[pos & (qc - 1)] = e;
+        atomicOr(const_cast<uint32_t*>(&misc[4 + (d & 31)]), 1u << (d >> 5));
+      }
     }
+    if (e.w > e.z) prefetch_l2(erec + 2 * e.z);
   }
 
-  __device__ __forceinline__ void complete(const uint4& e, long long t) {
-    const uint32_t sb = e.w;
-    const uint32_t cnt = e.z >> kCntShift;
-    const uint32_t se = cnt == kCntMax ? __ldg(&rec[e.x].w) : sb + cnt;
-    for (uint32_t k = sb; k < se; ++k) {
-      const uint4 x = __ldg(erec + k);
-      if (x.z & kFMulti) {
-        const uint32_t sh = 8u * (x.x & 3u);
-        const uint32_t old = atomicSub(&cnt32[x.x >> 2], 1u << sh);
+  // Completion of op e at t: successors (replay.cpp:100-103).
+  __device__ __forceinline__ void complete(const uint4& e, uint32_t t) {
+    for (uint32_t k = e.z; k < e.w; ++k) {
+      const uint4 a = __ldg(erec + 2 * k);
+      const uint4 b = __ldg(erec + 2 * k + 1);
+      if (a.z & kFMulti) {
+        const uint32_t sh = 8u * (b.y & 3u);
+        const uint32_t old = atomicSub(&cw[b.y >> 2], 1u << sh);
         if (((old >> sh) & 0xFFu) != 1u) continue;
       }
-      ready(x, t);
+      ready(a, b, t);
     }
   }
 
-  __device__ void drain_virtual(long long t, int lane) {
+  __device__ void drain_virtual(uint32_t t, int lane) {
     __syncwarp();
     for (;;) {
       const uint32_t n = misc[0];
@@ -123,18 +131,23 @@ struct FastWarp {
     }
   }
 
-  __device__ __forceinline__ void dispatch_dev(uint32_t d, long long t,
-                                               long long& lane_min, bool& lane_zero) {
+  // Owner-lane dispatch(t) for device d (replay.cpp:74-90) after merging
+  // this round's arrivals into the (ready, index)-ordered tail segment.
+  // Returns the device's in-flight end (kT32Inf when idle); sets *zero when
+  // zero-duration ops were dispatched (they complete next round).
+  __device__ __forceinline__ uint32_t dispatch_dev(uint32_t d, uint32_t t, uint32_t iend,
+                                                   bool* zero) {
     DevF& s = dv[d];
     uint4* r = ring(d);
     const uint32_t tail = *reinterpret_cast<volatile uint32_t*>(&s.tail);
     const uint32_t m = qc - 1;
+    uint32_t head = s.head;
     if (tail != s.tsort) {
       if (s.segt != t) {
         s.segbeg = s.tsort;
         s.segt = t;
       }
-      const uint32_t lo = max(s.segbeg, s.head);
+      const uint32_t lo = max(s.segbeg, head);
       for (uint32_t p = s.tsort; p < tail; ++p) {
         const uint4 x = r[p & m];
         uint32_t qq = p;
@@ -148,108 +161,88 @@ struct FastWarp {
       }
       s.tsort = tail;
     }
-    if (s.iop == kNone && s.head < tail) {
-      const uint32_t zlo = s.head;
-      uint32_t h = s.head;
-      long long busy = 0;
+    if (iend == kT32Inf && head < tail) {
+      const uint32_t zlo = head;
+      uint32_t busy = 0;
       const uint32_t base = devoff[d];
       bool infl = false;
-      while (h < tail) {
-        const uint4 x = r[h & m];
-        const long long du = static_cast<int>(x.y);
-        const long long en = t + du;
+      while (head < tail) {
+        const uint4 x = r[head & m];
+        const uint32_t en = t + x.y;
         if (want) {
           start[x.x] = t;
           end[x.x] = en;
-          qpos[x.x] = base + h;
+          qpos[x.x] = base + head;
         }
-        qbuf[base + h] = x.x;
-        ++h;
+        qbuf[base + head] = x.x;
+        ++head;
         ++dcount;
-        busy += du;
+        busy += x.y;
         tmax = max(tmax, en);
-        prefetch_l2(erec + x.w);
-        if (du > 0) {
-          s.iop = x.x;
-          s.iend = en;
+        if (x.y > 0) {
           s.ient = x;
+          iend = en;
           infl = true;
           break;
         }
       }
       s.busy += busy;
-      s.head = h;
+      s.head = head;
       s.zlo = zlo;
-      s.zhi = infl ? h - 1 : h;
+      const uint32_t zhi = infl ? head - 1 : head;
+      s.zhi = zhi;
+      if (zlo < zhi) *zero = true;
     }
-    if (s.iop != kNone) lane_min = min(lane_min, s.iend);
-    if (s.zlo < s.zhi) lane_zero = true;
+    return iend;
   }
 };
 
 // Returns false when the candidate must take the general path.
+template <int KD>
 __device__ bool replay_fast(const Cand& c, int cid, const uint4* rec, const uint4* erec,
-                            const uint8_t* cnt0, unsigned char* wsm, const FastCfg& F,
-                            const Scratch& S, const Outs& O, bool want_schedule) {
+                            const uint8_t* cnt0, const uint32_t* srcs, const PackInfo& info,
+                            unsigned char* wsm, const FastCfg& F, const Scratch& S,
+                            const Outs& O, bool want_schedule) {
   const int lane = threadIdx.x & 31;
   const uint32_t n = c.n, D = c.d;
   DevF* dv = reinterpret_cast<DevF*>(wsm);
   uint4* q = reinterpret_cast<uint4*>(wsm + sizeof(DevF) * F.dcap);
   uint4* vstk = q + (size_t)F.dcap * F.qc;
   volatile uint32_t* misc = reinterpret_cast<volatile uint32_t*>(vstk + F.vs);
-  uint32_t* cnt32 = const_cast<uint32_t*>(misc) + 4;
+  uint32_t* cw = const_cast<uint32_t*>(misc) + fast_misc_words();
   const unsigned long long oo = c.op_off;
 
-  FastWarp W{c, rec, erec, dv, q, vstk, cnt32, misc, F.qc, F.vs,
-             S.qbuf + oo, S.qpos + oo, S.devoff + c.dof_off,
-             want_schedule ? O.start + oo : nullptr, want_schedule ? O.end + oo : nullptr,
-             want_schedule};
+  FastWarp<KD> W{erec, dv, q, vstk, misc, cw, F.qc, F.vs, S.qbuf + oo, S.qpos + oo,
+                 S.devoff + c.dof_off,
+                 want_schedule ? O.start + oo : nullptr,
+                 want_schedule ? O.end + oo : nullptr, want_schedule};
 
-  // ---- state init: counters (16 B vector copies), devices ----
+  // ---- state init ----
   {
-    const uint32_t nv = (n + 15) / 16;
+    const uint32_t nv = (info.n_cnt + 15) / 16;
     const uint4* src = reinterpret_cast<const uint4*>(cnt0);
-    uint4* dst = reinterpret_cast<uint4*>(cnt32);
+    uint4* dst = reinterpret_cast<uint4*>(cw);
     for (uint32_t i = lane; i < nv; i += 32) dst[i] = __ldg(src + i);
   }
   for (uint32_t d = lane; d < D; d += 32) {
     DevF z;
     z.head = z.tail = z.tsort = z.segbeg = 0;
-    z.zlo = z.zhi = 0;
-    z.iop = kNone;
-    z.pad = 0;
-    z.iend = 0;
-    z.segt = 0;
-    z.busy = 0;
-    z.pad2 = 0;
+    z.zlo = z.zhi = z.segt = z.busy = 0;
     z.ient = make_uint4(0, 0, 0, 0);
     dv[d] = z;
   }
-  if (lane == 0) {
-    misc[0] = 0;
-    misc[1] = 0;
-  }
+  if (lane < 4) misc[lane] = 0;
+  misc[4 + lane] = 0;
   __syncwarp();
-  // ---- sources (replay.cpp:92-94): indeg-0 ops in index order. Virtual
-  // sources never reach here (pack flags them), so there are no cascades and
-  // no init quirk; arrivals at t=0 are sorted per device below. ----
-  {
-    const uint32_t nw = (n + 3) / 4;
-    for (uint32_t w = lane; w < nw; w += 32) {
-      const uint32_t v = cnt32[w];
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const uint32_t i = w * 4 + b;
-        if (i < n && ((v >> (8 * b)) & 0xFFu) == 0u) {
-          const uint4 r = __ldg(rec + i);
-          W.ready(make_uint4(i, r.x, r.y, r.z), 0);
-        }
-      }
-    }
+  // ---- sources (replay.cpp:92-94). No virtual sources reach the fast path
+  // (pack flags them), so there are no cascades and no init quirk. ----
+  for (uint32_t k = lane; k < info.n_src; k += 32) {
+    const uint32_t i = __ldg(srcs + k);
+    W.ready(__ldg(rec + 2 * i), __ldg(rec + 2 * i + 1), 0u);
   }
   __syncwarp();
   if (__any_sync(kFull, misc[1] != 0)) return false;
-  for (uint32_t d = lane; d < D; d += 32) {  // sort the t=0 arrivals by index
+  for (uint32_t d = lane; d < D; d += 32) {  // t = 0 arrivals in index order
     DevF& s = dv[d];
     uint4* r = W.ring(d);
     const uint32_t m = F.qc - 1;
@@ -266,40 +259,73 @@ __device__ bool replay_fast(const Cand& c, int cid, const uint4* rec, const uint
   }
   __syncwarp();
 
-  // ---- dispatch(0) + event loop ----
-  long long lane_min = kTInf, t = 0;
-  bool lane_zero = false;
-  for (uint32_t d = lane; d < D; d += 32) W.dispatch_dev(d, 0, lane_min, lane_zero);
-  for (;;) {
-    const bool zero_round = __any_sync(kFull, lane_zero);
-    if (!zero_round) {
-      const long long tn = warp_min64(lane_min);
-      if (tn == kTInf) break;
-      t = tn;
+  // ---- dispatch(0) + event loop (replay.cpp:95-106) ----
+  uint32_t iend[KD];
+  uint32_t zmask = 0;
+#pragma unroll
+  for (int j = 0; j < KD; ++j) {
+    iend[j] = kT32Inf;
+    const uint32_t d = lane + 32 * j;
+    if (d < D) {
+      bool z = false;
+      iend[j] = W.dispatch_dev(d, 0u, kT32Inf, &z);
+      if (z) zmask |= 1u << j;
     }
-    for (uint32_t d = lane; d < D; d += 32) {
-      DevF& s = dv[d];
-      if (zero_round) {
+  }
+  if (lane < 32) misc[4 + lane] = 0;  // all devices were just visited
+  uint32_t t = 0;
+  for (;;) {
+    const bool zero_round = __any_sync(kFull, zmask != 0);
+    uint32_t freed = 0;
+    if (zero_round) {
+      // zero-duration ops dispatched last round complete now (same t)
+      uint32_t zm = zmask;
+      while (zm) {
+        const int j = __ffs(zm) - 1;
+        zm &= zm - 1;
+        const uint32_t d = lane + 32 * j;
+        DevF& s = dv[d];
         const uint4* r = W.ring(d);
-        for (uint32_t p = s.zlo; p < s.zhi; ++p) W.complete(r[p & (F.qc - 1)], t);
-        *reinterpret_cast<volatile uint32_t*>(&s.zlo) = s.zhi;
-      } else if (s.iop != kNone && s.iend == t) {
-        s.iop = kNone;
-        W.complete(s.ient, t);
+        const uint32_t zh = s.zhi;
+        for (uint32_t p = s.zlo; p < zh; ++p) W.complete(r[p & (F.qc - 1)], t);
+        *reinterpret_cast<volatile uint32_t*>(&s.zlo) = zh;
+      }
+      zmask = 0;
+    } else {
+      uint32_t lmin = kT32Inf;
+#pragma unroll
+      for (int j = 0; j < KD; ++j) lmin = min(lmin, iend[j]);
+      const uint32_t tn = __reduce_min_sync(kFull, lmin);
+      if (tn == kT32Inf) break;
+      t = tn;
+#pragma unroll
+      for (int j = 0; j < KD; ++j) {
+        if (iend[j] == t) {
+          iend[j] = kT32Inf;
+          freed |= 1u << j;
+          W.complete(dv[lane + 32 * j].ient, t);
+        }
       }
     }
     W.drain_virtual(t, lane);
     __syncwarp();
     if (__any_sync(kFull, misc[1] != 0)) return false;
-    lane_min = kTInf;
-    lane_zero = false;
-    for (uint32_t d = lane; d < D; d += 32) W.dispatch_dev(d, t, lane_min, lane_zero);
+    uint32_t todo = freed | misc[4 + lane];
+    misc[4 + lane] = 0;
+#pragma unroll
+    for (int j = 0; j < KD; ++j) {
+      if (todo & (1u << j)) {
+        bool z = false;
+        iend[j] = W.dispatch_dev(lane + 32 * j, t, iend[j], &z);
+        if (z) zmask |= 1u << j;
+      }
+    }
   }
 
-  const unsigned long long vc = warp_sum64(W.vcount);
-  const unsigned long long dc = warp_sum64(W.dcount);
+  const uint32_t vc = __reduce_add_sync(kFull, W.vcount);
+  const uint32_t dc = __reduce_add_sync(kFull, W.dcount);
   if (vc + dc != n) return false;  // cycle: the general path reports it exactly
-  const long long T = warp_max64(W.tmax);
+  const uint32_t T = __reduce_max_sync(kFull, W.tmax);
   for (uint32_t d = lane; d < D; d += 32) {
     S.busy[c.dev_off + d] = dv[d].busy;
     S.dhead[c.dev_off + d] = W.devoff[d] + dv[d].head;
@@ -312,6 +338,7 @@ __device__ bool replay_fast(const Cand& c, int cid, const uint4* rec, const uint
   return true;
 }
 
+template <int KD>
 __global__ void __launch_bounds__(32) replay_fast_kernel(
     const Cand* __restrict__ cands, int n_cands, Scratch S, Outs O, PackOut P,
     FastCfg F, int want_schedule, unsigned* work, unsigned* fallbacks) {
@@ -332,9 +359,10 @@ __global__ void __launch_bounds__(32) replay_fast_kernel(
       continue;
     }
     bool done = false;
-    if (info.not_fast == 0 && c.d <= F.dcap && c.n <= F.vcap)
-      done = replay_fast(c, cid, P.rec + c.op_off, P.erec + P.e_off[cid],
-                         P.cnt0 + P.c_off[cid], fsm, F, S, O, want_schedule != 0);
+    if (info.not_fast == 0 && c.d <= F.dcap && c.d <= 32u * KD && info.n_cnt <= F.ccap)
+      done = replay_fast<KD>(c, cid, P.rec + 2 * c.op_off, P.erec + 2 * P.e_off[cid],
+                             P.cnt0 + P.c_off[cid], P.srcs + c.op_off, info, fsm, F, S, O,
+                             want_schedule != 0);
     __syncwarp();
     if (!done) {
       if (threadIdx.x == 0) atomicAdd(fallbacks, 1u);
