@@ -303,28 +303,32 @@ int build_batch(dpro_ctx* ctx, dpro_batch* b, const dpro_csr* cands) {
   CU(b->work.ensure(16));
   // packed replay layout (pack_kernel.cuh)
   {
-    std::vector<unsigned long long> e_off(n), c_off(n);
-    unsigned long long eo = 0, co = 0;
+    std::vector<unsigned long long> r_off(n), e_off(n), c_off(n);
+    unsigned long long ro = 0, eo = 0, co = 0;
     for (int32_t i = 0; i < n; ++i) {
+      r_off[i] = ro;
       e_off[i] = eo;
       c_off[i] = co;
+      ro += b->n_ops[i] + 1;
       eo += b->n_edges[i];
       co += (b->n_ops[i] + 15) & ~15u;
     }
-    const size_t s_rec = align16(so * 32 + 32), s_erec = align16(eo * 32 + 32),
+    const size_t s_rec = align16(ro * 16 + 16), s_erec = align16(eo * 16 + 16),
                  s_cnt = align16(co + 16), s_u32 = align16(so * 4 + 4),
                  s_off = align16(size_t(n) * 8 + 8),
                  s_info = align16(size_t(n) * sizeof(dpro_k::PackInfo) + 16);
-    CU(b->pack.ensure(s_rec + s_erec + s_cnt + 2 * s_u32 + 2 * s_off + s_info));
+    CU(b->pack.ensure(s_rec + s_erec + s_cnt + 2 * s_u32 + 3 * s_off + s_info));
     size_t po = 0;
     b->P.rec = b->pack.as<uint4>(po); po += s_rec;
     b->P.erec = b->pack.as<uint4>(po); po += s_erec;
     b->P.cnt0 = b->pack.as<uint8_t>(po); po += s_cnt;
     b->P.srcs = b->pack.as<uint32_t>(po); po += s_u32;
     b->P.cidx = b->pack.as<uint32_t>(po); po += s_u32;
+    b->P.r_off = b->pack.as<unsigned long long>(po); po += s_off;
     b->P.e_off = b->pack.as<unsigned long long>(po); po += s_off;
     b->P.c_off = b->pack.as<unsigned long long>(po); po += s_off;
     b->P.info = b->pack.as<dpro_k::PackInfo>(po); po += s_info;
+    CU(cudaMemcpyAsync(b->P.r_off, r_off.data(), size_t(n) * 8, cudaMemcpyHostToDevice, ctx->stream));
     CU(cudaMemcpyAsync(b->P.e_off, e_off.data(), size_t(n) * 8, cudaMemcpyHostToDevice, ctx->stream));
     CU(cudaMemcpyAsync(b->P.c_off, c_off.data(), size_t(n) * 8, cudaMemcpyHostToDevice, ctx->stream));
     CU(cudaMemsetAsync(b->P.cnt0, 0, s_cnt, ctx->stream));
@@ -448,7 +452,7 @@ int launch_general(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
 // devices x (DevF + ring) + virtual worklist + misc words + u8 counters.
 size_t fast_bytes(uint32_t dcap, uint32_t qc, uint32_t vs, uint32_t ccap) {
   return size_t(dcap) * (sizeof(dpro_k::DevF) + 16 * qc) + 16 * vs +
-         4 * dpro_k::fast_misc_words() + ccap;
+         16 * 32 * dpro_k::kZStage + 4 * dpro_k::fast_misc_words() + ccap;
 }
 
 template <int KD>
@@ -479,6 +483,7 @@ int launch_fast(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
   for (const auto& inf : b->info) max_cnt = std::max(max_cnt, inf.n_cnt);
   uint32_t kd = std::max<uint32_t>(1, (b->max_d + 31) / 32);
   if (kd > 8) kd = kd <= 12 ? 12 : 16;
+  if (b->max_d > dpro_k::kMaxDev) kd = 16;
   F.kd = kd;
   F.dcap = std::max<uint32_t>(1, std::min<uint32_t>(b->max_d, 32 * kd));
   F.ccap = (max_cnt + 15) & ~15u;

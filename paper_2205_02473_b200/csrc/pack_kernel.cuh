@@ -1,8 +1,8 @@
 // Pack: caller CSR (SoA, index order) -> the engine's replay layout.
 //
 // Runs once when a batch is registered (engine.cu). Per candidate:
-//   rec[i]  = 32-byte record of op i     {i, dur, devflags, sb | se, cidx}
-//   erec[k] = the record of s for edge k: i -> s (same 32-byte format)
+//   rec[i]  = 16-byte record of op i (format below), plus a sentinel rec[n]
+//   erec[k] = the record of s for edge k: i -> s (same format)
 //   cnt0[c] = indeg of the c-th multi-predecessor op (compact u8 counters)
 //   srcs    = ops with no predecessor (unordered; the replay sorts them)
 //   devoff  = exclusive scan of non-virtual ops per device (timeline regions)
@@ -17,15 +17,29 @@
 
 namespace dpro_k {
 
-constexpr uint32_t kDevMask = 0xFFFFu;
-constexpr uint32_t kFVirt = 1u << 16;
-constexpr uint32_t kFMulti = 1u << 17;  // >= 2 predecessors: has a counter
+// 16-byte op record (rec[i] for op i; erec[k] = record of s for edge i->s):
+//   x = s (24 bits) | cidx bits 0..7 << 24
+//   y = dur (int32; 0 for virtual ops, which never run)
+//   z = dev (10 bits) | virtual << 10 | multi << 11 | succ count (6 bits,
+//       63 = "read succ_end from rec[s+1].w") << 12 | cidx bits 8..21 << 18
+//   w = succ_beg
+// rec has n+1 entries; rec[n].w = n_edges, so succ_end(s) = rec[s+1].w.
+constexpr uint32_t kOpMask = 0xFFFFFFu;
+constexpr uint32_t kDevMask = 0x3FFu;
+constexpr uint32_t kFVirt = 1u << 10;
+constexpr uint32_t kFMulti = 1u << 11;  // >= 2 predecessors: has a counter
+constexpr uint32_t kCntShift = 12;
+constexpr uint32_t kCntMax = 63u;
+constexpr uint32_t kMaxOps = 1u << 24;
+constexpr uint32_t kMaxDev = 1u << 10;
+constexpr uint32_t kMaxCnt = 1u << 22;
 
 // not_fast bits
 constexpr uint32_t kNfDur = 1u;       // |dur| >= 2^31 or sum of dur >= 2^31
 constexpr uint32_t kNfIndeg = 2u;     // some indeg >= 255
 constexpr uint32_t kNfVsrc = 4u;      // virtual op without predecessors
-constexpr uint32_t kNfDev = 8u;       // device id out of range
+constexpr uint32_t kNfDev = 8u;       // device id out of range / > 1024 devices
+constexpr uint32_t kNfSize = 16u;     // >= 2^24 ops or >= 2^22 counters
 
 struct PackInfo {
   uint32_t first_missing;  // kNone: every non-virtual op has dur >= 0
@@ -36,25 +50,29 @@ struct PackInfo {
 };
 
 struct PackOut {
-  uint4* rec;                  // [2 * sum n]
-  uint4* erec;                 // [2 * sum e]
+  uint4* rec;                  // [sum (n+1)]
+  uint4* erec;                 // [sum e]
   uint8_t* cnt0;               // [sum n16]
   uint32_t* srcs;              // [sum n]
   uint32_t* cidx;              // [sum n] scratch: counter slot per op
+  unsigned long long* r_off;   // per candidate offset into rec (in records)
   unsigned long long* e_off;   // per candidate offset into erec (in edges)
   unsigned long long* c_off;   // per candidate byte offset into cnt0
   PackInfo* info;              // [B]
 };
 
-__device__ __forceinline__ void put_rec(uint4* dst, uint32_t s, const Cand& c,
-                                        const uint32_t* indeg, const uint32_t* cidx) {
+__device__ __forceinline__ uint4 make_rec(uint32_t s, const Cand& c, const uint32_t* indeg,
+                                          const uint32_t* cidx) {
   const uint32_t f = c.flags[s];
   const uint32_t ind = indeg[s];
-  const uint32_t df = (uint32_t(c.dev[s]) & kDevMask) | ((f & 1u) ? kFVirt : 0u) |
-                      (ind >= 2 ? kFMulti : 0u);
-  const long long du = ld_dur(c, s);
-  dst[0] = make_uint4(s, static_cast<uint32_t>(static_cast<int>(du)), df, c.succ_off[s]);
-  dst[1] = make_uint4(c.succ_off[s + 1], ind >= 2 ? cidx[s] : 0u, 0u, 0u);
+  const bool virt = f & 1u;
+  const uint32_t ci = ind >= 2 ? cidx[s] : 0u;
+  const uint32_t cnt = min(c.succ_off[s + 1] - c.succ_off[s], kCntMax);
+  const uint32_t z = (uint32_t(c.dev[s]) & kDevMask) | (virt ? kFVirt : 0u) |
+                     (ind >= 2 ? kFMulti : 0u) | (cnt << kCntShift) | ((ci >> 8) << 18);
+  const long long du = virt ? 0 : ld_dur(c, s);
+  return make_uint4((s & kOpMask) | ((ci & 0xFFu) << 24),
+                    static_cast<uint32_t>(static_cast<int>(du)), z, c.succ_off[s]);
 }
 
 // One block per candidate (grid-stride). indeg must be present (host upload
@@ -68,14 +86,14 @@ __global__ void __launch_bounds__(256) pack_kernel(const Cand* __restrict__ cand
     const Cand c = cands[cid];
     const uint32_t n = c.n;
     const uint32_t* indeg = c.indeg ? c.indeg : S.indeg + c.op_off;
-    uint4* rec = P.rec + 2 * c.op_off;
-    uint4* erec = P.erec + 2 * P.e_off[cid];
+    uint4* rec = P.rec + P.r_off[cid];
+    uint4* erec = P.erec + P.e_off[cid];
     uint8_t* cnt0 = P.cnt0 + P.c_off[cid];
     uint32_t* srcs = P.srcs + c.op_off;
     uint32_t* cidx = P.cidx + c.op_off;
     if (threadIdx.x == 0) {
       s_first = kNone;
-      s_flags = 0;
+      s_flags = (n >= kMaxOps ? kNfSize : 0u) | (c.d > kMaxDev ? kNfDev : 0u);
       s_ncnt = 0;
       s_nsrc = 0;
       s_sum = 0;
@@ -89,7 +107,7 @@ __global__ void __launch_bounds__(256) pack_kernel(const Cand* __restrict__ cand
       const bool virt = c.flags[i] & 1u;
       const uint32_t ind = indeg[i];
       if (!virt && du < 0) first = min(first, i);
-      if (du > 0x7FFFFFFFLL || du < -0x80000000LL) flags |= kNfDur;
+      if (!virt && (du > 0x7FFFFFFFLL || du < -0x80000000LL)) flags |= kNfDur;
       if (!virt && du > 0) sum += static_cast<unsigned long long>(du);
       if (ind >= 255u) flags |= kNfIndeg;
       if (virt && ind == 0u) flags |= kNfVsrc;
@@ -97,7 +115,7 @@ __global__ void __launch_bounds__(256) pack_kernel(const Cand* __restrict__ cand
       if (ind >= 2u) {
         const uint32_t slot = atomicAdd(&s_ncnt, 1u);
         cidx[i] = slot;
-        cnt0[slot] = static_cast<uint8_t>(min(ind, 255u));
+        if (slot < kMaxCnt) cnt0[slot] = static_cast<uint8_t>(min(ind, 255u));
       } else if (ind == 0u) {
         srcs[atomicAdd(&s_nsrc, 1u)] = i;
       }
@@ -108,14 +126,16 @@ __global__ void __launch_bounds__(256) pack_kernel(const Cand* __restrict__ cand
     __syncthreads();
     // pass 2: records
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-      put_rec(rec + 2 * i, i, c, indeg, cidx);
+      rec[i] = make_rec(i, c, indeg, cidx);
       for (uint32_t k = c.succ_off[i]; k < c.succ_off[i + 1]; ++k)
-        put_rec(erec + 2 * k, c.succ[k], c, indeg, cidx);
+        erec[k] = make_rec(c.succ[k], c, indeg, cidx);
     }
     if (threadIdx.x == 0) {
+      rec[n] = make_uint4(0u, 0u, 0u, c.succ_off[n]);
       PackInfo inf;
       inf.first_missing = s_first;
-      inf.not_fast = s_flags | (s_sum >= 0x7FFFFFFFull ? kNfDur : 0u);
+      inf.not_fast = s_flags | (s_sum >= 0x7FFFFFFFull ? kNfDur : 0u) |
+                     (s_ncnt >= kMaxCnt ? kNfSize : 0u);
       inf.n_cnt = s_ncnt;
       inf.n_src = s_nsrc;
       inf.dur_sum = s_sum;

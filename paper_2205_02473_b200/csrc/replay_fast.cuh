@@ -12,8 +12,11 @@
 //     {op, dur, succ_beg, succ_end}, sorted by (ready, index) on arrival;
 //   * in-degree countdowns exist only for ops with >= 2 predecessors, as
 //     compact u8 counters in shared memory (4 per word, word atomics);
-//   * the only global read in a round is the completing op's 32-byte edge
-//     records (pack_kernel.cuh), prefetched to L2 when the op is enqueued.
+//   * the completing op's 16-byte edge records (pack_kernel.cuh) are loaded
+//     when the op is dispatched -- into registers for the in-flight
+//     positive-duration op of each owned device, into a per-lane cp.async
+//     stage for zero-duration ops (which complete next round) -- so the
+//     completion itself rarely waits on memory.
 // Whatever the fast path cannot represent (ring or worklist overflow, a
 // virtual source -> init quirk, indeg >= 255, durations that need 64-bit
 // times, too many devices / counters, a cycle) falls back inside the same
@@ -36,7 +39,7 @@ struct __align__(16) DevF {
 static_assert(sizeof(DevF) == 48, "DevF layout");
 
 struct FastCfg {
-  uint32_t dcap;   // devices per warp (multiple of 32)
+  uint32_t dcap;   // devices per warp
   uint32_t ccap;   // compact counters per warp (bytes, multiple of 16)
   uint32_t qc;     // ring capacity per device (power of two)
   uint32_t vs;     // virtual worklist capacity
@@ -44,18 +47,33 @@ struct FastCfg {
   uint32_t kd;     // devices per lane (template parameter)
 };
 
+constexpr int kStage = 2;   // edge records staged in registers per in-flight op
+constexpr int kZStage = 4;  // zero-duration ops staged per lane per round
+
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(a), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 __host__ __device__ constexpr size_t fast_misc_words() { return 4 + 32; }
 
 template <int KD>
 struct FastWarp {
-  const uint4* __restrict__ erec;  // 2 x uint4 per edge
+  const uint4* __restrict__ rec;
+  const uint4* __restrict__ erec;
   DevF* dv;
   uint4* q;                 // [dcap][qc]
   uint4* vstk;              // [vs]
+  uint4* zst;               // [32][kZStage] zero-op staging (cp.async)
   volatile uint32_t* misc;  // [0] vtop [1] overflow [4..35] dirty masks
   uint32_t* cw;             // compact counters (u8 in words)
   uint32_t qc, vs;
@@ -65,17 +83,21 @@ struct FastWarp {
   long long* start;
   long long* end;
   bool want;
-  uint32_t vcount = 0, dcount = 0, tmax = 0;
+  int lane;
+  uint32_t vcount = 0, dcount = 0, tmax = 0, zn = 0;
 
   __device__ __forceinline__ uint4* ring(uint32_t d) { return q + (size_t)d * qc; }
 
-  // ready(s, t) of replay.cpp:60-72 for s reached through an edge record.
-  __device__ __forceinline__ void ready(const uint4& a, const uint4& b, uint32_t t) {
-    const uint4 e = make_uint4(a.x, a.y, a.w, b.x);  // {op, dur, sb, se}
+  // ready(s, t) of replay.cpp:60-72 for s reached through a packed record.
+  __device__ __forceinline__ void ready(const uint4& a, uint32_t t) {
+    const uint32_t s = a.x & kOpMask;
+    const uint32_t cnt = (a.z >> kCntShift) & kCntMax;
+    const uint32_t se = cnt == kCntMax ? __ldg(&rec[s + 1].w) : a.w + cnt;
+    const uint4 e = make_uint4(s, a.y, a.w, se);  // {op, dur, sb, se}
     if (a.z & kFVirt) {
       if (want) {
-        start[a.x] = t;
-        end[a.x] = t;
+        start[s] = t;
+        end[s] = t;
       }
       ++vcount;
       tmax = max(tmax, t);
@@ -86,11 +108,11 @@ struct FastWarp {
         misc[1] = 1u;
     } else {
       const uint32_t d = a.z & kDevMask;
-      DevF& s = dv[d];
-      const uint32_t pos = atomicAdd(&s.tail, 1u);
-      const uint32_t zl = *reinterpret_cast<volatile uint32_t*>(&s.zlo);
-      const uint32_t zh = *reinterpret_cast<volatile uint32_t*>(&s.zhi);
-      const uint32_t low = zl < zh ? zl : *reinterpret_cast<volatile uint32_t*>(&s.head);
+      DevF& sd = dv[d];
+      const uint32_t pos = atomicAdd(&sd.tail, 1u);
+      const uint32_t zl = *reinterpret_cast<volatile uint32_t*>(&sd.zlo);
+      const uint32_t zh = *reinterpret_cast<volatile uint32_t*>(&sd.zhi);
+      const uint32_t low = zl < zh ? zl : *reinterpret_cast<volatile uint32_t*>(&sd.head);
       if (pos - low >= qc) {
         misc[1] = 1u;
       } else {
@@ -98,24 +120,35 @@ struct FastWarp {
         atomicOr(const_cast<uint32_t*>(&misc[4 + (d & 31)]), 1u << (d >> 5));
       }
     }
-    if (e.w > e.z) prefetch_l2(erec + 2 * e.z);
+    if (se > a.w) prefetch_l2(erec + a.w);
   }
 
-  // Completion of op e at t: successors (replay.cpp:100-103).
-  __device__ __forceinline__ void complete(const uint4& e, uint32_t t) {
-    for (uint32_t k = e.z; k < e.w; ++k) {
-      const uint4 a = __ldg(erec + 2 * k);
-      const uint4 b = __ldg(erec + 2 * k + 1);
-      if (a.z & kFMulti) {
-        const uint32_t sh = 8u * (b.y & 3u);
-        const uint32_t old = atomicSub(&cw[b.y >> 2], 1u << sh);
-        if (((old >> sh) & 0xFFu) != 1u) continue;
-      }
-      ready(a, b, t);
+  __device__ __forceinline__ void edge(const uint4& a, uint32_t t) {
+    if (a.z & kFMulti) {
+      const uint32_t ci = (a.x >> 24) | ((a.z >> 18) << 8);
+      const uint32_t sh = 8u * (ci & 3u);
+      const uint32_t old = atomicSub(&cw[ci >> 2], 1u << sh);
+      if (((old >> sh) & 0xFFu) != 1u) return;
     }
+    ready(a, t);
   }
 
-  __device__ void drain_virtual(uint32_t t, int lane) {
+  // Completion of e at t (replay.cpp:100-103); the first kStage records were
+  // loaded into `st` when e was dispatched.
+  __device__ __forceinline__ void complete_staged(const uint4& e, const uint4 (&st)[kStage],
+                                                  uint32_t t) {
+    const uint32_t n = e.w - e.z;
+#pragma unroll
+    for (int f = 0; f < kStage; ++f)
+      if (f < n) edge(st[f], t);
+    for (uint32_t k = e.z + kStage; k < e.w; ++k) edge(__ldg(erec + k), t);
+  }
+
+  __device__ __forceinline__ void complete(const uint4& e, uint32_t t) {
+    for (uint32_t k = e.z; k < e.w; ++k) edge(__ldg(erec + k), t);
+  }
+
+  __device__ void drain_virtual(uint32_t t) {
     __syncwarp();
     for (;;) {
       const uint32_t n = misc[0];
@@ -133,10 +166,11 @@ struct FastWarp {
 
   // Owner-lane dispatch(t) for device d (replay.cpp:74-90) after merging
   // this round's arrivals into the (ready, index)-ordered tail segment.
-  // Returns the device's in-flight end (kT32Inf when idle); sets *zero when
-  // zero-duration ops were dispatched (they complete next round).
+  // Returns the in-flight end (kT32Inf: idle); loads the in-flight op's first
+  // edge records into `st`; stages the first record of zero-duration ops
+  // (they complete next round) with cp.async; sets *zero when any ran.
   __device__ __forceinline__ uint32_t dispatch_dev(uint32_t d, uint32_t t, uint32_t iend,
-                                                   bool* zero) {
+                                                   uint4 (&st)[kStage], bool* zero) {
     DevF& s = dv[d];
     uint4* r = ring(d);
     const uint32_t tail = *reinterpret_cast<volatile uint32_t*>(&s.tail);
@@ -183,8 +217,13 @@ struct FastWarp {
           s.ient = x;
           iend = en;
           infl = true;
+#pragma unroll
+          for (int f = 0; f < kStage; ++f)
+            if (x.z + f < x.w) st[f] = __ldg(erec + x.z + f);
+          if (x.w > x.z + kStage) prefetch_l2(erec + x.z + kStage);
           break;
         }
+        if (x.w > x.z && zn < kZStage) cp_async16(zst + lane * kZStage + zn++, erec + x.z);
       }
       s.busy += busy;
       s.head = head;
@@ -208,14 +247,15 @@ __device__ bool replay_fast(const Cand& c, int cid, const uint4* rec, const uint
   DevF* dv = reinterpret_cast<DevF*>(wsm);
   uint4* q = reinterpret_cast<uint4*>(wsm + sizeof(DevF) * F.dcap);
   uint4* vstk = q + (size_t)F.dcap * F.qc;
-  volatile uint32_t* misc = reinterpret_cast<volatile uint32_t*>(vstk + F.vs);
+  uint4* zst = vstk + F.vs;
+  volatile uint32_t* misc = reinterpret_cast<volatile uint32_t*>(zst + 32 * kZStage);
   uint32_t* cw = const_cast<uint32_t*>(misc) + fast_misc_words();
   const unsigned long long oo = c.op_off;
 
-  FastWarp<KD> W{erec, dv, q, vstk, misc, cw, F.qc, F.vs, S.qbuf + oo, S.qpos + oo,
+  FastWarp<KD> W{rec, erec, dv, q, vstk, zst, misc, cw, F.qc, F.vs, S.qbuf + oo, S.qpos + oo,
                  S.devoff + c.dof_off,
                  want_schedule ? O.start + oo : nullptr,
-                 want_schedule ? O.end + oo : nullptr, want_schedule};
+                 want_schedule ? O.end + oo : nullptr, want_schedule, lane};
 
   // ---- state init ----
   {
@@ -236,10 +276,7 @@ __device__ bool replay_fast(const Cand& c, int cid, const uint4* rec, const uint
   __syncwarp();
   // ---- sources (replay.cpp:92-94). No virtual sources reach the fast path
   // (pack flags them), so there are no cascades and no init quirk. ----
-  for (uint32_t k = lane; k < info.n_src; k += 32) {
-    const uint32_t i = __ldg(srcs + k);
-    W.ready(__ldg(rec + 2 * i), __ldg(rec + 2 * i + 1), 0u);
-  }
+  for (uint32_t k = lane; k < info.n_src; k += 32) W.ready(__ldg(rec + __ldg(srcs + k)), 0u);
   __syncwarp();
   if (__any_sync(kFull, misc[1] != 0)) return false;
   for (uint32_t d = lane; d < D; d += 32) {  // t = 0 arrivals in index order
@@ -261,24 +298,31 @@ __device__ bool replay_fast(const Cand& c, int cid, const uint4* rec, const uint
 
   // ---- dispatch(0) + event loop (replay.cpp:95-106) ----
   uint32_t iend[KD];
+  uint4 stg[KD][kStage];
   uint32_t zmask = 0;
 #pragma unroll
   for (int j = 0; j < KD; ++j) {
     iend[j] = kT32Inf;
+#pragma unroll
+    for (int f = 0; f < kStage; ++f) stg[j][f] = make_uint4(0, 0, 0, 0);
     const uint32_t d = lane + 32 * j;
     if (d < D) {
       bool z = false;
-      iend[j] = W.dispatch_dev(d, 0u, kT32Inf, &z);
+      iend[j] = W.dispatch_dev(d, 0u, kT32Inf, stg[j], &z);
       if (z) zmask |= 1u << j;
     }
   }
-  if (lane < 32) misc[4 + lane] = 0;  // all devices were just visited
+  cp_async_commit();
+  misc[4 + lane] = 0;  // all devices were just visited
   uint32_t t = 0;
   for (;;) {
     const bool zero_round = __any_sync(kFull, zmask != 0);
     uint32_t freed = 0;
     if (zero_round) {
-      // zero-duration ops dispatched last round complete now (same t)
+      // zero-duration ops dispatched last round complete now (same t); their
+      // first edge records were staged by cp.async in that dispatch
+      cp_async_wait_all();
+      uint32_t zi = 0;
       uint32_t zm = zmask;
       while (zm) {
         const int j = __ffs(zm) - 1;
@@ -287,7 +331,17 @@ __device__ bool replay_fast(const Cand& c, int cid, const uint4* rec, const uint
         DevF& s = dv[d];
         const uint4* r = W.ring(d);
         const uint32_t zh = s.zhi;
-        for (uint32_t p = s.zlo; p < zh; ++p) W.complete(r[p & (F.qc - 1)], t);
+        for (uint32_t p = s.zlo; p < zh; ++p) {
+          const uint4 e = r[p & (F.qc - 1)];
+          if (e.w > e.z) {
+            uint32_t k = e.z;
+            if (zi < kZStage) {
+              W.edge(zst[lane * kZStage + zi++], t);
+              ++k;
+            }
+            for (; k < e.w; ++k) W.edge(__ldg(erec + k), t);
+          }
+        }
         *reinterpret_cast<volatile uint32_t*>(&s.zlo) = zh;
       }
       zmask = 0;
@@ -303,24 +357,27 @@ __device__ bool replay_fast(const Cand& c, int cid, const uint4* rec, const uint
         if (iend[j] == t) {
           iend[j] = kT32Inf;
           freed |= 1u << j;
-          W.complete(dv[lane + 32 * j].ient, t);
+          W.complete_staged(dv[lane + 32 * j].ient, stg[j], t);
         }
       }
     }
-    W.drain_virtual(t, lane);
+    W.drain_virtual(t);
     __syncwarp();
     if (__any_sync(kFull, misc[1] != 0)) return false;
-    uint32_t todo = freed | misc[4 + lane];
+    const uint32_t todo = freed | misc[4 + lane];
     misc[4 + lane] = 0;
+    W.zn = 0;
 #pragma unroll
     for (int j = 0; j < KD; ++j) {
       if (todo & (1u << j)) {
         bool z = false;
-        iend[j] = W.dispatch_dev(lane + 32 * j, t, iend[j], &z);
+        iend[j] = W.dispatch_dev(lane + 32 * j, t, iend[j], stg[j], &z);
         if (z) zmask |= 1u << j;
       }
     }
+    cp_async_commit();
   }
+  cp_async_wait_all();
 
   const uint32_t vc = __reduce_add_sync(kFull, W.vcount);
   const uint32_t dc = __reduce_add_sync(kFull, W.dcount);
@@ -360,7 +417,7 @@ __global__ void __launch_bounds__(32) replay_fast_kernel(
     }
     bool done = false;
     if (info.not_fast == 0 && c.d <= F.dcap && c.d <= 32u * KD && info.n_cnt <= F.ccap)
-      done = replay_fast<KD>(c, cid, P.rec + 2 * c.op_off, P.erec + 2 * P.e_off[cid],
+      done = replay_fast<KD>(c, cid, P.rec + P.r_off[cid], P.erec + P.e_off[cid],
                              P.cnt0 + P.c_off[cid], P.srcs + c.op_off, info, fsm, F, S, O,
                              want_schedule != 0);
     __syncwarp();
