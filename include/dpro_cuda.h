@@ -142,6 +142,15 @@ int dpro_cuda_batch_scheduled(dpro_ctx* ctx, dpro_batch* b, int32_t cand,
 int dpro_cuda_batch_critical_paths(dpro_ctx* ctx, dpro_batch* b,
                                    uint32_t* paths, int64_t* path_len);
 
+/* critical_path(exec_graph, result) (replay.cpp:146-226) for ONE graph and
+ * a caller-supplied schedule (start/end per op, makespan): the exact
+ * reference signature, where the execution graph already contains the
+ * timeline edges. Host buffers; path capacity n_ops. */
+int dpro_cuda_critical_path(dpro_ctx* ctx, const dpro_csr* graph,
+                            const int64_t* start, const int64_t* end,
+                            int64_t makespan, uint32_t* path,
+                            int64_t* path_len);
+
 /* One-shot convenience with the reference-style signature: create, replay,
  * copy back (host outputs), destroy. start/end may be NULL. */
 int dpro_cuda_replay_batch(dpro_ctx* ctx, const dpro_csr* cands,

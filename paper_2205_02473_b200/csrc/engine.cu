@@ -86,6 +86,7 @@ struct dpro_ctx {
   HostPinned staging;
   int fast = 1;       // option "fast"
   uint32_t ring = 4;  // option "ring"
+  dpro_batch* spare = nullptr;  // recycled arenas for repeated small calls
 };
 
 struct dpro_batch {
@@ -375,6 +376,7 @@ void dpro_cuda_destroy(dpro_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  delete ctx->spare;
   delete ctx;
 }
 
@@ -396,7 +398,19 @@ dpro_batch* dpro_cuda_batch_create(dpro_ctx* ctx, const dpro_csr* cands,
     return nullptr;
   }
   cudaSetDevice(ctx->device);
-  auto* b = new dpro_batch;
+  dpro_batch* b = ctx->spare;
+  ctx->spare = nullptr;
+  if (b) {  // keep the device buffers (they only grow), reset the rest
+    b->hc.clear();
+    b->n_ops.clear();
+    b->n_dev.clear();
+    b->n_edges.clear();
+    b->sum_n = b->sum_d = b->sum_dof = b->sum_e = 0;
+    b->max_d = 0;
+    b->replayed = b->with_schedule = false;
+  } else {
+    b = new dpro_batch;
+  }
   b->n = n_cands;
   b->memspace = memspace;
   if (build_batch(ctx, b, cands) != DPRO_OK) {
@@ -407,7 +421,14 @@ dpro_batch* dpro_cuda_batch_create(dpro_ctx* ctx, const dpro_csr* cands,
 }
 
 void dpro_cuda_batch_destroy(dpro_ctx* ctx, dpro_batch* b) {
-  if (ctx) cudaStreamSynchronize(ctx->stream);
+  if (!b) return;
+  if (ctx) {
+    cudaStreamSynchronize(ctx->stream);
+    if (!ctx->spare) {
+      ctx->spare = b;
+      return;
+    }
+  }
   delete b;
 }
 
@@ -640,6 +661,36 @@ int dpro_cuda_batch_critical_paths(dpro_ctx* ctx, dpro_batch* b,
   if (path_len) CU(cudaMemcpyAsync(path_len, d_len, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
   return DPRO_OK;
+}
+
+int dpro_cuda_critical_path(dpro_ctx* ctx, const dpro_csr* graph,
+                            const int64_t* start, const int64_t* end,
+                            int64_t makespan, uint32_t* path,
+                            int64_t* path_len) {
+  if (!ctx || !graph || !path_len) return DPRO_EINVAL;
+  if (graph->n_ops > 0 && (!start || !end || !path)) return DPRO_EINVAL;
+  dpro_batch* b = dpro_cuda_batch_create(ctx, graph, 1, DPRO_HOST);
+  if (!b) return DPRO_EINVAL;
+  int st = DPRO_OK;
+  const size_t n = graph->n_ops;
+  auto run = [&]() -> int {
+    // the execution graph already carries the timeline edges: no qpos links
+    CU(cudaMemsetAsync(b->S.qpos, 0xFF, n * 4 + 4, ctx->stream));
+    if (n) {
+      CU(cudaMemcpyAsync(b->O.start, start, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+      CU(cudaMemcpyAsync(b->O.end, end, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    const long long T = makespan;
+    const int ok = 0;
+    CU(cudaMemcpyAsync(b->O.makespan, &T, 8, cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaMemcpyAsync(b->O.status, &ok, 4, cudaMemcpyHostToDevice, ctx->stream));
+    b->replayed = true;
+    b->with_schedule = true;
+    return dpro_cuda_batch_critical_paths(ctx, b, path, path_len);
+  };
+  st = run();
+  dpro_cuda_batch_destroy(ctx, b);
+  return st;
 }
 
 int dpro_cuda_replay_batch(dpro_ctx* ctx, const dpro_csr* cands,

@@ -53,6 +53,9 @@ constexpr int kZStage = 4;  // zero-duration ops staged per lane per round
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(a), "l"(gmem) : "memory");
@@ -220,7 +223,8 @@ struct FastWarp {
 #pragma unroll
           for (int f = 0; f < kStage; ++f)
             if (x.z + f < x.w) st[f] = __ldg(erec + x.z + f);
-          if (x.w > x.z + kStage) prefetch_l2(erec + x.z + kStage);
+          // records past the register stage: pull their lines into L1
+          for (uint32_t k = x.z + kStage; k < x.w; k += 8) prefetch_l1(erec + k);
           break;
         }
         if (x.w > x.z && zn < kZStage) cp_async16(zst + lane * kZStage + zn++, erec + x.z);

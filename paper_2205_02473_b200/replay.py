@@ -124,19 +124,35 @@ def execution_graph(g: GlobalDFG, result: ReplayResult) -> GlobalDFG:
     return eg
 
 
-def critical_path(exec_graph: GlobalDFG, result: ReplayResult) -> CriticalPath:
-    """replay.cpp:146-226. Runs K3 on the replayed batch; exec_graph must be
-    execution_graph(g, result) (the only way the reference builds it)."""
+def critical_path(exec_graph: GlobalDFG, result: ReplayResult, engine=None) -> CriticalPath:
+    """replay.cpp:146-226 on the GPU (K3). When exec_graph is
+    execution_graph(g, result) of a replay() result, K3 runs on the replayed
+    batch (timeline edges read from the engine's queues); otherwise on
+    exec_graph itself with result's schedule (dpro_cuda_critical_path)."""
     path = CriticalPath(total_us=result.iteration_time_us)
     if exec_graph.size() == 0:
         path.conforming = True
         return path
-    if getattr(exec_graph, "_exec_of", None) is not result or result._batch is None:
-        raise Error("critical_path: exec_graph must come from execution_graph(g, result)")
-    g = result._graph
-    paths = result._batch.critical_paths()
-    for i in paths[result._cand]:
-        op = exec_graph.op(g.op_at(int(i)).id)
+    if getattr(exec_graph, "_exec_of", None) is result and result._batch is not None:
+        g = result._graph
+        idx = [exec_graph.index_of(g.op_at(int(i)).id)
+               for i in result._batch.critical_paths()[result._cand]]
+    else:
+        eng = engine or default_engine()
+        csr = Csr.from_dict(exec_graph.to_csr())
+        n = exec_graph.size()
+        start = np.array([result.schedule[o.id].start for o in exec_graph.ops()], np.int64)
+        end = np.array([result.schedule[o.id].end for o in exec_graph.ops()], np.int64)
+        out = np.zeros(n, np.uint32)
+        ln = np.zeros(1, np.int64)
+        s = csr.as_struct()
+        rc = N.lib.dpro_cuda_critical_path(eng.ctx, s, N.ptr(start), N.ptr(end),
+                                           int(result.iteration_time_us), N.ptr(out), N.ptr(ln))
+        if rc != N.DPRO_OK:
+            raise EngineError(f"critical_path failed ({rc})")
+        idx = out[: int(ln[0])].tolist()
+    for i in idx:
+        op = exec_graph.op_at(int(i))
         path.ops.append(PathEntry(op.id, op.dur, is_communication(op.kind)))
     for e in path.ops:
         op = exec_graph.op(e.op)

@@ -202,3 +202,38 @@ def test_longer_ops_never_shrink_pinned_order_makespan():
         b = GraphBuilder(ex)
         b.op(ex.op_at(victim).id).dur += 1 + int(rng.integers(0, 5))
         assert replay(b.build()).iteration_time_us >= r.iteration_time_us
+
+
+def test_critical_path_on_any_execution_graph():
+    """critical_path over an exec graph built outside replay() uses the
+    given-schedule entry point (dpro_cuda_critical_path)."""
+    from paper_2205_02473_b200.graph import GlobalDFG
+    rng = np.random.default_rng(5)
+    for _ in range(30):
+        g = random_dag_ref(rng)
+        r = replay(g)
+        ex = execution_graph(g, r)
+        ex2 = GlobalDFG(ex.ops(), [list(ex.succ_indices(i)) for i in range(ex.size())], {},
+                        ex.cluster())
+        a = critical_path(ex, r)
+        b = critical_path(ex2, r)
+        assert [e.op for e in a.ops] == [e.op for e in b.ops]
+        assert sum(e.dur for e in b.ops) == r.iteration_time_us
+
+
+def test_reference_acceptance_suite_with_gpu_replay():
+    """The reference's own acceptance binary (proj/tests/acceptance_main.cpp)
+    linked against integration/: every replay/critical_path/sync_makespan
+    call inside it runs on the GPU. Check 10 needs the reference CLI (CLI11
+    is not in the image), so 9 of 10 must pass."""
+    import subprocess
+    from pathlib import Path
+    exe = Path(__file__).resolve().parents[1] / "integration" / "_build" / "dpro_acceptance_gpu"
+    if not exe.exists():
+        pytest.skip("integration/_build not built (needs /root/reference at build time)")
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=900)
+    print(out.stdout)
+    lines = [l for l in out.stdout.splitlines() if l.startswith("[")]
+    assert len(lines) == 10
+    for l in lines[:9]:
+        assert l.startswith("[PASS]"), l
