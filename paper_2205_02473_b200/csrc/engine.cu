@@ -318,13 +318,15 @@ int build_batch(dpro_ctx* ctx, dpro_batch* b, const dpro_csr* cands) {
                  s_cnt = align16(co + 16), s_u32 = align16(so * 4 + 4),
                  s_off = align16(size_t(n) * 8 + 8),
                  s_info = align16(size_t(n) * sizeof(dpro_k::PackInfo) + 16);
-    CU(b->pack.ensure(s_rec + s_erec + s_cnt + 2 * s_u32 + 3 * s_off + s_info));
+    const size_t s_xoff = align16(ro * 4 + 16);
+    CU(b->pack.ensure(s_rec + s_erec + s_cnt + 2 * s_u32 + s_xoff + 3 * s_off + s_info));
     size_t po = 0;
     b->P.rec = b->pack.as<uint4>(po); po += s_rec;
     b->P.erec = b->pack.as<uint4>(po); po += s_erec;
     b->P.cnt0 = b->pack.as<uint8_t>(po); po += s_cnt;
     b->P.srcs = b->pack.as<uint32_t>(po); po += s_u32;
     b->P.cidx = b->pack.as<uint32_t>(po); po += s_u32;
+    b->P.xoff = b->pack.as<uint32_t>(po); po += s_xoff;
     b->P.r_off = b->pack.as<unsigned long long>(po); po += s_off;
     b->P.e_off = b->pack.as<unsigned long long>(po); po += s_off;
     b->P.c_off = b->pack.as<unsigned long long>(po); po += s_off;

@@ -7,6 +7,12 @@
 //   srcs    = ops with no predecessor (unordered; the replay sorts them)
 //   devoff  = exclusive scan of non-virtual ops per device (timeline regions)
 //   info    = first op without duration, fast-path eligibility, sizes.
+// Virtual ops with exactly one predecessor are SPLICED: in the predecessor's
+// list the edge to v becomes a stamp record for v (virtual, not multi)
+// followed by v's own (expanded) successors. replay.cpp:60-72 completes such
+// a v in the same round as its predecessor and readies its successors at the
+// same t, so processing them from the predecessor's list is exact; the
+// expanded lists have exactly E entries in total.
 // The per-edge record carries everything the replay needs at the moment the
 // edge's completion makes s ready (device, virtual flag, duration, successor
 // range, counter slot) -- exactly what proj/src/replay.cpp:60-72,80-87 reads
@@ -40,6 +46,8 @@ constexpr uint32_t kNfIndeg = 2u;     // some indeg >= 255
 constexpr uint32_t kNfVsrc = 4u;      // virtual op without predecessors
 constexpr uint32_t kNfDev = 8u;       // device id out of range / > 1024 devices
 constexpr uint32_t kNfSize = 16u;     // >= 2^24 ops or >= 2^22 counters
+constexpr uint32_t kNfChain = 32u;    // virtual chain deeper than kMaxSplice
+constexpr int kMaxSplice = 8;
 
 struct PackInfo {
   uint32_t first_missing;  // kNone: every non-virtual op has dur >= 0
@@ -55,24 +63,60 @@ struct PackOut {
   uint8_t* cnt0;               // [sum n16]
   uint32_t* srcs;              // [sum n]
   uint32_t* cidx;              // [sum n] scratch: counter slot per op
+  uint32_t* xoff;              // [sum (n+1)] scratch: expanded list offsets
   unsigned long long* r_off;   // per candidate offset into rec (in records)
   unsigned long long* e_off;   // per candidate offset into erec (in edges)
   unsigned long long* c_off;   // per candidate byte offset into cnt0
   PackInfo* info;              // [B]
 };
 
+__device__ __forceinline__ bool spliced(const Cand& c, const uint32_t* indeg, uint32_t s) {
+  return (c.flags[s] & 1u) && indeg[s] == 1u;
+}
+
+// Record of s; its successor range is its EXPANDED list [xoff[s], xoff[s+1]).
 __device__ __forceinline__ uint4 make_rec(uint32_t s, const Cand& c, const uint32_t* indeg,
-                                          const uint32_t* cidx) {
+                                          const uint32_t* cidx, const uint32_t* xoff) {
   const uint32_t f = c.flags[s];
   const uint32_t ind = indeg[s];
   const bool virt = f & 1u;
   const uint32_t ci = ind >= 2 ? cidx[s] : 0u;
-  const uint32_t cnt = min(c.succ_off[s + 1] - c.succ_off[s], kCntMax);
+  const uint32_t cnt = min(xoff[s + 1] - xoff[s], kCntMax);
   const uint32_t z = (uint32_t(c.dev[s]) & kDevMask) | (virt ? kFVirt : 0u) |
                      (ind >= 2 ? kFMulti : 0u) | (cnt << kCntShift) | ((ci >> 8) << 18);
   const long long du = virt ? 0 : ld_dur(c, s);
   return make_uint4((s & kOpMask) | ((ci & 0xFFu) << 24),
-                    static_cast<uint32_t>(static_cast<int>(du)), z, c.succ_off[s]);
+                    static_cast<uint32_t>(static_cast<int>(du)), z, xoff[s]);
+}
+
+// Walks the expanded successor list of op i (DFS through spliced virtual
+// successors, in order). emit(rec) per entry; returns false when a spliced
+// chain is deeper than kMaxSplice.
+template <bool kBuild, typename Emit>
+__device__ bool expand_list(uint32_t i, const Cand& c, const uint32_t* indeg,
+                            const uint32_t* cidx, const uint32_t* xoff, Emit&& emit) {
+  uint32_t stk_op[kMaxSplice], stk_k[kMaxSplice];
+  int sp = 0;
+  stk_op[0] = i;
+  stk_k[0] = c.succ_off[i];
+  for (;;) {
+    const uint32_t v = stk_op[sp];
+    if (stk_k[sp] == c.succ_off[v + 1]) {
+      if (sp == 0) return true;
+      --sp;
+      continue;
+    }
+    const uint32_t s = c.succ[stk_k[sp]++];
+    if (spliced(c, indeg, s)) {
+      emit(make_uint4(s & kOpMask, 0u, kFVirt, 0u));  // stamp: virtual, not multi
+      if (sp + 1 >= kMaxSplice) return false;
+      ++sp;
+      stk_op[sp] = s;
+      stk_k[sp] = c.succ_off[s];
+    } else {
+      emit(kBuild ? make_rec(s, c, indeg, cidx, xoff) : make_uint4(0, 0, 0, 0));
+    }
+  }
 }
 
 // One block per candidate (grid-stride). indeg must be present (host upload
@@ -124,14 +168,54 @@ __global__ void __launch_bounds__(256) pack_kernel(const Cand* __restrict__ cand
     if (flags) atomicOr(&s_flags, flags);
     if (sum) atomicAdd(&s_sum, sum);
     __syncthreads();
-    // pass 2: records
+    // pass 2: expanded list sizes (spliced virtual ops own no list)
+    uint32_t* xoff = P.xoff + P.r_off[cid];
+    bool deep = false;
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-      rec[i] = make_rec(i, c, indeg, cidx);
-      for (uint32_t k = c.succ_off[i]; k < c.succ_off[i + 1]; ++k)
-        erec[k] = make_rec(c.succ[k], c, indeg, cidx);
+      uint32_t len = 0;
+      if (!spliced(c, indeg, i))
+        deep |= !expand_list<false>(i, c, indeg, cidx, xoff, [&](const uint4&) { ++len; });
+      xoff[i] = len;
+    }
+    if (deep) atomicOr(&s_flags, kNfChain);
+    __syncthreads();
+    // exclusive scan of xoff[0..n) (chunked block scan), xoff[n] = total
+    {
+      __shared__ uint32_t s_part[256];
+      const uint32_t chunk = (n + blockDim.x - 1) / blockDim.x;
+      const uint32_t lo = min(n, threadIdx.x * chunk), hi = min(n, lo + chunk);
+      uint32_t sum = 0;
+      for (uint32_t i = lo; i < hi; ++i) sum += xoff[i];
+      s_part[threadIdx.x] = sum;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        uint32_t run = 0;
+        for (uint32_t t = 0; t < blockDim.x; ++t) {
+          const uint32_t v = s_part[t];
+          s_part[t] = run;
+          run += v;
+        }
+        xoff[n] = run;
+      }
+      __syncthreads();
+      uint32_t run = s_part[threadIdx.x];
+      for (uint32_t i = lo; i < hi; ++i) {
+        const uint32_t v = xoff[i];
+        xoff[i] = run;
+        run += v;
+      }
+    }
+    __syncthreads();
+    // pass 3: records and expanded lists
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+      rec[i] = make_rec(i, c, indeg, cidx, xoff);
+      if (!spliced(c, indeg, i)) {
+        uint4* dst = erec + xoff[i];
+        expand_list<true>(i, c, indeg, cidx, xoff, [&](const uint4& r) { *dst++ = r; });
+      }
     }
     if (threadIdx.x == 0) {
-      rec[n] = make_uint4(0u, 0u, 0u, c.succ_off[n]);
+      rec[n] = make_uint4(0u, 0u, 0u, xoff[n]);
       PackInfo inf;
       inf.first_missing = s_first;
       inf.not_fast = s_flags | (s_sum >= 0x7FFFFFFFull ? kNfDur : 0u) |

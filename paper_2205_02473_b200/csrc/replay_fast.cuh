@@ -47,7 +47,7 @@ struct FastCfg {
   uint32_t kd;     // devices per lane (template parameter)
 };
 
-constexpr int kStage = 2;   // edge records staged in registers per in-flight op
+constexpr int kStage = 3;   // edge records staged in registers per in-flight op
 constexpr int kZStage = 4;  // zero-duration ops staged per lane per round
 
 __device__ __forceinline__ void prefetch_l2(const void* p) {
@@ -127,6 +127,16 @@ struct FastWarp {
   }
 
   __device__ __forceinline__ void edge(const uint4& a, uint32_t t) {
+    if ((a.z & (kFVirt | kFMulti)) == kFVirt) {  // spliced single-pred virtual
+      const uint32_t s = a.x & kOpMask;
+      if (want) {
+        start[s] = t;
+        end[s] = t;
+      }
+      ++vcount;
+      tmax = max(tmax, t);
+      return;  // its successors follow in this same list
+    }
     if (a.z & kFMulti) {
       const uint32_t ci = (a.x >> 24) | ((a.z >> 18) << 8);
       const uint32_t sh = 8u * (ci & 3u);
@@ -400,7 +410,7 @@ __device__ bool replay_fast(const Cand& c, int cid, const uint4* rec, const uint
 }
 
 template <int KD>
-__global__ void __launch_bounds__(32) replay_fast_kernel(
+__global__ void __launch_bounds__(32, 8) replay_fast_kernel(
     const Cand* __restrict__ cands, int n_cands, Scratch S, Outs O, PackOut P,
     FastCfg F, int want_schedule, unsigned* work, unsigned* fallbacks) {
   extern __shared__ __align__(16) unsigned char fsm[];
