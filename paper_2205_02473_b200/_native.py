@@ -12,7 +12,8 @@ from pathlib import Path
 import numpy as np
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "libdpro_cuda.so"
+# DPRO_LIB: an alternative build of the same library (kernel A/B experiments)
+LIB_PATH = Path(os.environ.get("DPRO_LIB", str(_HERE / "libdpro_cuda.so")))
 
 DPRO_OK, DPRO_MISSING_PROFILE, DPRO_CYCLE, DPRO_EINVAL = 0, 1, 2, 3
 DPRO_ECUDA, DPRO_ENOMEM, DPRO_EUNSUPPORTED = 4, 5, 6

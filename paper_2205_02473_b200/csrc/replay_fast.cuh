@@ -47,7 +47,10 @@ struct FastCfg {
   uint32_t kd;     // devices per lane (template parameter)
 };
 
-constexpr int kStage = 3;   // edge records staged in registers per in-flight op
+#ifndef DPRO_KSTAGE
+#define DPRO_KSTAGE 1
+#endif
+constexpr int kStage = DPRO_KSTAGE;  // edge records staged in registers per in-flight op
 constexpr int kZStage = 4;  // zero-duration ops staged per lane per round
 
 __device__ __forceinline__ void prefetch_l2(const void* p) {
@@ -233,8 +236,7 @@ struct FastWarp {
 #pragma unroll
           for (int f = 0; f < kStage; ++f)
             if (x.z + f < x.w) st[f] = __ldg(erec + x.z + f);
-          // records past the register stage: pull their lines into L1
-          for (uint32_t k = x.z + kStage; k < x.w; k += 8) prefetch_l1(erec + k);
+          if (x.w > x.z + kStage) prefetch_l2(erec + x.z + kStage);
           break;
         }
         if (x.w > x.z && zn < kZStage) cp_async16(zst + lane * kZStage + zn++, erec + x.z);
@@ -410,7 +412,10 @@ __device__ bool replay_fast(const Cand& c, int cid, const uint4* rec, const uint
 }
 
 template <int KD>
-__global__ void __launch_bounds__(32, 8) replay_fast_kernel(
+#ifndef DPRO_MINB
+#define DPRO_MINB 8
+#endif
+__global__ void __launch_bounds__(32, DPRO_MINB) replay_fast_kernel(
     const Cand* __restrict__ cands, int n_cands, Scratch S, Outs O, PackOut P,
     FastCfg F, int want_schedule, unsigned* work, unsigned* fallbacks) {
   extern __shared__ __align__(16) unsigned char fsm[];
