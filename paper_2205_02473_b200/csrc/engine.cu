@@ -4,6 +4,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -23,6 +27,20 @@ dpro_graph* dpro_internal_tsync_graph(const dpro_cluster_desc* cluster,
                                       std::string* err);
 
 namespace {
+
+// DPRO_TRACE=1: per-phase wall times of batch registration on stderr.
+struct Tracer {
+  bool on = std::getenv("DPRO_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  void mark(const char* what, cudaStream_t s = nullptr, bool sync = false) {
+    if (!on) return;
+    if (sync) cudaStreamSynchronize(s);
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[dpro] %-28s %8.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(t - t0).count());
+    t0 = t;
+  }
+};
 
 using dpro_k::Cand;
 using dpro_k::CpScratch;
@@ -135,88 +153,134 @@ bool fits_i32(const int64_t* d, uint32_t n) {
   return true;
 }
 
-// Uploads host CSR arrays into one device arena via a pinned staging buffer
-// (packed on `threads` host threads, one H2D copy). dur -> int32 when exact.
+// Uploads host CSR arrays into one device arena through pinned staging.
+// Host threads (1) check which candidates' durations fit int32, (2) pack
+// candidates in order into staging; the calling thread issues one H2D copy
+// per finished chunk of candidates, so packing overlaps the DMA.
 int upload_host(dpro_ctx* ctx, dpro_batch* b, const dpro_csr* cands) {
+  Tracer tr;
   const int32_t n = b->n;
-  std::vector<size_t> off(n + 1, 0);
+  const int nt = std::max(1, std::min<int>(n, (int)std::thread::hardware_concurrency()));
+  auto parallel = [&](auto&& fn) {
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t) pool.emplace_back(fn, t);
+    fn(0);
+    for (auto& th : pool) th.join();
+  };
   std::vector<uint8_t> d32(n, 0);
+  {
+    std::atomic<int32_t> next{0};
+    parallel([&](int) {
+      for (int32_t i; (i = next.fetch_add(1)) < n;) {
+        const dpro_csr& c = cands[i];
+        d32[i] = c.dur_bits == 32 || c.n_ops == 0 ||
+                 fits_i32(static_cast<const int64_t*>(c.dur), c.n_ops);
+      }
+    });
+  }
+  std::vector<size_t> off(n + 1, 0);
   for (int32_t i = 0; i < n; ++i) {
     const dpro_csr& c = cands[i];
-    const bool narrow = c.dur_bits == 32 || c.n_ops == 0 ||
-                        fits_i32(static_cast<const int64_t*>(c.dur), c.n_ops);
-    d32[i] = narrow;
-    size_t s = align16(size_t(c.n_ops) * (narrow ? 4 : 8));
-    s += align16(size_t(c.n_ops) * 2);
-    s += align16(size_t(c.n_ops));
-    s += align16(size_t(c.n_ops + 1) * 4);
-    s += align16(size_t(c.n_edges) * 4);
-    s += align16(size_t(c.n_ops) * 4);
-    off[i + 1] = off[i] + s;
+    size_t sz = align16(size_t(c.n_ops) * (d32[i] ? 4 : 8));
+    sz += align16(size_t(c.n_ops) * 2);
+    sz += align16(size_t(c.n_ops));
+    sz += align16(size_t(c.n_ops + 1) * 4);
+    sz += align16(size_t(c.n_edges) * 4);
+    sz += align16(size_t(c.n_ops) * 4);
+    off[i + 1] = off[i] + sz;
   }
   const size_t total = off[n];
+  tr.mark("host: sizes + dur range");
   // the staging buffer may still feed an earlier in-flight upload
   CU(cudaStreamSynchronize(ctx->stream));
   CU(b->arena.ensure(total));
   CU(ctx->staging.ensure(total));
   char* stage = static_cast<char*>(ctx->staging.p);
-  auto pack = [&](int tid, int nt) {
-    for (int32_t i = tid; i < n; i += nt) {
-      const dpro_csr& c = cands[i];
-      char* p = stage + off[i];
-      size_t o = 0;
-      Cand& hc = b->hc[i];
-      const size_t base = off[i];
-      if (d32[i]) {
-        int32_t* dd = reinterpret_cast<int32_t*>(p + o);
-        if (c.n_ops == 0) {
-        } else if (c.dur_bits == 32)
-          std::memcpy(dd, c.dur, size_t(c.n_ops) * 4);
-        else
-          for (uint32_t k = 0; k < c.n_ops; ++k)
-            dd[k] = static_cast<int32_t>(static_cast<const int64_t*>(c.dur)[k]);
-        hc.dur64 = 0;
+  auto pack_one = [&](int32_t i) {
+    const dpro_csr& c = cands[i];
+    char* p = stage + off[i];
+    size_t o = 0;
+    Cand& hc = b->hc[i];
+    const size_t base = off[i];
+    if (d32[i]) {
+      int32_t* dd = reinterpret_cast<int32_t*>(p + o);
+      if (c.n_ops == 0) {
+      } else if (c.dur_bits == 32) {
+        std::memcpy(dd, c.dur, size_t(c.n_ops) * 4);
       } else {
-        std::memcpy(p + o, c.dur, size_t(c.n_ops) * 8);
-        hc.dur64 = 1;
+        const int64_t* src = static_cast<const int64_t*>(c.dur);
+        for (uint32_t k = 0; k < c.n_ops; ++k) dd[k] = static_cast<int32_t>(src[k]);
       }
-      hc.dur = b->arena.as<void>(base + o);
-      o += align16(size_t(c.n_ops) * (d32[i] ? 4 : 8));
-      if (c.n_ops) std::memcpy(p + o, c.dev, size_t(c.n_ops) * 2);
-      hc.dev = b->arena.as<uint16_t>(base + o);
-      o += align16(size_t(c.n_ops) * 2);
-      if (c.n_ops) std::memcpy(p + o, c.flags, c.n_ops);
-      hc.flags = b->arena.as<uint8_t>(base + o);
-      o += align16(c.n_ops);
-      if (c.succ_off)
-        std::memcpy(p + o, c.succ_off, size_t(c.n_ops + 1) * 4);
-      else
-        std::memset(p + o, 0, 4);
-      hc.succ_off = b->arena.as<uint32_t>(base + o);
-      o += align16(size_t(c.n_ops + 1) * 4);
-      if (c.n_edges) std::memcpy(p + o, c.succ, size_t(c.n_edges) * 4);
-      hc.succ = b->arena.as<uint32_t>(base + o);
-      o += align16(size_t(c.n_edges) * 4);
-      uint32_t* ind = reinterpret_cast<uint32_t*>(p + o);
-      if (c.indeg) {
-        if (c.n_ops) std::memcpy(ind, c.indeg, size_t(c.n_ops) * 4);
-      } else {
-        std::memset(ind, 0, size_t(c.n_ops) * 4);
-        for (uint32_t e = 0; e < c.n_edges; ++e) ind[c.succ[e]]++;
-      }
-      hc.indeg = b->arena.as<uint32_t>(base + o);
+      hc.dur64 = 0;
+    } else {
+      std::memcpy(p + o, c.dur, size_t(c.n_ops) * 8);
+      hc.dur64 = 1;
+    }
+    hc.dur = b->arena.as<void>(base + o);
+    o += align16(size_t(c.n_ops) * (d32[i] ? 4 : 8));
+    if (c.n_ops) std::memcpy(p + o, c.dev, size_t(c.n_ops) * 2);
+    hc.dev = b->arena.as<uint16_t>(base + o);
+    o += align16(size_t(c.n_ops) * 2);
+    if (c.n_ops) std::memcpy(p + o, c.flags, c.n_ops);
+    hc.flags = b->arena.as<uint8_t>(base + o);
+    o += align16(c.n_ops);
+    if (c.succ_off)
+      std::memcpy(p + o, c.succ_off, size_t(c.n_ops + 1) * 4);
+    else
+      std::memset(p + o, 0, 4);
+    hc.succ_off = b->arena.as<uint32_t>(base + o);
+    o += align16(size_t(c.n_ops + 1) * 4);
+    if (c.n_edges) std::memcpy(p + o, c.succ, size_t(c.n_edges) * 4);
+    hc.succ = b->arena.as<uint32_t>(base + o);
+    o += align16(size_t(c.n_edges) * 4);
+    uint32_t* ind = reinterpret_cast<uint32_t*>(p + o);
+    if (c.indeg) {
+      if (c.n_ops) std::memcpy(ind, c.indeg, size_t(c.n_ops) * 4);
+    } else {
+      std::memset(ind, 0, size_t(c.n_ops) * 4);
+      for (uint32_t e = 0; e < c.n_edges; ++e) ind[c.succ[e]]++;
+    }
+    hc.indeg = b->arena.as<uint32_t>(base + o);
+  };
+  // chunks of ~16 MB; workers pack candidates in order, the caller copies
+  std::vector<int32_t> chunk_end;
+  for (int32_t i = 0; i < n;) {
+    int32_t j = i + 1;
+    while (j < n && off[j] - off[i] < (size_t(16) << 20)) ++j;
+    chunk_end.push_back(j);
+    i = j;
+  }
+  const int nchunks = static_cast<int>(chunk_end.size());
+  std::vector<std::atomic<int32_t>> left(nchunks);
+  std::vector<int> chunk_of(n);
+  for (int k = 0, i = 0; k < nchunks; ++k) {
+    left[k] = chunk_end[k] - i;
+    for (; i < chunk_end[k]; ++i) chunk_of[i] = k;
+  }
+  std::atomic<int32_t> next{0};
+  auto worker = [&](int) {
+    for (int32_t i; (i = next.fetch_add(1)) < n;) {
+      pack_one(i);
+      left[chunk_of[i]].fetch_sub(1, std::memory_order_release);
     }
   };
-  const int nt = std::max(1, std::min<int>(n, (int)std::thread::hardware_concurrency()));
-  if (total > (size_t(8) << 20) && nt > 1) {
-    std::vector<std::thread> pool;
-    for (int t = 1; t < nt; ++t) pool.emplace_back(pack, t, nt);
-    pack(0, nt);
-    for (auto& th : pool) th.join();
-  } else {
-    pack(0, 1);
+  std::vector<std::thread> pool;
+  for (int t = 0; t < nt; ++t) pool.emplace_back(worker, t);
+  int err = DPRO_OK;
+  for (int k = 0, i = 0; k < nchunks; ++k) {
+    while (left[k].load(std::memory_order_acquire) > 0) std::this_thread::yield();
+    const size_t a = off[i], z = off[chunk_end[k]];
+    if (err == DPRO_OK && z > a) {
+      const cudaError_t e = cudaMemcpyAsync(b->arena.as<char>(a), stage + a, z - a,
+                                            cudaMemcpyHostToDevice, ctx->stream);
+      if (e != cudaSuccess) err = set_err(ctx, DPRO_ECUDA, cudaGetErrorString(e));
+    }
+    i = chunk_end[k];
   }
-  CU(cudaMemcpyAsync(b->arena.p, stage, total, cudaMemcpyHostToDevice, ctx->stream));
+  for (auto& th : pool) th.join();
+  tr.mark("host pack || H2D (issued)");
+  if (err != DPRO_OK) return err;
+  tr.mark("H2D", ctx->stream, true);
   return DPRO_OK;
 }
 
@@ -342,8 +406,10 @@ int build_batch(dpro_ctx* ctx, dpro_batch* b, const dpro_csr* cands) {
       for (int32_t i = 0; i < n; ++i) need_indeg |= (b->hc[i].indeg == nullptr);
       if (need_indeg)
         dpro_k::count_indeg_kernel<<<grid, 256, 0, ctx->stream>>>(b->desc.as<Cand>(), n, b->S);
+      Tracer tr;
       dpro_k::pack_kernel<<<grid, 256, 0, ctx->stream>>>(b->desc.as<Cand>(), n, b->S, b->P);
       CU(cudaGetLastError());
+      tr.mark("pack kernel", ctx->stream, true);
       CU(cudaMemcpyAsync(b->info.data(), b->P.info, size_t(n) * sizeof(dpro_k::PackInfo),
                          cudaMemcpyDeviceToHost, ctx->stream));
       CU(cudaStreamSynchronize(ctx->stream));
