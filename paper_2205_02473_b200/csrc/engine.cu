@@ -539,9 +539,9 @@ int launch_general(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
 
 // Fast-path shared memory per candidate (one warp per block):
 // devices x (DevF + ring) + virtual worklist + misc words + u8 counters.
-size_t fast_bytes(uint32_t dcap, uint32_t qc, uint32_t vs, uint32_t ccap) {
-  return size_t(dcap) * (sizeof(dpro_k::DevF) + 16 * qc) + 16 * vs +
-         16 * 32 * dpro_k::kZStage + 4 * dpro_k::fast_misc_words() + ccap;
+size_t fast_bytes(uint32_t dcap, uint32_t qc, uint32_t rl, uint32_t ccap) {
+  return size_t(dcap) * (sizeof(dpro_k::DevF) + 16 * qc) + 12 * size_t(rl) +
+         4 * dpro_k::fast_misc_words() + ccap;
 }
 
 template <int KD>
@@ -567,7 +567,7 @@ int launch_fast_kd(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule, FastCfg 
 int launch_fast(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
   FastCfg F;
   F.qc = ctx->ring;
-  F.vs = 64;
+  F.rl = 128;
   uint32_t max_cnt = 16;
   for (const auto& inf : b->info) max_cnt = std::max(max_cnt, inf.n_cnt);
   uint32_t kd = std::max<uint32_t>(1, (b->max_d + 31) / 32);
@@ -577,10 +577,10 @@ int launch_fast(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
   F.dcap = std::max<uint32_t>(1, std::min<uint32_t>(b->max_d, 32 * kd));
   F.ccap = (max_cnt + 15) & ~15u;
   const size_t limit = ctx->smem_optin;
-  while (fast_bytes(F.dcap, F.qc, F.vs, F.ccap) > limit && F.ccap > 16)
+  while (fast_bytes(F.dcap, F.qc, F.rl, F.ccap) > limit && F.ccap > 16)
     F.ccap = std::max<uint32_t>(16, (F.ccap / 2 + 15) & ~15u);
-  while (fast_bytes(F.dcap, F.qc, F.vs, F.ccap) > limit && F.dcap > 1) F.dcap /= 2;
-  F.warp_bytes = static_cast<uint32_t>(fast_bytes(F.dcap, F.qc, F.vs, F.ccap));
+  while (fast_bytes(F.dcap, F.qc, F.rl, F.ccap) > limit && F.dcap > 1) F.dcap /= 2;
+  F.warp_bytes = static_cast<uint32_t>(fast_bytes(F.dcap, F.qc, F.rl, F.ccap));
   switch (kd) {
     case 1: return launch_fast_kd<1>(ctx, b, want_schedule, F);
     case 2: return launch_fast_kd<2>(ctx, b, want_schedule, F);

@@ -12,11 +12,11 @@
 //     {op, dur, succ_beg, succ_end}, sorted by (ready, index) on arrival;
 //   * in-degree countdowns exist only for ops with >= 2 predecessors, as
 //     compact u8 counters in shared memory (4 per word, word atomics);
-//   * the completing op's 16-byte edge records (pack_kernel.cuh) are loaded
-//     when the op is dispatched -- into registers for the in-flight
-//     positive-duration op of each owned device, into a per-lane cp.async
-//     stage for zero-duration ops (which complete next round) -- so the
-//     completion itself rarely waits on memory.
+//   * the out-edge records of every op completing in a round (16-byte
+//     records, pack_kernel.cuh) are expanded by all 32 lanes at once: the
+//     completing lanes publish {succ_beg, count} ranges, a warp scan assigns
+//     records to lanes, so a round costs one record-load latency however
+//     many successors complete (a PS push RECV has 16);
 // Whatever the fast path cannot represent (ring or worklist overflow, a
 // virtual source -> init quirk, indeg >= 255, durations that need 64-bit
 // times, too many devices / counters, a cycle) falls back inside the same
@@ -42,34 +42,16 @@ struct FastCfg {
   uint32_t dcap;   // devices per warp
   uint32_t ccap;   // compact counters per warp (bytes, multiple of 16)
   uint32_t qc;     // ring capacity per device (power of two)
-  uint32_t vs;     // virtual worklist capacity
+  uint32_t rl;     // successor-range list capacity per round
   uint32_t warp_bytes;
   uint32_t kd;     // devices per lane (template parameter)
 };
 
-#ifndef DPRO_KSTAGE
-#define DPRO_KSTAGE 1
-#endif
-constexpr int kStage = DPRO_KSTAGE;  // edge records staged in registers per in-flight op
-constexpr int kZStage = 4;  // zero-duration ops staged per lane per round
-
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
-__device__ __forceinline__ void prefetch_l1(const void* p) {
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
-}
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(a), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.wait_all;" ::: "memory");
-}
 
+// misc words: [0] range count, [1] overflow, [4..35] per-lane dirty masks
 __host__ __device__ constexpr size_t fast_misc_words() { return 4 + 32; }
 
 template <int KD>
@@ -77,12 +59,12 @@ struct FastWarp {
   const uint4* __restrict__ rec;
   const uint4* __restrict__ erec;
   DevF* dv;
-  uint4* q;                 // [dcap][qc]
-  uint4* vstk;              // [vs]
-  uint4* zst;               // [32][kZStage] zero-op staging (cp.async)
-  volatile uint32_t* misc;  // [0] vtop [1] overflow [4..35] dirty masks
+  uint4* q;                 // [dcap][qc] per-device rings
+  uint2* rl;                // [rlcap] {succ_beg, count} ranges to expand
+  uint32_t* rloff;          // [rlcap] exclusive item offsets (per group)
+  volatile uint32_t* misc;
   uint32_t* cw;             // compact counters (u8 in words)
-  uint32_t qc, vs;
+  uint32_t qc, rlcap;
   uint32_t* qbuf;
   uint32_t* qpos;
   const uint32_t* devoff;
@@ -90,45 +72,49 @@ struct FastWarp {
   long long* end;
   bool want;
   int lane;
-  uint32_t vcount = 0, dcount = 0, tmax = 0, zn = 0;
+  uint32_t vcount = 0, dcount = 0, tmax = 0;
 
   __device__ __forceinline__ uint4* ring(uint32_t d) { return q + (size_t)d * qc; }
+
+  __device__ __forceinline__ void push_range(uint32_t sb, uint32_t n) {
+    const uint32_t p = atomicAdd(const_cast<uint32_t*>(&misc[0]), 1u);
+    if (p < rlcap)
+      rl[p] = make_uint2(sb, n);
+    else
+      misc[1] = 1u;
+  }
 
   // ready(s, t) of replay.cpp:60-72 for s reached through a packed record.
   __device__ __forceinline__ void ready(const uint4& a, uint32_t t) {
     const uint32_t s = a.x & kOpMask;
     const uint32_t cnt = (a.z >> kCntShift) & kCntMax;
     const uint32_t se = cnt == kCntMax ? __ldg(&rec[s + 1].w) : a.w + cnt;
-    const uint4 e = make_uint4(s, a.y, a.w, se);  // {op, dur, sb, se}
-    if (a.z & kFVirt) {
+    if (a.z & kFVirt) {  // multi-predecessor virtual: completes now, cascade
       if (want) {
         start[s] = t;
         end[s] = t;
       }
       ++vcount;
       tmax = max(tmax, t);
-      const uint32_t p = atomicAdd(const_cast<uint32_t*>(&misc[0]), 1u);
-      if (p < vs)
-        vstk[p] = e;
-      else
-        misc[1] = 1u;
-    } else {
-      const uint32_t d = a.z & kDevMask;
-      DevF& sd = dv[d];
-      const uint32_t pos = atomicAdd(&sd.tail, 1u);
-      const uint32_t zl = *reinterpret_cast<volatile uint32_t*>(&sd.zlo);
-      const uint32_t zh = *reinterpret_cast<volatile uint32_t*>(&sd.zhi);
-      const uint32_t low = zl < zh ? zl : *reinterpret_cast<volatile uint32_t*>(&sd.head);
-      if (pos - low >= qc) {
-        misc[1] = 1u;
-      } else {
-        ring(d)[pos & (qc - 1)] = e;
-        atomicOr(const_cast<uint32_t*>(&misc[4 + (d & 31)]), 1u << (d >> 5));
-      }
+      if (se > a.w) push_range(a.w, se - a.w);
+      return;
     }
-    if (se > a.w) prefetch_l2(erec + a.w);
+    const uint32_t d = a.z & kDevMask;
+    DevF& sd = dv[d];
+    const uint32_t pos = atomicAdd(&sd.tail, 1u);
+    const uint32_t zl = *reinterpret_cast<volatile uint32_t*>(&sd.zlo);
+    const uint32_t zh = *reinterpret_cast<volatile uint32_t*>(&sd.zhi);
+    const uint32_t low = zl < zh ? zl : *reinterpret_cast<volatile uint32_t*>(&sd.head);
+    if (pos - low >= qc) {
+      misc[1] = 1u;
+    } else {
+      ring(d)[pos & (qc - 1)] = make_uint4(s, a.y, a.w, se);  // {op, dur, sb, se}
+      atomicOr(const_cast<uint32_t*>(&misc[4 + (d & 31)]), 1u << (d >> 5));
+    }
+    if (se > a.w) prefetch_l2(erec + a.w);  // read when s completes
   }
 
+  // One out-edge record of a completing op (replay.cpp:100-103).
   __device__ __forceinline__ void edge(const uint4& a, uint32_t t) {
     if ((a.z & (kFVirt | kFMulti)) == kFVirt) {  // spliced single-pred virtual
       const uint32_t s = a.x & kOpMask;
@@ -149,44 +135,46 @@ struct FastWarp {
     ready(a, t);
   }
 
-  // Completion of e at t (replay.cpp:100-103); the first kStage records were
-  // loaded into `st` when e was dispatched.
-  __device__ __forceinline__ void complete_staged(const uint4& e, const uint4 (&st)[kStage],
-                                                  uint32_t t) {
-    const uint32_t n = e.w - e.z;
-#pragma unroll
-    for (int f = 0; f < kStage; ++f)
-      if (f < n) edge(st[f], t);
-    for (uint32_t k = e.z + kStage; k < e.w; ++k) edge(__ldg(erec + k), t);
-  }
-
-  __device__ __forceinline__ void complete(const uint4& e, uint32_t t) {
-    for (uint32_t k = e.z; k < e.w; ++k) edge(__ldg(erec + k), t);
-  }
-
-  __device__ void drain_virtual(uint32_t t) {
-    __syncwarp();
+  // Expands every range pushed this round (and the virtual cascades they
+  // trigger) with all 32 lanes: the round's out-edge records are loaded and
+  // applied in parallel instead of one lane walking each list.
+  __device__ __forceinline__ bool expand(uint32_t t) {
+    uint32_t lo = 0;
     for (;;) {
-      const uint32_t n = misc[0];
-      if (n == 0 || misc[1]) break;
-      const uint32_t k = n < 32 ? n : 32;
-      uint4 item = make_uint4(kNone, 0, 0, 0);
-      if ((uint32_t)lane < k) item = vstk[n - 1 - lane];
       __syncwarp();
-      if (lane == 0) misc[0] = n - k;
-      __syncwarp();
-      if (item.x != kNone) complete(item, t);
-      __syncwarp();
+      const uint32_t hi = misc[0];
+      if (misc[1] || hi > rlcap) return false;
+      if (lo == hi) return true;
+      for (uint32_t g = lo; g < hi; g += 32) {
+        const uint32_t r = g + lane;
+        const uint32_t len = r < hi ? rl[r].y : 0u;
+        uint32_t incl = len;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(kFull, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const uint32_t total = __shfl_sync(kFull, incl, 31);
+        if (r < hi) rloff[r] = incl - len;
+        __syncwarp();
+        const uint32_t nr = min(32u, hi - g);
+        for (uint32_t qi = lane; qi < total; qi += 32) {
+          uint32_t k = g;  // last range whose offset <= qi
+          while (k + 1 < g + nr && rloff[k + 1] <= qi) ++k;
+          edge(__ldg(erec + rl[k].x + (qi - rloff[k])), t);
+        }
+        __syncwarp();
+      }
+      lo = hi;
     }
   }
 
   // Owner-lane dispatch(t) for device d (replay.cpp:74-90) after merging
   // this round's arrivals into the (ready, index)-ordered tail segment.
-  // Returns the in-flight end (kT32Inf: idle); loads the in-flight op's first
-  // edge records into `st`; stages the first record of zero-duration ops
-  // (they complete next round) with cp.async; sets *zero when any ran.
+  // Returns the in-flight end (kT32Inf: idle); sets *zero when
+  // zero-duration ops ran (they complete next round).
   __device__ __forceinline__ uint32_t dispatch_dev(uint32_t d, uint32_t t, uint32_t iend,
-                                                   uint4 (&st)[kStage], bool* zero) {
+                                                   bool* zero) {
     DevF& s = dv[d];
     uint4* r = ring(d);
     const uint32_t tail = *reinterpret_cast<volatile uint32_t*>(&s.tail);
@@ -233,13 +221,8 @@ struct FastWarp {
           s.ient = x;
           iend = en;
           infl = true;
-#pragma unroll
-          for (int f = 0; f < kStage; ++f)
-            if (x.z + f < x.w) st[f] = __ldg(erec + x.z + f);
-          if (x.w > x.z + kStage) prefetch_l2(erec + x.z + kStage);
           break;
         }
-        if (x.w > x.z && zn < kZStage) cp_async16(zst + lane * kZStage + zn++, erec + x.z);
       }
       s.busy += busy;
       s.head = head;
@@ -262,13 +245,13 @@ __device__ bool replay_fast(const Cand& c, int cid, const uint4* rec, const uint
   const uint32_t n = c.n, D = c.d;
   DevF* dv = reinterpret_cast<DevF*>(wsm);
   uint4* q = reinterpret_cast<uint4*>(wsm + sizeof(DevF) * F.dcap);
-  uint4* vstk = q + (size_t)F.dcap * F.qc;
-  uint4* zst = vstk + F.vs;
-  volatile uint32_t* misc = reinterpret_cast<volatile uint32_t*>(zst + 32 * kZStage);
+  uint2* rl = reinterpret_cast<uint2*>(q + (size_t)F.dcap * F.qc);
+  uint32_t* rloff = reinterpret_cast<uint32_t*>(rl + F.rl);
+  volatile uint32_t* misc = reinterpret_cast<volatile uint32_t*>(rloff + F.rl);
   uint32_t* cw = const_cast<uint32_t*>(misc) + fast_misc_words();
   const unsigned long long oo = c.op_off;
 
-  FastWarp<KD> W{rec, erec, dv, q, vstk, zst, misc, cw, F.qc, F.vs, S.qbuf + oo, S.qpos + oo,
+  FastWarp<KD> W{rec, erec, dv, q, rl, rloff, misc, cw, F.qc, F.rl, S.qbuf + oo, S.qpos + oo,
                  S.devoff + c.dof_off,
                  want_schedule ? O.start + oo : nullptr,
                  want_schedule ? O.end + oo : nullptr, want_schedule, lane};
@@ -314,86 +297,72 @@ __device__ bool replay_fast(const Cand& c, int cid, const uint4* rec, const uint
 
   // ---- dispatch(0) + event loop (replay.cpp:95-106) ----
   uint32_t iend[KD];
-  uint4 stg[KD][kStage];
   uint32_t zmask = 0;
 #pragma unroll
   for (int j = 0; j < KD; ++j) {
     iend[j] = kT32Inf;
-#pragma unroll
-    for (int f = 0; f < kStage; ++f) stg[j][f] = make_uint4(0, 0, 0, 0);
     const uint32_t d = lane + 32 * j;
     if (d < D) {
       bool z = false;
-      iend[j] = W.dispatch_dev(d, 0u, kT32Inf, stg[j], &z);
+      iend[j] = W.dispatch_dev(d, 0u, kT32Inf, &z);
       if (z) zmask |= 1u << j;
     }
   }
-  cp_async_commit();
   misc[4 + lane] = 0;  // all devices were just visited
   uint32_t t = 0;
   for (;;) {
     const bool zero_round = __any_sync(kFull, zmask != 0);
     uint32_t freed = 0;
-    if (zero_round) {
-      // zero-duration ops dispatched last round complete now (same t); their
-      // first edge records were staged by cp.async in that dispatch
-      cp_async_wait_all();
-      uint32_t zi = 0;
-      uint32_t zm = zmask;
-      while (zm) {
-        const int j = __ffs(zm) - 1;
-        zm &= zm - 1;
-        const uint32_t d = lane + 32 * j;
-        DevF& s = dv[d];
-        const uint4* r = W.ring(d);
-        const uint32_t zh = s.zhi;
-        for (uint32_t p = s.zlo; p < zh; ++p) {
-          const uint4 e = r[p & (F.qc - 1)];
-          if (e.w > e.z) {
-            uint32_t k = e.z;
-            if (zi < kZStage) {
-              W.edge(zst[lane * kZStage + zi++], t);
-              ++k;
-            }
-            for (; k < e.w; ++k) W.edge(__ldg(erec + k), t);
-          }
-        }
-        *reinterpret_cast<volatile uint32_t*>(&s.zlo) = zh;
-      }
-      zmask = 0;
-    } else {
+    if (!zero_round) {
       uint32_t lmin = kT32Inf;
 #pragma unroll
       for (int j = 0; j < KD; ++j) lmin = min(lmin, iend[j]);
       const uint32_t tn = __reduce_min_sync(kFull, lmin);
       if (tn == kT32Inf) break;
       t = tn;
+    }
+    if (lane == 0) misc[0] = 0;
+    __syncwarp();
+    if (zero_round) {
+      // zero-duration ops dispatched last round complete now (same t)
+      uint32_t zm = zmask;
+      while (zm) {
+        const int j = __ffs(zm) - 1;
+        zm &= zm - 1;
+        DevF& s = dv[lane + 32 * j];
+        const uint4* r = W.ring(lane + 32 * j);
+        const uint32_t zh = s.zhi;
+        for (uint32_t p = s.zlo; p < zh; ++p) {
+          const uint4 e = r[p & (F.qc - 1)];
+          if (e.w > e.z) W.push_range(e.z, e.w - e.z);
+        }
+        *reinterpret_cast<volatile uint32_t*>(&s.zlo) = zh;
+      }
+      zmask = 0;
+    } else {
 #pragma unroll
       for (int j = 0; j < KD; ++j) {
         if (iend[j] == t) {
           iend[j] = kT32Inf;
           freed |= 1u << j;
-          W.complete_staged(dv[lane + 32 * j].ient, stg[j], t);
+          const uint4 e = dv[lane + 32 * j].ient;
+          if (e.w > e.z) W.push_range(e.z, e.w - e.z);
         }
       }
     }
-    W.drain_virtual(t);
+    if (!W.expand(t)) return false;
     __syncwarp();
-    if (__any_sync(kFull, misc[1] != 0)) return false;
     const uint32_t todo = freed | misc[4 + lane];
     misc[4 + lane] = 0;
-    W.zn = 0;
 #pragma unroll
     for (int j = 0; j < KD; ++j) {
       if (todo & (1u << j)) {
         bool z = false;
-        iend[j] = W.dispatch_dev(lane + 32 * j, t, iend[j], stg[j], &z);
+        iend[j] = W.dispatch_dev(lane + 32 * j, t, iend[j], &z);
         if (z) zmask |= 1u << j;
       }
     }
-    cp_async_commit();
   }
-  cp_async_wait_all();
 
   const uint32_t vc = __reduce_add_sync(kFull, W.vcount);
   const uint32_t dc = __reduce_add_sync(kFull, W.dcount);
@@ -411,10 +380,10 @@ __device__ bool replay_fast(const Cand& c, int cid, const uint4* rec, const uint
   return true;
 }
 
-template <int KD>
 #ifndef DPRO_MINB
 #define DPRO_MINB 8
 #endif
+template <int KD>
 __global__ void __launch_bounds__(32, DPRO_MINB) replay_fast_kernel(
     const Cand* __restrict__ cands, int n_cands, Scratch S, Outs O, PackOut P,
     FastCfg F, int want_schedule, unsigned* work, unsigned* fallbacks) {
