@@ -611,6 +611,15 @@ int dpro_cuda_batch_replay(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) 
   return DPRO_OK;
 }
 
+#ifdef DPRO_PROFILE
+extern "C" int dpro_debug_prof(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, dpro_k::g_prof, sizeof(unsigned long long) * 16);
+  unsigned long long z[16] = {0};
+  cudaMemcpyToSymbol(dpro_k::g_prof, z, sizeof z);
+  return 0;
+}
+#endif
+
 int dpro_cuda_batch_stats(dpro_ctx* ctx, dpro_batch* b, int64_t* stats) {
   if (!ctx || !b || !stats) return DPRO_EINVAL;
   CU(cudaSetDevice(ctx->device));

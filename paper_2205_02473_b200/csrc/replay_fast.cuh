@@ -51,6 +51,11 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
+#ifndef DPRO_MLP
+#define DPRO_MLP 4
+#endif
+constexpr int kMlp = DPRO_MLP;  // record loads in flight per lane in expand()
+
 // misc words: [0] range count, [1] overflow, [4..35] per-lane dirty masks
 __host__ __device__ constexpr size_t fast_misc_words() { return 4 + 32; }
 
@@ -158,10 +163,23 @@ struct FastWarp {
         if (r < hi) rloff[r] = incl - len;
         __syncwarp();
         const uint32_t nr = min(32u, hi - g);
-        for (uint32_t qi = lane; qi < total; qi += 32) {
-          uint32_t k = g;  // last range whose offset <= qi
-          while (k + 1 < g + nr && rloff[k + 1] <= qi) ++k;
-          edge(__ldg(erec + rl[k].x + (qi - rloff[k])), t);
+        // memory-level parallelism: each lane issues up to kMlp record loads
+        // back to back, then applies them (edge() has atomics, so the
+        // compiler would otherwise serialize load -> apply -> next load)
+        for (uint32_t base = 0; base < total; base += 32u * kMlp) {
+          uint4 a[kMlp];
+#pragma unroll
+          for (int b = 0; b < kMlp; ++b) {
+            const uint32_t qi = base + lane + 32u * b;
+            if (qi < total) {
+              uint32_t k = g;  // last range whose offset <= qi
+              while (k + 1 < g + nr && rloff[k + 1] <= qi) ++k;
+              a[b] = __ldg(erec + rl[k].x + (qi - rloff[k]));
+            }
+          }
+#pragma unroll
+          for (int b = 0; b < kMlp; ++b)
+            if (base + lane + 32u * b < total) edge(a[b], t);
         }
         __syncwarp();
       }
@@ -234,6 +252,17 @@ struct FastWarp {
     return iend;
   }
 };
+
+#ifdef DPRO_PROFILE
+// per-candidate phase counters (experiment builds only): written to
+// Scratch::busy of device 0 region? no -- to a global debug array.
+__device__ unsigned long long g_prof[16];
+#define PROF_T(v) const long long v = clock64()
+#define PROF_ADD(i, x) if (lane == 0) atomicAdd(&g_prof[i], (unsigned long long)(x))
+#else
+#define PROF_T(v)
+#define PROF_ADD(i, x)
+#endif
 
 // Returns false when the candidate must take the general path.
 template <int KD>
@@ -311,6 +340,7 @@ __device__ bool replay_fast(const Cand& c, int cid, const uint4* rec, const uint
   misc[4 + lane] = 0;  // all devices were just visited
   uint32_t t = 0;
   for (;;) {
+    PROF_T(p0);
     const bool zero_round = __any_sync(kFull, zmask != 0);
     uint32_t freed = 0;
     if (!zero_round) {
@@ -321,6 +351,7 @@ __device__ bool replay_fast(const Cand& c, int cid, const uint4* rec, const uint
       if (tn == kT32Inf) break;
       t = tn;
     }
+    PROF_T(p1);
     if (lane == 0) misc[0] = 0;
     __syncwarp();
     if (zero_round) {
@@ -350,8 +381,13 @@ __device__ bool replay_fast(const Cand& c, int cid, const uint4* rec, const uint
         }
       }
     }
+    PROF_T(p2);
+#ifdef DPRO_PROFILE
+    const uint32_t nranges = misc[0];
+#endif
     if (!W.expand(t)) return false;
     __syncwarp();
+    PROF_T(p3);
     const uint32_t todo = freed | misc[4 + lane];
     misc[4 + lane] = 0;
 #pragma unroll
@@ -362,6 +398,19 @@ __device__ bool replay_fast(const Cand& c, int cid, const uint4* rec, const uint
         if (z) zmask |= 1u << j;
       }
     }
+#ifdef DPRO_PROFILE
+    __syncwarp();
+    PROF_T(p4);
+    PROF_ADD(0, 1);
+    PROF_ADD(1, zero_round ? 1 : 0);
+    PROF_ADD(2, p1 - p0);
+    PROF_ADD(3, p2 - p1);
+    PROF_ADD(4, p3 - p2);
+    PROF_ADD(5, p4 - p3);
+    PROF_ADD(6, nranges);
+    const uint32_t ndisp = __popc(__ballot_sync(kFull, todo != 0));
+    PROF_ADD(7, ndisp);
+#endif
   }
 
   const uint32_t vc = __reduce_add_sync(kFull, W.vcount);

@@ -1,0 +1,34 @@
+"""Phase breakdown of the fast replay (needs a -DDPRO_PROFILE build in DPRO_LIB)."""
+import ctypes as C
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2205_02473_b200 import _native as N  # noqa: E402
+from paper_2205_02473_b200.engine import Engine  # noqa: E402
+from paper_2205_02473_b200.ingest import layered_graphs  # noqa: E402
+from paper_2205_02473_b200.workloads import workload  # noqa: E402
+
+cfg = int(os.environ.get("CFG", "2"))
+nb = int(os.environ.get("NB", "1024"))
+w = workload(cfg)
+graphs = layered_graphs(w.model, w.cluster, w.candidate_partitions(nb), threads=16)
+eng = Engine(0)
+b = eng.batch([g.csr for g in graphs])
+fn = N.lib.dpro_debug_prof
+fn.argtypes = [C.c_void_p]
+buf = np.zeros(16, np.uint64)
+b.replay(True); b.results(); fn(buf.ctypes.data)
+b.replay(True); b.results(); fn(buf.ctypes.data)
+rounds, zr = int(buf[0]), int(buf[1])
+print(f"candidates {nb}: rounds/cand {rounds/nb:.0f} (zero rounds {zr/nb:.0f})")
+names = ["reduce+zero-check", "collect ranges", "expand", "dispatch"]
+tot = sum(int(buf[i]) for i in range(2, 6))
+for i, nm in enumerate(names):
+    v = int(buf[2 + i])
+    print(f"  {nm:18s} {v/rounds:8.1f} cycles/round ({100*v/tot:4.1f}%)")
+print(f"  total {tot/rounds:.1f} cycles/round; ranges/round {int(buf[6])/rounds:.2f}; "
+      f"dispatching lanes/round {int(buf[7])/rounds:.2f}")
