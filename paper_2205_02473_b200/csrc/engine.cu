@@ -104,6 +104,7 @@ struct dpro_ctx {
   HostPinned staging;
   int fast = 1;       // option "fast"
   uint32_t ring = 4;  // option "ring"
+  int warps = 1;      // option "warps": warps (1, 2, 4) per candidate
   dpro_batch* spare = nullptr;  // recycled arenas for repeated small calls
 };
 
@@ -507,6 +508,10 @@ int dpro_cuda_set_option(dpro_ctx* ctx, const char* key, int64_t value) {
     ctx->fast = static_cast<int>(value);
     return DPRO_OK;
   }
+  if (k == "warps" && (value == 1 || value == 2 || value == 4)) {
+    ctx->warps = static_cast<int>(value);
+    return DPRO_OK;
+  }
   if (k == "ring" && value >= 2 && value <= 64 && (value & (value - 1)) == 0) {
     ctx->ring = static_cast<uint32_t>(value);
     return DPRO_OK;
@@ -539,59 +544,69 @@ int launch_general(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
 
 // Fast-path shared memory per candidate (one warp per block):
 // devices x (DevF + ring) + virtual worklist + misc words + u8 counters.
-size_t fast_bytes(uint32_t dcap, uint32_t qc, uint32_t rl, uint32_t ccap) {
-  return size_t(dcap) * (sizeof(dpro_k::DevF) + 16 * qc) + 12 * size_t(rl) +
-         4 * dpro_k::fast_misc_words() + ccap;
+size_t fast_bytes(uint32_t dcap, uint32_t qc, uint32_t rl, uint32_t ccap, int nw) {
+  return size_t(dcap) * (sizeof(dpro_k::DevF) + 16 * qc) + 8 * size_t(rl) +
+         4 * dpro_k::fast_misc_words(nw) + ccap;
 }
 
-template <int KD>
+template <int NW, int KD>
 int launch_fast_kd(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule, FastCfg F) {
   const size_t smem = F.warp_bytes;
-  CU(cudaFuncSetAttribute(dpro_k::replay_fast_kernel<KD>,
+  CU(cudaFuncSetAttribute(dpro_k::replay_fast_kernel<NW, KD>,
                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int blocks_per_sm = 0;
-  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm,
-                                                   dpro_k::replay_fast_kernel<KD>, 32, smem));
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &blocks_per_sm, dpro_k::replay_fast_kernel<NW, KD>, 32 * NW, smem));
   blocks_per_sm = std::max(blocks_per_sm, 1);
   b->blocks_per_sm_fast = blocks_per_sm;
   const int grid = std::max(1, std::min(b->n, ctx->sm_count * blocks_per_sm));
   CU(cudaMemsetAsync(b->work.p, 0, 8, ctx->stream));
   b->F = F;
-  dpro_k::replay_fast_kernel<KD><<<grid, 32, smem, ctx->stream>>>(
+  dpro_k::replay_fast_kernel<NW, KD><<<grid, 32 * NW, smem, ctx->stream>>>(
       b->desc.as<Cand>(), b->n, b->S, b->O, b->P, F, want_schedule ? 1 : 0,
       b->work.as<unsigned>(), b->work.as<unsigned>() + 1);
   CU(cudaGetLastError());
   return DPRO_OK;
 }
 
-int launch_fast(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
+template <int NW>
+int launch_fast_nw(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
   FastCfg F;
   F.qc = ctx->ring;
   F.rl = 128;
   uint32_t max_cnt = 16;
   for (const auto& inf : b->info) max_cnt = std::max(max_cnt, inf.n_cnt);
-  uint32_t kd = std::max<uint32_t>(1, (b->max_d + 31) / 32);
+  const uint32_t nt = 32 * NW;
+  uint32_t kd = std::max<uint32_t>(1, (b->max_d + nt - 1) / nt);
   if (kd > 8) kd = kd <= 12 ? 12 : 16;
   if (b->max_d > dpro_k::kMaxDev) kd = 16;
   F.kd = kd;
-  F.dcap = std::max<uint32_t>(1, std::min<uint32_t>(b->max_d, 32 * kd));
+  F.dcap = std::max<uint32_t>(1, std::min<uint32_t>(b->max_d, nt * kd));
   F.ccap = (max_cnt + 15) & ~15u;
-  const size_t limit = ctx->smem_optin;
-  while (fast_bytes(F.dcap, F.qc, F.rl, F.ccap) > limit && F.ccap > 16)
+  const size_t limit = ctx->smem_optin - 64;
+  while (fast_bytes(F.dcap, F.qc, F.rl, F.ccap, NW) > limit && F.ccap > 16)
     F.ccap = std::max<uint32_t>(16, (F.ccap / 2 + 15) & ~15u);
-  while (fast_bytes(F.dcap, F.qc, F.rl, F.ccap) > limit && F.dcap > 1) F.dcap /= 2;
-  F.warp_bytes = static_cast<uint32_t>(fast_bytes(F.dcap, F.qc, F.rl, F.ccap));
+  while (fast_bytes(F.dcap, F.qc, F.rl, F.ccap, NW) > limit && F.dcap > 1) F.dcap /= 2;
+  F.warp_bytes = static_cast<uint32_t>(fast_bytes(F.dcap, F.qc, F.rl, F.ccap, NW));
   switch (kd) {
-    case 1: return launch_fast_kd<1>(ctx, b, want_schedule, F);
-    case 2: return launch_fast_kd<2>(ctx, b, want_schedule, F);
-    case 3: return launch_fast_kd<3>(ctx, b, want_schedule, F);
-    case 4: return launch_fast_kd<4>(ctx, b, want_schedule, F);
-    case 5: return launch_fast_kd<5>(ctx, b, want_schedule, F);
-    case 6: return launch_fast_kd<6>(ctx, b, want_schedule, F);
-    case 7: return launch_fast_kd<7>(ctx, b, want_schedule, F);
-    case 8: return launch_fast_kd<8>(ctx, b, want_schedule, F);
-    case 12: return launch_fast_kd<12>(ctx, b, want_schedule, F);
-    default: return launch_fast_kd<16>(ctx, b, want_schedule, F);
+    case 1: return launch_fast_kd<NW, 1>(ctx, b, want_schedule, F);
+    case 2: return launch_fast_kd<NW, 2>(ctx, b, want_schedule, F);
+    case 3: return launch_fast_kd<NW, 3>(ctx, b, want_schedule, F);
+    case 4: return launch_fast_kd<NW, 4>(ctx, b, want_schedule, F);
+    case 5: return launch_fast_kd<NW, 5>(ctx, b, want_schedule, F);
+    case 6: return launch_fast_kd<NW, 6>(ctx, b, want_schedule, F);
+    case 7: return launch_fast_kd<NW, 7>(ctx, b, want_schedule, F);
+    case 8: return launch_fast_kd<NW, 8>(ctx, b, want_schedule, F);
+    case 12: return launch_fast_kd<NW, 12>(ctx, b, want_schedule, F);
+    default: return launch_fast_kd<NW, 16>(ctx, b, want_schedule, F);
+  }
+}
+
+int launch_fast(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
+  switch (ctx->warps) {
+    case 1: return launch_fast_nw<1>(ctx, b, want_schedule);
+    case 2: return launch_fast_nw<2>(ctx, b, want_schedule);
+    default: return launch_fast_nw<4>(ctx, b, want_schedule);
   }
 }
 

@@ -56,17 +56,71 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
 #endif
 constexpr int kMlp = DPRO_MLP;  // record loads in flight per lane in expand()
 
-// misc words: [0] range count, [1] overflow, [4..35] per-lane dirty masks
-__host__ __device__ constexpr size_t fast_misc_words() { return 4 + 32; }
+// misc words: [0] range count, [1] overflow, [4, 4+NT) per-thread dirty
+// masks, then 2*NW words of double-buffered reduction scratch.
+__host__ __device__ constexpr size_t fast_misc_words(int nw) { return 4 + 32 * nw + 2 * nw; }
 
-template <int KD>
+// Group-wide collectives for one candidate replayed by NW warps (one CTA).
+template <int NW>
+__device__ __forceinline__ void gsync() {
+  if (NW == 1)
+    __syncwarp();
+  else
+    __syncthreads();
+}
+template <int NW>
+__device__ __forceinline__ bool gany(bool p) {
+  if (NW == 1) return __any_sync(kFull, p);
+  return __syncthreads_or(p) != 0;
+}
+template <int NW>
+__device__ __forceinline__ uint32_t gmin(uint32_t v, volatile uint32_t* red, uint32_t& par) {
+  v = __reduce_min_sync(kFull, v);
+  if (NW == 1) return v;
+  volatile uint32_t* r = red + (par & 1u) * NW;
+  ++par;
+  if ((threadIdx.x & 31) == 0) r[threadIdx.x >> 5] = v;
+  __syncthreads();
+  uint32_t m = r[0];
+#pragma unroll
+  for (int w = 1; w < NW; ++w) m = min(m, r[w]);
+  return m;
+}
+template <int NW>
+__device__ __forceinline__ uint32_t gsum(uint32_t v, volatile uint32_t* red, uint32_t& par) {
+  v = __reduce_add_sync(kFull, v);
+  if (NW == 1) return v;
+  volatile uint32_t* r = red + (par & 1u) * NW;
+  ++par;
+  if ((threadIdx.x & 31) == 0) r[threadIdx.x >> 5] = v;
+  __syncthreads();
+  uint32_t m = 0;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) m += r[w];
+  return m;
+}
+template <int NW>
+__device__ __forceinline__ uint32_t gmax(uint32_t v, volatile uint32_t* red, uint32_t& par) {
+  v = __reduce_max_sync(kFull, v);
+  if (NW == 1) return v;
+  volatile uint32_t* r = red + (par & 1u) * NW;
+  ++par;
+  if ((threadIdx.x & 31) == 0) r[threadIdx.x >> 5] = v;
+  __syncthreads();
+  uint32_t m = 0;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) m = max(m, r[w]);
+  return m;
+}
+
+template <int NW, int KD>
 struct FastWarp {
+  static constexpr uint32_t NT = 32u * NW;
   const uint4* __restrict__ rec;
   const uint4* __restrict__ erec;
   DevF* dv;
   uint4* q;                 // [dcap][qc] per-device rings
   uint2* rl;                // [rlcap] {succ_beg, count} ranges to expand
-  uint32_t* rloff;          // [rlcap] exclusive item offsets (per group)
   volatile uint32_t* misc;
   uint32_t* cw;             // compact counters (u8 in words)
   uint32_t qc, rlcap;
@@ -77,6 +131,7 @@ struct FastWarp {
   long long* end;
   bool want;
   int lane;
+  int tid;
   uint32_t vcount = 0, dcount = 0, tmax = 0;
 
   __device__ __forceinline__ uint4* ring(uint32_t d) { return q + (size_t)d * qc; }
@@ -114,7 +169,7 @@ struct FastWarp {
       misc[1] = 1u;
     } else {
       ring(d)[pos & (qc - 1)] = make_uint4(s, a.y, a.w, se);  // {op, dur, sb, se}
-      atomicOr(const_cast<uint32_t*>(&misc[4 + (d & 31)]), 1u << (d >> 5));
+      atomicOr(const_cast<uint32_t*>(&misc[4 + (d % NT)]), 1u << (d / NT));
     }
     if (se > a.w) prefetch_l2(erec + a.w);  // read when s completes
   }
@@ -146,42 +201,49 @@ struct FastWarp {
   __device__ __forceinline__ bool expand(uint32_t t) {
     uint32_t lo = 0;
     for (;;) {
-      __syncwarp();
+      gsync<NW>();
       const uint32_t hi = misc[0];
       if (misc[1] || hi > rlcap) return false;
       if (lo == hi) return true;
       for (uint32_t g = lo; g < hi; g += 32) {
         const uint32_t r = g + lane;
-        const uint32_t len = r < hi ? rl[r].y : 0u;
-        uint32_t incl = len;
+        uint2 mine = make_uint2(0u, 0u);
+        if (r < hi) mine = rl[r];
+        uint32_t incl = mine.y;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const uint32_t y = __shfl_up_sync(kFull, incl, o);
           if (lane >= o) incl += y;
         }
         const uint32_t total = __shfl_sync(kFull, incl, 31);
-        if (r < hi) rloff[r] = incl - len;
-        __syncwarp();
         const uint32_t nr = min(32u, hi - g);
+        // lane r holds range r's first item index; items map to ranges by a
+        // 5-step shuffle binary search (no shared-memory walk)
+        const uint32_t excl = (uint32_t)lane < nr ? incl - mine.y : 0xFFFFFFFFu;
         // memory-level parallelism: each lane issues up to kMlp record loads
         // back to back, then applies them (edge() has atomics, so the
         // compiler would otherwise serialize load -> apply -> next load)
-        for (uint32_t base = 0; base < total; base += 32u * kMlp) {
+        for (uint32_t base = 0; base < total; base += NT * kMlp) {
           uint4 a[kMlp];
 #pragma unroll
           for (int b = 0; b < kMlp; ++b) {
-            const uint32_t qi = base + lane + 32u * b;
-            if (qi < total) {
-              uint32_t k = g;  // last range whose offset <= qi
-              while (k + 1 < g + nr && rloff[k + 1] <= qi) ++k;
-              a[b] = __ldg(erec + rl[k].x + (qi - rloff[k]));
+            const uint32_t qi = base + tid + NT * b;
+            int k = 0;
+#pragma unroll
+            for (int step = 16; step; step >>= 1) {
+              const int cand = k + step;
+              const uint32_t v = __shfl_sync(kFull, excl, cand & 31);
+              if (cand < 32 && v <= qi) k = cand;
             }
+            const uint32_t sb = __shfl_sync(kFull, mine.x, k);
+            const uint32_t ex = __shfl_sync(kFull, excl, k);
+            if (qi < total) a[b] = __ldg(erec + sb + (qi - ex));
           }
 #pragma unroll
           for (int b = 0; b < kMlp; ++b)
-            if (base + lane + 32u * b < total) edge(a[b], t);
+            if (base + tid + NT * b < total) edge(a[b], t);
         }
-        __syncwarp();
+        gsync<NW>();
       }
       lo = hi;
     }
@@ -258,56 +320,59 @@ struct FastWarp {
 // Scratch::busy of device 0 region? no -- to a global debug array.
 __device__ unsigned long long g_prof[16];
 #define PROF_T(v) const long long v = clock64()
-#define PROF_ADD(i, x) if (lane == 0) atomicAdd(&g_prof[i], (unsigned long long)(x))
+#define PROF_ADD(i, x) if (threadIdx.x == 0) atomicAdd(&g_prof[i], (unsigned long long)(x))
 #else
 #define PROF_T(v)
 #define PROF_ADD(i, x)
 #endif
 
 // Returns false when the candidate must take the general path.
-template <int KD>
+template <int NW, int KD>
 __device__ bool replay_fast(const Cand& c, int cid, const uint4* rec, const uint4* erec,
                             const uint8_t* cnt0, const uint32_t* srcs, const PackInfo& info,
                             unsigned char* wsm, const FastCfg& F, const Scratch& S,
                             const Outs& O, bool want_schedule) {
+  constexpr uint32_t NT = 32u * NW;
   const int lane = threadIdx.x & 31;
+  const int tid = threadIdx.x;
   const uint32_t n = c.n, D = c.d;
   DevF* dv = reinterpret_cast<DevF*>(wsm);
   uint4* q = reinterpret_cast<uint4*>(wsm + sizeof(DevF) * F.dcap);
   uint2* rl = reinterpret_cast<uint2*>(q + (size_t)F.dcap * F.qc);
-  uint32_t* rloff = reinterpret_cast<uint32_t*>(rl + F.rl);
-  volatile uint32_t* misc = reinterpret_cast<volatile uint32_t*>(rloff + F.rl);
-  uint32_t* cw = const_cast<uint32_t*>(misc) + fast_misc_words();
+  volatile uint32_t* misc = reinterpret_cast<volatile uint32_t*>(rl + F.rl);
+  uint32_t* cw = const_cast<uint32_t*>(misc) + fast_misc_words(NW);
+  volatile uint32_t* red = misc + 4 + NT;
+  uint32_t par = 0;
   const unsigned long long oo = c.op_off;
 
-  FastWarp<KD> W{rec, erec, dv, q, rl, rloff, misc, cw, F.qc, F.rl, S.qbuf + oo, S.qpos + oo,
+  FastWarp<NW, KD> W{rec, erec, dv, q, rl, misc, cw, F.qc, F.rl, S.qbuf + oo, S.qpos + oo,
                  S.devoff + c.dof_off,
                  want_schedule ? O.start + oo : nullptr,
-                 want_schedule ? O.end + oo : nullptr, want_schedule, lane};
+                 want_schedule ? O.end + oo : nullptr, want_schedule, lane, tid};
 
   // ---- state init ----
   {
     const uint32_t nv = (info.n_cnt + 15) / 16;
     const uint4* src = reinterpret_cast<const uint4*>(cnt0);
     uint4* dst = reinterpret_cast<uint4*>(cw);
-    for (uint32_t i = lane; i < nv; i += 32) dst[i] = __ldg(src + i);
+    for (uint32_t i = tid; i < nv; i += NT) dst[i] = __ldg(src + i);
   }
-  for (uint32_t d = lane; d < D; d += 32) {
+  for (uint32_t d = tid; d < D; d += NT) {
     DevF z;
     z.head = z.tail = z.tsort = z.segbeg = 0;
     z.zlo = z.zhi = z.segt = z.busy = 0;
     z.ient = make_uint4(0, 0, 0, 0);
     dv[d] = z;
   }
-  if (lane < 4) misc[lane] = 0;
-  misc[4 + lane] = 0;
-  __syncwarp();
+  if (tid < 4) misc[tid] = 0;
+  misc[4 + tid] = 0;
+  gsync<NW>();
   // ---- sources (replay.cpp:92-94). No virtual sources reach the fast path
   // (pack flags them), so there are no cascades and no init quirk. ----
-  for (uint32_t k = lane; k < info.n_src; k += 32) W.ready(__ldg(rec + __ldg(srcs + k)), 0u);
-  __syncwarp();
-  if (__any_sync(kFull, misc[1] != 0)) return false;
-  for (uint32_t d = lane; d < D; d += 32) {  // t = 0 arrivals in index order
+  for (uint32_t k = tid; k < info.n_src; k += NT) W.ready(__ldg(rec + __ldg(srcs + k)), 0u);
+  gsync<NW>();
+  if (gany<NW>(misc[1] != 0)) return false;
+  for (uint32_t d = tid; d < D; d += NT) {  // t = 0 arrivals in index order
     DevF& s = dv[d];
     uint4* r = W.ring(d);
     const uint32_t m = F.qc - 1;
@@ -322,7 +387,7 @@ __device__ bool replay_fast(const Cand& c, int cid, const uint4* rec, const uint
     }
     s.tsort = s.tail;
   }
-  __syncwarp();
+  gsync<NW>();
 
   // ---- dispatch(0) + event loop (replay.cpp:95-106) ----
   uint32_t iend[KD];
@@ -330,38 +395,38 @@ __device__ bool replay_fast(const Cand& c, int cid, const uint4* rec, const uint
 #pragma unroll
   for (int j = 0; j < KD; ++j) {
     iend[j] = kT32Inf;
-    const uint32_t d = lane + 32 * j;
+    const uint32_t d = tid + NT * j;
     if (d < D) {
       bool z = false;
       iend[j] = W.dispatch_dev(d, 0u, kT32Inf, &z);
       if (z) zmask |= 1u << j;
     }
   }
-  misc[4 + lane] = 0;  // all devices were just visited
+  misc[4 + tid] = 0;  // all devices were just visited
   uint32_t t = 0;
   for (;;) {
     PROF_T(p0);
-    const bool zero_round = __any_sync(kFull, zmask != 0);
+    const bool zero_round = gany<NW>(zmask != 0);
     uint32_t freed = 0;
     if (!zero_round) {
       uint32_t lmin = kT32Inf;
 #pragma unroll
       for (int j = 0; j < KD; ++j) lmin = min(lmin, iend[j]);
-      const uint32_t tn = __reduce_min_sync(kFull, lmin);
+      const uint32_t tn = gmin<NW>(lmin, red, par);
       if (tn == kT32Inf) break;
       t = tn;
     }
     PROF_T(p1);
-    if (lane == 0) misc[0] = 0;
-    __syncwarp();
+    if (tid == 0) misc[0] = 0;
+    gsync<NW>();
     if (zero_round) {
       // zero-duration ops dispatched last round complete now (same t)
       uint32_t zm = zmask;
       while (zm) {
         const int j = __ffs(zm) - 1;
         zm &= zm - 1;
-        DevF& s = dv[lane + 32 * j];
-        const uint4* r = W.ring(lane + 32 * j);
+        DevF& s = dv[tid + NT * j];
+        const uint4* r = W.ring(tid + NT * j);
         const uint32_t zh = s.zhi;
         for (uint32_t p = s.zlo; p < zh; ++p) {
           const uint4 e = r[p & (F.qc - 1)];
@@ -376,7 +441,7 @@ __device__ bool replay_fast(const Cand& c, int cid, const uint4* rec, const uint
         if (iend[j] == t) {
           iend[j] = kT32Inf;
           freed |= 1u << j;
-          const uint4 e = dv[lane + 32 * j].ient;
+          const uint4 e = dv[tid + NT * j].ient;
           if (e.w > e.z) W.push_range(e.z, e.w - e.z);
         }
       }
@@ -386,20 +451,20 @@ __device__ bool replay_fast(const Cand& c, int cid, const uint4* rec, const uint
     const uint32_t nranges = misc[0];
 #endif
     if (!W.expand(t)) return false;
-    __syncwarp();
+    gsync<NW>();
     PROF_T(p3);
-    const uint32_t todo = freed | misc[4 + lane];
-    misc[4 + lane] = 0;
+    const uint32_t todo = freed | misc[4 + tid];
+    misc[4 + tid] = 0;
 #pragma unroll
     for (int j = 0; j < KD; ++j) {
       if (todo & (1u << j)) {
         bool z = false;
-        iend[j] = W.dispatch_dev(lane + 32 * j, t, iend[j], &z);
+        iend[j] = W.dispatch_dev(tid + NT * j, t, iend[j], &z);
         if (z) zmask |= 1u << j;
       }
     }
 #ifdef DPRO_PROFILE
-    __syncwarp();
+    gsync<NW>();
     PROF_T(p4);
     PROF_ADD(0, 1);
     PROF_ADD(1, zero_round ? 1 : 0);
@@ -408,20 +473,20 @@ __device__ bool replay_fast(const Cand& c, int cid, const uint4* rec, const uint
     PROF_ADD(4, p3 - p2);
     PROF_ADD(5, p4 - p3);
     PROF_ADD(6, nranges);
-    const uint32_t ndisp = __popc(__ballot_sync(kFull, todo != 0));
+    const uint32_t ndisp = gsum<NW>(todo != 0 ? 1u : 0u, red, par);
     PROF_ADD(7, ndisp);
 #endif
   }
 
-  const uint32_t vc = __reduce_add_sync(kFull, W.vcount);
-  const uint32_t dc = __reduce_add_sync(kFull, W.dcount);
+  const uint32_t vc = gsum<NW>(W.vcount, red, par);
+  const uint32_t dc = gsum<NW>(W.dcount, red, par);
   if (vc + dc != n) return false;  // cycle: the general path reports it exactly
-  const uint32_t T = __reduce_max_sync(kFull, W.tmax);
-  for (uint32_t d = lane; d < D; d += 32) {
+  const uint32_t T = gmax<NW>(W.tmax, red, par);
+  for (uint32_t d = tid; d < D; d += NT) {
     S.busy[c.dev_off + d] = dv[d].busy;
     S.dhead[c.dev_off + d] = W.devoff[d] + dv[d].head;
   }
-  if (lane == 0) {
+  if (tid == 0) {
     O.status[cid] = kOk;
     O.err[cid] = 0;
     O.makespan[cid] = T;
@@ -429,18 +494,18 @@ __device__ bool replay_fast(const Cand& c, int cid, const uint4* rec, const uint
   return true;
 }
 
-#ifndef DPRO_MINB
-#define DPRO_MINB 8
-#endif
-template <int KD>
-__global__ void __launch_bounds__(32, DPRO_MINB) replay_fast_kernel(
+// One CTA of NW warps per candidate, persistent over the batch.
+template <int NW, int KD>
+__global__ void __launch_bounds__(32 * NW) replay_fast_kernel(
     const Cand* __restrict__ cands, int n_cands, Scratch S, Outs O, PackOut P,
     FastCfg F, int want_schedule, unsigned* work, unsigned* fallbacks) {
   extern __shared__ __align__(16) unsigned char fsm[];
+  __shared__ int s_cid;
   for (;;) {
-    int cid = 0;
-    if (threadIdx.x == 0) cid = static_cast<int>(atomicAdd(work, 1u));
-    cid = __shfl_sync(kFull, cid, 0);
+    if (threadIdx.x == 0) s_cid = static_cast<int>(atomicAdd(work, 1u));
+    __syncthreads();
+    const int cid = s_cid;
+    __syncthreads();
     if (cid >= n_cands) break;
     const Cand c = cands[cid];
     const PackInfo info = P.info[cid];
@@ -453,17 +518,19 @@ __global__ void __launch_bounds__(32, DPRO_MINB) replay_fast_kernel(
       continue;
     }
     bool done = false;
-    if (info.not_fast == 0 && c.d <= F.dcap && c.d <= 32u * KD && info.n_cnt <= F.ccap)
-      done = replay_fast<KD>(c, cid, P.rec + P.r_off[cid], P.erec + P.e_off[cid],
-                             P.cnt0 + P.c_off[cid], P.srcs + c.op_off, info, fsm, F, S, O,
-                             want_schedule != 0);
-    __syncwarp();
-    if (!done) {
+    if (info.not_fast == 0 && c.d <= F.dcap && c.d <= 32u * NW * KD && info.n_cnt <= F.ccap)
+      done = replay_fast<NW, KD>(c, cid, P.rec + P.r_off[cid], P.erec + P.e_off[cid],
+                                 P.cnt0 + P.c_off[cid], P.srcs + c.op_off, info, fsm, F, S,
+                                 O, want_schedule != 0);
+    __syncthreads();
+    if (!done) {  // the general kernel is warp-level: warp 0 runs it
       if (threadIdx.x == 0) atomicAdd(fallbacks, 1u);
-      volatile uint32_t* vtop = reinterpret_cast<volatile uint32_t*>(fsm);
-      replay_candidate(c, cid, S.dstate + c.dev_off, vtop, S, O, want_schedule != 0);
+      if (threadIdx.x < 32) {
+        volatile uint32_t* vtop = reinterpret_cast<volatile uint32_t*>(fsm);
+        replay_candidate(c, cid, S.dstate + c.dev_off, vtop, S, O, want_schedule != 0);
+      }
     }
-    __syncwarp();
+    __syncthreads();
   }
 }
 

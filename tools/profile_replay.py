@@ -25,6 +25,10 @@ def main():
     w = workload(a.config)
     graphs = layered_graphs(w.model, w.cluster, w.candidate_partitions(a.batch), threads=16)
     eng = Engine(0)
+    import os
+    for key in ("warps", "ring", "fast"):
+        if os.environ.get("DPRO_" + key.upper()):
+            eng.set_option(key, int(os.environ["DPRO_" + key.upper()]))
     b = eng.batch([g.csr for g in graphs])
     for _ in range(a.iters):
         t = time.perf_counter()
