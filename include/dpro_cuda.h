@@ -192,6 +192,16 @@ typedef struct dpro_layered_model {
 dpro_graph* dpro_graph_layered(const dpro_layered_model* model,
                                const dpro_cluster_desc* cluster,
                                const int32_t* part_k, int32_t* status);
+/* Tensor-fusion + partition candidate: n_groups synchronization units; unit
+ * q fuses layers members[group_off[q] .. group_off[q+1]) in that order
+ * (apply_tensor_fusion, optimize.cpp:366-455: unit "g3+g4" feeds every
+ * member's UPDATE and waits for every member's BW) and is partitioned
+ * group_k[q] ways (NULL: 1). The groups must partition the layers. */
+dpro_graph* dpro_graph_layered_groups(const dpro_layered_model* model,
+                                      const dpro_cluster_desc* cluster,
+                                      int32_t n_groups, const int32_t* group_off,
+                                      const int32_t* members,
+                                      const int32_t* group_k, int32_t* status);
 /* n graphs with part_k[n*layers], built on `threads` host threads. */
 int dpro_graph_layered_batch(const dpro_layered_model* model,
                              const dpro_cluster_desc* cluster,

@@ -277,18 +277,42 @@ dpro_graph* finalize(Gen& g) {
   return out;
 }
 
-dpro_graph* build_layered(const dpro_layered_model& m, const Cluster& c,
-                          const int32_t* part_k) {
+// Synchronization units of a layered candidate: groups of layer tensors
+// fused in the given member order (apply_tensor_fusion, optimize.cpp:366-455
+// -- fusing t1 then t2 names the unit "t1+t2", its IN is fed by every
+// member's producer and its OUT feeds every member's consumer), each
+// partitioned k ways (apply_tensor_partition, optimize.cpp:459-492).
+struct Groups {
+  std::vector<std::vector<int>> members;
+  std::vector<int> k;
+};
+
+dpro_graph* build_layered(const dpro_layered_model& m, const Cluster& c, const Groups& G) {
   Gen g;
   const int L = m.layers;
   if (L < 1) throw std::runtime_error("synthetic model needs at least one layer");
   const int N = static_cast<int>(c.nodes.size());
+  const int NG = static_cast<int>(G.members.size());
+  std::vector<int> group_of(L, -1);
+  std::vector<std::string> gname(NG);
+  for (int q = 0; q < NG; ++q) {
+    if (G.members[q].empty()) throw std::runtime_error("empty tensor group");
+    for (size_t x = 0; x < G.members[q].size(); ++x) {
+      const int i = G.members[q][x];
+      if (i < 0 || i >= L || group_of[i] >= 0)
+        throw std::runtime_error("tensor groups must partition the layers");
+      group_of[i] = q;
+      gname[q] += (x ? "+g" : "g") + std::to_string(i);
+    }
+  }
+  for (int i = 0; i < L; ++i)
+    if (group_of[i] < 0) throw std::runtime_error("tensor groups must cover every layer");
   std::vector<int> workers;
   for (int i = 0; i < N; ++i)
     if (c.role[i] == 0) workers.push_back(i);
-  // per tensor layer i: IN/OUT creation index per node
-  std::vector<std::vector<uint32_t>> in_op(L, std::vector<uint32_t>(N, UINT32_MAX));
-  std::vector<std::vector<uint32_t>> out_op(L, std::vector<uint32_t>(N, UINT32_MAX));
+  // per group: IN/OUT creation index per node
+  std::vector<std::vector<uint32_t>> in_op(NG, std::vector<uint32_t>(N, UINT32_MAX));
+  std::vector<std::vector<uint32_t>> out_op(NG, std::vector<uint32_t>(N, UINT32_MAX));
   for (int w : workers) {
     const std::string& node = c.nodes[w];
     const uint32_t dv = g.device(0, node, "");
@@ -298,35 +322,56 @@ dpro_graph* build_layered(const dpro_layered_model& m, const Cluster& c,
       fw[i] = g.add(node + "->FW.l" + li, kFw, dv, m.fw_dur[i]);
       bw[i] = g.add(node + "->BW.l" + li, kBw, dv, m.bw_dur[i]);
       up[i] = g.add(node + "->UPDATE.l" + li, kUpdate, dv, m.update_dur);
-      in_op[i][w] = g.add(node + "->IN.g" + li, kVin, dv, 0);
-      out_op[i][w] = g.add(node + "->OUT.g" + li, kVout, dv, 0);
+    }
+    for (int q = 0; q < NG; ++q) {
+      in_op[q][w] = g.add(node + "->IN." + gname[q], kVin, dv, 0);
+      out_op[q][w] = g.add(node + "->OUT." + gname[q], kVout, dv, 0);
     }
     // synth.cpp:200-212 deps, resolved by build_local_dfg (ingest.cpp:243-265)
     for (int i = 0; i < L; ++i) {
       if (i > 0) g.edge(fw[i - 1], fw[i]);
       if (i + 1 < L) g.edge(bw[i + 1], bw[i]);
       g.edge(fw[i], bw[i]);
-      g.edge(bw[i], in_op[i][w]);   // producer feeds IN (ingest.cpp:242)
-      g.edge(out_op[i][w], up[i]);  // OUT(g_i) -> UPDATE.l_i
+      g.edge(bw[i], in_op[group_of[i]][w]);   // producer feeds IN (ingest.cpp:242)
+      g.edge(out_op[group_of[i]][w], up[i]);  // OUT(g_i) -> UPDATE.l_i
     }
   }
-  for (int i = 0; i < L; ++i) {
-    const std::string t = "g" + std::to_string(i);
-    const int64_t bytes = m.tensor_bytes[i];
-    const int k = part_k ? part_k[i] : 1;
+  for (int q = 0; q < NG; ++q) {
+    int64_t bytes = 0;
+    for (int i : G.members[q]) bytes += m.tensor_bytes[i];
+    const int k = G.k[q];
     if (k < 1)
       throw std::runtime_error("partition count must be >= 1, got " + std::to_string(k));
     if (k > bytes)
-      throw std::runtime_error("cannot split " + std::to_string(bytes) +
-                               " bytes of " + t + " into " + std::to_string(k) +
-                               " partitions");
+      throw std::runtime_error("cannot split " + std::to_string(bytes) + " bytes of " +
+                               gname[q] + " into " + std::to_string(k) + " partitions");
     const int64_t base = bytes / k, rem = bytes % k;
     for (int p = 0; p < k; ++p) {
-      const std::string unit = k == 1 ? t : t + "#p" + std::to_string(p);
-      expand_unit(g, c, unit, base + (p < rem ? 1 : 0), &in_op[i], &out_op[i]);
+      const std::string unit = k == 1 ? gname[q] : gname[q] + "#p" + std::to_string(p);
+      expand_unit(g, c, unit, base + (p < rem ? 1 : 0), &in_op[q], &out_op[q]);
     }
   }
   return finalize(g);
+}
+
+dpro_graph* build_layered(const dpro_layered_model& m, const Cluster& c,
+                          const int32_t* part_k) {
+  Groups G;
+  for (int i = 0; i < m.layers; ++i) {
+    G.members.push_back({i});
+    G.k.push_back(part_k ? part_k[i] : 1);
+  }
+  return build_layered(m, c, G);
+}
+
+Groups make_groups(int32_t n_groups, const int32_t* group_off, const int32_t* members,
+                   const int32_t* group_k) {
+  Groups G;
+  for (int q = 0; q < n_groups; ++q) {
+    G.members.emplace_back(members + group_off[q], members + group_off[q + 1]);
+    G.k.push_back(group_k ? group_k[q] : 1);
+  }
+  return G;
 }
 
 dpro_graph* build_tsync(const Cluster& c, int64_t bytes, int k) {
@@ -401,6 +446,18 @@ int dpro_graph_layered_batch(const dpro_layered_model* model,
       return st[i];
     }
   return DPRO_OK;
+}
+
+dpro_graph* dpro_graph_layered_groups(const dpro_layered_model* model,
+                                      const dpro_cluster_desc* cluster, int32_t n_groups,
+                                      const int32_t* group_off, const int32_t* members,
+                                      const int32_t* group_k, int32_t* status) {
+  return guarded(
+      [&] {
+        return build_layered(*model, Cluster(*cluster),
+                             make_groups(n_groups, group_off, members, group_k));
+      },
+      status);
 }
 
 dpro_graph* dpro_graph_tsync(const dpro_cluster_desc* cluster, int64_t bytes,

@@ -104,7 +104,7 @@ struct dpro_ctx {
   HostPinned staging;
   int fast = 1;       // option "fast"
   uint32_t ring = 4;  // option "ring"
-  int warps = 1;      // option "warps": warps (1, 2, 4) per candidate
+  int warps = 4;      // option "warps": warps (1, 2, 4) per candidate
   dpro_batch* spare = nullptr;  // recycled arenas for repeated small calls
 };
 

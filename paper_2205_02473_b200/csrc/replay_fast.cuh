@@ -58,7 +58,10 @@ constexpr int kMlp = DPRO_MLP;  // record loads in flight per lane in expand()
 
 // misc words: [0] range count, [1] overflow, [4, 4+NT) per-thread dirty
 // masks, then 2*NW words of double-buffered reduction scratch.
-__host__ __device__ constexpr size_t fast_misc_words(int nw) { return 4 + 32 * nw + 2 * nw; }
+// (rounded up to 4 words: the u8 counters after it are copied as uint4)
+__host__ __device__ constexpr size_t fast_misc_words(int nw) {
+  return (4 + 32 * nw + 2 * nw + 3) & ~size_t(3);
+}
 
 // Group-wide collectives for one candidate replayed by NW warps (one CTA).
 template <int NW>

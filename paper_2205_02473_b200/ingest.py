@@ -249,6 +249,23 @@ def layered_graph(model: LayeredModel, cluster: ClusterSpec,
     return NativeGraph(h)
 
 
+def layered_graph_groups(model: LayeredModel, cluster: ClusterSpec,
+                         groups: Sequence[Sequence[int]],
+                         ks: Sequence[int] | None = None) -> NativeGraph:
+    """Tensor-fusion + partition candidate: groups[q] lists the layers fused
+    into unit q in fusion order ("g3+g4"), ks[q] its partition count."""
+    m = model.struct()
+    holder = N.ClusterDescHolder(cluster)
+    off = np.zeros(len(groups) + 1, np.int32)
+    off[1:] = np.cumsum([len(g) for g in groups])
+    mem = np.ascontiguousarray([i for g in groups for i in g], np.int32)
+    kk = None if ks is None else np.ascontiguousarray(ks, np.int32)
+    st = C.c_int32(0)
+    h = N.lib.dpro_graph_layered_groups(C.byref(m), C.byref(holder.desc), len(groups),
+                                        N.ptr(off), N.ptr(mem), N.ptr(kk), C.byref(st))
+    return NativeGraph(h)
+
+
 def layered_graphs(model: LayeredModel, cluster: ClusterSpec, part_k: np.ndarray,
                    threads: int = 8) -> list[NativeGraph]:
     """Candidate batch: one graph per row of part_k [n, layers]."""

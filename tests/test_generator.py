@@ -92,3 +92,23 @@ def test_generator_errors():
     c = synth_cluster("ring", 3, 0, 1.0, 0.0)
     with pytest.raises(Exception, match="cannot split 10 bytes"):
         layered_graph(LayeredModel([1], [1], [10]), c, [11])
+
+
+@pytest.mark.parametrize("scheme,W,S", [("ring", 4, 0), ("ps", 5, 2), ("ring", 11, 0)])
+def test_generator_tensor_fusion_matches_reference(ref, scheme, W, S):
+    """apply_tensor_fusion chains (+ a partition of the fused unit) through the
+    reference vs the generator's fused groups."""
+    from paper_2205_02473_b200.ingest import layered_graph_groups
+    L = 6
+    rng = np.random.default_rng(W)
+    spec = {"layers": L, "fw_dur_us": rng.integers(1, 99, L).tolist(),
+            "bw_dur_us": rng.integers(1, 99, L).tolist(),
+            "tensor_bytes": rng.integers(20, 90000, L).tolist(), "update_dur_us": 5,
+            "scheme": scheme, "workers": W, "ps_count": S, "bandwidth_bytes_per_us": 33.0,
+            "latency_us": 2.5}
+    rg = ref.RefGraph.synth(spec)
+    rg = rg.tensor_fusion("g1", "g2").tensor_fusion("g1+g2", "g3")
+    rg = rg.tensor_fusion("g5", "g0").partition("g5+g0", 3).partition("g4", 2)
+    groups = [[1, 2, 3], [5, 0], [4]]
+    ng = layered_graph_groups(_model(spec), _cluster(spec), groups, [1, 3, 2])
+    _same_csr(rg.export(), ng, rg)

@@ -45,15 +45,18 @@ def _batch_check(engine, graphs, expects, label):
                     assert (busy[d] / T if T > 0 else 0.0) == pytest.approx(u, abs=0), name
 
 
-@pytest.fixture(params=["fast", "general", "fast_ring2"])
+@pytest.fixture(params=["fast", "fast_w1", "fast_w2", "general", "fast_ring2"])
 def mode_engine(engine, request):
-    """Both kernels: the on-chip fast path (with exact fallback) and the
-    general global-memory kernel; ring=2 forces frequent fast-path bail-outs."""
+    """Both kernels: the on-chip fast path (1, 2 or 4 warps per candidate,
+    with exact fallback) and the general global-memory kernel; ring=2 forces
+    frequent fast-path bail-outs."""
     engine.set_option("fast", 0 if request.param == "general" else 1)
     engine.set_option("ring", 2 if request.param == "fast_ring2" else 4)
+    engine.set_option("warps", {"fast_w1": 1, "fast_w2": 2}.get(request.param, 4))
     yield engine
     engine.set_option("fast", 1)
     engine.set_option("ring", 4)
+    engine.set_option("warps", 4)
 
 
 def test_reference_golden_vectors_bit_exact(mode_engine):
