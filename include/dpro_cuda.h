@@ -92,7 +92,7 @@ void dpro_cuda_destroy(dpro_ctx* ctx);
 int dpro_cuda_set_stream(dpro_ctx* ctx, void* stream);
 /* Engine options: "fast" (1: on-chip fast path with exact fallback, 0: the
  * general kernel only), "ring" (fast-path queue capacity per device, power
- * of two), "warps" (1, 2 or 4 warps = one CTA cooperating on a candidate in
+ * of two), "warps" (1, 2, 4 or 8 warps = one CTA cooperating on a candidate in
  * the fast path). Returns DPRO_EINVAL for unknown keys or values. */
 int dpro_cuda_set_option(dpro_ctx* ctx, const char* key, int64_t value);
 const char* dpro_cuda_last_error(dpro_ctx* ctx);

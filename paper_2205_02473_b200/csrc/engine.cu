@@ -508,7 +508,7 @@ int dpro_cuda_set_option(dpro_ctx* ctx, const char* key, int64_t value) {
     ctx->fast = static_cast<int>(value);
     return DPRO_OK;
   }
-  if (k == "warps" && (value == 1 || value == 2 || value == 4)) {
+  if (k == "warps" && (value == 1 || value == 2 || value == 4 || value == 8)) {
     ctx->warps = static_cast<int>(value);
     return DPRO_OK;
   }
@@ -606,6 +606,7 @@ int launch_fast(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
   switch (ctx->warps) {
     case 1: return launch_fast_nw<1>(ctx, b, want_schedule);
     case 2: return launch_fast_nw<2>(ctx, b, want_schedule);
+    case 8: return launch_fast_nw<8>(ctx, b, want_schedule);
     default: return launch_fast_nw<4>(ctx, b, want_schedule);
   }
 }

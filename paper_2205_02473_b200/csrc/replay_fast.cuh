@@ -323,7 +323,7 @@ struct FastWarp {
 // Scratch::busy of device 0 region? no -- to a global debug array.
 __device__ unsigned long long g_prof[16];
 #define PROF_T(v) const long long v = clock64()
-#define PROF_ADD(i, x) if (threadIdx.x == 0) atomicAdd(&g_prof[i], (unsigned long long)(x))
+#define PROF_ADD(i_, v_) if (threadIdx.x == 0) atomicAdd(&g_prof[i_], (unsigned long long)(v_))
 #else
 #define PROF_T(v)
 #define PROF_ADD(i, x)

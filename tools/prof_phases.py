@@ -17,6 +17,7 @@ nb = int(os.environ.get("NB", "1024"))
 w = workload(cfg)
 graphs = layered_graphs(w.model, w.cluster, w.candidate_partitions(nb), threads=16)
 eng = Engine(0)
+eng.set_option("warps", int(os.environ.get("DPRO_WARPS", "4")))
 b = eng.batch([g.csr for g in graphs])
 fn = N.lib.dpro_debug_prof
 fn.argtypes = [C.c_void_p]
