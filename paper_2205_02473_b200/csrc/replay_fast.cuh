@@ -56,11 +56,12 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
 #endif
 constexpr int kMlp = DPRO_MLP;  // record loads in flight per lane in expand()
 
-// misc words: [0] range count, [1] overflow, [4, 4+NT) per-thread dirty
-// masks, then 2*NW words of double-buffered reduction scratch.
+// misc words: [0],[2] range counts (double-buffered by round parity),
+// [1] overflow, [4, 4+NT) per-thread dirty masks, then 4*NW words of
+// double-buffered reduction scratch.
 // (rounded up to 4 words: the u8 counters after it are copied as uint4)
 __host__ __device__ constexpr size_t fast_misc_words(int nw) {
-  return (4 + 32 * nw + 2 * nw + 3) & ~size_t(3);
+  return (4 + 32 * nw + 4 * nw + 3) & ~size_t(3);
 }
 
 // Group-wide collectives for one candidate replayed by NW warps (one CTA).
@@ -89,6 +90,36 @@ __device__ __forceinline__ uint32_t gmin(uint32_t v, volatile uint32_t* red, uin
   for (int w = 1; w < NW; ++w) m = min(m, r[w]);
   return m;
 }
+// Round head: (any thread has zero-duration completions pending, min next
+// event time) in ONE barrier. red holds 2 x NW words per parity buffer.
+template <int NW>
+__device__ __forceinline__ void round_head(bool zero, uint32_t lmin, volatile uint32_t* red,
+                                           uint32_t& par, bool& any_zero, uint32_t& tmin) {
+  const bool wz = __any_sync(kFull, zero);
+  const uint32_t wm = __reduce_min_sync(kFull, lmin);
+  if (NW == 1) {
+    any_zero = wz;
+    tmin = wm;
+    return;
+  }
+  volatile uint32_t* r = red + (par & 1u) * 2 * NW;
+  ++par;
+  if ((threadIdx.x & 31) == 0) {
+    r[threadIdx.x >> 5] = wz ? 1u : 0u;
+    r[NW + (threadIdx.x >> 5)] = wm;
+  }
+  __syncthreads();
+  bool z = false;
+  uint32_t m = kT32Inf;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) {
+    z |= r[w] != 0u;
+    m = min(m, r[NW + w]);
+  }
+  any_zero = z;
+  tmin = m;
+}
+
 template <int NW>
 __device__ __forceinline__ uint32_t gsum(uint32_t v, volatile uint32_t* red, uint32_t& par) {
   v = __reduce_add_sync(kFull, v);
@@ -139,8 +170,10 @@ struct FastWarp {
 
   __device__ __forceinline__ uint4* ring(uint32_t d) { return q + (size_t)d * qc; }
 
+  volatile uint32_t* rlc = nullptr;  // this round's range counter
+
   __device__ __forceinline__ void push_range(uint32_t sb, uint32_t n) {
-    const uint32_t p = atomicAdd(const_cast<uint32_t*>(&misc[0]), 1u);
+    const uint32_t p = atomicAdd(const_cast<uint32_t*>(rlc), 1u);
     if (p < rlcap)
       rl[p] = make_uint2(sb, n);
     else
@@ -201,11 +234,13 @@ struct FastWarp {
   // Expands every range pushed this round (and the virtual cascades they
   // trigger) with all 32 lanes: the round's out-edge records are loaded and
   // applied in parallel instead of one lane walking each list.
+  // The caller has made this round's ranges visible (barrier). Each pass
+  // expands ranges [lo, hi) and ends with a barrier; virtual cascades
+  // pushed during a pass are expanded by the next one.
   __device__ __forceinline__ bool expand(uint32_t t) {
     uint32_t lo = 0;
     for (;;) {
-      gsync<NW>();
-      const uint32_t hi = misc[0];
+      const uint32_t hi = *rlc;
       if (misc[1] || hi > rlcap) return false;
       if (lo == hi) return true;
       for (uint32_t g = lo; g < hi; g += 32) {
@@ -223,8 +258,8 @@ struct FastWarp {
         // lane r holds range r's first item index; items map to ranges by a
         // 5-step shuffle binary search (no shared-memory walk)
         const uint32_t excl = (uint32_t)lane < nr ? incl - mine.y : 0xFFFFFFFFu;
-        // memory-level parallelism: each lane issues up to kMlp record loads
-        // back to back, then applies them (edge() has atomics, so the
+        // memory-level parallelism: each thread issues up to kMlp record
+        // loads back to back, then applies them (edge() has atomics, so the
         // compiler would otherwise serialize load -> apply -> next load)
         for (uint32_t base = 0; base < total; base += NT * kMlp) {
           uint4 a[kMlp];
@@ -246,8 +281,8 @@ struct FastWarp {
           for (int b = 0; b < kMlp; ++b)
             if (base + tid + NT * b < total) edge(a[b], t);
         }
-        gsync<NW>();
       }
+      gsync<NW>();
       lo = hi;
     }
   }
@@ -344,7 +379,7 @@ __device__ bool replay_fast(const Cand& c, int cid, const uint4* rec, const uint
   uint2* rl = reinterpret_cast<uint2*>(q + (size_t)F.dcap * F.qc);
   volatile uint32_t* misc = reinterpret_cast<volatile uint32_t*>(rl + F.rl);
   uint32_t* cw = const_cast<uint32_t*>(misc) + fast_misc_words(NW);
-  volatile uint32_t* red = misc + 4 + NT;
+  volatile uint32_t* red = misc + 4 + NT;  // 4 * NW words
   uint32_t par = 0;
   const unsigned long long oo = c.op_off;
 
@@ -369,6 +404,7 @@ __device__ bool replay_fast(const Cand& c, int cid, const uint4* rec, const uint
   }
   if (tid < 4) misc[tid] = 0;
   misc[4 + tid] = 0;
+  W.rlc = misc;  // sources never push ranges (no virtual sources)
   gsync<NW>();
   // ---- sources (replay.cpp:92-94). No virtual sources reach the fast path
   // (pack flags them), so there are no cascades and no init quirk. ----
@@ -407,21 +443,25 @@ __device__ bool replay_fast(const Cand& c, int cid, const uint4* rec, const uint
   }
   misc[4 + tid] = 0;  // all devices were just visited
   uint32_t t = 0;
+  uint32_t rpar = 0;
   for (;;) {
     PROF_T(p0);
-    const bool zero_round = gany<NW>(zmask != 0);
+    uint32_t lmin = kT32Inf;
+#pragma unroll
+    for (int j = 0; j < KD; ++j) lmin = min(lmin, iend[j]);
+    bool zero_round;
+    uint32_t tn;
+    round_head<NW>(zmask != 0, lmin, red, par, zero_round, tn);
     uint32_t freed = 0;
     if (!zero_round) {
-      uint32_t lmin = kT32Inf;
-#pragma unroll
-      for (int j = 0; j < KD; ++j) lmin = min(lmin, iend[j]);
-      const uint32_t tn = gmin<NW>(lmin, red, par);
       if (tn == kT32Inf) break;
       t = tn;
     }
     PROF_T(p1);
-    if (tid == 0) misc[0] = 0;
-    gsync<NW>();
+    // range counters alternate by round: this round's was zeroed last round
+    W.rlc = misc + 2 * (rpar & 1u);
+    if (tid == 0) misc[2 * ((rpar + 1) & 1u)] = 0;
+    ++rpar;
     if (zero_round) {
       // zero-duration ops dispatched last round complete now (same t)
       uint32_t zm = zmask;
@@ -449,12 +489,12 @@ __device__ bool replay_fast(const Cand& c, int cid, const uint4* rec, const uint
         }
       }
     }
+    gsync<NW>();
     PROF_T(p2);
 #ifdef DPRO_PROFILE
-    const uint32_t nranges = misc[0];
+    const uint32_t nranges = *W.rlc;
 #endif
     if (!W.expand(t)) return false;
-    gsync<NW>();
     PROF_T(p3);
     const uint32_t todo = freed | misc[4 + tid];
     misc[4 + tid] = 0;
