@@ -81,7 +81,7 @@ template <int NW>
 __device__ __forceinline__ uint32_t gmin(uint32_t v, volatile uint32_t* red, uint32_t& par) {
   v = __reduce_min_sync(kFull, v);
   if (NW == 1) return v;
-  volatile uint32_t* r = red + (par & 1u) * NW;
+  volatile uint32_t* r = red + (par & 1u) * 2 * NW;  // same buffers as round_head
   ++par;
   if ((threadIdx.x & 31) == 0) r[threadIdx.x >> 5] = v;
   __syncthreads();
@@ -124,7 +124,7 @@ template <int NW>
 __device__ __forceinline__ uint32_t gsum(uint32_t v, volatile uint32_t* red, uint32_t& par) {
   v = __reduce_add_sync(kFull, v);
   if (NW == 1) return v;
-  volatile uint32_t* r = red + (par & 1u) * NW;
+  volatile uint32_t* r = red + (par & 1u) * 2 * NW;  // same buffers as round_head
   ++par;
   if ((threadIdx.x & 31) == 0) r[threadIdx.x >> 5] = v;
   __syncthreads();
@@ -137,7 +137,7 @@ template <int NW>
 __device__ __forceinline__ uint32_t gmax(uint32_t v, volatile uint32_t* red, uint32_t& par) {
   v = __reduce_max_sync(kFull, v);
   if (NW == 1) return v;
-  volatile uint32_t* r = red + (par & 1u) * NW;
+  volatile uint32_t* r = red + (par & 1u) * 2 * NW;  // same buffers as round_head
   ++par;
   if ((threadIdx.x & 31) == 0) r[threadIdx.x >> 5] = v;
   __syncthreads();
