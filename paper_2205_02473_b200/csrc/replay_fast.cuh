@@ -52,7 +52,7 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
 }
 
 #ifndef DPRO_MLP
-#define DPRO_MLP 4
+#define DPRO_MLP 1
 #endif
 constexpr int kMlp = DPRO_MLP;  // record loads in flight per lane in expand()
 
@@ -248,11 +248,21 @@ struct FastWarp {
         uint2 mine = make_uint2(0u, 0u);
         if (r < hi) mine = rl[r];
         uint32_t incl = mine.y;
+#ifndef DPRO_SCAN_SKIP
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const uint32_t y = __shfl_up_sync(kFull, incl, o);
           if (lane >= o) incl += y;
         }
+#else
+        if (hi - g > 1) {
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += y;
+          }
+        }
+#endif
         const uint32_t total = __shfl_sync(kFull, incl, 31);
         const uint32_t nr = min(32u, hi - g);
         // lane r holds range r's first item index; items map to ranges by a
@@ -267,8 +277,13 @@ struct FastWarp {
           for (int b = 0; b < kMlp; ++b) {
             const uint32_t qi = base + tid + NT * b;
             int k = 0;
+#ifdef DPRO_SEARCH_STEPS
+#pragma unroll
+            for (int step = DPRO_SEARCH_STEPS; step; step >>= 1) {
+#else
 #pragma unroll
             for (int step = 16; step; step >>= 1) {
+#endif
               const int cand = k + step;
               const uint32_t v = __shfl_sync(kFull, excl, cand & 31);
               if (cand < 32 && v <= qi) k = cand;

@@ -31,5 +31,8 @@ tot = sum(int(buf[i]) for i in range(2, 6))
 for i, nm in enumerate(names):
     v = int(buf[2 + i])
     print(f"  {nm:18s} {v/rounds:8.1f} cycles/round ({100*v/tot:4.1f}%)")
+print(f"  expand passes/round {int(buf[8])/rounds:.2f}, records/round {int(buf[9])/rounds:.1f}, "
+      f"thread0 work {int(buf[10])/rounds:.0f} cyc/round, barrier wait {int(buf[11])/rounds:.0f} cyc/round")
+print(f"  thread0: waiting for record loads {int(buf[12])/rounds:.0f} cyc/round, applying {int(buf[13])/rounds:.0f} cyc/round")
 print(f"  total {tot/rounds:.1f} cycles/round; ranges/round {int(buf[6])/rounds:.2f}; "
       f"dispatching lanes/round {int(buf[7])/rounds:.2f}")
