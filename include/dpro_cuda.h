@@ -130,7 +130,9 @@ int dpro_cuda_batch_timelines(dpro_ctx* ctx, dpro_batch* b, int32_t cand,
                               int64_t* busy);
 /* Counters of the last replay: stats[0] = candidates that took the general
  * (fallback) path, stats[1] = fast-path shared memory bytes per candidate,
- * stats[2] = fast-path candidates resident per SM. */
+ * stats[2] = fast-path candidates resident per SM, stats[3] = ring capacity
+ * per device, stats[4] = candidates re-run with deep rings (second pass).
+ * stats must hold 5 entries. */
 int dpro_cuda_batch_stats(dpro_ctx* ctx, dpro_batch* b, int64_t* stats);
 /* scheduled[i] = 1 for ops the replay scheduled (host buffer [n_ops]); the
  * ids with 0 form CycleError::cycle (replay.cpp:108-117). */

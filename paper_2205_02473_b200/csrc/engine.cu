@@ -100,6 +100,7 @@ struct dpro_ctx {
   cudaStream_t stream = nullptr;
   int sm_count = 148;
   size_t smem_optin = 0;
+  int smem_per_sm = 228 * 1024;
   std::string err;
   HostPinned staging;
   int fast = 1;       // option "fast"
@@ -436,6 +437,7 @@ dpro_ctx* dpro_cuda_create(int device) {
   int optin = 0;
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   ctx->smem_optin = static_cast<size_t>(optin);
+  cudaDeviceGetAttribute(&ctx->smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
   cudaFuncSetAttribute(dpro_k::replay_batch_kernel,
                        cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
   return ctx;
@@ -544,6 +546,8 @@ int launch_general(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
 
 // Fast-path shared memory per candidate (one warp per block):
 // devices x (DevF + ring) + virtual worklist + misc words + u8 counters.
+size_t fast_bytes(uint32_t dcap, uint32_t qc, uint32_t rl, uint32_t ccap, int nw);
+
 size_t fast_bytes(uint32_t dcap, uint32_t qc, uint32_t rl, uint32_t ccap, int nw) {
   return size_t(dcap) * (sizeof(dpro_k::DevF) + 16 * qc) + 8 * size_t(rl) +
          4 * dpro_k::fast_misc_words(nw) + ccap;
@@ -551,20 +555,29 @@ size_t fast_bytes(uint32_t dcap, uint32_t qc, uint32_t rl, uint32_t ccap, int nw
 
 template <int NW, int KD>
 int launch_fast_kd(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule, FastCfg F) {
+  auto kern = dpro_k::replay_fast_kernel<NW, KD>;
   const size_t smem = F.warp_bytes;
-  CU(cudaFuncSetAttribute(dpro_k::replay_fast_kernel<NW, KD>,
-                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)ctx->smem_optin));
   int blocks_per_sm = 0;
-  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &blocks_per_sm, dpro_k::replay_fast_kernel<NW, KD>, 32 * NW, smem));
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, 32 * NW, smem));
   blocks_per_sm = std::max(blocks_per_sm, 1);
   b->blocks_per_sm_fast = blocks_per_sm;
   const int grid = std::max(1, std::min(b->n, ctx->sm_count * blocks_per_sm));
-  CU(cudaMemsetAsync(b->work.p, 0, 8, ctx->stream));
+  CU(cudaMemsetAsync(b->work.p, 0, 16, ctx->stream));
   b->F = F;
-  dpro_k::replay_fast_kernel<NW, KD><<<grid, 32 * NW, smem, ctx->stream>>>(
-      b->desc.as<Cand>(), b->n, b->S, b->O, b->P, F, want_schedule ? 1 : 0,
-      b->work.as<unsigned>(), b->work.as<unsigned>() + 1);
+  kern<<<grid, 32 * NW, smem, ctx->stream>>>(b->desc.as<Cand>(), b->n, b->S, b->O, b->P, F,
+                                             want_schedule ? 1 : 0, b->work.as<unsigned>(), 0);
+  CU(cudaGetLastError());
+  // pass 1: candidates whose device queues outgrew the ring, one CTA per SM
+  // with the deepest rings the shared memory holds
+  FastCfg D = F;
+  const size_t limit = ctx->smem_optin - 64;
+  while (D.qc < 4096 && fast_bytes(D.dcap, D.qc * 2, D.rl, D.ccap, NW) <= limit) D.qc *= 2;
+  D.warp_bytes = static_cast<uint32_t>(fast_bytes(D.dcap, D.qc, D.rl, D.ccap, NW));
+  kern<<<ctx->sm_count, 32 * NW, D.warp_bytes, ctx->stream>>>(
+      b->desc.as<Cand>(), b->n, b->S, b->O, b->P, D, want_schedule ? 1 : 0,
+      b->work.as<unsigned>(), 1);
   CU(cudaGetLastError());
   return DPRO_OK;
 }
@@ -587,6 +600,13 @@ int launch_fast_nw(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
   while (fast_bytes(F.dcap, F.qc, F.rl, F.ccap, NW) > limit && F.ccap > 16)
     F.ccap = std::max<uint32_t>(16, (F.ccap / 2 + 15) & ~15u);
   while (fast_bytes(F.dcap, F.qc, F.rl, F.ccap, NW) > limit && F.dcap > 1) F.dcap /= 2;
+  // Deeper rings while the candidate still fits the residency target (the
+  // whole batch resident: ~8 candidates per SM) -- deep device queues
+  // (e.g. ring all-reduce links) otherwise fall back to the general kernel.
+  const size_t target = std::max<size_t>(fast_bytes(F.dcap, F.qc, F.rl, F.ccap, NW),
+                                         size_t(ctx->smem_per_sm) / 8 - 1024);
+  while (F.qc < 64 && fast_bytes(F.dcap, F.qc * 2, F.rl, F.ccap, NW) <= std::min(target, limit))
+    F.qc *= 2;
   F.warp_bytes = static_cast<uint32_t>(fast_bytes(F.dcap, F.qc, F.rl, F.ccap, NW));
   switch (kd) {
     case 1: return launch_fast_kd<NW, 1>(ctx, b, want_schedule, F);
@@ -639,12 +659,14 @@ extern "C" int dpro_debug_prof(unsigned long long* out) {
 int dpro_cuda_batch_stats(dpro_ctx* ctx, dpro_batch* b, int64_t* stats) {
   if (!ctx || !b || !stats) return DPRO_EINVAL;
   CU(cudaSetDevice(ctx->device));
-  unsigned w[2] = {0, 0};
-  CU(cudaMemcpyAsync(w, b->work.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  unsigned w[4] = {0, 0, 0, 0};
+  CU(cudaMemcpyAsync(w, b->work.p, 16, cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
   stats[0] = ctx->fast ? w[1] : b->n;
   stats[1] = b->F.warp_bytes;
   stats[2] = b->blocks_per_sm_fast;
+  stats[3] = b->F.qc;
+  stats[4] = ctx->fast ? w[3] : 0;
   return DPRO_OK;
 }
 

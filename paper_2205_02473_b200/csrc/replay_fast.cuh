@@ -30,6 +30,9 @@
 namespace dpro_k {
 
 constexpr uint32_t kT32Inf = 0xFFFFFFFFu;
+// replay_fast outcomes / bail-out causes
+constexpr uint32_t kDone = 0, kBailRing = 1, kBailOther = 2;
+constexpr int kRetry = 9;  // status of a candidate queued for the deep-ring pass
 
 struct __align__(16) DevF {
   uint32_t head, tail, tsort, segbeg;
@@ -177,7 +180,7 @@ struct FastWarp {
     if (p < rlcap)
       rl[p] = make_uint2(sb, n);
     else
-      misc[1] = 1u;
+      atomicOr(const_cast<uint32_t*>(&misc[1]), kBailOther);
   }
 
   // ready(s, t) of replay.cpp:60-72 for s reached through a packed record.
@@ -202,7 +205,7 @@ struct FastWarp {
     const uint32_t zh = *reinterpret_cast<volatile uint32_t*>(&sd.zhi);
     const uint32_t low = zl < zh ? zl : *reinterpret_cast<volatile uint32_t*>(&sd.head);
     if (pos - low >= qc) {
-      misc[1] = 1u;
+      atomicOr(const_cast<uint32_t*>(&misc[1]), kBailRing);
     } else {
       ring(d)[pos & (qc - 1)] = make_uint4(s, a.y, a.w, se);  // {op, dur, sb, se}
       atomicOr(const_cast<uint32_t*>(&misc[4 + (d % NT)]), 1u << (d / NT));
@@ -237,12 +240,14 @@ struct FastWarp {
   // The caller has made this round's ranges visible (barrier). Each pass
   // expands ranges [lo, hi) and ends with a barrier; virtual cascades
   // pushed during a pass are expanded by the next one.
-  __device__ __forceinline__ bool expand(uint32_t t) {
+  // Returns kDone, or the bail-out cause.
+  __device__ __forceinline__ uint32_t expand(uint32_t t) {
     uint32_t lo = 0;
     for (;;) {
       const uint32_t hi = *rlc;
-      if (misc[1] || hi > rlcap) return false;
-      if (lo == hi) return true;
+      if (misc[1]) return misc[1] == kBailRing ? kBailRing : kBailOther;
+      if (hi > rlcap) return kBailOther;
+      if (lo == hi) return kDone;
       for (uint32_t g = lo; g < hi; g += 32) {
         const uint32_t r = g + lane;
         uint2 mine = make_uint2(0u, 0u);
@@ -379,9 +384,10 @@ __device__ unsigned long long g_prof[16];
 #define PROF_ADD(i, x)
 #endif
 
-// Returns false when the candidate must take the general path.
+// Returns kDone, kBailRing (a device queue outgrew its ring: retry with
+// deeper rings) or kBailOther (take the general path).
 template <int NW, int KD>
-__device__ bool replay_fast(const Cand& c, int cid, const uint4* rec, const uint4* erec,
+__device__ uint32_t replay_fast(const Cand& c, int cid, const uint4* rec, const uint4* erec,
                             const uint8_t* cnt0, const uint32_t* srcs, const PackInfo& info,
                             unsigned char* wsm, const FastCfg& F, const Scratch& S,
                             const Outs& O, bool want_schedule) {
@@ -425,7 +431,7 @@ __device__ bool replay_fast(const Cand& c, int cid, const uint4* rec, const uint
   // (pack flags them), so there are no cascades and no init quirk. ----
   for (uint32_t k = tid; k < info.n_src; k += NT) W.ready(__ldg(rec + __ldg(srcs + k)), 0u);
   gsync<NW>();
-  if (gany<NW>(misc[1] != 0)) return false;
+  if (gany<NW>(misc[1] != 0)) return misc[1] == kBailRing ? kBailRing : kBailOther;
   for (uint32_t d = tid; d < D; d += NT) {  // t = 0 arrivals in index order
     DevF& s = dv[d];
     uint4* r = W.ring(d);
@@ -509,7 +515,7 @@ __device__ bool replay_fast(const Cand& c, int cid, const uint4* rec, const uint
 #ifdef DPRO_PROFILE
     const uint32_t nranges = *W.rlc;
 #endif
-    if (!W.expand(t)) return false;
+    if (const uint32_t bail = W.expand(t)) return bail;
     PROF_T(p3);
     const uint32_t todo = freed | misc[4 + tid];
     misc[4 + tid] = 0;
@@ -538,7 +544,7 @@ __device__ bool replay_fast(const Cand& c, int cid, const uint4* rec, const uint
 
   const uint32_t vc = gsum<NW>(W.vcount, red, par);
   const uint32_t dc = gsum<NW>(W.dcount, red, par);
-  if (vc + dc != n) return false;  // cycle: the general path reports it exactly
+  if (vc + dc != n) return kBailOther;  // cycle: the general path reports it exactly
   const uint32_t T = gmax<NW>(W.tmax, red, par);
   for (uint32_t d = tid; d < D; d += NT) {
     S.busy[c.dev_off + d] = dv[d].busy;
@@ -549,22 +555,29 @@ __device__ bool replay_fast(const Cand& c, int cid, const uint4* rec, const uint
     O.err[cid] = 0;
     O.makespan[cid] = T;
   }
-  return true;
+  return kDone;
 }
 
 // One CTA of NW warps per candidate, persistent over the batch.
+// pass 0: every candidate; ring overflows are marked kRetry.
+// pass 1: only kRetry candidates, with rings as deep as shared memory allows
+// (one CTA per SM); anything still failing takes the general path.
+// work: [0] pass-0 counter, [1] general fallbacks, [2] pass-1 counter,
+// [3] deep-ring retries.
 template <int NW, int KD>
 __global__ void __launch_bounds__(32 * NW) replay_fast_kernel(
     const Cand* __restrict__ cands, int n_cands, Scratch S, Outs O, PackOut P,
-    FastCfg F, int want_schedule, unsigned* work, unsigned* fallbacks) {
+    FastCfg F, int want_schedule, unsigned* work, int pass) {
   extern __shared__ __align__(16) unsigned char fsm[];
   __shared__ int s_cid;
+  unsigned* counter = work + (pass ? 2 : 0);
   for (;;) {
-    if (threadIdx.x == 0) s_cid = static_cast<int>(atomicAdd(work, 1u));
+    if (threadIdx.x == 0) s_cid = static_cast<int>(atomicAdd(counter, 1u));
     __syncthreads();
     const int cid = s_cid;
     __syncthreads();
     if (cid >= n_cands) break;
+    if (pass == 1 && O.status[cid] != kRetry) continue;
     const Cand c = cands[cid];
     const PackInfo info = P.info[cid];
     if (info.first_missing != kNone) {  // replay.cpp:39-44
@@ -575,14 +588,19 @@ __global__ void __launch_bounds__(32 * NW) replay_fast_kernel(
       }
       continue;
     }
-    bool done = false;
+    uint32_t rc = kBailOther;
     if (info.not_fast == 0 && c.d <= F.dcap && c.d <= 32u * NW * KD && info.n_cnt <= F.ccap)
-      done = replay_fast<NW, KD>(c, cid, P.rec + P.r_off[cid], P.erec + P.e_off[cid],
-                                 P.cnt0 + P.c_off[cid], P.srcs + c.op_off, info, fsm, F, S,
-                                 O, want_schedule != 0);
+      rc = replay_fast<NW, KD>(c, cid, P.rec + P.r_off[cid], P.erec + P.e_off[cid],
+                               P.cnt0 + P.c_off[cid], P.srcs + c.op_off, info, fsm, F, S, O,
+                               want_schedule != 0);
     __syncthreads();
-    if (!done) {  // the general kernel is warp-level: warp 0 runs it
-      if (threadIdx.x == 0) atomicAdd(fallbacks, 1u);
+    if (rc == kBailRing && pass == 0) {
+      if (threadIdx.x == 0) {
+        O.status[cid] = kRetry;
+        atomicAdd(work + 3, 1u);
+      }
+    } else if (rc != kDone) {  // the general kernel is warp-level: warp 0 runs it
+      if (threadIdx.x == 0) atomicAdd(work + 1, 1u);
       if (threadIdx.x < 32) {
         volatile uint32_t* vtop = reinterpret_cast<volatile uint32_t*>(fsm);
         replay_candidate(c, cid, S.dstate + c.dev_off, vtop, S, O, want_schedule != 0);

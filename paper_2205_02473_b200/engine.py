@@ -149,11 +149,12 @@ class Batch:
         self.with_schedule = want_schedule
 
     def stats(self) -> dict:
-        st = np.zeros(3, np.int64)
+        st = np.zeros(5, np.int64)
         _check(self.engine.ctx, N.lib.dpro_cuda_batch_stats(self.engine.ctx, self.handle,
                                                             N.ptr(st)), "batch_stats")
         return {"fallbacks": int(st[0]), "fast_smem_bytes": int(st[1]),
-                "fast_blocks_per_sm": int(st[2])}
+                "fast_blocks_per_sm": int(st[2]), "ring": int(st[3]),
+                "deep_ring_retries": int(st[4])}
 
     def device_results(self) -> dict:
         ps = [C.c_void_p() for _ in range(5)]

@@ -35,7 +35,7 @@ def main():
         b.replay(bool(a.schedule))
         ms, st, *_ = b.results()
         print(f"replay {1e3 * (time.perf_counter() - t):.2f} ms, ok={int((st == 0).sum())}, "
-              f"makespan[0]={ms[0]}")
+              f"makespan[0]={ms[0]} V={int(b.n_ops.mean())} stats={b.stats()}")
 
 
 if __name__ == "__main__":
