@@ -557,8 +557,10 @@ template <int NW, int KD>
 int launch_fast_kd(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule, FastCfg F) {
   auto kern = dpro_k::replay_fast_kernel<NW, KD>;
   const size_t smem = F.warp_bytes;
-  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)ctx->smem_optin));
+  cudaFuncAttributes fa{};
+  CU(cudaFuncGetAttributes(&fa, kern));
+  const size_t dyn_max = ctx->smem_optin - fa.sharedSizeBytes;
+  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_max));
   int blocks_per_sm = 0;
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, 32 * NW, smem));
   blocks_per_sm = std::max(blocks_per_sm, 1);
@@ -572,7 +574,7 @@ int launch_fast_kd(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule, FastCfg 
   // pass 1: candidates whose device queues outgrew the ring, one CTA per SM
   // with the deepest rings the shared memory holds
   FastCfg D = F;
-  const size_t limit = ctx->smem_optin - 64;
+  const size_t limit = dyn_max;
   while (D.qc < 4096 && fast_bytes(D.dcap, D.qc * 2, D.rl, D.ccap, NW) <= limit) D.qc *= 2;
   D.warp_bytes = static_cast<uint32_t>(fast_bytes(D.dcap, D.qc, D.rl, D.ccap, NW));
   kern<<<ctx->sm_count, 32 * NW, D.warp_bytes, ctx->stream>>>(
