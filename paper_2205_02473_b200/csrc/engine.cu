@@ -574,6 +574,7 @@ int launch_fast_kd(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule, FastCfg 
   // pass 1: candidates whose device queues outgrew the ring, one CTA per SM
   // with the deepest rings the shared memory holds
   FastCfg D = F;
+  D.rl = std::max<uint32_t>(F.rl, 2048);
   const size_t limit = dyn_max;
   while (D.qc < 4096 && fast_bytes(D.dcap, D.qc * 2, D.rl, D.ccap, NW) <= limit) D.qc *= 2;
   D.warp_bytes = static_cast<uint32_t>(fast_bytes(D.dcap, D.qc, D.rl, D.ccap, NW));

@@ -180,7 +180,7 @@ struct FastWarp {
     if (p < rlcap)
       rl[p] = make_uint2(sb, n);
     else
-      atomicOr(const_cast<uint32_t*>(&misc[1]), kBailOther);
+      atomicOr(const_cast<uint32_t*>(&misc[1]), kBailRing);  // capacity: retry deeper
   }
 
   // ready(s, t) of replay.cpp:60-72 for s reached through a packed record.
@@ -246,7 +246,7 @@ struct FastWarp {
     for (;;) {
       const uint32_t hi = *rlc;
       if (misc[1]) return misc[1] == kBailRing ? kBailRing : kBailOther;
-      if (hi > rlcap) return kBailOther;
+      if (hi > rlcap) return kBailRing;
       if (lo == hi) return kDone;
       for (uint32_t g = lo; g < hi; g += 32) {
         const uint32_t r = g + lane;
@@ -384,8 +384,8 @@ __device__ unsigned long long g_prof[16];
 #define PROF_ADD(i, x)
 #endif
 
-// Returns kDone, kBailRing (a device queue outgrew its ring: retry with
-// deeper rings) or kBailOther (take the general path).
+// Returns kDone, kBailRing (a device queue outgrew its ring or a round its
+// range list: retry with deeper ones) or kBailOther (take the general path).
 template <int NW, int KD>
 __device__ uint32_t replay_fast(const Cand& c, int cid, const uint4* rec, const uint4* erec,
                             const uint8_t* cnt0, const uint32_t* srcs, const PackInfo& info,
