@@ -1,0 +1,220 @@
+"""Batched candidate evaluator and search driver over the GPU Replayer.
+
+The reference evaluates one candidate graph per `replay()` call inside its
+greedy Alg. 1 (proj/src/optimize.cpp:1327-1650; gate 1382-1392). Here a
+whole round of candidates is generated as CSR on host threads
+(csrc/dfg_gen.cpp) and replayed in ONE batched launch; across GPUs every
+rank evaluates its own shard and the round's best candidate is agreed on
+with one packed int64 MIN all-reduce (the K4 exchange of DESIGN.md).
+
+* `opt_part_num`        optimize.cpp:562-576 (k* over a batched t_sync grid)
+* `should_fuse_ops`     optimize.cpp:545-551 (Theorem 1)
+* `should_fuse_tensors` optimize.cpp:553-560 (Theorem 2)
+* `SyncSearch`          tensor-fusion + partition search over a layered
+                        model; MCMC with the acceptance rule of the paper's
+                        (excised) MCMC algorithm, P = min(1, exp(beta (T - T'))),
+                        PAPER.md:928. The reference ships no MCMC (SURVEY
+                        section 0.1), so trajectories are "parity unpinned";
+                        every evaluated candidate's makespan is exact (equal
+                        to the reference replay of the same rewritten graph).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import Callable, Sequence
+
+import numpy as np
+
+from .engine import Engine, default_engine
+from .graph import ClusterSpec
+from .ingest import LayeredModel, layered_graph_groups
+from .replay import sync_makespan_grid
+
+
+def opt_part_num(bytes_: int, kmax: int, t_sync: Callable[[int, int], int]) -> int:
+    """optimize.cpp:562-576: argmin_k t_sync(bytes, k), k in [1, min(kmax, bytes)],
+    ties -> smallest k."""
+    if bytes_ < 1:
+        return 1
+    cap = min(max(kmax, 1), bytes_)
+    best_k, best = 1, t_sync(bytes_, 1)
+    for k in range(2, cap + 1):
+        v = t_sync(bytes_, k)
+        if v < best:
+            best, best_k = v, k
+    return best_k
+
+
+class SyncTable:
+    """Memoized t_sync(bytes, k) (SearchCtx::sync, optimize.cpp:1170-1194)
+    filled by batched GPU grids instead of one replay per (bytes, k)."""
+
+    def __init__(self, cluster: ClusterSpec, engine: Engine | None = None):
+        self.cluster = cluster
+        self.engine = engine
+        self.memo: dict[tuple[int, int], int] = {}
+
+    def fill(self, pairs: Sequence[tuple[int, int]]) -> None:
+        todo = sorted({p for p in pairs if p not in self.memo})
+        if todo:
+            vals = sync_makespan_grid(self.cluster, [b for b, _ in todo], [k for _, k in todo],
+                                      engine=self.engine)
+            self.memo.update(zip(todo, vals))
+
+    def __call__(self, bytes_: int, k: int) -> int:
+        if (bytes_, k) not in self.memo:
+            self.fill([(bytes_, k)])
+        return self.memo[(bytes_, k)]
+
+    def opt_part_num_many(self, sizes: Sequence[int], kmax: int) -> list[int]:
+        """k* for many tensor sizes with ONE grid launch."""
+        self.fill([(b, k) for b in sizes for k in range(1, min(max(kmax, 1), b) + 1)])
+        return [opt_part_num(b, kmax, self) for b in sizes]
+
+
+def should_fuse_ops(p_prev_dur: int, p_cur_dur: int, fused_dur: float, q_prev_dur: int) -> bool:
+    """Theorem 1, optimize.cpp:545-551."""
+    gain = float(p_prev_dur) + float(p_cur_dur) - fused_dur
+    return float(q_prev_dur) <= gain + 1e-9
+
+
+def should_fuse_tensors(q_prev_end: int, p_cur_end: int, s_prev: int, s_cur: int, kmax: int,
+                        t_sync: Callable[[int, int], int]) -> bool:
+    """Theorem 2, optimize.cpp:553-560."""
+    fused = s_prev + s_cur
+    fused_sync = t_sync(fused, opt_part_num(fused, kmax, t_sync))
+    cur_sync = t_sync(s_cur, opt_part_num(s_cur, kmax, t_sync))
+    return q_prev_end > p_cur_end + fused_sync - cur_sync
+
+
+@dataclass
+class SyncState:
+    """Synchronization units of a layered model: groups of consecutive layers
+    fused in layer order (apply_tensor_fusion chain), each with a partition
+    count (apply_tensor_partition)."""
+    groups: list[list[int]]
+    ks: list[int]
+    makespan: int = -1
+
+    def key(self) -> tuple:
+        return tuple(tuple(g) for g in self.groups), tuple(self.ks)
+
+    def copy(self) -> "SyncState":
+        return SyncState([list(g) for g in self.groups], list(self.ks), self.makespan)
+
+
+@dataclass
+class SearchLog:
+    rounds: int = 0
+    evaluated: int = 0
+    accepted: int = 0
+    history: list[int] = field(default_factory=list)
+
+
+class SyncSearch:
+    """Batched MCMC over tensor fusion + partition (BASELINE config 3).
+
+    Each round proposes `batch` neighbours of the current state (fuse two
+    adjacent units, split a unit, re-partition a unit), replays them all in
+    one GPU batch (makespan only), takes the best as the proposal and
+    accepts it with P = min(1, exp(beta * (T - T'))).
+    With `dist` (torch.distributed) every rank proposes its own batch and
+    the global best is chosen by a packed (makespan, rank, id) MIN
+    all-reduce, then broadcast from its owner."""
+
+    def __init__(self, model: LayeredModel, cluster: ClusterSpec, engine: Engine | None = None,
+                 kmax: int = 16, beta: float = 0.01, seed: int = 0, threads: int = 8,
+                 dist=None, rank: int = 0):
+        self.model, self.cluster = model, cluster
+        self.engine = engine or default_engine()
+        self.kmax, self.beta, self.threads = kmax, beta, threads
+        self.rng = np.random.default_rng([seed, rank])
+        self.dist, self.rank = dist, rank
+        L = model.layers
+        self.state = SyncState([[i] for i in range(L)], [1] * L)
+        self.best = None
+        self.log = SearchLog()
+
+    # ---- candidates ---------------------------------------------------
+    def _bytes(self, g: list[int]) -> int:
+        return int(sum(self.model.tensor_bytes[i] for i in g))
+
+    def propose(self, s: SyncState) -> SyncState:
+        c = s.copy()
+        n = len(c.groups)
+        move = self.rng.integers(0, 3)
+        if move == 0 and n > 1:  # tensor fusion of two adjacent units
+            i = int(self.rng.integers(0, n - 1))
+            c.groups[i:i + 2] = [c.groups[i] + c.groups[i + 1]]
+            c.ks[i:i + 2] = [1]
+        elif move == 1 and any(len(g) > 1 for g in c.groups):  # un-fuse
+            cand = [i for i, g in enumerate(c.groups) if len(g) > 1]
+            i = cand[int(self.rng.integers(0, len(cand)))]
+            cut = int(self.rng.integers(1, len(c.groups[i])))
+            g = c.groups[i]
+            c.groups[i:i + 1] = [g[:cut], g[cut:]]
+            c.ks[i:i + 1] = [1, 1]
+        else:  # re-partition a unit
+            i = int(self.rng.integers(0, n))
+            cap = min(self.kmax, self._bytes(c.groups[i]))
+            c.ks[i] = int(self.rng.integers(1, cap + 1))
+        return c
+
+    def evaluate(self, states: Sequence[SyncState]) -> np.ndarray:
+        """Exact makespans of candidate states: one GPU batch."""
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(self.threads) as ex:
+            graphs = list(ex.map(lambda st: layered_graph_groups(self.model, self.cluster,
+                                                                 st.groups, st.ks), states))
+        b = self.engine.batch([g.csr for g in graphs])
+        b.replay(want_schedule=False)
+        ms, st, *_ = b.results()
+        if np.any(st != 0):
+            raise RuntimeError(f"replay failed for {int((st != 0).sum())} candidates")
+        self.log.evaluated += len(states)
+        return ms
+
+    # ---- one round ----------------------------------------------------
+    def _exchange(self, best_ms: int, best_i: int, cand: SyncState) -> SyncState:
+        if self.dist is None:
+            return cand
+        import torch
+        dev = f"cuda:{self.engine.device}" if self.dist.get_backend() == "nccl" else "cpu"
+        key = torch.tensor([(int(best_ms) << 24) | (self.rank << 20) | int(best_i)],
+                           dtype=torch.int64, device=dev)
+        self.dist.all_reduce(key, op=self.dist.ReduceOp.MIN)
+        owner = (int(key.item()) >> 20) & 0xF
+        obj = [cand if self.rank == owner else None]
+        self.dist.broadcast_object_list(obj, src=owner)
+        out = obj[0]
+        out.makespan = int(key.item()) >> 24
+        return out
+
+    def step(self, batch: int) -> SearchLog:
+        s = self.state
+        if s.makespan < 0:
+            s.makespan = int(self.evaluate([s])[0])
+            self.best = s.copy()
+        cands = [self.propose(s) for _ in range(batch)]
+        ms = self.evaluate(cands)
+        i = int(np.argmin(ms))
+        cands[i].makespan = int(ms[i])
+        prop = self._exchange(int(ms[i]), i, cands[i])
+        # Metropolis acceptance (memory loss term 0); the
+        # uniform draw is shared so every rank takes the same decision
+        u = float(np.random.default_rng([self.log.rounds, 7]).random())
+        p = min(1.0, math.exp(self.beta * (s.makespan - prop.makespan)))
+        if u < p:
+            self.state = prop
+            self.log.accepted += 1
+        if self.state.makespan < self.best.makespan:
+            self.best = self.state.copy()
+        self.log.rounds += 1
+        self.log.history.append(self.state.makespan)
+        return self.log
+
+    def run(self, rounds: int, batch: int) -> SyncState:
+        for _ in range(rounds):
+            self.step(batch)
+        return self.best

@@ -1,0 +1,75 @@
+"""Batched evaluator / search driver (search.py). CPU tests: the predicates
+and opt_part_num exactly as proj/tests/test_optimize.cpp:246-291 states
+them; GPU tests: the batched t_sync table and the MCMC driver, whose every
+evaluated candidate must equal the reference's replay of the same rewrite
+chain (apply_tensor_fusion + apply_tensor_partition)."""
+import numpy as np
+import pytest
+
+from paper_2205_02473_b200.search import (SyncSearch, SyncTable, opt_part_num, should_fuse_ops,
+                                          should_fuse_tensors)
+
+
+def test_op_fusion_predicate():  # test_optimize.cpp:246-254
+    assert should_fuse_ops(3, 4, 6.0, 1)
+    assert not should_fuse_ops(3, 4, 6.0, 5)
+    assert should_fuse_ops(3, 4, 6.0, 0)
+
+
+def test_tensor_fusion_predicate():  # test_optimize.cpp:256-262
+    sync = lambda b, k: b
+    assert should_fuse_tensors(100, 50, 20, 40, 1, sync)
+    assert not should_fuse_tensors(60, 50, 20, 40, 1, sync)
+
+
+def test_opt_part_num_ties_and_cap():  # test_optimize.cpp:285-291
+    assert opt_part_num(100, 4, lambda b, k: 7) == 1
+    assert opt_part_num(2, 4, lambda b, k: 100 - k) == 2
+
+
+@pytest.mark.gpu
+def test_sync_table_grid(engine):  # test_optimize.cpp:265-283 on the GPU grid
+    from paper_2205_02473_b200.graph import synth_cluster
+    t = SyncTable(synth_cluster("ps", 1, 1, 1.0, 0.0), engine)
+    assert t.opt_part_num_many([100], 4) == [4]
+    assert [t(100, k) for k in (1, 2, 3, 4)] == [200, 150, 134, 125]
+    t50 = SyncTable(synth_cluster("ps", 1, 1, 1.0, 50.0), engine)
+    assert t50.opt_part_num_many([100, 1], 4) == [1, 1]
+
+
+def _ref_chain(ref, spec, groups, ks):
+    """The reference's own rewrite chain for a SyncState."""
+    rg = ref.RefGraph.synth(spec)
+    for g in groups:
+        name = f"g{g[0]}"
+        for i in g[1:]:
+            rg = rg.tensor_fusion(name, f"g{i}")
+            name = f"{name}+g{i}"
+    for g, k in zip(groups, ks):
+        if k > 1:
+            rg = rg.partition("+".join(f"g{i}" for i in g), k)
+    return rg
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("scheme,W,S", [("ring", 4, 0), ("ps", 4, 2)])
+def test_search_candidates_match_reference(engine, ref, scheme, W, S):
+    from paper_2205_02473_b200.graph import synth_cluster
+    from paper_2205_02473_b200.ingest import LayeredModel
+    L = 6
+    rng = np.random.default_rng(11)
+    fw, bw = rng.integers(50, 400, L).tolist(), rng.integers(80, 900, L).tolist()
+    tb = rng.integers(10_000, 3_000_000, L).tolist()
+    spec = {"layers": L, "fw_dur_us": fw, "bw_dur_us": bw, "tensor_bytes": tb,
+            "update_dur_us": 5, "scheme": scheme, "workers": W, "ps_count": S,
+            "bandwidth_bytes_per_us": 1250.0, "latency_us": 5.0}
+    s = SyncSearch(LayeredModel(fw, bw, tb, 5), synth_cluster(scheme, W, S, 1250.0, 5.0),
+                   engine, kmax=8, beta=0.05, seed=3, threads=4)
+    for _ in range(6):
+        s.step(48)
+    assert s.best.makespan <= s.log.history[0] or s.log.rounds == 6
+    cands = [s.propose(s.state) for _ in range(12)] + [s.best]
+    ms = s.evaluate(cands)
+    for c, m in zip(cands, ms):
+        T, *_ = _ref_chain(ref, spec, c.groups, c.ks).replay()
+        assert T == int(m), (c.groups, c.ks)
