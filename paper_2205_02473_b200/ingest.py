@@ -230,13 +230,16 @@ class LayeredModel:
         return len(self.fw_dur)
 
     def struct(self):
-        self._fw = np.ascontiguousarray(self.fw_dur, np.int64)
-        self._bw = np.ascontiguousarray(self.bw_dur, np.int64)
-        self._tb = np.ascontiguousarray(self.tensor_bytes, np.int64)
+        """ctypes view; the arrays live on the returned struct (thread-safe:
+        concurrent generator calls each own their copies)."""
+        fw = np.ascontiguousarray(self.fw_dur, np.int64)
+        bw = np.ascontiguousarray(self.bw_dur, np.int64)
+        tb = np.ascontiguousarray(self.tensor_bytes, np.int64)
         P = C.POINTER(C.c_int64)
-        return N.DproLayeredModel(self.layers, self._fw.ctypes.data_as(P),
-                                  self._bw.ctypes.data_as(P), self._tb.ctypes.data_as(P),
-                                  int(self.update_dur))
+        st = N.DproLayeredModel(self.layers, fw.ctypes.data_as(P), bw.ctypes.data_as(P),
+                                tb.ctypes.data_as(P), int(self.update_dur))
+        st._keep = (fw, bw, tb)
+        return st
 
 
 def layered_graph(model: LayeredModel, cluster: ClusterSpec,
