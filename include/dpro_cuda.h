@@ -204,6 +204,16 @@ dpro_graph* dpro_graph_layered_groups(const dpro_layered_model* model,
                                       int32_t n_groups, const int32_t* group_off,
                                       const int32_t* members,
                                       const int32_t* group_k, int32_t* status);
+/* n fusion/partition candidates on `threads` host threads. Candidate i owns
+ * groups [spec_off[i], spec_off[i] + n_groups[i]) of the flattened arrays:
+ * group g spans members[group_off[g] .. group_off[g+1]) with partition
+ * count group_k[g]. */
+int dpro_graph_layered_groups_batch(const dpro_layered_model* model,
+                                    const dpro_cluster_desc* cluster, int32_t n,
+                                    const int32_t* n_groups, const int64_t* spec_off,
+                                    const int32_t* group_off, const int32_t* members,
+                                    const int32_t* group_k, int32_t threads,
+                                    dpro_graph** out);
 /* n graphs with part_k[n*layers], built on `threads` host threads. */
 int dpro_graph_layered_batch(const dpro_layered_model* model,
                              const dpro_cluster_desc* cluster,

@@ -87,6 +87,7 @@ SIGNATURES = {
     "dpro_graph_layered": (_P, [C.POINTER(DproLayeredModel), C.POINTER(DproClusterDesc), _P, _P]),
     "dpro_graph_layered_batch": (C.c_int, [C.POINTER(DproLayeredModel), C.POINTER(DproClusterDesc), _P, _I32, _I32, _P]),
     "dpro_graph_layered_groups": (_P, [C.POINTER(DproLayeredModel), C.POINTER(DproClusterDesc), _I32, _P, _P, _P, _P]),
+    "dpro_graph_layered_groups_batch": (C.c_int, [C.POINTER(DproLayeredModel), C.POINTER(DproClusterDesc), _I32, _P, _P, _P, _P, _P, _I32, _P]),
     "dpro_graph_tsync": (_P, [C.POINTER(DproClusterDesc), _I64, _I32, _P]),
     "dpro_graph_csr": (C.c_int, [_P, C.POINTER(DproCsr)]),
     "dpro_graph_op_id": (C.c_char_p, [_P, _U32]),

@@ -10,7 +10,11 @@
 // Op ids are generated with the reference naming so the byte-lexicographic
 // sort reproduces the reference op index (the replay tie-break order).
 #include <algorithm>
+#include <array>
+#include <atomic>
+#include <charconv>
 #include <cmath>
+#include <unordered_map>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -104,16 +108,17 @@ struct Gen {
   };
   std::vector<Op> ops;
   std::vector<std::pair<uint32_t, uint32_t>> edges;  // creation indices
-  std::map<std::pair<int, std::string>, uint32_t> devkeys;  // (kind, str)
+  // devices keyed by (kind, node index, peer index); resolved to DeviceId
+  // order (kind, node name, peer name -- graph.hpp:57-72) in finalize()
+  std::unordered_map<uint64_t, uint32_t> devkeys;
+  std::vector<std::array<int, 3>> devs;  // key id -> (kind, node, peer)
+  const std::vector<std::string>* names = nullptr;
 
-  uint32_t device(int dkind, const std::string& node, const std::string& peer) {
-    // DeviceId order: kind (compute < link), node, peer (graph.hpp:57-72).
-    // Encode as (kind, node + '\0' + peer) which sorts identically.
-    std::string key = node;
-    key.push_back('\0');
-    key += peer;
-    auto it = devkeys.emplace(std::make_pair(dkind, key),
-                              static_cast<uint32_t>(devkeys.size()));
+  uint32_t device(int dkind, int node, int peer) {
+    const uint64_t key = (uint64_t(dkind) << 62) | (uint64_t(uint32_t(node)) << 31) |
+                         uint64_t(uint32_t(peer + 1));
+    auto it = devkeys.emplace(key, static_cast<uint32_t>(devs.size()));
+    if (it.second) devs.push_back({dkind, node, peer});
     return it.first->second;
   }
   uint32_t add(std::string id, int32_t kind, uint32_t dev, int64_t dur) {
@@ -123,15 +128,20 @@ struct Gen {
   void edge(uint32_t a, uint32_t b) { edges.emplace_back(a, b); }
 };
 
+// Appends decimal v to s (no temporaries).
+inline void append_num(std::string& s, int64_t v) {
+  char buf[24];
+  const auto r = std::to_chars(buf, buf + sizeof buf, v);
+  s.append(buf, r.ptr);
+}
+
 // One tensor unit's comm topology spliced onto per-node IN/OUT ops
 // (ingest.cpp:268-384 expansion + assemble_global_dfg 404-441 splice).
 // in_op/out_op: node index -> creation index (UINT32_MAX when absent).
 void expand_unit(Gen& g, const Cluster& c, const std::string& unit,
                  int64_t bytes, const std::vector<uint32_t>* in_op,
                  const std::vector<uint32_t>* out_op) {
-  auto link_dev = [&](int s, int d) {
-    return g.device(1, c.nodes[s], c.nodes[d]);
-  };
+  auto link_dev = [&](int s, int d) { return g.device(1, s, d); };
   auto need = [&](const std::vector<uint32_t>* v, int node) -> uint32_t {
     if (!v) return UINT32_MAX;
     uint32_t x = (*v)[node];
@@ -153,12 +163,23 @@ void expand_unit(Gen& g, const Cluster& c, const std::string& unit,
       for (int s = 0; s < steps; ++s) {
         const int src = c.ring[(ch + s) % n];
         const int dst = c.ring[(ch + s + 1) % n];
-        const std::string txn = unit + "#c" + std::to_string(ch) + "#s" +
-                                std::to_string(s) + "#" + c.nodes[src] + "#" +
-                                c.nodes[dst];
+        std::string txn;
+        txn.reserve(unit.size() + 32);
+        txn += unit;
+        txn += "#c";
+        append_num(txn, ch);
+        txn += "#s";
+        append_num(txn, s);
+        txn += '#';
+        txn += c.nodes[src];
+        txn += '#';
+        txn += c.nodes[dst];
         const uint32_t dv = link_dev(src, dst);
-        const uint32_t snd = g.add("SEND." + txn, kSend, dv, 0);
-        const uint32_t rcv = g.add("RECV." + txn, kRecv, dv, c.hop(cb, src, dst));
+        std::string sid = "SEND.", rid = "RECV.";
+        sid += txn;
+        rid += txn;
+        const uint32_t snd = g.add(std::move(sid), kSend, dv, 0);
+        const uint32_t rcv = g.add(std::move(rid), kRecv, dv, c.hop(cb, src, dst));
         g.edge(snd, rcv);
         if (s == 0) {
           const uint32_t in = need(in_op, src);
@@ -221,29 +242,59 @@ namespace {
 // DeviceId order, ascending deduplicated succ lists (std::set of edges).
 dpro_graph* finalize(Gen& g) {
   const uint32_t n = static_cast<uint32_t>(g.ops.size());
+  // byte-lexicographic order of ids (std::map<std::string> order): compare
+  // 16-byte big-endian prefixes first, full strings only on prefix ties
+  struct Key {
+    uint64_t a, b;
+    uint32_t i;
+  };
+  std::vector<Key> keys(n);
+  for (uint32_t i = 0; i < n; ++i) {
+    unsigned char buf[16] = {0};
+    const std::string& id = g.ops[i].id;
+    std::memcpy(buf, id.data(), std::min<size_t>(16, id.size()));
+    uint64_t a = 0, b = 0;
+    for (int k = 0; k < 8; ++k) a = (a << 8) | buf[k];
+    for (int k = 8; k < 16; ++k) b = (b << 8) | buf[k];
+    keys[i] = {a, b, i};
+  }
+  std::sort(keys.begin(), keys.end(), [&](const Key& x, const Key& y) {
+    if (x.a != y.a) return x.a < y.a;
+    if (x.b != y.b) return x.b < y.b;
+    return g.ops[x.i].id < g.ops[y.i].id;  // shared 16-byte prefix (or short ids)
+  });
   std::vector<uint32_t> order(n);
-  std::iota(order.begin(), order.end(), 0u);
-  std::sort(order.begin(), order.end(),
-            [&](uint32_t a, uint32_t b) { return g.ops[a].id < g.ops[b].id; });
+  for (uint32_t i = 0; i < n; ++i) order[i] = keys[i].i;
   for (uint32_t i = 1; i < n; ++i)
     if (g.ops[order[i]].id == g.ops[order[i - 1]].id)
       throw std::runtime_error("duplicate op id '" + g.ops[order[i]].id + "'");
   std::vector<uint32_t> rank(n);
   for (uint32_t i = 0; i < n; ++i) rank[order[i]] = i;
 
-  std::vector<uint32_t> dev_rank(g.devkeys.size());
+  // dense device ids in DeviceId order: (kind, node name, peer name)
+  const std::vector<std::string>& nm = *g.names;
+  std::vector<uint32_t> dorder(g.devs.size());
+  std::iota(dorder.begin(), dorder.end(), 0u);
+  auto dname = [&](int idx) -> const std::string& {
+    static const std::string empty;
+    return idx < 0 ? empty : nm[idx];
+  };
+  std::sort(dorder.begin(), dorder.end(), [&](uint32_t x, uint32_t y) {
+    const auto& a = g.devs[x];
+    const auto& b = g.devs[y];
+    if (a[0] != b[0]) return a[0] < b[0];
+    const int cn = dname(a[1]).compare(dname(b[1]));
+    if (cn != 0) return cn < 0;
+    return dname(a[2]) < dname(b[2]);
+  });
+  std::vector<uint32_t> dev_rank(g.devs.size());
   auto* out = new dpro_graph;
-  {
-    uint32_t k = 0;
-    for (const auto& [key, id] : g.devkeys) {  // map order == DeviceId order
-      dev_rank[id] = k++;
-      const std::string& s = key.second;
-      const auto z = s.find('\0');
-      out->device_strs.push_back(key.first == 0 ? s.substr(0, z)
-                                                : s.substr(0, z) + ">" + s.substr(z + 1));
-    }
+  for (uint32_t k = 0; k < dorder.size(); ++k) {
+    dev_rank[dorder[k]] = k;
+    const auto& d = g.devs[dorder[k]];
+    out->device_strs.push_back(d[0] == 0 ? dname(d[1]) : dname(d[1]) + ">" + dname(d[2]));
   }
-  if (g.devkeys.size() > 65535) {
+  if (g.devs.size() > 65535) {
     delete out;
     throw std::runtime_error("more than 65535 devices");
   }
@@ -289,6 +340,7 @@ struct Groups {
 
 dpro_graph* build_layered(const dpro_layered_model& m, const Cluster& c, const Groups& G) {
   Gen g;
+  g.names = &c.nodes;
   const int L = m.layers;
   if (L < 1) throw std::runtime_error("synthetic model needs at least one layer");
   const int N = static_cast<int>(c.nodes.size());
@@ -315,7 +367,7 @@ dpro_graph* build_layered(const dpro_layered_model& m, const Cluster& c, const G
   std::vector<std::vector<uint32_t>> out_op(NG, std::vector<uint32_t>(N, UINT32_MAX));
   for (int w : workers) {
     const std::string& node = c.nodes[w];
-    const uint32_t dv = g.device(0, node, "");
+    const uint32_t dv = g.device(0, w, -1);
     std::vector<uint32_t> fw(L), bw(L), up(L);
     for (int i = 0; i < L; ++i) {
       const std::string li = std::to_string(i);
@@ -379,6 +431,7 @@ dpro_graph* build_tsync(const Cluster& c, int64_t bytes, int k) {
     throw std::invalid_argument("sync_makespan: partition count must be >= 1, got " +
                                 std::to_string(k));
   Gen g;
+  g.names = &c.nodes;
   const int64_t base = bytes / k, rem = bytes % k;
   for (int i = 0; i < k; ++i) {
     const std::string unit = k == 1 ? "tsync" : "tsync#p" + std::to_string(i);
@@ -458,6 +511,49 @@ dpro_graph* dpro_graph_layered_groups(const dpro_layered_model* model,
                              make_groups(n_groups, group_off, members, group_k));
       },
       status);
+}
+
+int dpro_graph_layered_groups_batch(const dpro_layered_model* model,
+                                    const dpro_cluster_desc* cluster, int32_t n,
+                                    const int32_t* n_groups, const int64_t* spec_off,
+                                    const int32_t* group_off, const int32_t* members,
+                                    const int32_t* group_k, int32_t threads,
+                                    dpro_graph** out) {
+  const Cluster c(*cluster);
+  if (threads < 1) threads = 1;
+  std::vector<int32_t> st(n, DPRO_OK);
+  std::vector<std::string> errs(threads);
+  std::atomic<int32_t> next{0};
+  auto work = [&](int tid) {
+    for (int32_t i; (i = next.fetch_add(1)) < n;) {
+      try {
+        // candidate i: groups [spec_off[i], spec_off[i] + n_groups[i]) of
+        // the flattened group_off / group_k arrays (group_off is global)
+        const int64_t g0 = spec_off[i];
+        Groups G;
+        for (int32_t q = 0; q < n_groups[i]; ++q) {
+          G.members.emplace_back(members + group_off[g0 + q], members + group_off[g0 + q + 1]);
+          G.k.push_back(group_k ? group_k[g0 + q] : 1);
+        }
+        out[i] = build_layered(*model, c, G);
+      } catch (const std::exception& e) {
+        out[i] = nullptr;
+        st[i] = DPRO_EINVAL;
+        errs[tid] = e.what();
+      }
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < threads; ++t) pool.emplace_back(work, t);
+  work(0);
+  for (auto& th : pool) th.join();
+  for (int32_t i = 0; i < n; ++i)
+    if (st[i] != DPRO_OK) {
+      for (auto& e : errs)
+        if (!e.empty()) g_gen_err = e;
+      return st[i];
+    }
+  return DPRO_OK;
 }
 
 dpro_graph* dpro_graph_tsync(const dpro_cluster_desc* cluster, int64_t bytes,

@@ -269,6 +269,32 @@ def layered_graph_groups(model: LayeredModel, cluster: ClusterSpec,
     return NativeGraph(h)
 
 
+def layered_graphs_groups(model: LayeredModel, cluster: ClusterSpec,
+                          specs: Sequence[tuple[Sequence[Sequence[int]], Sequence[int]]],
+                          threads: int = 8) -> list[NativeGraph]:
+    """Batch of fusion/partition candidates [(groups, ks), ...] built on
+    native threads (no Python per candidate)."""
+    m = model.struct()
+    holder = N.ClusterDescHolder(cluster)
+    n = len(specs)
+    n_groups = np.array([len(g) for g, _ in specs], np.int32)
+    spec_off = np.zeros(n, np.int64)
+    spec_off[1:] = np.cumsum(n_groups[:-1])
+    sizes = [len(m_) for g, _ in specs for m_ in g]
+    group_off = np.zeros(len(sizes) + 1, np.int32)
+    group_off[1:] = np.cumsum(sizes)
+    members = np.ascontiguousarray([i for g, _ in specs for m_ in g for i in m_], np.int32)
+    ks = np.ascontiguousarray([k for _, kk in specs for k in kk], np.int32)
+    out = (C.c_void_p * n)()
+    rc = N.lib.dpro_graph_layered_groups_batch(C.byref(m), C.byref(holder.desc), n,
+                                               N.ptr(n_groups), N.ptr(spec_off),
+                                               N.ptr(group_off), N.ptr(members), N.ptr(ks),
+                                               threads, out)
+    if rc != N.DPRO_OK:
+        raise Error(N.lib.dpro_graph_last_error().decode())
+    return [NativeGraph(out[i]) for i in range(n)]
+
+
 def layered_graphs(model: LayeredModel, cluster: ClusterSpec, part_k: np.ndarray,
                    threads: int = 8) -> list[NativeGraph]:
     """Candidate batch: one graph per row of part_k [n, layers]."""

@@ -28,7 +28,7 @@ import numpy as np
 
 from .engine import Engine, default_engine
 from .graph import ClusterSpec
-from .ingest import LayeredModel, layered_graph_groups
+from .ingest import LayeredModel, layered_graphs_groups
 from .replay import sync_makespan_grid
 
 
@@ -163,10 +163,8 @@ class SyncSearch:
 
     def evaluate(self, states: Sequence[SyncState]) -> np.ndarray:
         """Exact makespans of candidate states: one GPU batch."""
-        from concurrent.futures import ThreadPoolExecutor
-        with ThreadPoolExecutor(self.threads) as ex:
-            graphs = list(ex.map(lambda st: layered_graph_groups(self.model, self.cluster,
-                                                                 st.groups, st.ks), states))
+        graphs = layered_graphs_groups(self.model, self.cluster,
+                                       [(st.groups, st.ks) for st in states], self.threads)
         b = self.engine.batch([g.csr for g in graphs])
         b.replay(want_schedule=False)
         ms, st, *_ = b.results()

@@ -38,12 +38,10 @@ def main():
 
     def timed(states):
         nonlocal t_gen, t_gpu
-        from concurrent.futures import ThreadPoolExecutor
-        from paper_2205_02473_b200.ingest import layered_graph_groups
+        from paper_2205_02473_b200.ingest import layered_graphs_groups
         t0 = time.perf_counter()
-        with ThreadPoolExecutor(threads) as ex:
-            graphs = list(ex.map(lambda st: layered_graph_groups(s.model, s.cluster, st.groups,
-                                                                 st.ks), states))
+        graphs = layered_graphs_groups(s.model, s.cluster, [(st.groups, st.ks) for st in states],
+                                       threads)
         t1 = time.perf_counter()
         b = eng.batch([g.csr for g in graphs])
         b.replay(want_schedule=False)
