@@ -214,6 +214,21 @@ int dpro_graph_layered_groups_batch(const dpro_layered_model* model,
                                     const int32_t* group_off, const int32_t* members,
                                     const int32_t* group_k, int32_t threads,
                                     dpro_graph** out);
+/* Delta construction: a base layered graph (every
+ * tensor its own unit, k = 1) built once; candidates are then produced as
+ * base minus their changed units' ops plus the re-expanded ones, merged into
+ * the base index order -- the same CSR a full rebuild gives, without
+ * re-naming and re-sorting the unchanged ops. Spec arrays as in
+ * dpro_graph_layered_groups_batch. */
+typedef struct dpro_base dpro_base;
+dpro_base* dpro_base_layered(const dpro_layered_model* model,
+                             const dpro_cluster_desc* cluster, int32_t* status);
+void dpro_base_free(dpro_base* base);
+int dpro_graph_from_base_batch(const dpro_base* base, int32_t n,
+                               const int32_t* n_groups, const int64_t* spec_off,
+                               const int32_t* group_off, const int32_t* members,
+                               const int32_t* group_k, int32_t threads,
+                               dpro_graph** out);
 /* n graphs with part_k[n*layers], built on `threads` host threads. */
 int dpro_graph_layered_batch(const dpro_layered_model* model,
                              const dpro_cluster_desc* cluster,

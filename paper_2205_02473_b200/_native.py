@@ -88,6 +88,9 @@ SIGNATURES = {
     "dpro_graph_layered_batch": (C.c_int, [C.POINTER(DproLayeredModel), C.POINTER(DproClusterDesc), _P, _I32, _I32, _P]),
     "dpro_graph_layered_groups": (_P, [C.POINTER(DproLayeredModel), C.POINTER(DproClusterDesc), _I32, _P, _P, _P, _P]),
     "dpro_graph_layered_groups_batch": (C.c_int, [C.POINTER(DproLayeredModel), C.POINTER(DproClusterDesc), _I32, _P, _P, _P, _P, _P, _I32, _P]),
+    "dpro_base_layered": (_P, [C.POINTER(DproLayeredModel), C.POINTER(DproClusterDesc), _P]),
+    "dpro_base_free": (None, [_P]),
+    "dpro_graph_from_base_batch": (C.c_int, [_P, _I32, _P, _P, _P, _P, _P, _I32, _P]),
     "dpro_graph_tsync": (_P, [C.POINTER(DproClusterDesc), _I64, _I32, _P]),
     "dpro_graph_csr": (C.c_int, [_P, C.POINTER(DproCsr)]),
     "dpro_graph_op_id": (C.c_char_p, [_P, _U32]),
@@ -144,7 +147,7 @@ def check_symbols() -> list[str]:
     """Names declared in include/dpro_cuda.h that the library fails to export."""
     header = (_HERE.parent / "include" / "dpro_cuda.h").read_text()
     import re
-    declared = set(re.findall(r"\b(dpro_(?:cuda|graph)_\w+)\s*\(", header))
+    declared = set(re.findall(r"\b(dpro_(?:cuda|graph|base)_\w+)\s*\(", header))
     missing = [n for n in sorted(declared) if not hasattr(lib, n)]
     return missing + [n for n in sorted(declared) if n not in SIGNATURES]
 

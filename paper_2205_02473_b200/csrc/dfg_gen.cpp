@@ -227,7 +227,13 @@ void expand_unit(Gen& g, const Cluster& c, const std::string& unit,
 }  // namespace
 
 struct dpro_graph {
+  // ids of a full build; delta builds (dpro_graph_from_base_batch) leave it
+  // empty and resolve ids through the shared base graph instead
   std::vector<std::string> ids;
+  std::shared_ptr<const void> base_keep;
+  const std::vector<std::string>* base_ids = nullptr;
+  std::vector<uint32_t> id_ref;  // high bit: new_ids index, else base index
+  std::vector<std::string> new_ids;
   std::vector<int32_t> kind;
   std::vector<int64_t> dur;
   std::vector<uint16_t> dev;
@@ -240,7 +246,8 @@ namespace {
 
 // Sort ops by id (std::map order in GraphBuilder::build), dense device ids in
 // DeviceId order, ascending deduplicated succ lists (std::set of edges).
-dpro_graph* finalize(Gen& g) {
+dpro_graph* finalize(Gen& g, std::vector<uint32_t>* rank_out = nullptr,
+                     std::vector<std::array<int, 3>>* devs_out = nullptr) {
   const uint32_t n = static_cast<uint32_t>(g.ops.size());
   // byte-lexicographic order of ids (std::map<std::string> order): compare
   // 16-byte big-endian prefixes first, full strings only on prefix ties
@@ -325,6 +332,9 @@ dpro_graph* finalize(Gen& g) {
     out->succ[e] = g.edges[e].second;
   }
   for (uint32_t i = 0; i < n; ++i) out->succ_off[i + 1] += out->succ_off[i];
+  if (rank_out) *rank_out = std::move(rank);
+  if (devs_out)
+    for (uint32_t k = 0; k < dorder.size(); ++k) devs_out->push_back(g.devs[dorder[k]]);
   return out;
 }
 
@@ -338,7 +348,17 @@ struct Groups {
   std::vector<int> k;
 };
 
-dpro_graph* build_layered(const dpro_layered_model& m, const Cluster& c, const Groups& G) {
+// Creation indices of the structural ops of a layered build (for delta
+// construction against it).
+struct Record {
+  std::vector<std::vector<uint32_t>> fw, bw, up;  // [node][layer]
+  std::vector<std::vector<uint32_t>> in, out;     // [group][node]
+  std::vector<std::pair<uint32_t, uint32_t>> comm;  // [group] creation range
+};
+
+dpro_graph* build_layered(const dpro_layered_model& m, const Cluster& c, const Groups& G,
+                          Record* rec = nullptr, std::vector<uint32_t>* rank_out = nullptr,
+                          std::vector<std::array<int, 3>>* devs_out = nullptr) {
   Gen g;
   g.names = &c.nodes;
   const int L = m.layers;
@@ -362,6 +382,12 @@ dpro_graph* build_layered(const dpro_layered_model& m, const Cluster& c, const G
   std::vector<int> workers;
   for (int i = 0; i < N; ++i)
     if (c.role[i] == 0) workers.push_back(i);
+  if (rec) {
+    rec->fw.assign(N, std::vector<uint32_t>(L, UINT32_MAX));
+    rec->bw = rec->fw;
+    rec->up = rec->fw;
+    rec->comm.assign(NG, {0, 0});
+  }
   // per group: IN/OUT creation index per node
   std::vector<std::vector<uint32_t>> in_op(NG, std::vector<uint32_t>(N, UINT32_MAX));
   std::vector<std::vector<uint32_t>> out_op(NG, std::vector<uint32_t>(N, UINT32_MAX));
@@ -374,6 +400,11 @@ dpro_graph* build_layered(const dpro_layered_model& m, const Cluster& c, const G
       fw[i] = g.add(node + "->FW.l" + li, kFw, dv, m.fw_dur[i]);
       bw[i] = g.add(node + "->BW.l" + li, kBw, dv, m.bw_dur[i]);
       up[i] = g.add(node + "->UPDATE.l" + li, kUpdate, dv, m.update_dur);
+      if (rec) {
+        rec->fw[w][i] = fw[i];
+        rec->bw[w][i] = bw[i];
+        rec->up[w][i] = up[i];
+      }
     }
     for (int q = 0; q < NG; ++q) {
       in_op[q][w] = g.add(node + "->IN." + gname[q], kVin, dv, 0);
@@ -398,12 +429,18 @@ dpro_graph* build_layered(const dpro_layered_model& m, const Cluster& c, const G
       throw std::runtime_error("cannot split " + std::to_string(bytes) + " bytes of " +
                                gname[q] + " into " + std::to_string(k) + " partitions");
     const int64_t base = bytes / k, rem = bytes % k;
+    const uint32_t c0 = static_cast<uint32_t>(g.ops.size());
     for (int p = 0; p < k; ++p) {
       const std::string unit = k == 1 ? gname[q] : gname[q] + "#p" + std::to_string(p);
       expand_unit(g, c, unit, base + (p < rem ? 1 : 0), &in_op[q], &out_op[q]);
     }
+    if (rec) rec->comm[q] = {c0, static_cast<uint32_t>(g.ops.size())};
   }
-  return finalize(g);
+  if (rec) {
+    rec->in = in_op;
+    rec->out = out_op;
+  }
+  return finalize(g, rank_out, devs_out);
 }
 
 dpro_graph* build_layered(const dpro_layered_model& m, const Cluster& c,
@@ -454,6 +491,284 @@ dpro_graph* guarded(F&& f, int32_t* status) {
     if (status) *status = DPRO_EINVAL;
   }
   return nullptr;
+}
+
+
+// ---------------------------------------------------------------------------
+// Delta construction: a fusion/partition candidate is the
+// base layered graph minus the comm ops (and, for fused units, the IN/OUT
+// ops) of its changed units plus the newly expanded ones. Only the new ops
+// are named and sorted; they are merged into the base's index order by
+// binary search, and every kept base op keeps its relative order, so the
+// result is the same index-ordered CSR a full rebuild produces (tested
+// against it and against the reference's rewrite chain).
+// ---------------------------------------------------------------------------
+struct BaseData {
+  Cluster c;
+  std::vector<int64_t> fw_dur, bw_dur, tensor_bytes;
+  int64_t update_dur = 0;
+  int L = 0, N = 0;
+  std::vector<int> workers;
+  std::unique_ptr<dpro_graph> g;
+  std::vector<std::array<int, 3>> devs;  // dense id -> (kind, node, peer)
+  std::vector<std::vector<uint32_t>> fw, bw, up;  // [node][layer] final index
+  std::vector<std::vector<uint32_t>> in, out;     // [layer][node]
+  std::vector<std::vector<uint32_t>> comm;        // [layer] comm op final indices
+  explicit BaseData(const dpro_cluster_desc& d) : c(d) {}
+};
+
+constexpr uint32_t kBaseRef = 0x80000000u;
+
+bool dev_less(const std::vector<std::string>& nm, const std::array<int, 3>& a,
+              const std::array<int, 3>& b) {
+  static const std::string empty;
+  auto nmf = [&](int i) -> const std::string& { return i < 0 ? empty : nm[i]; };
+  if (a[0] != b[0]) return a[0] < b[0];
+  const int cn = nmf(a[1]).compare(nmf(b[1]));
+  if (cn != 0) return cn < 0;
+  return nmf(a[2]) < nmf(b[2]);
+}
+
+std::shared_ptr<BaseData> build_base(const dpro_layered_model& m, const dpro_cluster_desc& cd) {
+  auto B = std::make_shared<BaseData>(cd);
+  B->L = m.layers;
+  B->N = static_cast<int>(B->c.nodes.size());
+  B->fw_dur.assign(m.fw_dur, m.fw_dur + m.layers);
+  B->bw_dur.assign(m.bw_dur, m.bw_dur + m.layers);
+  B->tensor_bytes.assign(m.tensor_bytes, m.tensor_bytes + m.layers);
+  B->update_dur = m.update_dur;
+  for (int i = 0; i < B->N; ++i)
+    if (B->c.role[i] == 0) B->workers.push_back(i);
+  Groups G;
+  for (int i = 0; i < m.layers; ++i) {
+    G.members.push_back({i});
+    G.k.push_back(1);
+  }
+  Record rec;
+  std::vector<uint32_t> rank;
+  B->g.reset(build_layered(m, B->c, G, &rec, &rank, &B->devs));
+  auto R = [&](uint32_t ci) { return ci == UINT32_MAX ? UINT32_MAX : rank[ci]; };
+  auto map2 = [&](const std::vector<std::vector<uint32_t>>& v) {
+    std::vector<std::vector<uint32_t>> o(v.size());
+    for (size_t a = 0; a < v.size(); ++a)
+      for (uint32_t x : v[a]) o[a].push_back(R(x));
+    return o;
+  };
+  B->fw = map2(rec.fw);
+  B->bw = map2(rec.bw);
+  B->up = map2(rec.up);
+  B->in = map2(rec.in);
+  B->out = map2(rec.out);
+  B->comm.resize(m.layers);
+  for (int i = 0; i < m.layers; ++i)
+    for (uint32_t ci = rec.comm[i].first; ci < rec.comm[i].second; ++ci)
+      B->comm[i].push_back(rank[ci]);
+  return B;
+}
+
+dpro_graph* build_delta(const std::shared_ptr<BaseData>& Bp, const Groups& G) {
+  const BaseData& B = *Bp;
+  const dpro_graph& bg = *B.g;
+  const int L = B.L, NG = static_cast<int>(G.members.size());
+  const uint32_t nb = static_cast<uint32_t>(bg.kind.size());
+  // validate: groups partition the layers
+  std::vector<int> group_of(L, -1);
+  std::vector<std::string> gname(NG);
+  for (int q = 0; q < NG; ++q) {
+    if (G.members[q].empty()) throw std::runtime_error("empty tensor group");
+    for (size_t x = 0; x < G.members[q].size(); ++x) {
+      const int i = G.members[q][x];
+      if (i < 0 || i >= L || group_of[i] >= 0)
+        throw std::runtime_error("tensor groups must partition the layers");
+      group_of[i] = q;
+      gname[q] += (x ? "+g" : "g") + std::to_string(i);
+    }
+  }
+  for (int i = 0; i < L; ++i)
+    if (group_of[i] < 0) throw std::runtime_error("tensor groups must cover every layer");
+
+  Gen g;  // new ops only; edges hold refs (kBaseRef | base index, or new index)
+  g.names = &B.c.nodes;
+  std::vector<uint8_t> removed(nb, 0);
+  for (int q = 0; q < NG; ++q) {
+    const auto& mem = G.members[q];
+    const int k = G.k[q];
+    const bool fused = mem.size() > 1;
+    if (!fused && k == 1) continue;
+    int64_t bytes = 0;
+    for (int i : mem) bytes += B.tensor_bytes[i];
+    if (k < 1)
+      throw std::runtime_error("partition count must be >= 1, got " + std::to_string(k));
+    if (k > bytes)
+      throw std::runtime_error("cannot split " + std::to_string(bytes) + " bytes of " +
+                               gname[q] + " into " + std::to_string(k) + " partitions");
+    for (int i : mem)
+      for (uint32_t b : B.comm[i]) removed[b] = 1;
+    std::vector<uint32_t> in_ref(B.N, UINT32_MAX), out_ref(B.N, UINT32_MAX);
+    if (fused) {
+      for (int i : mem)
+        for (int w : B.workers) {
+          removed[B.in[i][w]] = 1;
+          removed[B.out[i][w]] = 1;
+        }
+      for (int w : B.workers) {
+        const uint32_t dv = g.device(0, w, -1);
+        in_ref[w] = g.add(B.c.nodes[w] + "->IN." + gname[q], kVin, dv, 0);
+        out_ref[w] = g.add(B.c.nodes[w] + "->OUT." + gname[q], kVout, dv, 0);
+        for (int i : mem) {
+          g.edge(kBaseRef | B.bw[w][i], in_ref[w]);   // every producer feeds IN
+          g.edge(out_ref[w], kBaseRef | B.up[w][i]);  // OUT feeds every consumer
+        }
+      }
+    } else {
+      for (int w : B.workers) {
+        in_ref[w] = kBaseRef | B.in[mem[0]][w];
+        out_ref[w] = kBaseRef | B.out[mem[0]][w];
+      }
+    }
+    const int64_t base = bytes / k, rem = bytes % k;
+    for (int p = 0; p < k; ++p) {
+      const std::string unit = k == 1 ? gname[q] : gname[q] + "#p" + std::to_string(p);
+      expand_unit(g, B.c, unit, base + (p < rem ? 1 : 0), &in_ref, &out_ref);
+    }
+  }
+  const uint32_t nn = static_cast<uint32_t>(g.ops.size());
+  // sort the new ops, then place each among the base ids (binary search)
+  std::vector<uint32_t> snew(nn);
+  std::iota(snew.begin(), snew.end(), 0u);
+  std::sort(snew.begin(), snew.end(),
+            [&](uint32_t a, uint32_t b) { return g.ops[a].id < g.ops[b].id; });
+  std::vector<uint32_t> pos(nn);
+  for (uint32_t j = 0; j < nn; ++j) {
+    const std::string& id = g.ops[snew[j]].id;
+    const auto it = std::lower_bound(bg.ids.begin(), bg.ids.end(), id);
+    if (it != bg.ids.end() && *it == id && !removed[it - bg.ids.begin()])
+      throw std::runtime_error("duplicate op id '" + id + "'");
+    pos[j] = static_cast<uint32_t>(it - bg.ids.begin());
+  }
+  // final order: merge kept base ops with the new ops at their positions
+  std::vector<uint32_t> fb(nb, UINT32_MAX), fnew(nn, UINT32_MAX);
+  auto* out = new dpro_graph;
+  out->base_keep = Bp;
+  out->base_ids = &bg.ids;
+  uint32_t f = 0;
+  {
+    uint32_t j = 0;
+    out->id_ref.reserve(nb + nn);
+    for (uint32_t b = 0; b <= nb; ++b) {
+      for (; j < nn && pos[j] == b; ++j) {
+        fnew[snew[j]] = f++;
+        out->id_ref.push_back(kBaseRef | snew[j]);
+      }
+      if (b < nb && !removed[b]) {
+        fb[b] = f++;
+        out->id_ref.push_back(b);
+      }
+    }
+  }
+  const uint32_t n = f;
+  for (auto& op : g.ops) out->new_ids.push_back(std::move(op.id));
+  // devices: union of the base's and the new ops' devices, DeviceId order
+  std::vector<std::array<int, 3>> udev = B.devs;
+  for (const auto& d : g.devs)
+    if (std::find(udev.begin(), udev.end(), d) == udev.end()) udev.push_back(d);
+  std::sort(udev.begin(), udev.end(),
+            [&](const auto& a, const auto& b) { return dev_less(B.c.nodes, a, b); });
+  if (udev.size() > 65535) {
+    delete out;
+    throw std::runtime_error("more than 65535 devices");
+  }
+  auto dense = [&](const std::array<int, 3>& d) {
+    return static_cast<uint16_t>(std::lower_bound(udev.begin(), udev.end(), d,
+                                                  [&](const auto& a, const auto& b) {
+                                                    return dev_less(B.c.nodes, a, b);
+                                                  }) - udev.begin());
+  };
+  std::vector<uint16_t> bdev(B.devs.size()), ndev(g.devs.size());
+  for (size_t d = 0; d < B.devs.size(); ++d) bdev[d] = dense(B.devs[d]);
+  for (size_t d = 0; d < g.devs.size(); ++d) ndev[d] = dense(g.devs[d]);
+  for (const auto& d : udev) {
+    static const std::string empty;
+    const std::string& a = d[1] < 0 ? empty : B.c.nodes[d[1]];
+    out->device_strs.push_back(d[0] == 0 ? a : a + ">" + B.c.nodes[d[2]]);
+  }
+  out->kind.resize(n);
+  out->dur.resize(n);
+  out->dev.resize(n);
+  out->flags.resize(n);
+  for (uint32_t b = 0; b < nb; ++b) {
+    const uint32_t x = fb[b];
+    if (x == UINT32_MAX) continue;
+    out->kind[x] = bg.kind[b];
+    out->dur[x] = bg.dur[b];
+    out->dev[x] = bdev[bg.dev[b]];
+    out->flags[x] = bg.flags[b];
+  }
+  for (uint32_t j = 0; j < nn; ++j) {
+    const uint32_t x = fnew[j];
+    const auto& op = g.ops[j];
+    out->kind[x] = op.kind;
+    out->dur[x] = op.dur;
+    out->dev[x] = ndev[op.devkey];
+    out->flags[x] = static_cast<uint8_t>(
+        (op.kind == kVin || op.kind == kVout ? DPRO_FLAG_VIRTUAL : 0u) |
+        (op.kind == kSend || op.kind == kRecv ? DPRO_FLAG_COMM : 0u));
+  }
+  // devices whose every op was removed disappear (DeviceId order over the
+  // ops actually present, like a full build)
+  {
+    std::vector<uint16_t> remap(udev.size(), 0xFFFF);
+    for (uint32_t i = 0; i < n; ++i) remap[out->dev[i]] = 0;
+    std::vector<std::string> strs;
+    uint16_t k = 0;
+    for (size_t d = 0; d < udev.size(); ++d)
+      if (remap[d] == 0) {
+        remap[d] = k++;
+        strs.push_back(out->device_strs[d]);
+      }
+    if (k != udev.size()) {
+      for (uint32_t i = 0; i < n; ++i) out->dev[i] = remap[out->dev[i]];
+      out->device_strs = std::move(strs);
+    }
+  }
+  // edges: kept base edges (remapped) + new edges, ascending per source
+  auto fin = [&](uint32_t r) { return (r & kBaseRef) ? fb[r & ~kBaseRef] : fnew[r]; };
+  std::vector<std::pair<uint32_t, uint32_t>> extra;
+  extra.reserve(g.edges.size());
+  for (const auto& e : g.edges) extra.emplace_back(fin(e.first), fin(e.second));
+  std::sort(extra.begin(), extra.end());
+  extra.erase(std::unique(extra.begin(), extra.end()), extra.end());
+  out->succ_off.assign(n + 1, 0);
+  std::vector<uint32_t> bcnt(n, 0);  // kept base successors per op
+  for (uint32_t b = 0; b < nb; ++b) {
+    if (fb[b] == UINT32_MAX) continue;
+    uint32_t cnt = 0;
+    for (uint32_t e = bg.succ_off[b]; e < bg.succ_off[b + 1]; ++e)
+      cnt += fb[bg.succ[e]] != UINT32_MAX;
+    bcnt[fb[b]] = cnt;
+    out->succ_off[fb[b] + 1] = cnt;
+  }
+  for (const auto& e : extra) out->succ_off[e.first + 1]++;
+  for (uint32_t i = 0; i < n; ++i) out->succ_off[i + 1] += out->succ_off[i];
+  out->succ.resize(out->succ_off[n]);
+  std::vector<uint32_t> fill(out->succ_off.begin(), out->succ_off.end() - 1);
+  for (uint32_t b = 0; b < nb; ++b) {
+    const uint32_t x = fb[b];
+    if (x == UINT32_MAX) continue;
+    for (uint32_t e = bg.succ_off[b]; e < bg.succ_off[b + 1]; ++e) {
+      const uint32_t t = fb[bg.succ[e]];
+      if (t != UINT32_MAX) out->succ[fill[x]++] = t;  // ascending: fb is monotone
+    }
+  }
+  for (const auto& e : extra) out->succ[fill[e.first]++] = e.second;  // ascending
+  out->indeg.assign(n, 0);
+  for (uint32_t i = 0; i < n; ++i) {
+    uint32_t* a = out->succ.data() + out->succ_off[i];
+    uint32_t* z = out->succ.data() + out->succ_off[i + 1];
+    if (bcnt[i] && a + bcnt[i] < z) std::inplace_merge(a, a + bcnt[i], z);
+    for (uint32_t* p = a; p < z; ++p) out->indeg[*p]++;
+  }
+  return out;
 }
 
 }  // namespace
@@ -563,7 +878,7 @@ dpro_graph* dpro_graph_tsync(const dpro_cluster_desc* cluster, int64_t bytes,
 
 int dpro_graph_csr(const dpro_graph* g, dpro_csr* out) {
   if (!g || !out) return DPRO_EINVAL;
-  out->n_ops = static_cast<uint32_t>(g->ids.size());
+  out->n_ops = static_cast<uint32_t>(g->kind.size());
   out->n_edges = static_cast<uint32_t>(g->succ.size());
   out->n_devices = static_cast<uint32_t>(g->device_strs.size());
   out->dur_bits = 64;
@@ -577,7 +892,67 @@ int dpro_graph_csr(const dpro_graph* g, dpro_csr* out) {
 }
 
 const char* dpro_graph_op_id(const dpro_graph* g, uint32_t i) {
-  return g->ids.at(i).c_str();
+  if (!g->ids.empty() || !g->base_ids) return g->ids.at(i).c_str();
+  const uint32_t r = g->id_ref.at(i);
+  return (r & kBaseRef) ? g->new_ids.at(r & ~kBaseRef).c_str() : g->base_ids->at(r).c_str();
+}
+
+struct dpro_base {
+  std::shared_ptr<BaseData> b;
+};
+
+dpro_base* dpro_base_layered(const dpro_layered_model* model,
+                             const dpro_cluster_desc* cluster, int32_t* status) {
+  try {
+    auto* out = new dpro_base{build_base(*model, *cluster)};
+    if (status) *status = DPRO_OK;
+    return out;
+  } catch (const std::exception& e) {
+    g_gen_err = e.what();
+    if (status) *status = DPRO_EINVAL;
+    return nullptr;
+  }
+}
+
+void dpro_base_free(dpro_base* b) { delete b; }
+
+int dpro_graph_from_base_batch(const dpro_base* base, int32_t n, const int32_t* n_groups,
+                               const int64_t* spec_off, const int32_t* group_off,
+                               const int32_t* members, const int32_t* group_k,
+                               int32_t threads, dpro_graph** out) {
+  if (!base) return DPRO_EINVAL;
+  if (threads < 1) threads = 1;
+  std::vector<int32_t> st(n, DPRO_OK);
+  std::vector<std::string> errs(threads);
+  std::atomic<int32_t> next{0};
+  auto work = [&](int tid) {
+    for (int32_t i; (i = next.fetch_add(1)) < n;) {
+      try {
+        const int64_t g0 = spec_off[i];
+        Groups G;
+        for (int32_t q = 0; q < n_groups[i]; ++q) {
+          G.members.emplace_back(members + group_off[g0 + q], members + group_off[g0 + q + 1]);
+          G.k.push_back(group_k ? group_k[g0 + q] : 1);
+        }
+        out[i] = build_delta(base->b, G);
+      } catch (const std::exception& e) {
+        out[i] = nullptr;
+        st[i] = DPRO_EINVAL;
+        errs[tid] = e.what();
+      }
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < threads; ++t) pool.emplace_back(work, t);
+  work(0);
+  for (auto& th : pool) th.join();
+  for (int32_t i = 0; i < n; ++i)
+    if (st[i] != DPRO_OK) {
+      for (auto& e : errs)
+        if (!e.empty()) g_gen_err = e;
+      return st[i];
+    }
+  return DPRO_OK;
 }
 int32_t dpro_graph_op_kind(const dpro_graph* g, uint32_t i) { return g->kind.at(i); }
 const char* dpro_graph_device_str(const dpro_graph* g, uint32_t d) {

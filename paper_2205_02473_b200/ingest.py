@@ -295,6 +295,44 @@ def layered_graphs_groups(model: LayeredModel, cluster: ClusterSpec,
     return [NativeGraph(out[i]) for i in range(n)]
 
 
+class LayeredBase:
+    """Base graph for delta construction (dpro_base_layered)."""
+
+    def __init__(self, model: LayeredModel, cluster: ClusterSpec):
+        self._m = model.struct()
+        self._holder = N.ClusterDescHolder(cluster)
+        st = C.c_int32(0)
+        self.handle = N.lib.dpro_base_layered(C.byref(self._m), C.byref(self._holder.desc),
+                                              C.byref(st))
+        if not self.handle:
+            raise Error(N.lib.dpro_graph_last_error().decode())
+
+    def __del__(self):  # pragma: no cover
+        if getattr(self, "handle", None):
+            N.lib.dpro_base_free(self.handle)
+            self.handle = None
+
+    def candidates(self, specs: Sequence[tuple[Sequence[Sequence[int]], Sequence[int]]],
+                   threads: int = 8) -> list[NativeGraph]:
+        """[(groups, ks), ...] -> graphs by delta construction."""
+        n = len(specs)
+        n_groups = np.array([len(g) for g, _ in specs], np.int32)
+        spec_off = np.zeros(n, np.int64)
+        spec_off[1:] = np.cumsum(n_groups[:-1])
+        sizes = [len(m_) for g, _ in specs for m_ in g]
+        group_off = np.zeros(len(sizes) + 1, np.int32)
+        group_off[1:] = np.cumsum(sizes)
+        members = np.ascontiguousarray([i for g, _ in specs for m_ in g for i in m_], np.int32)
+        ks = np.ascontiguousarray([k for _, kk in specs for k in kk], np.int32)
+        out = (C.c_void_p * n)()
+        rc = N.lib.dpro_graph_from_base_batch(self.handle, n, N.ptr(n_groups), N.ptr(spec_off),
+                                              N.ptr(group_off), N.ptr(members), N.ptr(ks),
+                                              threads, out)
+        if rc != N.DPRO_OK:
+            raise Error(N.lib.dpro_graph_last_error().decode())
+        return [NativeGraph(out[i]) for i in range(n)]
+
+
 def layered_graphs(model: LayeredModel, cluster: ClusterSpec, part_k: np.ndarray,
                    threads: int = 8) -> list[NativeGraph]:
     """Candidate batch: one graph per row of part_k [n, layers]."""

@@ -1,9 +1,11 @@
 """Batched candidate evaluator and search driver over the GPU Replayer.
 
 The reference evaluates one candidate graph per `replay()` call inside its
-greedy Alg. 1 (proj/src/optimize.cpp:1327-1650; gate 1382-1392). Here a
-whole round of candidates is generated as CSR on host threads
-(csrc/dfg_gen.cpp) and replayed in ONE batched launch; across GPUs every
+greedy Alg. 1 (proj/src/optimize.cpp:1327-1650; gate 1382-1392), building
+each through string-keyed GraphBuilder copies. Here a whole round of
+candidates is built as CSR deltas of one base graph on host threads
+(csrc/dfg_gen.cpp, dpro_graph_from_base_batch) and replayed in ONE batched
+launch; across GPUs every
 rank evaluates its own shard and the round's best candidate is agreed on
 with one packed int64 MIN all-reduce (the K4 exchange of DESIGN.md).
 
@@ -28,7 +30,7 @@ import numpy as np
 
 from .engine import Engine, default_engine
 from .graph import ClusterSpec
-from .ingest import LayeredModel, layered_graphs_groups
+from .ingest import LayeredBase, LayeredModel
 from .replay import sync_makespan_grid
 
 
@@ -132,6 +134,7 @@ class SyncSearch:
         self.rng = np.random.default_rng([seed, rank])
         self.dist, self.rank = dist, rank
         L = model.layers
+        self.base = LayeredBase(model, cluster)  # delta construction of candidates
         self.state = SyncState([[i] for i in range(L)], [1] * L)
         self.best = None
         self.log = SearchLog()
@@ -163,8 +166,7 @@ class SyncSearch:
 
     def evaluate(self, states: Sequence[SyncState]) -> np.ndarray:
         """Exact makespans of candidate states: one GPU batch."""
-        graphs = layered_graphs_groups(self.model, self.cluster,
-                                       [(st.groups, st.ks) for st in states], self.threads)
+        graphs = self.base.candidates([(st.groups, st.ks) for st in states], self.threads)
         b = self.engine.batch([g.csr for g in graphs])
         b.replay(want_schedule=False)
         ms, st, *_ = b.results()

@@ -112,3 +112,32 @@ def test_generator_tensor_fusion_matches_reference(ref, scheme, W, S):
     groups = [[1, 2, 3], [5, 0], [4]]
     ng = layered_graph_groups(_model(spec), _cluster(spec), groups, [1, 3, 2])
     _same_csr(rg.export(), ng, rg)
+
+
+@pytest.mark.parametrize("scheme,W,S,L", [("ring", 8, 0, 12), ("ps", 16, 4, 9), ("ring", 11, 0, 6),
+                                          ("ps", 3, 2, 7)])
+def test_delta_construction_equals_full_build(scheme, W, S, L):
+    """Candidates built as base + delta (dpro_graph_from_base_batch) are the
+    exact CSR of a full rebuild (same ids, devices, durations, edges)."""
+    from paper_2205_02473_b200.ingest import LayeredBase, layered_graphs_groups
+    rng = np.random.default_rng(L * 7 + W)
+    model = LayeredModel(rng.integers(10, 900, L).tolist(), rng.integers(10, 900, L).tolist(),
+                         rng.integers(100, 4_000_000, L).tolist(), 5)
+    cluster = synth_cluster(scheme, W, S, 12500.0, 5.0)
+    specs = []
+    for _ in range(24):
+        groups, i = [], 0
+        while i < L:
+            n = int(rng.choice([1, 1, 1, 2, 3]))
+            groups.append(list(range(i, min(L, i + n))))
+            i += n
+        ks = [int(rng.choice([1, 1, 2, 3, 4, 12])) for _ in groups]
+        specs.append((groups, ks))
+    specs.append(([[i] for i in range(L)], [1] * L))  # the base itself
+    full = layered_graphs_groups(model, cluster, specs, threads=4)
+    delta = LayeredBase(model, cluster).candidates(specs, threads=4)
+    for a, b in zip(full, delta):
+        assert a.op_ids() == b.op_ids()
+        assert a.device_strs() == b.device_strs()
+        for k in ("dur", "dev", "flags", "succ_off", "succ", "indeg"):
+            assert np.array_equal(getattr(a.csr, k), getattr(b.csr, k)), k

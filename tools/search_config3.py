@@ -38,10 +38,8 @@ def main():
 
     def timed(states):
         nonlocal t_gen, t_gpu
-        from paper_2205_02473_b200.ingest import layered_graphs_groups
         t0 = time.perf_counter()
-        graphs = layered_graphs_groups(s.model, s.cluster, [(st.groups, st.ks) for st in states],
-                                       threads)
+        graphs = s.base.candidates([(st.groups, st.ks) for st in states], threads)
         t1 = time.perf_counter()
         b = eng.batch([g.csr for g in graphs])
         b.replay(want_schedule=False)
