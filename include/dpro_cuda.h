@@ -145,6 +145,18 @@ int dpro_cuda_batch_scheduled(dpro_ctx* ctx, dpro_batch* b, int32_t cand,
 int dpro_cuda_batch_critical_paths(dpro_ctx* ctx, dpro_batch* b,
                                    uint32_t* paths, int64_t* path_len);
 
+/* estimate_peak_memory (proj/src/memory.cpp:122-167) for every candidate of
+ * the last replay (want_schedule=1), on the schedule already in HBM. Host
+ * inputs, flat in batch order: op_bytes [sum n_ops] output buffer bytes of
+ * each computation op (0: none; the caller resolves output_bytes_for and
+ * raises MissingMetaError), op_node [sum n_ops] dense compute node of each
+ * computation op (-1 for other ops), n_nodes [n_cands], persistent
+ * [sum n_nodes]. Output peak [sum n_nodes]: persistent + max live bytes. */
+int dpro_cuda_batch_peak_memory(dpro_ctx* ctx, dpro_batch* b,
+                                const int64_t* op_bytes, const int32_t* op_node,
+                                const int32_t* n_nodes, const int64_t* persistent,
+                                int64_t* peak);
+
 /* critical_path(exec_graph, result) (replay.cpp:146-226) for ONE graph and
  * a caller-supplied schedule (start/end per op, makespan): the exact
  * reference signature, where the execution graph already contains the

@@ -69,6 +69,8 @@ def ref_lib():
             "ref_critical_path": (_I32, [_P, _P, _P, _P, _P, _P, _P, _P, _P]),
             "ref_execution_graph_edges": (_I64, [_P]),
             "ref_sync_makespan": (_I32, [C.c_char_p, _I64, _I32, _P]),
+            "ref_peak_memory": (_I32, [_P, C.c_char_p, _P, _P]),
+            "ref_peak_node": (C.c_char_p, [_I32]),
             "ref_partial_replay": (_I32, [_P, C.c_char_p, _I32, _P]),
             "ref_tsync_graph": (_P, [C.c_char_p, _I64, _I32, _P]),
             "ref_replay_bench": (_I32, [_P, _I64, _I64, _I32, _P, _P]),
@@ -243,6 +245,14 @@ class RefGraph:
                 "conforming": bool(conf.value),
                 "runs": list(zip(rc[:k].tolist(), rd[:k].tolist(), rl[:k].tolist()))}
 
+    def peak_memory(self, meta: dict) -> dict:
+        """estimate_peak_memory(g, replay(g), meta) -> {node: peak bytes}."""
+        peaks = np.zeros(4096, np.int64)
+        nn = C.c_int32(0)
+        _raise(self.lib, self.lib.ref_peak_memory(self.h, json.dumps(meta).encode(), _ptr(peaks),
+                                                  C.byref(nn)))
+        return {self.lib.ref_peak_node(i).decode(): int(peaks[i]) for i in range(nn.value)}
+
     def exec_edge_count(self) -> int:
         return self.lib.ref_execution_graph_edges(self.h)
 
@@ -250,6 +260,66 @@ class RefGraph:
         out = C.c_int64(0)
         _raise(self.lib, self.lib.ref_partial_replay(self.h, tensor.encode(), k, C.byref(out)))
         return out.value
+
+
+def port_peak_memory(ops, succ, start, end, meta: dict) -> dict:
+    """Restatement of estimate_peak_memory (proj/src/memory.cpp:122-167) and
+    output_bytes_for (memory.cpp:71-119) in plain Python, for checking.
+    ops: [(id, kind, node)] (kind as the OpKind int: FW=0, BW=1, UPDATE=2),
+    succ: successor index lists, start/end: the replayed schedule, meta: the
+    ModelMeta json. Returns {node: peak} or raises KeyError(message) where
+    the reference raises MissingMetaError."""
+    out_b = meta.get("output_bytes", {})
+    pers = meta.get("persistent_bytes", {})
+
+    def local_bytes(local):  # memory.cpp:73-92
+        if out_b.get(local, -1) >= 0:
+            return out_b[local]
+        at = local.rfind("@mb")
+        if at >= 0 and out_b.get(local[:at], -1) >= 0:
+            return (out_b[local[:at]] + 1) // 2
+        if local.startswith("RFW."):
+            return out_b.get("FW." + local[4:], -1)
+        return -1
+
+    def bytes_for(op_id):  # memory.cpp:96-119
+        if op_id in out_b:
+            return out_b[op_id]
+        local = op_id.split("->", 1)[1] if "->" in op_id else op_id
+        v = local_bytes(local)
+        if v >= 0 or "+" not in local:
+            return v
+        parts = [local_bytes(p) for p in local.split("+")]
+        return -1 if min(parts) < 0 else sum(parts)
+
+    comp = lambda k: k in (0, 1, 2)  # noqa: E731  graph.hpp:43-45
+    events: dict[str, list] = {}
+    for i, (oid, kind, node) in enumerate(ops):
+        if not comp(kind):
+            continue
+        events.setdefault(node, [])
+        b = bytes_for(oid)
+        if b < 0:
+            if kind != 2:
+                raise KeyError(f"no output bytes for op {oid}")
+            b = 0
+        if b == 0:
+            continue
+        freed = int(end[i])
+        for s in succ[i]:
+            if comp(ops[s][1]):
+                freed = max(freed, int(end[s]))
+        events[node] += [(int(start[i]), b), (freed, -b)]
+    peak = {}
+    for node in sorted(events):
+        if node not in pers:
+            raise KeyError(f"no persistent bytes for node {node}")
+        live = best = 0
+        for _, d in sorted(events[node]):
+            live += d
+            best = max(best, live)
+        peak[node] = pers[node] + best
+    return peak
 
 
 def ref_sync_makespan(cluster_json: dict, bytes_: int, k: int) -> int:

@@ -27,6 +27,7 @@
 
 #include "dpro/errors.hpp"
 #include "dpro/ingest.hpp"
+#include "dpro/memory.hpp"
 #include "dpro/optimize.hpp"
 #include "dpro/replay.hpp"
 #include "dpro/synth.hpp"
@@ -90,6 +91,9 @@ int guarded(F&& fn) {
   } catch (const TransformError& e) {
     g_err = e.what();
     return 5;
+  } catch (const MissingMetaError& e) {
+    g_err = e.what();
+    return 6;
   } catch (const std::exception& e) {
     return fail(e);
   }
@@ -285,6 +289,27 @@ int64_t ref_execution_graph_edges(void* hv) {
   const ReplayResult r = replay(h->g);
   return static_cast<int64_t>(execution_graph(h->g, r).edge_count());
 }
+
+// estimate_peak_memory(g, replay(g), meta) (memory.cpp:122-167): peaks per
+// compute node in node-name order (the result map's order); names via
+// ref_peak_node(i).
+thread_local std::vector<std::string> g_peak_nodes;
+int32_t ref_peak_memory(void* hv, const char* meta_json, int64_t* peaks, int32_t* n_nodes) {
+  auto* h = static_cast<Handle*>(hv);
+  return guarded([&] {
+    const ModelMeta meta = ModelMeta::from_json(nlohmann::json::parse(meta_json));
+    const auto peak = estimate_peak_memory(h->g, replay(h->g), meta);
+    g_peak_nodes.clear();
+    int32_t k = 0;
+    for (const auto& [node, v] : peak) {
+      if (peaks) peaks[k] = v;
+      g_peak_nodes.push_back(node);
+      ++k;
+    }
+    *n_nodes = k;
+  });
+}
+const char* ref_peak_node(int32_t i) { return g_peak_nodes.at(i).c_str(); }
 
 int32_t ref_sync_makespan(const char* cluster_json, int64_t bytes, int32_t k,
                           int64_t* out) {

@@ -81,6 +81,7 @@ SIGNATURES = {
     "dpro_cuda_batch_timelines": (C.c_int, [_P, _P, _I32, _P, _P, _P]),
     "dpro_cuda_batch_critical_paths": (C.c_int, [_P, _P, _P, _P]),
     "dpro_cuda_batch_scheduled": (C.c_int, [_P, _P, _I32, _P]),
+    "dpro_cuda_batch_peak_memory": (C.c_int, [_P, _P, _P, _P, _P, _P, _P]),
     "dpro_cuda_critical_path": (C.c_int, [_P, C.POINTER(DproCsr), _P, _P, _I64, _P, _P]),
     "dpro_cuda_replay_batch": (C.c_int, [_P, C.POINTER(DproCsr), _I32, _I32, _P, _P, _P, _P, _P]),
     "dpro_cuda_tsync_grid": (C.c_int, [_P, C.POINTER(DproClusterDesc), _P, _P, _I32, _P, _P]),

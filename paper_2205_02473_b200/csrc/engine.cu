@@ -15,7 +15,10 @@
 #include <thread>
 #include <vector>
 
+#include <cub/cub.cuh>
+
 #include "critical_path_kernel.cuh"
+#include "memory_kernel.cuh"
 #include "dpro_cuda.h"
 #include "pack_kernel.cuh"
 #include "replay_fast.cuh"
@@ -777,6 +780,87 @@ int dpro_cuda_batch_critical_paths(dpro_ctx* ctx, dpro_batch* b,
   CU(cudaGetLastError());
   if (paths) CU(cudaMemcpyAsync(paths, d_paths, b->sum_n * 4, cudaMemcpyDeviceToHost, ctx->stream));
   if (path_len) CU(cudaMemcpyAsync(path_len, d_len, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return DPRO_OK;
+}
+
+int dpro_cuda_batch_peak_memory(dpro_ctx* ctx, dpro_batch* b, const int64_t* op_bytes,
+                                const int32_t* op_node, const int32_t* n_nodes,
+                                const int64_t* persistent, int64_t* peak) {
+  if (!ctx || !b || !op_bytes || !op_node || !n_nodes || !persistent || !peak)
+    return DPRO_EINVAL;
+  if (!b->replayed || !b->with_schedule)
+    return set_err(ctx, DPRO_EINVAL, "peak memory needs a replay with want_schedule");
+  CU(cudaSetDevice(ctx->device));
+  const size_t n = b->n, N = b->sum_n;
+  std::vector<unsigned long long> seg0(n);
+  unsigned long long S = 0;
+  for (size_t i = 0; i < n; ++i) {
+    seg0[i] = S;
+    S += static_cast<unsigned long long>(std::max(0, n_nodes[i]));
+  }
+  // event count bound: 2 per op (exact counts come from mem_count_kernel)
+  const size_t s_b = align16(N * 8 + 8), s_n = align16(N * 4 + 4), s_s0 = align16(n * 8 + 8),
+               s_cnt = align16(S * 4 + 4), s_off = align16((S + 1) * 8 + 8),
+               s_ev = align16(2 * N * 8 + 8), s_seg8 = align16(S * 8 + 8);
+  DevBuf buf;
+  size_t cub_tmp = 0, sort_tmp = 0;
+  CU(cub::DeviceScan::ExclusiveSum(nullptr, cub_tmp, (unsigned int*)nullptr,
+                                   (unsigned long long*)nullptr, (int)std::max<unsigned long long>(S + 1, 1)));
+  CU(cub::DeviceSegmentedRadixSort::SortPairs(
+      nullptr, sort_tmp, (const unsigned long long*)nullptr, (unsigned long long*)nullptr,
+      (const long long*)nullptr, (long long*)nullptr, (int64_t)(2 * N), (int64_t)S,
+      (const unsigned long long*)nullptr, (const unsigned long long*)nullptr));
+  const size_t s_tmp = align16(std::max(cub_tmp, sort_tmp) + 16);
+  CU(buf.ensure(s_b + s_n + s_s0 + s_cnt + 2 * s_off + 4 * s_ev + 2 * s_seg8 + s_tmp));
+  size_t o = 0;
+  auto take = [&](size_t bytes) { void* q = buf.as<char>(o); o += bytes; return q; };
+  dpro_k::MemIn M;
+  long long* d_bytes = static_cast<long long*>(take(s_b));
+  int* d_node = static_cast<int*>(take(s_n));
+  unsigned long long* d_seg0 = static_cast<unsigned long long*>(take(s_s0));
+  M.seg_cnt = static_cast<unsigned int*>(take(s_cnt));
+  M.seg_off = static_cast<unsigned long long*>(take(s_off));
+  M.cursor = static_cast<unsigned long long*>(take(s_off));
+  M.keys = static_cast<unsigned long long*>(take(s_ev));
+  unsigned long long* keys_out = static_cast<unsigned long long*>(take(s_ev));
+  M.vals = static_cast<long long*>(take(s_ev));
+  long long* vals_sorted = static_cast<long long*>(take(s_ev));
+  long long* d_pers = static_cast<long long*>(take(s_seg8));
+  long long* d_peak = static_cast<long long*>(take(s_seg8));
+  void* tmp = take(s_tmp);
+  M.bytes = d_bytes;
+  M.node = d_node;
+  M.seg0 = d_seg0;
+  CU(cudaMemcpyAsync(d_bytes, op_bytes, N * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaMemcpyAsync(d_node, op_node, N * 4, cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaMemcpyAsync(d_seg0, seg0.data(), n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  if (S) CU(cudaMemcpyAsync(d_pers, persistent, S * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaMemsetAsync(M.seg_cnt, 0, s_cnt, ctx->stream));
+  const int grid = std::max<int>(1, std::min<int>((int)n, ctx->sm_count * 8));
+  dpro_k::mem_count_kernel<<<grid, 256, 0, ctx->stream>>>(b->desc.as<Cand>(), b->n, M);
+  CU(cudaGetLastError());
+  size_t t1 = cub_tmp;
+  CU(cub::DeviceScan::ExclusiveSum(tmp, t1, M.seg_cnt, M.seg_off, (int)(S + 1), ctx->stream));
+  CU(cudaMemcpyAsync(M.cursor, M.seg_off, S * 8 + 8, cudaMemcpyDeviceToDevice, ctx->stream));
+  dpro_k::mem_fill_kernel<<<grid, 256, 0, ctx->stream>>>(b->desc.as<Cand>(), b->n, b->O, M);
+  CU(cudaGetLastError());
+  unsigned long long total = 0;
+  CU(cudaMemcpyAsync(&total, M.seg_off + S, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  if (total > 0) {
+    size_t t2 = sort_tmp;
+    CU(cub::DeviceSegmentedRadixSort::SortPairs(tmp, t2, M.keys, keys_out, M.vals, vals_sorted,
+                                                (int64_t)total, (int64_t)S, M.seg_off,
+                                                M.seg_off + 1, 0, 64, ctx->stream));
+  }
+  if (S) {
+    const int sg = std::max<int>(1, std::min<int>((int)((S * 32 + 255) / 256), ctx->sm_count * 16));
+    dpro_k::mem_scan_kernel<<<sg, 256, 0, ctx->stream>>>(S, M.seg_off, vals_sorted, d_pers,
+                                                         d_peak);
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(peak, d_peak, S * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  }
   CU(cudaStreamSynchronize(ctx->stream));
   return DPRO_OK;
 }

@@ -38,3 +38,19 @@ class TopologyError(Error):
 
 class EngineError(Error):
     """CUDA / engine failure (no reference counterpart: the reference is CPU)."""
+
+
+class MissingMetaError(Error):
+    """dpro::MissingMetaError (errors.hpp:99-102)."""
+
+
+class ParseError(Error):
+    """dpro::ParseError (errors.hpp:32-38)."""
+
+    def __init__(self, what: str, byte_offset: int):
+        super().__init__(f"{what} (byte offset {byte_offset})")
+        self.byte_offset = byte_offset
+
+
+class IoError(Error):
+    """dpro::IoError (errors.hpp:117-120)."""

@@ -96,3 +96,69 @@ def fuzz_dag(rng: np.random.Generator, max_ops: int = 40, zero_p: float = 0.3,
         if kinds[nm] and not any(b.has_edge(names[order[a]], nm) for a in range(pos)):
             b.add_edge(names[order[int(rng.integers(0, pos))]], nm)
     return b.build()
+
+
+def memory_dag(rng: np.random.Generator, max_ops: int = 30):
+    """Graphs + ModelMeta json for estimate_peak_memory (memory.cpp:122-167):
+    FW/BW/UPDATE ops named like the reference's ingest ("<node>->FW.t3",
+    "@mb1" micro-batch copies, "RFW." recomputation, '+'-fused locals),
+    communication and virtual ops in between, zero durations, and metas
+    that sometimes miss an entry (MissingMetaError / UPDATE -> 0)."""
+    n = int(rng.integers(2, max_ops + 1))
+    nodes = [f"w{i}" for i in range(int(rng.integers(1, 5)))]
+    b = GraphBuilder()
+    ids, locals_ = [], set()
+    for i in range(n):
+        node = nodes[int(rng.integers(0, len(nodes)))]
+        r = rng.random()
+        if r < 0.12 and i > 0:
+            kind = OpKind.VIRTUAL_IN
+            oid, dev, dur = f"{node}->VIN.v{i}", DeviceId.compute(node), 0
+        elif r < 0.24 and len(nodes) > 1:
+            peer = nodes[(nodes.index(node) + 1) % len(nodes)]
+            kind = OpKind.SEND if rng.random() < 0.5 else OpKind.RECV
+            oid, dev = f"{node}->{kind.name}.t{i}", DeviceId.link(node, peer)
+            dur = int(rng.integers(0, 10))
+        else:
+            kind = [OpKind.FW, OpKind.BW, OpKind.UPDATE][int(rng.choice(3, p=[0.45, 0.4, 0.15]))]
+            tag = {OpKind.FW: "FW", OpKind.BW: "BW", OpKind.UPDATE: "UPDATE"}[kind]
+            form = rng.random()
+            if form < 0.15:
+                local = f"{tag}.t{i}@mb{int(rng.integers(0, 2))}"
+                locals_.add(f"{tag}.t{i}")
+            elif form < 0.25 and kind == OpKind.FW:
+                local = f"RFW.t{i}"
+                locals_.add(f"FW.t{i}")
+            elif form < 0.4:
+                local = f"{tag}.t{i}+{tag}.u{i}"
+                locals_.update({f"{tag}.t{i}", f"{tag}.u{i}"})
+            else:
+                local = f"{tag}.t{i}"
+                locals_.add(local)
+            oid, dev = f"{node}->{local}", DeviceId.compute(node)
+            dur = 0 if rng.random() < 0.2 else int(rng.integers(1, 10))
+        ids.append(oid)
+        b.add_op(Op(id=oid, kind=kind, node=node, device=dev, dur=dur))
+    order = rng.permutation(n)
+    ep = float(rng.uniform(0.08, 0.4))
+    for a in range(n):
+        for c in range(a + 1, n):
+            if rng.random() < ep:
+                b.add_edge(ids[order[a]], ids[order[c]])
+    for pos in range(1, n):  # virtual ops get a predecessor (init quirk)
+        nm = ids[order[pos]]
+        if "->VIN." in nm and not any(b.has_edge(ids[order[a]], nm) for a in range(pos)):
+            b.add_edge(ids[order[int(rng.integers(0, pos))]], nm)
+    miss = rng.random() < 0.15
+    out = {}
+    for loc in sorted(locals_):
+        if miss and rng.random() < 0.2:
+            continue
+        out[loc] = int(rng.integers(0, 1000)) if rng.random() < 0.9 else 0
+    for oid in ids:  # a few direct full-id entries win over locals
+        if rng.random() < 0.1:
+            out[oid] = int(rng.integers(0, 5000))
+    pers = {nd: int(rng.integers(0, 10**6)) for nd in nodes
+            if not (rng.random() < 0.05)}
+    meta = {"output_bytes": out, "persistent_bytes": pers, "microbatch_scale": 0.5}
+    return b.build(), meta

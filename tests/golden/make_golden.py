@@ -22,7 +22,7 @@ ROOT = Path(__file__).resolve().parents[2]
 sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tests"))
 
-from dags import acceptance_dag, fuzz_dag, random_dag_ref  # noqa: E402
+from dags import acceptance_dag, fuzz_dag, memory_dag, random_dag_ref  # noqa: E402
 from oracle.oracle import RefError, RefGraph, ref_sync_makespan  # noqa: E402
 from paper_2205_02473_b200.graph import (DeviceId, GraphBuilder, Op, OpKind, comp,  # noqa: E402
                                          synth_cluster)
@@ -236,5 +236,88 @@ def main():
     print(f"{len(vectors)} replay vectors, {len(tsync)} t_sync vectors, {len(synth)} synth vectors")
 
 
+def memory_cases():
+    """proj/tests/test_memory.cpp cases (graph, meta)."""
+    cases = {}
+    b = GraphBuilder()  # test_memory.cpp:58-70
+    b.add_op(comp("w0->FW.a", "w0", 10)); b.add_op(comp("w0->FW.b", "w0", 10))
+    b.add_edge("w0->FW.a", "w0->FW.b")
+    cases["chained"] = (b.build(), {"output_bytes": {"FW.a": 10, "FW.b": 10},
+                                    "persistent_bytes": {"w0": 100}})
+    b = GraphBuilder()  # 72-79
+    b.add_op(comp("w0->UPDATE.a", "w0", 5, OpKind.UPDATE))
+    cases["persistent_only"] = (b.build(), {"persistent_bytes": {"w0": 77}})
+    b = GraphBuilder()  # 81-94
+    for n, t in [("a", 4), ("b", 4), ("c", 2)]:
+        b.add_op(comp(f"w0->FW.{n}", "w0", t))
+    b.add_edge("w0->FW.a", "w0->FW.c"); b.add_edge("w0->FW.b", "w0->FW.c")
+    cases["fan_in"] = (b.build(), {"output_bytes": {"FW.a": 10, "FW.b": 10, "FW.c": 0},
+                                   "persistent_bytes": {"w0": 100}})
+    b = GraphBuilder()  # 96-108
+    b.add_op(comp("w0->FW.a", "w0", 4))
+    g = b.build()
+    cases["missing_sizes"] = (g, {"persistent_bytes": {"w0": 1}})
+    cases["missing_persistent"] = (g, {"output_bytes": {"FW.a": 10}})
+    b = GraphBuilder()  # 110-128
+    for n in "abcd":
+        b.add_op(comp(f"w0->FW.{n}", "w0", 2))
+    for x, y in [("a", "b"), ("a", "d"), ("b", "c"), ("c", "d")]:
+        b.add_edge(f"w0->FW.{x}", f"w0->FW.{y}")
+    cases["last_consumer"] = (b.build(), {"output_bytes": {"FW.a": 8, "FW.b": 2, "FW.c": 2,
+                                                           "FW.d": 0},
+                                          "persistent_bytes": {"w0": 0}})
+    return cases
+
+
+def memory_expect(g, meta):
+    try:
+        return {"status": 0, "peak": RefGraph.from_dfg(g).peak_memory(meta)}
+    except RefError as err:
+        return {"status": err.status, "message": err.msg}
+
+
+def memory_main():
+    """estimate_peak_memory vectors: test_memory.cpp cases, random
+    memory_dag graphs, ingest-built layered graphs (with partitions)."""
+    vecs = []
+    for name, (g, meta) in memory_cases().items():
+        vecs.append({"name": name, "graph": g_to_json(g), "meta": meta,
+                     "expect": memory_expect(g, meta)})
+    rng = np.random.default_rng(20261018)
+    for t in range(300):
+        g, meta = memory_dag(rng)
+        vecs.append({"name": f"memory_dag_{t}", "graph": g_to_json(g), "meta": meta,
+                     "expect": memory_expect(g, meta)})
+    layered = []
+    srng = np.random.default_rng(11)
+    for scheme, W, S, L in [("ring", 4, 0, 6), ("ps", 3, 2, 6), ("ring", 8, 0, 12),
+                            ("ps", 16, 4, 5)]:
+        spec = {"layers": L, "fw_dur_us": srng.integers(10, 400, L).tolist(),
+                "bw_dur_us": srng.integers(10, 800, L).tolist(),
+                "tensor_bytes": srng.integers(1000, 4_000_000, L).tolist(),
+                "update_dur_us": 5, "scheme": scheme, "workers": W, "ps_count": S,
+                "bandwidth_bytes_per_us": 12500.0, "latency_us": 5.0}
+        act = srng.integers(1, 1 << 24, L).tolist()
+        meta = {"output_bytes": {**{f"FW.l{i}": act[i] for i in range(L)},
+                                 **{f"BW.l{i}": act[i] // 2 for i in range(L)}},
+                "persistent_bytes": {}}
+        for variant in range(2):
+            k = [1] * L if variant == 0 else srng.choice([1, 2, 3, 4], L).tolist()
+            rg = RefGraph.synth(spec)
+            for i, ki in enumerate(k):
+                rg = rg.partition(f"g{i}", int(ki))
+            nodes = sorted({d.split("->")[0] for d in rg.op_ids() if "->" in d})
+            meta["persistent_bytes"] = {nd: 4 * sum(spec["tensor_bytes"]) for nd in nodes}
+            layered.append({"spec": spec, "part_k": [int(x) for x in k], "meta": dict(meta),
+                            "peak": rg.peak_memory(meta)})
+    (OUT / "memory_vectors.json").write_text(json.dumps({"graphs": vecs, "layered": layered},
+                                                        separators=(",", ":")))
+    print(f"{len(vecs)} memory vectors, {len(layered)} layered memory vectors")
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["memory"]:
+        memory_main()
+    else:
+        main()
+        memory_main()
