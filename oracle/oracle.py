@@ -71,6 +71,8 @@ def ref_lib():
             "ref_sync_makespan": (_I32, [C.c_char_p, _I64, _I32, _P]),
             "ref_peak_memory": (_I32, [_P, C.c_char_p, _P, _P]),
             "ref_peak_node": (C.c_char_p, [_I32]),
+            "ref_apply_memory_strategy": (_P, [_P, _I32, C.c_char_p, _P]),
+            "ref_memory_pass": (_P, [_P, _I64, C.c_char_p, _P, _P, _P, _P]),
             "ref_partial_replay": (_I32, [_P, C.c_char_p, _I32, _P]),
             "ref_tsync_graph": (_P, [C.c_char_p, _I64, _I32, _P]),
             "ref_replay_bench": (_I32, [_P, _I64, _I64, _I32, _P, _P]),
@@ -167,6 +169,27 @@ class RefGraph:
         h = self.lib.ref_apply_tensor_fusion(self.h, t1.encode(), t2.encode(), C.byref(st))
         _raise(self.lib, st.value)
         return RefGraph(h)
+
+    def apply_memory_strategy(self, kind: int, meta: dict) -> "RefGraph":
+        """apply_strategy(kRecompute=3 | kGradAccum=4)."""
+        st = C.c_int32(0)
+        h = self.lib.ref_apply_memory_strategy(self.h, kind, json.dumps(meta).encode(),
+                                               C.byref(st))
+        _raise(self.lib, st.value)
+        return RefGraph(h)
+
+    def memory_pass(self, budget: int, meta: dict):
+        """-> (graph, applied kind or -1, k); RefError status 7 carries
+        best_peak in .best_peak."""
+        st, kind, k, best = C.c_int32(0), C.c_int32(-1), C.c_int32(0), C.c_int64(0)
+        h = self.lib.ref_memory_pass(self.h, budget, json.dumps(meta).encode(), C.byref(st),
+                                     C.byref(kind), C.byref(k), C.byref(best))
+        try:
+            _raise(self.lib, st.value)
+        except RefError as e:
+            e.best_peak = best.value
+            raise
+        return RefGraph(h), kind.value, k.value
 
     def with_durations(self, dur: np.ndarray) -> "RefGraph":
         st = C.c_int32(0)

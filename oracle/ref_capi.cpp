@@ -94,6 +94,9 @@ int guarded(F&& fn) {
   } catch (const MissingMetaError& e) {
     g_err = e.what();
     return 6;
+  } catch (const BudgetError& e) {
+    g_err = e.what();
+    return 7;
   } catch (const std::exception& e) {
     return fail(e);
   }
@@ -170,6 +173,43 @@ void* ref_apply_op_fusion(void* h, const char* a, const char* b,
     CostModel cost;
     out = wrap(apply_op_fusion(static_cast<Handle*>(h)->g, a, b, cost,
                                dur_override));
+  });
+  return out;
+}
+
+// apply_strategy for the parameterless memory rewrites (kind 3 recompute,
+// 4 grad-accum), optimize.cpp:506-531.
+void* ref_apply_memory_strategy(void* h, int32_t kind, const char* meta_json,
+                                int32_t* status) {
+  Handle* out = nullptr;
+  *status = guarded([&] {
+    const ModelMeta meta = ModelMeta::from_json(nlohmann::json::parse(meta_json));
+    Strategy st;
+    st.kind = static_cast<StrategyKind>(kind);
+    out = wrap(apply_strategy(static_cast<Handle*>(h)->g, st, CostModel{}, meta));
+  });
+  return out;
+}
+
+// memory_pass (optimize.cpp:972-1021): the returned graph, the applied
+// strategy kind (-1 none) and k, or status 7 with best_peak (BudgetError).
+void* ref_memory_pass(void* h, int64_t budget, const char* meta_json, int32_t* status,
+                      int32_t* applied_kind, int32_t* applied_k, int64_t* best_peak) {
+  Handle* out = nullptr;
+  *applied_kind = -1;
+  *status = guarded([&] {
+    const ModelMeta meta = ModelMeta::from_json(nlohmann::json::parse(meta_json));
+    std::vector<Strategy> applied;
+    try {
+      out = wrap(memory_pass(static_cast<Handle*>(h)->g, budget, meta, &applied));
+    } catch (const BudgetError& e) {
+      *best_peak = e.best_peak_bytes;
+      throw;
+    }
+    if (!applied.empty()) {
+      *applied_kind = static_cast<int32_t>(applied[0].kind);
+      *applied_k = applied[0].k;
+    }
   });
   return out;
 }

@@ -7,12 +7,14 @@ no CPU fallback -- importing this package fails if the library is missing.
 from . import _native  # noqa: F401  (fails loudly without libdpro_cuda.so)
 from .engine import Batch, Csr, Engine, default_engine
 from .errors import (CycleError, EngineError, Error, IoError, LookupError_, MissingMetaError,
-                     MissingProfileError, ParseError)
+                     MissingProfileError, ParseError, TopologyError, TransformError)
 from .graph import (ClusterSpec, DeviceId, DeviceKind, GlobalDFG, GraphBuilder, LinkSpec,
                     NodeSpec, Op, OpKind, TensorUnit, comp, round_us, synth_cluster)
 from .replay import (CriticalPath, PathEntry, PathRun, ReplayResult, ScheduleEntry,
                      critical_path, execution_graph, partial_replay, replay, replay_many,
                      sync_makespan, sync_makespan_grid)
+from .rewrite import (BudgetError, Strategy, StrategyKind, apply_grad_accum, apply_recompute,
+                      memory_pass)
 from .memory import (ModelMeta, estimate_peak_memory, estimate_peak_memory_many,
                      output_bytes_for)
 
@@ -24,5 +26,7 @@ __all__ = [
     "ReplayResult", "ScheduleEntry", "critical_path", "execution_graph", "partial_replay",
     "replay", "replay_many", "sync_makespan", "sync_makespan_grid", "IoError",
     "MissingMetaError", "ParseError", "ModelMeta", "estimate_peak_memory",
-    "estimate_peak_memory_many", "output_bytes_for",
+    "estimate_peak_memory_many", "output_bytes_for", "TopologyError", "TransformError",
+    "BudgetError", "Strategy", "StrategyKind", "apply_grad_accum", "apply_recompute",
+    "memory_pass",
 ]

@@ -353,3 +353,42 @@ def tsync_graph(cluster: ClusterSpec, bytes_: int, k: int) -> NativeGraph:
     st = C.c_int32(0)
     return NativeGraph(N.lib.dpro_graph_tsync(C.byref(holder.desc), int(bytes_), int(k),
                                               C.byref(st)))
+
+
+def layered_global_dfg(model: LayeredModel, cluster: ClusterSpec,
+                       part_k: Sequence[int] | None = None) -> GlobalDFG:
+    """The same layered graph as layered_graph(), built op by op through
+    GraphBuilder with full Op fields and tensor units (synth.cpp:200-217 deps
+    through build_local_dfg + assemble_global_dfg, ingest.cpp:243-265,
+    404-441). Small models only: the graph rewrites of rewrite.py and the
+    reference-shaped API take this form; the search uses the native one."""
+    b = GraphBuilder()
+    b.set_cluster(cluster)
+    L = model.layers
+    for w in cluster.workers():
+        dv = DeviceId.compute(w)
+        for i in range(L):
+            b.add_op(Op(f"{w}->FW.l{i}", OpKind.FW, w, dv, int(model.fw_dur[i])))
+            b.add_op(Op(f"{w}->BW.l{i}", OpKind.BW, w, dv, int(model.bw_dur[i]),
+                        produces=[f"g{i}"]))
+            b.add_op(Op(f"{w}->UPDATE.l{i}", OpKind.UPDATE, w, dv, int(model.update_dur)))
+            b.add_op(Op(f"{w}->IN.g{i}", OpKind.VIRTUAL_IN, w, dv, 0))
+            b.add_op(Op(f"{w}->OUT.g{i}", OpKind.VIRTUAL_OUT, w, dv, 0))
+        for i in range(L):
+            if i > 0:
+                b.add_edge(f"{w}->FW.l{i - 1}", f"{w}->FW.l{i}")
+            if i + 1 < L:
+                b.add_edge(f"{w}->BW.l{i + 1}", f"{w}->BW.l{i}")
+            b.add_edge(f"{w}->FW.l{i}", f"{w}->BW.l{i}")
+            b.add_edge(f"{w}->BW.l{i}", f"{w}->IN.g{i}")
+            b.add_edge(f"{w}->OUT.g{i}", f"{w}->UPDATE.l{i}")
+    for i in range(L):
+        k = int(part_k[i]) if part_k is not None else 1
+        nbytes = int(model.tensor_bytes[i])
+        base, rem = divmod(nbytes, k)
+        for p in range(k):
+            unit = f"g{i}" if k == 1 else f"g{i}#p{p}"
+            topo = expand_tensor(unit, base + (1 if p < rem else 0), cluster)
+            topo.part_index, topo.part_count = p, k
+            splice(b, topo, f"g{i}")
+    return b.build()

@@ -162,3 +162,37 @@ def memory_dag(rng: np.random.Generator, max_ops: int = 30):
             if not (rng.random() < 0.05)}
     meta = {"output_bytes": out, "persistent_bytes": pers, "microbatch_scale": 0.5}
     return b.build(), meta
+
+
+def rewrite_dag(rng: np.random.Generator):
+    """Valid graphs for the memory rewrites (optimize.cpp:819-959): per node
+    an FW chain, a mirrored BW chain, FW.l_i -> BW.l_i, UPDATE ops after
+    their BW, plus random extra FW->BW / BW->UPDATE edges and cross-node
+    edges; no comm or virtual ops (validate() would need tensor units)."""
+    b = GraphBuilder()
+    nodes = [f"w{i}" for i in range(int(rng.integers(1, 4)))]
+    for nd in nodes:
+        L = int(rng.integers(1, 11))
+        for i in range(L):
+            b.add_op(Op(f"{nd}->FW.l{i}", OpKind.FW, nd, DeviceId.compute(nd),
+                        int(rng.integers(0, 50))))
+            b.add_op(Op(f"{nd}->BW.l{i}", OpKind.BW, nd, DeviceId.compute(nd),
+                        int(rng.integers(0, 80))))
+            if rng.random() < 0.6:
+                b.add_op(Op(f"{nd}->UPDATE.l{i}", OpKind.UPDATE, nd, DeviceId.compute(nd),
+                            int(rng.integers(0, 9))))
+                b.add_edge(f"{nd}->BW.l{i}", f"{nd}->UPDATE.l{i}")
+        for i in range(L):
+            if i > 0:
+                b.add_edge(f"{nd}->FW.l{i - 1}", f"{nd}->FW.l{i}")
+            if i + 1 < L:
+                b.add_edge(f"{nd}->BW.l{i + 1}", f"{nd}->BW.l{i}")
+            b.add_edge(f"{nd}->FW.l{i}", f"{nd}->BW.l{i}")
+            for j in range(i + 1, L):  # skip connections used by later backward ops
+                if rng.random() < 0.03:
+                    b.add_edge(f"{nd}->FW.l{i}", f"{nd}->BW.l{j}")
+        if len(nodes) > 1 and rng.random() < 0.5:  # a cross-node dependency
+            other = nodes[(nodes.index(nd) + 1) % len(nodes)]
+            if b.has_op(f"{other}->BW.l0") and not b.has_edge(f"{other}->BW.l0", f"{nd}->FW.l0"):
+                b.add_edge(f"{nd}->FW.l0", f"{other}->BW.l0")
+    return b.build()

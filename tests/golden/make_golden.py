@@ -22,7 +22,8 @@ ROOT = Path(__file__).resolve().parents[2]
 sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tests"))
 
-from dags import acceptance_dag, fuzz_dag, memory_dag, random_dag_ref  # noqa: E402
+from dags import acceptance_dag, fuzz_dag, memory_dag, random_dag_ref, rewrite_dag  # noqa: E402
+from golden_io import rows_digest  # noqa: E402
 from oracle.oracle import RefError, RefGraph, ref_sync_makespan  # noqa: E402
 from paper_2205_02473_b200.graph import (DeviceId, GraphBuilder, Op, OpKind, comp,  # noqa: E402
                                          synth_cluster)
@@ -315,9 +316,83 @@ def memory_main():
     print(f"{len(vecs)} memory vectors, {len(layered)} layered memory vectors")
 
 
+def ref_rows(rg):
+    ex = rg.export()
+    ids, ds = rg.op_ids(), rg.device_strs()
+    so, su = ex["succ_off"], ex["succ"]
+    return [(ids[i], int(ex["kind"][i]), ds[int(ex["dev"][i])], int(ex["dur"][i]),
+             [ids[s] for s in su[so[i]:so[i + 1]]]) for i in range(len(ids))]
+
+
+def _max_peak(rg, meta):
+    return max(rg.peak_memory(meta).values(), default=0)
+
+
+def rewrite_main():
+    """apply_strategy(recompute | grad-accum) and memory_pass vectors
+    (optimize.cpp:506-531, 819-1021) on layered synth graphs and random
+    rewrite_dag graphs; rewritten graphs are pinned by a digest of their
+    (id, kind, device, dur, successors) rows."""
+    out = {"sources": [], "apply": [], "memory_pass": []}
+    srng = np.random.default_rng(29)
+    sources = []
+    for scheme, W, S, L in [("ring", 4, 0, 6), ("ps", 3, 2, 9), ("ring", 8, 0, 16),
+                            ("ring", 2, 0, 1), ("ps", 4, 1, 25)]:
+        spec = {"layers": L, "fw_dur_us": srng.integers(10, 400, L).tolist(),
+                "bw_dur_us": srng.integers(10, 800, L).tolist(),
+                "tensor_bytes": srng.integers(1000, 4_000_000, L).tolist(),
+                "update_dur_us": 5, "scheme": scheme, "workers": W, "ps_count": S,
+                "bandwidth_bytes_per_us": 12500.0, "latency_us": 5.0}
+        rg = RefGraph.synth(spec)
+        act = srng.integers(1, 1 << 26, L).tolist()
+        meta = {"output_bytes": {**{f"FW.l{i}": act[i] for i in range(L)},
+                                 **{f"BW.l{i}": spec["tensor_bytes"][i] for i in range(L)}},
+                "persistent_bytes": {f"w{i}": sum(spec["tensor_bytes"]) for i in range(W)},
+                "microbatch_scale": float(srng.choice([0.5, 0.37]))}
+        sources.append(({"synth": spec}, rg, meta))
+    rng = np.random.default_rng(31)
+    for t in range(120):
+        g = rewrite_dag(rng)
+        meta = {"output_bytes": {f"{k}.l{i}": int(rng.integers(0, 1 << 20))
+                                 for k in ("FW", "BW") for i in range(10)},
+                "persistent_bytes": {f"w{i}": int(rng.integers(0, 1 << 20)) for i in range(3)},
+                "microbatch_scale": float(rng.choice([0.5, 0.25, 0.37]))}
+        sources.append(({"graph": g_to_json(g)}, RefGraph.from_dfg(g), meta))
+    for si, (src, rg, meta) in enumerate(sources):
+        out["sources"].append({**src, "meta": meta})
+        for kind in (3, 4):
+            try:
+                res = {"status": 0, "digest": rows_digest(ref_rows(rg.apply_memory_strategy(kind, meta)))}
+            except RefError as err:
+                res = {"status": err.status, "message": err.msg}
+            out["apply"].append({"src": si, "kind": kind, "expect": res})
+        base = _max_peak(rg, meta)
+        peaks = []
+        for kind in (3, 4):
+            try:
+                peaks.append(_max_peak(rg.apply_memory_strategy(kind, meta), meta))
+            except RefError:
+                pass
+        budgets = sorted({0, base, base + 1, max(1, base - 1)} |
+                         {p for p in peaks} | {max(1, min(peaks + [base]) - 1)})
+        for budget in budgets:
+            try:
+                g2, kind, k = rg.memory_pass(budget, meta)
+                res = {"status": 0, "kind": kind, "k": k, "digest": rows_digest(ref_rows(g2))}
+            except RefError as err:
+                res = {"status": err.status, "message": err.msg,
+                       "best_peak": getattr(err, "best_peak", None)}
+            out["memory_pass"].append({"src": si, "budget": int(budget), "expect": res})
+    (OUT / "rewrite_vectors.json").write_text(json.dumps(out, separators=(",", ":")))
+    print(f"{len(out['apply'])} rewrite vectors, {len(out['memory_pass'])} memory_pass vectors")
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["memory"]:
         memory_main()
+    elif sys.argv[1:] == ["rewrite"]:
+        rewrite_main()
     else:
         main()
         memory_main()
+        rewrite_main()

@@ -42,3 +42,23 @@ def tl_pos_from(order, dev_off, n):
         for p in range(a, b):
             tl[int(order[p])] = p - a
     return tl
+
+
+def rows_digest(rows) -> str:
+    """sha256 over (id, kind, device, dur, successor ids) rows in index order."""
+    import hashlib
+    h = hashlib.sha256()
+    for oid, kind, dev, dur, succ in rows:
+        h.update(f"{oid}|{kind}|{dev}|{dur}|{','.join(succ)}\n".encode())
+    return h.hexdigest()
+
+
+def dfg_rows(g):
+    c = g.to_csr()
+    ds = [d.str() for d in c["devices"]]
+    return [(o.id, int(o.kind), ds[int(c["dev"][i])], int(o.dur),
+             [g.op_at(s).id for s in g.succ_indices(i)]) for i, o in enumerate(g.ops())]
+
+
+def rewrite_vectors():
+    return json.loads((GOLDEN / "rewrite_vectors.json").read_text())
