@@ -6,10 +6,13 @@
 Workload (N=1 line = BASELINE configs[1]): BERT-base parameter-server DFG,
 16 workers / 4 servers, 199 tensors, a batch of 1024 candidate graphs (each
 re-partitions 8 seeded tensors with k in {1,2,4}, the reference's
-apply_tensor_partition rewrite). One step = one exact replay of every
-candidate (K1: per-op start/end + makespan) followed by the per-round
-best-cost exchange (argmin; NCCL MIN all-reduce across ranks when N > 1).
-Inputs (1.27 GB of CSR) are larger than L2, so no flush is needed.
+apply_tensor_partition rewrite). Candidates are deltas of
+one resident base graph (include/dpro_cuda.h dpro_delta). One step = the
+device-side merge of every delta (K0) + the pack kernel + one exact replay
+of every candidate (K1: per-op start/end + makespan) + the per-round
+best-cost exchange (argmin; NCCL MIN all-reduce across ranks when N > 1),
+with the inputs (base graph + deltas) resident in HBM. The per-step working
+set (merged CSR + packed records, ~3.9 GB) is larger than L2: no flush.
 
 Multi-GPU: one process per GPU (torchrun), each rank replays its own 1024
 candidates (weak scaling); timing is the max over ranks of CUDA-event time.
@@ -182,6 +185,8 @@ def run_reference(args) -> None:
 
 
 def run_ours(args) -> None:
+    import ctypes as C
+
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -193,18 +198,24 @@ def run_ours(args) -> None:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2205_02473_b200 import _native as N
     from paper_2205_02473_b200.engine import Engine
+    from paper_2205_02473_b200.ingest import LayeredBase
+    from paper_2205_02473_b200.workloads import workload
 
     threads = max(1, (os.cpu_count() or 8) // max(world, 1))
+    w = workload(args.config)
+    pk = w.candidate_partitions(args.batch, rank=rank)
+    specs = [([[i] for i in range(w.layers)], pk[c].tolist()) for c in range(args.batch)]
     t0 = time.perf_counter()
-    w, graphs = build_candidates(args.config, args.batch, rank, threads)
+    base = LayeredBase(w.model, w.cluster)
+    deltas = base.deltas(specs, threads=threads)  # candidates as deltas of the base
     t_build = time.perf_counter() - t0
     stream = torch.cuda.current_stream()
     eng = Engine(local)
     eng.set_stream(stream.cuda_stream)
-    batch = eng.batch([g.csr for g in graphs])  # uploaded once: resident in HBM
+    resident = eng.resident(base.graph().csr)  # base graph: uploaded once, stays in HBM
+    batch = eng.delta_batch(resident, deltas)   # deltas uploaded once: inputs in HBM
     algo_bytes = batch.algorithmic_bytes()
     B = batch.n
-    # zero-copy torch view of the engine's device makespan buffer
     mk_view = _device_view(batch.device_results()["makespan"], B, local)
 
     def exchange():
@@ -217,7 +228,8 @@ def run_ours(args) -> None:
         return key
 
     def step():
-        batch.replay(want_schedule=True)
+        batch.prepare()                    # K0 delta merge + pack kernel
+        batch.replay(want_schedule=True)   # K1 replay: makespan + per-op start/end
         return exchange()
 
     for _ in range(args.warmup):
@@ -225,23 +237,21 @@ def run_ours(args) -> None:
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    mids = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
-        t_wall = time.perf_counter()
         for i in range(args.steps):
-            starts[i].record(stream)
+            ev[i][0].record(stream)
+            batch.prepare()
+            ev[i][1].record(stream)
             batch.replay(want_schedule=True)
-            mids[i].record(stream)
+            ev[i][2].record(stream)
             exchange()
-            ends[i].record(stream)
+            ev[i][3].record(stream)
         torch.cuda.synchronize()
-        t_wall = time.perf_counter() - t_wall
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    kern_ms = [s.elapsed_time(m) for s, m in zip(starts, mids)]
-    total_ms = starts[0].elapsed_time(ends[-1])
+    prep_ms = [e[0].elapsed_time(e[1]) for e in ev]
+    kern_ms = [e[1].elapsed_time(e[2]) for e in ev]
+    total_ms = ev[0][0].elapsed_time(ev[-1][3])
     if dist is not None:
         t = torch.tensor([total_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -250,33 +260,44 @@ def run_ours(args) -> None:
     ok = int((st == 0).sum())
     kstats = batch.stats()
 
-    # e2e: the C-ABI one-shot call with HOST buffers (H2D upload of every
-    # candidate + D2H of makespans/status/err inside the timed region)
-    import ctypes as C
-    structs = [g.csr.as_struct() for g in graphs]
-    arr = (N.DproCsr * B)(*structs)
+    # e2e through the C ABI with HOST buffers: the search's call
+    # (dpro_cuda_replay_delta_batch: H2D of the deltas, merge, pack, replay,
+    # D2H of makespan/status/err), and for reference the full-CSR call
+    # (dpro_cuda_replay_batch: H2D of every candidate's CSR)
     hm = np.zeros(B, np.int64)
     hs = np.zeros(B, np.int32)
     he = np.zeros(B, np.int64)
-    e2e_times = []
-    for i in range(max(2, min(args.steps, 5)) + 1):
-        torch.cuda.synchronize()
+
+    def timed(fn):
+        out = []
+        for i in range(max(2, min(args.steps, 5)) + 1):
+            torch.cuda.synchronize()
+            if dist is not None:
+                dist.barrier()
+            t0 = time.perf_counter()
+            assert fn() == 0
+            el = time.perf_counter() - t0
+            if i > 0:
+                out.append(el)
+        e = float(np.median(out))
         if dist is not None:
-            dist.barrier()
-        t0 = time.perf_counter()
-        rc = N.lib.dpro_cuda_replay_batch(eng.ctx, arr, B, N.DPRO_HOST, N.ptr(hm), None, None,
-                                          N.ptr(hs), N.ptr(he))
-        el = time.perf_counter() - t0
-        assert rc == 0
-        if i > 0:
-            e2e_times.append(el)
-    e2e_s = float(np.median(e2e_times))
-    if dist is not None:
-        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+            t = torch.tensor([e], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e = float(t.item())
+        return e
+
+    e2e_s = timed(lambda: N.lib.dpro_cuda_replay_delta_batch(
+        eng.ctx, resident.handle, C.cast(deltas.array, C.c_void_p), B, N.ptr(hm), N.ptr(hs),
+        N.ptr(he)))
     assert np.array_equal(hm, ms), "e2e makespans differ from the device-resident run"
-    h2d = int(sum(_packed_bytes(g) for g in graphs))
+    graphs = base.candidates(specs, threads=threads)  # host-merged full CSRs
+    arr = (N.DproCsr * B)(*[g.csr.as_struct() for g in graphs])
+    hm2 = np.zeros(B, np.int64)
+    full_s = timed(lambda: N.lib.dpro_cuda_replay_batch(eng.ctx, arr, B, N.DPRO_HOST,
+                                                        N.ptr(hm2), None, None, N.ptr(hs),
+                                                        N.ptr(he)))
+    assert np.array_equal(hm2, ms), "full-CSR makespans differ from the delta run"
+    h2d = int(sum(_delta_bytes(deltas[i]) for i in range(B)))
     d2h = B * (8 + 4 + 8)
 
     if rank != 0:
@@ -301,27 +322,46 @@ def run_ours(args) -> None:
                    "global_batch": B * world, "n_ops_mean": float(batch.n_ops.mean()),
                    "n_edges_mean": float(batch.n_edges.mean()),
                    "parallelism": f"candidates sharded over {world} GPU(s)",
-                   "l2": "inputs (%.2f GB CSR) larger than L2; no flush" % (algo_bytes / 1e9),
+                   "step": "delta merge (K0) + pack + replay (K1, per-op start/end) + "
+                           "best-cost exchange, inputs (base graph + deltas) resident in HBM",
+                   "l2": "per-step working set (%.2f GB of merged CSR + packed records) "
+                         "larger than L2; no flush" % (algo_bytes * 3 / 1e9),
                    "node_updates_per_s": value * float(batch.n_ops.mean()),
+                   "prepare_ms_mean": float(np.mean(prep_ms)),
+                   "replay_ms_mean": kmean * 1e3,
+                   "replay_only_per_s": world * B / kmean,
                    "build_s": round(t_build, 2), "status_ok": ok,
                    "kernel": "replay_fast_kernel (general-path fallbacks: %d)" % kstats["fallbacks"],
                    "fast_smem_bytes_per_candidate": kstats["fast_smem_bytes"],
                    "fast_candidates_per_sm": kstats["fast_blocks_per_sm"]},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": _ncu_traffic(),
+                     "kernel": "replay_fast_kernel",
                      "algorithmic_bytes_per_launch": algo_bytes, "peak_source": peak_src,
                      "kernel_ms_mean": kmean * 1e3},
         "cpu_baseline": cpu,
         "e2e": {"value": world * B / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
-                "note": "dpro_cuda_replay_batch with host CSR (pack + H2D + replay, "
-                        "makespan-only) per step"},
-        "gpu_launches": args.steps,
+                "note": "dpro_cuda_replay_delta_batch with host deltas (H2D + merge + pack + "
+                        "replay, makespan-only) per step",
+                "full_csr": {"value": world * B / full_s,
+                             "h2d_bytes_per_step": int(sum(_packed_bytes(g) for g in graphs)),
+                             "note": "dpro_cuda_replay_batch with every candidate's host CSR"}},
+        "gpu_launches": 3 * args.steps,
         "clocks": clocks,
     }
     print(json.dumps(line))
     if dist is not None:
         dist.destroy_process_group()
+
+
+def _delta_bytes(d) -> int:
+    import ctypes as C
+    a = lambda x: (x + 15) & ~15
+    nn = d.n_new
+    ne = C.cast(d.new_succ_off, C.POINTER(C.c_uint32))[nn] if d.new_succ_off else 0
+    return (a(4 * d.n_removed) + a(4 * nn) + a(8 * nn) + a(2 * nn) + a(nn) + a(4 * (nn + 1)) +
+            a(4 * ne) + 2 * a(4 * d.n_extra) + a(4 * d.n_cut))
 
 
 def _packed_bytes(g) -> int:

@@ -174,6 +174,65 @@ int dpro_cuda_replay_batch(dpro_ctx* ctx, const dpro_csr* cands,
                            int32_t* status, int64_t* err);
 
 /* ------------------------------------------------------------------------
+ * Resident base graph + per-candidate deltas (SURVEY 7 "Scale", 8(f) row
+ * 1). The search's candidates differ from one base graph in a few units, so
+ * the base CSR is uploaded once and stays in HBM (and L2); a batch uploads
+ * only each candidate's delta and the engine merges it on the GPU into the
+ * index-ordered CSR the replay kernels read. No counterpart in the
+ * reference, whose search builds every candidate with a GraphBuilder copy
+ * (optimize.cpp:1211-1227, 1382-1392).
+ *
+ * A candidate = base minus `removed` base ops (and their edges) minus the
+ * `cut` base edges plus `n_new` ops, in the base's index order: new op j
+ * sits before base op new_pos[j] (its lower_bound among the base ids); new
+ * ops sharing a position keep their order. Final indices: kept base op b ->
+ * b - #removed<b + #new_pos<=b; new op j -> new_pos[j] - #removed<new_pos[j]
+ * + j. Added edges: out of new ops in new_succ, out of kept base ops in
+ * extra_src/extra_dst; destinations are final indices.
+ * --------------------------------------------------------------------- */
+typedef struct dpro_delta {
+  uint32_t n_devices;            /* base dense ids, new devices appended    */
+  uint32_t n_removed;
+  const uint32_t* removed;       /* [n_removed] ascending base indices      */
+  uint32_t n_new;
+  const uint32_t* new_pos;       /* [n_new] non-decreasing, <= base n_ops   */
+  const int64_t* new_dur;        /* [n_new]                                 */
+  const uint16_t* new_dev;       /* [n_new]                                 */
+  const uint8_t* new_flags;      /* [n_new] DPRO_FLAG_*                     */
+  const uint32_t* new_succ_off;  /* [n_new+1]                               */
+  const uint32_t* new_succ;      /* final indices, ascending per op         */
+  uint32_t n_extra;
+  const uint32_t* extra_src;     /* [n_extra] kept base index, ascending    */
+  const uint32_t* extra_dst;     /* [n_extra] final index, ascending per src */
+  uint32_t n_cut;
+  const uint32_t* cut;           /* [n_cut] ascending positions in the base
+                                    succ[] of dropped edges between kept ops */
+} dpro_delta;
+
+typedef struct dpro_resident dpro_resident;
+/* Uploads a base graph (host CSR) to HBM; it stays resident until destroyed. */
+dpro_resident* dpro_cuda_resident_create(dpro_ctx* ctx, const dpro_csr* base);
+void dpro_cuda_resident_destroy(dpro_ctx* ctx, dpro_resident* r);
+/* A batch of n candidates given as host deltas against r: one H2D copy of
+ * the deltas, the merge on the GPU, then the same packing as
+ * dpro_cuda_batch_create. The resident must outlive nothing: the batch
+ * holds merged copies. */
+dpro_batch* dpro_cuda_batch_create_delta(dpro_ctx* ctx, const dpro_resident* r,
+                                         const dpro_delta* deltas, int32_t n);
+/* Per-candidate op / edge / device counts of a registered batch (any
+ * argument may be NULL). */
+int dpro_cuda_batch_sizes(dpro_batch* b, uint32_t* n_ops, uint32_t* n_edges,
+                          uint32_t* n_devices);
+/* Re-runs a batch's device-side preparation on the inputs already in HBM
+ * (delta merge for delta batches, then the pack kernel): with a replay, one
+ * full pass of the path without host work -- what bench.py times. */
+int dpro_cuda_batch_prepare(dpro_ctx* ctx, dpro_batch* b);
+/* One-shot: create from deltas, replay (makespan only), copy back, destroy. */
+int dpro_cuda_replay_delta_batch(dpro_ctx* ctx, const dpro_resident* r,
+                                 const dpro_delta* deltas, int32_t n,
+                                 int64_t* makespan, int32_t* status, int64_t* err);
+
+/* ------------------------------------------------------------------------
  * t_sync grid (replaces sync_makespan, replay.cpp:228-246, and the memoized
  * SearchCtx::sync grid of optimize.cpp:562-576,1170-1194): out[i] =
  * makespan of syncing bytes[i] as k[i] balanced partitions under the
@@ -241,6 +300,24 @@ int dpro_graph_from_base_batch(const dpro_base* base, int32_t n,
                                const int32_t* group_off, const int32_t* members,
                                const int32_t* group_k, int32_t threads,
                                dpro_graph** out);
+/* The same candidates as dpro_graph_from_base_batch, left as deltas against
+ * the base graph (dpro_delta, above) for dpro_cuda_batch_create_delta: only
+ * the changed units' ops are named, sorted and placed; the O(V) merge runs
+ * on the GPU. Device ids are the base graph's (new devices appended). */
+typedef struct dpro_delta_set dpro_delta_set;
+int dpro_base_delta_batch(const dpro_base* base, int32_t n,
+                          const int32_t* n_groups, const int64_t* spec_off,
+                          const int32_t* group_off, const int32_t* members,
+                          const int32_t* group_k, int32_t threads,
+                          dpro_delta_set** out);
+const dpro_delta* dpro_delta_set_deltas(const dpro_delta_set* s);  /* [size] */
+int32_t dpro_delta_set_size(const dpro_delta_set* s);
+const char* dpro_delta_set_device_str(const dpro_delta_set* s, int32_t cand,
+                                      uint32_t d);
+void dpro_delta_set_free(dpro_delta_set* s);
+/* The base graph itself (owned by the base; CSR via dpro_graph_csr). */
+const dpro_graph* dpro_base_graph(const dpro_base* base);
+
 /* n graphs with part_k[n*layers], built on `threads` host threads. */
 int dpro_graph_layered_batch(const dpro_layered_model* model,
                              const dpro_cluster_desc* cluster,

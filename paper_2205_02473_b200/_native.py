@@ -63,6 +63,18 @@ class DproLayeredModel(C.Structure):
     ]
 
 
+class DproDelta(C.Structure):
+    _fields_ = [
+        ("n_devices", C.c_uint32),
+        ("n_removed", C.c_uint32), ("removed", C.c_void_p),
+        ("n_new", C.c_uint32), ("new_pos", C.c_void_p), ("new_dur", C.c_void_p),
+        ("new_dev", C.c_void_p), ("new_flags", C.c_void_p), ("new_succ_off", C.c_void_p),
+        ("new_succ", C.c_void_p),
+        ("n_extra", C.c_uint32), ("extra_src", C.c_void_p), ("extra_dst", C.c_void_p),
+        ("n_cut", C.c_uint32), ("cut", C.c_void_p),
+    ]
+
+
 # (name, restype, argtypes) for every symbol include/dpro_cuda.h declares.
 _P, _I32, _I64, _U32 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint32
 SIGNATURES = {
@@ -84,6 +96,18 @@ SIGNATURES = {
     "dpro_cuda_batch_peak_memory": (C.c_int, [_P, _P, _P, _P, _P, _P, _P]),
     "dpro_cuda_critical_path": (C.c_int, [_P, C.POINTER(DproCsr), _P, _P, _I64, _P, _P]),
     "dpro_cuda_replay_batch": (C.c_int, [_P, C.POINTER(DproCsr), _I32, _I32, _P, _P, _P, _P, _P]),
+    "dpro_cuda_resident_create": (_P, [_P, C.POINTER(DproCsr)]),
+    "dpro_cuda_resident_destroy": (None, [_P, _P]),
+    "dpro_cuda_batch_create_delta": (_P, [_P, _P, _P, _I32]),
+    "dpro_cuda_batch_prepare": (C.c_int, [_P, _P]),
+    "dpro_cuda_batch_sizes": (C.c_int, [_P, _P, _P, _P]),
+    "dpro_cuda_replay_delta_batch": (C.c_int, [_P, _P, _P, _I32, _P, _P, _P]),
+    "dpro_base_delta_batch": (C.c_int, [_P, _I32, _P, _P, _P, _P, _P, _I32, _P]),
+    "dpro_delta_set_deltas": (_P, [_P]),
+    "dpro_delta_set_size": (_I32, [_P]),
+    "dpro_delta_set_device_str": (C.c_char_p, [_P, _I32, _U32]),
+    "dpro_delta_set_free": (None, [_P]),
+    "dpro_base_graph": (_P, [_P]),
     "dpro_cuda_tsync_grid": (C.c_int, [_P, C.POINTER(DproClusterDesc), _P, _P, _I32, _P, _P]),
     "dpro_graph_layered": (_P, [C.POINTER(DproLayeredModel), C.POINTER(DproClusterDesc), _P, _P]),
     "dpro_graph_layered_batch": (C.c_int, [C.POINTER(DproLayeredModel), C.POINTER(DproClusterDesc), _P, _I32, _I32, _P]),

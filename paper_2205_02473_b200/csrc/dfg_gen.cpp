@@ -116,7 +116,7 @@ struct Gen {
 
   uint32_t device(int dkind, int node, int peer) {
     const uint64_t key = (uint64_t(dkind) << 62) | (uint64_t(uint32_t(node)) << 31) |
-                         uint64_t(uint32_t(peer + 1));
+                         uint64_t(uint32_t(peer + 1));  // == dev_key()
     auto it = devkeys.emplace(key, static_cast<uint32_t>(devs.size()));
     if (it.second) devs.push_back({dkind, node, peer});
     return it.first->second;
@@ -514,8 +514,13 @@ struct BaseData {
   std::vector<std::vector<uint32_t>> fw, bw, up;  // [node][layer] final index
   std::vector<std::vector<uint32_t>> in, out;     // [layer][node]
   std::vector<std::vector<uint32_t>> comm;        // [layer] comm op final indices
+  std::unordered_map<uint64_t, uint16_t> devindex;  // Gen device key -> dense id
   explicit BaseData(const dpro_cluster_desc& d) : c(d) {}
 };
+
+inline uint64_t dev_key(int dkind, int node, int peer) {
+  return (uint64_t(dkind) << 62) | (uint64_t(uint32_t(node)) << 31) | uint64_t(uint32_t(peer + 1));
+}
 
 constexpr uint32_t kBaseRef = 0x80000000u;
 
@@ -563,11 +568,21 @@ std::shared_ptr<BaseData> build_base(const dpro_layered_model& m, const dpro_clu
   for (int i = 0; i < m.layers; ++i)
     for (uint32_t ci = rec.comm[i].first; ci < rec.comm[i].second; ++ci)
       B->comm[i].push_back(rank[ci]);
+  for (size_t d = 0; d < B->devs.size(); ++d)
+    B->devindex[dev_key(B->devs[d][0], B->devs[d][1], B->devs[d][2])] = static_cast<uint16_t>(d);
   return B;
 }
 
-dpro_graph* build_delta(const std::shared_ptr<BaseData>& Bp, const Groups& G) {
-  const BaseData& B = *Bp;
+// The changed part of a candidate: new ops (Gen, creation order; edges hold
+// kBaseRef | base index or creation index), the removed base ops, the new
+// ops in id order (snew) and their insertion points among the base ids.
+struct DeltaParts {
+  Gen g;
+  std::vector<uint8_t> removed;  // [nb]
+  std::vector<uint32_t> snew, pos;
+};
+
+void prepare_delta(const BaseData& B, const Groups& G, DeltaParts& P) {
   const dpro_graph& bg = *B.g;
   const int L = B.L, NG = static_cast<int>(G.members.size());
   const uint32_t nb = static_cast<uint32_t>(bg.kind.size());
@@ -587,9 +602,10 @@ dpro_graph* build_delta(const std::shared_ptr<BaseData>& Bp, const Groups& G) {
   for (int i = 0; i < L; ++i)
     if (group_of[i] < 0) throw std::runtime_error("tensor groups must cover every layer");
 
-  Gen g;  // new ops only; edges hold refs (kBaseRef | base index, or new index)
+  Gen& g = P.g;
   g.names = &B.c.nodes;
-  std::vector<uint8_t> removed(nb, 0);
+  std::vector<uint8_t>& removed = P.removed;
+  removed.assign(nb, 0);
   for (int q = 0; q < NG; ++q) {
     const auto& mem = G.members[q];
     const int k = G.k[q];
@@ -634,18 +650,31 @@ dpro_graph* build_delta(const std::shared_ptr<BaseData>& Bp, const Groups& G) {
   }
   const uint32_t nn = static_cast<uint32_t>(g.ops.size());
   // sort the new ops, then place each among the base ids (binary search)
-  std::vector<uint32_t> snew(nn);
-  std::iota(snew.begin(), snew.end(), 0u);
-  std::sort(snew.begin(), snew.end(),
+  P.snew.resize(nn);
+  std::iota(P.snew.begin(), P.snew.end(), 0u);
+  std::sort(P.snew.begin(), P.snew.end(),
             [&](uint32_t a, uint32_t b) { return g.ops[a].id < g.ops[b].id; });
-  std::vector<uint32_t> pos(nn);
+  P.pos.resize(nn);
   for (uint32_t j = 0; j < nn; ++j) {
-    const std::string& id = g.ops[snew[j]].id;
+    const std::string& id = g.ops[P.snew[j]].id;
     const auto it = std::lower_bound(bg.ids.begin(), bg.ids.end(), id);
     if (it != bg.ids.end() && *it == id && !removed[it - bg.ids.begin()])
       throw std::runtime_error("duplicate op id '" + id + "'");
-    pos[j] = static_cast<uint32_t>(it - bg.ids.begin());
+    P.pos[j] = static_cast<uint32_t>(it - bg.ids.begin());
   }
+}
+
+dpro_graph* build_delta(const std::shared_ptr<BaseData>& Bp, const Groups& G) {
+  const BaseData& B = *Bp;
+  const dpro_graph& bg = *B.g;
+  const uint32_t nb = static_cast<uint32_t>(bg.kind.size());
+  DeltaParts P;
+  prepare_delta(B, G, P);
+  Gen& g = P.g;
+  const std::vector<uint8_t>& removed = P.removed;
+  const std::vector<uint32_t>& snew = P.snew;
+  const std::vector<uint32_t>& pos = P.pos;
+  const uint32_t nn = static_cast<uint32_t>(g.ops.size());
   // final order: merge kept base ops with the new ops at their positions
   std::vector<uint32_t> fb(nb, UINT32_MAX), fnew(nn, UINT32_MAX);
   auto* out = new dpro_graph;
@@ -769,6 +798,103 @@ dpro_graph* build_delta(const std::shared_ptr<BaseData>& Bp, const Groups& G) {
     for (uint32_t* p = a; p < z; ++p) out->indeg[*p]++;
   }
   return out;
+}
+
+// A candidate as a dpro_delta against the base (include/dpro_cuda.h): the
+// same candidate build_delta() merges on the host, left unmerged for the
+// engine to merge next to the resident base graph in HBM.
+struct DeltaHost {
+  std::vector<uint32_t> removed, new_pos, new_succ_off, new_succ, extra_src, extra_dst;
+  std::vector<int64_t> new_dur;
+  std::vector<uint16_t> new_dev;
+  std::vector<uint8_t> new_flags;
+  std::vector<std::string> extra_dev_strs;  // devices beyond the base's
+  uint32_t n_devices = 0;
+};
+
+void emit_delta(const BaseData& B, const Groups& G, DeltaHost& D) {
+  const dpro_graph& bg = *B.g;
+  DeltaParts P;
+  prepare_delta(B, G, P);
+  const Gen& g = P.g;
+  const uint32_t nb = static_cast<uint32_t>(bg.kind.size());
+  const uint32_t nn = static_cast<uint32_t>(g.ops.size());
+  D.removed.clear();
+  for (uint32_t b = 0; b < nb; ++b)
+    if (P.removed[b]) D.removed.push_back(b);
+  const auto& R = D.removed;
+  auto r_of = [&](uint32_t x) {
+    return static_cast<uint32_t>(std::lower_bound(R.begin(), R.end(), x) - R.begin());
+  };
+  auto q_of = [&](uint32_t b) {
+    return static_cast<uint32_t>(std::upper_bound(P.pos.begin(), P.pos.end(), b) - P.pos.begin());
+  };
+  std::vector<uint32_t> sorted_of(nn), fnew(nn);
+  for (uint32_t j = 0; j < nn; ++j) {
+    sorted_of[P.snew[j]] = j;
+    fnew[P.snew[j]] = P.pos[j] - r_of(P.pos[j]) + j;
+  }
+  auto fin = [&](uint32_t ref) {  // kBaseRef marks base indices
+    if (!(ref & kBaseRef)) return fnew[ref];
+    const uint32_t b = ref & ~kBaseRef;
+    return b - r_of(b) + q_of(b);
+  };
+  // devices: the base's dense ids, unseen ones appended
+  std::vector<uint16_t> ndev(g.devs.size());
+  D.extra_dev_strs.clear();
+  uint32_t nd = static_cast<uint32_t>(bg.device_strs.size());
+  for (size_t d = 0; d < g.devs.size(); ++d) {
+    const auto& k = g.devs[d];
+    const auto it = B.devindex.find(dev_key(k[0], k[1], k[2]));
+    if (it != B.devindex.end()) {
+      ndev[d] = it->second;
+    } else {
+      if (nd >= 65535) throw std::runtime_error("more than 65535 devices");
+      ndev[d] = static_cast<uint16_t>(nd++);
+      const std::string& a = B.c.nodes[k[1]];
+      D.extra_dev_strs.push_back(k[0] == 0 ? a : a + ">" + B.c.nodes[k[2]]);
+    }
+  }
+  D.n_devices = nd;
+  D.new_pos = P.pos;
+  D.new_dur.resize(nn);
+  D.new_dev.resize(nn);
+  D.new_flags.resize(nn);
+  for (uint32_t j = 0; j < nn; ++j) {
+    const auto& op = g.ops[P.snew[j]];
+    D.new_dur[j] = op.dur;
+    D.new_dev[j] = ndev[op.devkey];
+    D.new_flags[j] = static_cast<uint8_t>(
+        (op.kind == kVin || op.kind == kVout ? DPRO_FLAG_VIRTUAL : 0u) |
+        (op.kind == kSend || op.kind == kRecv ? DPRO_FLAG_COMM : 0u));
+  }
+  // edges out of new ops -> new_succ (by sorted position); out of base ops -> extra
+  std::vector<std::pair<uint32_t, uint32_t>> ne, xe;
+  ne.reserve(g.edges.size());
+  for (const auto& e : g.edges) {
+    const uint32_t dst = fin(e.second);
+    if (e.first & kBaseRef)
+      xe.emplace_back(e.first & ~kBaseRef, dst);
+    else
+      ne.emplace_back(sorted_of[e.first], dst);
+  }
+  std::sort(ne.begin(), ne.end());
+  ne.erase(std::unique(ne.begin(), ne.end()), ne.end());
+  std::sort(xe.begin(), xe.end());
+  xe.erase(std::unique(xe.begin(), xe.end()), xe.end());
+  D.new_succ_off.assign(nn + 1, 0);
+  D.new_succ.resize(ne.size());
+  for (size_t k = 0; k < ne.size(); ++k) {
+    D.new_succ_off[ne[k].first + 1]++;
+    D.new_succ[k] = ne[k].second;
+  }
+  for (uint32_t j = 0; j < nn; ++j) D.new_succ_off[j + 1] += D.new_succ_off[j];
+  D.extra_src.resize(xe.size());
+  D.extra_dst.resize(xe.size());
+  for (size_t k = 0; k < xe.size(); ++k) {
+    D.extra_src[k] = xe[k].first;
+    D.extra_dst[k] = xe[k].second;
+  }
 }
 
 }  // namespace
@@ -954,6 +1080,84 @@ int dpro_graph_from_base_batch(const dpro_base* base, int32_t n, const int32_t* 
     }
   return DPRO_OK;
 }
+struct dpro_delta_set {
+  std::shared_ptr<BaseData> base;
+  std::vector<DeltaHost> d;
+  std::vector<dpro_delta> views;
+};
+
+int dpro_base_delta_batch(const dpro_base* base, int32_t n, const int32_t* n_groups,
+                          const int64_t* spec_off, const int32_t* group_off,
+                          const int32_t* members, const int32_t* group_k, int32_t threads,
+                          dpro_delta_set** out) {
+  if (!base || !out || n < 0) return DPRO_EINVAL;
+  *out = nullptr;
+  if (threads < 1) threads = 1;
+  auto set = std::make_unique<dpro_delta_set>();
+  set->base = base->b;
+  set->d.resize(n);
+  std::vector<int32_t> st(n, DPRO_OK);
+  std::vector<std::string> errs(threads);
+  std::atomic<int32_t> next{0};
+  auto work = [&](int tid) {
+    for (int32_t i; (i = next.fetch_add(1)) < n;) {
+      try {
+        const int64_t g0 = spec_off[i];
+        Groups G;
+        for (int32_t q = 0; q < n_groups[i]; ++q) {
+          G.members.emplace_back(members + group_off[g0 + q], members + group_off[g0 + q + 1]);
+          G.k.push_back(group_k ? group_k[g0 + q] : 1);
+        }
+        emit_delta(*base->b, G, set->d[i]);
+      } catch (const std::exception& e) {
+        st[i] = DPRO_EINVAL;
+        errs[tid] = e.what();
+      }
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < threads; ++t) pool.emplace_back(work, t);
+  work(0);
+  for (auto& th : pool) th.join();
+  for (int32_t i = 0; i < n; ++i)
+    if (st[i] != DPRO_OK) {
+      for (auto& e : errs)
+        if (!e.empty()) g_gen_err = e;
+      return st[i];
+    }
+  set->views.resize(n);
+  for (int32_t i = 0; i < n; ++i) {
+    const DeltaHost& D = set->d[i];
+    dpro_delta& v = set->views[i];
+    std::memset(&v, 0, sizeof v);
+    v.n_devices = D.n_devices;
+    v.n_removed = static_cast<uint32_t>(D.removed.size());
+    v.removed = D.removed.data();
+    v.n_new = static_cast<uint32_t>(D.new_pos.size());
+    v.new_pos = D.new_pos.data();
+    v.new_dur = D.new_dur.data();
+    v.new_dev = D.new_dev.data();
+    v.new_flags = D.new_flags.data();
+    v.new_succ_off = D.new_succ_off.data();
+    v.new_succ = D.new_succ.data();
+    v.n_extra = static_cast<uint32_t>(D.extra_src.size());
+    v.extra_src = D.extra_src.data();
+    v.extra_dst = D.extra_dst.data();
+  }
+  *out = set.release();
+  return DPRO_OK;
+}
+
+const dpro_delta* dpro_delta_set_deltas(const dpro_delta_set* s) { return s->views.data(); }
+int32_t dpro_delta_set_size(const dpro_delta_set* s) { return static_cast<int32_t>(s->views.size()); }
+const char* dpro_delta_set_device_str(const dpro_delta_set* s, int32_t cand, uint32_t d) {
+  const dpro_graph& bg = *s->base->g;
+  if (d < bg.device_strs.size()) return bg.device_strs[d].c_str();
+  return s->d.at(cand).extra_dev_strs.at(d - bg.device_strs.size()).c_str();
+}
+void dpro_delta_set_free(dpro_delta_set* s) { delete s; }
+const dpro_graph* dpro_base_graph(const dpro_base* base) { return base->b->g.get(); }
+
 int32_t dpro_graph_op_kind(const dpro_graph* g, uint32_t i) { return g->kind.at(i); }
 const char* dpro_graph_device_str(const dpro_graph* g, uint32_t d) {
   return g->device_strs.at(d).c_str();

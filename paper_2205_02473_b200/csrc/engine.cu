@@ -6,7 +6,9 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <condition_variable>
 #include <cstdio>
+#include <functional>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -19,6 +21,7 @@
 
 #include "critical_path_kernel.cuh"
 #include "memory_kernel.cuh"
+#include "delta_kernel.cuh"
 #include "dpro_cuda.h"
 #include "pack_kernel.cuh"
 #include "replay_fast.cuh"
@@ -96,6 +99,80 @@ struct HostPinned {
   }
 };
 
+// Persistent host worker threads (one pool per context): jobs are index
+// ranges handed out through an atomic counter; the caller may keep working
+// (e.g. issuing H2D copies) until wait().
+class Pool {
+ public:
+  Pool() {
+    const int n = std::max(1, (int)std::thread::hardware_concurrency());
+    for (int t = 0; t < n; ++t) th_.emplace_back([this] { loop(); });
+  }
+  ~Pool() {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  int size() const { return static_cast<int>(th_.size()); }
+  void start(int32_t n, std::function<void(int32_t)> fn) {
+    std::lock_guard<std::mutex> g(m_);
+    fn_ = std::move(fn);
+    n_ = n;
+    next_ = 0;
+    left_ = n;
+    ++gen_;
+    cv_.notify_all();
+  }
+  void wait() {
+    std::unique_lock<std::mutex> g(m_);
+    done_.wait(g, [this] { return left_ == 0 && active_ == 0; });
+  }
+  void run(int32_t n, std::function<void(int32_t)> fn) {
+    start(n, std::move(fn));
+    wait();
+  }
+
+ private:
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      std::function<void(int32_t)> fn;
+      int32_t n;
+      {
+        std::unique_lock<std::mutex> g(m_);
+        cv_.wait(g, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+        fn = fn_;
+        n = n_;
+        ++active_;  // wait() returns only once no worker can touch this job
+      }
+      int32_t did = 0;
+      for (int32_t i; (i = next_.fetch_add(1)) < n;) {
+        fn(i);
+        ++did;
+      }
+      {
+        std::lock_guard<std::mutex> g(m_);
+        left_ -= did;
+        --active_;
+        if (left_ == 0 && active_ == 0) done_.notify_all();
+      }
+    }
+  }
+  std::vector<std::thread> th_;
+  std::mutex m_;
+  std::condition_variable cv_, done_;
+  std::function<void(int32_t)> fn_;
+  int32_t n_ = 0, left_ = 0, active_ = 0;
+  std::atomic<int32_t> next_{0};
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
 }  // namespace
 
 struct dpro_ctx {
@@ -106,10 +183,23 @@ struct dpro_ctx {
   int smem_per_sm = 228 * 1024;
   std::string err;
   HostPinned staging;
+  std::unique_ptr<Pool> pool;  // created on first use
+  Pool& workers() {
+    if (!pool) pool = std::make_unique<Pool>();
+    return *pool;
+  }
   int fast = 1;       // option "fast"
   uint32_t ring = 4;  // option "ring"
   int warps = 4;      // option "warps": warps (1, 2, 4) per candidate
   dpro_batch* spare = nullptr;  // recycled arenas for repeated small calls
+};
+
+struct dpro_resident {
+  DevBuf buf;
+  dpro_k::ResDev dev{};
+  uint32_t n = 0, e = 0, d = 0;
+  bool dur32 = true;
+  std::vector<uint32_t> succ_off, succ, indeg;  // host copy (edge counts)
 };
 
 struct dpro_batch {
@@ -126,6 +216,12 @@ struct dpro_batch {
   DevBuf work;    // work counter
   DevBuf cp;      // critical-path scratch
   DevBuf pack;    // packed replay layout (rec, erec, cnt0, offsets, info)
+  DevBuf dblob;   // uploaded deltas (delta batches)
+  DevBuf ddesc;   // DeltaDev[n]
+  DevBuf rank;    // merge rank scratch
+  const dpro_resident* res = nullptr;  // delta batches: the base
+  uint32_t smem_ind = 0;               // merge kernel in-degree smem words
+  size_t s_cnt0 = 0;
   Scratch S{};
   Outs O{};
   PackOut P{};
@@ -289,6 +385,10 @@ int upload_host(dpro_ctx* ctx, dpro_batch* b, const dpro_csr* cands) {
   return DPRO_OK;
 }
 
+int finish_batch(dpro_ctx* ctx, dpro_batch* b);
+int run_pack(dpro_ctx* ctx, dpro_batch* b);
+int run_merge(dpro_ctx* ctx, dpro_batch* b);
+
 int build_batch(dpro_ctx* ctx, dpro_batch* b, const dpro_csr* cands) {
   const int32_t n = b->n;
   b->hc.resize(n);
@@ -338,6 +438,14 @@ int build_batch(dpro_ctx* ctx, dpro_batch* b, const dpro_csr* cands) {
     int st = upload_host(ctx, b, cands);
     if (st != DPRO_OK) return st;
   }
+  return finish_batch(ctx, b);
+}
+
+// Scratch, outputs, descriptors and the pack kernel for a batch whose
+// b->hc descriptors point at device CSR arrays.
+int finish_batch(dpro_ctx* ctx, dpro_batch* b) {
+  const int32_t n = b->n;
+  const unsigned long long so = b->sum_n, sd = b->sum_d, sdo = b->sum_dof;
   // scratch: indeg, qbuf, qpos, vstack (u32), sched (u8), devoff, dstate, busy
   const size_t s_u32 = align16(so * 4 + 4);
   const size_t s_u8 = align16(so + 1);
@@ -387,8 +495,8 @@ int build_batch(dpro_ctx* ctx, dpro_batch* b, const dpro_csr* cands) {
                  s_cnt = align16(co + 16), s_u32 = align16(so * 4 + 4),
                  s_off = align16(size_t(n) * 8 + 8),
                  s_info = align16(size_t(n) * sizeof(dpro_k::PackInfo) + 16);
-    const size_t s_xoff = align16(ro * 4 + 16);
-    CU(b->pack.ensure(s_rec + s_erec + s_cnt + 2 * s_u32 + s_xoff + 3 * s_off + s_info));
+    const size_t s_xoff = align16(ro * 4 + 16), s_spl = align16(so + 16);
+    CU(b->pack.ensure(s_rec + s_erec + s_cnt + 2 * s_u32 + s_xoff + s_spl + 3 * s_off + s_info));
     size_t po = 0;
     b->P.rec = b->pack.as<uint4>(po); po += s_rec;
     b->P.erec = b->pack.as<uint4>(po); po += s_erec;
@@ -396,6 +504,7 @@ int build_batch(dpro_ctx* ctx, dpro_batch* b, const dpro_csr* cands) {
     b->P.srcs = b->pack.as<uint32_t>(po); po += s_u32;
     b->P.cidx = b->pack.as<uint32_t>(po); po += s_u32;
     b->P.xoff = b->pack.as<uint32_t>(po); po += s_xoff;
+    b->P.spl = b->pack.as<uint8_t>(po); po += s_spl;
     b->P.r_off = b->pack.as<unsigned long long>(po); po += s_off;
     b->P.e_off = b->pack.as<unsigned long long>(po); po += s_off;
     b->P.c_off = b->pack.as<unsigned long long>(po); po += s_off;
@@ -403,23 +512,33 @@ int build_batch(dpro_ctx* ctx, dpro_batch* b, const dpro_csr* cands) {
     CU(cudaMemcpyAsync(b->P.r_off, r_off.data(), size_t(n) * 8, cudaMemcpyHostToDevice, ctx->stream));
     CU(cudaMemcpyAsync(b->P.e_off, e_off.data(), size_t(n) * 8, cudaMemcpyHostToDevice, ctx->stream));
     CU(cudaMemcpyAsync(b->P.c_off, c_off.data(), size_t(n) * 8, cudaMemcpyHostToDevice, ctx->stream));
-    CU(cudaMemsetAsync(b->P.cnt0, 0, s_cnt, ctx->stream));
-    b->info.assign(n, dpro_k::PackInfo{});
-    if (n > 0) {
-      const int grid = std::min<int>(n, ctx->sm_count * 8);
-      bool need_indeg = false;
-      for (int32_t i = 0; i < n; ++i) need_indeg |= (b->hc[i].indeg == nullptr);
-      if (need_indeg)
-        dpro_k::count_indeg_kernel<<<grid, 256, 0, ctx->stream>>>(b->desc.as<Cand>(), n, b->S);
-      Tracer tr;
-      dpro_k::pack_kernel<<<grid, 256, 0, ctx->stream>>>(b->desc.as<Cand>(), n, b->S, b->P);
-      CU(cudaGetLastError());
-      tr.mark("pack kernel", ctx->stream, true);
-      CU(cudaMemcpyAsync(b->info.data(), b->P.info, size_t(n) * sizeof(dpro_k::PackInfo),
-                         cudaMemcpyDeviceToHost, ctx->stream));
-      CU(cudaStreamSynchronize(ctx->stream));
-    }
+    b->s_cnt0 = s_cnt;
   }
+  return run_pack(ctx, b);
+}
+
+// The pack kernel (and count_indeg when a candidate came without in-degrees)
+// on the batch's device CSR, then the per-candidate PackInfo to the host.
+int run_pack(dpro_ctx* ctx, dpro_batch* b) {
+  const int32_t n = b->n;
+  CU(cudaMemsetAsync(b->P.cnt0, 0, b->s_cnt0, ctx->stream));
+  b->info.assign(n, dpro_k::PackInfo{});
+  if (n > 0) {
+    const int grid = std::min<int>(n, ctx->sm_count * 8);
+    bool need_indeg = false;
+    for (int32_t i = 0; i < n; ++i) need_indeg |= (b->hc[i].indeg == nullptr);
+    if (need_indeg)
+      dpro_k::count_indeg_kernel<<<grid, 256, 0, ctx->stream>>>(b->desc.as<Cand>(), n, b->S);
+    Tracer tr;
+    dpro_k::pack_kernel<<<std::min<int>(n, ctx->sm_count), dpro_k::kPackThreads, 0,
+                          ctx->stream>>>(b->desc.as<Cand>(), n, b->S, b->P);
+    CU(cudaGetLastError());
+    tr.mark("pack kernel", ctx->stream, true);
+    CU(cudaMemcpyAsync(b->info.data(), b->P.info, size_t(n) * sizeof(dpro_k::PackInfo),
+                       cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+  }
+  b->replayed = b->with_schedule = false;
   return DPRO_OK;
 }
 
@@ -464,14 +583,11 @@ const char* dpro_cuda_last_error(dpro_ctx* ctx) {
   return ctx ? ctx->err.c_str() : "null context";
 }
 
-dpro_batch* dpro_cuda_batch_create(dpro_ctx* ctx, const dpro_csr* cands,
-                                   int32_t n_cands, int32_t memspace) {
-  if (!ctx || (n_cands > 0 && !cands) || n_cands < 0 ||
-      (memspace != DPRO_HOST && memspace != DPRO_DEVICE)) {
-    if (ctx) ctx->err = "bad batch arguments";
-    return nullptr;
-  }
-  cudaSetDevice(ctx->device);
+}  // extern "C"
+
+namespace {
+
+dpro_batch* acquire_batch(dpro_ctx* ctx, int32_t n, int32_t memspace) {
   dpro_batch* b = ctx->spare;
   ctx->spare = nullptr;
   if (b) {  // keep the device buffers (they only grow), reset the rest
@@ -485,8 +601,372 @@ dpro_batch* dpro_cuda_batch_create(dpro_ctx* ctx, const dpro_csr* cands,
   } else {
     b = new dpro_batch;
   }
-  b->n = n_cands;
+  b->n = n;
   b->memspace = memspace;
+  b->res = nullptr;
+  return b;
+}
+
+template <typename F>
+void parallel_for(int32_t n, F&& fn) {
+  const int nt = std::max(1, std::min<int>(n, (int)std::thread::hardware_concurrency()));
+  std::atomic<int32_t> next{0};
+  auto work = [&]() {
+    for (int32_t i; (i = next.fetch_add(1)) < n;) fn(i);
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < nt; ++t) pool.emplace_back(work);
+  work();
+  for (auto& th : pool) th.join();
+}
+
+bool ascending(const uint32_t* a, uint32_t n, bool strict) {
+  for (uint32_t i = 1; i < n; ++i)
+    if (strict ? a[i] <= a[i - 1] : a[i] < a[i - 1]) return false;
+  return true;
+}
+
+// Host checks of one delta and its merged sizes (include/dpro_cuda.h).
+std::string check_delta(const dpro_resident& r, const dpro_delta& D, uint32_t& n_ops,
+                        uint32_t& n_edges, bool& dur32) {
+  const uint32_t nb = r.n;
+  if ((D.n_removed && !D.removed) || (D.n_new && (!D.new_pos || !D.new_dur || !D.new_dev ||
+                                                  !D.new_flags)) ||
+      !D.new_succ_off || (D.n_extra && (!D.extra_src || !D.extra_dst)) || (D.n_cut && !D.cut))
+    return "null delta array";
+  if (!ascending(D.removed, D.n_removed, true) || (D.n_removed && D.removed[D.n_removed - 1] >= nb))
+    return "removed must be ascending base indices";
+  if (!ascending(D.new_pos, D.n_new, false) || (D.n_new && D.new_pos[D.n_new - 1] > nb))
+    return "new_pos must be non-decreasing and <= base n_ops";
+  if (D.n_devices < r.d) return "n_devices below the base's";
+  n_ops = nb - D.n_removed + D.n_new;
+  const uint32_t ne = D.new_succ_off[D.n_new];
+  if (D.new_succ_off[0] != 0 || !ascending(D.new_succ_off, D.n_new + 1, false) || (ne && !D.new_succ))
+    return "bad new_succ_off";
+  auto removed = [&](uint32_t b) {
+    return std::binary_search(D.removed, D.removed + D.n_removed, b);
+  };
+  dur32 = r.dur32;
+  for (uint32_t j = 0; j < D.n_new; ++j) {
+    if (D.new_dev[j] >= D.n_devices) return "new_dev out of range";
+    if (D.new_dur[j] > INT32_MAX || D.new_dur[j] < INT32_MIN) dur32 = false;
+    for (uint32_t k = D.new_succ_off[j]; k < D.new_succ_off[j + 1]; ++k)
+      if (D.new_succ[k] >= n_ops || (k > D.new_succ_off[j] && D.new_succ[k] <= D.new_succ[k - 1]))
+        return "new_succ must be ascending final indices";
+  }
+  for (uint32_t k = 0; k < D.n_extra; ++k) {
+    if (D.extra_src[k] >= nb || removed(D.extra_src[k]) || D.extra_dst[k] >= n_ops)
+      return "extra edge out of range";
+    if (k && (D.extra_src[k] < D.extra_src[k - 1] ||
+              (D.extra_src[k] == D.extra_src[k - 1] && D.extra_dst[k] <= D.extra_dst[k - 1])))
+      return "extra edges must be sorted by (src, dst)";
+  }
+  // kept base edges: all minus those touching removed ops minus cut ones
+  uint64_t lost = 0;
+  for (uint32_t k = 0; k < D.n_removed; ++k) {
+    const uint32_t u = D.removed[k];
+    lost += r.succ_off[u + 1] - r.succ_off[u];  // out-edges of u
+    lost += r.indeg[u];                          // in-edges of u ...
+    for (uint32_t e = r.succ_off[u]; e < r.succ_off[u + 1]; ++e)
+      lost -= removed(r.succ[e]);                // ... counted once
+  }
+  if (!ascending(D.cut, D.n_cut, true)) return "cut must be ascending";
+  for (uint32_t k = 0; k < D.n_cut; ++k) {
+    const uint32_t e = D.cut[k];
+    if (e >= r.e) return "cut edge out of range";
+    const uint32_t u = static_cast<uint32_t>(
+        std::upper_bound(r.succ_off.begin(), r.succ_off.end(), e) - r.succ_off.begin() - 1);
+    if (removed(u) || removed(r.succ[e])) return "cut edges must join kept ops";
+    ++lost;
+  }
+  n_edges = static_cast<uint32_t>(uint64_t(r.e) - lost + D.n_extra + ne);
+  return "";
+}
+
+int build_delta_batch(dpro_ctx* ctx, dpro_batch* b, const dpro_resident* r,
+                      const dpro_delta* deltas) {
+  Tracer tr;
+  const int32_t n = b->n;
+  // delta blob layout (sizes need no checks); null arrays are caught below
+  std::vector<size_t> boff(n + 1, 0);
+  for (int32_t i = 0; i < n; ++i) {
+    const dpro_delta& D = deltas[i];
+    const size_t nn = D.n_new;
+    const size_t ne = D.new_succ_off ? D.new_succ_off[nn] : 0;
+    boff[i + 1] = boff[i] + align16(size_t(D.n_removed) * 4) + align16(nn * 4) +
+                  align16(nn * 8) + align16(nn * 2) + align16(nn) + align16((nn + 1) * 4) +
+                  align16(ne * 4) + 2 * align16(size_t(D.n_extra) * 4) +
+                  align16(size_t(D.n_cut) * 4);
+  }
+  CU(cudaStreamSynchronize(ctx->stream));  // staging may feed an earlier copy
+  CU(b->dblob.ensure(boff[n] + 16));
+  CU(ctx->staging.ensure(boff[n] + 16));
+  char* stage = static_cast<char*>(ctx->staging.p);
+  const uint32_t W = (r->n >> 5) + 1;
+  const size_t rank_words = 3 * size_t(W) + 1;
+  std::vector<dpro_k::DeltaDev> dd(n);
+  std::vector<uint32_t> nops(n), nedges(n);
+  std::vector<uint8_t> d32(n);
+  std::vector<std::string> errs(n);
+  // one pass per candidate on the pool: check, count, pack into staging;
+  // this thread copies each finished ~16 MB chunk while the rest packs
+  std::vector<int32_t> chunk_end;
+  for (int32_t i = 0; i < n;) {
+    int32_t j = i + 1;
+    while (j < n && boff[j] - boff[i] < (size_t(16) << 20)) ++j;
+    chunk_end.push_back(j);
+    i = j;
+  }
+  const int nchunks = static_cast<int>(chunk_end.size());
+  std::vector<std::atomic<int32_t>> left(nchunks);
+  std::vector<int> chunk_of(n);
+  for (int k = 0, i = 0; k < nchunks; ++k) {
+    left[k] = chunk_end[k] - i;
+    for (; i < chunk_end[k]; ++i) chunk_of[i] = k;
+  }
+  ctx->workers().start(n, [&](int32_t i) {
+    const dpro_delta& D = deltas[i];
+    bool f = true;
+    errs[i] = check_delta(*r, D, nops[i], nedges[i], f);
+    d32[i] = f;
+    if (errs[i].empty()) {
+      dpro_k::DeltaDev& x = dd[i];
+      size_t o = boff[i];
+      auto put = [&](const void* src, size_t bytes) {
+        if (bytes) std::memcpy(stage + o, src, bytes);
+        const void* dptr = b->dblob.as<char>(o);
+        o += align16(bytes);
+        return dptr;
+      };
+      const size_t nn = D.n_new;
+      x.removed = static_cast<const uint32_t*>(put(D.removed, size_t(D.n_removed) * 4));
+      x.new_pos = static_cast<const uint32_t*>(put(D.new_pos, nn * 4));
+      x.new_dur = static_cast<const long long*>(put(D.new_dur, nn * 8));
+      x.new_dev = static_cast<const uint16_t*>(put(D.new_dev, nn * 2));
+      x.new_flags = static_cast<const uint8_t*>(put(D.new_flags, nn));
+      x.new_succ_off = static_cast<const uint32_t*>(put(D.new_succ_off, (nn + 1) * 4));
+      x.new_succ = static_cast<const uint32_t*>(put(D.new_succ, size_t(D.new_succ_off[nn]) * 4));
+      x.extra_src = static_cast<const uint32_t*>(put(D.extra_src, size_t(D.n_extra) * 4));
+      x.extra_dst = static_cast<const uint32_t*>(put(D.extra_dst, size_t(D.n_extra) * 4));
+      x.cut = static_cast<const uint32_t*>(put(D.cut, size_t(D.n_cut) * 4));
+      x.n_removed = D.n_removed;
+      x.n_new = D.n_new;
+      x.n_extra = D.n_extra;
+      x.n_cut = D.n_cut;
+      x.rank_off = rank_words * size_t(i);
+    }
+    left[chunk_of[i]].fetch_sub(1, std::memory_order_release);
+  });
+  int err = DPRO_OK;
+  for (int k = 0, i = 0; k < nchunks; ++k) {
+    while (left[k].load(std::memory_order_acquire) > 0) std::this_thread::yield();
+    const size_t a0 = boff[i], z0 = boff[chunk_end[k]];
+    if (err == DPRO_OK && z0 > a0) {
+      const cudaError_t e = cudaMemcpyAsync(b->dblob.as<char>(a0), stage + a0, z0 - a0,
+                                            cudaMemcpyHostToDevice, ctx->stream);
+      if (e != cudaSuccess) err = set_err(ctx, DPRO_ECUDA, cudaGetErrorString(e));
+    }
+    i = chunk_end[k];
+  }
+  ctx->workers().wait();
+  if (err != DPRO_OK) return err;
+  for (int32_t i = 0; i < n; ++i)
+    if (!errs[i].empty())
+      return set_err(ctx, DPRO_EINVAL, "delta " + std::to_string(i) + ": " + errs[i]);
+  tr.mark("host: check + pack || H2D");
+  b->hc.resize(n);
+  b->n_ops.resize(n);
+  b->n_dev.resize(n);
+  b->n_edges.resize(n);
+  std::vector<size_t> aoff(n + 1, 0);
+  for (int32_t i = 0; i < n; ++i) {
+    const size_t v = nops[i], e = nedges[i];
+    aoff[i + 1] = aoff[i] + align16(v * (d32[i] ? 4 : 8)) + align16(v * 2) + align16(v) +
+                  align16((v + 1) * 4) + align16(e * 4) + align16(v * 4);
+  }
+  CU(b->arena.ensure(aoff[n] + 16));
+  CU(b->rank.ensure(rank_words * 4 * size_t(std::max(n, 1))));
+  CU(b->ddesc.ensure(sizeof(dpro_k::DeltaDev) * std::max(n, 1)));
+  unsigned long long so = 0, sd = 0, sdo = 0, se = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    Cand& h = b->hc[i];
+    std::memset(&h, 0, sizeof h);
+    h.n = nops[i];
+    h.e = nedges[i];
+    h.d = deltas[i].n_devices;
+    h.op_off = so;
+    h.dev_off = sd;
+    h.dof_off = sdo;
+    h.dur64 = d32[i] ? 0 : 1;
+    size_t o = aoff[i];
+    h.dur = b->arena.as<void>(o); o += align16(size_t(h.n) * (d32[i] ? 4 : 8));
+    h.dev = b->arena.as<uint16_t>(o); o += align16(size_t(h.n) * 2);
+    h.flags = b->arena.as<uint8_t>(o); o += align16(h.n);
+    h.succ_off = b->arena.as<uint32_t>(o); o += align16((size_t(h.n) + 1) * 4);
+    h.succ = b->arena.as<uint32_t>(o); o += align16(size_t(h.e) * 4);
+    h.indeg = b->arena.as<uint32_t>(o);  // written by the merge
+    b->n_ops[i] = h.n;
+    b->n_dev[i] = h.d;
+    b->n_edges[i] = h.e;
+    b->max_d = std::max(b->max_d, h.d);
+    so += h.n;
+    sd += h.d;
+    sdo += h.d + 1;
+    se += h.e;
+  }
+  b->sum_n = so;
+  b->sum_d = sd;
+  b->sum_dof = sdo;
+  b->sum_e = se;
+  CU(cudaMemcpyAsync(b->ddesc.p, dd.data(), sizeof(dpro_k::DeltaDev) * n,
+                     cudaMemcpyHostToDevice, ctx->stream));
+  CU(b->desc.ensure(sizeof(Cand) * std::max(n, 1)));
+  CU(cudaMemcpyAsync(b->desc.p, b->hc.data(), sizeof(Cand) * n, cudaMemcpyHostToDevice,
+                     ctx->stream));
+  uint32_t max_n = 0;
+  for (int32_t i = 0; i < n; ++i) max_n = std::max(max_n, nops[i]);
+  b->res = r;
+  b->smem_ind = std::min(max_n, dpro_k::kMergeIndegSmem);
+  const int st = run_merge(ctx, b);
+  if (st != DPRO_OK) return st;
+  tr.mark("merge kernel", ctx->stream, true);
+  return finish_batch(ctx, b);
+}
+
+int run_merge(dpro_ctx* ctx, dpro_batch* b) {
+  if (b->n == 0) return DPRO_OK;
+  const size_t smem = size_t(b->smem_ind) * 4;
+  CU(cudaFuncSetAttribute(dpro_k::delta_merge_kernel,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dpro_k::delta_merge_kernel<<<std::min<int>(b->n, ctx->sm_count), dpro_k::kMergeThreads, smem,
+                               ctx->stream>>>(b->res->dev, b->ddesc.as<dpro_k::DeltaDev>(),
+                                              b->desc.as<Cand>(), b->n, b->rank.as<uint32_t>(),
+                                              b->smem_ind);
+  CU(cudaGetLastError());
+  return DPRO_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+dpro_resident* dpro_cuda_resident_create(dpro_ctx* ctx, const dpro_csr* c) {
+  if (!ctx || !c) return nullptr;
+  if (c->n_ops > 0 && (!c->dur || !c->dev || !c->flags || !c->succ_off) ||
+      (c->n_edges > 0 && !c->succ) || (c->dur_bits != 32 && c->dur_bits != 64)) {
+    ctx->err = "bad base CSR";
+    return nullptr;
+  }
+  if (cudaSetDevice(ctx->device) != cudaSuccess) return nullptr;
+  auto r = std::make_unique<dpro_resident>();
+  r->n = c->n_ops;
+  r->e = c->n_edges;
+  r->d = c->n_devices;
+  r->succ_off.assign(c->succ_off, c->succ_off + c->n_ops + 1);
+  r->succ.assign(c->succ, c->succ + c->n_edges);
+  r->indeg.assign(c->n_ops, 0);
+  for (uint32_t x : r->succ) r->indeg.at(x)++;
+  r->dur32 = c->dur_bits == 32 || fits_i32(static_cast<const int64_t*>(c->dur), c->n_ops);
+  const size_t v = c->n_ops, sd = align16(v * (r->dur32 ? 4 : 8)), s2 = align16(v * 2),
+               s1 = align16(v), so = align16((v + 1) * 4), se = align16(size_t(c->n_edges) * 4);
+  if (r->buf.ensure(sd + s2 + s1 + so + se + 16) != cudaSuccess) {
+    ctx->err = "resident base: out of device memory";
+    return nullptr;
+  }
+  std::vector<int32_t> d32;
+  const void* dsrc = c->dur;
+  if (r->dur32 && c->dur_bits == 64) {
+    d32.resize(v);
+    for (size_t i = 0; i < v; ++i) d32[i] = static_cast<int32_t>(static_cast<const int64_t*>(c->dur)[i]);
+    dsrc = d32.data();
+  }
+  char* p = r->buf.as<char>();
+  bool ok = cudaMemcpy(p, dsrc, v * (r->dur32 ? 4 : 8), cudaMemcpyHostToDevice) == cudaSuccess &&
+            cudaMemcpy(p + sd, c->dev, v * 2, cudaMemcpyHostToDevice) == cudaSuccess &&
+            cudaMemcpy(p + sd + s2, c->flags, v, cudaMemcpyHostToDevice) == cudaSuccess &&
+            cudaMemcpy(p + sd + s2 + s1, c->succ_off, (v + 1) * 4, cudaMemcpyHostToDevice) ==
+                cudaSuccess &&
+            (c->n_edges == 0 || cudaMemcpy(p + sd + s2 + s1 + so, c->succ,
+                                           size_t(c->n_edges) * 4,
+                                           cudaMemcpyHostToDevice) == cudaSuccess);
+  if (!ok) {
+    ctx->err = "resident base: upload failed";
+    return nullptr;
+  }
+  r->dev = {p, reinterpret_cast<const uint16_t*>(p + sd),
+            reinterpret_cast<const uint8_t*>(p + sd + s2),
+            reinterpret_cast<const uint32_t*>(p + sd + s2 + s1),
+            reinterpret_cast<const uint32_t*>(p + sd + s2 + s1 + so), r->n,
+            r->dur32 ? 0u : 1u};
+  return r.release();
+}
+
+void dpro_cuda_resident_destroy(dpro_ctx* ctx, dpro_resident* r) {
+  if (!r) return;
+  if (ctx) {
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+  }
+  delete r;
+}
+
+dpro_batch* dpro_cuda_batch_create_delta(dpro_ctx* ctx, const dpro_resident* r,
+                                         const dpro_delta* deltas, int32_t n) {
+  if (!ctx || !r || n < 0 || (n > 0 && !deltas)) {
+    if (ctx) ctx->err = "bad delta batch arguments";
+    return nullptr;
+  }
+  cudaSetDevice(ctx->device);
+  dpro_batch* b = acquire_batch(ctx, n, DPRO_DEVICE);
+  if (build_delta_batch(ctx, b, r, deltas) != DPRO_OK) {
+    delete b;
+    return nullptr;
+  }
+  return b;
+}
+
+int dpro_cuda_batch_sizes(dpro_batch* b, uint32_t* n_ops, uint32_t* n_edges,
+                          uint32_t* n_devices) {
+  if (!b) return DPRO_EINVAL;
+  for (int32_t i = 0; i < b->n; ++i) {
+    if (n_ops) n_ops[i] = b->n_ops[i];
+    if (n_edges) n_edges[i] = b->n_edges[i];
+    if (n_devices) n_devices[i] = b->n_dev[i];
+  }
+  return DPRO_OK;
+}
+
+int dpro_cuda_batch_prepare(dpro_ctx* ctx, dpro_batch* b) {
+  if (!ctx || !b) return DPRO_EINVAL;
+  CU(cudaSetDevice(ctx->device));
+  if (b->res) {
+    const int st = run_merge(ctx, b);
+    if (st != DPRO_OK) return st;
+  }
+  return run_pack(ctx, b);
+}
+
+int dpro_cuda_replay_delta_batch(dpro_ctx* ctx, const dpro_resident* r,
+                                 const dpro_delta* deltas, int32_t n, int64_t* makespan,
+                                 int32_t* status, int64_t* err) {
+  if (!ctx) return DPRO_EINVAL;
+  dpro_batch* b = dpro_cuda_batch_create_delta(ctx, r, deltas, n);
+  if (!b) return DPRO_EINVAL;
+  int st = dpro_cuda_batch_replay(ctx, b, 0);
+  if (st == DPRO_OK) st = dpro_cuda_batch_results(ctx, b, makespan, status, err, nullptr, nullptr);
+  dpro_cuda_batch_destroy(ctx, b);
+  return st;
+}
+
+dpro_batch* dpro_cuda_batch_create(dpro_ctx* ctx, const dpro_csr* cands,
+                                   int32_t n_cands, int32_t memspace) {
+  if (!ctx || (n_cands > 0 && !cands) || n_cands < 0 ||
+      (memspace != DPRO_HOST && memspace != DPRO_DEVICE)) {
+    if (ctx) ctx->err = "bad batch arguments";
+    return nullptr;
+  }
+  cudaSetDevice(ctx->device);
+  dpro_batch* b = acquire_batch(ctx, n_cands, memspace);
   if (build_batch(ctx, b, cands) != DPRO_OK) {
     delete b;
     return nullptr;

@@ -19,6 +19,8 @@
 // about s then -- so an event round touches one record per edge.
 #pragma once
 
+#include <cub/block/block_scan.cuh>
+
 #include "replay_kernel.cuh"
 
 namespace dpro_k {
@@ -64,6 +66,7 @@ struct PackOut {
   uint32_t* srcs;              // [sum n]
   uint32_t* cidx;              // [sum n] scratch: counter slot per op
   uint32_t* xoff;              // [sum (n+1)] scratch: expanded list offsets
+  uint8_t* spl;                // [sum n] scratch: spliced virtual op marks
   unsigned long long* r_off;   // per candidate offset into rec (in records)
   unsigned long long* e_off;   // per candidate offset into erec (in edges)
   unsigned long long* c_off;   // per candidate byte offset into cnt0
@@ -90,11 +93,12 @@ __device__ __forceinline__ uint4 make_rec(uint32_t s, const Cand& c, const uint3
 }
 
 // Walks the expanded successor list of op i (DFS through spliced virtual
-// successors, in order). emit(rec) per entry; returns false when a spliced
-// chain is deeper than kMaxSplice.
-template <bool kBuild, typename Emit>
-__device__ bool expand_list(uint32_t i, const Cand& c, const uint32_t* indeg,
-                            const uint32_t* cidx, const uint32_t* xoff, Emit&& emit) {
+// successors, in order): emit(s, spliced) per entry. spl[s] = 1 for a
+// virtual op with exactly one predecessor. Returns false when a spliced
+// chain is deeper than kMaxSplice. Lists with splices at most one level
+// deep (all generated graphs) stay in registers; deeper ones use a stack.
+template <typename Emit>
+__device__ bool walk_deep(uint32_t i, const Cand& c, const uint8_t* spl, Emit&& emit) {
   uint32_t stk_op[kMaxSplice], stk_k[kMaxSplice];
   int sp = 0;
   stk_op[0] = i;
@@ -107,25 +111,74 @@ __device__ bool expand_list(uint32_t i, const Cand& c, const uint32_t* indeg,
       continue;
     }
     const uint32_t s = c.succ[stk_k[sp]++];
-    if (spliced(c, indeg, s)) {
-      emit(make_uint4(s & kOpMask, 0u, kFVirt, 0u));  // stamp: virtual, not multi
+    const bool sv = spl[s];
+    emit(s, sv);
+    if (sv) {
       if (sp + 1 >= kMaxSplice) return false;
       ++sp;
       stk_op[sp] = s;
       stk_k[sp] = c.succ_off[s];
-    } else {
-      emit(kBuild ? make_rec(s, c, indeg, cidx, xoff) : make_uint4(0, 0, 0, 0));
     }
   }
 }
 
-// One block per candidate (grid-stride). indeg must be present (host upload
-// computes it; device batches without it go through count_indeg_kernel).
-__global__ void __launch_bounds__(256) pack_kernel(const Cand* __restrict__ cands,
-                                                   int n_cands, Scratch S,
-                                                   PackOut P) {
-  __shared__ uint32_t s_first, s_flags, s_ncnt, s_nsrc;
+template <typename Emit>
+__device__ bool walk_list(uint32_t i, const Cand& c, const uint8_t* spl, Emit&& emit) {
+  // first pass over the top-level list: any splice with a spliced child?
+  const uint32_t a = c.succ_off[i], z = c.succ_off[i + 1];
+  bool nested = false;
+  for (uint32_t k = a; k < z && !nested; ++k) {
+    const uint32_t s = c.succ[k];
+    if (spl[s])
+      for (uint32_t t = c.succ_off[s]; t < c.succ_off[s + 1]; ++t) nested |= spl[c.succ[t]] != 0;
+  }
+  if (nested) return walk_deep(i, c, spl, emit);
+  for (uint32_t k = a; k < z; ++k) {
+    const uint32_t s = c.succ[k];
+    const bool sv = spl[s];
+    emit(s, sv);
+    if (sv)
+      for (uint32_t t = c.succ_off[s]; t < c.succ_off[s + 1]; ++t) emit(c.succ[t], false);
+  }
+  return true;
+}
+
+constexpr int kPackThreads = 1024;
+constexpr uint32_t kPackHist = 4096;  // devices counted in shared memory
+
+// In-place exclusive scan of a[0..n) by one block; returns the total.
+template <int NT, typename Scan>
+__device__ uint32_t block_exclusive_scan(uint32_t* a, uint32_t n,
+                                         typename Scan::TempStorage& tmp, uint32_t& s_carry) {
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  for (uint32_t base = 0; base < n; base += NT) {
+    const uint32_t i = base + threadIdx.x;
+    const uint32_t v = i < n ? a[i] : 0u;
+    uint32_t excl, total;
+    Scan(tmp).ExclusiveSum(v, excl, total);
+    const uint32_t carry = s_carry;
+    if (i < n) a[i] = carry + excl;
+    __syncthreads();
+    if (threadIdx.x == 0) s_carry = carry + total;
+    __syncthreads();
+  }
+  return s_carry;
+}
+
+// One 1024-thread block per candidate, one block per SM (grid = SM count):
+// the ~150 candidates in flight keep their CSR and scratch in L2, so the
+// per-edge gathers of pass 2/3b are L2 hits. indeg must be present (host
+// upload or delta merge) or computed by count_indeg_kernel.
+__global__ void __launch_bounds__(kPackThreads, 1) pack_kernel(const Cand* __restrict__ cands,
+                                                               int n_cands, Scratch S,
+                                                               PackOut P) {
+  using Scan = cub::BlockScan<uint32_t, kPackThreads>;
+  __shared__ typename Scan::TempStorage scan_tmp;
+  __shared__ uint32_t s_first, s_flags, s_ncnt, s_nsrc, s_carry;
   __shared__ unsigned long long s_sum;
+  __shared__ uint32_t s_hist[kPackHist];
+  const uint32_t lane = threadIdx.x & 31;
   for (int cid = blockIdx.x; cid < n_cands; cid += gridDim.x) {
     const Cand c = cands[cid];
     const uint32_t n = c.n;
@@ -135,6 +188,8 @@ __global__ void __launch_bounds__(256) pack_kernel(const Cand* __restrict__ cand
     uint8_t* cnt0 = P.cnt0 + P.c_off[cid];
     uint32_t* srcs = P.srcs + c.op_off;
     uint32_t* cidx = P.cidx + c.op_off;
+    uint8_t* spl = P.spl + c.op_off;
+    uint32_t* xoff = P.xoff + P.r_off[cid];
     if (threadIdx.x == 0) {
       s_first = kNone;
       s_flags = (n >= kMaxOps ? kNfSize : 0u) | (c.d > kMaxDev ? kNfDev : 0u);
@@ -142,26 +197,51 @@ __global__ void __launch_bounds__(256) pack_kernel(const Cand* __restrict__ cand
       s_nsrc = 0;
       s_sum = 0;
     }
+    const bool hist_smem = c.d <= kPackHist;
+    for (uint32_t d = threadIdx.x; d < kPackHist; d += kPackThreads) s_hist[d] = 0;
+    uint32_t* devoff = S.devoff + c.dof_off;
+    if (!hist_smem)
+      for (uint32_t d = threadIdx.x; d <= c.d; d += kPackThreads) devoff[d] = 0;
     __syncthreads();
+    // pass 1 (coalesced): checks, counter slots and sources (warp-aggregated),
+    // splice marks, per-device op counts
     uint32_t flags = 0, first = kNone;
     unsigned long long sum = 0;
-    // pass 1: counter slots, sources, checks
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-      const long long du = ld_dur(c, i);
-      const bool virt = c.flags[i] & 1u;
-      const uint32_t ind = indeg[i];
-      if (!virt && du < 0) first = min(first, i);
-      if (!virt && (du > 0x7FFFFFFFLL || du < -0x80000000LL)) flags |= kNfDur;
-      if (!virt && du > 0) sum += static_cast<unsigned long long>(du);
-      if (ind >= 255u) flags |= kNfIndeg;
-      if (virt && ind == 0u) flags |= kNfVsrc;
-      if (!virt && c.dev[i] >= c.d) flags |= kNfDev;
-      if (ind >= 2u) {
-        const uint32_t slot = atomicAdd(&s_ncnt, 1u);
+    const uint32_t n_up = (n + 31) & ~31u;
+    for (uint32_t i = threadIdx.x; i < n_up; i += kPackThreads) {
+      const bool ok = i < n;
+      uint32_t ind = 0;
+      bool virt = false;
+      if (ok) {
+        const long long du = ld_dur(c, i);
+        virt = c.flags[i] & 1u;
+        ind = indeg[i];
+        const uint32_t dv = c.dev[i];
+        if (!virt && du < 0) first = min(first, i);
+        if (!virt && (du > 0x7FFFFFFFLL || du < -0x80000000LL)) flags |= kNfDur;
+        if (!virt && du > 0) sum += static_cast<unsigned long long>(du);
+        if (ind >= 255u) flags |= kNfIndeg;
+        if (virt && ind == 0u) flags |= kNfVsrc;
+        if (!virt && dv >= c.d) flags |= kNfDev;
+        spl[i] = virt && ind == 1u;
+        if (!virt && dv < c.d) atomicAdd(hist_smem ? &s_hist[dv] : &devoff[dv], 1u);
+      }
+      const bool multi = ok && ind >= 2u, src = ok && ind == 0u;
+      const unsigned mm = __ballot_sync(kFull, multi), ms = __ballot_sync(kFull, src);
+      uint32_t bm = 0, bs = 0;
+      if (lane == 0) {
+        if (mm) bm = atomicAdd(&s_ncnt, __popc(mm));
+        if (ms) bs = atomicAdd(&s_nsrc, __popc(ms));
+      }
+      bm = __shfl_sync(kFull, bm, 0);
+      bs = __shfl_sync(kFull, bs, 0);
+      const unsigned lt = (1u << lane) - 1u;
+      if (multi) {
+        const uint32_t slot = bm + __popc(mm & lt);
         cidx[i] = slot;
         if (slot < kMaxCnt) cnt0[slot] = static_cast<uint8_t>(min(ind, 255u));
-      } else if (ind == 0u) {
-        srcs[atomicAdd(&s_nsrc, 1u)] = i;
+      } else if (src) {
+        srcs[bs + __popc(ms & lt)] = i;
       }
     }
     if (first != kNone) atomicMin(&s_first, first);
@@ -169,53 +249,30 @@ __global__ void __launch_bounds__(256) pack_kernel(const Cand* __restrict__ cand
     if (sum) atomicAdd(&s_sum, sum);
     __syncthreads();
     // pass 2: expanded list sizes (spliced virtual ops own no list)
-    uint32_t* xoff = P.xoff + P.r_off[cid];
     bool deep = false;
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+    for (uint32_t i = threadIdx.x; i < n; i += kPackThreads) {
       uint32_t len = 0;
-      if (!spliced(c, indeg, i))
-        deep |= !expand_list<false>(i, c, indeg, cidx, xoff, [&](const uint4&) { ++len; });
+      if (!spl[i]) deep |= !walk_list(i, c, spl, [&](uint32_t, bool) { ++len; });
       xoff[i] = len;
     }
     if (deep) atomicOr(&s_flags, kNfChain);
     __syncthreads();
-    // exclusive scan of xoff[0..n) (chunked block scan), xoff[n] = total
-    {
-      __shared__ uint32_t s_part[256];
-      const uint32_t chunk = (n + blockDim.x - 1) / blockDim.x;
-      const uint32_t lo = min(n, threadIdx.x * chunk), hi = min(n, lo + chunk);
-      uint32_t sum = 0;
-      for (uint32_t i = lo; i < hi; ++i) sum += xoff[i];
-      s_part[threadIdx.x] = sum;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        uint32_t run = 0;
-        for (uint32_t t = 0; t < blockDim.x; ++t) {
-          const uint32_t v = s_part[t];
-          s_part[t] = run;
-          run += v;
-        }
-        xoff[n] = run;
-      }
-      __syncthreads();
-      uint32_t run = s_part[threadIdx.x];
-      for (uint32_t i = lo; i < hi; ++i) {
-        const uint32_t v = xoff[i];
-        xoff[i] = run;
-        run += v;
-      }
-    }
+    const uint32_t total = block_exclusive_scan<kPackThreads, Scan>(xoff, n, scan_tmp, s_carry);
+    if (threadIdx.x == 0) xoff[n] = total;
     __syncthreads();
-    // pass 3: records and expanded lists
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-      rec[i] = make_rec(i, c, indeg, cidx, xoff);
-      if (!spliced(c, indeg, i)) {
-        uint4* dst = erec + xoff[i];
-        expand_list<true>(i, c, indeg, cidx, xoff, [&](const uint4& r) { *dst++ = r; });
-      }
+    // pass 3a (coalesced): every op's record
+    for (uint32_t i = threadIdx.x; i < n; i += kPackThreads) rec[i] = make_rec(i, c, indeg, cidx, xoff);
+    if (threadIdx.x == 0) rec[n] = make_uint4(0u, 0u, 0u, total);
+    __syncthreads();  // rec[] visible to the block
+    // pass 3b: expanded lists = gathered records (stamps for spliced ops)
+    for (uint32_t i = threadIdx.x; i < n; i += kPackThreads) {
+      if (spl[i]) continue;
+      uint4* dst = erec + xoff[i];
+      walk_list(i, c, spl, [&](uint32_t s, bool sv) {  // erec is write-once: stream it
+        __stcs(dst++, sv ? make_uint4(s & kOpMask, 0u, kFVirt, 0u) : rec[s]);
+      });
     }
     if (threadIdx.x == 0) {
-      rec[n] = make_uint4(0u, 0u, 0u, xoff[n]);
       PackInfo inf;
       inf.first_missing = s_first;
       inf.not_fast = s_flags | (s_sum >= 0x7FFFFFFFull ? kNfDur : 0u) |
@@ -225,22 +282,12 @@ __global__ void __launch_bounds__(256) pack_kernel(const Cand* __restrict__ cand
       inf.dur_sum = s_sum;
       P.info[cid] = inf;
     }
-    // timeline regions: per-device non-virtual op counts, exclusive scan
-    uint32_t* devoff = S.devoff + c.dof_off;
-    for (uint32_t d = threadIdx.x; d <= c.d; d += blockDim.x) devoff[d] = 0;
+    // timeline regions: exclusive scan of the per-device counts
+    if (hist_smem)
+      for (uint32_t d = threadIdx.x; d < c.d; d += kPackThreads) devoff[d] = s_hist[d];
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x)
-      if (!(c.flags[i] & 1u) && c.dev[i] < c.d) atomicAdd(&devoff[c.dev[i]], 1u);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      uint32_t run = 0;
-      for (uint32_t d = 0; d < c.d; ++d) {
-        const uint32_t v = devoff[d];
-        devoff[d] = run;
-        run += v;
-      }
-      devoff[c.d] = run;
-    }
+    const uint32_t dtot = block_exclusive_scan<kPackThreads, Scan>(devoff, c.d, scan_tmp, s_carry);
+    if (threadIdx.x == 0) devoff[c.d] = dtot;
     __syncthreads();
   }
 }

@@ -96,6 +96,15 @@ class Engine:
               memspace: int = N.DPRO_HOST) -> "Batch":
         return Batch(self, cands, memspace)
 
+    def resident(self, base: Csr | N.DproCsr) -> "Resident":
+        """Uploads a base graph that stays in HBM for delta batches."""
+        return Resident(self, base)
+
+    def delta_batch(self, resident: "Resident", deltas) -> "Batch":
+        """Batch of candidates given as deltas against `resident` (a
+        DeltaSet or a ctypes array of N.DproDelta): merged on the GPU."""
+        return Batch(self, deltas, N.DPRO_DEVICE, resident=resident)
+
     def tsync_grid(self, cluster, bytes_: Sequence[int], ks: Sequence[int]):
         """dpro_cuda_tsync_grid: (makespans, statuses)."""
         holder = N.ClusterDescHolder(cluster)
@@ -110,22 +119,62 @@ class Engine:
         return out, st
 
 
-class Batch:
-    def __init__(self, engine: Engine, cands, memspace: int):
+class Resident:
+    """A base graph resident in HBM (dpro_cuda_resident_create)."""
+
+    def __init__(self, engine: Engine, base):
         self.engine = engine
-        self._keep = list(cands)
-        structs = [c.as_struct() if isinstance(c, Csr) else c for c in cands]
-        self.n = len(structs)
-        self.n_ops = np.array([s.n_ops for s in structs], np.int64)
-        self.n_edges = np.array([s.n_edges for s in structs], np.int64)
-        self.n_devices = np.array([s.n_devices for s in structs], np.int64)
+        self._keep = base
+        st = base.as_struct() if isinstance(base, Csr) else base
+        self.n_ops = int(st.n_ops)
+        self.handle = N.lib.dpro_cuda_resident_create(engine.ctx, C.byref(st))
+        if not self.handle:
+            _check(engine.ctx, N.DPRO_EINVAL, "resident_create")
+
+    def close(self) -> None:
+        if self.handle:
+            N.lib.dpro_cuda_resident_destroy(self.engine.ctx, self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Batch:
+    def __init__(self, engine: Engine, cands, memspace: int, resident: Resident | None = None):
+        self.engine = engine
+        self._keep = cands if resident is not None else list(cands)
+        self.with_schedule = False
+        self.handle = None
+        if resident is not None:  # delta batch
+            arr, n = (cands.array, cands.n) if hasattr(cands, "array") else (cands, len(cands))
+            self.n = n
+            counts = [(resident.n_ops - arr[i].n_removed + arr[i].n_new, arr[i].n_devices)
+                      for i in range(n)]
+            self.n_ops = np.array([c[0] for c in counts], np.int64)
+            self.n_devices = np.array([c[1] for c in counts], np.int64)
+            self.handle = N.lib.dpro_cuda_batch_create_delta(engine.ctx, resident.handle,
+                                                             C.cast(arr, C.c_void_p), n)
+            if not self.handle:
+                _check(engine.ctx, N.DPRO_EINVAL, "batch_create_delta")
+            ne = np.zeros(max(1, n), np.uint32)
+            N.lib.dpro_cuda_batch_sizes(self.handle, None, N.ptr(ne), None)
+            self.n_edges = ne[:n].astype(np.int64)
+        else:
+            structs = [c.as_struct() if isinstance(c, Csr) else c for c in cands]
+            self.n = len(structs)
+            self.n_ops = np.array([s.n_ops for s in structs], np.int64)
+            self.n_edges = np.array([s.n_edges for s in structs], np.int64)
+            self.n_devices = np.array([s.n_devices for s in structs], np.int64)
+            arr = (N.DproCsr * max(1, self.n))(*structs)
+            self.handle = N.lib.dpro_cuda_batch_create(engine.ctx, arr, self.n, memspace)
+            if not self.handle:
+                _check(engine.ctx, N.DPRO_EINVAL, "batch_create")
         self.op_off = np.zeros(self.n + 1, np.int64)
         self.op_off[1:] = np.cumsum(self.n_ops)
-        arr = (N.DproCsr * max(1, self.n))(*structs)
-        self.handle = N.lib.dpro_cuda_batch_create(engine.ctx, arr, self.n, memspace)
-        if not self.handle:
-            _check(engine.ctx, N.DPRO_EINVAL, "batch_create")
-        self.with_schedule = False
 
     def close(self) -> None:
         if self.handle:
@@ -140,6 +189,12 @@ class Batch:
 
     def algorithmic_bytes(self) -> int:
         return int(32 * self.n_ops.sum() + 4 * self.n_edges.sum())
+
+    def prepare(self) -> None:
+        """Re-runs the device-side preparation (delta merge, pack) on the
+        inputs already in HBM."""
+        _check(self.engine.ctx, N.lib.dpro_cuda_batch_prepare(self.engine.ctx, self.handle),
+               "batch_prepare")
 
     def replay(self, want_schedule: bool = True) -> None:
         """Asynchronous on the engine's stream."""

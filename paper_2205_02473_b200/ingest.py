@@ -312,9 +312,8 @@ class LayeredBase:
             N.lib.dpro_base_free(self.handle)
             self.handle = None
 
-    def candidates(self, specs: Sequence[tuple[Sequence[Sequence[int]], Sequence[int]]],
-                   threads: int = 8) -> list[NativeGraph]:
-        """[(groups, ks), ...] -> graphs by delta construction."""
+    @staticmethod
+    def _spec_arrays(specs):
         n = len(specs)
         n_groups = np.array([len(g) for g, _ in specs], np.int32)
         spec_off = np.zeros(n, np.int64)
@@ -324,6 +323,13 @@ class LayeredBase:
         group_off[1:] = np.cumsum(sizes)
         members = np.ascontiguousarray([i for g, _ in specs for m_ in g for i in m_], np.int32)
         ks = np.ascontiguousarray([k for _, kk in specs for k in kk], np.int32)
+        return n_groups, spec_off, group_off, members, ks
+
+    def candidates(self, specs: Sequence[tuple[Sequence[Sequence[int]], Sequence[int]]],
+                   threads: int = 8) -> list[NativeGraph]:
+        """[(groups, ks), ...] -> graphs by delta construction (merged on the host)."""
+        n = len(specs)
+        n_groups, spec_off, group_off, members, ks = self._spec_arrays(specs)
         out = (C.c_void_p * n)()
         rc = N.lib.dpro_graph_from_base_batch(self.handle, n, N.ptr(n_groups), N.ptr(spec_off),
                                               N.ptr(group_off), N.ptr(members), N.ptr(ks),
@@ -331,6 +337,59 @@ class LayeredBase:
         if rc != N.DPRO_OK:
             raise Error(N.lib.dpro_graph_last_error().decode())
         return [NativeGraph(out[i]) for i in range(n)]
+
+
+    def deltas(self, specs: Sequence[tuple[Sequence[Sequence[int]], Sequence[int]]],
+               threads: int = 8) -> "DeltaSet":
+        """[(groups, ks), ...] -> unmerged deltas for Engine.delta_batch."""
+        n = len(specs)
+        n_groups, spec_off, group_off, members, ks = self._spec_arrays(specs)
+        out = C.c_void_p()
+        rc = N.lib.dpro_base_delta_batch(self.handle, n, N.ptr(n_groups), N.ptr(spec_off),
+                                         N.ptr(group_off), N.ptr(members), N.ptr(ks), threads,
+                                         C.byref(out))
+        if rc != N.DPRO_OK:
+            raise Error(N.lib.dpro_graph_last_error().decode())
+        return DeltaSet(out.value, self)
+
+    def graph(self) -> "BaseGraphView":
+        """The base graph's CSR / ids (owned by the base)."""
+        return BaseGraphView(N.lib.dpro_base_graph(self.handle), self)
+
+
+class BaseGraphView(NativeGraph):
+    """Non-owning NativeGraph over a base's graph."""
+
+    def __init__(self, handle: int, owner):
+        self._owner = owner
+        super().__init__(handle)
+
+    def __del__(self):  # pragma: no cover - owned by the base
+        self.handle = None
+
+
+class DeltaSet:
+    """Owning handle of a dpro_delta_set (candidates as deltas)."""
+
+    def __init__(self, handle: int, base: LayeredBase):
+        self.handle, self._base = handle, base
+        self.n = N.lib.dpro_delta_set_size(handle)
+        self.array = C.cast(N.lib.dpro_delta_set_deltas(handle),
+                            C.POINTER(N.DproDelta * max(1, self.n))).contents
+
+    def __len__(self) -> int:
+        return self.n
+
+    def __getitem__(self, i: int) -> N.DproDelta:
+        return self.array[i]
+
+    def device_str(self, cand: int, d: int) -> str:
+        return N.lib.dpro_delta_set_device_str(self.handle, cand, d).decode()
+
+    def __del__(self):  # pragma: no cover
+        if getattr(self, "handle", None):
+            N.lib.dpro_delta_set_free(self.handle)
+            self.handle = None
 
 
 def layered_graphs(model: LayeredModel, cluster: ClusterSpec, part_k: np.ndarray,

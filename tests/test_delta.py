@@ -1,0 +1,128 @@
+"""Resident base graph + per-candidate deltas (dpro_delta): the host delta
+emission against the full rebuild (CPU), and the GPU merge + replay against
+the host-merged candidates (bit-exact start/end/makespan, GPU)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from paper_2205_02473_b200 import _native as N
+from paper_2205_02473_b200.graph import synth_cluster
+from paper_2205_02473_b200.ingest import LayeredBase, LayeredModel
+
+
+def _arr(p, dt, n):
+    if n == 0:
+        return np.zeros(0, dt)
+    return np.ctypeslib.as_array(C.cast(p, C.POINTER(np.ctypeslib.as_ctypes_type(dt))),
+                                 (n,)).copy()
+
+
+def merge_host(bc, nb, d):
+    """Checker: the merge include/dpro_cuda.h defines for a dpro_delta."""
+    rem = _arr(d.removed, np.uint32, d.n_removed)
+    pos = _arr(d.new_pos, np.uint32, d.n_new)
+    keep = np.ones(nb, bool)
+    keep[rem] = False
+    b = np.arange(nb)
+    fb = b - np.searchsorted(rem, b, "left") + np.searchsorted(pos, b, "right")
+    fn = pos - np.searchsorted(rem, pos, "left") + np.arange(d.n_new)
+    n = nb - d.n_removed + d.n_new
+    dur = np.zeros(n, np.int64)
+    dev = np.zeros(n, np.uint16)
+    fl = np.zeros(n, np.uint8)
+    dur[fb[keep]], dev[fb[keep]], fl[fb[keep]] = bc.dur[keep], bc.dev[keep], bc.flags[keep]
+    dur[fn] = _arr(d.new_dur, np.int64, d.n_new)
+    dev[fn] = _arr(d.new_dev, np.uint16, d.n_new)
+    fl[fn] = _arr(d.new_flags, np.uint8, d.n_new)
+    succ = [[] for _ in range(n)]
+    for x in np.flatnonzero(keep):
+        succ[fb[x]] += [int(fb[s]) for s in bc.succ[bc.succ_off[x]:bc.succ_off[x + 1]] if keep[s]]
+    nso = _arr(d.new_succ_off, np.uint32, d.n_new + 1)
+    ns = _arr(d.new_succ, np.uint32, int(nso[-1]))
+    for k in range(d.n_new):
+        succ[fn[k]] += ns[nso[k]:nso[k + 1]].tolist()
+    for a, c in zip(_arr(d.extra_src, np.uint32, d.n_extra), _arr(d.extra_dst, np.uint32, d.n_extra)):
+        succ[fb[a]].append(int(c))
+    return dur, dev, fl, [sorted(x) for x in succ]
+
+
+def _setup(scheme, W, S, L, n, seed):
+    rng = np.random.default_rng(seed)
+    c = synth_cluster(scheme, W, S, 12500.0, 5.0)
+    m = LayeredModel(rng.integers(10, 400, L).tolist(), rng.integers(10, 800, L).tolist(),
+                     rng.integers(1000, 4_000_000, L).tolist(), 5)
+    specs = []
+    for _ in range(n):
+        cuts = sorted(rng.choice(np.arange(1, L), int(rng.integers(0, L // 2)),
+                                 replace=False).tolist())
+        groups, a = [], 0
+        for cp in cuts + [L]:
+            groups.append(list(range(a, cp)))
+            a = cp
+        specs.append((groups, [int(rng.integers(1, 5)) for _ in groups]))
+    return LayeredBase(m, c), specs
+
+
+CASES = [("ring", 4, 0, 8), ("ps", 4, 2, 10), ("ring", 8, 0, 16), ("ps", 16, 4, 12)]
+
+
+@pytest.mark.parametrize("scheme,W,S,L", CASES)
+def test_deltas_merge_to_the_full_candidates(scheme, W, S, L):
+    base, specs = _setup(scheme, W, S, L, 12, W * L)
+    bv = base.graph()
+    full = base.candidates(specs)
+    ds = base.deltas(specs)
+    for i, g in enumerate(full):
+        dur, dev, fl, succ = merge_host(bv.csr, bv.n_ops, ds[i])
+        cs = g.csr
+        assert len(dur) == g.n_ops
+        assert np.array_equal(dur, cs.dur) and np.array_equal(fl, cs.flags)
+        strs = g.device_strs()
+        assert [ds.device_str(i, int(x)) for x in dev] == [strs[int(x)] for x in cs.dev]
+        for k in range(g.n_ops):
+            assert succ[k] == cs.succ[cs.succ_off[k]:cs.succ_off[k + 1]].tolist(), (i, k)
+
+
+def test_delta_symbols_are_exported():
+    for name in ("dpro_cuda_resident_create", "dpro_cuda_batch_create_delta",
+                 "dpro_cuda_replay_delta_batch", "dpro_base_delta_batch"):
+        assert hasattr(N.lib, name)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("scheme,W,S,L", CASES + [("ring", 8, 0, 48)])
+def test_gpu_merge_replays_like_full_candidates(engine, scheme, W, S, L):
+    base, specs = _setup(scheme, W, S, L, 64, 1000 + W * L)
+    full = base.candidates(specs)
+    fb = engine.batch([g.csr for g in full])
+    fb.replay(want_schedule=True)
+    ms0, st0, er0, s0, e0 = fb.results(schedule=True)
+    res = engine.resident(base.graph().csr)
+    db = engine.delta_batch(res, base.deltas(specs))
+    db.replay(want_schedule=True)
+    ms1, st1, er1, s1, e1 = db.results(schedule=True)
+    assert np.array_equal(st0, st1) and np.all(st0 == 0)
+    assert np.array_equal(ms0, ms1)
+    assert np.array_equal(s0, s1) and np.array_equal(e0, e1)
+    # critical paths on the merged CSR equal those of the host-merged ones
+    for p0, p1 in zip(fb.critical_paths(), db.critical_paths()):
+        assert np.array_equal(p0, p1)
+
+
+@pytest.mark.gpu
+def test_gpu_delta_one_shot_and_makespan_only(engine):
+    base, specs = _setup("ps", 16, 4, 24, 256, 7)
+    full = base.candidates(specs)
+    fb = engine.batch([g.csr for g in full])
+    fb.replay(want_schedule=False)
+    ms0, *_ = fb.results()
+    res = engine.resident(base.graph().csr)
+    ds = base.deltas(specs)
+    ms = np.zeros(len(specs), np.int64)
+    st = np.zeros(len(specs), np.int32)
+    er = np.zeros(len(specs), np.int64)
+    rc = N.lib.dpro_cuda_replay_delta_batch(engine.ctx, res.handle, C.cast(ds.array, C.c_void_p),
+                                            len(specs), N.ptr(ms), N.ptr(st), N.ptr(er))
+    assert rc == 0 and np.all(st == 0)
+    assert np.array_equal(ms, ms0)
