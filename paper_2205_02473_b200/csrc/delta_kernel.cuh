@@ -41,7 +41,7 @@ struct DeltaDev {
   const uint32_t* extra_dst;
   const uint32_t* cut;
   uint32_t n_removed, n_new, n_extra, n_cut;
-  unsigned long long rank_off;  // words into the rank scratch
+  unsigned long long rank_off;  // words into the rank scratch (3W+1 rank words, nb map)
 };
 
 constexpr int kMergeThreads = 1024;
@@ -114,6 +114,11 @@ __global__ void __launch_bounds__(kMergeThreads, 1)
     }
     __syncthreads();
     const Ranks R{bits, rpre, qpre, D.new_pos, D.n_removed, D.n_new, nb};
+    // final index of every base op (removed ones: UINT32_MAX)
+    uint32_t* fmap = qpre + W + 1;
+    for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x)
+      fmap[b] = R.removed(b) ? UINT32_MAX : R.f(b);
+    __syncthreads();
     uint32_t* ind_g = const_cast<uint32_t*>(C.indeg);
     const bool ind_smem = C.n <= smem_ind;
     uint32_t* ind = ind_smem ? s_ind : ind_g;
@@ -124,8 +129,8 @@ __global__ void __launch_bounds__(kMergeThreads, 1)
     uint8_t* flags = const_cast<uint8_t*>(C.flags);
     // ---- per-op fields and out-degrees (written at off[f + 1])
     for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) {
-      if (R.removed(b)) continue;
-      const uint32_t f = R.f(b);
+      const uint32_t f = fmap[b];
+      if (f == UINT32_MAX) continue;
       const long long d = B.dur64 ? __ldg(static_cast<const long long*>(B.dur) + b)
                                   : (long long)__ldg(static_cast<const int*>(B.dur) + b);
       if (C.dur64) static_cast<long long*>(const_cast<void*>(C.dur))[f] = d;
@@ -135,7 +140,7 @@ __global__ void __launch_bounds__(kMergeThreads, 1)
       uint32_t deg = 0;
       const uint32_t e1 = __ldg(B.succ_off + b + 1);
       for (uint32_t e = __ldg(B.succ_off + b); e < e1; ++e)
-        deg += !R.removed(__ldg(B.succ + e)) && !is_cut(D, e);
+        deg += fmap[__ldg(B.succ + e)] != UINT32_MAX && !is_cut(D, e);
       if (D.n_extra) {
         const uint32_t x0 = lower_bound_u32(D.extra_src, D.n_extra, b);
         uint32_t x1 = x0;
@@ -173,8 +178,9 @@ __global__ void __launch_bounds__(kMergeThreads, 1)
     }
     // ---- successor lists
     for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) {
-      if (R.removed(b)) continue;
-      uint32_t o = off[R.f(b)];
+      const uint32_t fb = fmap[b];
+      if (fb == UINT32_MAX) continue;
+      uint32_t o = off[fb];
       uint32_t e = __ldg(B.succ_off + b);
       const uint32_t e1 = __ldg(B.succ_off + b + 1);
       uint32_t x = 0, x1 = 0;
@@ -187,9 +193,9 @@ __global__ void __launch_bounds__(kMergeThreads, 1)
       auto advance = [&]() {
         nxt = UINT32_MAX;
         for (; e < e1; ++e) {
-          const uint32_t s = __ldg(B.succ + e);
-          if (!R.removed(s) && !is_cut(D, e)) {
-            nxt = R.f(s);
+          const uint32_t m = fmap[__ldg(B.succ + e)];
+          if (m != UINT32_MAX && !is_cut(D, e)) {
+            nxt = m;
             ++e;
             break;
           }

@@ -184,6 +184,7 @@ struct dpro_ctx {
   std::string err;
   HostPinned staging;
   std::unique_ptr<Pool> pool;  // created on first use
+  int pack_clusters = 0;       // co-resident pack clusters (queried once)
   Pool& workers() {
     if (!pool) pool = std::make_unique<Pool>();
     return *pool;
@@ -530,7 +531,25 @@ int run_pack(dpro_ctx* ctx, dpro_batch* b) {
     if (need_indeg)
       dpro_k::count_indeg_kernel<<<grid, 256, 0, ctx->stream>>>(b->desc.as<Cand>(), n, b->S);
     Tracer tr;
-    dpro_k::pack_kernel<<<std::min<int>(n, ctx->sm_count), dpro_k::kPackThreads, 0,
+    if (ctx->pack_clusters == 0) {  // co-resident clusters of the pack kernel
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(dpro_k::kPackCluster * (ctx->sm_count / dpro_k::kPackCluster));
+      cfg.blockDim = dim3(dpro_k::kPackThreads);
+      cudaLaunchAttribute attr;
+      attr.id = cudaLaunchAttributeClusterDimension;
+      attr.val.clusterDim.x = dpro_k::kPackCluster;
+      attr.val.clusterDim.y = attr.val.clusterDim.z = 1;
+      cfg.attrs = &attr;
+      cfg.numAttrs = 1;
+      int m = 0;
+      if (cudaOccupancyMaxActiveClusters(&m, dpro_k::pack_kernel, &cfg) != cudaSuccess || m < 1)
+        m = ctx->sm_count / dpro_k::kPackCluster;
+      ctx->pack_clusters = m;
+      if (std::getenv("DPRO_TRACE"))
+        std::fprintf(stderr, "[dpro] pack kernel: %d co-resident clusters\n", m);
+    }
+    const int clusters = std::max(1, std::min<int>(n, ctx->pack_clusters));
+    dpro_k::pack_kernel<<<clusters * dpro_k::kPackCluster, dpro_k::kPackThreads, 0,
                           ctx->stream>>>(b->desc.as<Cand>(), n, b->S, b->P);
     CU(cudaGetLastError());
     tr.mark("pack kernel", ctx->stream, true);
@@ -703,7 +722,7 @@ int build_delta_batch(dpro_ctx* ctx, dpro_batch* b, const dpro_resident* r,
   CU(ctx->staging.ensure(boff[n] + 16));
   char* stage = static_cast<char*>(ctx->staging.p);
   const uint32_t W = (r->n >> 5) + 1;
-  const size_t rank_words = 3 * size_t(W) + 1;
+  const size_t rank_words = (3 * size_t(W) + 1 + r->n + 3) & ~size_t(3);
   std::vector<dpro_k::DeltaDev> dd(n);
   std::vector<uint32_t> nops(n), nedges(n);
   std::vector<uint8_t> d32(n);

@@ -19,6 +19,7 @@
 // about s then -- so an event round touches one record per edge.
 #pragma once
 
+#include <cooperative_groups.h>
 #include <cub/block/block_scan.cuh>
 
 #include "replay_kernel.cuh"
@@ -143,6 +144,122 @@ __device__ bool walk_list(uint32_t i, const Cand& c, const uint8_t* spl, Emit&& 
   return true;
 }
 
+// Warp-cooperative list passes for candidates without nested splices: a
+// warp takes 32 consecutive ops; their successor lists are one contiguous
+// range of succ[], which the lanes stride over (coalesced reads, 32 gathers
+// in flight, coalesced erec writes). src(k) comes from a shuffle binary
+// search over the 33 list offsets held one per lane.
+__device__ __forceinline__ uint32_t warp_src(uint32_t off_lane, uint32_t k) {
+  uint32_t j = 0;
+#pragma unroll
+  for (uint32_t step = 16; step; step >>= 1) {
+    const uint32_t v = __shfl_sync(kFull, off_lane, j + step);
+    if (j + step < 32 && v <= k) j += step;
+  }
+  return j;
+}
+
+// Expanded list sizes of ops [i0, i1) into xoff (0 for spliced ops).
+// Unrolled by 4 so four coalesced succ loads and four gathers are in
+// flight per lane (the loop is latency-bound otherwise).
+__device__ void coop_sizes(const Cand& c, const uint8_t* spl, uint32_t i0, uint32_t i1,
+                           uint32_t* xoff, uint32_t* wlen) {
+  constexpr int U = 4;
+  const uint32_t lane = threadIdx.x & 31;
+  wlen[lane] = 0;
+  const uint32_t me = min(i0 + lane, i1);
+  const uint32_t off = c.succ_off[me];
+  const bool mysp = i0 + lane < i1 && spl[i0 + lane];
+  const uint32_t spmask = __ballot_sync(kFull, mysp);
+  const uint32_t E0 = __shfl_sync(kFull, off, 0), E1 = c.succ_off[i1];
+  __syncwarp();
+  for (uint32_t kb = E0; kb < E1; kb += 32 * U) {
+    uint32_t sv[U], src[U];
+    bool live[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t k = kb + 32 * u + lane;
+      src[u] = warp_src(off, k);
+      live[u] = k < E1 && !((spmask >> src[u]) & 1u);
+      sv[u] = live[u] ? c.succ[k] : 0u;
+    }
+    uint32_t sp[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) sp[u] = live[u] ? __ldcg(spl + sv[u]) : 0u;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (live[u])
+        atomicAdd(&wlen[src[u]], sp[u] ? 1u + c.succ_off[sv[u] + 1] - c.succ_off[sv[u]] : 1u);
+  }
+  __syncwarp();
+  if (i0 + lane < i1) xoff[i0 + lane] = mysp ? 0u : wlen[lane];
+  __syncwarp();
+}
+
+// Expanded lists of ops [i0, i1) into erec (records gathered from rec);
+// unrolled by 2 with all loads of both halves issued first.
+__device__ void coop_lists(const Cand& c, const uint8_t* spl, uint32_t i0, uint32_t i1,
+                           const uint32_t* xoff, const uint4* rec, uint4* erec, uint32_t* segp) {
+  constexpr int U = 2;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t me = min(i0 + lane, i1);
+  const uint32_t off = c.succ_off[me];
+  const uint32_t xo = i0 + lane < i1 ? xoff[i0 + lane] : 0u;
+  const bool mysp = i0 + lane < i1 && spl[i0 + lane];
+  const uint32_t spmask = __ballot_sync(kFull, mysp);
+  const uint32_t E0 = __shfl_sync(kFull, off, 0), E1 = c.succ_off[i1];
+  uint32_t carry = 0;  // splice extras of earlier edges of this chunk
+  for (uint32_t kb = E0; kb < E1; kb += 32 * U) {
+    uint32_t s[U], src[U];
+    bool live[U], sv[U];
+    uint4 r[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t k = kb + 32 * u + lane;
+      src[u] = warp_src(off, k);
+      live[u] = k < E1 && !((spmask >> src[u]) & 1u);
+      s[u] = live[u] ? c.succ[k] : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) sv[u] = live[u] && __ldcg(spl + s[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      r[u] = (live[u] && !sv[u]) ? __ldcg(rec + s[u]) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t k = kb + 32 * u + lane;
+      const uint32_t o_src = __shfl_sync(kFull, off, src[u]);
+      const uint32_t x_src = __shfl_sync(kFull, xo, src[u]);
+      uint32_t sa = 0, sz = 0;
+      if (sv[u]) {
+        sa = c.succ_off[s[u]];
+        sz = c.succ_off[s[u] + 1];
+      }
+      const uint32_t ex = sz - sa;
+      uint32_t incl = ex;  // inclusive warp scan of the extras
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, incl, d);
+        if ((int)lane >= d) incl += y;
+      }
+      const uint32_t P = carry + incl - ex;
+      if (live[u] && k == o_src) segp[src[u]] = P;
+      __syncwarp();
+      if (live[u]) {
+        uint32_t pos = x_src + (k - o_src) + (P - segp[src[u]]);
+        if (sv[u]) {
+          __stcs(erec + pos, make_uint4(s[u] & kOpMask, 0u, kFVirt, 0u));
+          for (uint32_t t = sa; t < sz; ++t) __stcs(erec + (++pos), __ldcg(rec + c.succ[t]));
+        } else {
+          __stcs(erec + pos, r[u]);
+        }
+      }
+      carry += __shfl_sync(kFull, incl, 31);
+      __syncwarp();
+    }
+  }
+}
+
 constexpr int kPackThreads = 1024;
 constexpr uint32_t kPackHist = 4096;  // devices counted in shared memory
 
@@ -166,20 +283,40 @@ __device__ uint32_t block_exclusive_scan(uint32_t* a, uint32_t n,
   return s_carry;
 }
 
-// One 1024-thread block per candidate, one block per SM (grid = SM count):
-// the ~150 candidates in flight keep their CSR and scratch in L2, so the
-// per-edge gathers of pass 2/3b are L2 hits. indeg must be present (host
-// upload or delta merge) or computed by count_indeg_kernel.
-__global__ void __launch_bounds__(kPackThreads, 1) pack_kernel(const Cand* __restrict__ cands,
-                                                               int n_cands, Scratch S,
-                                                               PackOut P) {
+// One candidate per thread-block CLUSTER of kPackCluster CTAs (1024 threads
+// each, one per SM). Larger clusters keep fewer candidates in flight so their
+// CSR, scratch and records stay in L2 across the passes, but on config 2
+// (1,024 candidates, B200) the lost memory-level parallelism costs more:
+// cluster 1: 2.49 ms, 2: 3.09 ms, 4: 4.38 ms (33 co-resident clusters), so
+// kPackCluster = 1 (one candidate per SM). Rank r owns op chunks
+// [C*r/R, C*(r+1)/R) (chunks of 32 ops); per-candidate counters live in rank
+// 0's shared memory (DSMEM atomics); cluster barriers separate the passes,
+// and records written by other SMs are read through L2 (__ldcg). indeg must
+// be present (host upload / delta merge) or computed by count_indeg_kernel.
+constexpr int kPackCluster = 1;
+
+__global__ void __cluster_dims__(kPackCluster, 1, 1) __launch_bounds__(kPackThreads, 1)
+    pack_kernel(const Cand* __restrict__ cands, int n_cands, Scratch S, PackOut P) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
   using Scan = cub::BlockScan<uint32_t, kPackThreads>;
   __shared__ typename Scan::TempStorage scan_tmp;
-  __shared__ uint32_t s_first, s_flags, s_ncnt, s_nsrc, s_carry;
-  __shared__ unsigned long long s_sum;
-  __shared__ uint32_t s_hist[kPackHist];
-  const uint32_t lane = threadIdx.x & 31;
-  for (int cid = blockIdx.x; cid < n_cands; cid += gridDim.x) {
+  struct Ctr {  // per-candidate counters, used in rank 0's copy
+    unsigned long long sum;
+    uint32_t first, flags, ncnt, nsrc, nested;
+    uint32_t tot[kPackCluster];
+    uint32_t hist[kPackHist];
+  };
+  __shared__ Ctr s_ctr;
+  __shared__ uint32_t s_carry, s_len;
+  __shared__ uint32_t s_warp[kPackThreads];  // per-warp 32-word scratch
+  __shared__ uint32_t s_lhist[kPackHist];    // this CTA's device counts
+  const uint32_t rank = cluster.block_rank();
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t* wbuf = s_warp + 32 * warp;
+  Ctr* R0 = cluster.map_shared_rank(&s_ctr, 0);
+  const int n_clusters = gridDim.x / kPackCluster;
+  for (int cid = blockIdx.x / kPackCluster; cid < n_cands; cid += n_clusters) {
     const Cand c = cands[cid];
     const uint32_t n = c.n;
     const uint32_t* indeg = c.indeg ? c.indeg : S.indeg + c.op_off;
@@ -190,26 +327,36 @@ __global__ void __launch_bounds__(kPackThreads, 1) pack_kernel(const Cand* __res
     uint32_t* cidx = P.cidx + c.op_off;
     uint8_t* spl = P.spl + c.op_off;
     uint32_t* xoff = P.xoff + P.r_off[cid];
-    if (threadIdx.x == 0) {
-      s_first = kNone;
-      s_flags = (n >= kMaxOps ? kNfSize : 0u) | (c.d > kMaxDev ? kNfDev : 0u);
-      s_ncnt = 0;
-      s_nsrc = 0;
-      s_sum = 0;
-    }
-    const bool hist_smem = c.d <= kPackHist;
-    for (uint32_t d = threadIdx.x; d < kPackHist; d += kPackThreads) s_hist[d] = 0;
     uint32_t* devoff = S.devoff + c.dof_off;
-    if (!hist_smem)
-      for (uint32_t d = threadIdx.x; d <= c.d; d += kPackThreads) devoff[d] = 0;
-    __syncthreads();
+    const uint32_t n_chunks = (n + 31) / 32;
+    const uint32_t ch_lo = n_chunks * rank / kPackCluster;
+    const uint32_t ch_hi = n_chunks * (rank + 1) / kPackCluster;
+    const uint32_t lo = min(n, ch_lo * 32), hi = min(n, ch_hi * 32);
+    const bool hist_smem = c.d <= kPackHist;
+    if (rank == 0) {
+      if (threadIdx.x == 0) {
+        s_ctr.first = kNone;
+        s_ctr.flags = (n >= kMaxOps ? kNfSize : 0u) | (c.d > kMaxDev ? kNfDev : 0u);
+        s_ctr.ncnt = 0;
+        s_ctr.nsrc = 0;
+        s_ctr.sum = 0;
+        s_ctr.nested = 0;
+      }
+      for (uint32_t d = threadIdx.x; d < kPackHist; d += kPackThreads) s_ctr.hist[d] = 0;
+      if (!hist_smem)
+        for (uint32_t d = threadIdx.x; d <= c.d; d += kPackThreads) devoff[d] = 0;
+    }
+    if (threadIdx.x == 0) s_len = 0;
+    if (hist_smem)
+      for (uint32_t d = threadIdx.x; d < c.d; d += kPackThreads) s_lhist[d] = 0;
+    cluster.sync();
     // pass 1 (coalesced): checks, counter slots and sources (warp-aggregated),
     // splice marks, per-device op counts
     uint32_t flags = 0, first = kNone;
     unsigned long long sum = 0;
-    const uint32_t n_up = (n + 31) & ~31u;
-    for (uint32_t i = threadIdx.x; i < n_up; i += kPackThreads) {
-      const bool ok = i < n;
+    for (uint32_t i = lo + threadIdx.x; i < ((hi + 31) & ~31u) && lo < hi;
+         i += kPackThreads) {
+      const bool ok = i < hi;
       uint32_t ind = 0;
       bool virt = false;
       if (ok) {
@@ -224,14 +371,14 @@ __global__ void __launch_bounds__(kPackThreads, 1) pack_kernel(const Cand* __res
         if (virt && ind == 0u) flags |= kNfVsrc;
         if (!virt && dv >= c.d) flags |= kNfDev;
         spl[i] = virt && ind == 1u;
-        if (!virt && dv < c.d) atomicAdd(hist_smem ? &s_hist[dv] : &devoff[dv], 1u);
+        if (!virt && dv < c.d) atomicAdd(hist_smem ? &s_lhist[dv] : &devoff[dv], 1u);
       }
       const bool multi = ok && ind >= 2u, src = ok && ind == 0u;
       const unsigned mm = __ballot_sync(kFull, multi), ms = __ballot_sync(kFull, src);
       uint32_t bm = 0, bs = 0;
       if (lane == 0) {
-        if (mm) bm = atomicAdd(&s_ncnt, __popc(mm));
-        if (ms) bs = atomicAdd(&s_nsrc, __popc(ms));
+        if (mm) bm = atomicAdd(&R0->ncnt, __popc(mm));
+        if (ms) bs = atomicAdd(&R0->nsrc, __popc(ms));
       }
       bm = __shfl_sync(kFull, bm, 0);
       bs = __shfl_sync(kFull, bs, 0);
@@ -244,51 +391,115 @@ __global__ void __launch_bounds__(kPackThreads, 1) pack_kernel(const Cand* __res
         srcs[bs + __popc(ms & lt)] = i;
       }
     }
-    if (first != kNone) atomicMin(&s_first, first);
-    if (flags) atomicOr(&s_flags, flags);
-    if (sum) atomicAdd(&s_sum, sum);
+    if (first != kNone) atomicMin(&R0->first, first);
+    if (flags) atomicOr(&R0->flags, flags);
+    if (sum) atomicAdd(&R0->sum, sum);
     __syncthreads();
-    // pass 2: expanded list sizes (spliced virtual ops own no list)
-    bool deep = false;
-    for (uint32_t i = threadIdx.x; i < n; i += kPackThreads) {
-      uint32_t len = 0;
-      if (!spl[i]) deep |= !walk_list(i, c, spl, [&](uint32_t, bool) { ++len; });
-      xoff[i] = len;
-    }
-    if (deep) atomicOr(&s_flags, kNfChain);
-    __syncthreads();
-    const uint32_t total = block_exclusive_scan<kPackThreads, Scan>(xoff, n, scan_tmp, s_carry);
-    if (threadIdx.x == 0) xoff[n] = total;
-    __syncthreads();
-    // pass 3a (coalesced): every op's record
-    for (uint32_t i = threadIdx.x; i < n; i += kPackThreads) rec[i] = make_rec(i, c, indeg, cidx, xoff);
-    if (threadIdx.x == 0) rec[n] = make_uint4(0u, 0u, 0u, total);
-    __syncthreads();  // rec[] visible to the block
-    // pass 3b: expanded lists = gathered records (stamps for spliced ops)
-    for (uint32_t i = threadIdx.x; i < n; i += kPackThreads) {
-      if (spl[i]) continue;
-      uint4* dst = erec + xoff[i];
-      walk_list(i, c, spl, [&](uint32_t s, bool sv) {  // erec is write-once: stream it
-        __stcs(dst++, sv ? make_uint4(s & kOpMask, 0u, kFVirt, 0u) : rec[s]);
-      });
-    }
-    if (threadIdx.x == 0) {
-      PackInfo inf;
-      inf.first_missing = s_first;
-      inf.not_fast = s_flags | (s_sum >= 0x7FFFFFFFull ? kNfDur : 0u) |
-                     (s_ncnt >= kMaxCnt ? kNfSize : 0u);
-      inf.n_cnt = s_ncnt;
-      inf.n_src = s_nsrc;
-      inf.dur_sum = s_sum;
-      P.info[cid] = inf;
-    }
-    // timeline regions: exclusive scan of the per-device counts
     if (hist_smem)
-      for (uint32_t d = threadIdx.x; d < c.d; d += kPackThreads) devoff[d] = s_hist[d];
+      for (uint32_t d = threadIdx.x; d < c.d; d += kPackThreads)
+        if (s_lhist[d]) atomicAdd(&R0->hist[d], s_lhist[d]);
+    cluster.sync();  // spl complete
+    // nested splices (a spliced op with a spliced successor) take the
+    // per-thread DFS walk; otherwise the warp-cooperative passes
+    for (uint32_t i = lo + threadIdx.x; i < hi; i += kPackThreads)
+      if (spl[i])
+        for (uint32_t t = c.succ_off[i]; t < c.succ_off[i + 1]; ++t)
+          if (__ldcg(spl + c.succ[t])) atomicOr(&R0->nested, 1u);
+    cluster.sync();
+    const bool nested = R0->nested != 0;
+    // pass 2: expanded list sizes (spliced virtual ops own no list)
+    if (nested) {
+      bool deep = false;
+      uint32_t part = 0;
+      for (uint32_t i = lo + threadIdx.x; i < hi; i += kPackThreads) {
+        uint32_t len = 0;
+        if (!spl[i]) deep |= !walk_list(i, c, spl, [&](uint32_t, bool) { ++len; });
+        xoff[i] = len;
+        part += len;
+      }
+      if (deep) atomicOr(&R0->flags, kNfChain);
+      if (part) atomicAdd(&s_len, part);
+    } else {
+      uint32_t part = 0;
+      for (uint32_t ch = ch_lo + warp; ch < ch_hi; ch += kPackThreads / 32) {
+        coop_sizes(c, spl, ch * 32, min(n, ch * 32 + 32), xoff, wbuf);
+        if (ch * 32 + lane < n) part += xoff[ch * 32 + lane];
+      }
+      if (part) atomicAdd(&s_len, part);
+    }
     __syncthreads();
-    const uint32_t dtot = block_exclusive_scan<kPackThreads, Scan>(devoff, c.d, scan_tmp, s_carry);
-    if (threadIdx.x == 0) devoff[c.d] = dtot;
+    if (threadIdx.x == 0) R0->tot[rank] = s_len;
+    cluster.sync();
+    // exclusive scan of xoff over the cluster: local scan + lower ranks' totals
+    uint32_t base = 0, total = 0;
+    for (uint32_t r = 0; r < kPackCluster; ++r) {
+      const uint32_t t = R0->tot[r];
+      if (r < rank) base += t;
+      total += t;
+    }
+    if (threadIdx.x == 0) s_carry = base;
     __syncthreads();
+    for (uint32_t b0 = lo; b0 < hi; b0 += kPackThreads) {
+      const uint32_t i = b0 + threadIdx.x;
+      const uint32_t v = i < hi ? xoff[i] : 0u;
+      uint32_t excl, tsum;
+      Scan(scan_tmp).ExclusiveSum(v, excl, tsum);
+      const uint32_t carry = s_carry;
+      if (i < hi) xoff[i] = carry + excl;
+      __syncthreads();
+      if (threadIdx.x == 0) s_carry = carry + tsum;
+      __syncthreads();
+    }
+    if (rank == kPackCluster - 1 && threadIdx.x == 0) xoff[n] = total;
+    cluster.sync();  // xoff complete (rec[i] reads xoff[i + 1] across ranks)
+    // pass 3a (coalesced): every op's record
+    for (uint32_t i = lo + threadIdx.x; i < hi; i += kPackThreads) {
+      const uint32_t f = c.flags[i];
+      const uint32_t ind = indeg[i];
+      const bool virt = f & 1u;
+      const uint32_t ci = ind >= 2 ? cidx[i] : 0u;
+      const uint32_t x0 = xoff[i], x1 = __ldcg(xoff + i + 1);
+      const uint32_t cnt = min(x1 - x0, kCntMax);
+      const uint32_t z = (uint32_t(c.dev[i]) & kDevMask) | (virt ? kFVirt : 0u) |
+                         (ind >= 2 ? kFMulti : 0u) | (cnt << kCntShift) | ((ci >> 8) << 18);
+      const long long du = virt ? 0 : ld_dur(c, i);
+      rec[i] = make_uint4((i & kOpMask) | ((ci & 0xFFu) << 24),
+                          static_cast<uint32_t>(static_cast<int>(du)), z, x0);
+    }
+    if (rank == kPackCluster - 1 && threadIdx.x == 0) rec[n] = make_uint4(0u, 0u, 0u, total);
+    cluster.sync();  // rec visible to the cluster
+    // pass 3b: expanded lists = gathered records (stamps for spliced ops)
+    if (nested) {
+      for (uint32_t i = lo + threadIdx.x; i < hi; i += kPackThreads) {
+        if (spl[i]) continue;
+        uint4* dst = erec + xoff[i];
+        walk_list(i, c, spl, [&](uint32_t s, bool sv) {
+          __stcs(dst++, sv ? make_uint4(s & kOpMask, 0u, kFVirt, 0u) : __ldcg(rec + s));
+        });
+      }
+    } else {
+      for (uint32_t ch = ch_lo + warp; ch < ch_hi; ch += kPackThreads / 32)
+        coop_lists(c, spl, ch * 32, min(n, ch * 32 + 32), xoff, rec, erec, wbuf);
+    }
+    // rank 0: info and timeline regions (exclusive scan of per-device counts)
+    if (rank == 0) {
+      if (threadIdx.x == 0) {
+        PackInfo inf;
+        inf.first_missing = s_ctr.first;
+        inf.not_fast = s_ctr.flags | (s_ctr.sum >= 0x7FFFFFFFull ? kNfDur : 0u) |
+                       (s_ctr.ncnt >= kMaxCnt ? kNfSize : 0u);
+        inf.n_cnt = s_ctr.ncnt;
+        inf.n_src = s_ctr.nsrc;
+        inf.dur_sum = s_ctr.sum;
+        P.info[cid] = inf;
+      }
+      if (hist_smem)
+        for (uint32_t d = threadIdx.x; d < c.d; d += kPackThreads) devoff[d] = s_ctr.hist[d];
+      __syncthreads();
+      const uint32_t dtot = block_exclusive_scan<kPackThreads, Scan>(devoff, c.d, scan_tmp, s_carry);
+      if (threadIdx.x == 0) devoff[c.d] = dtot;
+    }
+    cluster.sync();  // rank 0's counters are reset for the next candidate
   }
 }
 
