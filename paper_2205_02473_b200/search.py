@@ -3,9 +3,10 @@
 The reference evaluates one candidate graph per `replay()` call inside its
 greedy Alg. 1 (proj/src/optimize.cpp:1327-1650; gate 1382-1392), building
 each through string-keyed GraphBuilder copies. Here a whole round of
-candidates is built as CSR deltas of one base graph on host threads
-(csrc/dfg_gen.cpp, dpro_graph_from_base_batch) and replayed in ONE batched
-launch; across GPUs every
+candidates is built as deltas of one base graph on host threads
+(csrc/dfg_gen.cpp, dpro_base_delta_batch), uploaded as deltas, merged into
+the resident base graph on the GPU and replayed in ONE batched launch;
+across GPUs every
 rank evaluates its own shard and the round's best candidate is agreed on
 with one packed int64 MIN all-reduce (the K4 exchange of DESIGN.md).
 
@@ -135,6 +136,8 @@ class SyncSearch:
         self.dist, self.rank = dist, rank
         L = model.layers
         self.base = LayeredBase(model, cluster)  # delta construction of candidates
+        # the base graph stays in HBM; each round uploads only the deltas
+        self.resident = self.engine.resident(self.base.graph().csr)
         self.state = SyncState([[i] for i in range(L)], [1] * L)
         self.best = None
         self.log = SearchLog()
@@ -165,9 +168,10 @@ class SyncSearch:
         return c
 
     def evaluate(self, states: Sequence[SyncState]) -> np.ndarray:
-        """Exact makespans of candidate states: one GPU batch."""
-        graphs = self.base.candidates([(st.groups, st.ks) for st in states], self.threads)
-        b = self.engine.batch([g.csr for g in graphs])
+        """Exact makespans of candidate states: deltas against the resident
+        base graph, merged, packed and replayed in one GPU batch."""
+        deltas = self.base.deltas([(st.groups, st.ks) for st in states], self.threads)
+        b = self.engine.delta_batch(self.resident, deltas)
         b.replay(want_schedule=False)
         ms, st, *_ = b.results()
         if np.any(st != 0):

@@ -39,9 +39,9 @@ def main():
     def timed(states):
         nonlocal t_gen, t_gpu
         t0 = time.perf_counter()
-        graphs = s.base.candidates([(st.groups, st.ks) for st in states], threads)
+        deltas = s.base.deltas([(st.groups, st.ks) for st in states], threads)
         t1 = time.perf_counter()
-        b = eng.batch([g.csr for g in graphs])
+        b = eng.delta_batch(s.resident, deltas)
         b.replay(want_schedule=False)
         ms, st, *_ = b.results()
         t2 = time.perf_counter()
