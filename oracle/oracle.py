@@ -164,6 +164,14 @@ class RefGraph:
         _raise(self.lib, st.value)
         return RefGraph(h)
 
+    def op_fusion(self, a: str, b: str, dur_override: int = -1) -> "RefGraph":
+        """apply_op_fusion with the default CostModel (ratio 0.8)."""
+        st = C.c_int32(0)
+        h = self.lib.ref_apply_op_fusion(self.h, a.encode(), b.encode(), dur_override,
+                                         C.byref(st))
+        _raise(self.lib, st.value)
+        return RefGraph(h)
+
     def tensor_fusion(self, t1: str, t2: str) -> "RefGraph":
         st = C.c_int32(0)
         h = self.lib.ref_apply_tensor_fusion(self.h, t1.encode(), t2.encode(), C.byref(st))

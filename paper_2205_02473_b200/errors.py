@@ -54,3 +54,15 @@ class ParseError(Error):
 
 class IoError(Error):
     """dpro::IoError (errors.hpp:117-120)."""
+
+
+class SchemaError(Error):
+    """dpro::SchemaError (errors.hpp:41-46)."""
+
+    def __init__(self, what: str, field: str):
+        super().__init__(f"{what}: field '{field}'")
+        self.field = field
+
+
+class SpliceError(Error):
+    """dpro::SpliceError (errors.hpp:62-65)."""

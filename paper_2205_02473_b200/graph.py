@@ -290,6 +290,10 @@ class GlobalDFG:
     def has_base(self, base: str) -> bool:
         return any(u.base == base for u in self._tensors.values())
 
+    def units_of_base(self, base: str) -> list[str]:
+        """graph.cpp:119-125 (unit names in name order)."""
+        return [n for n, u in self._tensors.items() if u.base == base]
+
     def base_bytes(self, base: str) -> int:
         units = [u for u in self._tensors.values() if u.base == base]
         if not units:
@@ -361,10 +365,29 @@ class GraphBuilder:
         return self._ops[id_]
 
     def remove_op(self, id_: str) -> None:
-        if id_ not in self._ops:
-            raise LookupError_(f"no op '{id_}' to remove")
-        del self._ops[id_]
-        self._edges = {e for e in self._edges if id_ not in e}
+        self.remove_ops([id_])
+
+    def remove_ops(self, ids) -> None:
+        """remove_op for several ops with one pass over the edges."""
+        gone = set()
+        for id_ in ids:
+            if id_ not in self._ops:
+                raise LookupError_(f"no op '{id_}' to remove")
+            del self._ops[id_]
+            gone.add(id_)
+        if gone:
+            self._edges = {e for e in self._edges if e[0] not in gone and e[1] not in gone}
+
+    def remove_tensor_unit(self, name: str) -> None:
+        if name not in self._tensors:
+            raise LookupError_(f"no tensor unit '{name}' to remove")
+        del self._tensors[name]
+
+    def preds(self, id_: str) -> list[str]:
+        return sorted(a for a, b in self._edges if b == id_)
+
+    def succs(self, id_: str) -> list[str]:
+        return sorted(b for a, b in self._edges if a == id_)
 
     def add_edge(self, a: str, b: str) -> None:
         if a not in self._ops:

@@ -1,7 +1,13 @@
-"""Memory rewrites and the memory pass (proj/src/optimize.cpp:815-1021),
-evaluated on the GPU: every candidate is replayed in one batched launch and
-its peak memory estimated by K5 on the schedule already in HBM.
+"""Graph rewrites of the reference's optimizer (proj/src/optimize.cpp) on a
+GlobalDFG, and the memory pass evaluated on the GPU: every candidate is
+replayed in one batched launch and its peak memory estimated by K5 on the
+schedule already in HBM.
 
+    CostModel                       optimize.cpp:82-145 (fused-op table)
+    apply_op_fusion(g, a, b, ...)   optimize.cpp:245-317
+    apply_tensor_fusion(g, t1, t2)  optimize.cpp:366-455
+    apply_tensor_partition(g, t, k) optimize.cpp:459-492
+    apply_strategy / _set           optimize.cpp:506-541
     validate(g)                     graph.cpp:332-425 (validity only)
     recompute_candidate(g)          optimize.cpp:819-877 (sqrt(N) checkpoints)
     grad_accum_candidate(g, meta)   optimize.cpp:879-959 (2 micro-batches)
@@ -17,11 +23,15 @@ from __future__ import annotations
 import copy
 import enum
 import math
+import re
 from collections import deque
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
-from .errors import Error, TransformError
-from .graph import (GlobalDFG, GraphBuilder, OpKind, is_communication, is_virtual, round_us)
+from .errors import (CycleError, Error, IoError, LookupError_, SchemaError, SpliceError,
+                     TransformError)
+from .graph import (DeviceId, GlobalDFG, GraphBuilder, Op, OpKind, TensorUnit, is_communication,
+                    is_computation, is_virtual, round_us)
+from .ingest import CommTopology, expand_tensor
 from .memory import ModelMeta, estimate_peak_memory_many
 from .replay import replay_many
 
@@ -60,6 +70,229 @@ def local_part(op_id: str) -> str:
     """optimize.cpp:41-44."""
     arrow = op_id.find("->")
     return op_id if arrow < 0 else op_id[arrow + 2:]
+
+
+_STOD = re.compile(r"^[+-]?((\d+\.?\d*|\.\d+)([eE][+-]?\d+)?|inf(inity)?|nan)$", re.I)
+
+
+@dataclass
+class CostModel:
+    """optimize.hpp:35-46: fused durations by (op a, op b), with a ratio
+    fallback."""
+    fused_us: dict[tuple[str, str], float] = field(default_factory=dict)
+    fallback_ratio: float = 0.8
+
+    def fused_dur_us(self, a, b) -> float:
+        """optimize.cpp:84-103: table entry (full ids, then local parts) if
+        it does not exceed a.dur + b.dur, else fallback_ratio * (a + b)."""
+        cap = float(a.dur) + float(b.dur)
+
+        def lookup(ka: str, kb: str) -> float:
+            v = self.fused_us.get((ka, kb))
+            return -1.0 if v is None or v > cap else v
+
+        v = lookup(a.id, b.id)
+        if v >= 0:
+            return v
+        v = lookup(local_part(a.id), local_part(b.id))
+        if v >= 0:
+            return v
+        return self.fallback_ratio * cap
+
+    @staticmethod
+    def from_csv(text: str) -> "CostModel":
+        """optimize.cpp:105-137: rows "op_a, op_b, fused_dur_us"."""
+        m = CostModel()
+        for line in text.splitlines():
+            row = line.strip(" \t\r\n")
+            if not row or row[0] == "#":
+                continue
+            fields = row.split(",")
+            if len(fields) != 3:
+                raise SchemaError(f"cost model row needs op_a, op_b, fused_dur_us: {row}",
+                                  "fused_dur_us")
+            a, b, val = (f.strip(" \t\r\n") for f in fields)
+            if val == "fused_dur_us":
+                continue  # header row
+            if not _STOD.match(val):  # what std::stod consumes whole
+                raise SchemaError(f"cost model duration is not a number: {row}", "fused_dur_us")
+            dur = float(val)
+            m.fused_us[(a, b)] = dur
+        return m
+
+    @staticmethod
+    def load(path: str) -> "CostModel":
+        try:
+            with open(path) as f:
+                return CostModel.from_csv(f.read())
+        except OSError as e:
+            raise IoError(f"cannot open cost model: {path}") from e
+
+
+def fused_op_id(a: str, b: str) -> str:
+    """optimize.cpp:76-78."""
+    return a + "+" + local_part(b)
+
+
+def apply_op_fusion(g: GlobalDFG, a: str, b: str, cost: CostModel | None = None,
+                    dur_us_override: int = -1) -> GlobalDFG:
+    """optimize.cpp:245-317: a and b (computation ops on one device joined
+    by an edge, with no second path a -> ... -> b) become one op."""
+    cost = cost or CostModel()
+    oa, ob = g.op(a), g.op(b)
+    if a == b:
+        raise TransformError(f"cannot fuse op {a} with itself")
+    if not is_computation(oa.kind) or not is_computation(ob.kind):
+        raise TransformError(f"op fusion requires computation ops: {a}, {b}")
+    if oa.device.str() != ob.device.str():
+        raise TransformError(f"ops {a} and {b} run on different devices")
+    if not g.has_edge(a, b):
+        raise TransformError(f"op fusion requires a direct edge {a} -> {b}")
+    parent: dict[str, str] = {}
+    frontier = deque()
+    for s in g.succs(a):
+        if s == b:
+            continue
+        if s not in parent:
+            parent[s] = a
+        frontier.append(s)
+    while frontier:
+        cur = frontier.popleft()
+        if cur == b:
+            witness = [b]
+            x = parent[b]
+            while x != a:
+                witness.append(x)
+                x = parent[x]
+            witness.append(a)
+            witness.reverse()
+            raise CycleError(f"fusing {a} and {b} would create a cycle", witness)
+        for s in g.succs(cur):
+            if s not in parent:
+                parent[s] = cur
+                frontier.append(s)
+    fused = copy.copy(oa)
+    fused.id = fused_op_id(a, b)
+    fused.dur = dur_us_override if dur_us_override >= 0 else round_us(cost.fused_dur_us(oa, ob))
+    fused.produces = list(oa.produces) + list(ob.produces)
+    preds = (set(g.preds(a)) | set(g.preds(b))) - {a, b}
+    succs = (set(g.succs(a)) | set(g.succs(b))) - {a, b}
+    bld = GraphBuilder(g)
+    bld.remove_ops([a, b])
+    bld.add_op(fused)
+    for p in preds:
+        bld.add_edge(p, fused.id)
+    for t in succs:
+        bld.add_edge(fused.id, t)
+    return bld.build()
+
+
+def splice_topology(bld: GraphBuilder, topo: CommTopology, base: str, part_index: int,
+                    part_count: int, vin: dict[str, str], vout: dict[str, str]) -> None:
+    """optimize.cpp:325-361."""
+    for op in topo.ops:
+        bld.add_op(op)
+    for x, y in topo.edges:
+        bld.add_edge(x, y)
+    unit = TensorUnit(topo.unit, base, topo.bytes, part_index, part_count, topo.ps_node,
+                      sorted(op.id for op in topo.ops))
+    for node, ids in topo.entry.items():
+        if node not in vin:
+            raise SpliceError(f"tensor {topo.unit} enters at node {node} which has no entry op")
+        for i in ids:
+            bld.add_edge(vin[node], i)
+        unit.vin[node] = vin[node]
+    for node, ids in topo.exit.items():
+        if node not in vout:
+            raise SpliceError(f"tensor {topo.unit} exits at node {node} which has no exit op")
+        for i in ids:
+            bld.add_edge(i, vout[node])
+        unit.vout[node] = vout[node]
+    bld.add_tensor_unit(unit)
+
+
+def apply_tensor_fusion(g: GlobalDFG, t1: str, t2: str) -> GlobalDFG:
+    """optimize.cpp:366-455: two unpartitioned tensors synchronize as one
+    unit "t1+t2" with new IN/OUT splice points per worker."""
+    if t1 == t2:
+        raise TransformError(f"cannot fuse tensor {t1} with itself")
+    if not g.has_base(t1):
+        raise LookupError_(f"unknown tensor: {t1}")
+    if not g.has_base(t2):
+        raise LookupError_(f"unknown tensor: {t2}")
+    n1, n2 = g.units_of_base(t1), g.units_of_base(t2)
+    if len(n1) != 1 or len(n2) != 1:
+        raise TransformError("tensor fusion needs unpartitioned inputs; merge "
+                             f"{t1 if len(n1) != 1 else t2} back first")
+    u1, u2 = g.tensor_unit(n1[0]), g.tensor_unit(n2[0])
+    if sorted(u1.vin) != sorted(u2.vin) or sorted(u1.vout) != sorted(u2.vout):
+        raise TransformError(f"tensors {t1} and {t2} attach to different worker sets")
+    fused = f"{t1}+{t2}"
+    bld = GraphBuilder(g)
+    vin: dict[str, str] = {}
+    vout: dict[str, str] = {}
+    for node in sorted(u1.vin):
+        dv = DeviceId.compute(node)
+        in_op = Op(f"{node}->IN.{fused}", OpKind.VIRTUAL_IN, node, dv, 0, tensor=fused)
+        out_op = Op(f"{node}->OUT.{fused}", OpKind.VIRTUAL_OUT, node, dv, 0, tensor=fused)
+        bld.add_op(in_op)
+        bld.add_op(out_op)
+        vin[node], vout[node] = in_op.id, out_op.id
+        for p in sorted(set(g.preds(u1.vin[node])) | set(g.preds(u2.vin[node]))):
+            bld.add_edge(p, in_op.id)
+        for t in sorted(set(g.succs(u1.vout[node])) | set(g.succs(u2.vout[node]))):
+            bld.add_edge(out_op.id, t)
+    gone = list(u1.comm_ops) + list(u2.comm_ops) + list(u1.vin.values()) + \
+        list(u1.vout.values()) + list(u2.vin.values()) + list(u2.vout.values())
+    bld.remove_ops(gone)
+    bld.remove_tensor_unit(u1.name)
+    bld.remove_tensor_unit(u2.name)
+    topo = expand_tensor(fused, u1.bytes + u2.bytes, g.cluster())
+    splice_topology(bld, topo, fused, 0, 1, vin, vout)
+    for op in g.ops():  # producers now advertise the fused unit
+        if not is_computation(op.kind):
+            continue
+        touched, produces = False, []
+        for t in op.produces:
+            if t in (t1, t2):
+                if not touched:
+                    produces.append(fused)
+                touched = True
+            else:
+                produces.append(t)
+        if touched:
+            c = copy.copy(bld.op(op.id))
+            c.produces = produces
+            bld._ops[op.id] = c  # noqa: SLF001 - GraphBuilder::op(id) mutation
+    return bld.build()
+
+
+def apply_tensor_partition(g: GlobalDFG, t: str, k: int) -> GlobalDFG:
+    """optimize.cpp:459-492: tensor t synchronizes as k balanced units
+    "t#p<i>" (or "t" for k = 1), spliced where its first unit was."""
+    if not g.has_base(t):
+        raise LookupError_(f"unknown tensor: {t}")
+    nbytes = g.base_bytes(t)
+    if k < 1:
+        raise TransformError(f"partition count must be >= 1, got {k}")
+    if k > nbytes:
+        raise TransformError(f"cannot split {nbytes} bytes of {t} into {k} partitions")
+    names = g.units_of_base(t)
+    first = g.tensor_unit(names[0])
+    if first.part_count == k:
+        return g
+    bld = GraphBuilder(g)
+    gone = []
+    for name in names:
+        gone += g.tensor_unit(name).comm_ops
+        bld.remove_tensor_unit(name)
+    bld.remove_ops(gone)
+    base, rem = divmod(nbytes, k)
+    for i in range(k):
+        name = t if k == 1 else f"{t}#p{i}"
+        topo = expand_tensor(name, base + (1 if i < rem else 0), g.cluster())
+        splice_topology(bld, topo, t, i, k, dict(first.vin), dict(first.vout))
+    return bld.build()
 
 
 def topo_order(g: GlobalDFG) -> list[int] | None:
@@ -229,6 +462,30 @@ def grad_accum_candidate(g: GlobalDFG, meta: ModelMeta) -> tuple[GlobalDFG, Stra
     if not validate(out):
         return None
     return out, Strategy(StrategyKind.GRAD_ACCUM, "", "", 2, -1)
+
+
+def apply_strategy(g: GlobalDFG, s: Strategy, cost: CostModel | None = None,
+                   meta: ModelMeta | None = None) -> GlobalDFG:
+    """optimize.cpp:506-531."""
+    if s.kind == StrategyKind.OP_FUSION:
+        return apply_op_fusion(g, s.a, s.b, cost, s.dur_us)
+    if s.kind == StrategyKind.TENSOR_FUSION:
+        return apply_tensor_fusion(g, s.a, s.b)
+    if s.kind == StrategyKind.PARTITION:
+        return apply_tensor_partition(g, s.a, s.k)
+    if s.kind == StrategyKind.RECOMPUTE:
+        return apply_recompute(g)
+    if s.kind == StrategyKind.GRAD_ACCUM:
+        return apply_grad_accum(g, meta or ModelMeta())
+    raise TransformError("unknown strategy kind")
+
+
+def apply_strategy_set(g: GlobalDFG, strategies, cost: CostModel | None = None,
+                       meta: ModelMeta | None = None) -> GlobalDFG:
+    """optimize.cpp:535-541."""
+    for s in strategies:
+        g = apply_strategy(g, s, cost, meta)
+    return g
 
 
 def apply_recompute(g: GlobalDFG) -> GlobalDFG:

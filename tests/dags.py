@@ -196,3 +196,29 @@ def rewrite_dag(rng: np.random.Generator):
             if b.has_op(f"{other}->BW.l0") and not b.has_edge(f"{other}->BW.l0", f"{nd}->FW.l0"):
                 b.add_edge(f"{nd}->FW.l0", f"{other}->BW.l0")
     return b.build()
+
+
+def strategy_chain(rng: np.random.Generator, g, n: int = 6):
+    """Random optimize.cpp strategies for a layered graph g: op fusion of
+    computation pairs (valid chains, cross-device and cycle-closing pairs
+    included), tensor fusion of two base tensors, partition with k in 1..4.
+    Returned as (kind, a, b, k) tuples; errors are part of the test."""
+    comp = [o.id for o in g.ops() if int(o.kind) in (0, 1, 2)]
+    bases = sorted({u.base for u in g.tensor_units().values()})
+    out = []
+    for _ in range(n):
+        r = rng.random()
+        if r < 0.4 and comp:
+            a = comp[int(rng.integers(0, len(comp)))]
+            succ = [s for s in g.succs(a)] if g.has_op(a) else []
+            if succ and rng.random() < 0.8:
+                b = succ[int(rng.integers(0, len(succ)))]
+            else:
+                b = comp[int(rng.integers(0, len(comp)))]
+            out.append((0, a, b, 1))
+        elif r < 0.7 and len(bases) > 1:
+            i, j = rng.choice(len(bases), 2, replace=False)
+            out.append((1, bases[int(i)], bases[int(j)], 1))
+        elif bases:
+            out.append((2, bases[int(rng.integers(0, len(bases)))], "", int(rng.integers(1, 5))))
+    return out

@@ -22,7 +22,8 @@ ROOT = Path(__file__).resolve().parents[2]
 sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tests"))
 
-from dags import acceptance_dag, fuzz_dag, memory_dag, random_dag_ref, rewrite_dag  # noqa: E402
+from dags import (acceptance_dag, fuzz_dag, memory_dag, random_dag_ref, rewrite_dag,
+                  strategy_chain)  # noqa: E402
 from golden_io import rows_digest  # noqa: E402
 from oracle.oracle import RefError, RefGraph, ref_sync_makespan  # noqa: E402
 from paper_2205_02473_b200.graph import (DeviceId, GraphBuilder, Op, OpKind, comp,  # noqa: E402
@@ -383,8 +384,40 @@ def rewrite_main():
                 res = {"status": err.status, "message": err.msg,
                        "best_peak": getattr(err, "best_peak", None)}
             out["memory_pass"].append({"src": si, "budget": int(budget), "expect": res})
+    # strategy chains (op fusion, tensor fusion, partition) on layered synth
+    # graphs, applied one by one; after an error the chain continues on the
+    # last good graph
+    from paper_2205_02473_b200.graph import synth_cluster
+    from paper_2205_02473_b200.ingest import LayeredModel, layered_global_dfg
+    out["chains"] = []
+    crng = np.random.default_rng(41)
+    for si, (src, rg0, meta) in enumerate(sources):
+        if "synth" not in src:
+            continue
+        sp = src["synth"]
+        g = layered_global_dfg(LayeredModel(sp["fw_dur_us"], sp["bw_dur_us"], sp["tensor_bytes"],
+                                            sp["update_dur_us"]),
+                               synth_cluster(sp["scheme"], sp["workers"], sp["ps_count"],
+                                             sp["bandwidth_bytes_per_us"], sp["latency_us"]))
+        for rep in range(6):
+            chain = strategy_chain(crng, g, 6)
+            rg, steps = rg0, []
+            for kind, a, b, k in chain:
+                try:
+                    if kind == 0:
+                        nrg = rg.op_fusion(a, b)
+                    elif kind == 1:
+                        nrg = rg.tensor_fusion(a, b)
+                    else:
+                        nrg = rg.partition(a, k)
+                    rg = nrg
+                    steps.append({"status": 0, "digest": rows_digest(ref_rows(rg))})
+                except RefError as err:
+                    steps.append({"status": err.status, "message": err.msg, "cycle": err.cycle})
+            out["chains"].append({"src": si, "chain": chain, "steps": steps})
     (OUT / "rewrite_vectors.json").write_text(json.dumps(out, separators=(",", ":")))
-    print(f"{len(out['apply'])} rewrite vectors, {len(out['memory_pass'])} memory_pass vectors")
+    print(f"{len(out['apply'])} rewrite vectors, {len(out['memory_pass'])} memory_pass vectors, "
+          f"{len(out['chains'])} strategy chains")
 
 
 if __name__ == "__main__":

@@ -104,3 +104,98 @@ def test_memory_pass_matches_reference_vectors(engine):
             assert str(ei.value) == exp["message"]
             assert ei.value.best_peak_bytes == exp["best_peak"]
     assert n_applied > 100
+
+
+def _apply_chain(g, chain):
+    from paper_2205_02473_b200 import CycleError, Error
+    from paper_2205_02473_b200.errors import LookupError_
+    from paper_2205_02473_b200.rewrite import (apply_op_fusion, apply_tensor_fusion,
+                                               apply_tensor_partition)
+    steps = []
+    for kind, a, b, k in chain:
+        try:
+            if kind == 0:
+                g = apply_op_fusion(g, a, b)
+            elif kind == 1:
+                g = apply_tensor_fusion(g, a, b)
+            else:
+                g = apply_tensor_partition(g, a, k)
+            steps.append({"status": 0, "digest": rows_digest(dfg_rows(g))})
+        except CycleError as e:
+            steps.append({"status": 2, "message": str(e), "cycle": e.cycle})
+        except LookupError_ as e:
+            steps.append({"status": 4, "message": str(e)})
+        except TransformError as e:
+            steps.append({"status": 5, "message": str(e)})
+        except Error as e:  # pragma: no cover - unexpected kind
+            steps.append({"status": 3, "message": str(e)})
+    return g, steps
+
+
+def test_strategy_chains_match_reference_vectors():
+    """op fusion / tensor fusion / partition chains (optimize.cpp:245-492)
+    against the reference: every intermediate graph row by row, every
+    error with its type, message and cycle witness."""
+    vecs = rewrite_vectors()
+    for v in vecs["chains"]:
+        g, _ = _source(vecs, v["src"])
+        _, steps = _apply_chain(g, [tuple(c) for c in v["chain"]])
+        for got, exp in zip(steps, v["steps"]):
+            exp = {k: x for k, x in exp.items() if not (k == "cycle" and exp["status"] != 2)}
+            got = {k: x for k, x in got.items() if k in exp}
+            assert got == exp, (v["chain"], got, exp)
+
+
+def test_strategy_chains_match_live_reference(ref):
+    from dags import strategy_chain
+    from golden.make_golden import ref_rows
+    rng = np.random.default_rng(5)
+    for scheme, W, S, L in [("ring", 3, 0, 5), ("ps", 4, 2, 6)]:
+        spec = {"layers": L, "fw_dur_us": rng.integers(10, 400, L).tolist(),
+                "bw_dur_us": rng.integers(10, 800, L).tolist(),
+                "tensor_bytes": rng.integers(1000, 4_000_000, L).tolist(),
+                "update_dur_us": 5, "scheme": scheme, "workers": W, "ps_count": S,
+                "bandwidth_bytes_per_us": 12500.0, "latency_us": 5.0}
+        c = synth_cluster(scheme, W, S, 12500.0, 5.0)
+        g0 = layered_global_dfg(LayeredModel(spec["fw_dur_us"], spec["bw_dur_us"],
+                                             spec["tensor_bytes"], 5), c)
+        for _ in range(8):
+            chain = strategy_chain(rng, g0, 5)
+            _, steps = _apply_chain(g0, chain)
+            rg = ref.RefGraph.synth(spec)
+            for (kind, a, b, k), got in zip(chain, steps):
+                try:
+                    rg = (rg.op_fusion(a, b) if kind == 0 else
+                          rg.tensor_fusion(a, b) if kind == 1 else rg.partition(a, k))
+                    exp = {"status": 0, "digest": rows_digest(ref_rows(rg))}
+                except ref.RefError as e:
+                    exp = {"status": e.status, "message": e.msg}
+                assert {k2: got.get(k2) for k2 in exp} == exp, (chain, kind, a, b, k)
+
+
+@pytest.mark.gpu
+def test_rewritten_graphs_replay_like_reference(engine, ref):
+    """GPU replay of rewritten graphs equals the reference replay of the
+    same rewrite chain (makespan and every start/end)."""
+    from paper_2205_02473_b200 import replay_many
+    from golden.make_golden import ref_rows  # noqa: F401 - import check
+    vecs = rewrite_vectors()
+    graphs, exps = [], []
+    for v in vecs["chains"][:12]:
+        g, _ = _source(vecs, v["src"])
+        g2, steps = _apply_chain(g, [tuple(c) for c in v["chain"]])
+        graphs.append(g2)
+        sp = vecs["sources"][v["src"]]["synth"]
+        rg = ref.RefGraph.synth(sp)
+        for kind, a, b, k in v["chain"]:
+            try:
+                rg = (rg.op_fusion(a, b) if kind == 0 else
+                      rg.tensor_fusion(a, b) if kind == 1 else rg.partition(a, k))
+            except ref.RefError:
+                pass
+        exps.append(rg.replay())
+    for r, (T, s, e, _, _) in zip(replay_many(graphs), exps):
+        assert r.iteration_time_us == T
+        order = sorted(r.schedule)
+        assert [r.schedule[i].start for i in order] == s.tolist()
+        assert [r.schedule[i].end for i in order] == e.tolist()
