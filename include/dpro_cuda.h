@@ -223,6 +223,10 @@ dpro_batch* dpro_cuda_batch_create_delta(dpro_ctx* ctx, const dpro_resident* r,
  * argument may be NULL). */
 int dpro_cuda_batch_sizes(dpro_batch* b, uint32_t* n_ops, uint32_t* n_edges,
                           uint32_t* n_devices);
+/* Pack diagnostics, 4 words per candidate: first op without a duration
+ * (UINT32_MAX: none), fast-path ineligibility bits (pack_kernel.cuh kNf*),
+ * multi-predecessor ops, source ops. */
+int dpro_cuda_batch_pack_info(dpro_batch* b, uint32_t* out);
 /* Re-runs a batch's device-side preparation on the inputs already in HBM
  * (delta merge for delta batches, then the pack kernel): with a replay, one
  * full pass of the path without host work -- what bench.py times. */

@@ -101,6 +101,7 @@ SIGNATURES = {
     "dpro_cuda_batch_create_delta": (_P, [_P, _P, _P, _I32]),
     "dpro_cuda_batch_prepare": (C.c_int, [_P, _P]),
     "dpro_cuda_batch_sizes": (C.c_int, [_P, _P, _P, _P]),
+    "dpro_cuda_batch_pack_info": (C.c_int, [_P, _P]),
     "dpro_cuda_replay_delta_batch": (C.c_int, [_P, _P, _P, _I32, _P, _P, _P]),
     "dpro_base_delta_batch": (C.c_int, [_P, _I32, _P, _P, _P, _P, _P, _I32, _P]),
     "dpro_delta_set_deltas": (_P, [_P]),

@@ -490,18 +490,20 @@ int finish_batch(dpro_ctx* ctx, dpro_batch* b) {
       c_off[i] = co;
       ro += b->n_ops[i] + 1;
       eo += b->n_edges[i];
-      co += (b->n_ops[i] + 15) & ~15u;
+      co += 2ull * ((b->n_ops[i] + 15) & ~15u);  // room for u16 counters
     }
     const size_t s_rec = align16(ro * 16 + 16), s_erec = align16(eo * 16 + 16),
                  s_cnt = align16(co + 16), s_u32 = align16(so * 4 + 4),
                  s_off = align16(size_t(n) * 8 + 8),
                  s_info = align16(size_t(n) * sizeof(dpro_k::PackInfo) + 16);
     const size_t s_xoff = align16(ro * 4 + 16), s_spl = align16(so + 16);
-    CU(b->pack.ensure(s_rec + s_erec + s_cnt + 2 * s_u32 + s_xoff + s_spl + 3 * s_off + s_info));
+    CU(b->pack.ensure(s_rec + s_erec + 2 * s_cnt + 2 * s_u32 + s_xoff + s_spl + 3 * s_off +
+                      s_info));
     size_t po = 0;
     b->P.rec = b->pack.as<uint4>(po); po += s_rec;
     b->P.erec = b->pack.as<uint4>(po); po += s_erec;
     b->P.cnt0 = b->pack.as<uint8_t>(po); po += s_cnt;
+    b->P.gcnt = b->pack.as<uint8_t>(po); po += s_cnt;
     b->P.srcs = b->pack.as<uint32_t>(po); po += s_u32;
     b->P.cidx = b->pack.as<uint32_t>(po); po += s_u32;
     b->P.xoff = b->pack.as<uint32_t>(po); po += s_xoff;
@@ -955,6 +957,18 @@ int dpro_cuda_batch_sizes(dpro_batch* b, uint32_t* n_ops, uint32_t* n_edges,
   return DPRO_OK;
 }
 
+int dpro_cuda_batch_pack_info(dpro_batch* b, uint32_t* out) {
+  if (!b || !out) return DPRO_EINVAL;
+  for (int32_t i = 0; i < b->n; ++i) {
+    const auto& f = b->info[i];
+    out[4 * i] = f.first_missing;
+    out[4 * i + 1] = f.not_fast;
+    out[4 * i + 2] = f.n_cnt;
+    out[4 * i + 3] = f.n_src;
+  }
+  return DPRO_OK;
+}
+
 int dpro_cuda_batch_prepare(dpro_ctx* ctx, dpro_batch* b) {
   if (!ctx || !b) return DPRO_EINVAL;
   CU(cudaSetDevice(ctx->device));
@@ -1070,8 +1084,12 @@ int launch_fast_kd(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule, FastCfg 
   const int grid = std::max(1, std::min(b->n, ctx->sm_count * blocks_per_sm));
   CU(cudaMemsetAsync(b->work.p, 0, 16, ctx->stream));
   b->F = F;
+  // graphs of millions of ops (configs 4/5) overflow the residency-sized
+  // rings every time: send them straight to the deep-ring pass
+  const bool deep_first = b->n > 0 && b->sum_n / b->n > 1000000ull;
   kern<<<grid, 32 * NW, smem, ctx->stream>>>(b->desc.as<Cand>(), b->n, b->S, b->O, b->P, F,
-                                             want_schedule ? 1 : 0, b->work.as<unsigned>(), 0);
+                                             want_schedule ? 1 : 0, b->work.as<unsigned>(),
+                                             deep_first ? 2 : 0);
   CU(cudaGetLastError());
   // pass 1: candidates whose device queues outgrew the ring, one CTA per SM
   // with the deepest rings the shared memory holds
@@ -1092,8 +1110,8 @@ int launch_fast_nw(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
   FastCfg F;
   F.qc = ctx->ring;
   F.rl = 128;
-  uint32_t max_cnt = 16;
-  for (const auto& inf : b->info) max_cnt = std::max(max_cnt, inf.n_cnt);
+  uint32_t max_cnt = 16;  // counter bytes
+  for (const auto& inf : b->info) max_cnt = std::max(max_cnt, (inf.wide ? 2u : 1u) * inf.n_cnt);
   const uint32_t nt = 32 * NW;
   uint32_t kd = std::max<uint32_t>(1, (b->max_d + nt - 1) / nt);
   if (kd > 8) kd = kd <= 12 ? 12 : 16;
@@ -1102,6 +1120,9 @@ int launch_fast_nw(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
   F.dcap = std::max<uint32_t>(1, std::min<uint32_t>(b->max_d, nt * kd));
   F.ccap = (max_cnt + 15) & ~15u;
   const size_t limit = ctx->smem_optin - 64;
+  // counters that would leave fewer than 4 candidates per SM stay in global
+  // scratch instead (large graphs: configs 4/5 have 10^5+ multi-pred ops)
+  if (fast_bytes(F.dcap, F.qc, F.rl, F.ccap, NW) > size_t(ctx->smem_per_sm) / 4) F.ccap = 16;
   while (fast_bytes(F.dcap, F.qc, F.rl, F.ccap, NW) > limit && F.ccap > 16)
     F.ccap = std::max<uint32_t>(16, (F.ccap / 2 + 15) & ~15u);
   while (fast_bytes(F.dcap, F.qc, F.rl, F.ccap, NW) > limit && F.dcap > 1) F.dcap /= 2;

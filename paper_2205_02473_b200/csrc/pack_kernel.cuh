@@ -45,7 +45,8 @@ constexpr uint32_t kMaxCnt = 1u << 22;
 
 // not_fast bits
 constexpr uint32_t kNfDur = 1u;       // |dur| >= 2^31 or sum of dur >= 2^31
-constexpr uint32_t kNfIndeg = 2u;     // some indeg >= 255
+constexpr uint32_t kNfIndeg = 2u;     // some indeg >= 65535
+constexpr uint32_t kWideCnt = 1u << 8;  // (PackInfo::wide) some indeg >= 255: u16 counters
 constexpr uint32_t kNfVsrc = 4u;      // virtual op without predecessors
 constexpr uint32_t kNfDev = 8u;       // device id out of range / > 1024 devices
 constexpr uint32_t kNfSize = 16u;     // >= 2^24 ops or >= 2^22 counters
@@ -58,12 +59,15 @@ struct PackInfo {
   uint32_t n_cnt;          // multi-predecessor ops (compact counters)
   uint32_t n_src;          // ops without predecessors
   unsigned long long dur_sum;
+  uint32_t wide;           // kWideCnt: u16 counters (cnt0 as uint16_t)
+  uint32_t pad;
 };
 
 struct PackOut {
   uint4* rec;                  // [sum (n+1)]
   uint4* erec;                 // [sum e]
-  uint8_t* cnt0;               // [sum n16]
+  uint8_t* cnt0;               // [sum 2*n16] u8 counters, or u16 for wide candidates
+  uint8_t* gcnt;               // [sum 2*n16] replay's counters when they exceed smem
   uint32_t* srcs;              // [sum n]
   uint32_t* cidx;              // [sum n] scratch: counter slot per op
   uint32_t* xoff;              // [sum (n+1)] scratch: expanded list offsets
@@ -367,7 +371,8 @@ __global__ void __cluster_dims__(kPackCluster, 1, 1) __launch_bounds__(kPackThre
         if (!virt && du < 0) first = min(first, i);
         if (!virt && (du > 0x7FFFFFFFLL || du < -0x80000000LL)) flags |= kNfDur;
         if (!virt && du > 0) sum += static_cast<unsigned long long>(du);
-        if (ind >= 255u) flags |= kNfIndeg;
+        if (ind >= 255u) flags |= kWideCnt;
+        if (ind >= 65535u) flags |= kNfIndeg;
         if (virt && ind == 0u) flags |= kNfVsrc;
         if (!virt && dv >= c.d) flags |= kNfDev;
         spl[i] = virt && ind == 1u;
@@ -385,8 +390,7 @@ __global__ void __cluster_dims__(kPackCluster, 1, 1) __launch_bounds__(kPackThre
       const unsigned lt = (1u << lane) - 1u;
       if (multi) {
         const uint32_t slot = bm + __popc(mm & lt);
-        cidx[i] = slot;
-        if (slot < kMaxCnt) cnt0[slot] = static_cast<uint8_t>(min(ind, 255u));
+        cidx[i] = slot;  // cnt0[slot] is written in pass 3a (u8 or u16)
       } else if (src) {
         srcs[bs + __popc(ms & lt)] = i;
       }
@@ -452,12 +456,18 @@ __global__ void __cluster_dims__(kPackCluster, 1, 1) __launch_bounds__(kPackThre
     }
     if (rank == kPackCluster - 1 && threadIdx.x == 0) xoff[n] = total;
     cluster.sync();  // xoff complete (rec[i] reads xoff[i + 1] across ranks)
-    // pass 3a (coalesced): every op's record
+    // pass 3a (coalesced): every op's record, and the counter of every
+    // multi-predecessor op (u16 when some in-degree exceeds a byte)
+    const bool wide = (R0->flags & kWideCnt) != 0;
     for (uint32_t i = lo + threadIdx.x; i < hi; i += kPackThreads) {
       const uint32_t f = c.flags[i];
       const uint32_t ind = indeg[i];
       const bool virt = f & 1u;
       const uint32_t ci = ind >= 2 ? cidx[i] : 0u;
+      if (ind >= 2 && ci < kMaxCnt) {
+        if (wide) reinterpret_cast<uint16_t*>(cnt0)[ci] = static_cast<uint16_t>(min(ind, 65535u));
+        else cnt0[ci] = static_cast<uint8_t>(ind);
+      }
       const uint32_t x0 = xoff[i], x1 = __ldcg(xoff + i + 1);
       const uint32_t cnt = min(x1 - x0, kCntMax);
       const uint32_t z = (uint32_t(c.dev[i]) & kDevMask) | (virt ? kFVirt : 0u) |
@@ -486,8 +496,10 @@ __global__ void __cluster_dims__(kPackCluster, 1, 1) __launch_bounds__(kPackThre
       if (threadIdx.x == 0) {
         PackInfo inf;
         inf.first_missing = s_ctr.first;
-        inf.not_fast = s_ctr.flags | (s_ctr.sum >= 0x7FFFFFFFull ? kNfDur : 0u) |
+        inf.not_fast = (s_ctr.flags & ~kWideCnt) | (s_ctr.sum >= 0x7FFFFFFFull ? kNfDur : 0u) |
                        (s_ctr.ncnt >= kMaxCnt ? kNfSize : 0u);
+        inf.wide = s_ctr.flags & kWideCnt;
+        inf.pad = 0;
         inf.n_cnt = s_ctr.ncnt;
         inf.n_src = s_ctr.nsrc;
         inf.dur_sum = s_ctr.sum;

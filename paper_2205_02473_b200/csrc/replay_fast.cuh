@@ -159,7 +159,7 @@ struct FastWarp {
   uint4* q;                 // [dcap][qc] per-device rings
   uint2* rl;                // [rlcap] {succ_beg, count} ranges to expand
   volatile uint32_t* misc;
-  uint32_t* cw;             // compact counters (u8 in words)
+  uint32_t* cw;             // compact counters (u8 or u16 in words)
   uint32_t qc, rlcap;
   uint32_t* qbuf;
   uint32_t* qpos;
@@ -170,6 +170,7 @@ struct FastWarp {
   int lane;
   int tid;
   uint32_t vcount = 0, dcount = 0, tmax = 0;
+  bool wide = false;  // u16 counters (some in-degree >= 255)
 
   __device__ __forceinline__ uint4* ring(uint32_t d) { return q + (size_t)d * qc; }
 
@@ -227,9 +228,15 @@ struct FastWarp {
     }
     if (a.z & kFMulti) {
       const uint32_t ci = (a.x >> 24) | ((a.z >> 18) << 8);
-      const uint32_t sh = 8u * (ci & 3u);
-      const uint32_t old = atomicSub(&cw[ci >> 2], 1u << sh);
-      if (((old >> sh) & 0xFFu) != 1u) return;
+      if (wide) {  // u16 counters, 2 per word
+        const uint32_t sh = 16u * (ci & 1u);
+        const uint32_t old = atomicSub(&cw[ci >> 1], 1u << sh);
+        if (((old >> sh) & 0xFFFFu) != 1u) return;
+      } else {     // u8 counters, 4 per word
+        const uint32_t sh = 8u * (ci & 3u);
+        const uint32_t old = atomicSub(&cw[ci >> 2], 1u << sh);
+        if (((old >> sh) & 0xFFu) != 1u) return;
+      }
     }
     ready(a, t);
   }
@@ -390,7 +397,7 @@ template <int NW, int KD>
 __device__ uint32_t replay_fast(const Cand& c, int cid, const uint4* rec, const uint4* erec,
                             const uint8_t* cnt0, const uint32_t* srcs, const PackInfo& info,
                             unsigned char* wsm, const FastCfg& F, const Scratch& S,
-                            const Outs& O, bool want_schedule) {
+                            const Outs& O, bool want_schedule, uint32_t* gcw) {
   constexpr uint32_t NT = 32u * NW;
   const int lane = threadIdx.x & 31;
   const int tid = threadIdx.x;
@@ -399,7 +406,9 @@ __device__ uint32_t replay_fast(const Cand& c, int cid, const uint4* rec, const 
   uint4* q = reinterpret_cast<uint4*>(wsm + sizeof(DevF) * F.dcap);
   uint2* rl = reinterpret_cast<uint2*>(q + (size_t)F.dcap * F.qc);
   volatile uint32_t* misc = reinterpret_cast<volatile uint32_t*>(rl + F.rl);
-  uint32_t* cw = const_cast<uint32_t*>(misc) + fast_misc_words(NW);
+  // compact counters: shared memory, or (graphs with more multi-predecessor
+  // ops than fit) this candidate's slice of global scratch, same word atomics
+  uint32_t* cw = gcw ? gcw : const_cast<uint32_t*>(misc) + fast_misc_words(NW);
   volatile uint32_t* red = misc + 4 + NT;  // 4 * NW words
   uint32_t par = 0;
   const unsigned long long oo = c.op_off;
@@ -408,10 +417,11 @@ __device__ uint32_t replay_fast(const Cand& c, int cid, const uint4* rec, const 
                  S.devoff + c.dof_off,
                  want_schedule ? O.start + oo : nullptr,
                  want_schedule ? O.end + oo : nullptr, want_schedule, lane, tid};
+  W.wide = info.wide != 0;
 
   // ---- state init ----
   {
-    const uint32_t nv = (info.n_cnt + 15) / 16;
+    const uint32_t nv = ((info.wide ? 2u : 1u) * info.n_cnt + 15) / 16;
     const uint4* src = reinterpret_cast<const uint4*>(cnt0);
     uint4* dst = reinterpret_cast<uint4*>(cw);
     for (uint32_t i = tid; i < nv; i += NT) dst[i] = __ldg(src + i);
@@ -562,6 +572,8 @@ __device__ uint32_t replay_fast(const Cand& c, int cid, const uint4* rec, const 
 // pass 0: every candidate; ring overflows are marked kRetry.
 // pass 1: only kRetry candidates, with rings as deep as shared memory allows
 // (one CTA per SM); anything still failing takes the general path.
+// pass 2 (instead of 0, for batches of multi-million-op graphs whose device
+// queues never fit the residency-sized rings): mark every candidate kRetry.
 // work: [0] pass-0 counter, [1] general fallbacks, [2] pass-1 counter,
 // [3] deep-ring retries.
 template <int NW, int KD>
@@ -570,7 +582,7 @@ __global__ void __launch_bounds__(32 * NW) replay_fast_kernel(
     FastCfg F, int want_schedule, unsigned* work, int pass) {
   extern __shared__ __align__(16) unsigned char fsm[];
   __shared__ int s_cid;
-  unsigned* counter = work + (pass ? 2 : 0);
+  unsigned* counter = work + (pass == 1 ? 2 : 0);  // pass 0 and 2 share slot 0
   for (;;) {
     if (threadIdx.x == 0) s_cid = static_cast<int>(atomicAdd(counter, 1u));
     __syncthreads();
@@ -578,6 +590,13 @@ __global__ void __launch_bounds__(32 * NW) replay_fast_kernel(
     __syncthreads();
     if (cid >= n_cands) break;
     if (pass == 1 && O.status[cid] != kRetry) continue;
+    if (pass == 2) {  // large graphs: straight to the deep-ring pass
+      if (threadIdx.x == 0) {
+        O.status[cid] = kRetry;
+        atomicAdd(work + 3, 1u);
+      }
+      continue;
+    }
     const Cand c = cands[cid];
     const PackInfo info = P.info[cid];
     if (info.first_missing != kNone) {  // replay.cpp:39-44
@@ -589,10 +608,13 @@ __global__ void __launch_bounds__(32 * NW) replay_fast_kernel(
       continue;
     }
     uint32_t rc = kBailOther;
-    if (info.not_fast == 0 && c.d <= F.dcap && c.d <= 32u * NW * KD && info.n_cnt <= F.ccap)
-      rc = replay_fast<NW, KD>(c, cid, P.rec + P.r_off[cid], P.erec + P.e_off[cid],
-                               P.cnt0 + P.c_off[cid], P.srcs + c.op_off, info, fsm, F, S, O,
-                               want_schedule != 0);
+    if (info.not_fast == 0 && c.d <= F.dcap && c.d <= 32u * NW * KD)
+      rc = replay_fast<NW, KD>(
+          c, cid, P.rec + P.r_off[cid], P.erec + P.e_off[cid], P.cnt0 + P.c_off[cid],
+          P.srcs + c.op_off, info, fsm, F, S, O, want_schedule != 0,
+          (info.wide ? 2u : 1u) * info.n_cnt <= F.ccap
+              ? nullptr
+              : reinterpret_cast<uint32_t*>(P.gcnt + P.c_off[cid]));
     __syncthreads();
     if (rc == kBailRing && pass == 0) {
       if (threadIdx.x == 0) {

@@ -211,6 +211,12 @@ class Batch:
                 "fast_blocks_per_sm": int(st[2]), "ring": int(st[3]),
                 "deep_ring_retries": int(st[4])}
 
+    def pack_info(self) -> np.ndarray:
+        """[n, 4]: first op without duration, not-fast bits, multi-pred ops, sources."""
+        out = np.zeros((max(1, self.n), 4), np.uint32)
+        N.lib.dpro_cuda_batch_pack_info(self.handle, N.ptr(out))
+        return out[: self.n]
+
     def device_results(self) -> dict:
         ps = [C.c_void_p() for _ in range(5)]
         N.lib.dpro_cuda_batch_device_results(self.handle, *[C.byref(p) for p in ps])
