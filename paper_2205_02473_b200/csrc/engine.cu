@@ -191,7 +191,9 @@ struct dpro_ctx {
   }
   int fast = 1;       // option "fast"
   uint32_t ring = 4;  // option "ring"
-  int warps = 4;      // option "warps": warps (1, 2, 4) per candidate
+  int warps = 4;      // option "warps": warps (1, 2, 4, 8) per candidate
+  int gcnt = 0;       // option "gcnt": 1 = fast-path counters always in global scratch
+  int deep_first = -1;  // option "deep_first": -1 auto (mean V > 1M), 0 never, 1 always
   dpro_batch* spare = nullptr;  // recycled arenas for repeated small calls
 };
 
@@ -1030,6 +1032,14 @@ int dpro_cuda_set_option(dpro_ctx* ctx, const char* key, int64_t value) {
     ctx->warps = static_cast<int>(value);
     return DPRO_OK;
   }
+  if (k == "gcnt" && (value == 0 || value == 1)) {
+    ctx->gcnt = static_cast<int>(value);
+    return DPRO_OK;
+  }
+  if (k == "deep_first" && value >= -1 && value <= 1) {
+    ctx->deep_first = static_cast<int>(value);
+    return DPRO_OK;
+  }
   if (k == "ring" && value >= 2 && value <= 64 && (value & (value - 1)) == 0) {
     ctx->ring = static_cast<uint32_t>(value);
     return DPRO_OK;
@@ -1086,7 +1096,9 @@ int launch_fast_kd(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule, FastCfg 
   b->F = F;
   // graphs of millions of ops (configs 4/5) overflow the residency-sized
   // rings every time: send them straight to the deep-ring pass
-  const bool deep_first = b->n > 0 && b->sum_n / b->n > 1000000ull;
+  const bool deep_first = ctx->deep_first >= 0
+                              ? ctx->deep_first == 1
+                              : (b->n > 0 && b->sum_n / b->n > 1000000ull);
   kern<<<grid, 32 * NW, smem, ctx->stream>>>(b->desc.as<Cand>(), b->n, b->S, b->O, b->P, F,
                                              want_schedule ? 1 : 0, b->work.as<unsigned>(),
                                              deep_first ? 2 : 0);
@@ -1122,7 +1134,8 @@ int launch_fast_nw(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
   const size_t limit = ctx->smem_optin - 64;
   // counters that would leave fewer than 4 candidates per SM stay in global
   // scratch instead (large graphs: configs 4/5 have 10^5+ multi-pred ops)
-  if (fast_bytes(F.dcap, F.qc, F.rl, F.ccap, NW) > size_t(ctx->smem_per_sm) / 4) F.ccap = 16;
+  if (ctx->gcnt || fast_bytes(F.dcap, F.qc, F.rl, F.ccap, NW) > size_t(ctx->smem_per_sm) / 4)
+    F.ccap = 16;
   while (fast_bytes(F.dcap, F.qc, F.rl, F.ccap, NW) > limit && F.ccap > 16)
     F.ccap = std::max<uint32_t>(16, (F.ccap / 2 + 15) & ~15u);
   while (fast_bytes(F.dcap, F.qc, F.rl, F.ccap, NW) > limit && F.dcap > 1) F.dcap /= 2;

@@ -45,18 +45,25 @@ def _batch_check(engine, graphs, expects, label):
                     assert (busy[d] / T if T > 0 else 0.0) == pytest.approx(u, abs=0), name
 
 
-@pytest.fixture(params=["fast", "fast_w1", "fast_w2", "general", "fast_ring2"])
+@pytest.fixture(params=["fast", "fast_w1", "fast_w2", "general", "fast_ring2", "fast_gcnt",
+                        "fast_deep"])
 def mode_engine(engine, request):
     """Both kernels: the on-chip fast path (1, 2 or 4 warps per candidate,
     with exact fallback) and the general global-memory kernel; ring=2 forces
-    frequent fast-path bail-outs."""
+    frequent fast-path bail-outs; gcnt keeps the fast path's counters in
+    global scratch (the large-graph layout); deep runs every candidate in
+    the deep-ring pass (the large-graph schedule)."""
     engine.set_option("fast", 0 if request.param == "general" else 1)
     engine.set_option("ring", 2 if request.param == "fast_ring2" else 4)
     engine.set_option("warps", {"fast_w1": 1, "fast_w2": 2}.get(request.param, 4))
+    engine.set_option("gcnt", 1 if request.param == "fast_gcnt" else 0)
+    engine.set_option("deep_first", 1 if request.param == "fast_deep" else -1)
     yield engine
     engine.set_option("fast", 1)
     engine.set_option("ring", 4)
     engine.set_option("warps", 4)
+    engine.set_option("gcnt", 0)
+    engine.set_option("deep_first", -1)
 
 
 def test_reference_golden_vectors_bit_exact(mode_engine):
@@ -240,3 +247,35 @@ def test_reference_acceptance_suite_with_gpu_replay():
     assert len(lines) == 10
     for l in lines[:9]:
         assert l.startswith("[PASS]"), l
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fan", [254, 255, 256, 600, 3000])
+def test_wide_counters_high_indegree(engine, port, fan):
+    """In-degrees past a byte switch the fast path to u16 counters
+    (PackInfo.wide); results must not change and no candidate may fall back
+    to the general kernel."""
+    rng = np.random.default_rng(fan)
+    graphs = []
+    for t in range(6):
+        b = GraphBuilder()
+        for i in range(fan):
+            b.add_op(comp(f"p{i:05d}", f"d{i % 24}", int(rng.integers(0, 7))))
+        b.add_op(comp("sink", "d0", 3))
+        b.add_op(comp("zz_after", "d1", 2))
+        for i in range(fan):
+            b.add_edge(f"p{i:05d}", "sink")
+        b.add_edge("sink", "zz_after")
+        for i in range(0, fan - 1, 7):  # some chains among the producers
+            b.add_edge(f"p{i:05d}", f"p{i + 1:05d}")
+        graphs.append(b.build())
+    batch = engine.batch([Csr.from_dict(g.to_csr()) for g in graphs])
+    batch.replay(want_schedule=True)
+    ms, st, er, start, end = batch.results(schedule=True)
+    assert batch.stats()["fallbacks"] == 0
+    assert batch.pack_info()[:, 1].tolist() == [0] * len(graphs)  # fast-path eligible
+    for i, g in enumerate(graphs):
+        exp = port.port_replay(Csr.from_dict(g.to_csr()))
+        a, z = int(batch.op_off[i]), int(batch.op_off[i + 1])
+        assert st[i] == 0 and ms[i] == exp["T"]
+        assert np.array_equal(start[a:z], exp["start"]) and np.array_equal(end[a:z], exp["end"])
