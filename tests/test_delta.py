@@ -126,3 +126,26 @@ def test_gpu_delta_one_shot_and_makespan_only(engine):
                                             len(specs), N.ptr(ms), N.ptr(st), N.ptr(er))
     assert rc == 0 and np.all(st == 0)
     assert np.array_equal(ms, ms0)
+
+
+@pytest.mark.gpu
+def test_config4_scale_candidates_match_oracle(engine, port):
+    """BASELINE config 4 shape (GPT-2 medium, 64-worker ring, 4.8M ops):
+    delta candidates on the fast path (u16 counters in global scratch,
+    deep-ring pass) equal the C oracle on the host-merged CSR."""
+    from paper_2205_02473_b200.workloads import workload
+    w = workload(4)
+    base = LayeredBase(w.model, w.cluster)
+    pk = w.candidate_partitions(2, tensors_per_cand=8)
+    specs = [([[i] for i in range(w.layers)], pk[c].tolist()) for c in range(2)]
+    res = engine.resident(base.graph().csr)
+    b = engine.delta_batch(res, base.deltas(specs, threads=16))
+    b.replay(want_schedule=True)
+    ms, st, er, s, e = b.results(schedule=True)
+    assert b.stats()["fallbacks"] == 0 and np.all(st == 0)
+    full = base.candidates(specs, threads=16)
+    for i, g in enumerate(full):
+        exp = port.port_replay(g.csr)
+        a, z = int(b.op_off[i]), int(b.op_off[i + 1])
+        assert ms[i] == exp["T"]
+        assert np.array_equal(s[a:z], exp["start"]) and np.array_equal(e[a:z], exp["end"])
