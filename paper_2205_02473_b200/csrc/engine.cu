@@ -390,7 +390,7 @@ int upload_host(dpro_ctx* ctx, dpro_batch* b, const dpro_csr* cands) {
 
 int finish_batch(dpro_ctx* ctx, dpro_batch* b);
 int run_pack(dpro_ctx* ctx, dpro_batch* b);
-int run_merge(dpro_ctx* ctx, dpro_batch* b);
+int run_merge(dpro_ctx* ctx, dpro_batch* b, int32_t c0, int32_t c1);
 
 int build_batch(dpro_ctx* ctx, dpro_batch* b, const dpro_csr* cands) {
   const int32_t n = b->n;
@@ -710,33 +710,62 @@ int build_delta_batch(dpro_ctx* ctx, dpro_batch* b, const dpro_resident* r,
                       const dpro_delta* deltas) {
   Tracer tr;
   const int32_t n = b->n;
-  // delta blob layout (sizes need no checks); null arrays are caught below
-  std::vector<size_t> boff(n + 1, 0);
+  // Sizes known without the checks: op counts exactly, edges as a bound
+  // (base edges + added ones), devices. They fix the arena and descriptor
+  // layouts up front, so every chunk of candidates can be copied and merged
+  // as soon as the pool has checked and staged it (host work || H2D || K0).
+  std::vector<size_t> boff(n + 1, 0), aoff(n + 1, 0);
+  std::vector<uint32_t> nops(n), nedges(n);
+  b->hc.assign(n, Cand{});
+  b->n_ops.resize(n);
+  b->n_dev.resize(n);
+  b->n_edges.resize(n);
+  unsigned long long so = 0, sd = 0, sdo = 0;
+  uint32_t max_n = 0;
   for (int32_t i = 0; i < n; ++i) {
     const dpro_delta& D = deltas[i];
+    if (!D.new_succ_off || D.n_removed > r->n)
+      return set_err(ctx, DPRO_EINVAL, "delta " + std::to_string(i) + ": bad sizes");
     const size_t nn = D.n_new;
-    const size_t ne = D.new_succ_off ? D.new_succ_off[nn] : 0;
+    const size_t ne = D.new_succ_off[nn];
     boff[i + 1] = boff[i] + align16(size_t(D.n_removed) * 4) + align16(nn * 4) +
                   align16(nn * 8) + align16(nn * 2) + align16(nn) + align16((nn + 1) * 4) +
                   align16(ne * 4) + 2 * align16(size_t(D.n_extra) * 4) +
                   align16(size_t(D.n_cut) * 4);
+    nops[i] = r->n - D.n_removed + D.n_new;
+    const size_t v = nops[i], e_bound = size_t(r->e) + D.n_extra + ne;
+    // dur slot sized for int64: the int32 decision needs the checks
+    aoff[i + 1] = aoff[i] + align16(v * 8) + align16(v * 2) + align16(v) +
+                  align16((v + 1) * 4) + align16(e_bound * 4) + align16(v * 4);
+    Cand& h = b->hc[i];
+    h.n = nops[i];
+    h.d = D.n_devices;
+    h.op_off = so;
+    h.dev_off = sd;
+    h.dof_off = sdo;
+    so += h.n;
+    sd += h.d;
+    sdo += h.d + 1;
+    max_n = std::max(max_n, h.n);
   }
   CU(cudaStreamSynchronize(ctx->stream));  // staging may feed an earlier copy
   CU(b->dblob.ensure(boff[n] + 16));
   CU(ctx->staging.ensure(boff[n] + 16));
-  char* stage = static_cast<char*>(ctx->staging.p);
+  CU(b->arena.ensure(aoff[n] + 16));
+  tr.mark("sizes + buffers");
   const uint32_t W = (r->n >> 5) + 1;
   const size_t rank_words = (3 * size_t(W) + 1 + r->n + 3) & ~size_t(3);
+  CU(b->rank.ensure(rank_words * 4 * size_t(std::max(n, 1))));
+  CU(b->ddesc.ensure(sizeof(dpro_k::DeltaDev) * std::max(n, 1)));
+  CU(b->desc.ensure(sizeof(Cand) * std::max(n, 1)));
+  b->res = r;
+  b->smem_ind = std::min(max_n, dpro_k::kMergeIndegSmem);
+  char* stage = static_cast<char*>(ctx->staging.p);
   std::vector<dpro_k::DeltaDev> dd(n);
-  std::vector<uint32_t> nops(n), nedges(n);
-  std::vector<uint8_t> d32(n);
   std::vector<std::string> errs(n);
-  // one pass per candidate on the pool: check, count, pack into staging;
-  // this thread copies each finished ~16 MB chunk while the rest packs
-  std::vector<int32_t> chunk_end;
+  std::vector<int32_t> chunk_end;  // one merge wave (a candidate per SM) per chunk
   for (int32_t i = 0; i < n;) {
-    int32_t j = i + 1;
-    while (j < n && boff[j] - boff[i] < (size_t(16) << 20)) ++j;
+    const int32_t j = std::min<int32_t>(n, i + ctx->sm_count);
     chunk_end.push_back(j);
     i = j;
   }
@@ -749,9 +778,9 @@ int build_delta_batch(dpro_ctx* ctx, dpro_batch* b, const dpro_resident* r,
   }
   ctx->workers().start(n, [&](int32_t i) {
     const dpro_delta& D = deltas[i];
-    bool f = true;
-    errs[i] = check_delta(*r, D, nops[i], nedges[i], f);
-    d32[i] = f;
+    bool d32 = true;
+    uint32_t v = 0;
+    errs[i] = check_delta(*r, D, v, nedges[i], d32);
     if (errs[i].empty()) {
       dpro_k::DeltaDev& x = dd[i];
       size_t o = boff[i];
@@ -777,94 +806,77 @@ int build_delta_batch(dpro_ctx* ctx, dpro_batch* b, const dpro_resident* r,
       x.n_extra = D.n_extra;
       x.n_cut = D.n_cut;
       x.rank_off = rank_words * size_t(i);
+      Cand& h = b->hc[i];
+      h.e = nedges[i];
+      h.dur64 = d32 ? 0 : 1;
+      size_t o2 = aoff[i];
+      h.dur = b->arena.as<void>(o2); o2 += align16(size_t(h.n) * 8);
+      h.dev = b->arena.as<uint16_t>(o2); o2 += align16(size_t(h.n) * 2);
+      h.flags = b->arena.as<uint8_t>(o2); o2 += align16(h.n);
+      h.succ_off = b->arena.as<uint32_t>(o2); o2 += align16((size_t(h.n) + 1) * 4);
+      h.succ = b->arena.as<uint32_t>(o2);
+      o2 += align16((size_t(r->e) + D.n_extra + D.new_succ_off[nn]) * 4);
+      h.indeg = b->arena.as<uint32_t>(o2);  // written by the merge
     }
     left[chunk_of[i]].fetch_sub(1, std::memory_order_release);
   });
   int err = DPRO_OK;
   for (int k = 0, i = 0; k < nchunks; ++k) {
     while (left[k].load(std::memory_order_acquire) > 0) std::this_thread::yield();
-    const size_t a0 = boff[i], z0 = boff[chunk_end[k]];
-    if (err == DPRO_OK && z0 > a0) {
-      const cudaError_t e = cudaMemcpyAsync(b->dblob.as<char>(a0), stage + a0, z0 - a0,
-                                            cudaMemcpyHostToDevice, ctx->stream);
+    const int32_t c0 = i, c1 = chunk_end[k];
+    bool ok = err == DPRO_OK;
+    for (int32_t j = c0; j < c1 && ok; ++j) ok = errs[j].empty();
+    if (ok) {  // this chunk: deltas, descriptors, merge -- while the pool stages the next
+      const size_t a0 = boff[c0], z0 = boff[c1];
+      cudaError_t e = cudaSuccess;
+      if (z0 > a0)
+        e = cudaMemcpyAsync(b->dblob.as<char>(a0), stage + a0, z0 - a0, cudaMemcpyHostToDevice,
+                            ctx->stream);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(b->ddesc.as<dpro_k::DeltaDev>() + c0, dd.data() + c0,
+                            sizeof(dpro_k::DeltaDev) * (c1 - c0), cudaMemcpyHostToDevice,
+                            ctx->stream);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(b->desc.as<Cand>() + c0, b->hc.data() + c0,
+                            sizeof(Cand) * (c1 - c0), cudaMemcpyHostToDevice, ctx->stream);
       if (e != cudaSuccess) err = set_err(ctx, DPRO_ECUDA, cudaGetErrorString(e));
+      if (err == DPRO_OK) err = run_merge(ctx, b, c0, c1);
     }
-    i = chunk_end[k];
+    i = c1;
   }
   ctx->workers().wait();
+  tr.mark("host check + stage (merges queued)");
   if (err != DPRO_OK) return err;
   for (int32_t i = 0; i < n; ++i)
     if (!errs[i].empty())
       return set_err(ctx, DPRO_EINVAL, "delta " + std::to_string(i) + ": " + errs[i]);
-  tr.mark("host: check + pack || H2D");
-  b->hc.resize(n);
-  b->n_ops.resize(n);
-  b->n_dev.resize(n);
-  b->n_edges.resize(n);
-  std::vector<size_t> aoff(n + 1, 0);
+  unsigned long long se = 0;
   for (int32_t i = 0; i < n; ++i) {
-    const size_t v = nops[i], e = nedges[i];
-    aoff[i + 1] = aoff[i] + align16(v * (d32[i] ? 4 : 8)) + align16(v * 2) + align16(v) +
-                  align16((v + 1) * 4) + align16(e * 4) + align16(v * 4);
-  }
-  CU(b->arena.ensure(aoff[n] + 16));
-  CU(b->rank.ensure(rank_words * 4 * size_t(std::max(n, 1))));
-  CU(b->ddesc.ensure(sizeof(dpro_k::DeltaDev) * std::max(n, 1)));
-  unsigned long long so = 0, sd = 0, sdo = 0, se = 0;
-  for (int32_t i = 0; i < n; ++i) {
-    Cand& h = b->hc[i];
-    std::memset(&h, 0, sizeof h);
-    h.n = nops[i];
-    h.e = nedges[i];
-    h.d = deltas[i].n_devices;
-    h.op_off = so;
-    h.dev_off = sd;
-    h.dof_off = sdo;
-    h.dur64 = d32[i] ? 0 : 1;
-    size_t o = aoff[i];
-    h.dur = b->arena.as<void>(o); o += align16(size_t(h.n) * (d32[i] ? 4 : 8));
-    h.dev = b->arena.as<uint16_t>(o); o += align16(size_t(h.n) * 2);
-    h.flags = b->arena.as<uint8_t>(o); o += align16(h.n);
-    h.succ_off = b->arena.as<uint32_t>(o); o += align16((size_t(h.n) + 1) * 4);
-    h.succ = b->arena.as<uint32_t>(o); o += align16(size_t(h.e) * 4);
-    h.indeg = b->arena.as<uint32_t>(o);  // written by the merge
+    const Cand& h = b->hc[i];
     b->n_ops[i] = h.n;
     b->n_dev[i] = h.d;
     b->n_edges[i] = h.e;
     b->max_d = std::max(b->max_d, h.d);
-    so += h.n;
-    sd += h.d;
-    sdo += h.d + 1;
     se += h.e;
   }
   b->sum_n = so;
   b->sum_d = sd;
   b->sum_dof = sdo;
   b->sum_e = se;
-  CU(cudaMemcpyAsync(b->ddesc.p, dd.data(), sizeof(dpro_k::DeltaDev) * n,
-                     cudaMemcpyHostToDevice, ctx->stream));
-  CU(b->desc.ensure(sizeof(Cand) * std::max(n, 1)));
-  CU(cudaMemcpyAsync(b->desc.p, b->hc.data(), sizeof(Cand) * n, cudaMemcpyHostToDevice,
-                     ctx->stream));
-  uint32_t max_n = 0;
-  for (int32_t i = 0; i < n; ++i) max_n = std::max(max_n, nops[i]);
-  b->res = r;
-  b->smem_ind = std::min(max_n, dpro_k::kMergeIndegSmem);
-  const int st = run_merge(ctx, b);
-  if (st != DPRO_OK) return st;
-  tr.mark("merge kernel", ctx->stream, true);
+  tr.mark("remaining H2D + merge", ctx->stream, true);
   return finish_batch(ctx, b);
 }
 
-int run_merge(dpro_ctx* ctx, dpro_batch* b) {
-  if (b->n == 0) return DPRO_OK;
+// K0 for candidates [c0, c1) (descriptors already on the device).
+int run_merge(dpro_ctx* ctx, dpro_batch* b, int32_t c0, int32_t c1) {
+  if (c1 <= c0) return DPRO_OK;
   const size_t smem = size_t(b->smem_ind) * 4;
   CU(cudaFuncSetAttribute(dpro_k::delta_merge_kernel,
                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  dpro_k::delta_merge_kernel<<<std::min<int>(b->n, ctx->sm_count), dpro_k::kMergeThreads, smem,
-                               ctx->stream>>>(b->res->dev, b->ddesc.as<dpro_k::DeltaDev>(),
-                                              b->desc.as<Cand>(), b->n, b->rank.as<uint32_t>(),
-                                              b->smem_ind);
+  dpro_k::delta_merge_kernel<<<std::min<int>(c1 - c0, ctx->sm_count), dpro_k::kMergeThreads,
+                               smem, ctx->stream>>>(
+      b->res->dev, b->ddesc.as<dpro_k::DeltaDev>() + c0, b->desc.as<Cand>() + c0, c1 - c0,
+      b->rank.as<uint32_t>(), b->smem_ind);
   CU(cudaGetLastError());
   return DPRO_OK;
 }
@@ -975,7 +987,7 @@ int dpro_cuda_batch_prepare(dpro_ctx* ctx, dpro_batch* b) {
   if (!ctx || !b) return DPRO_EINVAL;
   CU(cudaSetDevice(ctx->device));
   if (b->res) {
-    const int st = run_merge(ctx, b);
+    const int st = run_merge(ctx, b, 0, b->n);
     if (st != DPRO_OK) return st;
   }
   return run_pack(ctx, b);
