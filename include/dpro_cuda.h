@@ -213,10 +213,10 @@ typedef struct dpro_resident dpro_resident;
 /* Uploads a base graph (host CSR) to HBM; it stays resident until destroyed. */
 dpro_resident* dpro_cuda_resident_create(dpro_ctx* ctx, const dpro_csr* base);
 void dpro_cuda_resident_destroy(dpro_ctx* ctx, dpro_resident* r);
-/* A batch of n candidates given as host deltas against r: one H2D copy of
+/* A batch of n candidates given as host deltas against r: H2D copies of
  * the deltas, the merge on the GPU, then the same packing as
- * dpro_cuda_batch_create. The resident must outlive nothing: the batch
- * holds merged copies. */
+ * dpro_cuda_batch_create. The batch holds merged copies; r must stay alive
+ * only while dpro_cuda_batch_prepare may be called on the batch. */
 dpro_batch* dpro_cuda_batch_create_delta(dpro_ctx* ctx, const dpro_resident* r,
                                          const dpro_delta* deltas, int32_t n);
 /* Per-candidate op / edge / device counts of a registered batch (any

@@ -147,6 +147,7 @@ class Batch:
     def __init__(self, engine: Engine, cands, memspace: int, resident: Resident | None = None):
         self.engine = engine
         self._keep = cands if resident is not None else list(cands)
+        self._resident = resident  # prepare() re-reads the base graph in HBM
         self.with_schedule = False
         self.handle = None
         if resident is not None:  # delta batch
