@@ -89,7 +89,8 @@ __device__ __forceinline__ bool is_cut(const DeltaDev& D, uint32_t e) {
 // memory (dynamic smem of smem_ind words; larger candidates count in HBM).
 __global__ void __launch_bounds__(kMergeThreads, 1)
     delta_merge_kernel(ResDev B, const DeltaDev* __restrict__ deltas, const Cand* __restrict__ cands,
-                       int n_cands, uint32_t* __restrict__ rank_scratch, uint32_t smem_ind) {
+                       int n_cands, uint32_t* __restrict__ rank_scratch, uint32_t smem_ind,
+                       uint32_t* __restrict__ pred1) {
   using Scan = cub::BlockScan<uint32_t, kMergeThreads>;
   __shared__ typename Scan::TempStorage scan_tmp;
   __shared__ uint32_t s_carry;
@@ -124,6 +125,7 @@ __global__ void __launch_bounds__(kMergeThreads, 1)
     uint32_t* ind = ind_smem ? s_ind : ind_g;
     for (uint32_t i = threadIdx.x; i < C.n; i += blockDim.x) ind[i] = 0;
     uint32_t* off = const_cast<uint32_t*>(C.succ_off);
+    uint32_t* p1 = pred1 + C.op_off;  // a predecessor of every op (exact when indeg is 1)
     uint32_t* succ = const_cast<uint32_t*>(C.succ);
     uint16_t* dev = const_cast<uint16_t*>(C.dev);
     uint8_t* flags = const_cast<uint8_t*>(C.flags);
@@ -207,21 +209,25 @@ __global__ void __launch_bounds__(kMergeThreads, 1)
         if (nxt <= xv) {  // extras never repeat a kept base edge (dpro_delta)
           succ[o++] = nxt;
           atomicAdd(&ind[nxt], 1u);
+          p1[nxt] = fb;
           advance();
         } else {
           succ[o++] = xv;
           atomicAdd(&ind[xv], 1u);
+          p1[xv] = fb;
           ++x;
         }
       }
     }
     for (uint32_t j = threadIdx.x; j < D.n_new; j += blockDim.x) {
       const uint32_t p = __ldg(D.new_pos + j);
-      uint32_t o = off[p - R.r(p) + j];
+      const uint32_t fj = p - R.r(p) + j;
+      uint32_t o = off[fj];
       for (uint32_t k = __ldg(D.new_succ_off + j); k < __ldg(D.new_succ_off + j + 1); ++k) {
         const uint32_t t = __ldg(D.new_succ + k);
         succ[o++] = t;
         atomicAdd(&ind[t], 1u);
+        p1[t] = fj;
       }
     }
     __syncthreads();

@@ -222,6 +222,7 @@ struct dpro_batch {
   DevBuf dblob;   // uploaded deltas (delta batches)
   DevBuf ddesc;   // DeltaDev[n]
   DevBuf rank;    // merge rank scratch
+  DevBuf pred1;   // delta batches: a predecessor per op (written by the merge)
   const dpro_resident* res = nullptr;  // delta batches: the base
   uint32_t smem_ind = 0;               // merge kernel in-degree smem words
   size_t s_cnt0 = 0;
@@ -510,6 +511,7 @@ int finish_batch(dpro_ctx* ctx, dpro_batch* b) {
     b->P.cidx = b->pack.as<uint32_t>(po); po += s_u32;
     b->P.xoff = b->pack.as<uint32_t>(po); po += s_xoff;
     b->P.spl = b->pack.as<uint8_t>(po); po += s_spl;
+    b->P.pred1 = b->res ? b->pred1.as<uint32_t>() : nullptr;
     b->P.r_off = b->pack.as<unsigned long long>(po); po += s_off;
     b->P.e_off = b->pack.as<unsigned long long>(po); po += s_off;
     b->P.c_off = b->pack.as<unsigned long long>(po); po += s_off;
@@ -758,6 +760,7 @@ int build_delta_batch(dpro_ctx* ctx, dpro_batch* b, const dpro_resident* r,
   CU(b->rank.ensure(rank_words * 4 * size_t(std::max(n, 1))));
   CU(b->ddesc.ensure(sizeof(dpro_k::DeltaDev) * std::max(n, 1)));
   CU(b->desc.ensure(sizeof(Cand) * std::max(n, 1)));
+  CU(b->pred1.ensure(so * 4 + 16));
   b->res = r;
   b->smem_ind = std::min(max_n, dpro_k::kMergeIndegSmem);
   char* stage = static_cast<char*>(ctx->staging.p);
@@ -876,7 +879,7 @@ int run_merge(dpro_ctx* ctx, dpro_batch* b, int32_t c0, int32_t c1) {
   dpro_k::delta_merge_kernel<<<std::min<int>(c1 - c0, ctx->sm_count), dpro_k::kMergeThreads,
                                smem, ctx->stream>>>(
       b->res->dev, b->ddesc.as<dpro_k::DeltaDev>() + c0, b->desc.as<Cand>() + c0, c1 - c0,
-      b->rank.as<uint32_t>(), b->smem_ind);
+      b->rank.as<uint32_t>(), b->smem_ind, b->pred1.as<uint32_t>());
   CU(cudaGetLastError());
   return DPRO_OK;
 }

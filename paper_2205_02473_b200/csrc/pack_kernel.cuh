@@ -72,6 +72,7 @@ struct PackOut {
   uint32_t* cidx;              // [sum n] scratch: counter slot per op
   uint32_t* xoff;              // [sum (n+1)] scratch: expanded list offsets
   uint8_t* spl;                // [sum n] scratch: spliced virtual op marks
+  const uint32_t* pred1;       // [sum n] a predecessor of each op (delta batches), or null
   unsigned long long* r_off;   // per candidate offset into rec (in records)
   unsigned long long* e_off;   // per candidate offset into erec (in edges)
   unsigned long long* c_off;   // per candidate byte offset into cnt0
@@ -422,6 +423,19 @@ __global__ void __cluster_dims__(kPackCluster, 1, 1) __launch_bounds__(kPackThre
         part += len;
       }
       if (deep) atomicOr(&R0->flags, kNfChain);
+      if (part) atomicAdd(&s_len, part);
+    } else if (P.pred1) {
+      // out-degrees, then each spliced op adds its list to its single
+      // predecessor's (O(V) + O(spliced) instead of a pass over the edges)
+      const uint32_t* p1 = P.pred1 + c.op_off;
+      for (uint32_t i = lo + threadIdx.x; i < hi; i += kPackThreads)
+        xoff[i] = spl[i] ? 0u : c.succ_off[i + 1] - c.succ_off[i];
+      cluster.sync();
+      for (uint32_t i = lo + threadIdx.x; i < hi; i += kPackThreads)
+        if (spl[i]) atomicAdd(&xoff[p1[i]], c.succ_off[i + 1] - c.succ_off[i]);
+      cluster.sync();
+      uint32_t part = 0;
+      for (uint32_t i = lo + threadIdx.x; i < hi; i += kPackThreads) part += __ldcg(xoff + i);
       if (part) atomicAdd(&s_len, part);
     } else {
       uint32_t part = 0;
