@@ -342,8 +342,17 @@ class LayeredBase:
     def deltas(self, specs: Sequence[tuple[Sequence[Sequence[int]], Sequence[int]]],
                threads: int = 8) -> "DeltaSet":
         """[(groups, ks), ...] -> unmerged deltas for Engine.delta_batch."""
-        n = len(specs)
-        n_groups, spec_off, group_off, members, ks = self._spec_arrays(specs)
+        return self.deltas_from_arrays(*self._spec_arrays(specs), threads=threads)
+
+    def deltas_from_arrays(self, n_groups, spec_off, group_off, members, ks,
+                           threads: int = 8) -> "DeltaSet":
+        """Same, from the flattened spec arrays of dpro_base_delta_batch."""
+        n = len(n_groups)
+        n_groups = np.ascontiguousarray(n_groups, np.int32)
+        spec_off = np.ascontiguousarray(spec_off, np.int64)
+        group_off = np.ascontiguousarray(group_off, np.int32)
+        members = np.ascontiguousarray(members, np.int32)
+        ks = np.ascontiguousarray(ks, np.int32)
         out = C.c_void_p()
         rc = N.lib.dpro_base_delta_batch(self.handle, n, N.ptr(n_groups), N.ptr(spec_off),
                                          N.ptr(group_off), N.ptr(members), N.ptr(ks), threads,

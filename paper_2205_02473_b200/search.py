@@ -167,6 +167,86 @@ class SyncSearch:
             c.ks[i] = int(self.rng.integers(1, cap + 1))
         return c
 
+    # ---- vectorized proposals --------------------------------------------
+    # A state of a layered model is its fusion boundaries (cuts[i]: layers i
+    # and i+1 sync as different units) plus the partition count of each unit
+    # (kl[start of unit]); units are always contiguous layer ranges.
+    def _cuts_kl(self, s: SyncState):
+        L = self.model.layers
+        cuts = np.zeros(max(L - 1, 0), bool)
+        kl = np.ones(L, np.int32)
+        for g, k in zip(s.groups, s.ks):
+            kl[g[0]] = k
+            if g[-1] < L - 1:
+                cuts[g[-1]] = True
+        return cuts, kl
+
+    @staticmethod
+    def _state(cuts: np.ndarray, kl: np.ndarray) -> SyncState:
+        starts = [0] + (np.flatnonzero(cuts) + 1).tolist()
+        ends = starts[1:] + [len(kl)]
+        return SyncState([list(range(a, b)) for a, b in zip(starts, ends)],
+                         [int(kl[a]) for a in starts])
+
+    def propose_many(self, s: SyncState, n: int):
+        """n neighbours of s at once (same moves and probabilities as
+        propose()): (cuts[n, L-1], kl[n, L])."""
+        L = self.model.layers
+        cuts0, kl0 = self._cuts_kl(s)
+        starts = np.array([g[0] for g in s.groups])
+        sizes = np.array([len(g) for g in s.groups])
+        G = len(starts)
+        ctb = np.concatenate([[0], np.cumsum(np.asarray(self.model.tensor_bytes, np.int64))])
+        gbytes = ctb[starts + sizes] - ctb[starts]
+        multi = np.flatnonzero(sizes > 1)
+        cuts = np.repeat(cuts0[None], n, 0)
+        kl = np.repeat(kl0[None], n, 0)
+        move = self.rng.integers(0, 3, n)
+        m0 = (move == 0) & (G > 1)
+        m1 = (move == 1) & (len(multi) > 0)
+        m2 = ~(m0 | m1)
+        r0 = np.flatnonzero(m0)
+        if len(r0):  # fuse units j, j+1
+            j = self.rng.integers(0, G - 1, len(r0))
+            cuts[r0, starts[j + 1] - 1] = False
+            kl[r0, starts[j]] = 1
+        r1 = np.flatnonzero(m1)
+        if len(r1):  # split a multi-layer unit at a random inner point
+            gi = multi[self.rng.integers(0, len(multi), len(r1))]
+            cut = (self.rng.random(len(r1)) * (sizes[gi] - 1)).astype(np.int64) + 1
+            cuts[r1, starts[gi] + cut - 1] = True
+            kl[r1, starts[gi]] = 1
+            kl[r1, starts[gi] + cut] = 1
+        r2 = np.flatnonzero(m2)
+        if len(r2):  # re-partition a unit, k uniform in [1, min(kmax, bytes)]
+            gi = self.rng.integers(0, G, len(r2))
+            cap = np.minimum(self.kmax, gbytes[gi])
+            kl[r2, starts[gi]] = (self.rng.random(len(r2)) * cap).astype(np.int64) + 1
+        return cuts, kl
+
+    def _spec_arrays(self, cuts: np.ndarray, kl: np.ndarray):
+        """Flattened dpro_base_delta_batch specs of a proposal matrix."""
+        n, L = kl.shape
+        smask = np.concatenate([np.ones((n, 1), bool), cuts], axis=1)
+        r, p = np.nonzero(smask)  # row-major: units of each row in layer order
+        nxt = np.append(np.where(r[1:] == r[:-1], p[1:], L), L)
+        n_groups = np.bincount(r, minlength=n).astype(np.int32)
+        spec_off = np.concatenate([[0], np.cumsum(n_groups)[:-1]]).astype(np.int64)
+        group_off = np.concatenate([[0], np.cumsum(nxt - p)]).astype(np.int32)
+        members = np.tile(np.arange(L, dtype=np.int32), n)
+        return n_groups, spec_off, group_off, members, kl[r, p].astype(np.int32)
+
+    def evaluate_arrays(self, cuts: np.ndarray, kl: np.ndarray) -> np.ndarray:
+        """Exact makespans of a proposal matrix: one GPU batch."""
+        deltas = self.base.deltas_from_arrays(*self._spec_arrays(cuts, kl), threads=self.threads)
+        b = self.engine.delta_batch(self.resident, deltas)
+        b.replay(want_schedule=False)
+        ms, st, *_ = b.results()
+        if np.any(st != 0):
+            raise RuntimeError(f"replay failed for {int((st != 0).sum())} candidates")
+        self.log.evaluated += len(ms)
+        return ms
+
     def evaluate(self, states: Sequence[SyncState]) -> np.ndarray:
         """Exact makespans of candidate states: deltas against the resident
         base graph, merged, packed and replayed in one GPU batch."""
@@ -200,11 +280,12 @@ class SyncSearch:
         if s.makespan < 0:
             s.makespan = int(self.evaluate([s])[0])
             self.best = s.copy()
-        cands = [self.propose(s) for _ in range(batch)]
-        ms = self.evaluate(cands)
+        cuts, kl = self.propose_many(s, batch)
+        ms = self.evaluate_arrays(cuts, kl)
         i = int(np.argmin(ms))
-        cands[i].makespan = int(ms[i])
-        prop = self._exchange(int(ms[i]), i, cands[i])
+        cand = self._state(cuts[i], kl[i])
+        cand.makespan = int(ms[i])
+        prop = self._exchange(int(ms[i]), i, cand)
         # Metropolis acceptance (memory loss term 0); the
         # uniform draw is shared so every rank takes the same decision
         u = float(np.random.default_rng([self.log.rounds, 7]).random())

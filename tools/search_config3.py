@@ -32,14 +32,13 @@ def main():
     threads = max(1, (os.cpu_count() or 8) // world)
     s = SyncSearch(w.model, w.cluster, eng, kmax=16, beta=0.002, seed=3, threads=threads,
                    dist=dist, rank=rank)
-    # split timing: wrap evaluate
+    # split timing: wrap the batched evaluation
     t_gen = t_gpu = 0.0
-    orig = s.evaluate
 
-    def timed(states):
+    def timed(cuts, kl):
         nonlocal t_gen, t_gpu
         t0 = time.perf_counter()
-        deltas = s.base.deltas([(st.groups, st.ks) for st in states], threads)
+        deltas = s.base.deltas_from_arrays(*s._spec_arrays(cuts, kl), threads=threads)
         t1 = time.perf_counter()
         b = eng.delta_batch(s.resident, deltas)
         b.replay(want_schedule=False)
@@ -47,10 +46,10 @@ def main():
         t2 = time.perf_counter()
         t_gen += t1 - t0
         t_gpu += t2 - t1
-        s.log.evaluated += len(states)
+        s.log.evaluated += len(ms)
         return ms
 
-    s.evaluate = timed
+    s.evaluate_arrays = timed
     s.step(batch)  # warm-up round
     t_gen = t_gpu = 0.0
     t0 = time.perf_counter()
