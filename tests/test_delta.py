@@ -149,3 +149,35 @@ def test_config4_scale_candidates_match_oracle(engine, port):
         a, z = int(b.op_off[i]), int(b.op_off[i + 1])
         assert ms[i] == exp["T"]
         assert np.array_equal(s[a:z], exp["start"]) and np.array_equal(e[a:z], exp["end"])
+
+
+@pytest.mark.gpu
+def test_peak_memory_on_delta_batches(engine, port):
+    """K5 on the schedules of a delta batch (merged in HBM) equals the
+    oracle restatement on the host-merged candidates (memory.cpp:122-167)."""
+    from paper_2205_02473_b200.memory import ModelMeta, batch_peak_memory, resolve
+    from paper_2205_02473_b200.graph import synth_cluster
+    base, specs = _setup("ps", 4, 2, 10, 24, 77)
+    cluster = synth_cluster("ps", 4, 2, 12500.0, 5.0)
+    L = 10
+    meta = ModelMeta({**{f"FW.l{i}": 1000 * (i + 1) for i in range(L)},
+                      **{f"BW.l{i}": 300 * (i + 2) for i in range(L)}},
+                     {f"w{i}": 5000 * i for i in range(4)})
+    graphs = [g.to_global_dfg(cluster) for g in base.candidates(specs)]
+    res = engine.resident(base.graph().csr)
+    b = engine.delta_batch(res, base.deltas(specs))
+    b.replay(want_schedule=True)
+    ms, st, er, s, e = b.results(schedule=True)
+    parts = [resolve(g, meta) for g in graphs]
+    peak = batch_peak_memory(b, np.concatenate([p[1] for p in parts]),
+                             np.concatenate([p[2] for p in parts]),
+                             np.array([len(p[0]) for p in parts], np.int32),
+                             np.concatenate([p[3] for p in parts]))
+    o = 0
+    for i, (g, (nodes, *_)) in enumerate(zip(graphs, parts)):
+        a, z = int(b.op_off[i]), int(b.op_off[i + 1])
+        ops = [(op.id, int(op.kind), op.node) for op in g.ops()]
+        succ = [list(g.succ_indices(k)) for k in range(g.size())]
+        exp = port.port_peak_memory(ops, succ, s[a:z], e[a:z], meta.to_json())
+        assert {nd: int(peak[o + j]) for j, nd in enumerate(nodes)} == exp
+        o += len(nodes)
