@@ -35,6 +35,17 @@ from .ingest import LayeredBase, LayeredModel
 from .replay import sync_makespan_grid
 
 
+def _layers_of_op(op_id: str) -> list[int]:
+    """Layers an op of a layered-model graph belongs to: "w0->BW.l5" -> [5],
+    "SEND.g3+g4#p1#c0#s2#w0#w1" / "w1->IN.g3+g4" -> [3, 4]."""
+    local = op_id.split("->", 1)[1] if "->" in op_id else op_id
+    kind, _, rest = local.partition(".")
+    if kind in ("FW", "BW", "UPDATE", "RFW"):
+        return [int(rest[1:])] if rest.startswith("l") and rest[1:].isdigit() else []
+    unit = rest.split("#", 1)[0]
+    return [int(t[1:]) for t in unit.split("+") if t.startswith("g") and t[1:].isdigit()]
+
+
 def opt_part_num(bytes_: int, kmax: int, t_sync: Callable[[int, int], int]) -> int:
     """optimize.cpp:562-576: argmin_k t_sync(bytes, k), k in [1, min(kmax, bytes)],
     ties -> smallest k."""
@@ -128,10 +139,14 @@ class SyncSearch:
 
     def __init__(self, model: LayeredModel, cluster: ClusterSpec, engine: Engine | None = None,
                  kmax: int = 16, beta: float = 0.01, seed: int = 0, threads: int = 8,
-                 dist=None, rank: int = 0):
+                 dist=None, rank: int = 0, guided: float = 0.0):
         self.model, self.cluster = model, cluster
         self.engine = engine or default_engine()
         self.kmax, self.beta, self.threads = kmax, beta, threads
+        # fraction of proposals that modify a unit on the current critical
+        # path (CandidateSelection, Alg. 1; critical path = K3)
+        self.guided = guided
+        self._critical: np.ndarray | None = None
         self.rng = np.random.default_rng([seed, rank])
         self.dist, self.rank = dist, rank
         L = model.layers
@@ -188,6 +203,33 @@ class SyncSearch:
         return SyncState([list(range(a, b)) for a, b in zip(starts, ends)],
                          [int(kl[a]) for a in starts])
 
+    def critical_layers(self, s: SyncState) -> np.ndarray:
+        """Layers whose compute or synchronization ops lie on the critical
+        path of s (replay with schedule + K3 on the GPU): bool[L]."""
+        spec = [(s.groups, s.ks)]
+        b = self.engine.delta_batch(self.resident, self.base.deltas(spec, 1))
+        b.replay(want_schedule=True)
+        path = b.critical_paths()[0]
+        g = self.base.candidates(spec, 1)[0]
+        crit = np.zeros(self.model.layers, bool)
+        for i in path.tolist():
+            for layer in _layers_of_op(g.op_id(int(i))):
+                if 0 <= layer < len(crit):
+                    crit[layer] = True
+        return crit
+
+    def _pick_units(self, n: int, G: int, starts, sizes, allowed: np.ndarray | None):
+        """A unit index per row: uniform over all units, or (guided rows)
+        over units that contain a critical layer."""
+        gi = self.rng.integers(0, G, n)
+        if allowed is not None and self.guided > 0 and self._critical is not None:
+            crit_units = np.flatnonzero(allowed & np.array(
+                [self._critical[a:a + z].any() for a, z in zip(starts, sizes)]))
+            if len(crit_units):
+                g_rows = self.rng.random(n) < self.guided
+                gi[g_rows] = crit_units[self.rng.integers(0, len(crit_units), int(g_rows.sum()))]
+        return gi
+
     def propose_many(self, s: SyncState, n: int):
         """n neighbours of s at once (same moves and probabilities as
         propose()): (cuts[n, L-1], kl[n, L])."""
@@ -207,19 +249,27 @@ class SyncSearch:
         m2 = ~(m0 | m1)
         r0 = np.flatnonzero(m0)
         if len(r0):  # fuse units j, j+1
-            j = self.rng.integers(0, G - 1, len(r0))
+            ok = np.ones(G, bool)
+            ok[-1] = False
+            j = self._pick_units(len(r0), G, starts, sizes, ok)
+            j = np.minimum(j, G - 2)
             cuts[r0, starts[j + 1] - 1] = False
             kl[r0, starts[j]] = 1
         r1 = np.flatnonzero(m1)
         if len(r1):  # split a multi-layer unit at a random inner point
             gi = multi[self.rng.integers(0, len(multi), len(r1))]
+            if self.guided > 0 and self._critical is not None:
+                ok = np.zeros(G, bool)
+                ok[multi] = True
+                pick = self._pick_units(len(r1), G, starts, sizes, ok)
+                gi = np.where(ok[pick], pick, gi)
             cut = (self.rng.random(len(r1)) * (sizes[gi] - 1)).astype(np.int64) + 1
             cuts[r1, starts[gi] + cut - 1] = True
             kl[r1, starts[gi]] = 1
             kl[r1, starts[gi] + cut] = 1
         r2 = np.flatnonzero(m2)
         if len(r2):  # re-partition a unit, k uniform in [1, min(kmax, bytes)]
-            gi = self.rng.integers(0, G, len(r2))
+            gi = self._pick_units(len(r2), G, starts, sizes, np.ones(G, bool))
             cap = np.minimum(self.kmax, gbytes[gi])
             kl[r2, starts[gi]] = (self.rng.random(len(r2)) * cap).astype(np.int64) + 1
         return cuts, kl
@@ -280,6 +330,8 @@ class SyncSearch:
         if s.makespan < 0:
             s.makespan = int(self.evaluate([s])[0])
             self.best = s.copy()
+        if self.guided > 0 and self._critical is None:
+            self._critical = self.critical_layers(s)
         cuts, kl = self.propose_many(s, batch)
         ms = self.evaluate_arrays(cuts, kl)
         i = int(np.argmin(ms))
@@ -293,6 +345,7 @@ class SyncSearch:
         if u < p:
             self.state = prop
             self.log.accepted += 1
+            self._critical = None  # recomputed for the new state
         if self.state.makespan < self.best.makespan:
             self.best = self.state.copy()
         self.log.rounds += 1

@@ -52,8 +52,9 @@ def _ref_chain(ref, spec, groups, ks):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("scheme,W,S", [("ring", 4, 0), ("ps", 4, 2)])
-def test_search_candidates_match_reference(engine, ref, scheme, W, S):
+@pytest.mark.parametrize("scheme,W,S,guided", [("ring", 4, 0, 0.0), ("ps", 4, 2, 0.0),
+                                               ("ring", 4, 0, 0.8)])
+def test_search_candidates_match_reference(engine, ref, scheme, W, S, guided):
     from paper_2205_02473_b200.graph import synth_cluster
     from paper_2205_02473_b200.ingest import LayeredModel
     L = 6
@@ -64,7 +65,7 @@ def test_search_candidates_match_reference(engine, ref, scheme, W, S):
             "update_dur_us": 5, "scheme": scheme, "workers": W, "ps_count": S,
             "bandwidth_bytes_per_us": 1250.0, "latency_us": 5.0}
     s = SyncSearch(LayeredModel(fw, bw, tb, 5), synth_cluster(scheme, W, S, 1250.0, 5.0),
-                   engine, kmax=8, beta=0.05, seed=3, threads=4)
+                   engine, kmax=8, beta=0.05, seed=3, threads=4, guided=guided)
     for _ in range(6):
         s.step(48)
     assert s.best.makespan <= s.log.history[0] or s.log.rounds == 6
@@ -73,3 +74,21 @@ def test_search_candidates_match_reference(engine, ref, scheme, W, S):
     for c, m in zip(cands, ms):
         T, *_ = _ref_chain(ref, spec, c.groups, c.ks).replay()
         assert T == int(m), (c.groups, c.ks)
+
+
+@pytest.mark.gpu
+def test_critical_layers_follow_the_critical_path(engine):
+    """CandidateSelection input: the layers on K3's critical path of the
+    current state; the path itself is checked against the reference in
+    test_replay_gpu."""
+    from paper_2205_02473_b200.graph import synth_cluster
+    from paper_2205_02473_b200.ingest import LayeredModel
+    from paper_2205_02473_b200.search import _layers_of_op
+    L = 8
+    m = LayeredModel([100] * L, [200] * L, [4_000_000] * (L - 1) + [40_000_000], 5)
+    s = SyncSearch(m, synth_cluster("ring", 4, 0, 1250.0, 5.0), engine, guided=1.0, threads=2)
+    crit = s.critical_layers(s.state)
+    assert crit.dtype == bool and crit.any()
+    # the huge last-layer gradient dominates the tail of the iteration
+    assert crit[L - 1]
+    assert _layers_of_op("RECV.g7#c0#s1#w1#w2") == [7]

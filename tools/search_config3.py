@@ -27,11 +27,11 @@ def main():
     from paper_2205_02473_b200.engine import Engine
     from paper_2205_02473_b200.search import SyncSearch
     from paper_2205_02473_b200.workloads import workload
-    w = workload(3)
+    w = workload(int(os.environ.get("CONFIG", "3")))
     eng = Engine(local)
     threads = max(1, (os.cpu_count() or 8) // world)
     s = SyncSearch(w.model, w.cluster, eng, kmax=16, beta=0.002, seed=3, threads=threads,
-                   dist=dist, rank=rank)
+                   dist=dist, rank=rank, guided=float(os.environ.get("GUIDED", "0")))
     # split timing: wrap the batched evaluation
     t_gen = t_gpu = 0.0
 
