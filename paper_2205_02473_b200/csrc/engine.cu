@@ -668,9 +668,11 @@ std::string check_delta(const dpro_resident& r, const dpro_delta& D, uint32_t& n
   const uint32_t ne = D.new_succ_off[D.n_new];
   if (D.new_succ_off[0] != 0 || !ascending(D.new_succ_off, D.n_new + 1, false) || (ne && !D.new_succ))
     return "bad new_succ_off";
-  auto removed = [&](uint32_t b) {
-    return std::binary_search(D.removed, D.removed + D.n_removed, b);
-  };
+  // removed-op bitmap (thread-local, reused across candidates)
+  thread_local std::vector<uint64_t> bits;
+  bits.assign((nb >> 6) + 1, 0);
+  for (uint32_t k = 0; k < D.n_removed; ++k) bits[D.removed[k] >> 6] |= 1ull << (D.removed[k] & 63);
+  auto removed = [&](uint32_t b) { return (bits[b >> 6] >> (b & 63)) & 1ull; };
   dur32 = r.dur32;
   for (uint32_t j = 0; j < D.n_new; ++j) {
     if (D.new_dev[j] >= D.n_devices) return "new_dev out of range";
@@ -693,7 +695,7 @@ std::string check_delta(const dpro_resident& r, const dpro_delta& D, uint32_t& n
     lost += r.succ_off[u + 1] - r.succ_off[u];  // out-edges of u
     lost += r.indeg[u];                          // in-edges of u ...
     for (uint32_t e = r.succ_off[u]; e < r.succ_off[u + 1]; ++e)
-      lost -= removed(r.succ[e]);                // ... counted once
+      lost -= static_cast<uint64_t>(removed(r.succ[e]));  // ... counted once
   }
   if (!ascending(D.cut, D.n_cut, true)) return "cut must be ascending";
   for (uint32_t k = 0; k < D.n_cut; ++k) {
