@@ -185,6 +185,8 @@ struct dpro_ctx {
   HostPinned staging;
   std::unique_ptr<Pool> pool;  // created on first use
   int pack_clusters = 0;       // co-resident pack clusters (queried once)
+  cudaStream_t copy_stream = nullptr;  // H2D of delta chunks (overlaps the merges)
+  std::vector<cudaEvent_t> chunk_ev;   // one per in-flight chunk copy
   Pool& workers() {
     if (!pool) pool = std::make_unique<Pool>();
     return *pool;
@@ -594,6 +596,11 @@ void dpro_cuda_destroy(dpro_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  if (ctx->copy_stream) {
+    cudaStreamSynchronize(ctx->copy_stream);
+    cudaStreamDestroy(ctx->copy_stream);
+  }
+  for (cudaEvent_t ev : ctx->chunk_ev) cudaEventDestroy(ev);
   delete ctx->spare;
   delete ctx;
 }
@@ -753,6 +760,9 @@ int build_delta_batch(dpro_ctx* ctx, dpro_batch* b, const dpro_resident* r,
     max_n = std::max(max_n, h.n);
   }
   CU(cudaStreamSynchronize(ctx->stream));  // staging may feed an earlier copy
+  if (!ctx->copy_stream)
+    CU(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+  CU(cudaStreamSynchronize(ctx->copy_stream));
   CU(b->dblob.ensure(boff[n] + 16));
   CU(ctx->staging.ensure(boff[n] + 16));
   CU(b->arena.ensure(aoff[n] + 16));
@@ -831,19 +841,28 @@ int build_delta_batch(dpro_ctx* ctx, dpro_batch* b, const dpro_resident* r,
     const int32_t c0 = i, c1 = chunk_end[k];
     bool ok = err == DPRO_OK;
     for (int32_t j = c0; j < c1 && ok; ++j) ok = errs[j].empty();
-    if (ok) {  // this chunk: deltas, descriptors, merge -- while the pool stages the next
+    if (ok) {  // this chunk: copies on the copy stream, merge on the compute
+               // stream after them -- while the pool stages the next chunk and
+               // the copy stream uploads it
       const size_t a0 = boff[c0], z0 = boff[c1];
+      cudaStream_t cs = ctx->copy_stream;
       cudaError_t e = cudaSuccess;
-      if (z0 > a0)
+      while (ctx->chunk_ev.size() <= size_t(k) && e == cudaSuccess) {
+        cudaEvent_t ev;
+        e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+        if (e == cudaSuccess) ctx->chunk_ev.push_back(ev);
+      }
+      if (e == cudaSuccess && z0 > a0)
         e = cudaMemcpyAsync(b->dblob.as<char>(a0), stage + a0, z0 - a0, cudaMemcpyHostToDevice,
-                            ctx->stream);
+                            cs);
       if (e == cudaSuccess)
         e = cudaMemcpyAsync(b->ddesc.as<dpro_k::DeltaDev>() + c0, dd.data() + c0,
-                            sizeof(dpro_k::DeltaDev) * (c1 - c0), cudaMemcpyHostToDevice,
-                            ctx->stream);
+                            sizeof(dpro_k::DeltaDev) * (c1 - c0), cudaMemcpyHostToDevice, cs);
       if (e == cudaSuccess)
         e = cudaMemcpyAsync(b->desc.as<Cand>() + c0, b->hc.data() + c0,
-                            sizeof(Cand) * (c1 - c0), cudaMemcpyHostToDevice, ctx->stream);
+                            sizeof(Cand) * (c1 - c0), cudaMemcpyHostToDevice, cs);
+      if (e == cudaSuccess) e = cudaEventRecord(ctx->chunk_ev[k], cs);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->stream, ctx->chunk_ev[k], 0);
       if (e != cudaSuccess) err = set_err(ctx, DPRO_ECUDA, cudaGetErrorString(e));
       if (err == DPRO_OK) err = run_merge(ctx, b, c0, c1);
     }
