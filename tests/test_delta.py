@@ -36,8 +36,11 @@ def merge_host(bc, nb, d):
     dev[fn] = _arr(d.new_dev, np.uint16, d.n_new)
     fl[fn] = _arr(d.new_flags, np.uint8, d.n_new)
     succ = [[] for _ in range(n)]
+    cut = set(_arr(d.cut, np.uint32, d.n_cut).tolist())
     for x in np.flatnonzero(keep):
-        succ[fb[x]] += [int(fb[s]) for s in bc.succ[bc.succ_off[x]:bc.succ_off[x + 1]] if keep[s]]
+        a = int(bc.succ_off[x])
+        succ[fb[x]] += [int(fb[s]) for k, s in enumerate(bc.succ[a:int(bc.succ_off[x + 1])])
+                        if keep[s] and a + k not in cut]
     nso = _arr(d.new_succ_off, np.uint32, d.n_new + 1)
     ns = _arr(d.new_succ, np.uint32, int(nso[-1]))
     for k in range(d.n_new):
@@ -181,3 +184,85 @@ def test_peak_memory_on_delta_batches(engine, port):
         exp = port.port_peak_memory(ops, succ, s[a:z], e[a:z], meta.to_json())
         assert {nd: int(peak[o + j]) for j, nd in enumerate(nodes)} == exp
         o += len(nodes)
+
+
+def _rewrite_pairs(seed: int, count: int):
+    """(base, candidate) GlobalDFG pairs from the reference-pinned rewrites:
+    recompute (drops edges between kept ops: cut), grad-accum (replaces
+    every FW/BW op), op fusion / tensor fusion / partition on layered
+    graphs."""
+    from dags import rewrite_dag, strategy_chain
+    from paper_2205_02473_b200.graph import synth_cluster as sc
+    from paper_2205_02473_b200.ingest import layered_global_dfg
+    from paper_2205_02473_b200.memory import ModelMeta
+    from paper_2205_02473_b200.rewrite import (apply_op_fusion, apply_tensor_fusion,
+                                               apply_tensor_partition, grad_accum_candidate,
+                                               recompute_candidate)
+    from paper_2205_02473_b200 import Error
+    rng = np.random.default_rng(seed)
+    pairs = []
+    while len(pairs) < count:
+        g = rewrite_dag(rng)
+        for c in (recompute_candidate(g), grad_accum_candidate(g, ModelMeta())):
+            if c is not None:
+                pairs.append((g, c[0]))
+        L = int(rng.integers(3, 7))
+        m = LayeredModel(rng.integers(10, 400, L).tolist(), rng.integers(10, 800, L).tolist(),
+                         rng.integers(1000, 4_000_000, L).tolist(), 5)
+        lg = layered_global_dfg(m, sc("ring", 3, 0, 12500.0, 5.0))
+        cg = lg
+        for kind, a, b, k in strategy_chain(rng, lg, 4):
+            try:
+                cg = (apply_op_fusion(cg, a, b) if kind == 0 else
+                      apply_tensor_fusion(cg, a, b) if kind == 1 else
+                      apply_tensor_partition(cg, a, k))
+            except Error:
+                pass
+        pairs.append((lg, cg))
+    return pairs[:count]
+
+
+def test_make_delta_merges_to_the_candidate():
+    from paper_2205_02473_b200.delta import DeltaList, make_delta
+    from paper_2205_02473_b200.engine import Csr
+    pairs = _rewrite_pairs(3, 40)
+    n_cut = 0
+    for base, cand in pairs:
+        dl = DeltaList([make_delta(base, cand)])  # owns the arrays d points into
+        d = dl[0]
+        n_cut += d.n_cut
+        bc = Csr.from_dict(base.to_csr())
+        dur, dev, fl, succ = merge_host(bc, base.size(), d)
+        cc = cand.to_csr()
+        assert np.array_equal(dur, cc["dur"]) and np.array_equal(fl, cc["flags"])
+        bdevs = base.devices()
+        extra = [dv for dv in cc["devices"] if dv not in bdevs]
+        allv = bdevs + extra
+        assert [allv[int(x)] for x in dev] == [cc["devices"][int(x)] for x in cc["dev"]]
+        for k in range(cand.size()):
+            assert succ[k] == sorted(cand.succ_indices(k)), k
+    assert n_cut > 0  # the cut path is exercised
+
+
+@pytest.mark.gpu
+def test_gpu_replay_of_generic_deltas(engine):
+    """Rewritten GlobalDFGs evaluated as deltas of their base (cut edges,
+    removed/changed ops, new devices) replay exactly like the candidates."""
+    from paper_2205_02473_b200 import replay_many
+    from paper_2205_02473_b200.delta import DeltaList, make_delta
+    from paper_2205_02473_b200.engine import Csr
+    pairs = _rewrite_pairs(9, 30)
+    by_base = {}
+    for base, cand in pairs:
+        by_base.setdefault(id(base), (base, []))[1].append(cand)
+    for base, cands in by_base.values():
+        res = engine.resident(Csr.from_dict(base.to_csr()))
+        b = engine.delta_batch(res, DeltaList([make_delta(base, c) for c in cands]))
+        b.replay(want_schedule=True)
+        ms, st, er, s, e = b.results(schedule=True)
+        for i, r in enumerate(replay_many(cands)):
+            a, z = int(b.op_off[i]), int(b.op_off[i + 1])
+            assert st[i] == 0 and ms[i] == r.iteration_time_us
+            ids = [o.id for o in cands[i].ops()]
+            assert s[a:z].tolist() == [r.schedule[x].start for x in ids]
+            assert e[a:z].tolist() == [r.schedule[x].end for x in ids]
