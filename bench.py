@@ -347,7 +347,9 @@ def run_ours(args) -> None:
                 "full_csr": {"value": world * B / full_s,
                              "h2d_bytes_per_step": int(sum(_packed_bytes(g) for g in graphs)),
                              "note": "dpro_cuda_replay_batch with every candidate's host CSR"}},
-        "gpu_launches": 3 * args.steps,
+        # per step: delta_merge_kernel, pack_kernel, replay_fast_kernel pass 0 +
+        # deep-ring pass 1 (profiles/r01_delta_launches.csv)
+        "gpu_launches": 4 * args.steps,
         "clocks": clocks,
     }
     print(json.dumps(line))
