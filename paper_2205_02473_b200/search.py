@@ -356,3 +356,114 @@ class SyncSearch:
         for _ in range(rounds):
             self.step(batch)
         return self.best
+
+
+class StrategySearch:
+    """Batched MCMC over the reference's full strategy space on a GlobalDFG
+    (BASELINE config 4's op fusion + recomputation + gradient accumulation,
+    plus tensor fusion and partition): every round applies `batch` random
+    strategies to the current graph with the reference-exact rewrites
+    (rewrite.py), turns each result into a delta of the current graph
+    (delta.make_delta) and evaluates them all in ONE GPU batch against the
+    current graph resident in HBM; acceptance as SyncSearch. Host rewrites
+    cost O(V + E) Python per candidate, so this path suits graphs of up to
+    ~10^4 ops; layered models at scale use SyncSearch's native deltas."""
+
+    def __init__(self, g, engine: Engine | None = None, meta=None, cost=None, kmax: int = 8,
+                 beta: float = 0.01, seed: int = 0, kinds=(0, 1, 2, 3, 4)):
+        from .rewrite import CostModel
+        from .memory import ModelMeta
+        self.engine = engine or default_engine()
+        self.meta = meta or ModelMeta()
+        self.cost = cost or CostModel()
+        self.kmax, self.beta, self.kinds = kmax, beta, tuple(kinds)
+        self.rng = np.random.default_rng(seed)
+        self.g = g
+        self.makespan = -1
+        self.applied: list = []
+        self.best = (g, -1, [])
+        self.log = SearchLog()
+        self._resident = None
+
+    def _random_strategy(self, g):
+        from .rewrite import Strategy, StrategyKind
+        kind = StrategyKind(int(self.rng.choice(self.kinds)))
+        if kind == StrategyKind.OP_FUSION:
+            comp = [o.id for o in g.ops() if int(o.kind) in (0, 1)]
+            if not comp:
+                return None
+            a = comp[int(self.rng.integers(0, len(comp)))]
+            succ = [s for s in g.succs(a) if int(g.op(s).kind) in (0, 1)]
+            if not succ:
+                return None
+            return Strategy(kind, a, succ[int(self.rng.integers(0, len(succ)))])
+        bases = sorted({u.base for u in g.tensor_units().values()})
+        if kind == StrategyKind.TENSOR_FUSION:
+            if len(bases) < 2:
+                return None
+            i = int(self.rng.integers(0, len(bases) - 1))
+            return Strategy(kind, bases[i], bases[i + 1])
+        if kind == StrategyKind.PARTITION:
+            if not bases:
+                return None
+            return Strategy(kind, bases[int(self.rng.integers(0, len(bases)))], "",
+                            int(self.rng.integers(1, self.kmax + 1)))
+        return Strategy(kind)  # recompute / grad-accum
+
+    def propose(self, n: int):
+        """Up to n (strategy, graph) candidates (rewrites that raise the
+        reference's errors are dropped)."""
+        from .errors import Error
+        from .rewrite import apply_strategy
+        out = []
+        for _ in range(n * 3):
+            if len(out) == n:
+                break
+            st = self._random_strategy(self.g)
+            if st is None:
+                continue
+            try:
+                out.append((st, apply_strategy(self.g, st, self.cost, self.meta)))
+            except Error:
+                continue
+        return out
+
+    def evaluate(self, graphs) -> np.ndarray:
+        from .delta import DeltaList, make_delta
+        from .engine import Csr
+        if self._resident is None:
+            self._resident = self.engine.resident(Csr.from_dict(self.g.to_csr()))
+        b = self.engine.delta_batch(self._resident,
+                                    DeltaList([make_delta(self.g, c) for c in graphs]))
+        b.replay(want_schedule=False)
+        ms, st, *_ = b.results()
+        if np.any(st != 0):
+            raise RuntimeError(f"replay failed for {int((st != 0).sum())} candidates")
+        self.log.evaluated += len(graphs)
+        return ms
+
+    def step(self, batch: int) -> SearchLog:
+        from .replay import replay
+        if self.makespan < 0:
+            self.makespan = replay(self.g).iteration_time_us
+            self.best = (self.g, self.makespan, [])
+        cands = self.propose(batch)
+        if cands:
+            ms = self.evaluate([c[1] for c in cands])
+            i = int(np.argmin(ms))
+            u = float(np.random.default_rng([self.log.rounds, 11]).random())
+            if u < min(1.0, math.exp(self.beta * (self.makespan - int(ms[i])))):
+                self.g, self.makespan = cands[i][1], int(ms[i])
+                self.applied = self.applied + [cands[i][0]]
+                self._resident = None  # the next round's base is the new graph
+                self.log.accepted += 1
+                if self.makespan < self.best[1]:
+                    self.best = (self.g, self.makespan, list(self.applied))
+        self.log.rounds += 1
+        self.log.history.append(self.makespan)
+        return self.log
+
+    def run(self, rounds: int, batch: int):
+        for _ in range(rounds):
+            self.step(batch)
+        return self.best

@@ -92,3 +92,47 @@ def test_critical_layers_follow_the_critical_path(engine):
     # the huge last-layer gradient dominates the tail of the iteration
     assert crit[L - 1]
     assert _layers_of_op("RECV.g7#c0#s1#w1#w2") == [7]
+
+
+@pytest.mark.gpu
+def test_strategy_search_all_kinds_match_reference(engine, ref):
+    """StrategySearch (op fusion, tensor fusion, partition, recompute,
+    grad-accum on a GlobalDFG; candidates evaluated as deltas on the GPU):
+    every evaluated makespan equals the reference replay of the same
+    rewrite applied by the reference."""
+    from golden.make_golden import ref_rows  # noqa: F401
+    from paper_2205_02473_b200.graph import synth_cluster
+    from paper_2205_02473_b200.ingest import LayeredModel, layered_global_dfg
+    from paper_2205_02473_b200.memory import ModelMeta
+    from paper_2205_02473_b200.rewrite import StrategyKind
+    from paper_2205_02473_b200.search import StrategySearch
+    L = 5
+    rng = np.random.default_rng(21)
+    spec = {"layers": L, "fw_dur_us": rng.integers(50, 400, L).tolist(),
+            "bw_dur_us": rng.integers(80, 900, L).tolist(),
+            "tensor_bytes": rng.integers(10_000, 3_000_000, L).tolist(),
+            "update_dur_us": 5, "scheme": "ring", "workers": 3, "ps_count": 0,
+            "bandwidth_bytes_per_us": 1250.0, "latency_us": 5.0}
+    g0 = layered_global_dfg(LayeredModel(spec["fw_dur_us"], spec["bw_dur_us"],
+                                         spec["tensor_bytes"], 5),
+                            synth_cluster("ring", 3, 0, 1250.0, 5.0))
+    s = StrategySearch(g0, engine, meta=ModelMeta(microbatch_scale=0.5), seed=4, beta=0.05)
+    for _ in range(3):
+        s.step(12)
+    cands = s.propose(16)
+    kinds = {int(st.kind) for st, _ in cands}
+    ms = s.evaluate([c for _, c in cands])
+    # the same strategies applied by the reference to the same current graph
+    rg = ref.RefGraph.synth(spec)
+    for st in s.applied:
+        rg = (rg.op_fusion(st.a, st.b) if st.kind == StrategyKind.OP_FUSION else
+              rg.tensor_fusion(st.a, st.b) if st.kind == StrategyKind.TENSOR_FUSION else
+              rg.partition(st.a, st.k) if st.kind == StrategyKind.PARTITION else
+              rg.apply_memory_strategy(int(st.kind), {"microbatch_scale": 0.5}))
+    for (st, _), m in zip(cands, ms):
+        r = (rg.op_fusion(st.a, st.b) if st.kind == StrategyKind.OP_FUSION else
+             rg.tensor_fusion(st.a, st.b) if st.kind == StrategyKind.TENSOR_FUSION else
+             rg.partition(st.a, st.k) if st.kind == StrategyKind.PARTITION else
+             rg.apply_memory_strategy(int(st.kind), {"microbatch_scale": 0.5}))
+        assert r.replay()[0] == int(m), st
+    assert len(kinds) >= 3
