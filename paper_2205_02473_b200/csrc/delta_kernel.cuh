@@ -90,7 +90,7 @@ __device__ __forceinline__ bool is_cut(const DeltaDev& D, uint32_t e) {
 __global__ void __launch_bounds__(kMergeThreads, 1)
     delta_merge_kernel(ResDev B, const DeltaDev* __restrict__ deltas, const Cand* __restrict__ cands,
                        int n_cands, uint32_t* __restrict__ rank_scratch, uint32_t smem_ind,
-                       uint32_t* __restrict__ pred1) {
+                       uint32_t* __restrict__ pred1, uint32_t rank_smem) {
   using Scan = cub::BlockScan<uint32_t, kMergeThreads>;
   __shared__ typename Scan::TempStorage scan_tmp;
   __shared__ uint32_t s_carry;
@@ -99,7 +99,9 @@ __global__ void __launch_bounds__(kMergeThreads, 1)
   for (int cid = blockIdx.x; cid < n_cands; cid += gridDim.x) {
     const DeltaDev D = deltas[cid];
     const Cand C = cands[cid];
-    uint32_t* bits = rank_scratch + D.rank_off;
+    // rank structures in shared memory after the in-degree counters when
+    // they fit (rank_smem), else in this candidate's global scratch
+    uint32_t* bits = rank_smem ? s_ind + smem_ind : rank_scratch + D.rank_off;
     uint32_t* rpre = bits + W;
     uint32_t* qpre = rpre + W;
     // ---- rank structures
@@ -116,10 +118,18 @@ __global__ void __launch_bounds__(kMergeThreads, 1)
     __syncthreads();
     const Ranks R{bits, rpre, qpre, D.new_pos, D.n_removed, D.n_new, nb};
     // final index of every base op (removed ones: UINT32_MAX)
-    uint32_t* fmap = qpre + W + 1;
-    for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x)
-      fmap[b] = R.removed(b) ? UINT32_MAX : R.f(b);
-    __syncthreads();
+    // final index of base op b (UINT32_MAX: removed): from the shared-memory
+    // ranks directly, or through a map in global scratch when they are global
+    uint32_t* fmap = rank_scratch + D.rank_off + 3 * W + 1;
+    if (!rank_smem) {
+      for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x)
+        fmap[b] = R.removed(b) ? UINT32_MAX : R.f(b);
+      __syncthreads();
+    }
+    auto fm = [&](uint32_t b) -> uint32_t {
+      if (!rank_smem) return fmap[b];
+      return R.removed(b) ? UINT32_MAX : R.f(b);
+    };
     uint32_t* ind_g = const_cast<uint32_t*>(C.indeg);
     const bool ind_smem = C.n <= smem_ind;
     uint32_t* ind = ind_smem ? s_ind : ind_g;
@@ -131,7 +141,7 @@ __global__ void __launch_bounds__(kMergeThreads, 1)
     uint8_t* flags = const_cast<uint8_t*>(C.flags);
     // ---- per-op fields and out-degrees (written at off[f + 1])
     for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) {
-      const uint32_t f = fmap[b];
+      const uint32_t f = fm(b);
       if (f == UINT32_MAX) continue;
       const long long d = B.dur64 ? __ldg(static_cast<const long long*>(B.dur) + b)
                                   : (long long)__ldg(static_cast<const int*>(B.dur) + b);
@@ -142,7 +152,7 @@ __global__ void __launch_bounds__(kMergeThreads, 1)
       uint32_t deg = 0;
       const uint32_t e1 = __ldg(B.succ_off + b + 1);
       for (uint32_t e = __ldg(B.succ_off + b); e < e1; ++e)
-        deg += fmap[__ldg(B.succ + e)] != UINT32_MAX && !is_cut(D, e);
+        deg += !R.removed(__ldg(B.succ + e)) && !is_cut(D, e);
       if (D.n_extra) {
         const uint32_t x0 = lower_bound_u32(D.extra_src, D.n_extra, b);
         uint32_t x1 = x0;
@@ -180,7 +190,7 @@ __global__ void __launch_bounds__(kMergeThreads, 1)
     }
     // ---- successor lists
     for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) {
-      const uint32_t fb = fmap[b];
+      const uint32_t fb = fm(b);
       if (fb == UINT32_MAX) continue;
       uint32_t o = off[fb];
       uint32_t e = __ldg(B.succ_off + b);
@@ -195,7 +205,7 @@ __global__ void __launch_bounds__(kMergeThreads, 1)
       auto advance = [&]() {
         nxt = UINT32_MAX;
         for (; e < e1; ++e) {
-          const uint32_t m = fmap[__ldg(B.succ + e)];
+          const uint32_t m = fm(__ldg(B.succ + e));
           if (m != UINT32_MAX && !is_cut(D, e)) {
             nxt = m;
             ++e;

@@ -894,13 +894,19 @@ int build_delta_batch(dpro_ctx* ctx, dpro_batch* b, const dpro_resident* r,
 // K0 for candidates [c0, c1) (descriptors already on the device).
 int run_merge(dpro_ctx* ctx, dpro_batch* b, int32_t c0, int32_t c1) {
   if (c1 <= c0) return DPRO_OK;
-  const size_t smem = size_t(b->smem_ind) * 4;
+  // rank structures (3W+1 words) in shared memory next to the in-degree
+  // counters when both fit
+  const uint32_t W = (b->res->n >> 5) + 1;
+  const size_t rank_bytes = (3 * size_t(W) + 1) * 4;
+  const size_t limit = ctx->smem_optin - 8192;  // static smem + slack
+  const uint32_t rank_smem = size_t(b->smem_ind) * 4 + rank_bytes <= limit ? 1u : 0u;
+  const size_t smem = size_t(b->smem_ind) * 4 + (rank_smem ? rank_bytes : 0);
   CU(cudaFuncSetAttribute(dpro_k::delta_merge_kernel,
                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dpro_k::delta_merge_kernel<<<std::min<int>(c1 - c0, ctx->sm_count), dpro_k::kMergeThreads,
                                smem, ctx->stream>>>(
       b->res->dev, b->ddesc.as<dpro_k::DeltaDev>() + c0, b->desc.as<Cand>() + c0, c1 - c0,
-      b->rank.as<uint32_t>(), b->smem_ind, b->pred1.as<uint32_t>());
+      b->rank.as<uint32_t>(), b->smem_ind, b->pred1.as<uint32_t>(), rank_smem);
   CU(cudaGetLastError());
   return DPRO_OK;
 }
