@@ -322,6 +322,25 @@ void dpro_delta_set_free(dpro_delta_set* s);
 /* The base graph itself (owned by the base; CSR via dpro_graph_csr). */
 const dpro_graph* dpro_base_graph(const dpro_base* base);
 
+/* The layered graph with a memory rewrite applied while generating it:
+ * variant 1 = recompute_candidate, 2 = grad_accum_candidate with
+ * microbatch_scale (optimize.cpp:819-959), 0 = none. Same graph as the
+ * rewrite applied to dpro_graph_layered's output, at generator speed. */
+dpro_graph* dpro_graph_layered_variant(const dpro_layered_model* model,
+                                       const dpro_cluster_desc* cluster,
+                                       const int32_t* part_k, int32_t variant,
+                                       double microbatch_scale, int32_t* status);
+/* Inputs of dpro_cuda_batch_peak_memory for one generated graph, resolved
+ * natively (memory.cpp:71-157): op_bytes[i] = output_bytes_for(meta, op)
+ * over the (keys, bytes) table for computation ops (UPDATE without an entry
+ * -> 0; other ops 0), op_node[i] = dense compute node (-1 for other ops).
+ * *n_nodes = compute nodes, named by dpro_graph_memory_node in name order.
+ * DPRO_EINVAL with *missing_op = the first computation op without bytes
+ * (MissingMetaError). */
+int dpro_graph_memory_inputs(dpro_graph* g, int32_t n_entries, const char* const* keys,
+                             const int64_t* bytes, int64_t* op_bytes, int32_t* op_node,
+                             int32_t* n_nodes, uint32_t* missing_op);
+const char* dpro_graph_memory_node(const dpro_graph* g, int32_t i);
 /* n graphs with part_k[n*layers], built on `threads` host threads. */
 int dpro_graph_layered_batch(const dpro_layered_model* model,
                              const dpro_cluster_desc* cluster,

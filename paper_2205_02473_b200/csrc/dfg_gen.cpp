@@ -240,6 +240,7 @@ struct dpro_graph {
   std::vector<uint8_t> flags;
   std::vector<uint32_t> succ_off, succ, indeg;
   std::vector<std::string> device_strs;
+  std::vector<std::string> mem_nodes;  // dpro_graph_memory_inputs: compute nodes, name order
 };
 
 namespace {
@@ -356,9 +357,19 @@ struct Record {
   std::vector<std::pair<uint32_t, uint32_t>> comm;  // [group] creation range
 };
 
+// Memory rewrites applied while generating (optimize.cpp:819-959 on the
+// synth/ingest graph): 1 = recompute (sqrt(L) checkpoint segments per worker,
+// RFW.l<i> re-runs feeding the backward ops), 2 = grad-accum (two
+// micro-batches FW/BW.l<i>@mb0/@mb1 with round_us(dur * scale)).
+struct MemVariant {
+  int kind = 0;
+  double scale = 0.5;
+};
+
 dpro_graph* build_layered(const dpro_layered_model& m, const Cluster& c, const Groups& G,
                           Record* rec = nullptr, std::vector<uint32_t>* rank_out = nullptr,
-                          std::vector<std::array<int, 3>>* devs_out = nullptr) {
+                          std::vector<std::array<int, 3>>* devs_out = nullptr,
+                          MemVariant var = {}) {
   Gen g;
   g.names = &c.nodes;
   const int L = m.layers;
@@ -391,10 +402,44 @@ dpro_graph* build_layered(const dpro_layered_model& m, const Cluster& c, const G
   // per group: IN/OUT creation index per node
   std::vector<std::vector<uint32_t>> in_op(NG, std::vector<uint32_t>(N, UINT32_MAX));
   std::vector<std::vector<uint32_t>> out_op(NG, std::vector<uint32_t>(N, UINT32_MAX));
+  if (var.kind == 1 && L < 2)
+    throw std::runtime_error("re-computation does not apply to this graph");
   for (int w : workers) {
     const std::string& node = c.nodes[w];
     const uint32_t dv = g.device(0, w, -1);
     std::vector<uint32_t> fw(L), bw(L), up(L);
+    if (var.kind == 2) {  // grad-accum: micro-batch copies of every FW/BW op
+      std::vector<uint32_t> fw0(L), fw1(L), bw0(L), bw1(L);
+      auto mb = [&](int64_t d) { return round_half_even(static_cast<double>(d) * var.scale); };
+      for (int i = 0; i < L; ++i) {
+        const std::string li = std::to_string(i);
+        fw0[i] = g.add(node + "->FW.l" + li + "@mb0", kFw, dv, mb(m.fw_dur[i]));
+        fw1[i] = g.add(node + "->FW.l" + li + "@mb1", kFw, dv, mb(m.fw_dur[i]));
+        bw0[i] = g.add(node + "->BW.l" + li + "@mb0", kBw, dv, mb(m.bw_dur[i]));
+        bw1[i] = g.add(node + "->BW.l" + li + "@mb1", kBw, dv, mb(m.bw_dur[i]));
+        up[i] = g.add(node + "->UPDATE.l" + li, kUpdate, dv, m.update_dur);
+      }
+      for (int q = 0; q < NG; ++q) {
+        in_op[q][w] = g.add(node + "->IN." + gname[q], kVin, dv, 0);
+        out_op[q][w] = g.add(node + "->OUT." + gname[q], kVout, dv, 0);
+      }
+      for (int i = 0; i < L; ++i) {  // optimize.cpp:913-928 edge rules
+        if (i > 0) {
+          g.edge(fw0[i - 1], fw0[i]);
+          g.edge(fw1[i - 1], fw1[i]);
+        }
+        if (i + 1 < L) {
+          g.edge(bw0[i + 1], bw0[i]);
+          g.edge(bw1[i + 1], bw1[i]);
+        }
+        g.edge(fw0[i], bw0[i]);
+        g.edge(fw1[i], bw1[i]);
+        g.edge(bw1[i], in_op[group_of[i]][w]);   // duplicated -> plain: from @mb1
+        g.edge(out_op[group_of[i]][w], up[i]);
+      }
+      g.edge(bw0[0], fw1[0]);  // second micro-batch after the first's backward
+      continue;
+    }
     for (int i = 0; i < L; ++i) {
       const std::string li = std::to_string(i);
       fw[i] = g.add(node + "->FW.l" + li, kFw, dv, m.fw_dur[i]);
@@ -411,10 +456,35 @@ dpro_graph* build_layered(const dpro_layered_model& m, const Cluster& c, const G
       out_op[q][w] = g.add(node + "->OUT." + gname[q], kVout, dv, 0);
     }
     // synth.cpp:200-212 deps, resolved by build_local_dfg (ingest.cpp:243-265)
+    std::vector<uint8_t> fw_to_bw(L, 1);
+    if (var.kind == 1) {  // recompute, optimize.cpp:831-870
+      const int cseg = static_cast<int>(std::ceil(std::sqrt(static_cast<double>(L))));
+      const int seg_base = L / cseg, seg_rem = L % cseg;
+      int lo = 0, prev_cp = -1;
+      for (int sgi = 0; sgi < cseg; ++sgi) {
+        const int len = seg_base + (sgi < seg_rem ? 1 : 0);
+        const int cp = lo + len - 1;
+        uint32_t prev_rfw = UINT32_MAX;
+        for (int i = lo; i < cp; ++i) {
+          const uint32_t rfw = g.add(node + "->RFW.l" + std::to_string(i), kFw, dv, m.fw_dur[i]);
+          fw_to_bw[i] = 0;  // FW.l_i -> BW.l_i becomes RFW.l_i -> BW.l_i
+          g.edge(rfw, bw[i]);
+          if (prev_rfw == UINT32_MAX) {
+            if (prev_cp >= 0) g.edge(fw[prev_cp], rfw);
+            g.edge(bw[cp], rfw);  // gate: the checkpoint's backward
+          } else {
+            g.edge(prev_rfw, rfw);
+          }
+          prev_rfw = rfw;
+        }
+        prev_cp = cp;
+        lo += len;
+      }
+    }
     for (int i = 0; i < L; ++i) {
       if (i > 0) g.edge(fw[i - 1], fw[i]);
       if (i + 1 < L) g.edge(bw[i + 1], bw[i]);
-      g.edge(fw[i], bw[i]);
+      if (fw_to_bw[i]) g.edge(fw[i], bw[i]);
       g.edge(bw[i], in_op[group_of[i]][w]);   // producer feeds IN (ingest.cpp:242)
       g.edge(out_op[group_of[i]][w], up[i]);  // OUT(g_i) -> UPDATE.l_i
     }
@@ -910,6 +980,24 @@ dpro_graph* dpro_graph_layered(const dpro_layered_model* model,
                  status);
 }
 
+dpro_graph* dpro_graph_layered_variant(const dpro_layered_model* model,
+                                       const dpro_cluster_desc* cluster,
+                                       const int32_t* part_k, int32_t variant,
+                                       double microbatch_scale, int32_t* status) {
+  return guarded(
+      [&] {
+        if (variant < 0 || variant > 2) throw std::invalid_argument("unknown variant");
+        Groups G;
+        for (int i = 0; i < model->layers; ++i) {
+          G.members.push_back({i});
+          G.k.push_back(part_k ? part_k[i] : 1);
+        }
+        return build_layered(*model, Cluster(*cluster), G, nullptr, nullptr, nullptr,
+                             MemVariant{variant, microbatch_scale});
+      },
+      status);
+}
+
 int dpro_graph_layered_batch(const dpro_layered_model* model,
                              const dpro_cluster_desc* cluster,
                              const int32_t* part_k, int32_t n, int32_t threads,
@@ -1157,6 +1245,98 @@ const char* dpro_delta_set_device_str(const dpro_delta_set* s, int32_t cand, uin
 }
 void dpro_delta_set_free(dpro_delta_set* s) { delete s; }
 const dpro_graph* dpro_base_graph(const dpro_base* base) { return base->b->g.get(); }
+
+// memory.cpp:71-119 output_bytes_for over a (key -> bytes) table.
+namespace {
+int64_t local_output_bytes(const std::unordered_map<std::string, int64_t>& t, std::string local) {
+  auto lookup = [&](const std::string& k) -> int64_t {
+    const auto it = t.find(k);
+    return it == t.end() ? -1 : it->second;
+  };
+  int64_t v = lookup(local);
+  if (v >= 0) return v;
+  const auto at = local.rfind("@mb");
+  if (at != std::string::npos) {
+    local = local.substr(0, at);
+    v = lookup(local);
+    if (v >= 0) return (v + 1) / 2;
+  }
+  if (local.rfind("RFW.", 0) == 0) return lookup("FW." + local.substr(4));
+  return -1;
+}
+
+int64_t output_bytes_for(const std::unordered_map<std::string, int64_t>& t, const std::string& id) {
+  const auto d = t.find(id);
+  if (d != t.end()) return d->second;
+  std::string local = id;
+  const auto arrow = local.find("->");
+  if (arrow != std::string::npos) local = local.substr(arrow + 2);
+  const int64_t v = local_output_bytes(t, local);
+  if (v >= 0) return v;
+  if (local.find('+') == std::string::npos) return -1;
+  int64_t total = 0;
+  size_t pos = 0;
+  for (;;) {
+    const auto next = local.find('+', pos);
+    const int64_t pb = local_output_bytes(
+        t, next == std::string::npos ? local.substr(pos) : local.substr(pos, next - pos));
+    if (pb < 0) return -1;
+    total += pb;
+    if (next == std::string::npos) return total;
+    pos = next + 1;
+  }
+}
+}  // namespace
+
+int dpro_graph_memory_inputs(dpro_graph* g, int32_t n_entries, const char* const* keys,
+                             const int64_t* bytes, int64_t* op_bytes, int32_t* op_node,
+                             int32_t* n_nodes, uint32_t* missing_op) {
+  if (!g || (n_entries > 0 && (!keys || !bytes)) || !op_bytes || !op_node || !n_nodes)
+    return DPRO_EINVAL;
+  std::unordered_map<std::string, int64_t> table;
+  table.reserve(size_t(n_entries) * 2);
+  for (int32_t k = 0; k < n_entries; ++k) table[keys[k]] = bytes[k];
+  const uint32_t n = static_cast<uint32_t>(g->kind.size());
+  // compute nodes (the device of a computation op is its node), name order
+  std::vector<int32_t> node_of_dev(g->device_strs.size(), -1);
+  std::vector<uint8_t> used(g->device_strs.size(), 0);
+  for (uint32_t i = 0; i < n; ++i)
+    if (g->kind[i] == kFw || g->kind[i] == kBw || g->kind[i] == kUpdate) used[g->dev[i]] = 1;
+  std::vector<std::pair<std::string, uint32_t>> nodes;
+  for (size_t d = 0; d < used.size(); ++d)
+    if (used[d]) nodes.emplace_back(g->device_strs[d], static_cast<uint32_t>(d));
+  std::sort(nodes.begin(), nodes.end());
+  g->mem_nodes.clear();
+  for (size_t k = 0; k < nodes.size(); ++k) {
+    node_of_dev[nodes[k].second] = static_cast<int32_t>(k);
+    g->mem_nodes.push_back(nodes[k].first);
+  }
+  *n_nodes = static_cast<int32_t>(nodes.size());
+  if (missing_op) *missing_op = UINT32_MAX;
+  for (uint32_t i = 0; i < n; ++i) {
+    const int32_t k = g->kind[i];
+    if (k != kFw && k != kBw && k != kUpdate) {
+      op_bytes[i] = 0;
+      op_node[i] = -1;
+      continue;
+    }
+    op_node[i] = node_of_dev[g->dev[i]];
+    int64_t b = output_bytes_for(table, dpro_graph_op_id(g, i));
+    if (b < 0) {
+      if (k != kUpdate) {  // MissingMetaError("no output bytes for op <id>")
+        if (missing_op) *missing_op = i;
+        return DPRO_EINVAL;
+      }
+      b = 0;
+    }
+    op_bytes[i] = b;
+  }
+  return DPRO_OK;
+}
+
+const char* dpro_graph_memory_node(const dpro_graph* g, int32_t i) {
+  return g->mem_nodes.at(i).c_str();
+}
 
 int32_t dpro_graph_op_kind(const dpro_graph* g, uint32_t i) { return g->kind.at(i); }
 const char* dpro_graph_device_str(const dpro_graph* g, uint32_t d) {

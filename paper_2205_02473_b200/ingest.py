@@ -252,6 +252,22 @@ def layered_graph(model: LayeredModel, cluster: ClusterSpec,
     return NativeGraph(h)
 
 
+def layered_graph_variant(model: LayeredModel, cluster: ClusterSpec, variant: str,
+                          microbatch_scale: float = 0.5,
+                          part_k: Sequence[int] | None = None) -> NativeGraph:
+    """The layered graph with "recompute" or "grad-accum" applied while
+    generating it (dpro_graph_layered_variant) -- the graph
+    rewrite.apply_recompute / apply_grad_accum produce, at native speed."""
+    m = model.struct()
+    holder = N.ClusterDescHolder(cluster)
+    pk = None if part_k is None else np.ascontiguousarray(part_k, np.int32)
+    st = C.c_int32(0)
+    v = {"none": 0, "recompute": 1, "grad-accum": 2}[variant]
+    h = N.lib.dpro_graph_layered_variant(C.byref(m), C.byref(holder.desc), N.ptr(pk), v,
+                                         float(microbatch_scale), C.byref(st))
+    return NativeGraph(h)
+
+
 def layered_graph_groups(model: LayeredModel, cluster: ClusterSpec,
                          groups: Sequence[Sequence[int]],
                          ks: Sequence[int] | None = None) -> NativeGraph:

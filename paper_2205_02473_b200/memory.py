@@ -14,6 +14,7 @@ HBM (csrc/memory_kernel.cuh). No CPU fallback.
 """
 from __future__ import annotations
 
+import ctypes as C
 import json
 from dataclasses import dataclass, field
 from typing import Sequence
@@ -135,6 +136,30 @@ def resolve(g: GlobalDFG, meta: ModelMeta):
             raise MissingMetaError(f"no persistent bytes for node {nd}")
         pers[i] = meta.persistent_bytes[nd]
     return nodes, op_bytes, op_node, pers
+
+
+def native_inputs(graph, meta: ModelMeta):
+    """resolve() for a generated graph (ingest.NativeGraph), natively:
+    (nodes, op_bytes, op_node, persistent) for batch_peak_memory."""
+    keys = list(meta.output_bytes)
+    karr = (C.c_char_p * max(1, len(keys)))(*[k.encode() for k in keys])
+    barr = np.ascontiguousarray([meta.output_bytes[k] for k in keys], np.int64)
+    n = graph.n_ops
+    op_bytes = np.zeros(max(1, n), np.int64)
+    op_node = np.zeros(max(1, n), np.int32)
+    nn, miss = C.c_int32(0), C.c_uint32(0)
+    rc = N.lib.dpro_graph_memory_inputs(graph.handle, len(keys), karr, N.ptr(barr),
+                                        N.ptr(op_bytes), N.ptr(op_node), C.byref(nn),
+                                        C.byref(miss))
+    if rc != N.DPRO_OK:
+        raise MissingMetaError(f"no output bytes for op {graph.op_id(miss.value)}")
+    nodes = [N.lib.dpro_graph_memory_node(graph.handle, i).decode() for i in range(nn.value)]
+    pers = np.zeros(len(nodes), np.int64)
+    for i, nd in enumerate(nodes):
+        if nd not in meta.persistent_bytes:
+            raise MissingMetaError(f"no persistent bytes for node {nd}")
+        pers[i] = meta.persistent_bytes[nd]
+    return nodes, op_bytes[:n], op_node[:n], pers
 
 
 def batch_peak_memory(batch: Batch, op_bytes: np.ndarray, op_node: np.ndarray,

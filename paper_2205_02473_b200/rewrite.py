@@ -27,6 +27,8 @@ import re
 from collections import deque
 from dataclasses import dataclass, field
 
+import numpy as np
+
 from .errors import (CycleError, Error, IoError, LookupError_, SchemaError, SpliceError,
                      TransformError)
 from .graph import (DeviceId, GlobalDFG, GraphBuilder, Op, OpKind, TensorUnit, is_communication,
@@ -538,3 +540,64 @@ def memory_pass(g: GlobalDFG, budget_bytes: int, meta: ModelMeta,
     if applied is not None:
         applied.append(cands[best][1])
     return cands[best][0]
+
+
+def memory_pass_layered(model, cluster, budget_bytes: int, meta: ModelMeta, engine=None,
+                        part_k=None):
+    """memory_pass (optimize.cpp:972-1021) for a layered model at generator
+    speed: the base graph and its recompute / grad-accum variants are
+    generated natively (dpro_graph_layered_variant), replayed in ONE batch
+    and their peaks computed by ONE K5 launch from natively resolved
+    inputs. Returns (strategy or None, NativeGraph, max peak, makespan) with
+    memory_pass's choice and BudgetError; usable at config-4/5 scale."""
+    from .engine import default_engine
+    from .ingest import layered_graph_variant
+    from .memory import batch_peak_memory, native_inputs
+    eng = engine or default_engine()
+    names = ["none", "recompute", "grad-accum"]
+
+    def gen(v):  # the native generator releases the GIL: build all three at once
+        try:
+            return layered_graph_variant(model, cluster, v, meta.microbatch_scale, part_k)
+        except Error:
+            return None  # the rewrite does not apply (e.g. one layer)
+
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(3) as ex:
+        graphs = list(ex.map(gen, names))
+    live = [g for g in graphs if g is not None]
+    b = eng.batch([g.csr for g in live])
+    b.replay(want_schedule=True)
+    ms, st, *_ = b.results()
+    if np.any(st != 0):
+        raise Error(f"replay failed: statuses {st.tolist()}")
+    parts = [native_inputs(g, meta) for g in live]
+    peak = batch_peak_memory(b, np.concatenate([p[1] for p in parts]),
+                             np.concatenate([p[2] for p in parts]),
+                             np.array([len(p[0]) for p in parts], np.int32),
+                             np.concatenate([p[3] for p in parts]))
+    maxes, o = [], 0
+    for p in parts:
+        maxes.append(int(peak[o:o + len(p[0])].max()) if len(p[0]) else 0)
+        o += len(p[0])
+    res = {}
+    k = 0
+    for v, g in zip(names, graphs):
+        if g is not None:
+            res[v] = (g, maxes[k], int(ms[k]))
+            k += 1
+    base_g, base_peak, base_t = res["none"]
+    if budget_bytes <= 0 or base_peak <= budget_bytes:
+        return None, base_g, base_peak, base_t
+    best = None
+    for v in names[1:]:
+        if v in res and res[v][1] <= budget_bytes and (best is None or res[v][2] < res[best][2]):
+            best = v
+    if best is None:
+        reached = min([base_peak] + [res[v][1] for v in names[1:] if v in res])
+        raise BudgetError(f"peak memory {base_peak} bytes exceeds budget {budget_bytes} "
+                          "bytes and no rewrite closes the gap", reached)
+    kind = StrategyKind.RECOMPUTE if best == "recompute" else StrategyKind.GRAD_ACCUM
+    k = int(math.ceil(math.sqrt(model.layers))) if best == "recompute" else 2
+    g, pk, t = res[best]
+    return Strategy(kind, "", "", k, -1), g, pk, t

@@ -199,3 +199,86 @@ def test_rewritten_graphs_replay_like_reference(engine, ref):
         order = sorted(r.schedule)
         assert [r.schedule[i].start for i in order] == s.tolist()
         assert [r.schedule[i].end for i in order] == e.tolist()
+
+
+@pytest.mark.parametrize("scheme,W,S,L", [("ring", 3, 0, 1), ("ring", 4, 0, 7), ("ps", 3, 2, 10),
+                                          ("ring", 2, 0, 16)])
+def test_native_memory_variants_match_rewrites(scheme, W, S, L):
+    """dpro_graph_layered_variant == apply_recompute / apply_grad_accum on
+    the same layered graph (those are pinned to the reference above)."""
+    from paper_2205_02473_b200.ingest import layered_graph_variant
+    rng = np.random.default_rng(L)
+    c = synth_cluster(scheme, W, S, 12500.0, 5.0)
+    m = LayeredModel(rng.integers(10, 400, L).tolist(), rng.integers(11, 801, L).tolist(),
+                     rng.integers(1000, 4_000_000, L).tolist(), 5)
+    k = rng.choice([1, 2, 3], L).tolist()
+    g = layered_global_dfg(m, c, k)
+    for var, fn in (("recompute", lambda: apply_recompute(g)),
+                    ("grad-accum", lambda: apply_grad_accum(g, ModelMeta(microbatch_scale=0.37)))):
+        try:
+            exp = fn()
+        except TransformError as e:
+            with pytest.raises(Exception, match=str(e)):
+                layered_graph_variant(m, c, var, 0.37, k)
+            continue
+        ng = layered_graph_variant(m, c, var, 0.37, k)
+        a = exp.to_csr()
+        assert [o.id for o in exp.ops()] == ng.op_ids()
+        for f in ("dur", "dev", "flags", "succ_off", "succ", "indeg"):
+            assert np.array_equal(a[f], getattr(ng.csr, f)), (var, f)
+
+
+def test_native_memory_inputs_match_resolve():
+    from paper_2205_02473_b200 import MissingMetaError
+    from paper_2205_02473_b200.ingest import layered_graph_variant
+    from paper_2205_02473_b200.memory import native_inputs, resolve
+    L = 6
+    c = synth_cluster("ps", 3, 2, 12500.0, 5.0)
+    m = LayeredModel([100] * L, [200] * L, [1000 * (i + 1) for i in range(L)], 5)
+    meta = ModelMeta({**{f"FW.l{i}": 10 * (i + 1) for i in range(L)},
+                      **{f"BW.l{i}": 7 * (i + 1) for i in range(L)}},
+                     {f"w{i}": 1000 for i in range(3)})
+    for var in ("none", "recompute", "grad-accum"):
+        ng = layered_graph_variant(m, c, var, 0.5)
+        a, b = native_inputs(ng, meta), resolve(ng.to_global_dfg(c), meta)
+        assert a[0] == b[0]
+        for x, y in zip(a[1:], b[1:]):
+            assert np.array_equal(x, y), var
+    bad = ModelMeta({"FW.l0": 1}, {f"w{i}": 1 for i in range(3)})
+    ng = layered_graph_variant(m, c, "none", 0.5)
+    with pytest.raises(MissingMetaError) as e1:
+        native_inputs(ng, bad)
+    with pytest.raises(MissingMetaError) as e2:
+        resolve(ng.to_global_dfg(c), bad)
+    assert str(e1.value) == str(e2.value)
+
+
+@pytest.mark.gpu
+def test_memory_pass_layered_matches_memory_pass(engine):
+    """memory_pass_layered (native graphs, one batch, one K5 launch) makes
+    the same choice as memory_pass on the GlobalDFG for a range of budgets."""
+    from paper_2205_02473_b200.rewrite import memory_pass_layered
+    rng = np.random.default_rng(8)
+    L = 9
+    c = synth_cluster("ring", 4, 0, 12500.0, 5.0)
+    m = LayeredModel(rng.integers(100, 400, L).tolist(), rng.integers(100, 800, L).tolist(),
+                     rng.integers(1000, 4_000_000, L).tolist(), 5)
+    act = rng.integers(1, 1 << 26, L).tolist()
+    meta = ModelMeta({**{f"FW.l{i}": act[i] for i in range(L)},
+                      **{f"BW.l{i}": int(m.tensor_bytes[i]) for i in range(L)}},
+                     {f"w{i}": int(sum(m.tensor_bytes)) for i in range(4)}, 0.5)
+    g = layered_global_dfg(m, c)
+    _, base_g, base_peak, _ = memory_pass_layered(m, c, 0, meta, engine)
+    for budget in (0, base_peak, base_peak - 1, base_peak // 2, 1):
+        try:
+            applied = []
+            out = memory_pass(g, budget, meta, applied)
+            exp = ("ok", [int(a.kind) for a in applied], [o.id for o in out.ops()])
+        except BudgetError as e:
+            exp = ("budget", str(e), e.best_peak_bytes)
+        try:
+            st, ng, _, _ = memory_pass_layered(m, c, budget, meta, engine)
+            got = ("ok", [] if st is None else [int(st.kind)], ng.op_ids())
+        except BudgetError as e:
+            got = ("budget", str(e), e.best_peak_bytes)
+        assert got == exp, budget
