@@ -314,6 +314,23 @@ int dpro_base_delta_batch(const dpro_base* base, int32_t n,
                           const int32_t* group_off, const int32_t* members,
                           const int32_t* group_k, int32_t threads,
                           dpro_delta_set** out);
+/* The same with op fusion on every worker (optimize.cpp:245-317, applied
+ * left to right with the default cost model, ratio 0.8): fw_join[c*(L-1)+i]
+ * fuses FW.l<i> with FW.l<i+1>, bw_join[c*(L-1)+i] fuses BW.l<i+1> with
+ * BW.l<i> in candidate c (NULL: none). Fused ids are the reference's
+ * ("w0->FW.l3+FW.l4", "w0->BW.l4+BW.l3"). */
+int dpro_base_delta_batch_ops(const dpro_base* base, int32_t n,
+                              const int32_t* n_groups, const int64_t* spec_off,
+                              const int32_t* group_off, const int32_t* members,
+                              const int32_t* group_k, const uint8_t* fw_join,
+                              const uint8_t* bw_join, int32_t threads,
+                              dpro_delta_set** out);
+int dpro_graph_from_base_batch_ops(const dpro_base* base, int32_t n,
+                                   const int32_t* n_groups, const int64_t* spec_off,
+                                   const int32_t* group_off, const int32_t* members,
+                                   const int32_t* group_k, const uint8_t* fw_join,
+                                   const uint8_t* bw_join, int32_t threads,
+                                   dpro_graph** out);
 const dpro_delta* dpro_delta_set_deltas(const dpro_delta_set* s);  /* [size] */
 int32_t dpro_delta_set_size(const dpro_delta_set* s);
 const char* dpro_delta_set_device_str(const dpro_delta_set* s, int32_t cand,

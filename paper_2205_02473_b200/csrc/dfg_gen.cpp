@@ -347,6 +347,10 @@ dpro_graph* finalize(Gen& g, std::vector<uint32_t>* rank_out = nullptr,
 struct Groups {
   std::vector<std::vector<int>> members;
   std::vector<int> k;
+  // op fusion on every worker (optimize.cpp:245-317, applied left to right
+  // with the default cost model): fw_join[i] fuses FW.l<i> with FW.l<i+1>,
+  // bw_join[i] fuses BW.l<i+1> with BW.l<i>; empty = none
+  std::vector<uint8_t> fw_join, bw_join;
 };
 
 // Creation indices of the structural ops of a layered build (for delta
@@ -676,6 +680,67 @@ void prepare_delta(const BaseData& B, const Groups& G, DeltaParts& P) {
   g.names = &B.c.nodes;
   std::vector<uint8_t>& removed = P.removed;
   removed.assign(nb, 0);
+  // op fusion: refs of every worker's FW / BW op of each layer (a fused run
+  // is one new op; kBaseRef | base index otherwise)
+  const bool opf = !G.fw_join.empty() || !G.bw_join.empty();
+  if (opf && ((!G.fw_join.empty() && G.fw_join.size() != size_t(L - 1)) ||
+              (!G.bw_join.empty() && G.bw_join.size() != size_t(L - 1))))
+    throw std::runtime_error("op fusion joins need layers - 1 entries");
+  auto fwj = [&](int i) { return !G.fw_join.empty() && G.fw_join[i]; };
+  auto bwj = [&](int i) { return !G.bw_join.empty() && G.bw_join[i]; };
+  auto fused_dur = [](int64_t a, int64_t b) {  // CostModel{} fallback 0.8 (optimize.cpp:84-103)
+    return round_half_even(0.8 * (static_cast<double>(a) + static_cast<double>(b)));
+  };
+  std::vector<std::vector<uint32_t>> xr(B.N), yr(B.N);
+  for (int w : B.workers) {
+    xr[w].resize(L);
+    yr[w].resize(L);
+    for (int i = 0; i < L; ++i) {
+      xr[w][i] = kBaseRef | B.fw[w][i];
+      yr[w][i] = kBaseRef | B.bw[w][i];
+    }
+    if (!opf) continue;
+    const std::string& node = B.c.nodes[w];
+    const uint32_t dv = g.device(0, w, -1);
+    for (int a = 0; a < L;) {  // FW runs, fused left to right
+      int b = a;
+      while (b + 1 < L && fwj(b)) ++b;
+      if (b > a) {
+        std::string id = node + "->FW.l" + std::to_string(a);
+        int64_t d = B.fw_dur[a];
+        for (int j = a + 1; j <= b; ++j) {
+          id += "+FW.l" + std::to_string(j);
+          d = fused_dur(d, B.fw_dur[j]);
+        }
+        const uint32_t x = g.add(std::move(id), kFw, dv, d);
+        for (int j = a; j <= b; ++j) {
+          removed[B.fw[w][j]] = 1;
+          xr[w][j] = x;
+        }
+      }
+      a = b + 1;
+    }
+    for (int top = L - 1; top >= 0;) {  // BW runs, fused from the top layer down
+      int lo = top;
+      while (lo - 1 >= 0 && bwj(lo - 1)) --lo;
+      if (lo < top) {
+        std::string id = node + "->BW.l" + std::to_string(top);
+        int64_t d = B.bw_dur[top];
+        for (int j = top - 1; j >= lo; --j) {
+          id += "+BW.l" + std::to_string(j);
+          d = fused_dur(d, B.bw_dur[j]);
+        }
+        const uint32_t y = g.add(std::move(id), kBw, dv, d);
+        for (int j = lo; j <= top; ++j) {
+          removed[B.bw[w][j]] = 1;
+          yr[w][j] = y;
+        }
+      }
+      top = lo - 1;
+    }
+  }
+  // IN op of every (group, worker): the base one or the tensor-fused one
+  std::vector<std::vector<uint32_t>> in_of(NG, std::vector<uint32_t>(B.N, UINT32_MAX));
   for (int q = 0; q < NG; ++q) {
     const auto& mem = G.members[q];
     const int k = G.k[q];
@@ -702,7 +767,7 @@ void prepare_delta(const BaseData& B, const Groups& G, DeltaParts& P) {
         in_ref[w] = g.add(B.c.nodes[w] + "->IN." + gname[q], kVin, dv, 0);
         out_ref[w] = g.add(B.c.nodes[w] + "->OUT." + gname[q], kVout, dv, 0);
         for (int i : mem) {
-          g.edge(kBaseRef | B.bw[w][i], in_ref[w]);   // every producer feeds IN
+          g.edge(yr[w][i], in_ref[w]);                // every producer feeds IN
           g.edge(out_ref[w], kBaseRef | B.up[w][i]);  // OUT feeds every consumer
         }
       }
@@ -717,6 +782,25 @@ void prepare_delta(const BaseData& B, const Groups& G, DeltaParts& P) {
       const std::string unit = k == 1 ? gname[q] : gname[q] + "#p" + std::to_string(p);
       expand_unit(g, B.c, unit, base + (p < rem ? 1 : 0), &in_ref, &out_ref);
     }
+    if (fused)
+      for (int w : B.workers) in_of[q][w] = in_ref[w];
+  }
+  // op-fusion edges with a new endpoint (edges between kept base ops exist;
+  // those into removed ops vanish); duplicates are dropped when emitting
+  if (opf) {
+    auto is_new = [](uint32_t r) { return !(r & kBaseRef); };
+    auto add = [&](uint32_t a, uint32_t b) {
+      if (a != b && (is_new(a) || is_new(b))) g.edge(a, b);
+    };
+    for (int w : B.workers)
+      for (int i = 0; i < L; ++i) {
+        if (i > 0) add(xr[w][i - 1], xr[w][i]);
+        if (i + 1 < L) add(yr[w][i + 1], yr[w][i]);
+        add(xr[w][i], yr[w][i]);
+        const int q = group_of[i];
+        const uint32_t in = in_of[q][w] != UINT32_MAX ? in_of[q][w] : (kBaseRef | B.in[i][w]);
+        add(yr[w][i], in);
+      }
   }
   const uint32_t nn = static_cast<uint32_t>(g.ops.size());
   // sort the new ops, then place each among the base ids (binary search)
@@ -1130,12 +1214,14 @@ dpro_base* dpro_base_layered(const dpro_layered_model* model,
 
 void dpro_base_free(dpro_base* b) { delete b; }
 
-int dpro_graph_from_base_batch(const dpro_base* base, int32_t n, const int32_t* n_groups,
-                               const int64_t* spec_off, const int32_t* group_off,
-                               const int32_t* members, const int32_t* group_k,
-                               int32_t threads, dpro_graph** out) {
+int dpro_graph_from_base_batch_ops(const dpro_base* base, int32_t n, const int32_t* n_groups,
+                                   const int64_t* spec_off, const int32_t* group_off,
+                                   const int32_t* members, const int32_t* group_k,
+                                   const uint8_t* fw_join, const uint8_t* bw_join,
+                                   int32_t threads, dpro_graph** out) {
   if (!base) return DPRO_EINVAL;
   if (threads < 1) threads = 1;
+  const int L = base->b->L;
   std::vector<int32_t> st(n, DPRO_OK);
   std::vector<std::string> errs(threads);
   std::atomic<int32_t> next{0};
@@ -1148,6 +1234,8 @@ int dpro_graph_from_base_batch(const dpro_base* base, int32_t n, const int32_t* 
           G.members.emplace_back(members + group_off[g0 + q], members + group_off[g0 + q + 1]);
           G.k.push_back(group_k ? group_k[g0 + q] : 1);
         }
+        if (fw_join && L > 1) G.fw_join.assign(fw_join + size_t(i) * (L - 1), fw_join + size_t(i + 1) * (L - 1));
+        if (bw_join && L > 1) G.bw_join.assign(bw_join + size_t(i) * (L - 1), bw_join + size_t(i + 1) * (L - 1));
         out[i] = build_delta(base->b, G);
       } catch (const std::exception& e) {
         out[i] = nullptr;
@@ -1168,16 +1256,26 @@ int dpro_graph_from_base_batch(const dpro_base* base, int32_t n, const int32_t* 
     }
   return DPRO_OK;
 }
+
+int dpro_graph_from_base_batch(const dpro_base* base, int32_t n, const int32_t* n_groups,
+                               const int64_t* spec_off, const int32_t* group_off,
+                               const int32_t* members, const int32_t* group_k,
+                               int32_t threads, dpro_graph** out) {
+  return dpro_graph_from_base_batch_ops(base, n, n_groups, spec_off, group_off, members, group_k,
+                                        nullptr, nullptr, threads, out);
+}
 struct dpro_delta_set {
   std::shared_ptr<BaseData> base;
   std::vector<DeltaHost> d;
   std::vector<dpro_delta> views;
 };
 
-int dpro_base_delta_batch(const dpro_base* base, int32_t n, const int32_t* n_groups,
-                          const int64_t* spec_off, const int32_t* group_off,
-                          const int32_t* members, const int32_t* group_k, int32_t threads,
-                          dpro_delta_set** out) {
+int dpro_base_delta_batch_ops(const dpro_base* base, int32_t n, const int32_t* n_groups,
+                              const int64_t* spec_off, const int32_t* group_off,
+                              const int32_t* members, const int32_t* group_k,
+                              const uint8_t* fw_join, const uint8_t* bw_join, int32_t threads,
+                              dpro_delta_set** out) {
+  const int L = base ? base->b->L : 0;
   if (!base || !out || n < 0) return DPRO_EINVAL;
   *out = nullptr;
   if (threads < 1) threads = 1;
@@ -1196,6 +1294,8 @@ int dpro_base_delta_batch(const dpro_base* base, int32_t n, const int32_t* n_gro
           G.members.emplace_back(members + group_off[g0 + q], members + group_off[g0 + q + 1]);
           G.k.push_back(group_k ? group_k[g0 + q] : 1);
         }
+        if (fw_join && L > 1) G.fw_join.assign(fw_join + size_t(i) * (L - 1), fw_join + size_t(i + 1) * (L - 1));
+        if (bw_join && L > 1) G.bw_join.assign(bw_join + size_t(i) * (L - 1), bw_join + size_t(i + 1) * (L - 1));
         emit_delta(*base->b, G, set->d[i]);
       } catch (const std::exception& e) {
         st[i] = DPRO_EINVAL;
@@ -1234,6 +1334,14 @@ int dpro_base_delta_batch(const dpro_base* base, int32_t n, const int32_t* n_gro
   }
   *out = set.release();
   return DPRO_OK;
+}
+
+int dpro_base_delta_batch(const dpro_base* base, int32_t n, const int32_t* n_groups,
+                          const int64_t* spec_off, const int32_t* group_off,
+                          const int32_t* members, const int32_t* group_k, int32_t threads,
+                          dpro_delta_set** out) {
+  return dpro_base_delta_batch_ops(base, n, n_groups, spec_off, group_off, members, group_k,
+                                   nullptr, nullptr, threads, out);
 }
 
 const dpro_delta* dpro_delta_set_deltas(const dpro_delta_set* s) { return s->views.data(); }

@@ -316,6 +316,7 @@ class LayeredBase:
 
     def __init__(self, model: LayeredModel, cluster: ClusterSpec):
         self._m = model.struct()
+        self._layers = model.layers
         self._holder = N.ClusterDescHolder(cluster)
         st = C.c_int32(0)
         self.handle = N.lib.dpro_base_layered(C.byref(self._m), C.byref(self._holder.desc),
@@ -341,38 +342,51 @@ class LayeredBase:
         ks = np.ascontiguousarray([k for _, kk in specs for k in kk], np.int32)
         return n_groups, spec_off, group_off, members, ks
 
+    def _joins(self, n, fw_join, bw_join):
+        L = self._layers
+        conv = lambda j: None if j is None else np.ascontiguousarray(  # noqa: E731
+            np.asarray(j, np.uint8).reshape(n, max(L - 1, 0)))
+        return conv(fw_join), conv(bw_join)
+
     def candidates(self, specs: Sequence[tuple[Sequence[Sequence[int]], Sequence[int]]],
-                   threads: int = 8) -> list[NativeGraph]:
-        """[(groups, ks), ...] -> graphs by delta construction (merged on the host)."""
+                   threads: int = 8, fw_join=None, bw_join=None) -> list[NativeGraph]:
+        """[(groups, ks), ...] -> graphs by delta construction (merged on the
+        host); fw_join / bw_join [n, L-1]: op fusion of adjacent FW / BW ops
+        on every worker (dpro_graph_from_base_batch_ops)."""
         n = len(specs)
         n_groups, spec_off, group_off, members, ks = self._spec_arrays(specs)
+        fj, bj = self._joins(n, fw_join, bw_join)
         out = (C.c_void_p * n)()
-        rc = N.lib.dpro_graph_from_base_batch(self.handle, n, N.ptr(n_groups), N.ptr(spec_off),
-                                              N.ptr(group_off), N.ptr(members), N.ptr(ks),
-                                              threads, out)
+        rc = N.lib.dpro_graph_from_base_batch_ops(self.handle, n, N.ptr(n_groups),
+                                                  N.ptr(spec_off), N.ptr(group_off),
+                                                  N.ptr(members), N.ptr(ks), N.ptr(fj), N.ptr(bj),
+                                                  threads, out)
         if rc != N.DPRO_OK:
             raise Error(N.lib.dpro_graph_last_error().decode())
         return [NativeGraph(out[i]) for i in range(n)]
 
 
     def deltas(self, specs: Sequence[tuple[Sequence[Sequence[int]], Sequence[int]]],
-               threads: int = 8) -> "DeltaSet":
-        """[(groups, ks), ...] -> unmerged deltas for Engine.delta_batch."""
-        return self.deltas_from_arrays(*self._spec_arrays(specs), threads=threads)
+               threads: int = 8, fw_join=None, bw_join=None) -> "DeltaSet":
+        """[(groups, ks), ...] -> unmerged deltas for Engine.delta_batch
+        (fw_join / bw_join as in candidates())."""
+        return self.deltas_from_arrays(*self._spec_arrays(specs), threads=threads,
+                                       fw_join=fw_join, bw_join=bw_join)
 
     def deltas_from_arrays(self, n_groups, spec_off, group_off, members, ks,
-                           threads: int = 8) -> "DeltaSet":
+                           threads: int = 8, fw_join=None, bw_join=None) -> "DeltaSet":
         """Same, from the flattened spec arrays of dpro_base_delta_batch."""
         n = len(n_groups)
+        fj, bj = self._joins(n, fw_join, bw_join)
         n_groups = np.ascontiguousarray(n_groups, np.int32)
         spec_off = np.ascontiguousarray(spec_off, np.int64)
         group_off = np.ascontiguousarray(group_off, np.int32)
         members = np.ascontiguousarray(members, np.int32)
         ks = np.ascontiguousarray(ks, np.int32)
         out = C.c_void_p()
-        rc = N.lib.dpro_base_delta_batch(self.handle, n, N.ptr(n_groups), N.ptr(spec_off),
-                                         N.ptr(group_off), N.ptr(members), N.ptr(ks), threads,
-                                         C.byref(out))
+        rc = N.lib.dpro_base_delta_batch_ops(self.handle, n, N.ptr(n_groups), N.ptr(spec_off),
+                                             N.ptr(group_off), N.ptr(members), N.ptr(ks),
+                                             N.ptr(fj), N.ptr(bj), threads, C.byref(out))
         if rc != N.DPRO_OK:
             raise Error(N.lib.dpro_graph_last_error().decode())
         return DeltaSet(out.value, self)

@@ -266,3 +266,97 @@ def test_gpu_replay_of_generic_deltas(engine):
             ids = [o.id for o in cands[i].ops()]
             assert s[a:z].tolist() == [r.schedule[x].start for x in ids]
             assert e[a:z].tolist() == [r.schedule[x].end for x in ids]
+
+
+def _op_fusion_chain(g, workers, L, fj, bj):
+    """The reference's sequential op fusions for fw/bw joins (left to right
+    on FW chains, top-down on BW chains) via rewrite.apply_op_fusion."""
+    from paper_2205_02473_b200.rewrite import apply_op_fusion
+    for w in sorted(workers):
+        a = 0
+        while a < L:
+            b = a
+            while b + 1 < L and fj[b]:
+                b += 1
+            cur = f"{w}->FW.l{a}"
+            for j in range(a + 1, b + 1):
+                g = apply_op_fusion(g, cur, f"{w}->FW.l{j}")
+                cur += f"+FW.l{j}"
+            a = b + 1
+        top = L - 1
+        while top >= 0:
+            lo = top
+            while lo - 1 >= 0 and bj[lo - 1]:
+                lo -= 1
+            cur = f"{w}->BW.l{top}"
+            for j in range(top - 1, lo - 1, -1):
+                g = apply_op_fusion(g, cur, f"{w}->BW.l{j}")
+                cur += f"+BW.l{j}"
+            top = lo - 1
+    return g
+
+
+@pytest.mark.parametrize("scheme,W,S,L", [("ring", 3, 0, 6), ("ps", 3, 2, 7), ("ring", 4, 0, 9)])
+def test_native_op_fusion_candidates_match_rewrite_chain(scheme, W, S, L):
+    """dpro_graph_from_base_batch_ops / dpro_base_delta_batch_ops with op
+    fusion (+ tensor fusion + partition) == the reference-pinned rewrite
+    chain (apply_tensor_fusion / apply_tensor_partition / apply_op_fusion)."""
+    from paper_2205_02473_b200.graph import synth_cluster as sc
+    from paper_2205_02473_b200.ingest import layered_global_dfg
+    from paper_2205_02473_b200.rewrite import apply_tensor_fusion, apply_tensor_partition
+    rng = np.random.default_rng(L * 7 + W)
+    c = sc(scheme, W, S, 12500.0, 5.0)
+    m = LayeredModel(rng.integers(10, 400, L).tolist(), rng.integers(11, 801, L).tolist(),
+                     rng.integers(1000, 4_000_000, L).tolist(), 5)
+    base = LayeredBase(m, c)
+    bv = base.graph()
+    workers = [n.id for n in c.nodes if n.role == "worker"]
+    specs, fjs, bjs, exps = [], [], [], []
+    for t in range(6):
+        fj = (rng.random(L - 1) < 0.4).astype(np.uint8)
+        bj = (rng.random(L - 1) < 0.4).astype(np.uint8)
+        cut = int(rng.integers(1, L - 1))
+        groups = [list(range(0, cut + 1))] + [[i] for i in range(cut + 1, L)] if t % 2 else \
+            [[i] for i in range(L)]
+        ks = [int(rng.integers(1, 4)) for _ in groups]
+        g = layered_global_dfg(m, c)
+        if len(groups[0]) > 1:
+            name = "g0"
+            for i in groups[0][1:]:
+                g = apply_tensor_fusion(g, name, f"g{i}")
+                name += f"+g{i}"
+        for grp, k in zip(groups, ks):
+            g = apply_tensor_partition(g, "+".join(f"g{i}" for i in grp), k)
+        exps.append(_op_fusion_chain(g, workers, L, fj, bj))
+        specs.append((groups, ks))
+        fjs.append(fj)
+        bjs.append(bj)
+    full = base.candidates(specs, fw_join=fjs, bw_join=bjs)
+    ds = base.deltas(specs, fw_join=fjs, bw_join=bjs)
+    for i, (ng, g) in enumerate(zip(full, exps)):
+        a = g.to_csr()
+        assert [o.id for o in g.ops()] == ng.op_ids(), i
+        for f in ("dur", "dev", "flags", "succ_off", "succ", "indeg"):
+            assert np.array_equal(a[f], getattr(ng.csr, f)), (i, f)
+        dur, dev, fl, succ = merge_host(bv.csr, bv.n_ops, ds[i])  # the delta form too
+        assert np.array_equal(dur, ng.csr.dur) and np.array_equal(fl, ng.csr.flags)
+        for k in range(ng.n_ops):
+            assert succ[k] == ng.csr.succ[ng.csr.succ_off[k]:ng.csr.succ_off[k + 1]].tolist()
+
+
+@pytest.mark.gpu
+def test_gpu_op_fusion_deltas_replay_like_full(engine):
+    base, specs = _setup("ring", 8, 0, 24, 64, 5)
+    rng = np.random.default_rng(1)
+    fj = (rng.random((64, 23)) < 0.3).astype(np.uint8)
+    bj = (rng.random((64, 23)) < 0.3).astype(np.uint8)
+    full = base.candidates(specs, fw_join=fj, bw_join=bj)
+    fb = engine.batch([g.csr for g in full])
+    fb.replay(want_schedule=True)
+    ms0, st0, _, s0, e0 = fb.results(schedule=True)
+    res = engine.resident(base.graph().csr)
+    db = engine.delta_batch(res, base.deltas(specs, fw_join=fj, bw_join=bj))
+    db.replay(want_schedule=True)
+    ms1, st1, _, s1, e1 = db.results(schedule=True)
+    assert np.all(st0 == 0) and np.array_equal(ms0, ms1)
+    assert np.array_equal(s0, s1) and np.array_equal(e0, e1)
