@@ -71,9 +71,18 @@ struct DevBuf {
     if (bytes <= cap) return cudaSuccess;
     if (p) cudaFree(p);
     p = nullptr;
-    cap = 0;
-    cudaError_t e = cudaMalloc(&p, std::max<size_t>(bytes, 256));
-    if (e == cudaSuccess) cap = std::max<size_t>(bytes, 256);
+    // grow by >= 1.25x so batches that keep growing (a search whose accepted
+    // states add ops) do not reallocate every round
+    const size_t want = std::max<size_t>(std::max(bytes, cap + cap / 4), 256);
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e != cudaSuccess) {  // fall back to the exact size
+      cudaGetLastError();
+      e = cudaMalloc(&p, std::max<size_t>(bytes, 256));
+      if (e == cudaSuccess) cap = std::max<size_t>(bytes, 256);
+      else cap = 0;
+      return e;
+    }
+    cap = want;
     return e;
   }
   template <typename T>

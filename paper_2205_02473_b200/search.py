@@ -106,16 +106,21 @@ def should_fuse_tensors(q_prev_end: int, p_cur_end: int, s_prev: int, s_cur: int
 class SyncState:
     """Synchronization units of a layered model: groups of consecutive layers
     fused in layer order (apply_tensor_fusion chain), each with a partition
-    count (apply_tensor_partition)."""
+    count (apply_tensor_partition); optionally op fusion of adjacent FW / BW
+    ops on every worker (fw_join / bw_join, apply_op_fusion chains)."""
     groups: list[list[int]]
     ks: list[int]
     makespan: int = -1
+    fw_join: list[int] = field(default_factory=list)
+    bw_join: list[int] = field(default_factory=list)
 
     def key(self) -> tuple:
-        return tuple(tuple(g) for g in self.groups), tuple(self.ks)
+        return (tuple(tuple(g) for g in self.groups), tuple(self.ks), tuple(self.fw_join),
+                tuple(self.bw_join))
 
     def copy(self) -> "SyncState":
-        return SyncState([list(g) for g in self.groups], list(self.ks), self.makespan)
+        return SyncState([list(g) for g in self.groups], list(self.ks), self.makespan,
+                         list(self.fw_join), list(self.bw_join))
 
 
 @dataclass
@@ -139,7 +144,7 @@ class SyncSearch:
 
     def __init__(self, model: LayeredModel, cluster: ClusterSpec, engine: Engine | None = None,
                  kmax: int = 16, beta: float = 0.01, seed: int = 0, threads: int = 8,
-                 dist=None, rank: int = 0, guided: float = 0.0):
+                 dist=None, rank: int = 0, guided: float = 0.0, op_fusion: bool = False):
         self.model, self.cluster = model, cluster
         self.engine = engine or default_engine()
         self.kmax, self.beta, self.threads = kmax, beta, threads
@@ -147,6 +152,9 @@ class SyncSearch:
         # path (CandidateSelection, Alg. 1; critical path = K3)
         self.guided = guided
         self._critical: np.ndarray | None = None
+        # op-fusion moves (toggle FW.l<i>+FW.l<i+1> / BW.l<i+1>+BW.l<i> on
+        # every worker): BASELINE config 4's strategy mix
+        self.op_fusion = op_fusion
         self.rng = np.random.default_rng([seed, rank])
         self.dist, self.rank = dist, rank
         L = model.layers
@@ -197,11 +205,23 @@ class SyncSearch:
         return cuts, kl
 
     @staticmethod
-    def _state(cuts: np.ndarray, kl: np.ndarray) -> SyncState:
+    def _state(cuts: np.ndarray, kl: np.ndarray, fj=None, bj=None) -> SyncState:
         starts = [0] + (np.flatnonzero(cuts) + 1).tolist()
         ends = starts[1:] + [len(kl)]
         return SyncState([list(range(a, b)) for a, b in zip(starts, ends)],
-                         [int(kl[a]) for a in starts])
+                         [int(kl[a]) for a in starts], -1,
+                         [] if fj is None or not fj.any() else fj.astype(int).tolist(),
+                         [] if bj is None or not bj.any() else bj.astype(int).tolist())
+
+    def _joins0(self, s: SyncState):
+        L = self.model.layers
+        fj = np.zeros(max(L - 1, 0), np.uint8)
+        bj = np.zeros(max(L - 1, 0), np.uint8)
+        if s.fw_join:
+            fj[:] = s.fw_join
+        if s.bw_join:
+            bj[:] = s.bw_join
+        return fj, bj
 
     def critical_layers(self, s: SyncState) -> np.ndarray:
         """Layers whose compute or synchronization ops lie on the critical
@@ -243,10 +263,19 @@ class SyncSearch:
         multi = np.flatnonzero(sizes > 1)
         cuts = np.repeat(cuts0[None], n, 0)
         kl = np.repeat(kl0[None], n, 0)
-        move = self.rng.integers(0, 3, n)
+        fj0, bj0 = self._joins0(s)
+        fj = np.repeat(fj0[None], n, 0)
+        bj = np.repeat(bj0[None], n, 0)
+        move = self.rng.integers(0, 5 if self.op_fusion and L > 1 else 3, n)
+        for mv, arr in ((3, fj), (4, bj)):  # toggle one op-fusion join
+            rows = np.flatnonzero(move == mv)
+            if len(rows):
+                i = self.rng.integers(0, L - 1, len(rows))
+                arr[rows, i] ^= 1
+        move = np.where(move >= 3, -1, move)
         m0 = (move == 0) & (G > 1)
         m1 = (move == 1) & (len(multi) > 0)
-        m2 = ~(m0 | m1)
+        m2 = ~(m0 | m1) & (move >= 0)
         r0 = np.flatnonzero(m0)
         if len(r0):  # fuse units j, j+1
             ok = np.ones(G, bool)
@@ -272,6 +301,7 @@ class SyncSearch:
             gi = self._pick_units(len(r2), G, starts, sizes, np.ones(G, bool))
             cap = np.minimum(self.kmax, gbytes[gi])
             kl[r2, starts[gi]] = (self.rng.random(len(r2)) * cap).astype(np.int64) + 1
+        self._last_joins = (fj, bj)
         return cuts, kl
 
     def _spec_arrays(self, cuts: np.ndarray, kl: np.ndarray):
@@ -286,9 +316,10 @@ class SyncSearch:
         members = np.tile(np.arange(L, dtype=np.int32), n)
         return n_groups, spec_off, group_off, members, kl[r, p].astype(np.int32)
 
-    def evaluate_arrays(self, cuts: np.ndarray, kl: np.ndarray) -> np.ndarray:
+    def evaluate_arrays(self, cuts: np.ndarray, kl: np.ndarray, fj=None, bj=None) -> np.ndarray:
         """Exact makespans of a proposal matrix: one GPU batch."""
-        deltas = self.base.deltas_from_arrays(*self._spec_arrays(cuts, kl), threads=self.threads)
+        deltas = self.base.deltas_from_arrays(*self._spec_arrays(cuts, kl), threads=self.threads,
+                                              fw_join=fj, bw_join=bj)
         b = self.engine.delta_batch(self.resident, deltas)
         b.replay(want_schedule=False)
         ms, st, *_ = b.results()
@@ -300,7 +331,9 @@ class SyncSearch:
     def evaluate(self, states: Sequence[SyncState]) -> np.ndarray:
         """Exact makespans of candidate states: deltas against the resident
         base graph, merged, packed and replayed in one GPU batch."""
-        deltas = self.base.deltas([(st.groups, st.ks) for st in states], self.threads)
+        joins = [self._joins0(st) for st in states]
+        deltas = self.base.deltas([(st.groups, st.ks) for st in states], self.threads,
+                                  fw_join=[j[0] for j in joins], bw_join=[j[1] for j in joins])
         b = self.engine.delta_batch(self.resident, deltas)
         b.replay(want_schedule=False)
         ms, st, *_ = b.results()
@@ -333,9 +366,12 @@ class SyncSearch:
         if self.guided > 0 and self._critical is None:
             self._critical = self.critical_layers(s)
         cuts, kl = self.propose_many(s, batch)
-        ms = self.evaluate_arrays(cuts, kl)
+        fj, bj = self._last_joins if self.op_fusion else (None, None)
+        ms = self.evaluate_arrays(cuts, kl, fj, bj) if self.op_fusion else \
+            self.evaluate_arrays(cuts, kl)
         i = int(np.argmin(ms))
-        cand = self._state(cuts[i], kl[i])
+        cand = self._state(cuts[i], kl[i], None if fj is None else fj[i],
+                           None if bj is None else bj[i])
         cand.makespan = int(ms[i])
         prop = self._exchange(int(ms[i]), i, cand)
         # Metropolis acceptance (memory loss term 0); the

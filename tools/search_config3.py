@@ -31,19 +31,25 @@ def main():
     eng = Engine(local)
     threads = max(1, (os.cpu_count() or 8) // world)
     s = SyncSearch(w.model, w.cluster, eng, kmax=16, beta=0.002, seed=3, threads=threads,
-                   dist=dist, rank=rank, guided=float(os.environ.get("GUIDED", "0")))
+                   dist=dist, rank=rank, guided=float(os.environ.get("GUIDED", "0")),
+                   op_fusion=os.environ.get("OPF", "0") == "1")
     # split timing: wrap the batched evaluation
     t_gen = t_gpu = 0.0
 
-    def timed(cuts, kl):
+    def timed(cuts, kl, fj=None, bj=None):
         nonlocal t_gen, t_gpu
         t0 = time.perf_counter()
-        deltas = s.base.deltas_from_arrays(*s._spec_arrays(cuts, kl), threads=threads)
+        deltas = s.base.deltas_from_arrays(*s._spec_arrays(cuts, kl), threads=threads,
+                                           fw_join=fj, bw_join=bj)
         t1 = time.perf_counter()
         b = eng.delta_batch(s.resident, deltas)
+        t1b = time.perf_counter()
         b.replay(want_schedule=False)
         ms, st, *_ = b.results()
         t2 = time.perf_counter()
+        if os.environ.get("STATS"):
+            print(json.dumps({"prepare_s": round(t1b - t1, 4), "replay_s": round(t2 - t1b, 4),
+                              **b.stats()}), file=sys.stderr)
         t_gen += t1 - t0
         t_gpu += t2 - t1
         s.log.evaluated += len(ms)
