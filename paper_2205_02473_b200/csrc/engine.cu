@@ -1227,7 +1227,11 @@ extern "C" {
 
 int dpro_cuda_batch_replay(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
   if (!ctx || !b) return DPRO_EINVAL;
-  if (b->n == 0) return DPRO_OK;
+  if (b->n == 0) {  // nothing to launch; results are empty
+    b->replayed = true;
+    b->with_schedule = want_schedule != 0;
+    return DPRO_OK;
+  }
   CU(cudaSetDevice(ctx->device));
   const int st = ctx->fast ? launch_fast(ctx, b, want_schedule)
                            : launch_general(ctx, b, want_schedule);

@@ -360,3 +360,52 @@ def test_gpu_op_fusion_deltas_replay_like_full(engine):
     ms1, st1, _, s1, e1 = db.results(schedule=True)
     assert np.all(st0 == 0) and np.array_equal(ms0, ms1)
     assert np.array_equal(s0, s1) and np.array_equal(e0, e1)
+
+
+@pytest.mark.gpu
+def test_delta_batch_edge_cases(engine):
+    """Empty batches and malformed deltas: empty results, or the engine's
+    EINVAL with the reason (no device work, no crash)."""
+    from paper_2205_02473_b200.delta import DeltaArrays, DeltaList, make_delta
+    from paper_2205_02473_b200.engine import Csr
+    from paper_2205_02473_b200.errors import Error
+    base, specs = _setup("ring", 4, 0, 5, 2, 3)
+    res = engine.resident(base.graph().csr)
+    b = engine.delta_batch(res, DeltaList([]))
+    b.replay(want_schedule=False)
+    ms, st, *_ = b.results()
+    assert ms.size == 0 and st.size == 0
+    # a no-op delta replays the base itself
+    g = base.graph().to_global_dfg()
+    d0 = make_delta(g, g)
+    assert d0.removed.size == 0 and d0.new_pos.size == 0
+    b = engine.delta_batch(res, DeltaList([d0]))
+    b.replay(want_schedule=False)
+    fb = engine.batch([base.graph().csr])
+    fb.replay(want_schedule=False)
+    assert b.results()[0].tolist() == fb.results()[0].tolist()
+    # malformed: removed index out of range, new_pos not sorted, bad successor
+    u32 = lambda x: np.array(x, np.uint32)  # noqa: E731
+    empty = dict(new_pos=u32([]), new_dur=np.zeros(0, np.int64), new_dev=np.zeros(0, np.uint16),
+                 new_flags=np.zeros(0, np.uint8), new_succ_off=u32([0]), new_succ=u32([]),
+                 extra_src=u32([]), extra_dst=u32([]), cut=u32([]))
+    n = base.graph().n_ops
+    bad = [DeltaArrays(d0.n_devices, u32([n + 5]), **empty),
+           DeltaArrays(d0.n_devices, u32([]), **{**empty, "new_pos": u32([3, 1]),
+                                                  "new_dur": np.ones(2, np.int64),
+                                                  "new_dev": np.zeros(2, np.uint16),
+                                                  "new_flags": np.zeros(2, np.uint8),
+                                                  "new_succ_off": u32([0, 0, 0])}),
+           DeltaArrays(d0.n_devices, u32([]), **{**empty, "new_pos": u32([0]),
+                                                  "new_dur": np.ones(1, np.int64),
+                                                  "new_dev": np.zeros(1, np.uint16),
+                                                  "new_flags": np.zeros(1, np.uint8),
+                                                  "new_succ_off": u32([0, 1]),
+                                                  "new_succ": u32([n + 7])})]
+    for d in bad:
+        with pytest.raises(Error, match="delta 0"):
+            engine.delta_batch(res, DeltaList([d]))
+    # the engine stays usable afterwards
+    b = engine.delta_batch(res, base.deltas(specs))
+    b.replay(want_schedule=False)
+    assert np.all(b.results()[1] == 0)
