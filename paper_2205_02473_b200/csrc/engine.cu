@@ -202,7 +202,7 @@ struct dpro_ctx {
   }
   int fast = 1;       // option "fast"
   uint32_t ring = 4;  // option "ring"
-  int warps = 4;      // option "warps": warps (1, 2, 4, 8) per candidate
+  int warps = 0;      // option "warps": warps (1, 2, 4, 8) per candidate; 0 = by device count
   int gcnt = 0;       // option "gcnt": 1 = fast-path counters always in global scratch
   int deep_first = -1;  // option "deep_first": -1 auto (mean V > 1M), 0 never, 1 always
   dpro_batch* spare = nullptr;  // recycled arenas for repeated small calls
@@ -1079,7 +1079,7 @@ int dpro_cuda_set_option(dpro_ctx* ctx, const char* key, int64_t value) {
     ctx->fast = static_cast<int>(value);
     return DPRO_OK;
   }
-  if (k == "warps" && (value == 1 || value == 2 || value == 4 || value == 8)) {
+  if (k == "warps" && (value == 0 || value == 1 || value == 2 || value == 4 || value == 8)) {
     ctx->warps = static_cast<int>(value);
     return DPRO_OK;
   }
@@ -1213,7 +1213,13 @@ int launch_fast_nw(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
 }
 
 int launch_fast(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
-  switch (ctx->warps) {
+  // auto (option warps = 0): the CTA's lanes own the devices, so graphs with
+  // few devices waste most of a 4-warp CTA in every round's barriers
+  // (config 1, 16 devices: 1 warp 8.5 ms vs 4 warps 11.2 ms; config 2, 144
+  // devices: 4 warps 2.95 ms vs 1 warp 8.5 ms -- tools/warps_sweep.py)
+  int nw = ctx->warps;
+  if (nw == 0) nw = b->max_d <= 32 ? 1 : b->max_d <= 64 ? 2 : 4;
+  switch (nw) {
     case 1: return launch_fast_nw<1>(ctx, b, want_schedule);
     case 2: return launch_fast_nw<2>(ctx, b, want_schedule);
     case 8: return launch_fast_nw<8>(ctx, b, want_schedule);

@@ -55,13 +55,13 @@ def mode_engine(engine, request):
     the deep-ring pass (the large-graph schedule)."""
     engine.set_option("fast", 0 if request.param == "general" else 1)
     engine.set_option("ring", 2 if request.param == "fast_ring2" else 4)
-    engine.set_option("warps", {"fast_w1": 1, "fast_w2": 2}.get(request.param, 4))
+    engine.set_option("warps", {"fast_w1": 1, "fast_w2": 2}.get(request.param, 4))  # explicit
     engine.set_option("gcnt", 1 if request.param == "fast_gcnt" else 0)
     engine.set_option("deep_first", 1 if request.param == "fast_deep" else -1)
     yield engine
     engine.set_option("fast", 1)
     engine.set_option("ring", 4)
-    engine.set_option("warps", 4)
+    engine.set_option("warps", 0)  # back to automatic
     engine.set_option("gcnt", 0)
     engine.set_option("deep_first", -1)
 
