@@ -93,7 +93,11 @@ int dpro_cuda_set_stream(dpro_ctx* ctx, void* stream);
 /* Engine options: "fast" (1: on-chip fast path with exact fallback, 0: the
  * general kernel only), "ring" (fast-path queue capacity per device, power
  * of two), "warps" (1, 2, 4 or 8 warps = one CTA cooperating on a candidate in
- * the fast path). Returns DPRO_EINVAL for unknown keys or values. */
+ * the fast path; 0 = by device count, the default), "gcnt" (1: fast-path
+ * counters always in global scratch), "deep_first" (-1 auto, 0 never, 1
+ * always start in the deep-ring pass), "host_threads" (host pool size for
+ * delta batches; 0 = all hardware threads). Returns DPRO_EINVAL for unknown
+ * keys or values. */
 int dpro_cuda_set_option(dpro_ctx* ctx, const char* key, int64_t value);
 const char* dpro_cuda_last_error(dpro_ctx* ctx);
 

@@ -113,8 +113,8 @@ struct HostPinned {
 // (e.g. issuing H2D copies) until wait().
 class Pool {
  public:
-  Pool() {
-    const int n = std::max(1, (int)std::thread::hardware_concurrency());
+  explicit Pool(int threads) {
+    const int n = threads > 0 ? threads : std::max(1, (int)std::thread::hardware_concurrency());
     for (int t = 0; t < n; ++t) th_.emplace_back([this] { loop(); });
   }
   ~Pool() {
@@ -196,8 +196,9 @@ struct dpro_ctx {
   int pack_clusters = 0;       // co-resident pack clusters (queried once)
   cudaStream_t copy_stream = nullptr;  // H2D of delta chunks (overlaps the merges)
   std::vector<cudaEvent_t> chunk_ev;   // one per in-flight chunk copy
+  int host_threads = 0;  // option "host_threads": pool size (0 = all hardware threads)
   Pool& workers() {
-    if (!pool) pool = std::make_unique<Pool>();
+    if (!pool) pool = std::make_unique<Pool>(host_threads);
     return *pool;
   }
   int fast = 1;       // option "fast"
@@ -1081,6 +1082,11 @@ int dpro_cuda_set_option(dpro_ctx* ctx, const char* key, int64_t value) {
   }
   if (k == "warps" && (value == 0 || value == 1 || value == 2 || value == 4 || value == 8)) {
     ctx->warps = static_cast<int>(value);
+    return DPRO_OK;
+  }
+  if (k == "host_threads" && value >= 0 && value <= 4096) {
+    if (ctx->pool && ctx->host_threads != static_cast<int>(value)) ctx->pool.reset();
+    ctx->host_threads = static_cast<int>(value);
     return DPRO_OK;
   }
   if (k == "gcnt" && (value == 0 || value == 1)) {
