@@ -402,7 +402,11 @@ int upload_host(dpro_ctx* ctx, dpro_batch* b, const dpro_csr* cands) {
 }
 
 int finish_batch(dpro_ctx* ctx, dpro_batch* b);
+int alloc_batch(dpro_ctx* ctx, dpro_batch* b, const std::vector<uint32_t>& e_cap,
+                bool upload_desc);
 int run_pack(dpro_ctx* ctx, dpro_batch* b);
+int launch_pack(dpro_ctx* ctx, dpro_batch* b, int32_t c0, int32_t c1);
+int read_pack_info(dpro_ctx* ctx, dpro_batch* b);
 int run_merge(dpro_ctx* ctx, dpro_batch* b, int32_t c0, int32_t c1);
 
 int build_batch(dpro_ctx* ctx, dpro_batch* b, const dpro_csr* cands) {
@@ -460,6 +464,16 @@ int build_batch(dpro_ctx* ctx, dpro_batch* b, const dpro_csr* cands) {
 // Scratch, outputs, descriptors and the pack kernel for a batch whose
 // b->hc descriptors point at device CSR arrays.
 int finish_batch(dpro_ctx* ctx, dpro_batch* b) {
+  const int st = alloc_batch(ctx, b, b->n_edges, true);
+  if (st != DPRO_OK) return st;
+  return run_pack(ctx, b);
+}
+
+// Scratch, outputs and the packed layout of a batch. e_cap: per-candidate
+// edge capacity of the expanded lists (exact counts, or bounds when the
+// counts are not known yet); upload_desc: copy b->hc to the device.
+int alloc_batch(dpro_ctx* ctx, dpro_batch* b, const std::vector<uint32_t>& e_cap,
+                bool upload_desc) {
   const int32_t n = b->n;
   const unsigned long long so = b->sum_n, sd = b->sum_d, sdo = b->sum_dof;
   // scratch: indeg, qbuf, qpos, vstack (u32), sched (u8), devoff, dstate, busy
@@ -492,8 +506,9 @@ int finish_batch(dpro_ctx* ctx, dpro_batch* b) {
   b->O.start = b->outs.as<long long>(o); o += o_op;
   b->O.end = b->outs.as<long long>(o); o += o_op;
   CU(b->desc.ensure(sizeof(Cand) * std::max(n, 1)));
-  CU(cudaMemcpyAsync(b->desc.p, b->hc.data(), sizeof(Cand) * n,
-                     cudaMemcpyHostToDevice, ctx->stream));
+  if (upload_desc)
+    CU(cudaMemcpyAsync(b->desc.p, b->hc.data(), sizeof(Cand) * n, cudaMemcpyHostToDevice,
+                       ctx->stream));
   CU(b->work.ensure(16));
   // packed replay layout (pack_kernel.cuh)
   {
@@ -504,7 +519,7 @@ int finish_batch(dpro_ctx* ctx, dpro_batch* b) {
       e_off[i] = eo;
       c_off[i] = co;
       ro += b->n_ops[i] + 1;
-      eo += b->n_edges[i];
+      eo += e_cap[i];
       co += 2ull * ((b->n_ops[i] + 15) & ~15u);  // room for u16 counters
     }
     const size_t s_rec = align16(ro * 16 + 16), s_erec = align16(eo * 16 + 16),
@@ -533,50 +548,61 @@ int finish_batch(dpro_ctx* ctx, dpro_batch* b) {
     CU(cudaMemcpyAsync(b->P.c_off, c_off.data(), size_t(n) * 8, cudaMemcpyHostToDevice, ctx->stream));
     b->s_cnt0 = s_cnt;
   }
-  return run_pack(ctx, b);
+  return DPRO_OK;
 }
 
 // The pack kernel (and count_indeg when a candidate came without in-degrees)
-// on the batch's device CSR, then the per-candidate PackInfo to the host.
-int run_pack(dpro_ctx* ctx, dpro_batch* b) {
+// for candidates [c0, c1) on the batch's device CSR.
+int launch_pack(dpro_ctx* ctx, dpro_batch* b, int32_t c0, int32_t c1) {
+  if (c1 <= c0) return DPRO_OK;
+  bool need_indeg = false;
+  for (int32_t i = c0; i < c1; ++i) need_indeg |= (b->hc[i].indeg == nullptr);
+  if (need_indeg)
+    dpro_k::count_indeg_kernel<<<std::min<int>(c1 - c0, ctx->sm_count * 8), 256, 0,
+                                 ctx->stream>>>(b->desc.as<Cand>() + c0, c1 - c0, b->S);
+  if (ctx->pack_clusters == 0) {  // co-resident clusters of the pack kernel
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(dpro_k::kPackCluster * (ctx->sm_count / dpro_k::kPackCluster));
+    cfg.blockDim = dim3(dpro_k::kPackThreads);
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = dpro_k::kPackCluster;
+    attr.val.clusterDim.y = attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    int m = 0;
+    if (cudaOccupancyMaxActiveClusters(&m, dpro_k::pack_kernel, &cfg) != cudaSuccess || m < 1)
+      m = ctx->sm_count / dpro_k::kPackCluster;
+    ctx->pack_clusters = m;
+  }
+  const int clusters = std::max(1, std::min<int>(c1 - c0, ctx->pack_clusters));
+  dpro_k::pack_kernel<<<clusters * dpro_k::kPackCluster, dpro_k::kPackThreads, 0,
+                        ctx->stream>>>(b->desc.as<Cand>(), c0, c1, b->S, b->P);
+  CU(cudaGetLastError());
+  return DPRO_OK;
+}
+
+// PackInfo of every candidate to the host (the replay launch sizes its
+// shared memory from it).
+int read_pack_info(dpro_ctx* ctx, dpro_batch* b) {
   const int32_t n = b->n;
-  CU(cudaMemsetAsync(b->P.cnt0, 0, b->s_cnt0, ctx->stream));
   b->info.assign(n, dpro_k::PackInfo{});
   if (n > 0) {
-    const int grid = std::min<int>(n, ctx->sm_count * 8);
-    bool need_indeg = false;
-    for (int32_t i = 0; i < n; ++i) need_indeg |= (b->hc[i].indeg == nullptr);
-    if (need_indeg)
-      dpro_k::count_indeg_kernel<<<grid, 256, 0, ctx->stream>>>(b->desc.as<Cand>(), n, b->S);
-    Tracer tr;
-    if (ctx->pack_clusters == 0) {  // co-resident clusters of the pack kernel
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(dpro_k::kPackCluster * (ctx->sm_count / dpro_k::kPackCluster));
-      cfg.blockDim = dim3(dpro_k::kPackThreads);
-      cudaLaunchAttribute attr;
-      attr.id = cudaLaunchAttributeClusterDimension;
-      attr.val.clusterDim.x = dpro_k::kPackCluster;
-      attr.val.clusterDim.y = attr.val.clusterDim.z = 1;
-      cfg.attrs = &attr;
-      cfg.numAttrs = 1;
-      int m = 0;
-      if (cudaOccupancyMaxActiveClusters(&m, dpro_k::pack_kernel, &cfg) != cudaSuccess || m < 1)
-        m = ctx->sm_count / dpro_k::kPackCluster;
-      ctx->pack_clusters = m;
-      if (std::getenv("DPRO_TRACE"))
-        std::fprintf(stderr, "[dpro] pack kernel: %d co-resident clusters\n", m);
-    }
-    const int clusters = std::max(1, std::min<int>(n, ctx->pack_clusters));
-    dpro_k::pack_kernel<<<clusters * dpro_k::kPackCluster, dpro_k::kPackThreads, 0,
-                          ctx->stream>>>(b->desc.as<Cand>(), n, b->S, b->P);
-    CU(cudaGetLastError());
-    tr.mark("pack kernel", ctx->stream, true);
     CU(cudaMemcpyAsync(b->info.data(), b->P.info, size_t(n) * sizeof(dpro_k::PackInfo),
                        cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
   }
   b->replayed = b->with_schedule = false;
   return DPRO_OK;
+}
+
+int run_pack(dpro_ctx* ctx, dpro_batch* b) {
+  CU(cudaMemsetAsync(b->P.cnt0, 0, b->s_cnt0, ctx->stream));
+  Tracer tr;
+  const int st = launch_pack(ctx, b, 0, b->n);
+  if (st != DPRO_OK) return st;
+  tr.mark("pack kernel", ctx->stream, true);
+  return read_pack_info(ctx, b);
 }
 
 }  // namespace
@@ -785,6 +811,24 @@ int build_delta_batch(dpro_ctx* ctx, dpro_batch* b, const dpro_resident* r,
   CU(b->pred1.ensure(so * 4 + 16));
   b->res = r;
   b->smem_ind = std::min(max_n, dpro_k::kMergeIndegSmem);
+  // scratch, outputs and the packed layout (edge capacities = the bounds), so
+  // each wave can be packed right after its merge
+  std::vector<uint32_t> e_cap(n);
+  for (int32_t i = 0; i < n; ++i) {
+    b->n_ops[i] = b->hc[i].n;
+    b->n_dev[i] = b->hc[i].d;
+    b->max_d = std::max(b->max_d, b->hc[i].d);
+    e_cap[i] = static_cast<uint32_t>(size_t(r->e) + deltas[i].n_extra +
+                                     deltas[i].new_succ_off[deltas[i].n_new]);
+  }
+  b->sum_n = so;
+  b->sum_d = sd;
+  b->sum_dof = sdo;
+  {
+    const int st = alloc_batch(ctx, b, e_cap, false);
+    if (st != DPRO_OK) return st;
+  }
+  CU(cudaMemsetAsync(b->P.cnt0, 0, b->s_cnt0, ctx->stream));
   char* stage = static_cast<char*>(ctx->staging.p);
   std::vector<dpro_k::DeltaDev> dd(n);
   std::vector<std::string> errs(n);
@@ -875,6 +919,7 @@ int build_delta_batch(dpro_ctx* ctx, dpro_batch* b, const dpro_resident* r,
       if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->stream, ctx->chunk_ev[k], 0);
       if (e != cudaSuccess) err = set_err(ctx, DPRO_ECUDA, cudaGetErrorString(e));
       if (err == DPRO_OK) err = run_merge(ctx, b, c0, c1);
+      if (err == DPRO_OK) err = launch_pack(ctx, b, c0, c1);
     }
     i = c1;
   }
@@ -886,19 +931,15 @@ int build_delta_batch(dpro_ctx* ctx, dpro_batch* b, const dpro_resident* r,
       return set_err(ctx, DPRO_EINVAL, "delta " + std::to_string(i) + ": " + errs[i]);
   unsigned long long se = 0;
   for (int32_t i = 0; i < n; ++i) {
-    const Cand& h = b->hc[i];
-    b->n_ops[i] = h.n;
-    b->n_dev[i] = h.d;
-    b->n_edges[i] = h.e;
-    b->max_d = std::max(b->max_d, h.d);
-    se += h.e;
+    b->n_edges[i] = b->hc[i].e;
+    se += b->hc[i].e;
   }
-  b->sum_n = so;
-  b->sum_d = sd;
-  b->sum_dof = sdo;
   b->sum_e = se;
-  tr.mark("remaining H2D + merge", ctx->stream, true);
-  return finish_batch(ctx, b);
+  // exact descriptors (edge counts) for the replay; same stream order
+  CU(cudaMemcpyAsync(b->desc.p, b->hc.data(), sizeof(Cand) * n, cudaMemcpyHostToDevice,
+                     ctx->stream));
+  tr.mark("remaining H2D + merge + pack", ctx->stream, true);
+  return read_pack_info(ctx, b);
 }
 
 // K0 for candidates [c0, c1) (descriptors already on the device).

@@ -301,7 +301,7 @@ __device__ uint32_t block_exclusive_scan(uint32_t* a, uint32_t n,
 constexpr int kPackCluster = 1;
 
 __global__ void __cluster_dims__(kPackCluster, 1, 1) __launch_bounds__(kPackThreads, 1)
-    pack_kernel(const Cand* __restrict__ cands, int n_cands, Scratch S, PackOut P) {
+    pack_kernel(const Cand* __restrict__ cands, int c0, int n_cands, Scratch S, PackOut P) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   using Scan = cub::BlockScan<uint32_t, kPackThreads>;
@@ -321,7 +321,7 @@ __global__ void __cluster_dims__(kPackCluster, 1, 1) __launch_bounds__(kPackThre
   uint32_t* wbuf = s_warp + 32 * warp;
   Ctr* R0 = cluster.map_shared_rank(&s_ctr, 0);
   const int n_clusters = gridDim.x / kPackCluster;
-  for (int cid = blockIdx.x / kPackCluster; cid < n_cands; cid += n_clusters) {
+  for (int cid = c0 + blockIdx.x / kPackCluster; cid < n_cands; cid += n_clusters) {
     const Cand c = cands[cid];
     const uint32_t n = c.n;
     const uint32_t* indeg = c.indeg ? c.indeg : S.indeg + c.op_off;
