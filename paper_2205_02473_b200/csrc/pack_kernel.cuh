@@ -79,6 +79,16 @@ struct PackOut {
   PackInfo* info;              // [B]
 };
 
+constexpr int kPackClusterSize = 1;  // == kPackCluster (below); chooses the gather loads
+
+// Loads of data another CTA of the cluster may have written: through L2
+// when the cluster spans SMs, else the normal (L1-cached) path.
+template <typename T>
+__device__ __forceinline__ T ld_shared_pass(const T* p) {
+  if constexpr (kPackClusterSize > 1) return __ldcg(p);
+  else return *p;
+}
+
 __device__ __forceinline__ bool spliced(const Cand& c, const uint32_t* indeg, uint32_t s) {
   return (c.flags[s] & 1u) && indeg[s] == 1u;
 }
@@ -190,7 +200,7 @@ __device__ void coop_sizes(const Cand& c, const uint8_t* spl, uint32_t i0, uint3
     }
     uint32_t sp[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) sp[u] = live[u] ? __ldcg(spl + sv[u]) : 0u;
+    for (int u = 0; u < U; ++u) sp[u] = live[u] ? ld_shared_pass(spl + sv[u]) : 0u;
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (live[u])
@@ -226,10 +236,10 @@ __device__ void coop_lists(const Cand& c, const uint8_t* spl, uint32_t i0, uint3
       s[u] = live[u] ? c.succ[k] : 0u;
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u) sv[u] = live[u] && __ldcg(spl + s[u]);
+    for (int u = 0; u < U; ++u) sv[u] = live[u] && ld_shared_pass(spl + s[u]);
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      r[u] = (live[u] && !sv[u]) ? __ldcg(rec + s[u]) : make_uint4(0, 0, 0, 0);
+      r[u] = (live[u] && !sv[u]) ? ld_shared_pass(rec + s[u]) : make_uint4(0, 0, 0, 0);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint32_t k = kb + 32 * u + lane;
@@ -254,7 +264,7 @@ __device__ void coop_lists(const Cand& c, const uint8_t* spl, uint32_t i0, uint3
         uint32_t pos = x_src + (k - o_src) + (P - segp[src[u]]);
         if (sv[u]) {
           __stcs(erec + pos, make_uint4(s[u] & kOpMask, 0u, kFVirt, 0u));
-          for (uint32_t t = sa; t < sz; ++t) __stcs(erec + (++pos), __ldcg(rec + c.succ[t]));
+          for (uint32_t t = sa; t < sz; ++t) __stcs(erec + (++pos), ld_shared_pass(rec + c.succ[t]));
         } else {
           __stcs(erec + pos, r[u]);
         }
@@ -298,7 +308,7 @@ __device__ uint32_t block_exclusive_scan(uint32_t* a, uint32_t n,
 // 0's shared memory (DSMEM atomics); cluster barriers separate the passes,
 // and records written by other SMs are read through L2 (__ldcg). indeg must
 // be present (host upload / delta merge) or computed by count_indeg_kernel.
-constexpr int kPackCluster = 1;
+constexpr int kPackCluster = kPackClusterSize;
 
 __global__ void __cluster_dims__(kPackCluster, 1, 1) __launch_bounds__(kPackThreads, 1)
     pack_kernel(const Cand* __restrict__ cands, int c0, int n_cands, Scratch S, PackOut P) {
