@@ -72,6 +72,7 @@ def ref_lib():
             "ref_peak_memory": (_I32, [_P, C.c_char_p, _P, _P]),
             "ref_peak_node": (C.c_char_p, [_I32]),
             "ref_apply_memory_strategy": (_P, [_P, _I32, C.c_char_p, _P]),
+            "ref_timeline_json": (_I64, [_P, _P, _I64, _P]),
             "ref_memory_pass": (_P, [_P, _I64, C.c_char_p, _P, _P, _P, _P]),
             "ref_partial_replay": (_I32, [_P, C.c_char_p, _I32, _P]),
             "ref_tsync_graph": (_P, [C.c_char_p, _I64, _I32, _P]),
@@ -177,6 +178,15 @@ class RefGraph:
         h = self.lib.ref_apply_tensor_fusion(self.h, t1.encode(), t2.encode(), C.byref(st))
         _raise(self.lib, st.value)
         return RefGraph(h)
+
+    def timeline_json(self) -> bytes:
+        """The CLI's timeline.json bytes for replay(g) (dpro_main.cpp:90-116)."""
+        st = C.c_int32(0)
+        n = self.lib.ref_timeline_json(self.h, None, 0, C.byref(st))
+        _raise(self.lib, st.value)
+        buf = C.create_string_buffer(n)
+        self.lib.ref_timeline_json(self.h, buf, n, C.byref(st))
+        return buf.raw[:n]
 
     def apply_memory_strategy(self, kind: int, meta: dict) -> "RefGraph":
         """apply_strategy(kRecompute=3 | kGradAccum=4)."""

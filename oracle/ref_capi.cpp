@@ -177,6 +177,48 @@ void* ref_apply_op_fusion(void* h, const char* a, const char* b,
   return out;
 }
 
+// The CLI's timeline.json for replay(g) (checker for report.py): a
+// restatement of proj/tools/dpro_main.cpp:90-116 (timeline_json) and 64-70
+// (write_json: dump(2) + newline) on the reference's own GlobalDFG and
+// replay -- the CLI itself needs CLI11, absent here. Returns the byte size;
+// the text is copied into buf when cap is large enough.
+thread_local std::string g_timeline;
+int64_t ref_timeline_json(void* hv, char* buf, int64_t cap, int32_t* status) {
+  auto* h = static_cast<Handle*>(hv);
+  *status = guarded([&] {
+    const ReplayResult r = replay(h->g);
+    nlohmann::json events = nlohmann::json::array();
+    for (const auto& [id, entry] : r.schedule) {
+      const Op& op = h->g.op(id);
+      if (is_virtual(op.kind)) continue;
+      nlohmann::json e;
+      e["name"] = id;
+      e["ph"] = "X";
+      e["pid"] = entry.device.str();
+      e["tid"] = op.node;
+      e["ts"] = entry.start;
+      e["dur"] = entry.end - entry.start;
+      e["cat"] = to_string(op.kind);
+      e["args"]["kind"] = to_string(op.kind);
+      e["args"]["iteration"] = 0;
+      if (is_communication(op.kind)) {
+        e["args"]["tensor"] = op.tensor;
+        e["args"]["bytes"] = op.bytes;
+        e["args"]["transaction"] = op.transaction;
+      }
+      events.push_back(std::move(e));
+    }
+    nlohmann::json j;
+    j["traceEvents"] = std::move(events);
+    j["displayTimeUnit"] = "ms";
+    g_timeline = j.dump(2) + "\n";
+  });
+  if (*status) return 0;
+  if (buf && cap >= static_cast<int64_t>(g_timeline.size()))
+    std::memcpy(buf, g_timeline.data(), g_timeline.size());
+  return static_cast<int64_t>(g_timeline.size());
+}
+
 // apply_strategy for the parameterless memory rewrites (kind 3 recompute,
 // 4 grad-accum), optimize.cpp:506-531.
 void* ref_apply_memory_strategy(void* h, int32_t kind, const char* meta_json,

@@ -15,6 +15,7 @@ from .replay import (CriticalPath, PathEntry, PathRun, ReplayResult, ScheduleEnt
                      sync_makespan, sync_makespan_grid)
 from .rewrite import (BudgetError, Strategy, StrategyKind, apply_grad_accum, apply_recompute,
                       memory_pass)
+from .report import timeline_json, timeline_text, write_timeline
 from .memory import (ModelMeta, estimate_peak_memory, estimate_peak_memory_many,
                      output_bytes_for)
 
@@ -28,5 +29,5 @@ __all__ = [
     "MissingMetaError", "ParseError", "ModelMeta", "estimate_peak_memory",
     "estimate_peak_memory_many", "output_bytes_for", "TopologyError", "TransformError",
     "BudgetError", "Strategy", "StrategyKind", "apply_grad_accum", "apply_recompute",
-    "memory_pass",
+    "memory_pass", "timeline_json", "timeline_text", "write_timeline",
 ]
