@@ -362,6 +362,14 @@ int dpro_graph_memory_inputs(dpro_graph* g, int32_t n_entries, const char* const
                              const int64_t* bytes, int64_t* op_bytes, int32_t* op_node,
                              int32_t* n_nodes, uint32_t* missing_op);
 const char* dpro_graph_memory_node(const dpro_graph* g, int32_t i);
+/* Comm-op metadata (Op::tensor unit name, *bytes) of op i; NULL for other
+ * ops. The transaction is the op id after "SEND." / "RECV.". */
+const char* dpro_graph_comm_info(const dpro_graph* g, uint32_t i, int64_t* bytes);
+/* The CLI's timeline.json for a replayed schedule (start/end in the graph's
+ * index order), streamed natively: proj/tools/dpro_main.cpp:90-116 written
+ * as write_json does (64-70, nlohmann dump(2) + newline), byte for byte. */
+int dpro_graph_write_timeline(const dpro_graph* g, const int64_t* start,
+                              const int64_t* end, const char* path);
 /* n graphs with part_k[n*layers], built on `threads` host threads. */
 int dpro_graph_layered_batch(const dpro_layered_model* model,
                              const dpro_cluster_desc* cluster,

@@ -116,6 +116,8 @@ SIGNATURES = {
     "dpro_graph_layered_variant": (_P, [C.POINTER(DproLayeredModel), C.POINTER(DproClusterDesc), _P, _I32, C.c_double, _P]),
     "dpro_graph_memory_inputs": (C.c_int, [_P, _I32, _P, _P, _P, _P, _P, _P]),
     "dpro_graph_memory_node": (C.c_char_p, [_P, _I32]),
+    "dpro_graph_comm_info": (C.c_char_p, [_P, _U32, _P]),
+    "dpro_graph_write_timeline": (C.c_int, [_P, _P, _P, C.c_char_p]),
     "dpro_graph_layered_batch": (C.c_int, [C.POINTER(DproLayeredModel), C.POINTER(DproClusterDesc), _P, _I32, _I32, _P]),
     "dpro_graph_layered_groups": (_P, [C.POINTER(DproLayeredModel), C.POINTER(DproClusterDesc), _I32, _P, _P, _P, _P]),
     "dpro_graph_layered_groups_batch": (C.c_int, [C.POINTER(DproLayeredModel), C.POINTER(DproClusterDesc), _I32, _P, _P, _P, _P, _P, _I32, _P]),

@@ -10,6 +10,7 @@
 // Op ids are generated with the reference naming so the byte-lexicographic
 // sort reproduces the reference op index (the replay tie-break order).
 #include <algorithm>
+#include <cstdio>
 #include <array>
 #include <atomic>
 #include <charconv>
@@ -105,9 +106,12 @@ struct Gen {
     int32_t kind;
     uint32_t devkey;
     int64_t dur;
+    int32_t unit = -1;   // comm ops: tensor unit (index into units)
+    int64_t bytes = 0;   // comm ops: bytes moved
   };
   std::vector<Op> ops;
   std::vector<std::pair<uint32_t, uint32_t>> edges;  // creation indices
+  std::vector<std::string> units;  // tensor units named by comm ops
   // devices keyed by (kind, node index, peer index); resolved to DeviceId
   // order (kind, node name, peer name -- graph.hpp:57-72) in finalize()
   std::unordered_map<uint64_t, uint32_t> devkeys;
@@ -142,6 +146,12 @@ void expand_unit(Gen& g, const Cluster& c, const std::string& unit,
                  int64_t bytes, const std::vector<uint32_t>* in_op,
                  const std::vector<uint32_t>* out_op) {
   auto link_dev = [&](int s, int d) { return g.device(1, s, d); };
+  const int32_t uidx = static_cast<int32_t>(g.units.size());
+  g.units.push_back(unit);
+  auto tag = [&](uint32_t op, int64_t b) {  // Op::tensor / Op::bytes of a comm op
+    g.ops[op].unit = uidx;
+    g.ops[op].bytes = b;
+  };
   auto need = [&](const std::vector<uint32_t>* v, int node) -> uint32_t {
     if (!v) return UINT32_MAX;
     uint32_t x = (*v)[node];
@@ -180,6 +190,8 @@ void expand_unit(Gen& g, const Cluster& c, const std::string& unit,
         rid += txn;
         const uint32_t snd = g.add(std::move(sid), kSend, dv, 0);
         const uint32_t rcv = g.add(std::move(rid), kRecv, dv, c.hop(cb, src, dst));
+        tag(snd, cb);
+        tag(rcv, cb);
         g.edge(snd, rcv);
         if (s == 0) {
           const uint32_t in = need(in_op, src);
@@ -206,6 +218,8 @@ void expand_unit(Gen& g, const Cluster& c, const std::string& unit,
       const uint32_t dpush = link_dev(w, server);
       const uint32_t ps = g.add("SEND." + push, kSend, dpush, 0);
       const uint32_t pr = g.add("RECV." + push, kRecv, dpush, c.hop(bytes, w, server));
+      tag(ps, bytes);
+      tag(pr, bytes);
       g.edge(ps, pr);
       const uint32_t in = need(in_op, w);
       if (in != UINT32_MAX) g.edge(in, ps);
@@ -214,6 +228,8 @@ void expand_unit(Gen& g, const Cluster& c, const std::string& unit,
       const uint32_t dpull = link_dev(server, w);
       const uint32_t ls = g.add("SEND." + pull, kSend, dpull, 0);
       const uint32_t lr = g.add("RECV." + pull, kRecv, dpull, c.hop(bytes, server, w));
+      tag(ls, bytes);
+      tag(lr, bytes);
       g.edge(ls, lr);
       const uint32_t out = need(out_op, w);
       if (out != UINT32_MAX) g.edge(lr, out);
@@ -241,6 +257,11 @@ struct dpro_graph {
   std::vector<uint32_t> succ_off, succ, indeg;
   std::vector<std::string> device_strs;
   std::vector<std::string> mem_nodes;  // dpro_graph_memory_inputs: compute nodes, name order
+  // comm-op metadata (Op::tensor / bytes; the transaction is the id after
+  // "SEND." / "RECV."): unit index into units (-1 otherwise), bytes
+  std::vector<int32_t> cunit;
+  std::vector<int64_t> cbytes;
+  std::vector<std::string> units;
 };
 
 namespace {
@@ -311,8 +332,13 @@ dpro_graph* finalize(Gen& g, std::vector<uint32_t>* rank_out = nullptr,
   out->dur.resize(n);
   out->dev.resize(n);
   out->flags.resize(n);
+  out->cunit.resize(n);
+  out->cbytes.resize(n);
+  out->units = std::move(g.units);
   for (uint32_t i = 0; i < n; ++i) {
     auto& op = g.ops[order[i]];
+    out->cunit[i] = op.unit;
+    out->cbytes[i] = op.bytes;
     out->ids[i] = std::move(op.id);
     out->kind[i] = op.kind;
     out->dur[i] = op.dur;
@@ -879,6 +905,11 @@ dpro_graph* build_delta(const std::shared_ptr<BaseData>& Bp, const Groups& G) {
   out->dur.resize(n);
   out->dev.resize(n);
   out->flags.resize(n);
+  out->cunit.resize(n);
+  out->cbytes.resize(n);
+  out->units = bg.units;  // base units, then the candidate's new ones
+  const int32_t uoff = static_cast<int32_t>(bg.units.size());
+  out->units.insert(out->units.end(), g.units.begin(), g.units.end());
   for (uint32_t b = 0; b < nb; ++b) {
     const uint32_t x = fb[b];
     if (x == UINT32_MAX) continue;
@@ -886,10 +917,14 @@ dpro_graph* build_delta(const std::shared_ptr<BaseData>& Bp, const Groups& G) {
     out->dur[x] = bg.dur[b];
     out->dev[x] = bdev[bg.dev[b]];
     out->flags[x] = bg.flags[b];
+    out->cunit[x] = bg.cunit[b];
+    out->cbytes[x] = bg.cbytes[b];
   }
   for (uint32_t j = 0; j < nn; ++j) {
     const uint32_t x = fnew[j];
     const auto& op = g.ops[j];
+    out->cunit[x] = op.unit >= 0 ? op.unit + uoff : -1;
+    out->cbytes[x] = op.bytes;
     out->kind[x] = op.kind;
     out->dur[x] = op.dur;
     out->dev[x] = ndev[op.devkey];
@@ -1444,6 +1479,105 @@ int dpro_graph_memory_inputs(dpro_graph* g, int32_t n_entries, const char* const
 
 const char* dpro_graph_memory_node(const dpro_graph* g, int32_t i) {
   return g->mem_nodes.at(i).c_str();
+}
+
+const char* dpro_graph_comm_info(const dpro_graph* g, uint32_t i, int64_t* bytes) {
+  if (!g || i >= g->kind.size() || g->cunit.empty() || g->cunit[i] < 0) return nullptr;
+  if (bytes) *bytes = g->cbytes[i];
+  return g->units.at(g->cunit[i]).c_str();
+}
+
+namespace {
+const char* kind_name(int32_t k) {  // graph.cpp:25-43
+  static const char* names[] = {"FW", "BW", "UPDATE", "SEND", "RECV", "VIRTUAL_IN",
+                                "VIRTUAL_OUT"};
+  return (k >= 0 && k < 7) ? names[k] : "UNKNOWN";
+}
+// A JSON string as nlohmann::json::dump writes it (UTF-8 kept, control
+// characters escaped).
+void json_str(std::string& o, const std::string& v) {
+  o += '"';
+  for (const unsigned char ch : v) {
+    switch (ch) {
+      case '"': o += "\\\""; break;
+      case '\\': o += "\\\\"; break;
+      case '\b': o += "\\b"; break;
+      case '\f': o += "\\f"; break;
+      case '\n': o += "\\n"; break;
+      case '\r': o += "\\r"; break;
+      case '\t': o += "\\t"; break;
+      default:
+        if (ch < 0x20) {
+          char buf[8];
+          std::snprintf(buf, sizeof buf, "\\u%04x", ch);
+          o += buf;
+        } else {
+          o += static_cast<char>(ch);
+        }
+    }
+  }
+  o += '"';
+}
+}  // namespace
+
+int dpro_graph_write_timeline(const dpro_graph* g, const int64_t* start, const int64_t* end,
+                              const char* path) {
+  if (!g || !start || !end || !path) return DPRO_EINVAL;
+  std::FILE* f = std::fopen(path, "wb");
+  if (!f) {
+    g_gen_err = std::string("cannot open ") + path;
+    return DPRO_EINVAL;
+  }
+  // proj/tools/dpro_main.cpp:90-116 as written by write_json (64-70):
+  // nlohmann dump(2), keys in byte order, trailing newline
+  std::string o;
+  o.reserve(1 << 20);
+  o += "{\n  \"displayTimeUnit\": \"ms\",\n  \"traceEvents\": [";
+  bool any = false;
+  const uint32_t n = static_cast<uint32_t>(g->kind.size());
+  for (uint32_t i = 0; i < n; ++i) {
+    const int32_t k = g->kind[i];
+    if (k == kVin || k == kVout) continue;
+    const std::string id = dpro_graph_op_id(g, i);
+    const std::string& dev = g->device_strs[g->dev[i]];
+    std::string node = dev;
+    const bool comm = k == kSend || k == kRecv;
+    if (comm) {  // Op::node: the sender for SEND, the receiver for RECV
+      const auto gt = dev.find('>');
+      node = k == kSend ? dev.substr(0, gt) : dev.substr(gt + 1);
+    }
+    o += any ? ",\n    {\n" : "\n    {\n";
+    any = true;
+    o += "      \"args\": {\n";
+    if (comm) {
+      o += "        \"bytes\": " + std::to_string(g->cbytes.empty() ? 0 : g->cbytes[i]) + ",\n";
+    }
+    o += "        \"iteration\": 0,\n        \"kind\": ";
+    json_str(o, kind_name(k));
+    if (comm) {
+      o += ",\n        \"tensor\": ";
+      json_str(o, (g->cunit.empty() || g->cunit[i] < 0) ? std::string() : g->units[g->cunit[i]]);
+      o += ",\n        \"transaction\": ";
+      json_str(o, id.substr(5));  // "SEND." / "RECV." + transaction
+    }
+    o += "\n      },\n      \"cat\": ";
+    json_str(o, kind_name(k));
+    o += ",\n      \"dur\": " + std::to_string(end[i] - start[i]) + ",\n      \"name\": ";
+    json_str(o, id);
+    o += ",\n      \"ph\": \"X\",\n      \"pid\": ";
+    json_str(o, dev);
+    o += ",\n      \"tid\": ";
+    json_str(o, node);
+    o += ",\n      \"ts\": " + std::to_string(start[i]) + "\n    }";
+    if (o.size() > (1u << 20)) {
+      std::fwrite(o.data(), 1, o.size(), f);
+      o.clear();
+    }
+  }
+  o += any ? "\n  ]\n}\n" : "]\n}\n";
+  std::fwrite(o.data(), 1, o.size(), f);
+  const bool ok = std::fclose(f) == 0;
+  return ok ? DPRO_OK : DPRO_EINVAL;
 }
 
 int32_t dpro_graph_op_kind(const dpro_graph* g, uint32_t i) { return g->kind.at(i); }

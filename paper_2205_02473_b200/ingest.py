@@ -202,16 +202,33 @@ class NativeGraph:
         return [N.lib.dpro_graph_device_str(self.handle, d).decode()
                 for d in range(self.csr.n_devices)]
 
+    def write_timeline(self, path: str, start: np.ndarray, end: np.ndarray) -> None:
+        """The CLI's timeline.json for a replayed schedule, streamed natively
+        (dpro_graph_write_timeline); byte-identical to report.write_timeline."""
+        st = np.ascontiguousarray(start, np.int64)
+        en = np.ascontiguousarray(end, np.int64)
+        if st.size != self.n_ops or en.size != self.n_ops:
+            raise ValueError("start/end must cover every op")
+        if N.lib.dpro_graph_write_timeline(self.handle, N.ptr(st), N.ptr(en),
+                                           str(path).encode()) != N.DPRO_OK:
+            raise Error(N.lib.dpro_graph_last_error().decode())
+
     def to_global_dfg(self, cluster: ClusterSpec | None = None) -> GlobalDFG:
         """Python graph object (small graphs: tests / reference-shaped API)."""
         devs = self.device_strs()
         ids = self.op_ids()
         ops = []
+        b = C.c_int64(0)
         for i, id_ in enumerate(ids):
             ds = devs[int(self.csr.dev[i])]
             dev = DeviceId.link(*ds.split(">", 1)) if ">" in ds else DeviceId.compute(ds)
-            ops.append(Op(id=id_, kind=OpKind(self.op_kind(i)), node=dev.node, device=dev,
-                          dur=int(self.csr.dur[i])))
+            kind = OpKind(self.op_kind(i))
+            node = dev.peer if kind == OpKind.RECV else dev.node  # Op::node of a RECV: receiver
+            op = Op(id=id_, kind=kind, node=node, device=dev, dur=int(self.csr.dur[i]))
+            unit = N.lib.dpro_graph_comm_info(self.handle, i, C.byref(b))
+            if unit is not None:  # comm op: tensor unit, bytes, transaction
+                op.tensor, op.bytes, op.transaction = unit.decode(), int(b.value), id_[5:]
+            ops.append(op)
         so, su = self.csr.succ_off, self.csr.succ
         succs = [su[so[i]:so[i + 1]].tolist() for i in range(len(ids))]
         return GlobalDFG(ops, succs, {}, cluster or ClusterSpec())

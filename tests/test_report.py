@@ -61,3 +61,36 @@ def test_timeline_bytes_match_reference_cli_on_oracle_schedule(ref, port, scheme
     r.schedule = {op.id: ScheduleEntry(int(o["start"][i]), int(o["end"][i]), op.device)
                   for i, op in enumerate(g.ops())}
     assert timeline_text(g, r).encode() == ref.RefGraph.synth(sp).timeline_json()
+
+
+@pytest.mark.parametrize("scheme,W,S,L", SPECS)
+def test_native_timeline_writer_matches_reference(ref, port, tmp_path, scheme, W, S, L):
+    """dpro_graph_write_timeline (streamed, for 10^6+-op schedules) writes
+    the reference CLI's bytes; candidates built as host-merged deltas carry
+    the same comm metadata."""
+    from paper_2205_02473_b200.engine import Csr
+    from paper_2205_02473_b200.ingest import LayeredBase, layered_graph
+    sp = _spec(scheme, W, S, L, L + W)
+    m = LayeredModel(sp["fw_dur_us"], sp["bw_dur_us"], sp["tensor_bytes"], 5)
+    c = synth_cluster(scheme, W, S, 12500.0, 5.0)
+    ng = layered_graph(m, c)
+    o = port.port_replay(ng.csr)
+    path = tmp_path / "t.json"
+    ng.write_timeline(str(path), o["start"], o["end"])
+    assert path.read_bytes() == ref.RefGraph.synth(sp).timeline_json()
+    # a partition + fusion candidate (host-merged delta) against the Python
+    # writer on the same graph (which the reference pins above)
+    from paper_2205_02473_b200.replay import ScheduleEntry
+    base = LayeredBase(m, c)
+    groups = [[0, 1]] + [[i] for i in range(2, L)]
+    cand = base.candidates([(groups, [2] + [1] * (L - 2))])[0]
+    o2 = port.port_replay(cand.csr)
+    cand.write_timeline(str(path), o2["start"], o2["end"])
+    g = cand.to_global_dfg(c)
+
+    class R:
+        pass
+    r = R()
+    r.schedule = {op.id: ScheduleEntry(int(o2["start"][i]), int(o2["end"][i]), op.device)
+                  for i, op in enumerate(g.ops())}
+    assert path.read_text() == timeline_text(g, r)
