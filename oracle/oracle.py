@@ -73,6 +73,7 @@ def ref_lib():
             "ref_peak_node": (C.c_char_p, [_I32]),
             "ref_apply_memory_strategy": (_P, [_P, _I32, C.c_char_p, _P]),
             "ref_timeline_json": (_I64, [_P, _P, _I64, _P]),
+            "ref_search": (_I64, [_P, C.c_char_p, _P, _I64, _P]),
             "ref_memory_pass": (_P, [_P, _I64, C.c_char_p, _P, _P, _P, _P]),
             "ref_partial_replay": (_I32, [_P, C.c_char_p, _I32, _P]),
             "ref_tsync_graph": (_P, [C.c_char_p, _I64, _I32, _P]),
@@ -178,6 +179,16 @@ class RefGraph:
         h = self.lib.ref_apply_tensor_fusion(self.h, t1.encode(), t2.encode(), C.byref(st))
         _raise(self.lib, st.value)
         return RefGraph(h)
+
+    def search(self, options: dict) -> dict:
+        """dpro::search(g, options) -> {before_us, after_us, strategies}."""
+        st = C.c_int32(0)
+        o = json.dumps(options).encode()
+        n = self.lib.ref_search(self.h, o, None, 0, C.byref(st))
+        _raise(self.lib, st.value)
+        buf = C.create_string_buffer(n)
+        self.lib.ref_search(self.h, o, buf, n, C.byref(st))
+        return json.loads(buf.raw[:n].decode())
 
     def timeline_json(self) -> bytes:
         """The CLI's timeline.json bytes for replay(g) (dpro_main.cpp:90-116)."""

@@ -219,6 +219,39 @@ int64_t ref_timeline_json(void* hv, char* buf, int64_t cap, int32_t* status) {
   return static_cast<int64_t>(g_timeline.size());
 }
 
+// search(g, options) (optimize.cpp:1327-1650) -> {"before_us", "after_us",
+// "strategies": [Strategy::to_json()...]} as JSON text (checker for
+// search.reference_search).
+thread_local std::string g_search;
+int64_t ref_search(void* hv, const char* opts_json, char* buf, int64_t cap, int32_t* status) {
+  auto* h = static_cast<Handle*>(hv);
+  *status = guarded([&] {
+    const auto j = nlohmann::json::parse(opts_json);
+    SearchOptions o;
+    o.time_budget_s = j.value("time_budget_s", 30.0);
+    o.kmax = j.value("kmax", 16);
+    o.use_coarsen = j.value("use_coarsen", true);
+    o.use_symmetry = j.value("use_symmetry", true);
+    o.use_partial_replay = j.value("use_partial_replay", true);
+    o.use_theorems = j.value("use_theorems", true);
+    o.convergence_pct = j.value("convergence_pct", 0.5);
+    o.convergence_rounds = j.value("convergence_rounds", 5);
+    if (j.contains("passes"))
+      for (const auto& p : j["passes"]) o.passes.push_back(p.get<std::string>());
+    const SearchOutcome out = search(h->g, o);
+    nlohmann::json r;
+    r["before_us"] = out.strategies.before_us;
+    r["after_us"] = out.strategies.after_us;
+    r["strategies"] = nlohmann::json::array();
+    for (const auto& st : out.strategies.strategies) r["strategies"].push_back(st.to_json());
+    g_search = r.dump();
+  });
+  if (*status) return 0;
+  if (buf && cap >= static_cast<int64_t>(g_search.size()))
+    std::memcpy(buf, g_search.data(), g_search.size());
+  return static_cast<int64_t>(g_search.size());
+}
+
 // apply_strategy for the parameterless memory rewrites (kind 3 recompute,
 // 4 grad-accum), optimize.cpp:506-531.
 void* ref_apply_memory_strategy(void* h, int32_t kind, const char* meta_json,

@@ -16,6 +16,7 @@ from .replay import (CriticalPath, PathEntry, PathRun, ReplayResult, ScheduleEnt
 from .rewrite import (BudgetError, Strategy, StrategyKind, apply_grad_accum, apply_recompute,
                       memory_pass)
 from .report import timeline_json, timeline_text, write_timeline
+from .greedy import SearchOptions, SearchOutcome, reference_search
 from .memory import (ModelMeta, estimate_peak_memory, estimate_peak_memory_many,
                      output_bytes_for)
 
@@ -29,5 +30,6 @@ __all__ = [
     "MissingMetaError", "ParseError", "ModelMeta", "estimate_peak_memory",
     "estimate_peak_memory_many", "output_bytes_for", "TopologyError", "TransformError",
     "BudgetError", "Strategy", "StrategyKind", "apply_grad_accum", "apply_recompute",
-    "memory_pass", "timeline_json", "timeline_text", "write_timeline",
+    "memory_pass", "timeline_json", "timeline_text", "write_timeline", "SearchOptions",
+    "SearchOutcome", "reference_search",
 ]

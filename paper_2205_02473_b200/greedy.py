@@ -1,0 +1,358 @@
+"""The reference's own search driver (proj/src/optimize.cpp:1196-1650,
+Alg. 1: critical-path-guided greedy walk) with every replay, critical path
+and t_sync evaluated on the GPU.
+
+    SearchOptions             optimize.hpp:207-222
+    reference_search(g, opt)  search(), optimize.cpp:1327-1650
+
+Coarsening (optimize.cpp:580-684) and symmetry replication (686-813,
+1070-1168) are not ported: `use_coarsen` and `use_symmetry` must be False,
+the reference's own ablation switches. With them off, the same options give
+the same strategies, in the same order, with the same fused durations and
+the same before/after times as the reference (tests/test_greedy.py), since
+every decision depends only on bit-exact replays, critical paths and t_sync
+values. Registered (non-builtin) passes are not supported.
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+from .errors import Error
+from .graph import GlobalDFG, OpKind, is_computation
+from .memory import ModelMeta
+from .replay import critical_path, execution_graph, replay, sync_makespan
+from .rewrite import (CostModel, Strategy, StrategyKind, apply_strategy, apply_tensor_partition,
+                      fused_op_id, memory_pass)
+from .search import opt_part_num, should_fuse_ops, should_fuse_tensors
+
+
+@dataclass
+class SearchOptions:
+    """optimize.hpp:207-222 (coarsening / symmetry must stay off here)."""
+    time_budget_s: float = 30.0
+    memory_budget_bytes: int = 0
+    kmax: int = 16
+    use_coarsen: bool = False
+    use_symmetry: bool = False
+    use_partial_replay: bool = True
+    use_theorems: bool = True
+    passes: list[str] = field(default_factory=list)
+    cost: CostModel = field(default_factory=CostModel)
+    meta: ModelMeta = field(default_factory=ModelMeta)
+    convergence_pct: float = 0.5
+    convergence_rounds: int = 5
+
+
+@dataclass
+class SearchOutcome:
+    graph: GlobalDFG
+    strategies: list[Strategy]
+    before_us: int
+    after_us: int
+    search_wall_s: float = 0.0
+
+
+def _producers_of(g: GlobalDFG, base: str) -> dict[str, list[str]]:
+    """optimize.cpp:1197-1207: node -> ops producing `base`."""
+    out: dict[str, list[str]] = {}
+    for op in g.ops():
+        if not is_computation(op.kind):
+            continue
+        for t in op.produces:
+            if t == base:
+                out.setdefault(op.node, []).append(op.id)
+    return dict(sorted(out.items()))
+
+
+def _try_bundle(g: GlobalDFG, bundle: list[Strategy], opt: SearchOptions):
+    """optimize.cpp:1211-1227 (fills fused durations into the bundle)."""
+    cur = g
+    for s in bundle:
+        try:
+            cur = apply_strategy(cur, s, opt.cost, opt.meta)
+        except Error:
+            return None
+        if s.kind == StrategyKind.OP_FUSION and s.dur_us < 0:
+            s.dur_us = cur.op(fused_op_id(s.a, s.b)).dur
+    return cur
+
+
+def _append_pairing(g: GlobalDFG, base_a: str, base_b: str, walked_node: str,
+                    bundle: list[Strategy]) -> bool:
+    """optimize.cpp:1229-1262."""
+    pa_, pb_ = _producers_of(g, base_a), _producers_of(g, base_b)
+    for node in sorted(set(pa_) | set(pb_)):
+        if node == walked_node:
+            continue
+        if node not in pa_ or node not in pb_:
+            return False
+        if len(pa_[node]) != 1 or len(pb_[node]) != 1:
+            return False
+        a, b = pa_[node][0], pb_[node][0]
+        if a == b:
+            continue
+        if g.op(a).device.str() != g.op(b).device.str():
+            return False
+        if g.has_edge(a, b):
+            bundle.append(Strategy(StrategyKind.OP_FUSION, a, b, 1, -1))
+        elif g.has_edge(b, a):
+            bundle.append(Strategy(StrategyKind.OP_FUSION, b, a, 1, -1))
+        else:
+            return False
+    return True
+
+
+def _append_unpartitions(g: GlobalDFG, bases: list[str], bundle: list[Strategy]) -> None:
+    """optimize.cpp:1264-1272."""
+    for base in bases:
+        if g.has_base(base) and len(g.units_of_base(base)) > 1:
+            bundle.append(Strategy(StrategyKind.PARTITION, base, "", 1, -1))
+
+
+def _op_bases(op) -> list[str]:
+    out: list[str] = []
+    for t in op.produces:
+        if t not in out:
+            out.append(t)
+    return out
+
+
+def _strategy_key(s: Strategy) -> str:
+    return f"{s.kind}|{s.a}|{s.b}|{s.k}"
+
+
+class _Ctx:
+    """SearchCtx (optimize.cpp:1144-1168): memoized t_sync, time budget."""
+
+    def __init__(self, opt: SearchOptions, cluster):
+        self.opt, self.cluster = opt, cluster
+        self.cache: dict[tuple[int, int], int] = {}
+        self.started = time.monotonic()
+
+    def elapsed(self) -> float:
+        return time.monotonic() - self.started
+
+    def out_of_time(self) -> bool:
+        return self.elapsed() >= self.opt.time_budget_s
+
+    def sync(self, nbytes: int, k: int) -> int:
+        key = (int(nbytes), int(k))
+        if key not in self.cache:
+            self.cache[key] = sync_makespan(self.cluster, key[0], key[1])
+        return self.cache[key]
+
+
+def _finish_fusion_bundle(g: GlobalDFG, bundle: list[Strategy], bases: list[str], ctx: _Ctx):
+    """optimize.cpp:1277-1314."""
+    fused = bases[0]
+    for b in bases[1:]:
+        bundle.append(Strategy(StrategyKind.TENSOR_FUSION, fused, b, 1, -1))
+        fused += "+" + b
+    applied = _try_bundle(g, bundle, ctx.opt)
+    if applied is None:
+        return None
+    if not applied.has_base(fused):
+        return applied
+    nbytes = applied.base_bytes(fused)
+    best_k = 1
+    if ctx.opt.use_partial_replay:
+        best_k = opt_part_num(nbytes, ctx.opt.kmax, ctx.sync)
+    else:
+        cap = min(max(ctx.opt.kmax, 1), nbytes)
+        best = replay(applied).iteration_time_us
+        for k in range(2, cap + 1):
+            t = replay(apply_tensor_partition(applied, fused, k)).iteration_time_us
+            if t < best:
+                best, best_k = t, k
+    if best_k > 1:
+        part = Strategy(StrategyKind.PARTITION, fused, "", best_k, -1)
+        try:
+            applied = apply_strategy(applied, part, ctx.opt.cost, ctx.opt.meta)
+        except Error:
+            return None
+        bundle.append(part)
+    return applied
+
+
+def reference_search(g: GlobalDFG, opt: SearchOptions | None = None) -> SearchOutcome:
+    """search() of optimize.cpp:1327-1650 with use_coarsen = use_symmetry =
+    False."""
+    opt = opt or SearchOptions()
+    if opt.use_coarsen or opt.use_symmetry:
+        raise NotImplementedError("coarsening / symmetry replication are not ported")
+    builtin = ["op-fusion", "tensor-fusion", "partition", "memory"]
+    for name in opt.passes:
+        if name not in builtin:
+            raise Error(f"unknown pass: {name}")
+
+    def enabled(name: str) -> bool:
+        return not opt.passes or name in opt.passes
+
+    before = replay(g).iteration_time_us
+    out = SearchOutcome(g, [], before, before)
+    if opt.time_budget_s <= 0:
+        return out
+    ctx = _Ctx(opt, g.cluster())
+    graph = g
+    strategies: list[Strategy] = []
+    if opt.memory_budget_bytes > 0 and enabled("memory"):
+        graph = memory_pass(graph, opt.memory_budget_bytes, opt.meta, strategies)
+    current = replay(graph).iteration_time_us
+    seen: set[str] = set()
+
+    def gate(bundle, applied) -> bool:
+        nonlocal graph, current
+        if applied is None:
+            return False
+        t = replay(applied).iteration_time_us
+        if t >= current:
+            return False
+        graph, current = applied, t
+        strategies.extend(bundle)
+        seen.add(";".join(_strategy_key(s) for s in bundle) + ";")
+        return True
+
+    previous, flat, timed_out = current, 0, False
+    while not timed_out:
+        round_g = graph
+        round_res = replay(round_g)
+        path = critical_path(execution_graph(round_g, round_res), round_res)
+        accepted = 0
+
+        def attempt(bundle, applied):
+            nonlocal accepted
+            if gate(bundle, applied):
+                accepted += 1
+
+        if enabled("op-fusion"):  # computation runs, optimize.cpp:1410-1466
+            for run in path.runs:
+                if run.communication:
+                    continue
+                for i in range(len(run.ops) - 1):
+                    timed_out = ctx.out_of_time()
+                    if timed_out:
+                        break
+                    a, b = run.ops[i], run.ops[i + 1]
+                    if not graph.has_op(a) or not graph.has_op(b):
+                        continue
+                    pa, pb = graph.op(a), graph.op(b)
+                    if not is_computation(pa.kind) or not is_computation(pb.kind):
+                        continue
+                    if OpKind.UPDATE in (pa.kind, pb.kind):
+                        continue
+                    if pa.device.str() != pb.device.str() or not graph.has_edge(a, b):
+                        continue
+                    if opt.use_theorems:
+                        q_prev = 0
+                        if pa.produces:
+                            base = pa.produces[0]
+                            if not graph.has_base(base):
+                                continue
+                            q_prev = ctx.sync(graph.base_bytes(base),
+                                              len(graph.units_of_base(base)))
+                        if not should_fuse_ops(pa.dur, pb.dur, opt.cost.fused_dur_us(pa, pb),
+                                               q_prev):
+                            continue
+                    bases = _op_bases(pa)
+                    for base in _op_bases(pb):
+                        if base not in bases:
+                            bases.append(base)
+                    bundle: list[Strategy] = []
+                    _append_unpartitions(graph, bases, bundle)
+                    bundle.append(Strategy(StrategyKind.OP_FUSION, a, b, 1, -1))
+                    if pa.produces and pb.produces:
+                        if not enabled("tensor-fusion"):
+                            continue
+                        if not _append_pairing(graph, pa.produces[0], pb.produces[0], pa.node,
+                                               bundle):
+                            continue
+                    if len(bases) >= 2:
+                        attempt(bundle, _finish_fusion_bundle(graph, bundle, bases, ctx))
+                    else:
+                        attempt(bundle, _try_bundle(graph, bundle, opt))
+                if timed_out:
+                    break
+
+        def run_bases(runs):
+            order = []
+            for run in runs:
+                for oid in run.ops:
+                    op = round_g.op(oid)
+                    if not op.tensor or not round_g.has_tensor_unit(op.tensor):
+                        continue
+                    base = round_g.tensor_unit(op.tensor).base
+                    if base not in order:
+                        order.append(base)
+            return order
+
+        if enabled("tensor-fusion") and not timed_out:  # optimize.cpp:1468-1521
+            for run in path.runs:
+                if not run.communication:
+                    continue
+                order = run_bases([run])
+                for i in range(len(order) - 1):
+                    timed_out = ctx.out_of_time()
+                    if timed_out:
+                        break
+                    u, v = order[i], order[i + 1]
+                    if not graph.has_base(u) or not graph.has_base(v):
+                        continue
+                    if opt.use_theorems:
+                        q_prev_end = 0
+                        for name in round_g.units_of_base(u):
+                            for cid in round_g.tensor_unit(name).comm_ops:
+                                q_prev_end = max(q_prev_end, round_res.schedule[cid].end)
+                        p_cur_end = 0
+                        for ids in _producers_of(round_g, v).values():
+                            for oid in ids:
+                                p_cur_end = max(p_cur_end, round_res.schedule[oid].end)
+                        if not should_fuse_tensors(q_prev_end, p_cur_end, round_g.base_bytes(u),
+                                                   round_g.base_bytes(v), opt.kmax, ctx.sync):
+                            continue
+                    bundle = []
+                    _append_unpartitions(graph, [u, v], bundle)
+                    pairing: list[Strategy] = []
+                    if not _append_pairing(graph, u, v, "", pairing):
+                        continue
+                    if pairing and not enabled("op-fusion"):
+                        continue
+                    bundle += pairing
+                    attempt(bundle, _finish_fusion_bundle(graph, bundle, [u, v], ctx))
+                if timed_out:
+                    break
+
+        if enabled("partition") and not timed_out:  # optimize.cpp:1523-1561
+            for base in run_bases([r for r in path.runs if r.communication]):
+                timed_out = ctx.out_of_time()
+                if timed_out:
+                    break
+                if not graph.has_base(base):
+                    continue
+                nbytes = graph.base_bytes(base)
+                k_cur = len(graph.units_of_base(base))
+                k_best = k_cur
+                if opt.use_partial_replay:
+                    k_best = opt_part_num(nbytes, opt.kmax, ctx.sync)
+                else:
+                    cap = min(max(opt.kmax, 1), nbytes)
+                    best = current
+                    for k in range(1, cap + 1):
+                        if k == k_cur:
+                            continue
+                        t = replay(apply_tensor_partition(graph, base, k)).iteration_time_us
+                        if t < best:
+                            best, k_best = t, k
+                if k_best == k_cur:
+                    continue
+                bundle = [Strategy(StrategyKind.PARTITION, base, "", k_best, -1)]
+                attempt(bundle, _try_bundle(graph, bundle, opt))
+
+        if accepted == 0:
+            break
+        change = 100.0 * (previous - current) / previous if previous > 0 else 0.0
+        flat = flat + 1 if change < opt.convergence_pct else 0
+        previous = current
+        if flat >= opt.convergence_rounds:
+            break
+    return SearchOutcome(graph, strategies, before, current, ctx.elapsed())
