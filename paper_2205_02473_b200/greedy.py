@@ -5,36 +5,40 @@ and t_sync evaluated on the GPU.
     SearchOptions             optimize.hpp:207-222
     reference_search(g, opt)  search(), optimize.cpp:1327-1650
 
-Coarsening (optimize.cpp:580-684) and symmetry replication (686-813,
-1070-1168) are not ported: `use_coarsen` and `use_symmetry` must be False,
-the reference's own ablation switches. With them off, the same options give
-the same strategies, in the same order, with the same fused durations and
-the same before/after times as the reference (tests/test_greedy.py), since
-every decision depends only on bit-exact replays, critical paths and t_sync
-values. Registered (non-builtin) passes are not supported.
+    coarsen(g, cost)          optimize.cpp:580-684 (pre-fusion pass)
+    detect_symmetry(g)        optimize.cpp:686-813
+    symmetry replication      optimize.cpp:1070-1168, 1592-1621
+
+The same options give the same strategies, in the same order, with the
+same fused durations and the same before/after times as the reference
+(tests/test_greedy.py): every decision depends only on bit-exact replays,
+critical paths and t_sync values. Registered (non-builtin) passes are not
+supported.
 """
 from __future__ import annotations
 
 import time
+from collections import deque
 from dataclasses import dataclass, field
 
 from .errors import Error
 from .graph import GlobalDFG, OpKind, is_computation
 from .memory import ModelMeta
 from .replay import critical_path, execution_graph, replay, sync_makespan
-from .rewrite import (CostModel, Strategy, StrategyKind, apply_strategy, apply_tensor_partition,
-                      fused_op_id, memory_pass)
+from .rewrite import (CostModel, Strategy, StrategyKind, apply_op_fusion, apply_strategy,
+                      apply_tensor_fusion, apply_tensor_partition, fused_op_id, local_part,
+                      memory_pass, topo_order)
 from .search import opt_part_num, should_fuse_ops, should_fuse_tensors
 
 
 @dataclass
 class SearchOptions:
-    """optimize.hpp:207-222 (coarsening / symmetry must stay off here)."""
+    """optimize.hpp:207-222."""
     time_budget_s: float = 30.0
     memory_budget_bytes: int = 0
     kmax: int = 16
-    use_coarsen: bool = False
-    use_symmetry: bool = False
+    use_coarsen: bool = True
+    use_symmetry: bool = True
     use_partial_replay: bool = True
     use_theorems: bool = True
     passes: list[str] = field(default_factory=list)
@@ -175,12 +179,183 @@ def _finish_fusion_bundle(g: GlobalDFG, bundle: list[Strategy], bases: list[str]
     return applied
 
 
+def coarsen(g: GlobalDFG, cost: CostModel):
+    """optimize.cpp:580-662: (graph, applied strategies) of the backtracking
+    pre-fusion pass (the view's group tables are not needed by search)."""
+    graph, applied = g, []
+    merges = []
+    order = topo_order(g)
+    if order is not None:
+        for idx in reversed(order):
+            u = g.op_at(idx)
+            if not is_computation(u.kind) or u.kind == OpKind.UPDATE or u.produces:
+                continue
+            comp = [x for x in g.succs(u.id) if is_computation(g.op(x).kind)]
+            if len(comp) != 1:
+                continue
+            v = g.op(comp[0])
+            if v.kind == OpKind.UPDATE or u.device.str() != v.device.str():
+                continue
+            merges.append((u.id, v.id))
+    moved: dict[str, str] = {}
+    for uid, vid in merges:
+        cu, cv = moved.get(uid, uid), moved.get(vid, vid)
+        if cu == cv:
+            continue
+        try:
+            nxt = apply_op_fusion(graph, cu, cv, cost)
+        except Error:
+            continue
+        fid = fused_op_id(cu, cv)
+        applied.append(Strategy(StrategyKind.OP_FUSION, cu, cv, 1, nxt.op(fid).dur))
+        for k, v in list(moved.items()):
+            if v in (cu, cv):
+                moved[k] = fid
+        moved[uid] = moved[vid] = fid
+        graph = nxt
+    refused: set[tuple[str, str]] = set()
+    changed = True
+    while changed:  # fold multiple tensors of one producer into one unit
+        changed = False
+        for op in graph.ops():
+            if not is_computation(op.kind) or len(op.produces) < 2:
+                continue
+            t1, t2 = op.produces[0], op.produces[1]
+            if (t1, t2) in refused:
+                continue
+            try:
+                nxt = apply_tensor_fusion(graph, t1, t2)
+            except Error:
+                refused.add((t1, t2))
+                continue
+            applied.append(Strategy(StrategyKind.TENSOR_FUSION, t1, t2, 1, -1))
+            graph = nxt
+            changed = True
+            break
+    return graph, applied
+
+
+def _sig(g: GlobalDFG, op):
+    sizes = sorted(g.base_bytes(b) if g.has_base(b) else 0 for b in op.produces)
+    return (int(op.kind), int(op.dur), sizes)
+
+
+def _sig_match(a, b) -> bool:
+    if a[0] != b[0] or a[2] != b[2]:
+        return False
+    return abs(float(a[1] - b[1])) <= 0.01 * float(max(a[1], b[1])) + 1e-9
+
+
+def _produced_bases(g: GlobalDFG, ops) -> list[str]:
+    out: list[str] = []
+    for oid in ops:
+        for b in g.op(oid).produces:
+            if b not in out:
+                out.append(b)
+    return out
+
+
+def detect_symmetry(g: GlobalDFG) -> list[list[tuple[list[str], list[str]]]]:
+    """optimize.cpp:715-813: groups of segments (ops, tensors)."""
+    out = []
+    order = topo_order(g)
+    if order is None:
+        return out
+    chains: dict[str, list[str]] = {}
+    for idx in order:
+        op = g.op_at(idx)
+        if is_computation(op.kind):
+            chains.setdefault(op.node, []).append(op.id)
+    chains = dict(sorted(chains.items()))
+    sigs, sorted_ops = {}, {}
+    for node, ids in chains.items():  # worker replicas
+        by_local = sorted(ids, key=local_part)
+        sorted_ops[node] = by_local
+        sigs[node] = [_sig(g, g.op(i)) for i in by_local]
+    node_groups: list[list[str]] = []
+    for node, sig in sigs.items():
+        for grp in node_groups:
+            ref = sigs[grp[0]]
+            if len(ref) == len(sig) and all(_sig_match(x, y) for x, y in zip(ref, sig)):
+                grp.append(node)
+                break
+        else:
+            node_groups.append([node])
+    for grp in node_groups:
+        if len(grp) >= 2:
+            out.append([(sorted_ops[nd], _produced_bases(g, sorted_ops[nd])) for nd in grp])
+    if chains:  # periodic blocks tiling the first worker's chain
+        ids = next(iter(chains.values()))
+        n = len(ids)
+        items = [_sig(g, g.op(i)) for i in ids]
+        for w in range(1, n // 2 + 1):
+            if n % w:
+                continue
+            if all(_sig_match(items[j], items[b * w + j])
+                   for b in range(1, n // w) for j in range(w)):
+                out.append([(ids[b * w:(b + 1) * w], _produced_bases(g, ids[b * w:(b + 1) * w]))
+                            for b in range(n // w)])
+                break
+    return out
+
+
+def _symmetry_maps(groups):
+    """optimize.cpp:1080-1105: (op map, tensor map) per ordered segment pair."""
+    maps = []
+    for segs in groups:
+        for i, (fo, ft) in enumerate(segs):
+            for j, (to, tt) in enumerate(segs):
+                if i == j or len(fo) != len(to) or len(ft) != len(tt):
+                    continue
+                maps.append((dict(zip(fo, to)), dict(zip(ft, tt))))
+    return maps
+
+
+def _node_part(oid: str) -> str:
+    a = oid.find("->")
+    return "" if a < 0 else oid[:a]
+
+
+def _map_op_id(oid: str, m):
+    """optimize.cpp:1107-1126."""
+    node = _node_part(oid)
+    if not node:
+        return None
+    locals_, mapped_node = [], ""
+    for piece in local_part(oid).split("+"):
+        full = node + "->" + piece
+        target = m[0].get(full, full)
+        tnode = _node_part(target)
+        if not mapped_node:
+            mapped_node = tnode
+        elif mapped_node != tnode:
+            return None
+        locals_.append(local_part(target))
+    return mapped_node + "->" + "+".join(locals_)
+
+
+def _map_tensor(name: str, m) -> str:
+    return "+".join(m[1].get(p, p) for p in name.split("+"))
+
+
+def _map_strategy(s: Strategy, m):
+    """optimize.cpp:1136-1158."""
+    if s.kind == StrategyKind.OP_FUSION:
+        a, b = _map_op_id(s.a, m), _map_op_id(s.b, m)
+        if a is None or b is None:
+            return None
+        return Strategy(s.kind, a, b, s.k, -1)
+    if s.kind == StrategyKind.TENSOR_FUSION:
+        return Strategy(s.kind, _map_tensor(s.a, m), _map_tensor(s.b, m), s.k, s.dur_us)
+    if s.kind == StrategyKind.PARTITION:
+        return Strategy(s.kind, _map_tensor(s.a, m), s.b, s.k, s.dur_us)
+    return None
+
+
 def reference_search(g: GlobalDFG, opt: SearchOptions | None = None) -> SearchOutcome:
     """search() of optimize.cpp:1327-1650 with use_coarsen = use_symmetry =
     False."""
     opt = opt or SearchOptions()
-    if opt.use_coarsen or opt.use_symmetry:
-        raise NotImplementedError("coarsening / symmetry replication are not ported")
     builtin = ["op-fusion", "tensor-fusion", "partition", "memory"]
     for name in opt.passes:
         if name not in builtin:
@@ -199,6 +374,15 @@ def reference_search(g: GlobalDFG, opt: SearchOptions | None = None) -> SearchOu
     if opt.memory_budget_bytes > 0 and enabled("memory"):
         graph = memory_pass(graph, opt.memory_budget_bytes, opt.meta, strategies)
     current = replay(graph).iteration_time_us
+    if opt.use_coarsen and opt.memory_budget_bytes == 0 and enabled("op-fusion") and \
+            enabled("tensor-fusion"):
+        cg, applied = coarsen(graph, opt.cost)
+        if applied:
+            t = replay(cg).iteration_time_us
+            if t <= current:
+                graph, current = cg, t
+                strategies.extend(applied)
+    sym_maps = _symmetry_maps(detect_symmetry(graph)) if opt.use_symmetry else []
     seen: set[str] = set()
 
     def gate(bundle, applied) -> bool:
@@ -219,11 +403,14 @@ def reference_search(g: GlobalDFG, opt: SearchOptions | None = None) -> SearchOu
         round_res = replay(round_g)
         path = critical_path(execution_graph(round_g, round_res), round_res)
         accepted = 0
+        replication_queue: list[list[Strategy]] = []
 
         def attempt(bundle, applied):
             nonlocal accepted
             if gate(bundle, applied):
                 accepted += 1
+                replication_queue.append([Strategy(x.kind, x.a, x.b, x.k, x.dur_us)
+                                          for x in bundle])
 
         if enabled("op-fusion"):  # computation runs, optimize.cpp:1410-1466
             for run in path.runs:
@@ -347,6 +534,26 @@ def reference_search(g: GlobalDFG, opt: SearchOptions | None = None) -> SearchOu
                     continue
                 bundle = [Strategy(StrategyKind.PARTITION, base, "", k_best, -1)]
                 attempt(bundle, _try_bundle(graph, bundle, opt))
+
+        if sym_maps:  # replicate accepted bundles onto symmetric ops / tensors
+            queue = deque(replication_queue)
+            while queue and not timed_out:
+                bundle = queue.popleft()
+                for m in sym_maps:
+                    timed_out = ctx.out_of_time()
+                    if timed_out:
+                        break
+                    mapped = [_map_strategy(x, m) for x in bundle]
+                    if any(x is None for x in mapped):
+                        continue
+                    key = ";".join(_strategy_key(x) for x in mapped) + ";"
+                    if key in seen:
+                        continue
+                    seen.add(key)
+                    applied = _try_bundle(graph, mapped, opt)
+                    if gate(mapped, applied):
+                        accepted += 1
+                        queue.append(mapped)
 
         if accepted == 0:
             break

@@ -25,16 +25,21 @@ def _spec(scheme, W, S, L, bw, seed):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("scheme,W,S,L,bw,seed", CASES)
-@pytest.mark.parametrize("theorems", [True, False])
-def test_reference_search_matches_reference(engine, ref, scheme, W, S, L, bw, seed, theorems):
+@pytest.mark.parametrize("theorems,full", [(True, False), (False, False), (True, True),
+                                           (False, True)])
+def test_reference_search_matches_reference(engine, ref, scheme, W, S, L, bw, seed, theorems,
+                                            full):
+    """full: the reference's default options (coarsening + symmetry
+    replication on); else its ablation switches off."""
     from paper_2205_02473_b200.greedy import SearchOptions, reference_search
     sp = _spec(scheme, W, S, L, bw, seed)
     g = layered_global_dfg(LayeredModel(sp["fw_dur_us"], sp["bw_dur_us"], sp["tensor_bytes"], 5),
                            synth_cluster(scheme, W, S, bw, 5.0))
-    opts = {"time_budget_s": 600.0, "use_coarsen": False, "use_symmetry": False,
+    opts = {"time_budget_s": 600.0, "use_coarsen": full, "use_symmetry": full,
             "use_theorems": theorems, "kmax": 8}
     exp = ref.RefGraph.synth(sp).search(opts)
-    got = reference_search(g, SearchOptions(time_budget_s=600.0, use_theorems=theorems, kmax=8))
+    got = reference_search(g, SearchOptions(time_budget_s=600.0, use_theorems=theorems, kmax=8,
+                                            use_coarsen=full, use_symmetry=full))
     assert got.before_us == exp["before_us"]
     assert [{"kind": str(s.kind), "a": s.a, "b": s.b, "k": s.k, "dur_us": s.dur_us}
             for s in got.strategies] == exp["strategies"]
