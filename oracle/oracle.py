@@ -74,6 +74,8 @@ def ref_lib():
             "ref_apply_memory_strategy": (_P, [_P, _I32, C.c_char_p, _P]),
             "ref_timeline_json": (_I64, [_P, _P, _I64, _P]),
             "ref_search": (_I64, [_P, C.c_char_p, _P, _I64, _P]),
+            "ref_synth_bundle": (_I64, [C.c_char_p, _P, _I64, _P]),
+            "ref_ingest": (_P, [C.c_char_p, C.c_char_p, _P]),
             "ref_memory_pass": (_P, [_P, _I64, C.c_char_p, _P, _P, _P, _P]),
             "ref_partial_replay": (_I32, [_P, C.c_char_p, _I32, _P]),
             "ref_tsync_graph": (_P, [C.c_char_p, _I64, _I32, _P]),
@@ -149,6 +151,16 @@ class RefGraph:
         lib = ref_lib()
         st = C.c_int32(0)
         h = lib.ref_synth_graph(json.dumps(spec).encode(), C.byref(st))
+        _raise(lib, st.value)
+        return RefGraph(h)
+
+    @staticmethod
+    def ingest(bundle: dict, cluster_json: dict) -> "RefGraph":
+        """ingest_bundle on {events, deps} + a cluster (ClusterSpec JSON)."""
+        lib = ref_lib()
+        st = C.c_int32(0)
+        h = lib.ref_ingest(json.dumps(bundle).encode(), json.dumps(cluster_json).encode(),
+                           C.byref(st))
         _raise(lib, st.value)
         return RefGraph(h)
 
@@ -372,6 +384,18 @@ def port_peak_memory(ops, succ, start, end, meta: dict) -> dict:
             best = max(best, live)
         peak[node] = pers[node] + best
     return peak
+
+
+def ref_synth_bundle(spec: dict) -> dict:
+    """The reference generator's trace events + dependency spec (JSON)."""
+    lib = ref_lib()
+    st = C.c_int32(0)
+    o = json.dumps(spec).encode()
+    n = lib.ref_synth_bundle(o, None, 0, C.byref(st))
+    _raise(lib, st.value)
+    buf = C.create_string_buffer(n)
+    lib.ref_synth_bundle(o, buf, n, C.byref(st))
+    return json.loads(buf.raw[:n].decode())
 
 
 def ref_sync_makespan(cluster_json: dict, bytes_: int, k: int) -> int:

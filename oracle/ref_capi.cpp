@@ -252,6 +252,58 @@ int64_t ref_search(void* hv, const char* opts_json, char* buf, int64_t cap, int3
   return static_cast<int64_t>(g_search.size());
 }
 
+// The synthetic generator's trace bundle + dependency spec (gen_synthetic,
+// synth.cpp) as JSON, for checking ingest.ingest_bundle against the
+// reference's ingest_bundle (which ref_synth_graph runs on the same bundle).
+thread_local std::string g_bundle;
+int64_t ref_synth_bundle(const char* spec_json, char* buf, int64_t cap, int32_t* status) {
+  *status = guarded([&] {
+    const SynthSpec spec = SynthSpec::from_json(nlohmann::json::parse(spec_json));
+    const SynthResult r = gen_synthetic(spec);
+    nlohmann::json j;
+    j["events"] = nlohmann::json::array();
+    for (const auto& e : r.traces.events) {
+      j["events"].push_back({{"name", e.name}, {"node", e.node}, {"start", e.start},
+                             {"dur", e.dur}, {"kind", static_cast<int>(e.kind)},
+                             {"iteration", e.iteration}, {"tensor", e.tensor},
+                             {"bytes", e.bytes}, {"transaction", e.transaction}});
+    }
+    j["deps"] = r.deps.to_json();
+    g_bundle = j.dump();
+  });
+  if (*status) return 0;
+  if (buf && cap >= static_cast<int64_t>(g_bundle.size()))
+    std::memcpy(buf, g_bundle.data(), g_bundle.size());
+  return static_cast<int64_t>(g_bundle.size());
+}
+
+// ingest_bundle (ingest.cpp:452-493) on a bundle given as JSON: events as
+// ref_synth_bundle writes them, a DependencySpec, a ClusterSpec.
+void* ref_ingest(const char* bundle_json, const char* cluster_json, int32_t* status) {
+  Handle* out = nullptr;
+  *status = guarded([&] {
+    const auto j = nlohmann::json::parse(bundle_json);
+    TraceBundle tb;
+    for (const auto& e : j["events"]) {
+      TraceEvent ev;
+      ev.name = e["name"].get<std::string>();
+      ev.node = e["node"].get<std::string>();
+      ev.start = e.value("start", Us{0});
+      ev.dur = e.value("dur", Us{0});
+      ev.kind = static_cast<OpKind>(e.value("kind", 0));
+      ev.iteration = e.value("iteration", 0);
+      ev.tensor = e.value("tensor", std::string());
+      ev.bytes = e.value("bytes", std::int64_t{0});
+      ev.transaction = e.value("transaction", std::string());
+      tb.events.push_back(std::move(ev));
+    }
+    const DependencySpec deps = DependencySpec::from_json(j["deps"]);
+    const ClusterSpec cluster = ClusterSpec::from_json(nlohmann::json::parse(cluster_json));
+    out = wrap(ingest_bundle(tb, deps, cluster));
+  });
+  return out;
+}
+
 // apply_strategy for the parameterless memory rewrites (kind 3 recompute,
 // 4 grad-accum), optimize.cpp:506-531.
 void* ref_apply_memory_strategy(void* h, int32_t kind, const char* meta_json,

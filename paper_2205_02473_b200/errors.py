@@ -66,3 +66,11 @@ class SchemaError(Error):
 
 class SpliceError(Error):
     """dpro::SpliceError (errors.hpp:62-65)."""
+
+
+class UnknownSymbolError(Error):
+    """dpro::UnknownSymbolError (errors.hpp:48-53)."""
+
+    def __init__(self, symbol: str):
+        super().__init__(f"unknown symbol '{symbol}'")
+        self.symbol = symbol
