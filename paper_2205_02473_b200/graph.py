@@ -336,11 +336,14 @@ class GraphBuilder:
         self._edges: set[tuple[str, str]] = set()
         self._tensors: dict[str, TensorUnit] = {}
         self._cluster = ClusterSpec()
+        self._shared: set[str] = set()  # ops still shared with the source graph
         if g is not None:
-            import copy
             self._cluster = g.cluster()
+            # copy-on-write: GlobalDFG ops are immutable, so the builder shares
+            # them and copies one only when op(id) hands it out for mutation
             for op in g.ops():
-                self._ops[op.id] = copy.copy(op)
+                self._ops[op.id] = op
+            self._shared = set(self._ops)
             for i, ss in enumerate(g._succs):
                 for s in ss:
                     self._edges.add((g.op_at(i).id, g.op_at(s).id))
@@ -360,8 +363,14 @@ class GraphBuilder:
         return id_ in self._ops
 
     def op(self, id_: str) -> Op:
+        """The builder's op, mutable (GraphBuilder::op); a shared op is copied
+        first so the source graph is never changed."""
         if id_ not in self._ops:
             raise LookupError_(f"no op '{id_}' in builder")
+        if id_ in self._shared:
+            import copy
+            self._ops[id_] = copy.copy(self._ops[id_])
+            self._shared.discard(id_)
         return self._ops[id_]
 
     def remove_op(self, id_: str) -> None:
@@ -374,6 +383,7 @@ class GraphBuilder:
             if id_ not in self._ops:
                 raise LookupError_(f"no op '{id_}' to remove")
             del self._ops[id_]
+            self._shared.discard(id_)
             gone.add(id_)
         if gone:
             self._edges = {e for e in self._edges if e[0] not in gone and e[1] not in gone}

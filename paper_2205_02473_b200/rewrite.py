@@ -263,9 +263,7 @@ def apply_tensor_fusion(g: GlobalDFG, t1: str, t2: str) -> GlobalDFG:
             else:
                 produces.append(t)
         if touched:
-            c = copy.copy(bld.op(op.id))
-            c.produces = produces
-            bld._ops[op.id] = c  # noqa: SLF001 - GraphBuilder::op(id) mutation
+            bld.op(op.id).produces = produces  # copy-on-write in GraphBuilder.op
     return bld.build()
 
 
