@@ -273,6 +273,14 @@ class GlobalDFG:
     def edge_count(self) -> int:
         return self._edge_count
 
+    def edge_set(self) -> frozenset:
+        """All edges as (pred id, succ id) pairs (cached; the graph is immutable)."""
+        if getattr(self, "_edges", None) is None:
+            ids = [op.id for op in self._ops]
+            self._edges = frozenset((ids[a], ids[b]) for a, ss in enumerate(self._succs)
+                                    for b in ss)
+        return self._edges
+
     def cluster(self) -> ClusterSpec:
         return self._cluster
 
@@ -344,9 +352,7 @@ class GraphBuilder:
             for op in g.ops():
                 self._ops[op.id] = op
             self._shared = set(self._ops)
-            for i, ss in enumerate(g._succs):
-                for s in ss:
-                    self._edges.add((g.op_at(i).id, g.op_at(s).id))
+            self._edges = set(g.edge_set())
             self._tensors = dict(g.tensor_units())
 
     def set_cluster(self, c: ClusterSpec) -> None:
@@ -427,7 +433,9 @@ class GraphBuilder:
             succs[index[a]].append(index[b])
         for s in succs:
             s.sort()
-        return GlobalDFG([self._ops[k] for k in ids], succs, self._tensors, self._cluster)
+        g = GlobalDFG([self._ops[k] for k in ids], succs, self._tensors, self._cluster)
+        g._edges = frozenset(self._edges)  # edge_set() cache for the next builder
+        return g
 
 
 def comp(id_: str, dev: str, dur: int, kind: OpKind = OpKind.FW) -> Op:
