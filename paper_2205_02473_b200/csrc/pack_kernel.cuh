@@ -215,7 +215,10 @@ __device__ void coop_sizes(const Cand& c, const uint8_t* spl, uint32_t i0, uint3
 // unrolled by 2 with all loads of both halves issued first.
 __device__ void coop_lists(const Cand& c, const uint8_t* spl, uint32_t i0, uint32_t i1,
                            const uint32_t* xoff, const uint4* rec, uint4* erec, uint32_t* segp) {
-  constexpr int U = 2;
+#ifndef DPRO_LIST_U
+#define DPRO_LIST_U 2
+#endif
+  constexpr int U = DPRO_LIST_U;
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t me = min(i0 + lane, i1);
   const uint32_t off = c.succ_off[me];

@@ -17,6 +17,7 @@ supported.
 """
 from __future__ import annotations
 
+import os
 import time
 from collections import deque
 from dataclasses import dataclass, field
@@ -24,11 +25,19 @@ from dataclasses import dataclass, field
 from .errors import Error
 from .graph import GlobalDFG, OpKind, is_computation
 from .memory import ModelMeta
-from .replay import critical_path, execution_graph, replay, sync_makespan
+from .replay import critical_path, execution_graph, replay, replay_times, sync_makespan
 from .rewrite import (CostModel, Strategy, StrategyKind, apply_op_fusion, apply_strategy,
                       apply_tensor_fusion, apply_tensor_partition, fused_op_id, local_part,
                       memory_pass, topo_order)
 from .search import opt_part_num, should_fuse_ops, should_fuse_tensors
+
+# speculative gate batch width: starts at min, doubles while no candidate is
+# accepted, up to max. An acceptance discards the rest of the batch, so a wide
+# batch wastes candidate construction on walks that accept often. On the
+# 16-worker x 24-layer ring graph (390 acceptances, tools/greedy_speed.py,
+# B200) "1,1" ran 20.4 s, "1,16" 24.6 s, "4,64" 51.0 s: the default is
+# sequential makespan-only gates. DPRO_SPEC="min,max".
+_SPEC_MIN, _SPEC_MAX = (int(x) for x in os.environ.get("DPRO_SPEC", "1,1").split(","))
 
 
 @dataclass
@@ -405,61 +414,96 @@ def reference_search(g: GlobalDFG, opt: SearchOptions | None = None) -> SearchOu
         accepted = 0
         replication_queue: list[list[Strategy]] = []
 
-        def attempt(bundle, applied):
-            nonlocal accepted
-            if gate(bundle, applied):
-                accepted += 1
-                replication_queue.append([Strategy(x.kind, x.a, x.b, x.k, x.dur_us)
-                                          for x in bundle])
+        def accept(bundle, applied, t) -> None:
+            nonlocal graph, current, accepted
+            graph, current = applied, t
+            strategies.extend(bundle)
+            seen.add(";".join(_strategy_key(s) for s in bundle) + ";")
+            accepted += 1
+            replication_queue.append([Strategy(x.kind, x.a, x.b, x.k, x.dur_us)
+                                      for x in bundle])
+
+        def walk(items, make) -> bool:
+            """The sequential loop `for it in items: if out_of_time: break;
+            attempt(*make(it))`, with speculative batched gates: candidates
+            are built against the current graph and replayed in one GPU
+            launch, then gated in order. A rejection leaves the graph as it
+            was, so the candidates after it are still the ones the sequential
+            loop would build; after an acceptance they are discarded and the
+            walk resumes from the next item on the new graph. Same decisions,
+            same order; only the number of launches changes. Returns
+            timed_out."""
+            i, width = 0, _SPEC_MIN
+            while i < len(items):
+                pend, j, out = [], i, False
+                while j < len(items) and len(pend) < width:
+                    if ctx.out_of_time():
+                        out = True
+                        break
+                    r = make(items[j])
+                    if r is not None and r[1] is not None:
+                        pend.append((j, r[0], r[1]))
+                    j += 1
+                try:
+                    times = replay_times([c[2] for c in pend])
+                except Error:  # re-run one by one: errors surface in order
+                    times = [None] * len(pend)
+                hit = None
+                for (idx, bundle, applied), t in zip(pend, times):
+                    if t is None:  # raises the reference's replay error, in order
+                        t = replay(applied).iteration_time_us
+                    if t < current:
+                        accept(bundle, applied, t)
+                        hit = idx
+                        break
+                if hit is None:
+                    if out:
+                        return True
+                    i, width = j, min(2 * width, _SPEC_MAX)
+                else:
+                    i, width = hit + 1, _SPEC_MIN
+            return False
+
+        def make_opf(item):  # one step of optimize.cpp:1410-1466
+            a, b = item
+            if not graph.has_op(a) or not graph.has_op(b):
+                return None
+            pa, pb = graph.op(a), graph.op(b)
+            if not is_computation(pa.kind) or not is_computation(pb.kind):
+                return None
+            if OpKind.UPDATE in (pa.kind, pb.kind):
+                return None
+            if pa.device.str() != pb.device.str() or not graph.has_edge(a, b):
+                return None
+            if opt.use_theorems:
+                q_prev = 0
+                if pa.produces:
+                    base = pa.produces[0]
+                    if not graph.has_base(base):
+                        return None
+                    q_prev = ctx.sync(graph.base_bytes(base), len(graph.units_of_base(base)))
+                if not should_fuse_ops(pa.dur, pb.dur, opt.cost.fused_dur_us(pa, pb), q_prev):
+                    return None
+            bases = _op_bases(pa)
+            for base in _op_bases(pb):
+                if base not in bases:
+                    bases.append(base)
+            bundle: list[Strategy] = []
+            _append_unpartitions(graph, bases, bundle)
+            bundle.append(Strategy(StrategyKind.OP_FUSION, a, b, 1, -1))
+            if pa.produces and pb.produces:
+                if not enabled("tensor-fusion"):
+                    return None
+                if not _append_pairing(graph, pa.produces[0], pb.produces[0], pa.node, bundle):
+                    return None
+            if len(bases) >= 2:
+                return bundle, _finish_fusion_bundle(graph, bundle, bases, ctx)
+            return bundle, _try_bundle(graph, bundle, opt)
 
         if enabled("op-fusion"):  # computation runs, optimize.cpp:1410-1466
-            for run in path.runs:
-                if run.communication:
-                    continue
-                for i in range(len(run.ops) - 1):
-                    timed_out = ctx.out_of_time()
-                    if timed_out:
-                        break
-                    a, b = run.ops[i], run.ops[i + 1]
-                    if not graph.has_op(a) or not graph.has_op(b):
-                        continue
-                    pa, pb = graph.op(a), graph.op(b)
-                    if not is_computation(pa.kind) or not is_computation(pb.kind):
-                        continue
-                    if OpKind.UPDATE in (pa.kind, pb.kind):
-                        continue
-                    if pa.device.str() != pb.device.str() or not graph.has_edge(a, b):
-                        continue
-                    if opt.use_theorems:
-                        q_prev = 0
-                        if pa.produces:
-                            base = pa.produces[0]
-                            if not graph.has_base(base):
-                                continue
-                            q_prev = ctx.sync(graph.base_bytes(base),
-                                              len(graph.units_of_base(base)))
-                        if not should_fuse_ops(pa.dur, pb.dur, opt.cost.fused_dur_us(pa, pb),
-                                               q_prev):
-                            continue
-                    bases = _op_bases(pa)
-                    for base in _op_bases(pb):
-                        if base not in bases:
-                            bases.append(base)
-                    bundle: list[Strategy] = []
-                    _append_unpartitions(graph, bases, bundle)
-                    bundle.append(Strategy(StrategyKind.OP_FUSION, a, b, 1, -1))
-                    if pa.produces and pb.produces:
-                        if not enabled("tensor-fusion"):
-                            continue
-                        if not _append_pairing(graph, pa.produces[0], pb.produces[0], pa.node,
-                                               bundle):
-                            continue
-                    if len(bases) >= 2:
-                        attempt(bundle, _finish_fusion_bundle(graph, bundle, bases, ctx))
-                    else:
-                        attempt(bundle, _try_bundle(graph, bundle, opt))
-                if timed_out:
-                    break
+            items = [(run.ops[i], run.ops[i + 1]) for run in path.runs
+                     if not run.communication for i in range(len(run.ops) - 1)]
+            timed_out = walk(items, make_opf)
 
         def run_bases(runs):
             order = []
@@ -473,67 +517,65 @@ def reference_search(g: GlobalDFG, opt: SearchOptions | None = None) -> SearchOu
                         order.append(base)
             return order
 
+        def make_tf(item):  # one step of optimize.cpp:1468-1521
+            u, v = item
+            if not graph.has_base(u) or not graph.has_base(v):
+                return None
+            if opt.use_theorems:
+                q_prev_end = 0
+                for name in round_g.units_of_base(u):
+                    for cid in round_g.tensor_unit(name).comm_ops:
+                        q_prev_end = max(q_prev_end, round_res.schedule[cid].end)
+                p_cur_end = 0
+                for ids in _producers_of(round_g, v).values():
+                    for oid in ids:
+                        p_cur_end = max(p_cur_end, round_res.schedule[oid].end)
+                if not should_fuse_tensors(q_prev_end, p_cur_end, round_g.base_bytes(u),
+                                           round_g.base_bytes(v), opt.kmax, ctx.sync):
+                    return None
+            bundle = []
+            _append_unpartitions(graph, [u, v], bundle)
+            pairing: list[Strategy] = []
+            if not _append_pairing(graph, u, v, "", pairing):
+                return None
+            if pairing and not enabled("op-fusion"):
+                return None
+            bundle += pairing
+            return bundle, _finish_fusion_bundle(graph, bundle, [u, v], ctx)
+
         if enabled("tensor-fusion") and not timed_out:  # optimize.cpp:1468-1521
+            items = []
             for run in path.runs:
-                if not run.communication:
-                    continue
-                order = run_bases([run])
-                for i in range(len(order) - 1):
-                    timed_out = ctx.out_of_time()
-                    if timed_out:
-                        break
-                    u, v = order[i], order[i + 1]
-                    if not graph.has_base(u) or not graph.has_base(v):
-                        continue
-                    if opt.use_theorems:
-                        q_prev_end = 0
-                        for name in round_g.units_of_base(u):
-                            for cid in round_g.tensor_unit(name).comm_ops:
-                                q_prev_end = max(q_prev_end, round_res.schedule[cid].end)
-                        p_cur_end = 0
-                        for ids in _producers_of(round_g, v).values():
-                            for oid in ids:
-                                p_cur_end = max(p_cur_end, round_res.schedule[oid].end)
-                        if not should_fuse_tensors(q_prev_end, p_cur_end, round_g.base_bytes(u),
-                                                   round_g.base_bytes(v), opt.kmax, ctx.sync):
-                            continue
-                    bundle = []
-                    _append_unpartitions(graph, [u, v], bundle)
-                    pairing: list[Strategy] = []
-                    if not _append_pairing(graph, u, v, "", pairing):
-                        continue
-                    if pairing and not enabled("op-fusion"):
-                        continue
-                    bundle += pairing
-                    attempt(bundle, _finish_fusion_bundle(graph, bundle, [u, v], ctx))
-                if timed_out:
-                    break
+                if run.communication:
+                    order = run_bases([run])
+                    items += [(order[i], order[i + 1]) for i in range(len(order) - 1)]
+            timed_out = walk(items, make_tf)
+
+        def make_part(base):  # one step of optimize.cpp:1523-1561
+            if not graph.has_base(base):
+                return None
+            nbytes = graph.base_bytes(base)
+            k_cur = len(graph.units_of_base(base))
+            k_best = k_cur
+            if opt.use_partial_replay:
+                k_best = opt_part_num(nbytes, opt.kmax, ctx.sync)
+            else:  # every k of the sweep in one batched launch
+                cap = min(max(opt.kmax, 1), nbytes)
+                ks = [k for k in range(1, cap + 1) if k != k_cur]
+                gs = [apply_tensor_partition(graph, base, k) for k in ks]
+                best = current
+                for k, gk, t in zip(ks, gs, replay_times(gs)):
+                    if t is None:
+                        t = replay(gk).iteration_time_us
+                    if t < best:
+                        best, k_best = t, k
+            if k_best == k_cur:
+                return None
+            bundle = [Strategy(StrategyKind.PARTITION, base, "", k_best, -1)]
+            return bundle, _try_bundle(graph, bundle, opt)
 
         if enabled("partition") and not timed_out:  # optimize.cpp:1523-1561
-            for base in run_bases([r for r in path.runs if r.communication]):
-                timed_out = ctx.out_of_time()
-                if timed_out:
-                    break
-                if not graph.has_base(base):
-                    continue
-                nbytes = graph.base_bytes(base)
-                k_cur = len(graph.units_of_base(base))
-                k_best = k_cur
-                if opt.use_partial_replay:
-                    k_best = opt_part_num(nbytes, opt.kmax, ctx.sync)
-                else:
-                    cap = min(max(opt.kmax, 1), nbytes)
-                    best = current
-                    for k in range(1, cap + 1):
-                        if k == k_cur:
-                            continue
-                        t = replay(apply_tensor_partition(graph, base, k)).iteration_time_us
-                        if t < best:
-                            best, k_best = t, k
-                if k_best == k_cur:
-                    continue
-                bundle = [Strategy(StrategyKind.PARTITION, base, "", k_best, -1)]
-                attempt(bundle, _try_bundle(graph, bundle, opt))
+            timed_out = walk(run_bases([r for r in path.runs if r.communication]), make_part)
 
         if sym_maps:  # replicate accepted bundles onto symmetric ops / tensors
             queue = deque(replication_queue)

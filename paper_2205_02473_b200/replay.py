@@ -108,6 +108,19 @@ def replay_many(graphs: Sequence[GlobalDFG], engine=None) -> list[ReplayResult]:
     return out
 
 
+def replay_times(graphs: Sequence[GlobalDFG], engine=None) -> list[int | None]:
+    """Iteration times of several graphs from ONE makespan-only batched
+    launch. A graph whose replay fails gives None: replay(g) on it raises the
+    reference's error, so callers that must fail in order re-run it there."""
+    if not graphs:
+        return []
+    eng = engine or default_engine()
+    batch = eng.batch([Csr.from_dict(g.to_csr()) for g in graphs])
+    batch.replay(want_schedule=False)
+    ms, st, _, _, _ = batch.results(schedule=False)
+    return [int(ms[i]) if int(st[i]) == N.DPRO_OK else None for i in range(len(graphs))]
+
+
 def replay(g: GlobalDFG) -> ReplayResult:
     """dpro::replay (replay.hpp:40-48)."""
     return replay_many([g])[0]

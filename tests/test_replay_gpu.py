@@ -190,6 +190,26 @@ def test_cycles_and_unset_durations_raise():
         replay(b.build())
 
 
+def test_replay_times_matches_replay_and_marks_failures():
+    """The makespan-only batch the greedy driver gates with (greedy.walk)."""
+    from paper_2205_02473_b200.replay import replay_times
+    rng = np.random.default_rng(77)
+    graphs = [random_dag_ref(rng) for _ in range(50)]
+    b = GraphBuilder()
+    b.add_op(comp("a", "A", 1)); b.add_op(comp("b", "A", 1))
+    b.add_edge("a", "b"); b.add_edge("b", "a")
+    graphs.insert(7, b.build())
+    b = GraphBuilder()
+    b.add_op(comp("a", "A", -1))
+    graphs.insert(20, b.build())
+    times = replay_times(graphs)
+    assert times[7] is None and times[20] is None
+    for i, (g, t) in enumerate(zip(graphs, times)):
+        if i not in (7, 20):
+            assert t == replay(g).iteration_time_us
+    assert replay_times([]) == []
+
+
 def test_deterministic_and_critical_path_sums_to_T():
     rng = np.random.default_rng(1234)
     graphs = [random_dag_ref(rng) for _ in range(100)]
