@@ -211,23 +211,52 @@ def base_of_unit_name(name: str) -> str:
 # --------------------------------------------------------------------------
 # GlobalDFG / GraphBuilder (graph.hpp:106-202)
 # --------------------------------------------------------------------------
+class _CsrLists:
+    """Per-op index lists held as one CSR (flat, off): list i is sliced out
+    on access, so building a graph creates no per-op lists."""
+    __slots__ = ("flat_np", "off_np", "flat", "off")
+
+    def __init__(self, flat: np.ndarray, off: np.ndarray):
+        self.flat_np, self.off_np = flat, off
+        self.flat, self.off = flat.tolist(), off.tolist()
+
+    def __getitem__(self, i: int) -> list[int]:
+        return self.flat[self.off[i]:self.off[i + 1]]
+
+    def __len__(self) -> int:
+        return len(self.off) - 1
+
+    def __iter__(self):
+        fl, o = self.flat, self.off
+        return (fl[o[i]:o[i + 1]] for i in range(len(o) - 1))
+
+
 class GlobalDFG:
     """Immutable graph: ops sorted by id, ascending pred/succ index lists."""
 
     def __init__(self, ops: list[Op], succs: list[list[int]],
-                 tensors: dict[str, TensorUnit], cluster: ClusterSpec):
+                 tensors: dict[str, TensorUnit], cluster: ClusterSpec,
+                 index: dict[str, int] | None = None, edge_count: int | None = None):
         self._ops = ops
-        self._index = {op.id: i for i, op in enumerate(ops)}
+        self._index = index if index is not None else {op.id: i for i, op in enumerate(ops)}
         self._succs = succs
-        preds: list[list[int]] = [[] for _ in ops]
-        for a, ss in enumerate(succs):
-            for b in ss:
-                preds[b].append(a)
-        self._preds = preds
-        self._edge_count = sum(len(s) for s in succs)
+        self._preds_cache: list[list[int]] | None = None  # built on first use
+        self._edge_count = (edge_count if edge_count is not None
+                            else sum(len(s) for s in succs))
         self._tensors = dict(sorted(tensors.items()))
         self._cluster = cluster
         self._csr = None
+
+    @property
+    def _preds(self) -> list[list[int]]:
+        # ascending: successors are visited in index order
+        if self._preds_cache is None:
+            preds: list[list[int]] = [[] for _ in self._ops]
+            for a, ss in enumerate(self._succs):
+                for b in ss:
+                    preds[b].append(a)
+            self._preds_cache = preds
+        return self._preds_cache
 
     def size(self) -> int:
         return len(self._ops)
@@ -325,11 +354,16 @@ class GlobalDFG:
             flags = np.fromiter(
                 ((1 if is_virtual(op.kind) else 0) | (2 if is_communication(op.kind) else 0)
                  for op in self._ops), np.uint8, n)
-            succ_off = np.zeros(n + 1, np.uint32)
-            succ_off[1:] = np.cumsum([len(s) for s in self._succs], dtype=np.uint64)
-            succ = np.fromiter((s for ss in self._succs for s in ss), np.uint32,
-                               self._edge_count)
-            indeg = np.fromiter((len(p) for p in self._preds), np.uint32, n)
+            if isinstance(self._succs, _CsrLists):
+                succ_off = self._succs.off_np.astype(np.uint32)
+                succ = self._succs.flat_np.astype(np.uint32)
+                indeg = np.bincount(succ, minlength=n).astype(np.uint32)
+            else:
+                succ_off = np.zeros(n + 1, np.uint32)
+                succ_off[1:] = np.cumsum([len(s) for s in self._succs], dtype=np.uint64)
+                succ = np.fromiter((s for ss in self._succs for s in ss), np.uint32,
+                                   self._edge_count)
+                indeg = np.fromiter((len(p) for p in self._preds), np.uint32, n)
             self._csr = {"dur": dur, "dev": dev, "flags": flags, "succ_off": succ_off,
                          "succ": succ, "indeg": indeg, "devices": devs,
                          "n_devices": len(devs)}
@@ -345,6 +379,7 @@ class GraphBuilder:
         self._tensors: dict[str, TensorUnit] = {}
         self._cluster = ClusterSpec()
         self._shared: set[str] = set()  # ops still shared with the source graph
+        self._src_ids: list[str] | None = None  # the source graph's op order
         if g is not None:
             self._cluster = g.cluster()
             # copy-on-write: GlobalDFG ops are immutable, so the builder shares
@@ -352,6 +387,7 @@ class GraphBuilder:
             for op in g.ops():
                 self._ops[op.id] = op
             self._shared = set(self._ops)
+            self._src_ids = list(self._ops)  # sorted: build() merges added ids into it
             self._edges = set(g.edge_set())
             self._tensors = dict(g.tensor_units())
 
@@ -426,14 +462,34 @@ class GraphBuilder:
         self._tensors[unit.name] = unit
 
     def build(self) -> GlobalDFG:
-        ids = sorted(self._ops)  # std::map order == byte order for str
+        ops = self._ops
+        if self._src_ids is not None:
+            # the source's order minus removed ops, then the added ids:
+            # two sorted runs, which sort() merges in linear time
+            src = self._src_ids
+            ids = [k for k in src if k in ops]
+            if len(ids) != len(ops):
+                kept = set(ids)
+                ids += sorted(k for k in ops if k not in kept)
+                ids.sort()
+        else:
+            ids = sorted(ops)  # std::map order == byte order for str
         index = {k: i for i, k in enumerate(ids)}
-        succs: list[list[int]] = [[] for _ in ids]
-        for a, b in self._edges:
-            succs[index[a]].append(index[b])
-        for s in succs:
-            s.sort()
-        g = GlobalDFG([self._ops[k] for k in ids], succs, self._tensors, self._cluster)
+        n, m = len(ids), len(self._edges)
+        if m:
+            # edges -> (tail, head) indices with C-level lookups, one sort of
+            # tail * n + head, then ascending per-op lists sliced out of it
+            heads, tails = zip(*self._edges)
+            key = np.fromiter(map(index.__getitem__, heads), np.int64, m) * n
+            key += np.fromiter(map(index.__getitem__, tails), np.int64, m)
+            key.sort()
+            off = np.zeros(n + 1, np.int64)
+            np.cumsum(np.bincount(key // n, minlength=n), out=off[1:])
+            succs = _CsrLists(key % n, off)
+        else:
+            succs = [[] for _ in ids]
+        g = GlobalDFG([ops[k] for k in ids], succs, self._tensors, self._cluster, index,
+                      len(self._edges))
         g._edges = frozenset(self._edges)  # edge_set() cache for the next builder
         return g
 
