@@ -284,9 +284,6 @@ struct FastWarp {
         // loads back to back, then applies them (edge() has atomics, so the
         // compiler would otherwise serialize load -> apply -> next load)
         for (uint32_t base = 0; base < total; base += NT * kMlp) {
-          // warp-uniform: no item left for this warp's lanes (e.g. warps 2-3
-          // of a 4-warp CTA in a round of <= 64 records) -- skip the search
-          if (base + (static_cast<uint32_t>(tid) & ~31u) >= total) break;
           uint4 a[kMlp];
 #pragma unroll
           for (int b = 0; b < kMlp; ++b) {
