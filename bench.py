@@ -114,28 +114,40 @@ def build_candidates(config: int, batch: int, rank: int, threads: int):
     return w, graphs
 
 
-def cpu_reference_time(graphs, budget_s: float, threads: int):
+def ref_graphs(graphs, threads: int):
+    """The reference's own graph objects (oracle/_ref) for the bounded
+    sample, built once per run; None when the reference library is absent."""
+    from oracle import oracle
+    if not oracle.ref_available():
+        return None
+    sample = graphs[: max(threads * 2, 8)]
+    refs = []
+    for g in sample:
+        devs = g.device_strs()
+        ids = g.op_ids()
+        ops = []
+        for i, id_ in enumerate(ids):
+            ds = devs[int(g.csr.dev[i])]
+            if ">" in ds:
+                a, b = ds.split(">", 1)
+                dk, dn, dp = 1, a, b
+            else:
+                dk, dn, dp = 0, ds, ""
+            ops.append((id_, g.op_kind(i), dk, dn, dp, int(g.csr.dur[i])))
+        so, su = g.csr.succ_off, g.csr.succ
+        edges = [(ids[i], ids[int(s)]) for i in range(len(ids)) for s in su[so[i]:so[i + 1]]]
+        refs.append(oracle.RefGraph.from_ops(ops, edges))
+    return refs
+
+
+def cpu_reference_time(graphs, budget_s: float, threads: int, refs=None):
     """Times the reference replay() (oracle/_ref) on a bounded sample; falls
     back to the C port when the reference library is absent."""
     from oracle import oracle
     sample = graphs[: max(threads * 2, 8)]
-    if oracle.ref_available():
-        refs = []
-        for g in sample:
-            devs = g.device_strs()
-            ids = g.op_ids()
-            ops = []
-            for i, id_ in enumerate(ids):
-                ds = devs[int(g.csr.dev[i])]
-                if ">" in ds:
-                    a, b = ds.split(">", 1)
-                    dk, dn, dp = 1, a, b
-                else:
-                    dk, dn, dp = 0, ds, ""
-                ops.append((id_, g.op_kind(i), dk, dn, dp, int(g.csr.dur[i])))
-            so, su = g.csr.succ_off, g.csr.succ
-            edges = [(ids[i], ids[int(s)]) for i in range(len(ids)) for s in su[so[i]:so[i + 1]]]
-            refs.append(oracle.RefGraph.from_ops(ops, edges))
+    if refs is None:
+        refs = ref_graphs(graphs, threads)
+    if refs is not None:
         # calibrate: one round of len(refs) replays, then size to the budget
         sec, _ = oracle.ref_replay_bench(refs, len(refs), threads)
         per = sec / len(refs)
@@ -165,8 +177,9 @@ def run_reference(args) -> None:
     vals = []
     cpu = None
     per_step = min(args.ref_seconds, 150.0 / max(1, args.warmup + args.steps))
+    refs = ref_graphs(graphs, threads)  # once: the steps time only replay()
     for step in range(args.warmup + args.steps):
-        cpu = cpu_reference_time(graphs, budget_s=per_step, threads=threads)
+        cpu = cpu_reference_time(graphs, budget_s=per_step, threads=threads, refs=refs)
         if step >= args.warmup:
             vals.append(cpu["value"])
     value = float(np.mean(vals))
