@@ -207,7 +207,8 @@ typedef struct dpro_delta {
   const uint32_t* new_succ;      /* final indices, ascending per op         */
   uint32_t n_extra;
   const uint32_t* extra_src;     /* [n_extra] kept base index, ascending    */
-  const uint32_t* extra_dst;     /* [n_extra] final index, ascending per src */
+  const uint32_t* extra_dst;     /* [n_extra] final index, ascending per src;
+                                    never a kept, uncut base successor of src */
   uint32_t n_cut;
   const uint32_t* cut;           /* [n_cut] ascending positions in the base
                                     succ[] of dropped edges between kept ops */
@@ -329,6 +330,27 @@ int dpro_base_delta_batch_ops(const dpro_base* base, int32_t n,
                               const int32_t* group_k, const uint8_t* fw_join,
                               const uint8_t* bw_join, int32_t threads,
                               dpro_delta_set** out);
+/* As dpro_base_delta_batch_ops, with the op-fusion joins of candidate c
+ * applied on ONE worker, join_worker[c] (ordinal among the workers, see
+ * dpro_base_worker; -1 = every worker). A single-worker join is the
+ * reference's own op-fusion candidate: apply_op_fusion(g, a, b) on two
+ * adjacent ops of one node (optimize.cpp:245-318, 1424-1432). NULL
+ * join_worker = every worker. */
+int dpro_base_delta_batch_ex(const dpro_base* base, int32_t n,
+                             const int32_t* n_groups, const int64_t* spec_off,
+                             const int32_t* group_off, const int32_t* members,
+                             const int32_t* group_k, const uint8_t* fw_join,
+                             const uint8_t* bw_join, const int32_t* join_worker,
+                             int32_t threads, dpro_delta_set** out);
+/* Name of the k-th worker of the base's cluster (NULL when out of range). */
+const char* dpro_base_worker(const dpro_base* base, int32_t k);
+/* Any n graphs (e.g. recompute / grad-accum variants from
+ * dpro_graph_layered_variant) as deltas against the base: ops are matched
+ * by id (kept when id, kind, duration and device agree), kept ops'
+ * successor lists are diffed into extra and cut edges. Merging a delta
+ * reproduces the graph's own CSR exactly. */
+int dpro_base_delta_from_graphs(const dpro_base* base, const dpro_graph* const* graphs,
+                                int32_t n, int32_t threads, dpro_delta_set** out);
 int dpro_graph_from_base_batch_ops(const dpro_base* base, int32_t n,
                                    const int32_t* n_groups, const int64_t* spec_off,
                                    const int32_t* group_off, const int32_t* members,

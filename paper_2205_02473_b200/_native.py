@@ -105,6 +105,9 @@ SIGNATURES = {
     "dpro_cuda_replay_delta_batch": (C.c_int, [_P, _P, _P, _I32, _P, _P, _P]),
     "dpro_base_delta_batch": (C.c_int, [_P, _I32, _P, _P, _P, _P, _P, _I32, _P]),
     "dpro_base_delta_batch_ops": (C.c_int, [_P, _I32, _P, _P, _P, _P, _P, _P, _P, _I32, _P]),
+    "dpro_base_delta_batch_ex": (C.c_int, [_P, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _P]),
+    "dpro_base_worker": (C.c_char_p, [_P, _I32]),
+    "dpro_base_delta_from_graphs": (C.c_int, [_P, _P, _I32, _I32, _P]),
     "dpro_graph_from_base_batch_ops": (C.c_int, [_P, _I32, _P, _P, _P, _P, _P, _P, _P, _I32, _P]),
     "dpro_delta_set_deltas": (_P, [_P]),
     "dpro_delta_set_size": (_I32, [_P]),

@@ -377,6 +377,8 @@ struct Groups {
   // with the default cost model): fw_join[i] fuses FW.l<i> with FW.l<i+1>,
   // bw_join[i] fuses BW.l<i+1> with BW.l<i>; empty = none
   std::vector<uint8_t> fw_join, bw_join;
+  // the joins apply to this worker only (node index); -1 = every worker
+  int join_worker = -1;
 };
 
 // Creation indices of the structural ops of a layered build (for delta
@@ -725,7 +727,7 @@ void prepare_delta(const BaseData& B, const Groups& G, DeltaParts& P) {
       xr[w][i] = kBaseRef | B.fw[w][i];
       yr[w][i] = kBaseRef | B.bw[w][i];
     }
-    if (!opf) continue;
+    if (!opf || (G.join_worker >= 0 && w != G.join_worker)) continue;
     const std::string& node = B.c.nodes[w];
     const uint32_t dv = g.device(0, w, -1);
     for (int a = 0; a < L;) {  // FW runs, fused left to right
@@ -993,7 +995,7 @@ dpro_graph* build_delta(const std::shared_ptr<BaseData>& Bp, const Groups& G) {
 // same candidate build_delta() merges on the host, left unmerged for the
 // engine to merge next to the resident base graph in HBM.
 struct DeltaHost {
-  std::vector<uint32_t> removed, new_pos, new_succ_off, new_succ, extra_src, extra_dst;
+  std::vector<uint32_t> removed, new_pos, new_succ_off, new_succ, extra_src, extra_dst, cut;
   std::vector<int64_t> new_dur;
   std::vector<uint16_t> new_dev;
   std::vector<uint8_t> new_flags;
@@ -1303,13 +1305,15 @@ struct dpro_delta_set {
   std::shared_ptr<BaseData> base;
   std::vector<DeltaHost> d;
   std::vector<dpro_delta> views;
+  void fill_views();
 };
 
-int dpro_base_delta_batch_ops(const dpro_base* base, int32_t n, const int32_t* n_groups,
-                              const int64_t* spec_off, const int32_t* group_off,
-                              const int32_t* members, const int32_t* group_k,
-                              const uint8_t* fw_join, const uint8_t* bw_join, int32_t threads,
-                              dpro_delta_set** out) {
+int dpro_base_delta_batch_ex(const dpro_base* base, int32_t n, const int32_t* n_groups,
+                             const int64_t* spec_off, const int32_t* group_off,
+                             const int32_t* members, const int32_t* group_k,
+                             const uint8_t* fw_join, const uint8_t* bw_join,
+                             const int32_t* join_worker, int32_t threads,
+                             dpro_delta_set** out) {
   const int L = base ? base->b->L : 0;
   if (!base || !out || n < 0) return DPRO_EINVAL;
   *out = nullptr;
@@ -1331,6 +1335,11 @@ int dpro_base_delta_batch_ops(const dpro_base* base, int32_t n, const int32_t* n
         }
         if (fw_join && L > 1) G.fw_join.assign(fw_join + size_t(i) * (L - 1), fw_join + size_t(i + 1) * (L - 1));
         if (bw_join && L > 1) G.bw_join.assign(bw_join + size_t(i) * (L - 1), bw_join + size_t(i + 1) * (L - 1));
+        if (join_worker && join_worker[i] >= 0) {
+          if (join_worker[i] >= static_cast<int32_t>(base->b->workers.size()))
+            throw std::runtime_error("join_worker out of range");
+          G.join_worker = base->b->workers[join_worker[i]];
+        }
         emit_delta(*base->b, G, set->d[i]);
       } catch (const std::exception& e) {
         st[i] = DPRO_EINVAL;
@@ -1348,10 +1357,25 @@ int dpro_base_delta_batch_ops(const dpro_base* base, int32_t n, const int32_t* n
         if (!e.empty()) g_gen_err = e;
       return st[i];
     }
-  set->views.resize(n);
-  for (int32_t i = 0; i < n; ++i) {
-    const DeltaHost& D = set->d[i];
-    dpro_delta& v = set->views[i];
+  set->fill_views();
+  *out = set.release();
+  return DPRO_OK;
+}
+
+int dpro_base_delta_batch_ops(const dpro_base* base, int32_t n, const int32_t* n_groups,
+                              const int64_t* spec_off, const int32_t* group_off,
+                              const int32_t* members, const int32_t* group_k,
+                              const uint8_t* fw_join, const uint8_t* bw_join, int32_t threads,
+                              dpro_delta_set** out) {
+  return dpro_base_delta_batch_ex(base, n, n_groups, spec_off, group_off, members, group_k,
+                                  fw_join, bw_join, nullptr, threads, out);
+}
+
+void dpro_delta_set::fill_views() {
+  views.resize(d.size());
+  for (size_t i = 0; i < d.size(); ++i) {
+    const DeltaHost& D = d[i];
+    dpro_delta& v = views[i];
     std::memset(&v, 0, sizeof v);
     v.n_devices = D.n_devices;
     v.n_removed = static_cast<uint32_t>(D.removed.size());
@@ -1366,9 +1390,162 @@ int dpro_base_delta_batch_ops(const dpro_base* base, int32_t n, const int32_t* n
     v.n_extra = static_cast<uint32_t>(D.extra_src.size());
     v.extra_src = D.extra_src.data();
     v.extra_dst = D.extra_dst.data();
+    v.n_cut = static_cast<uint32_t>(D.cut.size());
+    v.cut = D.cut.data();
   }
+}
+
+// A generated graph (any rewrite: recompute, grad-accum, fusion, partition,
+// ...) as a delta against the base: both graphs are index-ordered by op id,
+// so one merge walk over the ids splits the ops into kept (same id, kind,
+// duration and device), removed and new; kept ops' successor lists are
+// diffed into extra and cut edges. Final indices equal the candidate's own
+// indices (tested: the engine's merge reproduces the candidate CSR).
+namespace {
+void delta_from_graph(const BaseData& B, const dpro_graph& g, DeltaHost& D) {
+  const dpro_graph& bg = *B.g;
+  const uint32_t nb = static_cast<uint32_t>(bg.kind.size());
+  const uint32_t nc = static_cast<uint32_t>(g.kind.size());
+  std::unordered_map<std::string, uint16_t> bdev;
+  for (size_t d = 0; d < bg.device_strs.size(); ++d)
+    bdev.emplace(bg.device_strs[d], static_cast<uint16_t>(d));
+  std::vector<uint16_t> cdev(g.device_strs.size());
+  D.extra_dev_strs.clear();
+  uint32_t nd = static_cast<uint32_t>(bg.device_strs.size());
+  for (size_t d = 0; d < g.device_strs.size(); ++d) {
+    const auto it = bdev.find(g.device_strs[d]);
+    if (it != bdev.end()) {
+      cdev[d] = it->second;
+    } else {
+      if (nd >= 65535) throw std::runtime_error("more than 65535 devices");
+      cdev[d] = static_cast<uint16_t>(nd++);
+      D.extra_dev_strs.push_back(g.device_strs[d]);
+    }
+  }
+  D.n_devices = nd;
+  auto bid = [&](uint32_t b) -> const std::string& { return bg.ids[b]; };
+  auto cid = [&](uint32_t x) -> const char* { return dpro_graph_op_id(&g, x); };
+  std::vector<uint32_t> fb(nb, UINT32_MAX);  // kept base op -> candidate index
+  std::vector<uint32_t> newj(nc, UINT32_MAX);
+  D.removed.clear();
+  D.new_pos.clear();
+  D.new_dur.clear();
+  D.new_dev.clear();
+  D.new_flags.clear();
+  uint32_t b = 0, x = 0;
+  while (b < nb || x < nc) {
+    int c;
+    if (b == nb) c = 1;
+    else if (x == nc) c = -1;
+    else c = bid(b).compare(cid(x));
+    if (c == 0) {
+      if (bg.kind[b] == g.kind[x] && bg.dur[b] == g.dur[x] &&
+          bg.dev[b] == cdev[g.dev[x]] && bg.flags[b] == g.flags[x]) {
+        fb[b] = x;
+      } else {  // same id, different op: removed + re-added at its place
+        D.removed.push_back(b);
+        newj[x] = static_cast<uint32_t>(D.new_pos.size());
+        D.new_pos.push_back(b);
+        D.new_dur.push_back(g.dur[x]);
+        D.new_dev.push_back(cdev[g.dev[x]]);
+        D.new_flags.push_back(g.flags[x]);
+      }
+      ++b;
+      ++x;
+    } else if (c < 0) {
+      D.removed.push_back(b++);
+    } else {
+      newj[x] = static_cast<uint32_t>(D.new_pos.size());
+      D.new_pos.push_back(b);  // lower_bound among the base ids
+      D.new_dur.push_back(g.dur[x]);
+      D.new_dev.push_back(cdev[g.dev[x]]);
+      D.new_flags.push_back(g.flags[x]);
+      ++x;
+    }
+  }
+  // removed came out ascending except for re-added ids (pushed in order too)
+  const uint32_t nn = static_cast<uint32_t>(D.new_pos.size());
+  D.new_succ_off.assign(nn + 1, 0);
+  D.new_succ.clear();
+  for (uint32_t y = 0; y < nc; ++y) {
+    if (newj[y] == UINT32_MAX) continue;
+    D.new_succ.insert(D.new_succ.end(), g.succ.begin() + g.succ_off[y],
+                      g.succ.begin() + g.succ_off[y + 1]);
+    D.new_succ_off[newj[y] + 1] = g.succ_off[y + 1] - g.succ_off[y];
+  }
+  for (uint32_t j = 0; j < nn; ++j) D.new_succ_off[j + 1] += D.new_succ_off[j];
+  D.extra_src.clear();
+  D.extra_dst.clear();
+  D.cut.clear();
+  for (uint32_t u = 0; u < nb; ++u) {
+    const uint32_t xu = fb[u];
+    if (xu == UINT32_MAX) continue;
+    uint32_t e = bg.succ_off[u];
+    const uint32_t ee = bg.succ_off[u + 1];
+    uint32_t k = g.succ_off[xu];
+    const uint32_t kk = g.succ_off[xu + 1];
+    while (e < ee || k < kk) {
+      if (e < ee && fb[bg.succ[e]] == UINT32_MAX) {  // edge to a removed op: gone anyway
+        ++e;
+        continue;
+      }
+      const uint32_t mb = e < ee ? fb[bg.succ[e]] : UINT32_MAX;
+      const uint32_t mc = k < kk ? g.succ[k] : UINT32_MAX;
+      if (mb == mc) {
+        ++e;
+        ++k;
+      } else if (mb < mc) {
+        D.cut.push_back(e++);
+      } else {
+        D.extra_src.push_back(u);
+        D.extra_dst.push_back(mc);
+        ++k;
+      }
+    }
+  }
+}
+}  // namespace
+
+int dpro_base_delta_from_graphs(const dpro_base* base, const dpro_graph* const* graphs,
+                                int32_t n, int32_t threads, dpro_delta_set** out) {
+  if (!base || !out || n < 0 || (n && !graphs)) return DPRO_EINVAL;
+  *out = nullptr;
+  if (threads < 1) threads = 1;
+  auto set = std::make_unique<dpro_delta_set>();
+  set->base = base->b;
+  set->d.resize(n);
+  std::vector<int32_t> st(n, DPRO_OK);
+  std::vector<std::string> errs(threads);
+  std::atomic<int32_t> next{0};
+  auto work = [&](int tid) {
+    for (int32_t i; (i = next.fetch_add(1)) < n;) {
+      try {
+        if (!graphs[i]) throw std::runtime_error("null graph");
+        delta_from_graph(*base->b, *graphs[i], set->d[i]);
+      } catch (const std::exception& e) {
+        st[i] = DPRO_EINVAL;
+        errs[tid] = e.what();
+      }
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < threads; ++t) pool.emplace_back(work, t);
+  work(0);
+  for (auto& th : pool) th.join();
+  for (int32_t i = 0; i < n; ++i)
+    if (st[i] != DPRO_OK) {
+      for (auto& e : errs)
+        if (!e.empty()) g_gen_err = e;
+      return st[i];
+    }
+  set->fill_views();
   *out = set.release();
   return DPRO_OK;
+}
+
+const char* dpro_base_worker(const dpro_base* base, int32_t k) {
+  if (!base || k < 0 || k >= static_cast<int32_t>(base->b->workers.size())) return nullptr;
+  return base->b->c.nodes[base->b->workers[k]].c_str();
 }
 
 int dpro_base_delta_batch(const dpro_base* base, int32_t n, const int32_t* n_groups,

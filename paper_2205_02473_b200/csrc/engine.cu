@@ -127,17 +127,18 @@ class Pool {
   }
   int size() const { return static_cast<int>(th_.size()); }
   void start(int32_t n, std::function<void(int32_t)> fn) {
+    auto j = std::make_shared<Job>();
+    j->fn = std::move(fn);
+    j->n = n;
+    j->left = n;
     std::lock_guard<std::mutex> g(m_);
-    fn_ = std::move(fn);
-    n_ = n;
-    next_ = 0;
-    left_ = n;
+    job_ = std::move(j);
     ++gen_;
     cv_.notify_all();
   }
   void wait() {
     std::unique_lock<std::mutex> g(m_);
-    done_.wait(g, [this] { return left_ == 0 && active_ == 0; });
+    done_.wait(g, [this] { return !job_ || job_->left == 0; });
   }
   void run(int32_t n, std::function<void(int32_t)> fn) {
     start(n, std::move(fn));
@@ -145,39 +146,42 @@ class Pool {
   }
 
  private:
+  // Every claim is tied to its job: a worker that wakes late for a finished
+  // job finds that job's counter exhausted and never runs its fn, and its
+  // completions are credited to that job only (not to the next one).
+  struct Job {
+    std::function<void(int32_t)> fn;
+    int32_t n = 0;
+    int32_t left = 0;  // guarded by m_
+    std::atomic<int32_t> next{0};
+  };
   void loop() {
     uint64_t seen = 0;
     for (;;) {
-      std::function<void(int32_t)> fn;
-      int32_t n;
+      std::shared_ptr<Job> j;
       {
         std::unique_lock<std::mutex> g(m_);
         cv_.wait(g, [&] { return stop_ || gen_ != seen; });
         if (stop_) return;
         seen = gen_;
-        fn = fn_;
-        n = n_;
-        ++active_;  // wait() returns only once no worker can touch this job
+        j = job_;
       }
       int32_t did = 0;
-      for (int32_t i; (i = next_.fetch_add(1)) < n;) {
-        fn(i);
+      for (int32_t i; (i = j->next.fetch_add(1)) < j->n;) {
+        j->fn(i);
         ++did;
       }
-      {
+      if (did) {
         std::lock_guard<std::mutex> g(m_);
-        left_ -= did;
-        --active_;
-        if (left_ == 0 && active_ == 0) done_.notify_all();
+        j->left -= did;
+        if (j->left == 0) done_.notify_all();
       }
     }
   }
   std::vector<std::thread> th_;
   std::mutex m_;
   std::condition_variable cv_, done_;
-  std::function<void(int32_t)> fn_;
-  int32_t n_ = 0, left_ = 0, active_ = 0;
-  std::atomic<int32_t> next_{0};
+  std::shared_ptr<Job> job_;
   uint64_t gen_ = 0;
   bool stop_ = false;
 };
@@ -748,6 +752,23 @@ std::string check_delta(const dpro_resident& r, const dpro_delta& D, uint32_t& n
         std::upper_bound(r.succ_off.begin(), r.succ_off.end(), e) - r.succ_off.begin() - 1);
     if (removed(u) || removed(r.succ[e])) return "cut edges must join kept ops";
     ++lost;
+  }
+  // an extra edge must not repeat a kept, uncut base edge (the merge would
+  // emit it twice: successor lists must stay strictly ascending and the
+  // in-degrees must match what GraphBuilder's edge set gives)
+  auto final_of = [&](uint32_t b) {
+    return b - static_cast<uint32_t>(std::lower_bound(D.removed, D.removed + D.n_removed, b) -
+                                     D.removed) +
+           static_cast<uint32_t>(std::upper_bound(D.new_pos, D.new_pos + D.n_new, b) -
+                                 D.new_pos);
+  };
+  for (uint32_t k = 0; k < D.n_extra; ++k) {
+    const uint32_t u = D.extra_src[k];
+    for (uint32_t e = r.succ_off[u]; e < r.succ_off[u + 1]; ++e) {
+      const uint32_t s = r.succ[e];
+      if (removed(s) || std::binary_search(D.cut, D.cut + D.n_cut, e)) continue;
+      if (final_of(s) == D.extra_dst[k]) return "extra edge repeats a kept base edge";
+    }
   }
   n_edges = static_cast<uint32_t>(uint64_t(r.e) - lost + D.n_extra + ne);
   return "";

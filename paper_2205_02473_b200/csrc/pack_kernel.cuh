@@ -44,7 +44,7 @@ constexpr uint32_t kMaxDev = 1u << 10;
 constexpr uint32_t kMaxCnt = 1u << 22;
 
 // not_fast bits
-constexpr uint32_t kNfDur = 1u;       // |dur| >= 2^31 or sum of dur >= 2^31
+constexpr uint32_t kNfDur = 1u;       // some |dur| >= 2^31 (the record holds int32)
 constexpr uint32_t kNfIndeg = 2u;     // some indeg >= 65535
 constexpr uint32_t kWideCnt = 1u << 8;  // (PackInfo::wide) some indeg >= 255: u16 counters
 constexpr uint32_t kNfVsrc = 4u;      // virtual op without predecessors
@@ -523,8 +523,9 @@ __global__ void __cluster_dims__(kPackCluster, 1, 1) __launch_bounds__(kPackThre
       if (threadIdx.x == 0) {
         PackInfo inf;
         inf.first_missing = s_ctr.first;
-        inf.not_fast = (s_ctr.flags & ~kWideCnt) | (s_ctr.sum >= 0x7FFFFFFFull ? kNfDur : 0u) |
-                       (s_ctr.ncnt >= kMaxCnt ? kNfSize : 0u);
+        // times are 64-bit in every kernel: only a single duration that
+        // does not fit the record's int32 field leaves the fast path
+        inf.not_fast = (s_ctr.flags & ~kWideCnt) | (s_ctr.ncnt >= kMaxCnt ? kNfSize : 0u);
         inf.wide = s_ctr.flags & kWideCnt;
         inf.pad = 0;
         inf.n_cnt = s_ctr.ncnt;

@@ -2,10 +2,12 @@
 //
 // Same round semantics as replay_kernel.cuh (proj/src/replay.cpp:37-134);
 // what changes is where the state lives and what an event round touches.
-//   * one warp per candidate; lane l owns devices d = l + 32 j (j < KD); the
-//     in-flight end time of each owned device lives in a lane register, so
-//     the next event time is one REDUX.MIN over the warp (32-bit times: the
-//     pack pass proves sum(dur) < 2^31, hence every time fits);
+//   * one CTA of NW warps per candidate (NW = 1, 2 or 4, chosen by device
+//     count); thread l owns devices d = l + 32 NW j (j < KD); the in-flight
+//     end time of each owned device lives in a register (64-bit: times are
+//     integer us or ns, and a config-4 makespan in ns is ~10^12), and the
+//     next event time is one REDUX.MIN over 32-bit offsets end - t (every
+//     in-flight end lies in (t, t + 2^31): op durations fit int32);
 //   * a round only visits devices that completed or received arrivals
 //     (per-lane dirty bitmask in shared memory, set by producers);
 //   * per-device FIFOs are shared-memory rings of 16-byte entries
@@ -18,9 +20,9 @@
 //     records to lanes, so a round costs one record-load latency however
 //     many successors complete (a PS push RECV has 16);
 // Whatever the fast path cannot represent (ring or worklist overflow, a
-// virtual source -> init quirk, indeg >= 255, durations that need 64-bit
-// times, too many devices / counters, a cycle) falls back inside the same
-// launch to the general kernel (replay_candidate, global state): every
+// virtual source -> init quirk, indeg >= 65535, an op duration >= 2^31,
+// too many devices / counters, a cycle) falls back inside the same launch
+// to the general kernel (replay_candidate, global state): every
 // candidate's result is exact either way.
 #pragma once
 
@@ -30,13 +32,17 @@
 namespace dpro_k {
 
 constexpr uint32_t kT32Inf = 0xFFFFFFFFu;
+constexpr unsigned long long kT64Inf = ~0ull;
 // replay_fast outcomes / bail-out causes
 constexpr uint32_t kDone = 0, kBailRing = 1, kBailOther = 2;
 constexpr int kRetry = 9;  // status of a candidate queued for the deep-ring pass
 
+// segt: the event-time EPOCH (count of distinct event times so far) of the
+// device's last arrival segment -- a time-independent stand-in for "the
+// arrivals at the current t", exact for any time unit.
 struct __align__(16) DevF {
   uint32_t head, tail, tsort, segbeg;
-  uint32_t zlo, zhi, segt, busy;
+  uint32_t zlo, zhi, segt, pad;
   uint4 ient;  // in-flight positive-duration op {op, dur, sb, se}
 };
 static_assert(sizeof(DevF) == 48, "DevF layout");
@@ -150,6 +156,14 @@ __device__ __forceinline__ uint32_t gmax(uint32_t v, volatile uint32_t* red, uin
   return m;
 }
 
+template <int NW>
+__device__ __forceinline__ unsigned long long gmax64(unsigned long long v, volatile uint32_t* red,
+                                                     uint32_t& par) {
+  const uint32_t hi = gmax<NW>(static_cast<uint32_t>(v >> 32), red, par);
+  const uint32_t lo = gmax<NW>((v >> 32) == hi ? static_cast<uint32_t>(v) : 0u, red, par);
+  return (static_cast<unsigned long long>(hi) << 32) | lo;
+}
+
 template <int NW, int KD>
 struct FastWarp {
   static constexpr uint32_t NT = 32u * NW;
@@ -169,7 +183,8 @@ struct FastWarp {
   bool want;
   int lane;
   int tid;
-  uint32_t vcount = 0, dcount = 0, tmax = 0;
+  uint32_t vcount = 0, dcount = 0;
+  unsigned long long tmax = 0;
   bool wide = false;  // u16 counters (some in-degree >= 255)
 
   __device__ __forceinline__ uint4* ring(uint32_t d) { return q + (size_t)d * qc; }
@@ -185,7 +200,7 @@ struct FastWarp {
   }
 
   // ready(s, t) of replay.cpp:60-72 for s reached through a packed record.
-  __device__ __forceinline__ void ready(const uint4& a, uint32_t t) {
+  __device__ __forceinline__ void ready(const uint4& a, unsigned long long t) {
     const uint32_t s = a.x & kOpMask;
     const uint32_t cnt = (a.z >> kCntShift) & kCntMax;
     const uint32_t se = cnt == kCntMax ? __ldg(&rec[s + 1].w) : a.w + cnt;
@@ -215,7 +230,7 @@ struct FastWarp {
   }
 
   // One out-edge record of a completing op (replay.cpp:100-103).
-  __device__ __forceinline__ void edge(const uint4& a, uint32_t t) {
+  __device__ __forceinline__ void edge(const uint4& a, unsigned long long t) {
     if ((a.z & (kFVirt | kFMulti)) == kFVirt) {  // spliced single-pred virtual
       const uint32_t s = a.x & kOpMask;
       if (want) {
@@ -248,7 +263,7 @@ struct FastWarp {
   // expands ranges [lo, hi) and ends with a barrier; virtual cascades
   // pushed during a pass are expanded by the next one.
   // Returns kDone, or the bail-out cause.
-  __device__ __forceinline__ uint32_t expand(uint32_t t) {
+  __device__ __forceinline__ uint32_t expand(unsigned long long t) {
     uint32_t lo = 0;
     for (;;) {
       const uint32_t hi = *rlc;
@@ -316,19 +331,23 @@ struct FastWarp {
 
   // Owner-lane dispatch(t) for device d (replay.cpp:74-90) after merging
   // this round's arrivals into the (ready, index)-ordered tail segment.
-  // Returns the in-flight end (kT32Inf: idle); sets *zero when
-  // zero-duration ops ran (they complete next round).
-  __device__ __forceinline__ uint32_t dispatch_dev(uint32_t d, uint32_t t, uint32_t iend,
-                                                   bool* zero) {
+  // Returns the in-flight end (kT64Inf: idle); sets *zero when
+  // zero-duration ops ran (they complete next round). epoch: number of
+  // distinct event times so far; busy: the device's summed dur (owner
+  // thread's register).
+  __device__ __forceinline__ unsigned long long dispatch_dev(uint32_t d, unsigned long long t,
+                                                             uint32_t epoch,
+                                                             unsigned long long iend, bool* zero,
+                                                             unsigned long long& busyd) {
     DevF& s = dv[d];
     uint4* r = ring(d);
     const uint32_t tail = *reinterpret_cast<volatile uint32_t*>(&s.tail);
     const uint32_t m = qc - 1;
     uint32_t head = s.head;
     if (tail != s.tsort) {
-      if (s.segt != t) {
+      if (s.segt != epoch) {
         s.segbeg = s.tsort;
-        s.segt = t;
+        s.segt = epoch;
       }
       const uint32_t lo = max(s.segbeg, head);
       for (uint32_t p = s.tsort; p < tail; ++p) {
@@ -344,14 +363,14 @@ struct FastWarp {
       }
       s.tsort = tail;
     }
-    if (iend == kT32Inf && head < tail) {
+    if (iend == kT64Inf && head < tail) {
       const uint32_t zlo = head;
-      uint32_t busy = 0;
+      unsigned long long busy = 0;
       const uint32_t base = devoff[d];
       bool infl = false;
       while (head < tail) {
         const uint4 x = r[head & m];
-        const uint32_t en = t + x.y;
+        const unsigned long long en = t + x.y;
         if (want) {
           start[x.x] = t;
           end[x.x] = en;
@@ -369,7 +388,7 @@ struct FastWarp {
           break;
         }
       }
-      s.busy += busy;
+      busyd += busy;
       s.head = head;
       s.zlo = zlo;
       const uint32_t zhi = infl ? head - 1 : head;
@@ -429,7 +448,7 @@ __device__ uint32_t replay_fast(const Cand& c, int cid, const uint4* rec, const 
   for (uint32_t d = tid; d < D; d += NT) {
     DevF z;
     z.head = z.tail = z.tsort = z.segbeg = 0;
-    z.zlo = z.zhi = z.segt = z.busy = 0;
+    z.zlo = z.zhi = z.segt = z.pad = 0;
     z.ient = make_uint4(0, 0, 0, 0);
     dv[d] = z;
   }
@@ -439,7 +458,7 @@ __device__ uint32_t replay_fast(const Cand& c, int cid, const uint4* rec, const 
   gsync<NW>();
   // ---- sources (replay.cpp:92-94). No virtual sources reach the fast path
   // (pack flags them), so there are no cascades and no init quirk. ----
-  for (uint32_t k = tid; k < info.n_src; k += NT) W.ready(__ldg(rec + __ldg(srcs + k)), 0u);
+  for (uint32_t k = tid; k < info.n_src; k += NT) W.ready(__ldg(rec + __ldg(srcs + k)), 0ull);
   gsync<NW>();
   if (gany<NW>(misc[1] != 0)) return misc[1] == kBailRing ? kBailRing : kBailOther;
   for (uint32_t d = tid; d < D; d += NT) {  // t = 0 arrivals in index order
@@ -460,33 +479,37 @@ __device__ uint32_t replay_fast(const Cand& c, int cid, const uint4* rec, const 
   gsync<NW>();
 
   // ---- dispatch(0) + event loop (replay.cpp:95-106) ----
-  uint32_t iend[KD];
-  uint32_t zmask = 0;
+  unsigned long long iend[KD], busyd[KD];
+  uint32_t zmask = 0, epoch = 0;
 #pragma unroll
   for (int j = 0; j < KD; ++j) {
-    iend[j] = kT32Inf;
+    iend[j] = kT64Inf;
+    busyd[j] = 0;
     const uint32_t d = tid + NT * j;
     if (d < D) {
       bool z = false;
-      iend[j] = W.dispatch_dev(d, 0u, kT32Inf, &z);
+      iend[j] = W.dispatch_dev(d, 0ull, 0u, kT64Inf, &z, busyd[j]);
       if (z) zmask |= 1u << j;
     }
   }
   misc[4 + tid] = 0;  // all devices were just visited
-  uint32_t t = 0;
+  unsigned long long t = 0;
   uint32_t rpar = 0;
   for (;;) {
     PROF_T(p0);
+    // in-flight ends are > t and < t + 2^31: reduce their 32-bit offsets
     uint32_t lmin = kT32Inf;
 #pragma unroll
-    for (int j = 0; j < KD; ++j) lmin = min(lmin, iend[j]);
+    for (int j = 0; j < KD; ++j)
+      if (iend[j] != kT64Inf) lmin = min(lmin, static_cast<uint32_t>(iend[j] - t));
     bool zero_round;
-    uint32_t tn;
-    round_head<NW>(zmask != 0, lmin, red, par, zero_round, tn);
+    uint32_t dt;
+    round_head<NW>(zmask != 0, lmin, red, par, zero_round, dt);
     uint32_t freed = 0;
     if (!zero_round) {
-      if (tn == kT32Inf) break;
-      t = tn;
+      if (dt == kT32Inf) break;
+      t += dt;
+      ++epoch;
     }
     PROF_T(p1);
     // range counters alternate by round: this round's was zeroed last round
@@ -513,7 +536,7 @@ __device__ uint32_t replay_fast(const Cand& c, int cid, const uint4* rec, const 
 #pragma unroll
       for (int j = 0; j < KD; ++j) {
         if (iend[j] == t) {
-          iend[j] = kT32Inf;
+          iend[j] = kT64Inf;
           freed |= 1u << j;
           const uint4 e = dv[tid + NT * j].ient;
           if (e.w > e.z) W.push_range(e.z, e.w - e.z);
@@ -533,7 +556,7 @@ __device__ uint32_t replay_fast(const Cand& c, int cid, const uint4* rec, const 
     for (int j = 0; j < KD; ++j) {
       if (todo & (1u << j)) {
         bool z = false;
-        iend[j] = W.dispatch_dev(tid + NT * j, t, iend[j], &z);
+        iend[j] = W.dispatch_dev(tid + NT * j, t, epoch, iend[j], &z, busyd[j]);
         if (z) zmask |= 1u << j;
       }
     }
@@ -555,15 +578,17 @@ __device__ uint32_t replay_fast(const Cand& c, int cid, const uint4* rec, const 
   const uint32_t vc = gsum<NW>(W.vcount, red, par);
   const uint32_t dc = gsum<NW>(W.dcount, red, par);
   if (vc + dc != n) return kBailOther;  // cycle: the general path reports it exactly
-  const uint32_t T = gmax<NW>(W.tmax, red, par);
-  for (uint32_t d = tid; d < D; d += NT) {
-    S.busy[c.dev_off + d] = dv[d].busy;
-    S.dhead[c.dev_off + d] = W.devoff[d] + dv[d].head;
+  const unsigned long long T = gmax64<NW>(W.tmax, red, par);
+#pragma unroll
+  for (int j = 0; j < KD; ++j) {
+    const uint32_t d = tid + NT * j;
+    if (d < D) S.busy[c.dev_off + d] = static_cast<long long>(busyd[j]);
   }
+  for (uint32_t d = tid; d < D; d += NT) S.dhead[c.dev_off + d] = W.devoff[d] + dv[d].head;
   if (tid == 0) {
     O.status[cid] = kOk;
     O.err[cid] = 0;
-    O.makespan[cid] = T;
+    O.makespan[cid] = static_cast<long long>(T);
   }
   return kDone;
 }

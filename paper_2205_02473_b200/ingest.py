@@ -332,6 +332,7 @@ class LayeredBase:
     """Base graph for delta construction (dpro_base_layered)."""
 
     def __init__(self, model: LayeredModel, cluster: ClusterSpec):
+        self.model, self.cluster = model, cluster
         self._m = model.struct()
         self._layers = model.layers
         self._holder = N.ClusterDescHolder(cluster)
@@ -384,26 +385,53 @@ class LayeredBase:
 
 
     def deltas(self, specs: Sequence[tuple[Sequence[Sequence[int]], Sequence[int]]],
-               threads: int = 8, fw_join=None, bw_join=None) -> "DeltaSet":
+               threads: int = 8, fw_join=None, bw_join=None, join_worker=None) -> "DeltaSet":
         """[(groups, ks), ...] -> unmerged deltas for Engine.delta_batch
-        (fw_join / bw_join as in candidates())."""
+        (fw_join / bw_join as in candidates(); join_worker as in
+        deltas_from_arrays())."""
         return self.deltas_from_arrays(*self._spec_arrays(specs), threads=threads,
-                                       fw_join=fw_join, bw_join=bw_join)
+                                       fw_join=fw_join, bw_join=bw_join,
+                                       join_worker=join_worker)
+
+    def deltas_from_graphs(self, graphs: Sequence["NativeGraph"], threads: int = 8) -> "DeltaSet":
+        """Any generated graphs (recompute / grad-accum variants, ...) as
+        deltas against this base (dpro_base_delta_from_graphs)."""
+        n = len(graphs)
+        arr = (C.c_void_p * max(1, n))(*[g.handle for g in graphs])
+        out = C.c_void_p()
+        rc = N.lib.dpro_base_delta_from_graphs(self.handle, arr, n, threads, C.byref(out))
+        if rc != N.DPRO_OK:
+            raise Error(N.lib.dpro_graph_last_error().decode())
+        ds = DeltaSet(out.value, self)
+        ds._graphs = list(graphs)
+        return ds
+
+    def worker(self, k: int) -> str:
+        """Name of the k-th worker (the join_worker ordinal)."""
+        name = N.lib.dpro_base_worker(self.handle, k)
+        if name is None:
+            raise IndexError(k)
+        return name.decode()
 
     def deltas_from_arrays(self, n_groups, spec_off, group_off, members, ks,
-                           threads: int = 8, fw_join=None, bw_join=None) -> "DeltaSet":
-        """Same, from the flattened spec arrays of dpro_base_delta_batch."""
+                           threads: int = 8, fw_join=None, bw_join=None,
+                           join_worker=None) -> "DeltaSet":
+        """Same, from the flattened spec arrays of dpro_base_delta_batch;
+        join_worker [n]: the worker ordinal the candidate's op-fusion joins
+        apply to (-1 = every worker; None = every worker for all)."""
         n = len(n_groups)
         fj, bj = self._joins(n, fw_join, bw_join)
+        jw = None if join_worker is None else np.ascontiguousarray(join_worker, np.int32)
         n_groups = np.ascontiguousarray(n_groups, np.int32)
         spec_off = np.ascontiguousarray(spec_off, np.int64)
         group_off = np.ascontiguousarray(group_off, np.int32)
         members = np.ascontiguousarray(members, np.int32)
         ks = np.ascontiguousarray(ks, np.int32)
         out = C.c_void_p()
-        rc = N.lib.dpro_base_delta_batch_ops(self.handle, n, N.ptr(n_groups), N.ptr(spec_off),
-                                             N.ptr(group_off), N.ptr(members), N.ptr(ks),
-                                             N.ptr(fj), N.ptr(bj), threads, C.byref(out))
+        rc = N.lib.dpro_base_delta_batch_ex(self.handle, n, N.ptr(n_groups), N.ptr(spec_off),
+                                            N.ptr(group_off), N.ptr(members), N.ptr(ks),
+                                            N.ptr(fj), N.ptr(bj), N.ptr(jw), threads,
+                                            C.byref(out))
         if rc != N.DPRO_OK:
             raise Error(N.lib.dpro_graph_last_error().decode())
         return DeltaSet(out.value, self)

@@ -8,7 +8,7 @@ candidates is built as deltas of one base graph on host threads
 the resident base graph on the GPU and replayed in ONE batched launch;
 across GPUs every
 rank evaluates its own shard and the round's best candidate is agreed on
-with one packed int64 MIN all-reduce (the K4 exchange of DESIGN.md).
+with two int64 MIN all-reduces (the K4 exchange of DESIGN.md, exchange.py).
 
 * `opt_part_num`        optimize.cpp:562-576 (k* over a batched t_sync grid)
 * `should_fuse_ops`     optimize.cpp:545-551 (Theorem 1)
@@ -23,7 +23,6 @@ with one packed int64 MIN all-reduce (the K4 exchange of DESIGN.md).
 """
 from __future__ import annotations
 
-import math
 from dataclasses import dataclass, field
 from typing import Callable, Sequence
 
@@ -32,6 +31,7 @@ import numpy as np
 from .engine import Engine, default_engine
 from .graph import ClusterSpec
 from .ingest import LayeredBase, LayeredModel
+from .exchange import broadcast_from, exchange_best, metropolis_accept
 from .replay import sync_makespan_grid
 
 
@@ -138,14 +138,23 @@ class SyncSearch:
     adjacent units, split a unit, re-partition a unit), replays them all in
     one GPU batch (makespan only), takes the best as the proposal and
     accepts it with P = min(1, exp(beta * (T - T'))).
-    With `dist` (torch.distributed) every rank proposes its own batch and
-    the global best is chosen by a packed (makespan, rank, id) MIN
-    all-reduce, then broadcast from its owner."""
+    With `dist` (torch.distributed) every rank proposes its own batch. In
+    the default "shared" mode the round's proposal is the global best (two
+    MIN all-reduces, exchange.exchange_best, then a broadcast from its
+    owner); with chains="independent" every rank runs its own chain and only
+    the best-cost strategy found so far is exchanged each round."""
 
     def __init__(self, model: LayeredModel, cluster: ClusterSpec, engine: Engine | None = None,
                  kmax: int = 16, beta: float = 0.01, seed: int = 0, threads: int = 8,
-                 dist=None, rank: int = 0, guided: float = 0.0, op_fusion: bool = False):
+                 dist=None, rank: int = 0, guided: float = 0.0, op_fusion: bool = False,
+                 chains: str = "shared"):
+        if chains not in ("shared", "independent"):
+            raise ValueError(f"chains must be 'shared' or 'independent', got {chains!r}")
         self.model, self.cluster = model, cluster
+        # "shared": one chain, each round's proposal is the best over all
+        # ranks' batches; "independent": one chain per rank (north_star),
+        # only the best-cost strategy is exchanged per round
+        self.chains, self.seed = chains, seed
         self.engine = engine or default_engine()
         self.kmax, self.beta, self.threads = kmax, beta, threads
         # fraction of proposals that modify a unit on the current critical
@@ -343,19 +352,18 @@ class SyncSearch:
         return ms
 
     # ---- one round ----------------------------------------------------
+    def _dev(self) -> str:
+        return f"cuda:{self.engine.device}" if self.dist.get_backend() == "nccl" else "cpu"
+
     def _exchange(self, best_ms: int, best_i: int, cand: SyncState) -> SyncState:
+        """The global best proposal of this round (exchange.exchange_best:
+        MIN makespan, then lowest (rank, index) among the ties), broadcast
+        from its owner."""
         if self.dist is None:
             return cand
-        import torch
-        dev = f"cuda:{self.engine.device}" if self.dist.get_backend() == "nccl" else "cpu"
-        key = torch.tensor([(int(best_ms) << 24) | (self.rank << 20) | int(best_i)],
-                           dtype=torch.int64, device=dev)
-        self.dist.all_reduce(key, op=self.dist.ReduceOp.MIN)
-        owner = (int(key.item()) >> 20) & 0xF
-        obj = [cand if self.rank == owner else None]
-        self.dist.broadcast_object_list(obj, src=owner)
-        out = obj[0]
-        out.makespan = int(key.item()) >> 24
+        ms, owner, _ = exchange_best(self.dist, best_ms, best_i, self.rank, self._dev())
+        out = broadcast_from(self.dist, cand, owner, self.rank)
+        out.makespan = ms
         return out
 
     def step(self, batch: int) -> SearchLog:
@@ -363,6 +371,8 @@ class SyncSearch:
         if s.makespan < 0:
             s.makespan = int(self.evaluate([s])[0])
             self.best = s.copy()
+            if self.dist is not None and self.chains == "independent":
+                self.best = self._exchange(self.best.makespan, 0, self.best.copy())
         if self.guided > 0 and self._critical is None:
             self._critical = self.critical_layers(s)
         cuts, kl = self.propose_many(s, batch)
@@ -373,16 +383,24 @@ class SyncSearch:
         cand = self._state(cuts[i], kl[i], None if fj is None else fj[i],
                            None if bj is None else bj[i])
         cand.makespan = int(ms[i])
-        prop = self._exchange(int(ms[i]), i, cand)
-        # Metropolis acceptance (memory loss term 0); the
-        # uniform draw is shared so every rank takes the same decision
-        u = float(np.random.default_rng([self.log.rounds, 7]).random())
-        p = min(1.0, math.exp(self.beta * (s.makespan - prop.makespan)))
-        if u < p:
+        if self.chains == "independent":
+            # every rank walks its own chain (own proposals, own uniform
+            # draw); only the best-cost strategy crosses ranks
+            prop = cand
+            u = float(np.random.default_rng([self.seed, self.rank, self.log.rounds, 7]).random())
+        else:
+            # one chain shared by all ranks: the global best proposal and a
+            # shared uniform draw, so every rank takes the same decision
+            prop = self._exchange(int(ms[i]), i, cand)
+            u = float(np.random.default_rng([self.log.rounds, 7]).random())
+        if metropolis_accept(self.beta, s.makespan, prop.makespan, u):
             self.state = prop
             self.log.accepted += 1
             self._critical = None  # recomputed for the new state
-        if self.state.makespan < self.best.makespan:
+        if self.chains == "independent" and self.dist is not None:
+            mine = self.state if self.state.makespan < self.best.makespan else self.best
+            self.best = self._exchange(mine.makespan, 0, mine.copy())
+        elif self.state.makespan < self.best.makespan:
             self.best = self.state.copy()
         self.log.rounds += 1
         self.log.history.append(self.state.makespan)
@@ -488,7 +506,7 @@ class StrategySearch:
             ms = self.evaluate([c[1] for c in cands])
             i = int(np.argmin(ms))
             u = float(np.random.default_rng([self.log.rounds, 11]).random())
-            if u < min(1.0, math.exp(self.beta * (self.makespan - int(ms[i])))):
+            if metropolis_accept(self.beta, self.makespan, int(ms[i]), u):
                 self.g, self.makespan = cands[i][1], int(ms[i])
                 self.applied = self.applied + [cands[i][0]]
                 self._resident = None  # the next round's base is the new graph

@@ -409,3 +409,65 @@ def test_delta_batch_edge_cases(engine):
     b = engine.delta_batch(res, base.deltas(specs))
     b.replay(want_schedule=False)
     assert np.all(b.results()[1] == 0)
+
+
+@pytest.mark.parametrize("scheme,W,S,L", [("ring", 4, 0, 8), ("ps", 3, 2, 7), ("ring", 11, 0, 5)])
+def test_graph_variants_as_deltas_merge_exactly(scheme, W, S, L):
+    """dpro_base_delta_from_graphs: recompute / grad-accum / partitioned /
+    fused graphs against the base; merging the delta gives the graph's own
+    CSR and device names."""
+    from paper_2205_02473_b200.ingest import layered_graph, layered_graph_variant
+    base, specs = _setup(scheme, W, S, L, 3, W + 7 * L)
+    m, c = base.model, base.cluster
+    graphs = [layered_graph_variant(m, c, "recompute", 0.5),
+              layered_graph_variant(m, c, "grad-accum", 0.55),
+              layered_graph_variant(m, c, "grad-accum", 0.5, [2] * L),
+              layered_graph(m, c, [3] * L)] + base.candidates(specs)
+    bv = base.graph()
+    ds = base.deltas_from_graphs(graphs, threads=3)
+    for i, g in enumerate(graphs):
+        dur, dev, fl, succ = merge_host(bv.csr, bv.n_ops, ds[i])
+        cs = g.csr
+        assert len(dur) == g.n_ops
+        assert np.array_equal(dur, cs.dur) and np.array_equal(fl, cs.flags)
+        strs = g.device_strs()
+        assert [ds.device_str(i, int(x)) for x in dev] == [strs[int(x)] for x in cs.dev]
+        for k in range(g.n_ops):
+            assert succ[k] == cs.succ[cs.succ_off[k]:cs.succ_off[k + 1]].tolist(), (i, k)
+    same_set = base.deltas_from_graphs([bv])
+    same = same_set[0]
+    assert same.n_removed == same.n_new == same.n_extra == same.n_cut == 0
+
+
+def test_single_worker_op_fusion_deltas_match_reference_rewrite(ref):
+    """join_worker: the reference's own op-fusion candidate, apply_op_fusion
+    (optimize.cpp:245-318) of two adjacent ops of ONE worker."""
+    spec = {"layers": 6, "fw_dur_us": [11, 23, 35, 47, 59, 61], "bw_dur_us": [13, 27, 31, 43, 57, 69],
+            "tensor_bytes": [1000, 25000, 3000, 40000, 500, 60000], "update_dur_us": 5,
+            "scheme": "ring", "workers": 11, "ps_count": 0, "bandwidth_bytes_per_us": 125.0,
+            "latency_us": 5.0}
+    m = LayeredModel(spec["fw_dur_us"], spec["bw_dur_us"], spec["tensor_bytes"], 5)
+    c = synth_cluster("ring", 11, 0, 125.0, 5.0)
+    base = LayeredBase(m, c)
+    L = 6
+    cases = [(3, "FW", 2), (10, "BW", 4), (0, "FW", 0), (7, "BW", 0)]
+    fj = np.zeros((len(cases), L - 1), np.uint8)
+    bj = np.zeros((len(cases), L - 1), np.uint8)
+    for r, (wk, kind, i) in enumerate(cases):
+        (fj if kind == "FW" else bj)[r, i] = 1
+    specs = [([[i] for i in range(L)], [1] * L)] * len(cases)
+    ds = base.deltas(specs, fw_join=fj, bw_join=bj, join_worker=[wk for wk, _, _ in cases])
+    bv = base.graph()
+    rg0 = ref.RefGraph.synth(spec)
+    for r, (wk, kind, i) in enumerate(cases):
+        w = base.worker(wk)
+        a, b = (f"{w}->FW.l{i}", f"{w}->FW.l{i + 1}") if kind == "FW" else \
+            (f"{w}->BW.l{i + 1}", f"{w}->BW.l{i}")
+        rg = rg0.op_fusion(a, b)
+        ex = rg.export()
+        dur, dev, fl, succ = merge_host(bv.csr, bv.n_ops, ds[r])
+        assert np.array_equal(dur, ex["dur"]) and np.array_equal(fl, ex["flags"])
+        rstr = rg.device_strs()
+        assert [ds.device_str(r, int(x)) for x in dev] == [rstr[int(x)] for x in ex["dev"]]
+        for k in range(len(dur)):
+            assert succ[k] == ex["succ"][ex["succ_off"][k]:ex["succ_off"][k + 1]].tolist()
