@@ -1,30 +1,37 @@
 """Benchmark: batched candidate-DFG replay (BASELINE.json metric) on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config 2] [--batch B]
+                    [--config 4] [--batch B]
 
-Workload (N=1 line = BASELINE configs[1]): BERT-base parameter-server DFG,
-16 workers / 4 servers, 199 tensors, a batch of 1024 candidate graphs (each
-re-partitions 8 seeded tensors with k in {1,2,4}, the reference's
-apply_tensor_partition rewrite). Candidates are deltas of
-one resident base graph (include/dpro_cuda.h dpro_delta). One step = the
-device-side merge of every delta (K0) + the pack kernel + one exact replay
+Workload (default: BASELINE configs[3], the largest single-GPU config):
+GPT-2 medium 64-worker ring-all-reduce DFG (292 tensors, 4.80M ops, 6.0M
+edges, 128 devices) and its per-round candidate mix:
+the recompute candidate, the grad-accum candidate and 146 single-worker
+adjacent op-fusion pairs -- 148 candidates per GPU, one per SM. Candidates
+are deltas of one resident base graph (include/dpro_cuda.h dpro_delta). One
+step = the device-side merge of every delta (K0) + pack + one exact replay
 of every candidate (K1: per-op start/end + makespan) + the per-round
-best-cost exchange (argmin; NCCL MIN all-reduce across ranks when N > 1),
-with the inputs (base graph + deltas) resident in HBM. The per-step working
-set (merged CSR + packed records, ~3.9 GB) is larger than L2: no flush.
+best-cost exchange (argmin; two NCCL MIN all-reduces across ranks when
+N > 1), with the inputs (base graph + deltas) resident in HBM. The step's
+working set (~60 GB of merged CSRs, packed records and schedules) is far
+larger than L2: no flush needed.
 
-Multi-GPU: one process per GPU (torchrun), each rank replays its own 1024
-candidates (weak scaling); timing is the max over ranks of CUDA-event time.
+Multi-GPU: one process per GPU (torchrun), each rank replays its own batch
+(weak scaling); time is the max over ranks of CUDA-event time.
 
---impl reference: the reference's own CPU replayer (oracle/_ref, the
-unmodified proj/src/replay.cpp) on all host cores, same workload/metric.
+--impl reference: the reference's own CPU replayer (oracle/_ref: the
+unmodified proj/src, compiled by oracle/Makefile) on all host cores, over
+the same workload's candidates built by the reference's own generator and
+rewrites (RefGraph.synth + apply_op_fusion / apply_strategy); it never
+imports the product package.
 """
 from __future__ import annotations
 
 import argparse
+import importlib.util
 import json
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -40,6 +47,36 @@ METRIC = "candidate DFG replays/sec"
 UNIT = "replays/s"
 
 
+def _specs_module():
+    """paper_2205_02473_b200/workloads.py loaded by path: the workload
+    definitions without importing the product package (no libdpro_cuda.so)."""
+    p = ROOT / "paper_2205_02473_b200" / "workloads.py"
+    spec = importlib.util.spec_from_file_location("_bench_workloads", p)
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules[spec.name] = mod  # dataclasses resolve their module here
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def bench_config(spec: dict, batch: int, world: int) -> dict:
+    """The `config` object -- identical in both arms."""
+    return {"workload": spec["description"], "model": spec["name"],
+            "batch_per_gpu": batch, "global_batch": batch * world,
+            "parallelism": f"candidates sharded over {world} GPU(s)",
+            "l2": "working set (merged CSRs, packed records, schedules) far larger than L2; "
+                  "no flush"}
+
+
+def _cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or "unknown"
+
+
 def _peak_hbm() -> tuple[float, str]:
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -47,11 +84,13 @@ def _peak_hbm() -> tuple[float, str]:
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def _ncu_traffic() -> float | None:
+def _ncu_traffic(config: int) -> dict | None:
+    """DRAM bytes per launch of the replay kernel from the committed
+    `ncu --set full` capture of this config (profiles/ncu_traffic.json)."""
     p = ROOT / "profiles" / "ncu_traffic.json"
     if p.exists():
         try:
-            return float(json.loads(p.read_text())["dram_bytes_per_launch"])
+            return json.loads(p.read_text()).get(f"config{config}")
         except Exception:
             return None
     return None
@@ -71,7 +110,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
@@ -105,98 +144,120 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def build_candidates(config: int, batch: int, rank: int, threads: int):
-    from paper_2205_02473_b200.ingest import layered_graphs
-    from paper_2205_02473_b200.workloads import workload
-    w = workload(config)
-    pk = w.candidate_partitions(batch, rank=rank)
-    graphs = layered_graphs(w.model, w.cluster, pk, threads=threads)
-    return w, graphs
-
-
-def ref_graphs(graphs, threads: int):
-    """The reference's own graph objects (oracle/_ref) for the bounded
-    sample, built once per run; None when the reference library is absent."""
+# --------------------------------------------------------------------------
+# the reference, built and run through oracle/_ref only
+# --------------------------------------------------------------------------
+def ref_sample_graphs(specs_mod, spec: dict, descs: list[tuple], log=print):
+    """The reference's own graphs for `descs`: RefGraph.synth (the reference
+    generator: synth.cpp + ingest) and the reference rewrites
+    (apply_op_fusion, apply_strategy kRecompute / kGradAccum, apply_partition)."""
     from oracle import oracle
-    if not oracle.ref_available():
-        return None
-    sample = graphs[: max(threads * 2, 8)]
-    refs = []
-    for g in sample:
-        devs = g.device_strs()
-        ids = g.op_ids()
-        ops = []
-        for i, id_ in enumerate(ids):
-            ds = devs[int(g.csr.dev[i])]
-            if ">" in ds:
-                a, b = ds.split(">", 1)
-                dk, dn, dp = 1, a, b
-            else:
-                dk, dn, dp = 0, ds, ""
-            ops.append((id_, g.op_kind(i), dk, dn, dp, int(g.csr.dur[i])))
-        so, su = g.csr.succ_off, g.csr.succ
-        edges = [(ids[i], ids[int(s)]) for i in range(len(ids)) for s in su[so[i]:so[i + 1]]]
-        refs.append(oracle.RefGraph.from_ops(ops, edges))
-    return refs
-
-
-def cpu_reference_time(graphs, budget_s: float, threads: int, refs=None):
-    """Times the reference replay() (oracle/_ref) on a bounded sample; falls
-    back to the C port when the reference library is absent."""
-    from oracle import oracle
-    sample = graphs[: max(threads * 2, 8)]
-    if refs is None:
-        refs = ref_graphs(graphs, threads)
-    if refs is not None:
-        # calibrate: one round of len(refs) replays, then size to the budget
-        sec, _ = oracle.ref_replay_bench(refs, len(refs), threads)
-        per = sec / len(refs)
-        n = int(max(len(refs), min(budget_s / max(per, 1e-9), 100_000)))
-        sec, ms = oracle.ref_replay_bench(refs, n, threads)
-        return {"value": n / sec, "unit": UNIT, "cores": threads, "kind": "reference",
-                "sample": f"{n} dpro::replay() calls over {len(refs)} of the workload's "
-                          f"candidate graphs on {threads} std::threads ({sec:.1f} s); graph "
-                          f"construction excluded",
-                "makespans": ms[: len(refs)].tolist()}
     t0 = time.perf_counter()
-    n = 0
-    while time.perf_counter() - t0 < budget_s:
-        oracle.port_replay(sample[n % len(sample)].csr)
-        n += 1
-    sec = time.perf_counter() - t0
-    return {"value": n / sec, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"{n} C-oracle replays (1 thread, {sec:.1f} s)"}
+    base = oracle.RefGraph.synth(specs_mod.synth_spec(spec))
+    log(f"reference synth: {base.n_ops} ops in {time.perf_counter() - t0:.1f} s")
+    out = []
+    for d in descs:
+        t1 = time.perf_counter()
+        if d[0] == "recompute":
+            g = base.apply_memory_strategy(3, {})
+        elif d[0] == "grad-accum":
+            g = base.apply_memory_strategy(4, {})
+        elif d[0] == "opf":
+            g = base.op_fusion(*specs_mod.opf_pair(d))
+        else:  # ("partition", ks)
+            g = base
+            for i, k in enumerate(d[1]):
+                if k != 1:
+                    g = g.partition(f"g{i}", int(k))
+        out.append(g)
+        log(f"reference candidate {d}: {g.n_ops} ops in {time.perf_counter() - t1:.1f} s")
+    return out, time.perf_counter() - t0
 
 
 def run_reference(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    S = _specs_module()
+    spec = S.workload_spec(args.config)
+    B = args.batch or spec["batch"]
     threads = os.cpu_count() or 1
-    w, graphs = build_candidates(args.config, min(args.batch, 4 * threads), 0, threads)
-    vals = []
-    cpu = None
-    per_step = min(args.ref_seconds, 150.0 / max(1, args.warmup + args.steps))
-    refs = ref_graphs(graphs, threads)  # once: the steps time only replay()
+    if spec["mix"] == "op_fusion":
+        descs = S.op_fusion_mix(spec["seed"], spec["workers"], spec["layers"], B, 0)
+        n_sample = args.ref_sample or 4
+    else:
+        pk = S.partition_specs(spec["seed"], spec["layers"], B, 0)
+        descs = [("partition", tuple(r)) for r in pk.tolist()]
+        n_sample = args.ref_sample or max(8, 2 * threads)
+    sample = descs[:n_sample]  # config 4: recompute, grad-accum, then op fusion
+    from oracle import oracle
+    graphs, build_s = ref_sample_graphs(S, spec, sample, log=lambda m: print(m, file=sys.stderr))
+    per_step = max(threads, len(graphs))  # replays per step: every thread busy
+    vals, step_ms = [], []
     for step in range(args.warmup + args.steps):
-        cpu = cpu_reference_time(graphs, budget_s=per_step, threads=threads, refs=refs)
+        t0 = time.perf_counter()
+        sec, ms = oracle.ref_replay_bench(graphs, per_step, threads)
+        wall = time.perf_counter() - t0
         if step >= args.warmup:
-            vals.append(cpu["value"])
+            vals.append(per_step / sec)
+            step_ms.append(1e3 * wall)
     value = float(np.mean(vals))
-    cpu = {k: v for k, v in cpu.items() if k != "makespans"}
-    cpu["value"] = value
+    cpu = {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+           "sample": f"each step: {per_step} dpro::replay() calls on {threads} std::threads over "
+                     f"{len(graphs)} of the workload's candidates ({[d[0] for d in sample]}), "
+                     f"built by the reference's generator + rewrites in {build_s:.0f} s "
+                     f"(excluded)",
+           "cpu_model": _cpu_model()}
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1000.0 * args.batch / value, "higher_is_better": True,
+        "ms_per_step": float(np.mean(step_ms)), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-        "config": {"workload": w.description, "batch": args.batch, "model": w.name,
-                   "n_ops": int(np.mean([g.n_ops for g in graphs]))},
+        "config": bench_config(spec, B, args.gpus),
         "cpu_baseline": cpu,
+        "reference_makespans": [int(x) for x in ms[: len(graphs)]],
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 
 
+def cpu_reference_sample(S, spec, descs, gpu_ms: np.ndarray, threads: int, budget_s: float):
+    """cpu_baseline of our line: the reference replay (oracle/_ref) timed on a
+    bounded sample of this batch's candidates, built by the reference; its
+    makespans must equal the GPU's for the same candidates."""
+    from oracle import oracle
+    if not oracle.ref_available():
+        return None, "oracle/_ref/libdpro_ref.so absent"
+    big = spec["mix"] == "op_fusion"
+    idx = [2, 3] if big and len(descs) > 3 else list(range(min(len(descs), max(8, threads))))
+    graphs, build_s = ref_sample_graphs(S, spec, [descs[i] for i in idx],
+                                        log=lambda m: print(m, file=sys.stderr))
+    # single thread: one replay
+    sec1, ms1 = oracle.ref_replay_bench(graphs[:1], 1, 1)
+    # all threads: as many concurrent replays as fit the budget
+    n = len(graphs) if big else max(len(graphs), int(budget_s / max(sec1, 1e-9)) * threads)
+    n = max(n, min(threads, len(graphs)))
+    secp, msp = oracle.ref_replay_bench(graphs, n, min(threads, n))
+    ok = all(int(msp[k]) == int(gpu_ms[idx[k % len(idx)]]) for k in range(len(graphs)))
+    assert ok, f"GPU makespans differ from the reference: {msp[:len(graphs)]} vs {gpu_ms[idx]}"
+    per_thread = 1.0 / sec1
+    used = min(threads, n)
+    measured = n / secp
+    out = {"value": measured if not big else per_thread * threads, "unit": UNIT,
+           "cores": threads, "kind": "reference", "cpu_model": _cpu_model(),
+           "single_thread_replays_per_s": per_thread,
+           "sample": (f"reference dpro::replay() on candidates {idx} of this batch, built by "
+                      f"the reference's generator + rewrites ({build_s:.0f} s, excluded); "
+                      f"1 replay on 1 thread: {sec1:.1f} s; {n} replays on {used} threads: "
+                      f"{secp:.1f} s ({measured:.3f}/s)" +
+                      (f"; value = {threads} threads x the single-thread rate (extrapolated: "
+                       f"replays are independent)" if big else "")),
+           "parity": f"reference makespans {[int(x) for x in msp[:len(graphs)]]} == GPU"}
+    return out, None
+
+
+# --------------------------------------------------------------------------
+# our arm
+# --------------------------------------------------------------------------
 def run_ours(args) -> None:
     import ctypes as C
 
@@ -211,16 +272,16 @@ def run_ours(args) -> None:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2205_02473_b200 import _native as N
     from paper_2205_02473_b200.engine import Engine
+    from paper_2205_02473_b200.exchange import exchange_best
     from paper_2205_02473_b200.ingest import LayeredBase
     from paper_2205_02473_b200.workloads import workload
 
     threads = max(1, (os.cpu_count() or 8) // max(world, 1))
     w = workload(args.config)
-    pk = w.candidate_partitions(args.batch, rank=rank)
-    specs = [([[i] for i in range(w.layers)], pk[c].tolist()) for c in range(args.batch)]
+    B = args.batch or w.batch
     t0 = time.perf_counter()
     base = LayeredBase(w.model, w.cluster)
-    deltas = base.deltas(specs, threads=threads)  # candidates as deltas of the base
+    deltas, descs = w.candidate_deltas(base, B, rank=rank, threads=threads)
     t_build = time.perf_counter() - t0
     stream = torch.cuda.current_stream()
     eng = Engine(local)
@@ -228,25 +289,21 @@ def run_ours(args) -> None:
     resident = eng.resident(base.graph().csr)  # base graph: uploaded once, stays in HBM
     batch = eng.delta_batch(resident, deltas)   # deltas uploaded once: inputs in HBM
     algo_bytes = batch.algorithmic_bytes()
-    B = batch.n
     mk_view = _device_view(batch.device_results()["makespan"], B, local)
+    dev = f"cuda:{local}"
 
     def exchange():
         # per-round best-cost exchange (K4): argmin over this rank's
-        # candidates, one packed int64 MIN all-reduce across ranks
+        # candidates, then MIN makespan / MIN (rank, index) across ranks
         best = torch.min(mk_view, dim=0)
-        key = (best.values << 24) | (rank << 20) | best.indices
         if dist is not None:
-            dist.all_reduce(key, op=dist.ReduceOp.MIN)
-        return key
-
-    def step():
-        batch.prepare()                    # K0 delta merge + pack kernel
-        batch.replay(want_schedule=True)   # K1 replay: makespan + per-op start/end
-        return exchange()
+            return exchange_best(dist, int(best.values), int(best.indices), rank, dev)
+        return best
 
     for _ in range(args.warmup):
-        step()
+        batch.prepare()
+        batch.replay(want_schedule=True)
+        exchange()
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
@@ -255,9 +312,9 @@ def run_ours(args) -> None:
         torch.cuda.synchronize()
         for i in range(args.steps):
             ev[i][0].record(stream)
-            batch.prepare()
+            batch.prepare()                    # K0 delta merge + pack kernel
             ev[i][1].record(stream)
-            batch.replay(want_schedule=True)
+            batch.replay(want_schedule=True)   # K1 replay: makespan + per-op start/end
             ev[i][2].record(stream)
             exchange()
             ev[i][3].record(stream)
@@ -266,24 +323,24 @@ def run_ours(args) -> None:
     kern_ms = [e[1].elapsed_time(e[2]) for e in ev]
     total_ms = ev[0][0].elapsed_time(ev[-1][3])
     if dist is not None:
-        t = torch.tensor([total_ms], device="cuda")
+        t = torch.tensor([total_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms, st, er, _, _ = batch.results()
     ok = int((st == 0).sum())
+    assert ok == B, f"{B - ok} candidates failed"
     kstats = batch.stats()
 
     # e2e through the C ABI with HOST buffers: the search's call
     # (dpro_cuda_replay_delta_batch: H2D of the deltas, merge, pack, replay,
-    # D2H of makespan/status/err), and for reference the full-CSR call
-    # (dpro_cuda_replay_batch: H2D of every candidate's CSR)
+    # D2H of makespan/status/err)
     hm = np.zeros(B, np.int64)
     hs = np.zeros(B, np.int32)
     he = np.zeros(B, np.int64)
 
-    def timed(fn):
+    def timed(fn, reps):
         out = []
-        for i in range(max(2, min(args.steps, 5)) + 1):
+        for i in range(reps + 1):
             torch.cuda.synchronize()
             if dist is not None:
                 dist.barrier()
@@ -294,22 +351,15 @@ def run_ours(args) -> None:
                 out.append(el)
         e = float(np.median(out))
         if dist is not None:
-            t = torch.tensor([e], device="cuda", dtype=torch.float64)
+            t = torch.tensor([e], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e = float(t.item())
         return e
 
     e2e_s = timed(lambda: N.lib.dpro_cuda_replay_delta_batch(
         eng.ctx, resident.handle, C.cast(deltas.array, C.c_void_p), B, N.ptr(hm), N.ptr(hs),
-        N.ptr(he)))
+        N.ptr(he)), max(2, min(args.steps, 3)))
     assert np.array_equal(hm, ms), "e2e makespans differ from the device-resident run"
-    graphs = base.candidates(specs, threads=threads)  # host-merged full CSRs
-    arr = (N.DproCsr * B)(*[g.csr.as_struct() for g in graphs])
-    hm2 = np.zeros(B, np.int64)
-    full_s = timed(lambda: N.lib.dpro_cuda_replay_batch(eng.ctx, arr, B, N.DPRO_HOST,
-                                                        N.ptr(hm2), None, None, N.ptr(hs),
-                                                        N.ptr(he)))
-    assert np.array_equal(hm2, ms), "full-CSR makespans differ from the delta run"
     h2d = int(sum(_delta_bytes(deltas[i]) for i in range(B)))
     d2h = B * (8 + 4 + 8)
 
@@ -321,47 +371,52 @@ def run_ours(args) -> None:
     kmean = float(np.mean(kern_ms)) / 1e3
     achieved = algo_bytes / kmean / 1e9
     value = world * B * args.steps / (total_ms / 1e3)
-    cpu = cpu_reference_time(graphs, budget_s=args.cpu_seconds, threads=os.cpu_count() or 1)
-    mk_cpu = cpu.pop("makespans", None)
-    if mk_cpu is not None:
-        assert mk_cpu == ms[: len(mk_cpu)].tolist(), "GPU makespans differ from the reference"
+    cpu, why = (None, "skipped (--cpu-seconds 0)")
+    if args.cpu_seconds > 0 and world == 1:
+        S = _specs_module()
+        cpu, why = cpu_reference_sample(S, S.workload_spec(args.config), descs, ms,
+                                        os.cpu_count() or 1, args.cpu_seconds)
+    traffic = _ncu_traffic(args.config)
     clocks = clk.summary()
+    n_ops = float(batch.n_ops.mean())
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
         "data": "synthetic",
-        "config": {"workload": w.description, "model": w.name, "batch_per_gpu": B,
-                   "global_batch": B * world, "n_ops_mean": float(batch.n_ops.mean()),
-                   "n_edges_mean": float(batch.n_edges.mean()),
-                   "parallelism": f"candidates sharded over {world} GPU(s)",
-                   "step": "delta merge (K0) + pack + replay (K1, per-op start/end) + "
-                           "best-cost exchange, inputs (base graph + deltas) resident in HBM",
-                   "l2": "per-step working set (%.2f GB of merged CSR + packed records) "
-                         "larger than L2; no flush" % (algo_bytes * 3 / 1e9),
-                   "node_updates_per_s": value * float(batch.n_ops.mean()),
-                   "prepare_ms_mean": float(np.mean(prep_ms)),
-                   "replay_ms_mean": kmean * 1e3,
-                   "replay_only_per_s": world * B / kmean,
-                   "build_s": round(t_build, 2), "status_ok": ok,
-                   "kernel": "replay_fast_kernel (general-path fallbacks: %d)" % kstats["fallbacks"],
-                   "fast_smem_bytes_per_candidate": kstats["fast_smem_bytes"],
-                   "fast_candidates_per_sm": kstats["fast_blocks_per_sm"]},
+        "config": bench_config(w.spec, B, world),
+        "details": {
+            "candidates": {k: sum(1 for d in descs if d[0] == k)
+                           for k in sorted({d[0] for d in descs})},
+            "n_ops_mean": n_ops, "n_edges_mean": float(batch.n_edges.mean()),
+            "step": "delta merge (K0) + pack + replay (K1, per-op start/end) + best-cost "
+                    "exchange, inputs (base graph + deltas) resident in HBM",
+            "node_updates_per_s": value * n_ops,
+            "prepare_ms_mean": float(np.mean(prep_ms)),
+            "replay_ms_mean": kmean * 1e3,
+            "replay_only_per_s": world * B / kmean,
+            "build_s": round(t_build, 2), "status_ok": ok,
+            "kernel": "replay_fast_kernel (general-path fallbacks: %d)" % kstats["fallbacks"],
+            "fast_smem_bytes_per_candidate": kstats["fast_smem_bytes"],
+            "fast_candidates_per_sm": kstats["fast_blocks_per_sm"],
+            "deep_ring_candidates": kstats["deep_ring_retries"]},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": _ncu_traffic(),
+                     "frac": achieved / peak,
+                     "traffic": traffic["dram_bytes_per_launch"] if traffic else None,
+                     "traffic_source": traffic.get("source") if traffic else None,
                      "kernel": "replay_fast_kernel",
-                     "algorithmic_bytes_per_launch": algo_bytes, "peak_source": peak_src,
-                     "kernel_ms_mean": kmean * 1e3},
-        "cpu_baseline": cpu,
+                     "algorithmic_bytes_per_launch": algo_bytes,
+                     "algorithmic_bytes": "32 V + 4 E per candidate (BASELINE.md section 2)",
+                     "peak_source": peak_src, "kernel_ms_mean": kmean * 1e3},
+        "cpu_baseline": cpu if cpu is not None else {"value": None, "unit": UNIT,
+                                                     "cores": 0, "kind": "reference",
+                                                     "sample": why},
         "e2e": {"value": world * B / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
                 "note": "dpro_cuda_replay_delta_batch with host deltas (H2D + merge + pack + "
-                        "replay, makespan-only) per step",
-                "full_csr": {"value": world * B / full_s,
-                             "h2d_bytes_per_step": int(sum(_packed_bytes(g) for g in graphs)),
-                             "note": "dpro_cuda_replay_batch with every candidate's host CSR"}},
-        # per step: delta_merge_kernel, pack_kernel, replay_fast_kernel pass 0 +
-        # deep-ring pass 1 (profiles/r01_delta_launches.csv)
+                        "replay, makespan-only) per step"},
+        # per step: delta_merge_kernel, pack_kernel, replay_fast_kernel x2
+        # (residency pass + deep-ring pass; profiles/r02_c4_launches.csv)
         "gpu_launches": 4 * args.steps,
         "clocks": clocks,
     }
@@ -372,17 +427,11 @@ def run_ours(args) -> None:
 
 def _delta_bytes(d) -> int:
     import ctypes as C
-    a = lambda x: (x + 15) & ~15
+    a = lambda x: (x + 15) & ~15  # noqa: E731
     nn = d.n_new
     ne = C.cast(d.new_succ_off, C.POINTER(C.c_uint32))[nn] if d.new_succ_off else 0
     return (a(4 * d.n_removed) + a(4 * nn) + a(8 * nn) + a(2 * nn) + a(nn) + a(4 * (nn + 1)) +
             a(4 * ne) + 2 * a(4 * d.n_extra) + a(4 * d.n_cut))
-
-
-def _packed_bytes(g) -> int:
-    n, e = g.n_ops, g.n_edges
-    a = lambda x: (x + 15) & ~15
-    return a(4 * n) + a(2 * n) + a(n) + a(4 * (n + 1)) + a(4 * e) + a(4 * n)
 
 
 def _device_view(ptr: int, n: int, device: int):
@@ -400,13 +449,15 @@ def _device_view(ptr: int, n: int, device: int):
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2)
-    ap.add_argument("--batch", type=int, default=1024)
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--ref-seconds", type=float, default=10.0)
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--batch", type=int, default=0, help="candidates per GPU (0: the config's)")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0,
+                    help="cpu_baseline budget (0: skip)")
+    ap.add_argument("--ref-sample", type=int, default=0,
+                    help="reference arm: candidate graphs built through oracle/_ref")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -452,6 +452,29 @@ class BaseGraphView(NativeGraph):
         self.handle = None
 
 
+class ConcatDeltas:
+    """Several delta sets as one candidate batch (a ctypes dpro_delta array
+    over their views; the sets stay alive here). Engine.delta_batch takes it
+    like a DeltaSet."""
+
+    def __init__(self, sets):
+        self._sets = list(sets)
+        items = [(s, i) for s in self._sets for i in range(len(s))]
+        self.n = len(items)
+        self.array = (N.DproDelta * max(1, self.n))(*[s[i] for s, i in items])
+        self._where = items
+
+    def __len__(self) -> int:
+        return self.n
+
+    def __getitem__(self, i: int) -> N.DproDelta:
+        return self.array[i]
+
+    def device_str(self, cand: int, d: int) -> str:
+        s, i = self._where[cand]
+        return s.device_str(i, d)
+
+
 class DeltaSet:
     """Owning handle of a dpro_delta_set (candidates as deltas)."""
 

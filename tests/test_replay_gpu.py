@@ -72,9 +72,14 @@ def test_reference_golden_vectors_bit_exact(mode_engine):
     _batch_check(mode_engine, graphs, [v["expect"] for v in vecs], "golden")
 
 
-@pytest.mark.parametrize("seed", range(4))
-def test_fuzz_against_c_oracle(mode_engine, port, seed):
-    engine = mode_engine
+_FUZZ: dict = {}
+
+
+def _fuzz_case(port, seed):
+    """1,500 fuzz graphs of one seed and their C-oracle expectations, built
+    once and shared by every engine mode (7 seeds: 10,500 graphs per mode)."""
+    if seed in _FUZZ:
+        return _FUZZ[seed]
     rng = np.random.default_rng(1000 + seed)
     graphs = []
     for t in range(1500):
@@ -104,7 +109,14 @@ def test_fuzz_against_c_oracle(mode_engine, port, seed):
             stuck = [g.op_at(j).id for j in np.flatnonzero(o["scheduled"] == 0)]
             expects.append({"status": 2, "cycle": stuck,
                             "message": f"replay requires an acyclic graph; {o['err']} ops never became ready"})
-    _batch_check(engine, graphs, expects, f"fuzz{seed}")
+    _FUZZ[seed] = (graphs, expects)
+    return _FUZZ[seed]
+
+
+@pytest.mark.parametrize("seed", range(7))
+def test_fuzz_against_c_oracle(mode_engine, port, seed):
+    graphs, expects = _fuzz_case(port, seed)
+    _batch_check(mode_engine, graphs, expects, f"fuzz{seed}")
 
 
 # ---- proj/tests/test_replay.cpp, through the reference-shaped API ----------
