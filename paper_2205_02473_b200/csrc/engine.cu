@@ -23,6 +23,7 @@
 #include "memory_kernel.cuh"
 #include "delta_kernel.cuh"
 #include "dpro_cuda.h"
+#include "overlay.h"
 #include "pack_kernel.cuh"
 #include "replay_fast.cuh"
 #include "replay_kernel.cuh"
@@ -210,6 +211,8 @@ struct dpro_ctx {
   int warps = 0;      // option "warps": warps (1, 2, 4, 8) per candidate; 0 = by device count
   int gcnt = 0;       // option "gcnt": 1 = fast-path counters always in global scratch
   int deep_first = -1;  // option "deep_first": -1 auto (mean V > 1M), 0 never, 1 always
+  int overlay = 0;      // option "overlay": 1 = delta batches replay on the base + overlays
+  DevBuf gring;         // pass 3 of the fast kernels: device rings in global memory
   dpro_batch* spare = nullptr;  // recycled arenas for repeated small calls
 };
 
@@ -219,6 +222,48 @@ struct dpro_resident {
   uint32_t n = 0, e = 0, d = 0;
   bool dur32 = true;
   std::vector<uint32_t> succ_off, succ, indeg;  // host copy (edge counts)
+  std::vector<int64_t> dur_h;                   // host copies for the overlay builder
+  std::vector<uint16_t> dev_h;
+  std::vector<uint8_t> flags_h;
+  // overlay batches (overlay.h): the base packed once (a 1-candidate batch
+  // over the resident CSR) and its host view
+  dpro_batch* packed = nullptr;
+  dpro_ov::BaseHost bh;
+  dpro_k::OvBase ob{};
+  ~dpro_resident();
+};
+
+// A deep host copy of a dpro_delta (overlay batches re-run rare candidates
+// through the materialized path after the replay).
+struct DeltaCopy {
+  dpro_delta d{};
+  std::vector<uint32_t> removed, new_pos, new_succ_off, new_succ, extra_src, extra_dst, cut;
+  std::vector<int64_t> new_dur;
+  std::vector<uint16_t> new_dev;
+  std::vector<uint8_t> new_flags;
+  void set(const dpro_delta& x) {
+    removed.assign(x.removed, x.removed + x.n_removed);
+    new_pos.assign(x.new_pos, x.new_pos + x.n_new);
+    new_dur.assign(x.new_dur, x.new_dur + x.n_new);
+    new_dev.assign(x.new_dev, x.new_dev + x.n_new);
+    new_flags.assign(x.new_flags, x.new_flags + x.n_new);
+    new_succ_off.assign(x.new_succ_off, x.new_succ_off + x.n_new + 1);
+    new_succ.assign(x.new_succ, x.new_succ + x.new_succ_off[x.n_new]);
+    extra_src.assign(x.extra_src, x.extra_src + x.n_extra);
+    extra_dst.assign(x.extra_dst, x.extra_dst + x.n_extra);
+    cut.assign(x.cut, x.cut + x.n_cut);
+    d = x;
+    d.removed = removed.data();
+    d.new_pos = new_pos.data();
+    d.new_dur = new_dur.data();
+    d.new_dev = new_dev.data();
+    d.new_flags = new_flags.data();
+    d.new_succ_off = new_succ_off.data();
+    d.new_succ = new_succ.data();
+    d.extra_src = extra_src.data();
+    d.extra_dst = extra_dst.data();
+    d.cut = cut.data();
+  }
 };
 
 struct dpro_batch {
@@ -250,7 +295,22 @@ struct dpro_batch {
   std::vector<dpro_k::PackInfo> info;  // host copy (read once after pack)
   bool replayed = false;
   bool with_schedule = false;
+  // overlay batches: candidates replayed on the resident base + overlays
+  bool overlay = false;
+  std::vector<dpro_ov::OverlayHost> ovh;
+  std::vector<DeltaCopy> dcopy;
+  std::vector<size_t> ov_off;   // per candidate byte offset in ovstage / ovarena
+  size_t ov_bytes = 0;
+  DevBuf ovarena;               // overlay arrays
+  DevBuf ovdesc;                // OvCand[n]
+  DevBuf ovgcnt;                // global counters (when they do not fit smem)
+  std::vector<dpro_k::OvCand> ovc;
+  std::vector<uint8_t> ovstage; // host image of ovarena
+  uint32_t max_cnt_ov = 0;      // max base + overlay counters of a candidate
+  int32_t n_mat = 0;            // candidates re-run through the materialized path
 };
+
+dpro_resident::~dpro_resident() { delete packed; }
 
 namespace {
 
@@ -513,7 +573,7 @@ int alloc_batch(dpro_ctx* ctx, dpro_batch* b, const std::vector<uint32_t>& e_cap
   if (upload_desc)
     CU(cudaMemcpyAsync(b->desc.p, b->hc.data(), sizeof(Cand) * n, cudaMemcpyHostToDevice,
                        ctx->stream));
-  CU(b->work.ensure(16));
+  CU(b->work.ensure(32));
   // packed replay layout (pack_kernel.cuh)
   {
     std::vector<unsigned long long> r_off(n), e_off(n), c_off(n);
@@ -670,6 +730,8 @@ dpro_batch* acquire_batch(dpro_ctx* ctx, int32_t n, int32_t memspace) {
     b->sum_n = b->sum_d = b->sum_dof = b->sum_e = 0;
     b->max_d = 0;
     b->replayed = b->with_schedule = false;
+    b->overlay = false;
+    b->n_mat = 0;
   } else {
     b = new dpro_batch;
   }
@@ -983,6 +1045,243 @@ int run_merge(dpro_ctx* ctx, dpro_batch* b, int32_t c0, int32_t c1) {
   return DPRO_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Overlay batches (overlay.h): delta candidates replayed on the resident
+// base's packed layout plus per-candidate overlays -- no per-candidate copy
+// of the graph, so far more candidates are resident at once.
+// ---------------------------------------------------------------------------
+
+// Packs the resident base once (a 1-candidate batch over its device CSR)
+// and builds the host view the overlay builder reads.
+int ensure_base_packed(dpro_ctx* ctx, dpro_resident* r) {
+  if (r->packed) return DPRO_OK;
+  Tracer tr;
+  dpro_csr c{r->n, r->e, r->d, r->dur32 ? 32 : 64, r->dev.dur, r->dev.dev, r->dev.flags,
+             r->dev.succ_off, r->dev.succ, nullptr};
+  auto* pb = new dpro_batch;
+  pb->n = 1;
+  pb->memspace = DPRO_DEVICE;
+  const int st = build_batch(ctx, pb, &c);
+  if (st != DPRO_OK) {
+    delete pb;
+    return st;
+  }
+  r->packed = pb;
+  dpro_ov::BaseHost& B = r->bh;
+  const dpro_k::PackInfo& inf = pb->info[0];
+  B.n = r->n;
+  B.e = r->e;
+  B.d = r->d;
+  B.dur = r->dur_h;
+  B.dev = r->dev_h;
+  B.flags = r->flags_h;
+  B.succ_off = r->succ_off;
+  B.succ = r->succ;
+  B.indeg = r->indeg;
+  B.ok = (inf.not_fast & ~dpro_k::kWideCnt) == 0;
+  B.wide = inf.wide != 0;
+  B.n_cnt = inf.n_cnt;
+  B.rec.resize(4 * (size_t(r->n) + 1));
+  CU(cudaMemcpyAsync(B.rec.data(), pb->P.rec, 16 * (size_t(r->n) + 1), cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  B.pred_off.assign(r->n + 1, 0);
+  for (uint32_t x : r->succ) B.pred_off[x + 1]++;
+  for (uint32_t i = 0; i < r->n; ++i) B.pred_off[i + 1] += B.pred_off[i];
+  B.pred.resize(r->e);
+  {
+    std::vector<uint32_t> fill(B.pred_off.begin(), B.pred_off.end() - 1);
+    for (uint32_t u = 0; u < r->n; ++u)
+      for (uint32_t e = r->succ_off[u]; e < r->succ_off[u + 1]; ++e) B.pred[fill[r->succ[e]]++] = u;
+  }
+  B.devcnt.assign(r->d, 0);
+  B.srcs.clear();
+  B.missing.clear();
+  for (uint32_t i = 0; i < r->n; ++i) {
+    const bool v = B.flags[i] & DPRO_FLAG_VIRTUAL;
+    if (!v && B.dev[i] < r->d) B.devcnt[B.dev[i]]++;
+    if (B.indeg[i] == 0) B.srcs.push_back(i);
+    if (!v && B.dur[i] < 0) B.missing.push_back(i);
+  }
+  r->ob = {pb->P.rec, pb->P.erec, pb->P.cnt0, B.n_cnt, B.wide ? 1u : 0u};
+  tr.mark("base packed for overlays");
+  return DPRO_OK;
+}
+
+// Host image of every candidate's overlay arrays (b->ovstage, offsets in
+// b->ov_off) and the OvCand descriptors pointing into b->ovarena.
+int stage_overlays(dpro_ctx* ctx, dpro_batch* b) {
+  const int32_t n = b->n;
+  const dpro_resident* r = b->res;
+  b->ov_off.assign(n + 1, 0);
+  size_t o = 0;
+  auto sz = [](size_t bytes) { return align16(bytes); };
+  for (int32_t i = 0; i < n; ++i) {
+    const auto& O = b->ovh[i];
+    b->ov_off[i] = o;
+    if (!O.fast) continue;
+    o += sz(O.rec.size() * 4) + sz(O.erec.size() * 4) + sz(O.fin.size() * 4) +
+         sz(O.cnt.size() * 2) + sz(O.src.size() * 4) + sz(O.blk.size() * 4) + sz(O.ovf.size() * 4);
+  }
+  b->ov_off[n] = o;
+  b->ov_bytes = o;
+  b->ovstage.resize(std::max<size_t>(o, 16));
+  CU(b->ovarena.ensure(std::max<size_t>(o, 16)));
+  b->ovc.assign(n, dpro_k::OvCand{});
+  // global counter slices (u16, base + overlay counters)
+  std::vector<unsigned long long> goff(n + 1, 0);
+  b->max_cnt_ov = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    const uint32_t nc = r->bh.n_cnt + static_cast<uint32_t>(b->ovh[i].cnt.size());
+    b->max_cnt_ov = std::max(b->max_cnt_ov, nc);
+    goff[i + 1] = goff[i] + align16(size_t(nc) * 2);
+  }
+  CU(b->ovgcnt.ensure(std::max<size_t>(goff[n], 16)));
+  ctx->workers().run(n, [&](int32_t i) {
+    const auto& O = b->ovh[i];
+    dpro_k::OvCand& c = b->ovc[i];
+    c.gcnt_off = goff[i];
+    c.first_missing = O.first_missing;
+    if (!O.fast) {
+      c.pad = 1;  // materialized path
+      return;
+    }
+    size_t q = b->ov_off[i];
+    auto put = [&](const void* src, size_t bytes) {
+      if (bytes) std::memcpy(b->ovstage.data() + q, src, bytes);
+      const char* dptr = b->ovarena.as<char>(q);
+      q += align16(bytes);
+      return dptr;
+    };
+    c.v.rec = reinterpret_cast<const uint4*>(put(O.rec.data(), O.rec.size() * 4));
+    c.v.erec = reinterpret_cast<const uint4*>(put(O.erec.data(), O.erec.size() * 4));
+    c.v.fin = reinterpret_cast<const uint32_t*>(put(O.fin.data(), O.fin.size() * 4));
+    c.cnt = reinterpret_cast<const uint16_t*>(put(O.cnt.data(), O.cnt.size() * 2));
+    c.src = reinterpret_cast<const uint4*>(put(O.src.data(), O.src.size() * 4));
+    c.v.blk = reinterpret_cast<const uint32_t*>(put(O.blk.data(), O.blk.size() * 4));
+    c.v.ovf = reinterpret_cast<const uint32_t*>(put(O.ovf.data(), O.ovf.size() * 4));
+    c.n_cnt = static_cast<uint32_t>(O.cnt.size());
+    c.n_src = static_cast<uint32_t>(O.src.size() / 4);
+    c.pad = 0;
+  });
+  return DPRO_OK;
+}
+
+// H2D of the staged overlays, descriptors and timeline regions: the
+// device-side preparation of an overlay batch (dpro_cuda_batch_prepare).
+int upload_overlays(dpro_ctx* ctx, dpro_batch* b) {
+  const int32_t n = b->n;
+  if (b->ov_bytes)
+    CU(cudaMemcpyAsync(b->ovarena.p, b->ovstage.data(), b->ov_bytes, cudaMemcpyHostToDevice,
+                       ctx->stream));
+  CU(b->ovdesc.ensure(sizeof(dpro_k::OvCand) * std::max(n, 1)));
+  if (n)
+    CU(cudaMemcpyAsync(b->ovdesc.p, b->ovc.data(), sizeof(dpro_k::OvCand) * n,
+                       cudaMemcpyHostToDevice, ctx->stream));
+  return DPRO_OK;
+}
+
+int build_overlay_batch(dpro_ctx* ctx, dpro_batch* b, dpro_resident* r,
+                        const dpro_delta* deltas) {
+  Tracer tr;
+  const int32_t n = b->n;
+  int st = ensure_base_packed(ctx, r);
+  if (st != DPRO_OK) return st;
+  b->res = r;
+  b->overlay = true;
+  b->ovh.resize(n);
+  b->dcopy.resize(n);
+  b->hc.assign(n, Cand{});
+  b->n_ops.resize(n);
+  b->n_dev.resize(n);
+  b->n_edges.resize(n);
+  std::vector<std::string> errs(n);
+  ctx->workers().run(n, [&](int32_t i) {
+    uint32_t v = 0, e = 0;
+    bool d32 = true;
+    errs[i] = check_delta(*r, deltas[i], v, e, d32);
+    if (!errs[i].empty()) return;
+    b->n_ops[i] = v;
+    b->n_edges[i] = e;
+    b->n_dev[i] = deltas[i].n_devices;
+    b->dcopy[i].set(deltas[i]);
+    dpro_ov::build_overlay(r->bh, b->dcopy[i].d, b->ovh[i]);
+  });
+  for (int32_t i = 0; i < n; ++i)
+    if (!errs[i].empty())
+      return set_err(ctx, DPRO_EINVAL, "delta " + std::to_string(i) + ": " + errs[i]);
+  tr.mark("overlays built");
+  unsigned long long so = 0, sd = 0, sdo = 0, se = 0;
+  b->n_mat = 0;
+  b->max_d = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    Cand& h = b->hc[i];
+    h.n = b->n_ops[i];
+    h.e = b->n_edges[i];
+    h.d = b->n_dev[i];
+    h.op_off = so;
+    h.dev_off = sd;
+    h.dof_off = sdo;
+    so += h.n;
+    sd += h.d;
+    sdo += h.d + 1;
+    se += h.e;
+    b->max_d = std::max(b->max_d, h.d);
+    b->n_mat += b->ovh[i].fast ? 0 : 1;
+  }
+  b->sum_n = so;
+  b->sum_d = sd;
+  b->sum_dof = sdo;
+  b->sum_e = se;
+  // scratch (timelines, regions, per-device busy / dispatched prefix) and outputs
+  const size_t s_u32 = align16(so * 4 + 4), s_dof = align16(sdo * 4 + 4),
+               s_busy = align16(sd * 8 + 8), s_dh = align16(sd * 4 + 4),
+               s_u8 = align16(so + 1);
+  CU(b->scratch.ensure(2 * s_u32 + s_dof + s_busy + s_dh + s_u8));
+  size_t o = 0;
+  b->S = Scratch{};
+  b->S.qbuf = b->scratch.as<uint32_t>(o); o += s_u32;
+  b->S.qpos = b->scratch.as<uint32_t>(o); o += s_u32;
+  b->S.devoff = b->scratch.as<uint32_t>(o); o += s_dof;
+  b->S.busy = b->scratch.as<long long>(o); o += s_busy;
+  b->S.dhead = b->scratch.as<uint32_t>(o); o += s_dh;
+  b->S.sched = b->scratch.as<uint8_t>(o); o += s_u8;
+  const size_t o_b64 = align16(size_t(n) * 8 + 8), o_b32 = align16(size_t(n) * 4 + 4),
+               o_op = align16(so * 8 + 8);
+  CU(b->outs.ensure(2 * o_b64 + o_b32 + 2 * o_op));
+  o = 0;
+  b->O.makespan = b->outs.as<long long>(o); o += o_b64;
+  b->O.err = b->outs.as<long long>(o); o += o_b64;
+  b->O.status = b->outs.as<int>(o); o += o_b32;
+  b->O.start = b->outs.as<long long>(o); o += o_op;
+  b->O.end = b->outs.as<long long>(o); o += o_op;
+  CU(b->desc.ensure(sizeof(Cand) * std::max(n, 1)));
+  if (n) CU(cudaMemcpyAsync(b->desc.p, b->hc.data(), sizeof(Cand) * n, cudaMemcpyHostToDevice,
+                            ctx->stream));
+  CU(b->work.ensure(32));
+  {  // timeline regions from the overlays (materialized candidates: their pack)
+    std::vector<uint32_t> dof(std::max<unsigned long long>(sdo, 1), 0);
+    for (int32_t i = 0; i < n; ++i)
+      if (b->ovh[i].fast)
+        std::copy(b->ovh[i].devoff.begin(), b->ovh[i].devoff.end(), dof.begin() + b->hc[i].dof_off);
+    if (sdo) CU(cudaMemcpyAsync(b->S.devoff, dof.data(), sdo * 4, cudaMemcpyHostToDevice,
+                                ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));  // dof is a local
+  }
+  st = stage_overlays(ctx, b);
+  if (st != DPRO_OK) return st;
+  st = upload_overlays(ctx, b);
+  if (st != DPRO_OK) return st;
+  b->info.assign(n, dpro_k::PackInfo{});
+  for (int32_t i = 0; i < n; ++i) {
+    b->info[i].first_missing = b->ovh[i].first_missing;
+    b->info[i].not_fast = b->ovh[i].fast ? 0u : 1u;
+  }
+  b->replayed = b->with_schedule = false;
+  tr.mark("overlay batch staged + uploaded", ctx->stream, true);
+  return DPRO_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1003,6 +1302,12 @@ dpro_resident* dpro_cuda_resident_create(dpro_ctx* ctx, const dpro_csr* c) {
   r->succ.assign(c->succ, c->succ + c->n_edges);
   r->indeg.assign(c->n_ops, 0);
   for (uint32_t x : r->succ) r->indeg.at(x)++;
+  r->dev_h.assign(c->dev, c->dev + c->n_ops);
+  r->flags_h.assign(c->flags, c->flags + c->n_ops);
+  r->dur_h.resize(c->n_ops);
+  for (uint32_t i = 0; i < c->n_ops; ++i)
+    r->dur_h[i] = c->dur_bits == 32 ? static_cast<const int32_t*>(c->dur)[i]
+                                    : static_cast<const int64_t*>(c->dur)[i];
   r->dur32 = c->dur_bits == 32 || fits_i32(static_cast<const int64_t*>(c->dur), c->n_ops);
   const size_t v = c->n_ops, sd = align16(v * (r->dur32 ? 4 : 8)), s2 = align16(v * 2),
                s1 = align16(v), so = align16((v + 1) * 4), se = align16(size_t(c->n_edges) * 4);
@@ -1054,6 +1359,16 @@ dpro_batch* dpro_cuda_batch_create_delta(dpro_ctx* ctx, const dpro_resident* r,
     return nullptr;
   }
   cudaSetDevice(ctx->device);
+  if (ctx->overlay) {
+    auto* b = new dpro_batch;
+    b->n = n;
+    b->memspace = DPRO_DEVICE;
+    if (build_overlay_batch(ctx, b, const_cast<dpro_resident*>(r), deltas) != DPRO_OK) {
+      delete b;
+      return nullptr;
+    }
+    return b;
+  }
   dpro_batch* b = acquire_batch(ctx, n, DPRO_DEVICE);
   if (build_delta_batch(ctx, b, r, deltas) != DPRO_OK) {
     delete b;
@@ -1088,6 +1403,7 @@ int dpro_cuda_batch_pack_info(dpro_batch* b, uint32_t* out) {
 int dpro_cuda_batch_prepare(dpro_ctx* ctx, dpro_batch* b) {
   if (!ctx || !b) return DPRO_EINVAL;
   CU(cudaSetDevice(ctx->device));
+  if (b->overlay) return upload_overlays(ctx, b);
   if (b->res) {
     const int st = run_merge(ctx, b, 0, b->n);
     if (st != DPRO_OK) return st;
@@ -1151,6 +1467,10 @@ int dpro_cuda_set_option(dpro_ctx* ctx, const char* key, int64_t value) {
     ctx->host_threads = static_cast<int>(value);
     return DPRO_OK;
   }
+  if (k == "overlay" && (value == 0 || value == 1)) {
+    ctx->overlay = static_cast<int>(value);
+    return DPRO_OK;
+  }
   if (k == "gcnt" && (value == 0 || value == 1)) {
     ctx->gcnt = static_cast<int>(value);
     return DPRO_OK;
@@ -1198,6 +1518,27 @@ size_t fast_bytes(uint32_t dcap, uint32_t qc, uint32_t rl, uint32_t ccap, int nw
          4 * dpro_k::fast_misc_words(nw) + ccap;
 }
 
+// Pass 3 (after the deep-ring pass): candidates whose device queues
+// outgrew even the deepest shared-memory rings (e.g. the grad-accum variant
+// of config 4: a 230-deep link queue), rings in global memory (one slice
+// per CTA, one CTA per SM). Returns false when there is nothing to gain.
+bool pass3_cfg(dpro_ctx* ctx, const FastCfg& deep, int nw, FastCfg& G) {
+  constexpr size_t kBudget = size_t(512) << 20;
+  G = deep;
+  G.qc = 4096;
+  while (G.qc > deep.qc && size_t(ctx->sm_count) * G.dcap * G.qc * 16 > kBudget) G.qc /= 2;
+  if (G.qc <= deep.qc) return false;
+  G.rl = 8192;
+  if (ctx->gring.ensure(size_t(ctx->sm_count) * G.dcap * G.qc * 16) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  G.gq = ctx->gring.as<uint4>();
+  G.warp_bytes = static_cast<uint32_t>(size_t(G.dcap) * sizeof(dpro_k::DevF) + 8 * size_t(G.rl) +
+                                       4 * dpro_k::fast_misc_words(nw) + G.ccap);
+  return G.warp_bytes + 1024 <= ctx->smem_optin;
+}
+
 template <int NW, int KD>
 int launch_fast_kd(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule, FastCfg F) {
   auto kern = dpro_k::replay_fast_kernel<NW, KD>;
@@ -1211,7 +1552,7 @@ int launch_fast_kd(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule, FastCfg 
   blocks_per_sm = std::max(blocks_per_sm, 1);
   b->blocks_per_sm_fast = blocks_per_sm;
   const int grid = std::max(1, std::min(b->n, ctx->sm_count * blocks_per_sm));
-  CU(cudaMemsetAsync(b->work.p, 0, 16, ctx->stream));
+  CU(cudaMemsetAsync(b->work.p, 0, 32, ctx->stream));
   b->F = F;
   // graphs of millions of ops (configs 4/5) overflow the residency-sized
   // rings every time: send them straight to the deep-ring pass
@@ -1233,6 +1574,13 @@ int launch_fast_kd(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule, FastCfg 
       b->desc.as<Cand>(), b->n, b->S, b->O, b->P, D, want_schedule ? 1 : 0,
       b->work.as<unsigned>(), 1);
   CU(cudaGetLastError());
+  FastCfg G;
+  if (pass3_cfg(ctx, D, NW, G)) {
+    kern<<<ctx->sm_count, 32 * NW, G.warp_bytes, ctx->stream>>>(
+        b->desc.as<Cand>(), b->n, b->S, b->O, b->P, G, want_schedule ? 1 : 0,
+        b->work.as<unsigned>(), 3);
+    CU(cudaGetLastError());
+  }
   return DPRO_OK;
 }
 
@@ -1295,6 +1643,142 @@ int launch_fast(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
   }
 }
 
+// Overlay batches: replay_ov_kernel, the same two passes as the fast path.
+template <int NW, int KD>
+int launch_ov_kd(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule, FastCfg F) {
+  auto kern = dpro_k::replay_ov_kernel<NW, KD>;
+  cudaFuncAttributes fa{};
+  CU(cudaFuncGetAttributes(&fa, kern));
+  const size_t dyn_max = ctx->smem_optin - fa.sharedSizeBytes;
+  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_max));
+  int blocks_per_sm = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, 32 * NW, F.warp_bytes));
+  blocks_per_sm = std::max(blocks_per_sm, 1);
+  b->blocks_per_sm_fast = blocks_per_sm;
+  const int grid = std::max(1, std::min(b->n, ctx->sm_count * blocks_per_sm));
+  CU(cudaMemsetAsync(b->work.p, 0, 32, ctx->stream));
+  b->F = F;
+  const dpro_resident* r = b->res;
+  kern<<<grid, 32 * NW, F.warp_bytes, ctx->stream>>>(
+      b->desc.as<Cand>(), b->ovdesc.as<dpro_k::OvCand>(), b->n, r->ob, b->S, b->O,
+      b->ovgcnt.as<uint8_t>(), F, want_schedule ? 1 : 0, b->work.as<unsigned>(), 0);
+  CU(cudaGetLastError());
+  FastCfg D = F;  // pass 1: ring overflows, one CTA per SM, deepest rings
+  D.rl = std::max<uint32_t>(F.rl, 2048);
+  while (D.qc < 4096 && fast_bytes(D.dcap, D.qc * 2, D.rl, D.ccap, NW) <= dyn_max) D.qc *= 2;
+  D.warp_bytes = static_cast<uint32_t>(fast_bytes(D.dcap, D.qc, D.rl, D.ccap, NW));
+  kern<<<ctx->sm_count, 32 * NW, D.warp_bytes, ctx->stream>>>(
+      b->desc.as<Cand>(), b->ovdesc.as<dpro_k::OvCand>(), b->n, r->ob, b->S, b->O,
+      b->ovgcnt.as<uint8_t>(), D, want_schedule ? 1 : 0, b->work.as<unsigned>(), 1);
+  CU(cudaGetLastError());
+  FastCfg G;
+  if (pass3_cfg(ctx, D, NW, G)) {
+    kern<<<ctx->sm_count, 32 * NW, G.warp_bytes, ctx->stream>>>(
+        b->desc.as<Cand>(), b->ovdesc.as<dpro_k::OvCand>(), b->n, r->ob, b->S, b->O,
+        b->ovgcnt.as<uint8_t>(), G, want_schedule ? 1 : 0, b->work.as<unsigned>(), 3);
+    CU(cudaGetLastError());
+  }
+  return DPRO_OK;
+}
+
+template <int NW>
+int launch_ov_nw(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
+  FastCfg F;
+  F.qc = ctx->ring;
+  F.rl = 128;
+  const uint32_t nt = 32 * NW;
+  uint32_t kd = std::max<uint32_t>(1, (b->max_d + nt - 1) / nt);
+  if (kd > 8) kd = kd <= 12 ? 12 : 16;
+  F.kd = kd;
+  F.dcap = std::max<uint32_t>(1, std::min<uint32_t>(b->max_d, nt * kd));
+  F.ccap = (2 * b->max_cnt_ov + 15) & ~15u;  // u16 counters
+  const size_t limit = ctx->smem_optin - 64;
+  if (ctx->gcnt || fast_bytes(F.dcap, F.qc, F.rl, F.ccap, NW) > size_t(ctx->smem_per_sm) / 4)
+    F.ccap = 16;
+  while (fast_bytes(F.dcap, F.qc, F.rl, F.ccap, NW) > limit && F.dcap > 1) F.dcap /= 2;
+  const size_t target = std::max<size_t>(fast_bytes(F.dcap, F.qc, F.rl, F.ccap, NW),
+                                         size_t(ctx->smem_per_sm) / 8 - 1024);
+  while (F.qc < 64 && fast_bytes(F.dcap, F.qc * 2, F.rl, F.ccap, NW) <= std::min(target, limit))
+    F.qc *= 2;
+  F.warp_bytes = static_cast<uint32_t>(fast_bytes(F.dcap, F.qc, F.rl, F.ccap, NW));
+  switch (kd) {
+    case 1: return launch_ov_kd<NW, 1>(ctx, b, want_schedule, F);
+    case 2: return launch_ov_kd<NW, 2>(ctx, b, want_schedule, F);
+    case 3: return launch_ov_kd<NW, 3>(ctx, b, want_schedule, F);
+    case 4: return launch_ov_kd<NW, 4>(ctx, b, want_schedule, F);
+    case 5: return launch_ov_kd<NW, 5>(ctx, b, want_schedule, F);
+    case 6: return launch_ov_kd<NW, 6>(ctx, b, want_schedule, F);
+    case 7: return launch_ov_kd<NW, 7>(ctx, b, want_schedule, F);
+    case 8: return launch_ov_kd<NW, 8>(ctx, b, want_schedule, F);
+    default: return set_err(ctx, DPRO_EUNSUPPORTED, "overlay replay: too many devices");
+  }
+}
+
+// Candidates the overlay replay could not finish (materialized: !fast
+// overlays, kRetryMat after the kernel) re-run as an ordinary delta batch;
+// their results are copied into this batch's layout.
+int finish_overlay_mat(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
+  unsigned w[4] = {0, 0, 0, 0};
+  CU(cudaMemcpyAsync(w, b->work.p, 16, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  if (b->n_mat == 0 && w[1] == 0) return DPRO_OK;
+  std::vector<int32_t> stv(b->n);
+  CU(cudaMemcpy(stv.data(), b->O.status, 4 * size_t(b->n), cudaMemcpyDeviceToHost));
+  std::vector<int32_t> idx;
+  std::vector<dpro_delta> ds;
+  for (int32_t i = 0; i < b->n; ++i)
+    if (!b->ovh[i].fast || stv[i] == dpro_k::kRetryMat) {
+      idx.push_back(i);
+      ds.push_back(b->dcopy[i].d);
+    }
+  if (idx.empty()) return DPRO_OK;
+  dpro_batch sub;
+  sub.n = static_cast<int32_t>(idx.size());
+  sub.memspace = DPRO_DEVICE;
+  int st = build_delta_batch(ctx, &sub, b->res, ds.data());
+  if (st != DPRO_OK) return st;
+  st = ctx->fast ? launch_fast(ctx, &sub, want_schedule) : launch_general(ctx, &sub, want_schedule);
+  if (st != DPRO_OK) return st;
+  for (size_t k = 0; k < idx.size(); ++k) {
+    const Cand& p = b->hc[idx[k]];
+    const Cand& q = sub.hc[k];
+    auto cp = [&](void* dst, const void* src, size_t bytes) {
+      return bytes ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, ctx->stream)
+                   : cudaSuccess;
+    };
+    const int32_t i = idx[k];
+    CU(cp(b->O.makespan + i, sub.O.makespan + k, 8));
+    CU(cp(b->O.err + i, sub.O.err + k, 8));
+    CU(cp(b->O.status + i, sub.O.status + k, 4));
+    if (want_schedule) {
+      CU(cp(b->O.start + p.op_off, sub.O.start + q.op_off, 8 * size_t(p.n)));
+      CU(cp(b->O.end + p.op_off, sub.O.end + q.op_off, 8 * size_t(p.n)));
+    }
+    CU(cp(b->S.qbuf + p.op_off, sub.S.qbuf + q.op_off, 4 * size_t(p.n)));
+    CU(cp(b->S.qpos + p.op_off, sub.S.qpos + q.op_off, 4 * size_t(p.n)));
+    CU(cp(b->S.sched + p.op_off, sub.S.sched + q.op_off, size_t(p.n)));
+    CU(cp(b->S.devoff + p.dof_off, sub.S.devoff + q.dof_off, 4 * (size_t(p.d) + 1)));
+    CU(cp(b->S.busy + p.dev_off, sub.S.busy + q.dev_off, 8 * size_t(p.d)));
+    CU(cp(b->S.dhead + p.dev_off, sub.S.dhead + q.dev_off, 4 * size_t(p.d)));
+  }
+  CU(cudaStreamSynchronize(ctx->stream));  // sub's buffers die here
+  return DPRO_OK;
+}
+
+int launch_overlay(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
+  int nw = ctx->warps;
+  if (nw == 0) nw = b->max_d <= 32 ? 1 : b->max_d <= 64 ? 2 : 4;
+  int st;
+  switch (nw) {
+    case 1: st = launch_ov_nw<1>(ctx, b, want_schedule); break;
+    case 2: st = launch_ov_nw<2>(ctx, b, want_schedule); break;
+    case 8: st = launch_ov_nw<8>(ctx, b, want_schedule); break;
+    default: st = launch_ov_nw<4>(ctx, b, want_schedule); break;
+  }
+  if (st != DPRO_OK) return st;
+  return finish_overlay_mat(ctx, b, want_schedule);
+}
+
 }  // namespace
 
 extern "C" {
@@ -1307,8 +1791,9 @@ int dpro_cuda_batch_replay(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) 
     return DPRO_OK;
   }
   CU(cudaSetDevice(ctx->device));
-  const int st = ctx->fast ? launch_fast(ctx, b, want_schedule)
-                           : launch_general(ctx, b, want_schedule);
+  const int st = b->overlay ? launch_overlay(ctx, b, want_schedule)
+                 : ctx->fast ? launch_fast(ctx, b, want_schedule)
+                             : launch_general(ctx, b, want_schedule);
   if (st != DPRO_OK) return st;
   b->replayed = true;
   b->with_schedule = want_schedule != 0;
@@ -1409,6 +1894,9 @@ int dpro_cuda_batch_critical_paths(dpro_ctx* ctx, dpro_batch* b,
   if (!ctx || !b) return DPRO_EINVAL;
   if (!b->replayed || !b->with_schedule)
     return set_err(ctx, DPRO_EINVAL, "critical path needs a replay with want_schedule");
+  if (b->overlay)
+    return set_err(ctx, DPRO_EUNSUPPORTED,
+                   "critical paths need materialized candidates (option overlay=0)");
   CU(cudaSetDevice(ctx->device));
   const size_t n = b->n;
   std::vector<unsigned long long> e_off(n), po_off(n);
@@ -1453,6 +1941,9 @@ int dpro_cuda_batch_peak_memory(dpro_ctx* ctx, dpro_batch* b, const int64_t* op_
     return DPRO_EINVAL;
   if (!b->replayed || !b->with_schedule)
     return set_err(ctx, DPRO_EINVAL, "peak memory needs a replay with want_schedule");
+  if (b->overlay)
+    return set_err(ctx, DPRO_EUNSUPPORTED,
+                   "peak memory needs materialized candidates (option overlay=0)");
   CU(cudaSetDevice(ctx->device));
   const size_t n = b->n, N = b->sum_n;
   std::vector<unsigned long long> seg0(n);

@@ -4,10 +4,11 @@
 // what changes is where the state lives and what an event round touches.
 //   * one CTA of NW warps per candidate (NW = 1, 2 or 4, chosen by device
 //     count); thread l owns devices d = l + 32 NW j (j < KD); the in-flight
-//     end time of each owned device lives in a register (64-bit: times are
-//     integer us or ns, and a config-4 makespan in ns is ~10^12), and the
-//     next event time is one REDUX.MIN over 32-bit offsets end - t (every
-//     in-flight end lies in (t, t + 2^31): op durations fit int32);
+//     end of each owned device lives in a register as a 32-bit offset from
+//     the current time t (every in-flight end lies in (t, t + 2^31): op
+//     durations fit int32), so the next event time is one REDUX.MIN and t
+//     itself is 64-bit (integer us or ns: a config-4 makespan in ns is
+//     ~10^12);
 //   * a round only visits devices that completed or received arrivals
 //     (per-lane dirty bitmask in shared memory, set by producers);
 //   * per-device FIFOs are shared-memory rings of 16-byte entries
@@ -32,10 +33,10 @@
 namespace dpro_k {
 
 constexpr uint32_t kT32Inf = 0xFFFFFFFFu;
-constexpr unsigned long long kT64Inf = ~0ull;
 // replay_fast outcomes / bail-out causes
 constexpr uint32_t kDone = 0, kBailRing = 1, kBailOther = 2;
-constexpr int kRetry = 9;  // status of a candidate queued for the deep-ring pass
+constexpr int kRetry = 9;   // status of a candidate queued for the deep-ring pass
+constexpr int kRetry2 = 11;  // queued for the global-ring pass (pass 3)
 
 // segt: the event-time EPOCH (count of distinct event times so far) of the
 // device's last arrival segment -- a time-independent stand-in for "the
@@ -43,7 +44,8 @@ constexpr int kRetry = 9;  // status of a candidate queued for the deep-ring pas
 struct __align__(16) DevF {
   uint32_t head, tail, tsort, segbeg;
   uint32_t zlo, zhi, segt, pad;
-  uint4 ient;  // in-flight positive-duration op {op, dur, sb, se}
+  uint32_t busy_lo, busy_hi;  // summed dur of the dispatched ops (64-bit)
+  uint32_t isb, ise;          // successor range of the in-flight op
 };
 static_assert(sizeof(DevF) == 48, "DevF layout");
 
@@ -54,6 +56,7 @@ struct FastCfg {
   uint32_t rl;     // successor-range list capacity per round
   uint32_t warp_bytes;
   uint32_t kd;     // devices per lane (template parameter)
+  uint4* gq = nullptr;  // pass 3: device rings in global memory, dcap * qc per CTA
 };
 
 __device__ __forceinline__ void prefetch_l2(const void* p) {
@@ -164,11 +167,48 @@ __device__ __forceinline__ unsigned long long gmax64(unsigned long long v, volat
   return (static_cast<unsigned long long>(hi) << 32) | lo;
 }
 
-template <int NW, int KD>
+// Overlay mode (OV, overlay.h): candidates replayed on the resident base's
+// packed layout plus a per-candidate overlay. rec/erec are the BASE arrays;
+// records in overlay form carry kOv in w (slot in x, final index in fin[]);
+// ranges and ring entries carry kOv in their start word when they index
+// the overlay's lists.
+constexpr uint32_t kOvF = 0x80000000u;
+constexpr uint32_t kBlkShiftF = 10;
+constexpr uint32_t kBlkOvfF = 0x80000000u;
+constexpr uint32_t kBlkBiasF = 0x40000000u;
+constexpr uint32_t kOvfDirtyF = 0x80000000u;
+
+struct OvView {
+  const uint4* rec;      // [no + 1] overlay records
+  const uint4* erec;     // overlay expanded lists
+  const uint32_t* fin;   // [no] final index per overlay op
+  const uint32_t* blk;   // per 1024 base ids: shift + kBlkBias, or kBlkOvf | block
+  const uint32_t* ovf;   // 1024 entries per flagged block
+};
+
+// One overlay candidate (device copy; arrays in the batch's overlay arena).
+struct OvCand {
+  OvView v;
+  const uint16_t* cnt;         // initial counts of the overlay counters
+  const uint4* src;            // source records (base or overlay form)
+  unsigned long long gcnt_off; // byte offset of the candidate's global counters
+  uint32_t n_cnt, n_src, first_missing, pad;
+};
+
+// The resident base's packed layout (overlay batches).
+struct OvBase {
+  const uint4* rec;
+  const uint4* erec;
+  const uint8_t* cnt0;  // u8, or u16 when wide
+  uint32_t n_cnt, wide;
+};
+
+template <int NW, int KD, bool OV = false>
 struct FastWarp {
   static constexpr uint32_t NT = 32u * NW;
   const uint4* __restrict__ rec;
   const uint4* __restrict__ erec;
+  OvView ov{};
   DevF* dv;
   uint4* q;                 // [dcap][qc] per-device rings
   uint2* rl;                // [rlcap] {succ_beg, count} ranges to expand
@@ -199,11 +239,34 @@ struct FastWarp {
       atomicOr(const_cast<uint32_t*>(&misc[1]), kBailRing);  // capacity: retry deeper
   }
 
-  // ready(s, t) of replay.cpp:60-72 for s reached through a packed record.
-  __device__ __forceinline__ void ready(const uint4& a, unsigned long long t) {
-    const uint32_t s = a.x & kOpMask;
+  // OV: final index of the op a record stands for; a base-form record of a
+  // dirty op is replaced by the op's overlay record (block table lookup).
+  __device__ __forceinline__ uint32_t resolve(uint4& a) const {
+    if constexpr (!OV) {
+      return a.x & kOpMask;
+    } else {
+      if (a.w & kOvF) return __ldg(ov.fin + (a.x & kOpMask));
+      const uint32_t b = a.x & kOpMask;
+      const uint32_t e = __ldg(ov.blk + (b >> kBlkShiftF));
+      if (!(e & kBlkOvfF)) return b + e - kBlkBiasF;
+      const uint32_t v = __ldg(ov.ovf + (size_t(e & ~kBlkOvfF) << kBlkShiftF) + (b & 1023u));
+      if (!(v & kOvfDirtyF)) return v;
+      const uint32_t slot = v & ~kOvfDirtyF;
+      a = __ldg(ov.rec + slot);
+      return __ldg(ov.fin + slot);
+    }
+  }
+
+  // ready(s, t) of replay.cpp:60-72 for s reached through a packed record
+  // (s = final index; OV: a may be in overlay form).
+  __device__ __forceinline__ void ready(const uint4& a, unsigned long long t, uint32_t s) {
     const uint32_t cnt = (a.z >> kCntShift) & kCntMax;
-    const uint32_t se = cnt == kCntMax ? __ldg(&rec[s + 1].w) : a.w + cnt;
+    const uint32_t fl = OV ? (a.w & kOvF) : 0u;  // list lives in the overlay
+    const uint32_t sb = a.w & ~fl;
+    uint32_t se;
+    if (cnt != kCntMax) se = sb + cnt;
+    else if (OV && fl) se = __ldg(&ov.rec[(a.x & kOpMask) + 1].w) & ~kOvF;
+    else se = __ldg(&rec[(a.x & kOpMask) + 1].w);
     if (a.z & kFVirt) {  // multi-predecessor virtual: completes now, cascade
       if (want) {
         start[s] = t;
@@ -211,7 +274,7 @@ struct FastWarp {
       }
       ++vcount;
       tmax = max(tmax, t);
-      if (se > a.w) push_range(a.w, se - a.w);
+      if (se > sb) push_range(sb | fl, se - sb);
       return;
     }
     const uint32_t d = a.z & kDevMask;
@@ -223,16 +286,16 @@ struct FastWarp {
     if (pos - low >= qc) {
       atomicOr(const_cast<uint32_t*>(&misc[1]), kBailRing);
     } else {
-      ring(d)[pos & (qc - 1)] = make_uint4(s, a.y, a.w, se);  // {op, dur, sb, se}
+      ring(d)[pos & (qc - 1)] = make_uint4(s, a.y, sb | fl, se);  // {op, dur, sb, se}
       atomicOr(const_cast<uint32_t*>(&misc[4 + (d % NT)]), 1u << (d / NT));
     }
-    if (se > a.w) prefetch_l2(erec + a.w);  // read when s completes
+    if (se > sb) prefetch_l2((OV && fl ? ov.erec : erec) + sb);  // read when s completes
   }
 
   // One out-edge record of a completing op (replay.cpp:100-103).
-  __device__ __forceinline__ void edge(const uint4& a, unsigned long long t) {
+  __device__ __forceinline__ void edge(uint4 a, unsigned long long t) {
+    const uint32_t s = resolve(a);
     if ((a.z & (kFVirt | kFMulti)) == kFVirt) {  // spliced single-pred virtual
-      const uint32_t s = a.x & kOpMask;
       if (want) {
         start[s] = t;
         end[s] = t;
@@ -253,7 +316,7 @@ struct FastWarp {
         if (((old >> sh) & 0xFFu) != 1u) return;
       }
     }
-    ready(a, t);
+    ready(a, t, s);
   }
 
   // Expands every range pushed this round (and the virtual cascades they
@@ -317,7 +380,10 @@ struct FastWarp {
             }
             const uint32_t sb = __shfl_sync(kFull, mine.x, k);
             const uint32_t ex = __shfl_sync(kFull, excl, k);
-            if (qi < total) a[b] = __ldg(erec + sb + (qi - ex));
+            if (qi < total) {
+              if (OV && (sb & kOvF)) a[b] = __ldg(ov.erec + (sb & ~kOvF) + (qi - ex));
+              else a[b] = __ldg(erec + sb + (qi - ex));
+            }
           }
 #pragma unroll
           for (int b = 0; b < kMlp; ++b)
@@ -331,14 +397,11 @@ struct FastWarp {
 
   // Owner-lane dispatch(t) for device d (replay.cpp:74-90) after merging
   // this round's arrivals into the (ready, index)-ordered tail segment.
-  // Returns the in-flight end (kT64Inf: idle); sets *zero when
+  // Returns the in-flight op's end - t (kT32Inf: idle); sets *zero when
   // zero-duration ops ran (they complete next round). epoch: number of
-  // distinct event times so far; busy: the device's summed dur (owner
-  // thread's register).
-  __device__ __forceinline__ unsigned long long dispatch_dev(uint32_t d, unsigned long long t,
-                                                             uint32_t epoch,
-                                                             unsigned long long iend, bool* zero,
-                                                             unsigned long long& busyd) {
+  // distinct event times so far.
+  __device__ __forceinline__ uint32_t dispatch_dev(uint32_t d, unsigned long long t,
+                                                   uint32_t epoch, uint32_t iend, bool* zero) {
     DevF& s = dv[d];
     uint4* r = ring(d);
     const uint32_t tail = *reinterpret_cast<volatile uint32_t*>(&s.tail);
@@ -363,7 +426,7 @@ struct FastWarp {
       }
       s.tsort = tail;
     }
-    if (iend == kT64Inf && head < tail) {
+    if (iend == kT32Inf && head < tail) {
       const uint32_t zlo = head;
       unsigned long long busy = 0;
       const uint32_t base = devoff[d];
@@ -382,13 +445,17 @@ struct FastWarp {
         busy += x.y;
         tmax = max(tmax, en);
         if (x.y > 0) {
-          s.ient = x;
-          iend = en;
+          s.isb = x.z;
+          s.ise = x.w;
+          iend = x.y;
           infl = true;
           break;
         }
       }
-      busyd += busy;
+      const unsigned long long bz =
+          ((static_cast<unsigned long long>(s.busy_hi) << 32) | s.busy_lo) + busy;
+      s.busy_lo = static_cast<uint32_t>(bz);
+      s.busy_hi = static_cast<uint32_t>(bz >> 32);
       s.head = head;
       s.zlo = zlo;
       const uint32_t zhi = infl ? head - 1 : head;
@@ -412,18 +479,21 @@ __device__ unsigned long long g_prof[16];
 
 // Returns kDone, kBailRing (a device queue outgrew its ring or a round its
 // range list: retry with deeper ones) or kBailOther (take the general path).
-template <int NW, int KD>
+template <int NW, int KD, bool OV = false>
 __device__ uint32_t replay_fast(const Cand& c, int cid, const uint4* rec, const uint4* erec,
                             const uint8_t* cnt0, const uint32_t* srcs, const PackInfo& info,
                             unsigned char* wsm, const FastCfg& F, const Scratch& S,
-                            const Outs& O, bool want_schedule, uint32_t* gcw) {
+                            const Outs& O, bool want_schedule, uint32_t* gcw,
+                            const OvCand* ovc = nullptr, const OvBase* ob = nullptr) {
   constexpr uint32_t NT = 32u * NW;
   const int lane = threadIdx.x & 31;
   const int tid = threadIdx.x;
   const uint32_t n = c.n, D = c.d;
   DevF* dv = reinterpret_cast<DevF*>(wsm);
-  uint4* q = reinterpret_cast<uint4*>(wsm + sizeof(DevF) * F.dcap);
-  uint2* rl = reinterpret_cast<uint2*>(q + (size_t)F.dcap * F.qc);
+  uint4* q = F.gq ? F.gq + size_t(blockIdx.x) * F.dcap * F.qc
+                  : reinterpret_cast<uint4*>(wsm + sizeof(DevF) * F.dcap);
+  uint2* rl = reinterpret_cast<uint2*>(wsm + sizeof(DevF) * F.dcap +
+                                       (F.gq ? 0 : 16 * size_t(F.dcap) * F.qc));
   volatile uint32_t* misc = reinterpret_cast<volatile uint32_t*>(rl + F.rl);
   // compact counters: shared memory, or (graphs with more multi-predecessor
   // ops than fit) this candidate's slice of global scratch, same word atomics
@@ -432,14 +502,24 @@ __device__ uint32_t replay_fast(const Cand& c, int cid, const uint4* rec, const 
   uint32_t par = 0;
   const unsigned long long oo = c.op_off;
 
-  FastWarp<NW, KD> W{rec, erec, dv, q, rl, misc, cw, F.qc, F.rl, S.qbuf + oo, S.qpos + oo,
-                 S.devoff + c.dof_off,
-                 want_schedule ? O.start + oo : nullptr,
-                 want_schedule ? O.end + oo : nullptr, want_schedule, lane, tid};
+  FastWarp<NW, KD, OV> W{rec, erec, {}, dv, q, rl, misc, cw, F.qc, F.rl, S.qbuf + oo,
+                     S.qpos + oo, S.devoff + c.dof_off,
+                     want_schedule ? O.start + oo : nullptr,
+                     want_schedule ? O.end + oo : nullptr, want_schedule, lane, tid};
   W.wide = info.wide != 0;
 
   // ---- state init ----
-  {
+  if constexpr (OV) {
+    // u16 counters: the base's (u8 or u16), then the overlay's
+    W.ov = ovc->v;
+    W.wide = true;
+    uint16_t* c16 = reinterpret_cast<uint16_t*>(cw);
+    const uint32_t nb = ob->n_cnt, nc = nb + ovc->n_cnt;
+    for (uint32_t i = tid; i < nc; i += NT)
+      c16[i] = i < nb ? (ob->wide ? __ldg(reinterpret_cast<const uint16_t*>(ob->cnt0) + i)
+                                  : static_cast<uint16_t>(__ldg(ob->cnt0 + i)))
+                      : __ldg(ovc->cnt + (i - nb));
+  } else {
     const uint32_t nv = ((info.wide ? 2u : 1u) * info.n_cnt + 15) / 16;
     const uint4* src = reinterpret_cast<const uint4*>(cnt0);
     uint4* dst = reinterpret_cast<uint4*>(cw);
@@ -449,7 +529,7 @@ __device__ uint32_t replay_fast(const Cand& c, int cid, const uint4* rec, const 
     DevF z;
     z.head = z.tail = z.tsort = z.segbeg = 0;
     z.zlo = z.zhi = z.segt = z.pad = 0;
-    z.ient = make_uint4(0, 0, 0, 0);
+    z.busy_lo = z.busy_hi = z.isb = z.ise = 0;
     dv[d] = z;
   }
   if (tid < 4) misc[tid] = 0;
@@ -458,7 +538,18 @@ __device__ uint32_t replay_fast(const Cand& c, int cid, const uint4* rec, const 
   gsync<NW>();
   // ---- sources (replay.cpp:92-94). No virtual sources reach the fast path
   // (pack flags them), so there are no cascades and no init quirk. ----
-  for (uint32_t k = tid; k < info.n_src; k += NT) W.ready(__ldg(rec + __ldg(srcs + k)), 0ull);
+  if constexpr (OV) {
+    for (uint32_t k = tid; k < ovc->n_src; k += NT) {
+      uint4 a = __ldg(ovc->src + k);
+      const uint32_t s = W.resolve(a);
+      W.ready(a, 0ull, s);
+    }
+  } else {
+    for (uint32_t k = tid; k < info.n_src; k += NT) {
+      const uint32_t s = __ldg(srcs + k);
+      W.ready(__ldg(rec + s), 0ull, s);
+    }
+  }
   gsync<NW>();
   if (gany<NW>(misc[1] != 0)) return misc[1] == kBailRing ? kBailRing : kBailOther;
   for (uint32_t d = tid; d < D; d += NT) {  // t = 0 arrivals in index order
@@ -479,16 +570,15 @@ __device__ uint32_t replay_fast(const Cand& c, int cid, const uint4* rec, const 
   gsync<NW>();
 
   // ---- dispatch(0) + event loop (replay.cpp:95-106) ----
-  unsigned long long iend[KD], busyd[KD];
+  uint32_t iend[KD];  // in-flight end - t per owned device (kT32Inf: idle)
   uint32_t zmask = 0, epoch = 0;
 #pragma unroll
   for (int j = 0; j < KD; ++j) {
-    iend[j] = kT64Inf;
-    busyd[j] = 0;
+    iend[j] = kT32Inf;
     const uint32_t d = tid + NT * j;
     if (d < D) {
       bool z = false;
-      iend[j] = W.dispatch_dev(d, 0ull, 0u, kT64Inf, &z, busyd[j]);
+      iend[j] = W.dispatch_dev(d, 0ull, 0u, kT32Inf, &z);
       if (z) zmask |= 1u << j;
     }
   }
@@ -497,11 +587,9 @@ __device__ uint32_t replay_fast(const Cand& c, int cid, const uint4* rec, const 
   uint32_t rpar = 0;
   for (;;) {
     PROF_T(p0);
-    // in-flight ends are > t and < t + 2^31: reduce their 32-bit offsets
     uint32_t lmin = kT32Inf;
 #pragma unroll
-    for (int j = 0; j < KD; ++j)
-      if (iend[j] != kT64Inf) lmin = min(lmin, static_cast<uint32_t>(iend[j] - t));
+    for (int j = 0; j < KD; ++j) lmin = min(lmin, iend[j]);
     bool zero_round;
     uint32_t dt;
     round_head<NW>(zmask != 0, lmin, red, par, zero_round, dt);
@@ -510,6 +598,9 @@ __device__ uint32_t replay_fast(const Cand& c, int cid, const uint4* rec, const 
       if (dt == kT32Inf) break;
       t += dt;
       ++epoch;
+#pragma unroll
+      for (int j = 0; j < KD; ++j)
+        if (iend[j] != kT32Inf) iend[j] -= dt;  // offsets from the new t
     }
     PROF_T(p1);
     // range counters alternate by round: this round's was zeroed last round
@@ -527,7 +618,8 @@ __device__ uint32_t replay_fast(const Cand& c, int cid, const uint4* rec, const 
         const uint32_t zh = s.zhi;
         for (uint32_t p = s.zlo; p < zh; ++p) {
           const uint4 e = r[p & (F.qc - 1)];
-          if (e.w > e.z) W.push_range(e.z, e.w - e.z);
+          const uint32_t eb = e.z & ~kOvF;
+          if (e.w > eb) W.push_range(e.z, e.w - eb);
         }
         *reinterpret_cast<volatile uint32_t*>(&s.zlo) = zh;
       }
@@ -535,11 +627,13 @@ __device__ uint32_t replay_fast(const Cand& c, int cid, const uint4* rec, const 
     } else {
 #pragma unroll
       for (int j = 0; j < KD; ++j) {
-        if (iend[j] == t) {
-          iend[j] = kT64Inf;
+        if (iend[j] == 0u) {
+          iend[j] = kT32Inf;
           freed |= 1u << j;
-          const uint4 e = dv[tid + NT * j].ient;
-          if (e.w > e.z) W.push_range(e.z, e.w - e.z);
+          const DevF& sd = dv[tid + NT * j];
+          const uint32_t ez = sd.isb, ew = sd.ise;
+          const uint32_t eb = ez & ~kOvF;
+          if (ew > eb) W.push_range(ez, ew - eb);
         }
       }
     }
@@ -556,7 +650,7 @@ __device__ uint32_t replay_fast(const Cand& c, int cid, const uint4* rec, const 
     for (int j = 0; j < KD; ++j) {
       if (todo & (1u << j)) {
         bool z = false;
-        iend[j] = W.dispatch_dev(tid + NT * j, t, epoch, iend[j], &z, busyd[j]);
+        iend[j] = W.dispatch_dev(tid + NT * j, t, epoch, iend[j], &z);
         if (z) zmask |= 1u << j;
       }
     }
@@ -579,12 +673,12 @@ __device__ uint32_t replay_fast(const Cand& c, int cid, const uint4* rec, const 
   const uint32_t dc = gsum<NW>(W.dcount, red, par);
   if (vc + dc != n) return kBailOther;  // cycle: the general path reports it exactly
   const unsigned long long T = gmax64<NW>(W.tmax, red, par);
-#pragma unroll
-  for (int j = 0; j < KD; ++j) {
-    const uint32_t d = tid + NT * j;
-    if (d < D) S.busy[c.dev_off + d] = static_cast<long long>(busyd[j]);
+  for (uint32_t d = tid; d < D; d += NT) {
+    S.busy[c.dev_off + d] =
+        static_cast<long long>((static_cast<unsigned long long>(dv[d].busy_hi) << 32) |
+                               dv[d].busy_lo);
+    S.dhead[c.dev_off + d] = W.devoff[d] + dv[d].head;
   }
-  for (uint32_t d = tid; d < D; d += NT) S.dhead[c.dev_off + d] = W.devoff[d] + dv[d].head;
   if (tid == 0) {
     O.status[cid] = kOk;
     O.err[cid] = 0;
@@ -607,7 +701,8 @@ __global__ void __launch_bounds__(32 * NW) replay_fast_kernel(
     FastCfg F, int want_schedule, unsigned* work, int pass) {
   extern __shared__ __align__(16) unsigned char fsm[];
   __shared__ int s_cid;
-  unsigned* counter = work + (pass == 1 ? 2 : 0);  // pass 0 and 2 share slot 0
+  // counters: [0] passes 0 and 2, [2] pass 1, [4] pass 3
+  unsigned* counter = work + (pass == 1 ? 2 : pass == 3 ? 4 : 0);
   for (;;) {
     if (threadIdx.x == 0) s_cid = static_cast<int>(atomicAdd(counter, 1u));
     __syncthreads();
@@ -615,6 +710,7 @@ __global__ void __launch_bounds__(32 * NW) replay_fast_kernel(
     __syncthreads();
     if (cid >= n_cands) break;
     if (pass == 1 && O.status[cid] != kRetry) continue;
+    if (pass == 3 && O.status[cid] != kRetry2) continue;
     if (pass == 2) {  // large graphs: straight to the deep-ring pass
       if (threadIdx.x == 0) {
         O.status[cid] = kRetry;
@@ -641,9 +737,9 @@ __global__ void __launch_bounds__(32 * NW) replay_fast_kernel(
               ? nullptr
               : reinterpret_cast<uint32_t*>(P.gcnt + P.c_off[cid]));
     __syncthreads();
-    if (rc == kBailRing && pass == 0) {
+    if (rc == kBailRing && (pass == 0 || pass == 1)) {
       if (threadIdx.x == 0) {
-        O.status[cid] = kRetry;
+        O.status[cid] = pass == 0 ? kRetry : kRetry2;
         atomicAdd(work + 3, 1u);
       }
     } else if (rc != kDone) {  // the general kernel is warp-level: warp 0 runs it
@@ -651,6 +747,61 @@ __global__ void __launch_bounds__(32 * NW) replay_fast_kernel(
       if (threadIdx.x < 32) {
         volatile uint32_t* vtop = reinterpret_cast<volatile uint32_t*>(fsm);
         replay_candidate(c, cid, S.dstate + c.dev_off, vtop, S, O, want_schedule != 0);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Overlay batches: one CTA of NW warps per candidate, persistent; the same
+// passes as replay_fast_kernel (0: residency rings, 1: deep rings for the
+// kRetry ones). Candidates the fast path cannot finish (kBailOther) are
+// marked kRetryMat: the host re-runs them through the materialized path.
+constexpr int kRetryMat = 10;
+
+template <int NW, int KD>
+__global__ void __launch_bounds__(32 * NW) replay_ov_kernel(
+    const Cand* __restrict__ cands, const OvCand* __restrict__ ovc, int n_cands, OvBase base,
+    Scratch S, Outs O, uint8_t* gcnt, FastCfg F, int want_schedule, unsigned* work, int pass) {
+  extern __shared__ __align__(16) unsigned char fsm[];
+  __shared__ int s_cid;
+  unsigned* counter = work + (pass == 1 ? 2 : pass == 3 ? 4 : 0);
+  for (;;) {
+    if (threadIdx.x == 0) s_cid = static_cast<int>(atomicAdd(counter, 1u));
+    __syncthreads();
+    const int cid = s_cid;
+    __syncthreads();
+    if (cid >= n_cands) break;
+    if (pass == 1 && O.status[cid] != kRetry) continue;
+    if (pass == 3 && O.status[cid] != kRetry2) continue;
+    const Cand c = cands[cid];
+    const OvCand oc = ovc[cid];
+    if (oc.pad) continue;  // materialized path (host)
+    if (oc.first_missing != kNone) {  // replay.cpp:39-44
+      if (threadIdx.x == 0) {
+        O.status[cid] = kMissing;
+        O.err[cid] = oc.first_missing;
+        O.makespan[cid] = 0;
+      }
+      continue;
+    }
+    PackInfo info{};
+    info.first_missing = kNone;
+    const uint32_t nc2 = 2u * (base.n_cnt + oc.n_cnt);
+    uint32_t rc = kBailOther;
+    if (c.d <= F.dcap && c.d <= 32u * NW * KD)
+      rc = replay_fast<NW, KD, true>(
+          c, cid, base.rec, base.erec, nullptr, nullptr, info, fsm, F, S, O,
+          want_schedule != 0,
+          nc2 <= F.ccap ? nullptr : reinterpret_cast<uint32_t*>(gcnt + oc.gcnt_off), &oc, &base);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (rc == kBailRing && (pass == 0 || pass == 1)) {
+        O.status[cid] = pass == 0 ? kRetry : kRetry2;
+        atomicAdd(work + 3, 1u);
+      } else if (rc != kDone) {
+        O.status[cid] = kRetryMat;
+        atomicAdd(work + 1, 1u);
       }
     }
     __syncthreads();
