@@ -305,7 +305,7 @@ struct dpro_batch {
   DevBuf ovdesc;                // OvCand[n]
   DevBuf ovgcnt;                // global counters (when they do not fit smem)
   std::vector<dpro_k::OvCand> ovc;
-  std::vector<uint8_t> ovstage; // host image of ovarena
+  HostPinned ovstage;           // host image of ovarena (pinned: fast H2D)
   uint32_t max_cnt_ov = 0;      // max base + overlay counters of a candidate
   int32_t n_mat = 0;            // candidates re-run through the materialized path
 };
@@ -1125,7 +1125,7 @@ int stage_overlays(dpro_ctx* ctx, dpro_batch* b) {
   }
   b->ov_off[n] = o;
   b->ov_bytes = o;
-  b->ovstage.resize(std::max<size_t>(o, 16));
+  CU(b->ovstage.ensure(std::max<size_t>(o, 16)));
   CU(b->ovarena.ensure(std::max<size_t>(o, 16)));
   b->ovc.assign(n, dpro_k::OvCand{});
   // global counter slices (u16, base + overlay counters)
@@ -1148,7 +1148,7 @@ int stage_overlays(dpro_ctx* ctx, dpro_batch* b) {
     }
     size_t q = b->ov_off[i];
     auto put = [&](const void* src, size_t bytes) {
-      if (bytes) std::memcpy(b->ovstage.data() + q, src, bytes);
+      if (bytes) std::memcpy(static_cast<char*>(b->ovstage.p) + q, src, bytes);
       const char* dptr = b->ovarena.as<char>(q);
       q += align16(bytes);
       return dptr;
@@ -1172,7 +1172,7 @@ int stage_overlays(dpro_ctx* ctx, dpro_batch* b) {
 int upload_overlays(dpro_ctx* ctx, dpro_batch* b) {
   const int32_t n = b->n;
   if (b->ov_bytes)
-    CU(cudaMemcpyAsync(b->ovarena.p, b->ovstage.data(), b->ov_bytes, cudaMemcpyHostToDevice,
+    CU(cudaMemcpyAsync(b->ovarena.p, b->ovstage.p, b->ov_bytes, cudaMemcpyHostToDevice,
                        ctx->stream));
   CU(b->ovdesc.ensure(sizeof(dpro_k::OvCand) * std::max(n, 1)));
   if (n)
@@ -1685,7 +1685,9 @@ template <int NW>
 int launch_ov_nw(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
   FastCfg F;
   F.qc = ctx->ring;
-  F.rl = 128;
+  // range list: every op completing in one round pushes one; identical
+  // workers complete together (config 4: 64 BW + 64 IN cascades per round)
+  F.rl = std::max<uint32_t>(128, std::min<uint32_t>(1024, 4 * b->max_d));
   const uint32_t nt = 32 * NW;
   uint32_t kd = std::max<uint32_t>(1, (b->max_d + nt - 1) / nt);
   if (kd > 8) kd = kd <= 12 ? 12 : 16;
@@ -1868,10 +1870,16 @@ int dpro_cuda_batch_timelines(dpro_ctx* ctx, dpro_batch* b, int32_t cand,
   if (h.d) CU(cudaMemcpyAsync(dh.data(), b->S.dhead + h.dev_off, size_t(h.d) * 4, cudaMemcpyDeviceToHost, ctx->stream));
   if (busy && h.d) CU(cudaMemcpyAsync(busy, b->S.busy + h.dev_off, size_t(h.d) * 8, cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
+  // a candidate that stopped before replaying (missing duration) has no
+  // timelines; regions are clamped so stale scratch can never overrun
+  int32_t stc = 0;
+  CU(cudaMemcpy(&stc, b->O.status + cand, 4, cudaMemcpyDeviceToHost));
   uint32_t k = 0;
   for (uint32_t d = 0; d < h.d; ++d) {
     if (dev_off) dev_off[d] = k;
-    for (uint32_t p = doff[d]; p < dh[d]; ++p, ++k)
+    if (stc == DPRO_MISSING_PROFILE) continue;
+    const uint32_t lo = std::min(doff[d], h.n), hi = std::min(std::min(dh[d], doff[d + 1]), h.n);
+    for (uint32_t p = lo; p < hi; ++p, ++k)
       if (order) order[k] = q[p];
   }
   if (dev_off) dev_off[h.d] = k;
