@@ -84,6 +84,7 @@ SIGNATURES = {
     "dpro_cuda_set_stream": (C.c_int, [_P, _P]),
     "dpro_cuda_set_option": (C.c_int, [_P, C.c_char_p, _I64]),
     "dpro_cuda_batch_stats": (C.c_int, [_P, _P, _P]),
+    "dpro_cuda_batch_diag": (C.c_int, [_P, _P, _P, _I32]),
     "dpro_cuda_last_error": (C.c_char_p, [_P]),
     "dpro_cuda_batch_create": (_P, [_P, C.POINTER(DproCsr), _I32, _I32]),
     "dpro_cuda_batch_destroy": (None, [_P, _P]),

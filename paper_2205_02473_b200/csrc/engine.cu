@@ -573,7 +573,7 @@ int alloc_batch(dpro_ctx* ctx, dpro_batch* b, const std::vector<uint32_t>& e_cap
   if (upload_desc)
     CU(cudaMemcpyAsync(b->desc.p, b->hc.data(), sizeof(Cand) * n, cudaMemcpyHostToDevice,
                        ctx->stream));
-  CU(b->work.ensure(32));
+  CU(b->work.ensure(48));
   // packed replay layout (pack_kernel.cuh)
   {
     std::vector<unsigned long long> r_off(n), e_off(n), c_off(n);
@@ -1121,7 +1121,8 @@ int stage_overlays(dpro_ctx* ctx, dpro_batch* b) {
     b->ov_off[i] = o;
     if (!O.fast) continue;
     o += sz(O.rec.size() * 4) + sz(O.erec.size() * 4) + sz(O.fin.size() * 4) +
-         sz(O.cnt.size() * 2) + sz(O.src.size() * 4) + sz(O.blk.size() * 4) + sz(O.ovf.size() * 4);
+         sz(O.cnt.size() * 2) + sz(O.src.size() * 4) + sz(O.blk.size() * 4) + sz(O.ovf.size() * 4) +
+         sz(O.sx.size() * 4) + sz(O.sbp.size() * 4);
   }
   b->ov_off[n] = o;
   b->ov_bytes = o;
@@ -1160,6 +1161,12 @@ int stage_overlays(dpro_ctx* ctx, dpro_batch* b) {
     c.src = reinterpret_cast<const uint4*>(put(O.src.data(), O.src.size() * 4));
     c.v.blk = reinterpret_cast<const uint32_t*>(put(O.blk.data(), O.blk.size() * 4));
     c.v.ovf = reinterpret_cast<const uint32_t*>(put(O.ovf.data(), O.ovf.size() * 4));
+    c.sx = reinterpret_cast<const uint2*>(put(O.sx.data(), O.sx.size() * 4));
+    c.sbp = reinterpret_cast<const uint2*>(put(O.sbp.data(), O.sbp.size() * 4));
+    c.n_sx = static_cast<uint32_t>(O.sx.size() / 2);
+    c.n_sbp = static_cast<uint32_t>(O.sbp.size() / 2);
+    c.ovmin = O.ovmin;
+    c.sparse = O.sparse ? 1u : 0u;
     c.n_cnt = static_cast<uint32_t>(O.cnt.size());
     c.n_src = static_cast<uint32_t>(O.src.size() / 4);
     c.pad = 0;
@@ -1258,7 +1265,7 @@ int build_overlay_batch(dpro_ctx* ctx, dpro_batch* b, dpro_resident* r,
   CU(b->desc.ensure(sizeof(Cand) * std::max(n, 1)));
   if (n) CU(cudaMemcpyAsync(b->desc.p, b->hc.data(), sizeof(Cand) * n, cudaMemcpyHostToDevice,
                             ctx->stream));
-  CU(b->work.ensure(32));
+  CU(b->work.ensure(48));
   {  // timeline regions from the overlays (materialized candidates: their pack)
     std::vector<uint32_t> dof(std::max<unsigned long long>(sdo, 1), 0);
     for (int32_t i = 0; i < n; ++i)
@@ -1522,7 +1529,7 @@ size_t fast_bytes(uint32_t dcap, uint32_t qc, uint32_t rl, uint32_t ccap, int nw
 // outgrew even the deepest shared-memory rings (e.g. the grad-accum variant
 // of config 4: a 230-deep link queue), rings in global memory (one slice
 // per CTA, one CTA per SM). Returns false when there is nothing to gain.
-bool pass3_cfg(dpro_ctx* ctx, const FastCfg& deep, int nw, FastCfg& G) {
+bool pass3_cfg(dpro_ctx* ctx, const FastCfg& deep, int nw, FastCfg& G, uint32_t extra = 0) {
   constexpr size_t kBudget = size_t(512) << 20;
   G = deep;
   G.qc = 4096;
@@ -1535,7 +1542,7 @@ bool pass3_cfg(dpro_ctx* ctx, const FastCfg& deep, int nw, FastCfg& G) {
   }
   G.gq = ctx->gring.as<uint4>();
   G.warp_bytes = static_cast<uint32_t>(size_t(G.dcap) * sizeof(dpro_k::DevF) + 8 * size_t(G.rl) +
-                                       4 * dpro_k::fast_misc_words(nw) + G.ccap);
+                                       4 * dpro_k::fast_misc_words(nw) + G.ccap) + extra;
   return G.warp_bytes + 1024 <= ctx->smem_optin;
 }
 
@@ -1552,7 +1559,7 @@ int launch_fast_kd(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule, FastCfg 
   blocks_per_sm = std::max(blocks_per_sm, 1);
   b->blocks_per_sm_fast = blocks_per_sm;
   const int grid = std::max(1, std::min(b->n, ctx->sm_count * blocks_per_sm));
-  CU(cudaMemsetAsync(b->work.p, 0, 32, ctx->stream));
+  CU(cudaMemsetAsync(b->work.p, 0, 48, ctx->stream));
   b->F = F;
   // graphs of millions of ops (configs 4/5) overflow the residency-sized
   // rings every time: send them straight to the deep-ring pass
@@ -1656,7 +1663,7 @@ int launch_ov_kd(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule, FastCfg F)
   blocks_per_sm = std::max(blocks_per_sm, 1);
   b->blocks_per_sm_fast = blocks_per_sm;
   const int grid = std::max(1, std::min(b->n, ctx->sm_count * blocks_per_sm));
-  CU(cudaMemsetAsync(b->work.p, 0, 32, ctx->stream));
+  CU(cudaMemsetAsync(b->work.p, 0, 48, ctx->stream));
   b->F = F;
   const dpro_resident* r = b->res;
   kern<<<grid, 32 * NW, F.warp_bytes, ctx->stream>>>(
@@ -1665,14 +1672,16 @@ int launch_ov_kd(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule, FastCfg F)
   CU(cudaGetLastError());
   FastCfg D = F;  // pass 1: ring overflows, one CTA per SM, deepest rings
   D.rl = std::max<uint32_t>(F.rl, 2048);
-  while (D.qc < 4096 && fast_bytes(D.dcap, D.qc * 2, D.rl, D.ccap, NW) <= dyn_max) D.qc *= 2;
-  D.warp_bytes = static_cast<uint32_t>(fast_bytes(D.dcap, D.qc, D.rl, D.ccap, NW));
+  const size_t lim = dyn_max - dpro_k::kOvListBytes;
+  while (D.qc < 4096 && fast_bytes(D.dcap, D.qc * 2, D.rl, D.ccap, NW) <= lim) D.qc *= 2;
+  D.warp_bytes = static_cast<uint32_t>(fast_bytes(D.dcap, D.qc, D.rl, D.ccap, NW)) +
+                 dpro_k::kOvListBytes;
   kern<<<ctx->sm_count, 32 * NW, D.warp_bytes, ctx->stream>>>(
       b->desc.as<Cand>(), b->ovdesc.as<dpro_k::OvCand>(), b->n, r->ob, b->S, b->O,
       b->ovgcnt.as<uint8_t>(), D, want_schedule ? 1 : 0, b->work.as<unsigned>(), 1);
   CU(cudaGetLastError());
   FastCfg G;
-  if (pass3_cfg(ctx, D, NW, G)) {
+  if (pass3_cfg(ctx, D, NW, G, dpro_k::kOvListBytes)) {
     kern<<<ctx->sm_count, 32 * NW, G.warp_bytes, ctx->stream>>>(
         b->desc.as<Cand>(), b->ovdesc.as<dpro_k::OvCand>(), b->n, r->ob, b->S, b->O,
         b->ovgcnt.as<uint8_t>(), G, want_schedule ? 1 : 0, b->work.as<unsigned>(), 3);
@@ -1702,7 +1711,8 @@ int launch_ov_nw(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
                                          size_t(ctx->smem_per_sm) / 8 - 1024);
   while (F.qc < 64 && fast_bytes(F.dcap, F.qc * 2, F.rl, F.ccap, NW) <= std::min(target, limit))
     F.qc *= 2;
-  F.warp_bytes = static_cast<uint32_t>(fast_bytes(F.dcap, F.qc, F.rl, F.ccap, NW));
+  F.warp_bytes = static_cast<uint32_t>(fast_bytes(F.dcap, F.qc, F.rl, F.ccap, NW)) +
+                 dpro_k::kOvListBytes;
   switch (kd) {
     case 1: return launch_ov_kd<NW, 1>(ctx, b, want_schedule, F);
     case 2: return launch_ov_kd<NW, 2>(ctx, b, want_schedule, F);
@@ -1822,6 +1832,17 @@ int dpro_cuda_batch_stats(dpro_ctx* ctx, dpro_batch* b, int64_t* stats) {
   stats[2] = b->blocks_per_sm_fast;
   stats[3] = b->F.qc;
   stats[4] = ctx->fast ? w[3] : 0;
+  return DPRO_OK;
+}
+
+int dpro_cuda_batch_diag(dpro_ctx* ctx, dpro_batch* b, int64_t* out, int32_t n) {
+  if (!ctx || !b || !out || n < 0) return DPRO_EINVAL;
+  CU(cudaSetDevice(ctx->device));
+  unsigned w[12] = {0};
+  CU(cudaMemcpyAsync(w, b->work.p, 48, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  const int64_t v[6] = {w[5], w[6], w[7], w[8], b->overlay ? 1 : 0, b->n_mat};
+  for (int32_t i = 0; i < n && i < 6; ++i) out[i] = v[i];
   return DPRO_OK;
 }
 

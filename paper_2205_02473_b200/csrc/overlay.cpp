@@ -125,6 +125,10 @@ void build_overlay(const BaseHost& B, const dpro_delta& D, OverlayHost& O) {
   O.blk.clear();
   O.ovf.clear();
   O.devoff.clear();
+  O.sx.clear();
+  O.sbp.clear();
+  O.sparse = false;
+  O.ovmin = 0;
   O.fast = true;
   O.why.clear();
   O.first_missing = UINT32_MAX;
@@ -336,6 +340,40 @@ void build_overlay(const BaseHost& B, const dpro_delta& D, OverlayHost& O) {
   for (uint32_t j = 0; j < nn; ++j)
     if (!(D.new_flags[j] & DPRO_FLAG_VIRTUAL)) O.devoff[D.new_dev[j] + 1] += 1;
   for (uint32_t d = 0; d < D.n_devices; ++d) O.devoff[d + 1] += O.devoff[d];
+  // sparse form: the shift of final(b) = b - #removed<b + #new_pos<=b
+  // changes at r + 1 for every removed r (-1) and at every new_pos (+1)
+  {
+    constexpr size_t kSparseMax = 64;
+    std::vector<std::pair<uint32_t, int32_t>> ch;
+    for (uint32_t k = 0; k < D.n_removed && ch.size() <= 2 * kSparseMax; ++k)
+      ch.emplace_back(D.removed[k] + 1, -1);
+    for (uint32_t j = 0; j < nn && ch.size() <= 2 * kSparseMax; ++j) ch.emplace_back(D.new_pos[j], 1);
+    if (nd <= kSparseMax && ch.size() <= 2 * kSparseMax) {
+      std::sort(ch.begin(), ch.end());
+      int32_t sh = 0;
+      for (size_t k = 0; k < ch.size();) {
+        const uint32_t pos = ch[k].first;
+        int32_t dsh = 0;
+        for (; k < ch.size() && ch[k].first == pos; ++k) dsh += ch[k].second;
+        if (dsh == 0) continue;
+        sh += dsh;
+        O.sbp.push_back(pos);
+        O.sbp.push_back(static_cast<uint32_t>(sh));
+      }
+      if (O.sbp.size() / 2 <= kSparseMax) {
+        O.sparse = true;
+        for (uint32_t s = 0; s < nd; ++s) {
+          O.sx.push_back(dl[s]);
+          O.sx.push_back(s);
+        }
+        O.ovmin = UINT32_MAX;
+        if (!O.sbp.empty()) O.ovmin = O.sbp[0];
+        if (nd) O.ovmin = std::min(O.ovmin, dl[0]);
+      } else {
+        O.sbp.clear();
+      }
+    }
+  }
   // block table: uniform shift, or per-op entries where removed ops, dirty
   // ops or insertion points fall inside the block
   const uint32_t nblk = (nb + kBlk - 1) / kBlk + 1;

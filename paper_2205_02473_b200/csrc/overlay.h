@@ -63,6 +63,13 @@ struct OverlayHost {
   std::vector<uint32_t> blk;   // per 1024-id base block
   std::vector<uint32_t> ovf;   // 1024 entries per flagged block
   std::vector<uint32_t> devoff;  // timeline regions [n_devices + 1]
+  // sparse form (few dirty ops and index shifts: op-fusion / partition
+  // candidates), read from shared memory: (base id, slot) of the dirty ops
+  // and (first base id, shift) runs of the final-index shift, both sorted;
+  // base ids below ovmin are pure with final index == base index
+  std::vector<uint32_t> sx, sbp;
+  uint32_t ovmin = 0;
+  bool sparse = false;
   uint32_t n_ops = 0, n_devices = 0;
   uint32_t first_missing = UINT32_MAX;  // final index, UINT32_MAX: none
   bool fast = true;            // false: needs the materialized path

@@ -34,7 +34,11 @@ namespace dpro_k {
 
 constexpr uint32_t kT32Inf = 0xFFFFFFFFu;
 // replay_fast outcomes / bail-out causes
-constexpr uint32_t kDone = 0, kBailRing = 1, kBailOther = 2;
+constexpr uint32_t kDone = 0, kBailRing = 1, kBailOther = 2, kBailRl = 3;
+constexpr uint32_t kMiscRl = 4;  // misc[1] bit: a round's range list overflowed
+__device__ __forceinline__ uint32_t bail_code(uint32_t m) {
+  return (m & kBailOther) ? kBailOther : (m & kBailRing) ? kBailRing : kBailRl;
+}
 constexpr int kRetry = 9;   // status of a candidate queued for the deep-ring pass
 constexpr int kRetry2 = 11;  // queued for the global-ring pass (pass 3)
 
@@ -191,9 +195,15 @@ struct OvCand {
   OvView v;
   const uint16_t* cnt;         // initial counts of the overlay counters
   const uint4* src;            // source records (base or overlay form)
+  const uint2* sx;             // sparse form: (base id, slot) of the dirty ops
+  const uint2* sbp;            // sparse form: (first base id, shift) runs
   unsigned long long gcnt_off; // byte offset of the candidate's global counters
   uint32_t n_cnt, n_src, first_missing, pad;
+  uint32_t n_sx, n_sbp, ovmin, sparse;
 };
+// shared memory for the sparse lists (64 + 64 pairs)
+constexpr uint32_t kOvListBytes = 1024;
+constexpr uint32_t kOvListMax = 64;
 
 // The resident base's packed layout (overlay batches).
 struct OvBase {
@@ -226,6 +236,10 @@ struct FastWarp {
   uint32_t vcount = 0, dcount = 0;
   unsigned long long tmax = 0;
   bool wide = false;  // u16 counters (some in-degree >= 255)
+  const uint2* sxs = nullptr;   // OV sparse lists in shared memory
+  const uint2* sbps = nullptr;
+  uint32_t n_sx = 0, n_sbp = 0, ovmin = 0;
+  bool sparse = false;
 
   __device__ __forceinline__ uint4* ring(uint32_t d) { return q + (size_t)d * qc; }
 
@@ -236,7 +250,7 @@ struct FastWarp {
     if (p < rlcap)
       rl[p] = make_uint2(sb, n);
     else
-      atomicOr(const_cast<uint32_t*>(&misc[1]), kBailRing);  // capacity: retry deeper
+      atomicOr(const_cast<uint32_t*>(&misc[1]), kMiscRl);  // capacity: retry deeper
   }
 
   // OV: final index of the op a record stands for; a base-form record of a
@@ -247,6 +261,28 @@ struct FastWarp {
     } else {
       if (a.w & kOvF) return __ldg(ov.fin + (a.x & kOpMask));
       const uint32_t b = a.x & kOpMask;
+      if (sparse) {  // shared-memory lists; most ops lie below every change
+        if (b < ovmin) return b;
+        uint32_t lo = 0, hi = n_sx;
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (sxs[mid].x < b) lo = mid + 1;
+          else hi = mid;
+        }
+        if (lo < n_sx && sxs[lo].x == b) {
+          const uint32_t slot = sxs[lo].y;
+          a = __ldg(ov.rec + slot);
+          return __ldg(ov.fin + slot);
+        }
+        lo = 0;
+        hi = n_sbp;
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (sbps[mid].x <= b) lo = mid + 1;
+          else hi = mid;
+        }
+        return lo ? b + sbps[lo - 1].y : b;
+      }
       const uint32_t e = __ldg(ov.blk + (b >> kBlkShiftF));
       if (!(e & kBlkOvfF)) return b + e - kBlkBiasF;
       const uint32_t v = __ldg(ov.ovf + (size_t(e & ~kBlkOvfF) << kBlkShiftF) + (b & 1023u));
@@ -330,8 +366,8 @@ struct FastWarp {
     uint32_t lo = 0;
     for (;;) {
       const uint32_t hi = *rlc;
-      if (misc[1]) return misc[1] == kBailRing ? kBailRing : kBailOther;
-      if (hi > rlcap) return kBailRing;
+      if (misc[1]) return bail_code(misc[1]);
+      if (hi > rlcap) return kBailRl;
       if (lo == hi) return kDone;
       for (uint32_t g = lo; g < hi; g += 32) {
         const uint32_t r = g + lane;
@@ -513,6 +549,18 @@ __device__ uint32_t replay_fast(const Cand& c, int cid, const uint4* rec, const 
     // u16 counters: the base's (u8 or u16), then the overlay's
     W.ov = ovc->v;
     W.wide = true;
+    if (ovc->sparse) {  // sparse lists after the counter region
+      uint2* sl = reinterpret_cast<uint2*>(reinterpret_cast<char*>(
+                      const_cast<uint32_t*>(misc) + fast_misc_words(NW)) + F.ccap);
+      for (uint32_t i = tid; i < ovc->n_sx; i += NT) sl[i] = __ldg(ovc->sx + i);
+      for (uint32_t i = tid; i < ovc->n_sbp; i += NT) sl[kOvListMax + i] = __ldg(ovc->sbp + i);
+      W.sxs = sl;
+      W.sbps = sl + kOvListMax;
+      W.n_sx = ovc->n_sx;
+      W.n_sbp = ovc->n_sbp;
+      W.ovmin = ovc->ovmin;
+      W.sparse = true;
+    }
     uint16_t* c16 = reinterpret_cast<uint16_t*>(cw);
     const uint32_t nb = ob->n_cnt, nc = nb + ovc->n_cnt;
     for (uint32_t i = tid; i < nc; i += NT)
@@ -551,7 +599,7 @@ __device__ uint32_t replay_fast(const Cand& c, int cid, const uint4* rec, const 
     }
   }
   gsync<NW>();
-  if (gany<NW>(misc[1] != 0)) return misc[1] == kBailRing ? kBailRing : kBailOther;
+  if (gany<NW>(misc[1] != 0)) return bail_code(misc[1]);
   for (uint32_t d = tid; d < D; d += NT) {  // t = 0 arrivals in index order
     DevF& s = dv[d];
     uint4* r = W.ring(d);
@@ -737,10 +785,11 @@ __global__ void __launch_bounds__(32 * NW) replay_fast_kernel(
               ? nullptr
               : reinterpret_cast<uint32_t*>(P.gcnt + P.c_off[cid]));
     __syncthreads();
-    if (rc == kBailRing && (pass == 0 || pass == 1)) {
+    if ((rc == kBailRing || rc == kBailRl) && (pass == 0 || pass == 1)) {
       if (threadIdx.x == 0) {
         O.status[cid] = pass == 0 ? kRetry : kRetry2;
         atomicAdd(work + 3, 1u);
+        atomicAdd(work + (rc == kBailRing ? 5 : 6) + (pass == 1 ? 2 : 0), 1u);
       }
     } else if (rc != kDone) {  // the general kernel is warp-level: warp 0 runs it
       if (threadIdx.x == 0) atomicAdd(work + 1, 1u);
@@ -796,9 +845,10 @@ __global__ void __launch_bounds__(32 * NW) replay_ov_kernel(
           nc2 <= F.ccap ? nullptr : reinterpret_cast<uint32_t*>(gcnt + oc.gcnt_off), &oc, &base);
     __syncthreads();
     if (threadIdx.x == 0) {
-      if (rc == kBailRing && (pass == 0 || pass == 1)) {
+      if ((rc == kBailRing || rc == kBailRl) && (pass == 0 || pass == 1)) {
         O.status[cid] = pass == 0 ? kRetry : kRetry2;
         atomicAdd(work + 3, 1u);
+        atomicAdd(work + (rc == kBailRing ? 5 : 6) + (pass == 1 ? 2 : 0), 1u);
       } else if (rc != kDone) {
         O.status[cid] = kRetryMat;
         atomicAdd(work + 1, 1u);

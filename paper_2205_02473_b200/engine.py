@@ -212,6 +212,14 @@ class Batch:
                 "fast_blocks_per_sm": int(st[2]), "ring": int(st[3]),
                 "deep_ring_retries": int(st[4])}
 
+    def diag(self) -> dict:
+        """Why candidates left the residency pass (dpro_cuda_batch_diag)."""
+        d = np.zeros(6, np.int64)
+        _check(self.engine.ctx, N.lib.dpro_cuda_batch_diag(self.engine.ctx, self.handle,
+                                                           N.ptr(d), 6), "batch_diag")
+        return {"pass0_ring": int(d[0]), "pass0_rl": int(d[1]), "deep_ring": int(d[2]),
+                "deep_rl": int(d[3]), "overlay": bool(d[4]), "materialized": int(d[5])}
+
     def pack_info(self) -> np.ndarray:
         """[n, 4]: first op without duration, not-fast bits, multi-pred ops, sources."""
         out = np.zeros((max(1, self.n), 4), np.uint32)

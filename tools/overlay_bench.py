@@ -45,7 +45,7 @@ def main():
             tr = time.perf_counter() - t
             print(f"overlay={ov} B={B}: create {tc:.2f} s, prepare {tp * 1e3:.1f} ms, replay "
                   f"{tr * 1e3:.1f} ms -> {B / (tp + tr):.0f} replays/s (replay only "
-                  f"{B / tr:.0f}/s); stats {b.stats()}", flush=True)
+                  f"{B / tr:.0f}/s); stats {b.stats()} diag {b.diag()}", flush=True)
         ms, st, *_ = b.results()
         out[ov] = ms
         print("status ok", int((st == 0).sum()), "of", B, flush=True)
