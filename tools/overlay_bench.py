@@ -24,10 +24,14 @@ def main():
     deltas, descs = w.candidate_deltas(base, B, threads=16)
     print(f"deltas {time.perf_counter() - t:.2f} s", flush=True)
     eng = Engine(0)
+    import os
+    for key in ("ring", "warps"):
+        if os.environ.get("DPRO_" + key.upper()):
+            eng.set_option(key, int(os.environ["DPRO_" + key.upper()]))
     res = eng.resident(base.graph().csr)
     out = {}
     for ov in (1, 0):
-        if ov == 0 and B > 296:
+        if ov == 0 and (B > 296 or os.environ.get('OV_ONLY')):
             continue
         eng.set_option("overlay", ov)
         t = time.perf_counter()
