@@ -141,7 +141,8 @@ int dpro_cuda_batch_stats(dpro_ctx* ctx, dpro_batch* b, int64_t* stats);
 /* Diagnostics of the last replay, up to n of: [0] pass-0 ring overflows,
  * [1] pass-0 range-list overflows, [2] / [3] the same in the deep-ring pass,
  * [4] 1 for an overlay batch, [5] overlay candidates on the materialized
- * path. */
+ * path, [6..9] microseconds of pass 0, the deep-ring pass, the global-ring
+ * pass and the general-kernel hand-off (-1: not timed). */
 int dpro_cuda_batch_diag(dpro_ctx* ctx, dpro_batch* b, int64_t* out, int32_t n);
 /* scheduled[i] = 1 for ops the replay scheduled (host buffer [n_ops]); the
  * ids with 0 form CycleError::cycle (replay.cpp:108-117). */

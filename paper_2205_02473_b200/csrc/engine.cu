@@ -308,6 +308,19 @@ struct dpro_batch {
   HostPinned ovstage;           // host image of ovarena (pinned: fast H2D)
   uint32_t max_cnt_ov = 0;      // max base + overlay counters of a candidate
   int32_t n_mat = 0;            // candidates re-run through the materialized path
+  uint32_t ring_hint = 0;       // residency-pass ring capacity learned from the last replay
+  // pass timing of the last fast / overlay replay (dpro_cuda_batch_diag):
+  // events before pass 0, after pass 0, 1, 3 and the general hand-off
+  cudaEvent_t pev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  bool pev_valid = false;
+  void mark(int k, cudaStream_t st) {
+    if (!pev[k] && cudaEventCreate(&pev[k]) != cudaSuccess) return;
+    cudaEventRecord(pev[k], st);
+  }
+  ~dpro_batch() {
+    for (auto& e : pev)
+      if (e) cudaEventDestroy(e);
+  }
 };
 
 dpro_resident::~dpro_resident() { delete packed; }
@@ -1497,7 +1510,9 @@ int dpro_cuda_set_option(dpro_ctx* ctx, const char* key, int64_t value) {
 
 namespace {
 
-int launch_general(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
+// filter != 0: only the candidates the fast kernel handed off (status ==
+// filter), after its passes on the same stream.
+int launch_general(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule, int filter = 0) {
   size_t budget = std::min<size_t>(ctx->smem_optin, 200 * 1024);
   uint32_t dcap = static_cast<uint32_t>((budget - kSmemHeader) / (kWarpsPerBlock * sizeof(DevSt)));
   dcap = std::min<uint32_t>(dcap, std::max<uint32_t>(b->max_d, 1));
@@ -1508,10 +1523,13 @@ int launch_general(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
   blocks_per_sm = std::max(blocks_per_sm, 1);
   const int need = (b->n + kWarpsPerBlock - 1) / kWarpsPerBlock;
   const int grid = std::max(1, std::min(need, ctx->sm_count * blocks_per_sm));
-  CU(cudaMemsetAsync(b->work.p, 0, 4, ctx->stream));
-  dpro_k::replay_batch_kernel<<<grid, 32 * kWarpsPerBlock, smem, ctx->stream>>>(
+  CU(cudaMemsetAsync(b->work.as<unsigned>() + (filter ? 9 : 0), 0, 4, ctx->stream));
+  const int g = filter ? std::max(1, std::min(ctx->sm_count * blocks_per_sm,
+                                              (b->n + kWarpsPerBlock - 1) / kWarpsPerBlock))
+                       : grid;
+  dpro_k::replay_batch_kernel<<<g, 32 * kWarpsPerBlock, smem, ctx->stream>>>(
       b->desc.as<Cand>(), b->n, b->S, b->O, want_schedule ? 1 : 0,
-      b->work.as<unsigned>(), dcap);
+      b->work.as<unsigned>(), dcap, filter);
   CU(cudaGetLastError());
   return DPRO_OK;
 }
@@ -1566,10 +1584,12 @@ int launch_fast_kd(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule, FastCfg 
   const bool deep_first = ctx->deep_first >= 0
                               ? ctx->deep_first == 1
                               : (b->n > 0 && b->sum_n / b->n > 1000000ull);
+  b->mark(0, ctx->stream);
   kern<<<grid, 32 * NW, smem, ctx->stream>>>(b->desc.as<Cand>(), b->n, b->S, b->O, b->P, F,
                                              want_schedule ? 1 : 0, b->work.as<unsigned>(),
                                              deep_first ? 2 : 0);
   CU(cudaGetLastError());
+  b->mark(1, ctx->stream);
   // pass 1: candidates whose device queues outgrew the ring, one CTA per SM
   // with the deepest rings the shared memory holds
   FastCfg D = F;
@@ -1581,6 +1601,7 @@ int launch_fast_kd(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule, FastCfg 
       b->desc.as<Cand>(), b->n, b->S, b->O, b->P, D, want_schedule ? 1 : 0,
       b->work.as<unsigned>(), 1);
   CU(cudaGetLastError());
+  b->mark(2, ctx->stream);
   FastCfg G;
   if (pass3_cfg(ctx, D, NW, G)) {
     kern<<<ctx->sm_count, 32 * NW, G.warp_bytes, ctx->stream>>>(
@@ -1588,7 +1609,12 @@ int launch_fast_kd(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule, FastCfg 
         b->work.as<unsigned>(), 3);
     CU(cudaGetLastError());
   }
-  return DPRO_OK;
+  b->mark(3, ctx->stream);
+  // whatever the fast passes could not represent: the general kernel
+  const int st = launch_general(ctx, b, want_schedule, dpro_k::kRetryGen);
+  b->mark(4, ctx->stream);
+  b->pev_valid = true;
+  return st;
 }
 
 template <int NW>
@@ -1666,10 +1692,12 @@ int launch_ov_kd(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule, FastCfg F)
   CU(cudaMemsetAsync(b->work.p, 0, 48, ctx->stream));
   b->F = F;
   const dpro_resident* r = b->res;
+  b->mark(0, ctx->stream);
   kern<<<grid, 32 * NW, F.warp_bytes, ctx->stream>>>(
       b->desc.as<Cand>(), b->ovdesc.as<dpro_k::OvCand>(), b->n, r->ob, b->S, b->O,
       b->ovgcnt.as<uint8_t>(), F, want_schedule ? 1 : 0, b->work.as<unsigned>(), 0);
   CU(cudaGetLastError());
+  b->mark(1, ctx->stream);
   FastCfg D = F;  // pass 1: ring overflows, one CTA per SM, deepest rings
   D.rl = std::max<uint32_t>(F.rl, 2048);
   const size_t lim = dyn_max - dpro_k::kOvListBytes;
@@ -1680,6 +1708,7 @@ int launch_ov_kd(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule, FastCfg F)
       b->desc.as<Cand>(), b->ovdesc.as<dpro_k::OvCand>(), b->n, r->ob, b->S, b->O,
       b->ovgcnt.as<uint8_t>(), D, want_schedule ? 1 : 0, b->work.as<unsigned>(), 1);
   CU(cudaGetLastError());
+  b->mark(2, ctx->stream);
   FastCfg G;
   if (pass3_cfg(ctx, D, NW, G, dpro_k::kOvListBytes)) {
     kern<<<ctx->sm_count, 32 * NW, G.warp_bytes, ctx->stream>>>(
@@ -1687,13 +1716,19 @@ int launch_ov_kd(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule, FastCfg F)
         b->ovgcnt.as<uint8_t>(), G, want_schedule ? 1 : 0, b->work.as<unsigned>(), 3);
     CU(cudaGetLastError());
   }
+  b->mark(3, ctx->stream);
+  b->mark(4, ctx->stream);
+  b->pev_valid = true;
   return DPRO_OK;
 }
 
 template <int NW>
 int launch_ov_nw(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
   FastCfg F;
-  F.qc = ctx->ring;
+  // multi-million-op graphs (configs 4/5) need 16-entry device rings in the
+  // residency pass; a replay that overflowed raises the hint for the next
+  F.qc = std::max<uint32_t>(ctx->ring, b->ring_hint);
+  if (b->n > 0 && b->sum_n / b->n > 1000000ull) F.qc = std::max<uint32_t>(F.qc, 16);
   // range list: every op completing in one round pushes one; identical
   // workers complete together (config 4: 64 BW + 64 IN cascades per round)
   F.rl = std::max<uint32_t>(128, std::min<uint32_t>(1024, 4 * b->max_d));
@@ -1730,9 +1765,10 @@ int launch_ov_nw(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
 // overlays, kRetryMat after the kernel) re-run as an ordinary delta batch;
 // their results are copied into this batch's layout.
 int finish_overlay_mat(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
-  unsigned w[4] = {0, 0, 0, 0};
-  CU(cudaMemcpyAsync(w, b->work.p, 16, cudaMemcpyDeviceToHost, ctx->stream));
+  unsigned w[12] = {0};
+  CU(cudaMemcpyAsync(w, b->work.p, 48, cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
+  if (w[5] > static_cast<unsigned>(b->n) / 8 && b->F.qc < 64) b->ring_hint = 2 * b->F.qc;
   if (b->n_mat == 0 && w[1] == 0) return DPRO_OK;
   std::vector<int32_t> stv(b->n);
   CU(cudaMemcpy(stv.data(), b->O.status, 4 * size_t(b->n), cudaMemcpyDeviceToHost));
@@ -1841,8 +1877,16 @@ int dpro_cuda_batch_diag(dpro_ctx* ctx, dpro_batch* b, int64_t* out, int32_t n) 
   unsigned w[12] = {0};
   CU(cudaMemcpyAsync(w, b->work.p, 48, cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
-  const int64_t v[6] = {w[5], w[6], w[7], w[8], b->overlay ? 1 : 0, b->n_mat};
-  for (int32_t i = 0; i < n && i < 6; ++i) out[i] = v[i];
+  int64_t v[10] = {w[5], w[6], w[7], w[8], b->overlay ? 1 : 0, b->n_mat, -1, -1, -1, -1};
+  if (b->pev_valid)
+    for (int k = 0; k < 4; ++k) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, b->pev[k], b->pev[k + 1]) == cudaSuccess)
+        v[6 + k] = static_cast<int64_t>(ms * 1000.0f);
+      else
+        cudaGetLastError();
+    }
+  for (int32_t i = 0; i < n && i < 10; ++i) out[i] = v[i];
   return DPRO_OK;
 }
 

@@ -41,6 +41,7 @@ __device__ __forceinline__ uint32_t bail_code(uint32_t m) {
 }
 constexpr int kRetry = 9;   // status of a candidate queued for the deep-ring pass
 constexpr int kRetry2 = 11;  // queued for the global-ring pass (pass 3)
+constexpr int kRetryGen = 12;  // handed to the general kernel (replay_batch_kernel)
 
 // segt: the event-time EPOCH (count of distinct event times so far) of the
 // device's last arrival segment -- a time-independent stand-in for "the
@@ -791,11 +792,10 @@ __global__ void __launch_bounds__(32 * NW) replay_fast_kernel(
         atomicAdd(work + 3, 1u);
         atomicAdd(work + (rc == kBailRing ? 5 : 6) + (pass == 1 ? 2 : 0), 1u);
       }
-    } else if (rc != kDone) {  // the general kernel is warp-level: warp 0 runs it
-      if (threadIdx.x == 0) atomicAdd(work + 1, 1u);
-      if (threadIdx.x < 32) {
-        volatile uint32_t* vtop = reinterpret_cast<volatile uint32_t*>(fsm);
-        replay_candidate(c, cid, S.dstate + c.dev_off, vtop, S, O, want_schedule != 0);
+    } else if (rc != kDone) {  // the general kernel runs it after the passes
+      if (threadIdx.x == 0) {
+        O.status[cid] = kRetryGen;
+        atomicAdd(work + 1, 1u);
       }
     }
     __syncthreads();

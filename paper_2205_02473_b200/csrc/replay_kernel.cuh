@@ -482,9 +482,11 @@ __device__ void replay_candidate(const Cand& c, int cid, DevSt* ds,
 }
 
 // Persistent warps pull candidates from a global counter (sizes vary).
+// filter != 0: only candidates whose status is `filter` (the fast kernels'
+// hand-offs), pulled from work[9].
 __global__ void __launch_bounds__(128) replay_batch_kernel(
     const Cand* __restrict__ cands, int n_cands, Scratch S, Outs O,
-    int want_schedule, unsigned* work, uint32_t dcap) {
+    int want_schedule, unsigned* work, uint32_t dcap, int filter = 0) {
   extern __shared__ unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5;
   const int wpb = blockDim.x >> 5;
@@ -492,9 +494,10 @@ __global__ void __launch_bounds__(128) replay_batch_kernel(
   DevSt* sdev = reinterpret_cast<DevSt*>(smem_raw + 16 * 8) + (size_t)warp * dcap;
   for (;;) {
     int cid = 0;
-    if ((threadIdx.x & 31) == 0) cid = static_cast<int>(atomicAdd(work, 1u));
+    if ((threadIdx.x & 31) == 0) cid = static_cast<int>(atomicAdd(work + (filter ? 9 : 0), 1u));
     cid = __shfl_sync(kFull, cid, 0);
     if (cid >= n_cands) break;
+    if (filter && O.status[cid] != filter) continue;
     const Cand c = cands[cid];
     DevSt* ds = (c.d <= dcap) ? sdev : S.dstate + c.dev_off;
     replay_candidate(c, cid, ds, vtops + warp * 4, S, O, want_schedule != 0);

@@ -214,11 +214,12 @@ class Batch:
 
     def diag(self) -> dict:
         """Why candidates left the residency pass (dpro_cuda_batch_diag)."""
-        d = np.zeros(6, np.int64)
+        d = np.zeros(10, np.int64)
         _check(self.engine.ctx, N.lib.dpro_cuda_batch_diag(self.engine.ctx, self.handle,
-                                                           N.ptr(d), 6), "batch_diag")
+                                                           N.ptr(d), 10), "batch_diag")
         return {"pass0_ring": int(d[0]), "pass0_rl": int(d[1]), "deep_ring": int(d[2]),
-                "deep_rl": int(d[3]), "overlay": bool(d[4]), "materialized": int(d[5])}
+                "deep_rl": int(d[3]), "overlay": bool(d[4]), "materialized": int(d[5]),
+                "pass_ms": [round(x / 1e3, 3) for x in d[6:10].tolist()]}
 
     def pack_info(self) -> np.ndarray:
         """[n, 4]: first op without duration, not-fast bits, multi-pred ops, sources."""
