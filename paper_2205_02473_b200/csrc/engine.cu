@@ -200,6 +200,8 @@ struct dpro_ctx {
   std::unique_ptr<Pool> pool;  // created on first use
   int pack_clusters = 0;       // co-resident pack clusters (queried once)
   cudaStream_t copy_stream = nullptr;  // H2D of delta chunks (overlaps the merges)
+  cudaStream_t side_stream = nullptr;  // overlay batches: known deep-queue candidates
+  cudaEvent_t side_ev[2] = {nullptr, nullptr};
   std::vector<cudaEvent_t> chunk_ev;   // one per in-flight chunk copy
   int host_threads = 0;  // option "host_threads": pool size (0 = all hardware threads)
   Pool& workers() {
@@ -309,6 +311,8 @@ struct dpro_batch {
   uint32_t max_cnt_ov = 0;      // max base + overlay counters of a candidate
   int32_t n_mat = 0;            // candidates re-run through the materialized path
   uint32_t ring_hint = 0;       // residency-pass ring capacity learned from the last replay
+  std::vector<int32_t> g3;      // candidates that needed global rings (run first next time)
+  DevBuf hint;                  // device list of this replay's global-ring candidates
   // pass timing of the last fast / overlay replay (dpro_cuda_batch_diag):
   // events before pass 0, after pass 0, 1, 3 and the general hand-off
   cudaEvent_t pev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -709,6 +713,11 @@ void dpro_cuda_destroy(dpro_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  if (ctx->side_stream) {
+    cudaStreamSynchronize(ctx->side_stream);
+    cudaStreamDestroy(ctx->side_stream);
+    for (auto e : ctx->side_ev) cudaEventDestroy(e);
+  }
   if (ctx->copy_stream) {
     cudaStreamSynchronize(ctx->copy_stream);
     cudaStreamDestroy(ctx->copy_stream);
@@ -1692,30 +1701,55 @@ int launch_ov_kd(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule, FastCfg F)
   CU(cudaMemsetAsync(b->work.p, 0, 48, ctx->stream));
   b->F = F;
   const dpro_resident* r = b->res;
+  CU(b->hint.ensure(4 * (size_t(b->n) + 1)));
+  unsigned* hint = b->hint.as<unsigned>();
   b->mark(0, ctx->stream);
-  kern<<<grid, 32 * NW, F.warp_bytes, ctx->stream>>>(
-      b->desc.as<Cand>(), b->ovdesc.as<dpro_k::OvCand>(), b->n, r->ob, b->S, b->O,
-      b->ovgcnt.as<uint8_t>(), F, want_schedule ? 1 : 0, b->work.as<unsigned>(), 0);
-  CU(cudaGetLastError());
-  b->mark(1, ctx->stream);
+  // candidates known (from an earlier replay) to need global rings start
+  // first, on the side stream, so they overlap the residency pass
   FastCfg D = F;  // pass 1: ring overflows, one CTA per SM, deepest rings
   D.rl = std::max<uint32_t>(F.rl, 2048);
   const size_t lim = dyn_max - dpro_k::kOvListBytes;
   while (D.qc < 4096 && fast_bytes(D.dcap, D.qc * 2, D.rl, D.ccap, NW) <= lim) D.qc *= 2;
   D.warp_bytes = static_cast<uint32_t>(fast_bytes(D.dcap, D.qc, D.rl, D.ccap, NW)) +
                  dpro_k::kOvListBytes;
+  FastCfg G;
+  const bool g3ok = pass3_cfg(ctx, D, NW, G, dpro_k::kOvListBytes);
+  const bool side = g3ok && !b->g3.empty();
+  if (side) {
+    if (!ctx->side_stream) {
+      CU(cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking));
+      CU(cudaEventCreateWithFlags(&ctx->side_ev[0], cudaEventDisableTiming));
+      CU(cudaEventCreateWithFlags(&ctx->side_ev[1], cudaEventDisableTiming));
+    }
+    const int32_t k3 = dpro_k::kRetry3;
+    for (int32_t c : b->g3)
+      CU(cudaMemcpyAsync(b->O.status + c, &k3, 4, cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaEventRecord(ctx->side_ev[0], ctx->stream));
+    CU(cudaStreamWaitEvent(ctx->side_stream, ctx->side_ev[0], 0));
+    const int g4 = std::max(1, std::min<int>(ctx->sm_count, static_cast<int>(b->g3.size())));
+    kern<<<g4, 32 * NW, G.warp_bytes, ctx->side_stream>>>(
+        b->desc.as<Cand>(), b->ovdesc.as<dpro_k::OvCand>(), b->n, r->ob, b->S, b->O,
+        b->ovgcnt.as<uint8_t>(), G, want_schedule ? 1 : 0, b->work.as<unsigned>(), 4, hint);
+    CU(cudaGetLastError());
+    CU(cudaEventRecord(ctx->side_ev[1], ctx->side_stream));
+  }
+  kern<<<grid, 32 * NW, F.warp_bytes, ctx->stream>>>(
+      b->desc.as<Cand>(), b->ovdesc.as<dpro_k::OvCand>(), b->n, r->ob, b->S, b->O,
+      b->ovgcnt.as<uint8_t>(), F, want_schedule ? 1 : 0, b->work.as<unsigned>(), 0, hint);
+  CU(cudaGetLastError());
+  b->mark(1, ctx->stream);
   kern<<<ctx->sm_count, 32 * NW, D.warp_bytes, ctx->stream>>>(
       b->desc.as<Cand>(), b->ovdesc.as<dpro_k::OvCand>(), b->n, r->ob, b->S, b->O,
-      b->ovgcnt.as<uint8_t>(), D, want_schedule ? 1 : 0, b->work.as<unsigned>(), 1);
+      b->ovgcnt.as<uint8_t>(), D, want_schedule ? 1 : 0, b->work.as<unsigned>(), 1, hint);
   CU(cudaGetLastError());
   b->mark(2, ctx->stream);
-  FastCfg G;
-  if (pass3_cfg(ctx, D, NW, G, dpro_k::kOvListBytes)) {
+  if (g3ok) {
     kern<<<ctx->sm_count, 32 * NW, G.warp_bytes, ctx->stream>>>(
         b->desc.as<Cand>(), b->ovdesc.as<dpro_k::OvCand>(), b->n, r->ob, b->S, b->O,
-        b->ovgcnt.as<uint8_t>(), G, want_schedule ? 1 : 0, b->work.as<unsigned>(), 3);
+        b->ovgcnt.as<uint8_t>(), G, want_schedule ? 1 : 0, b->work.as<unsigned>(), 3, hint);
     CU(cudaGetLastError());
   }
+  if (side) CU(cudaStreamWaitEvent(ctx->stream, ctx->side_ev[1], 0));
   b->mark(3, ctx->stream);
   b->mark(4, ctx->stream);
   b->pev_valid = true;
@@ -1769,6 +1803,13 @@ int finish_overlay_mat(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
   CU(cudaMemcpyAsync(w, b->work.p, 48, cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
   if (w[5] > static_cast<unsigned>(b->n) / 8 && b->F.qc < 64) b->ring_hint = 2 * b->F.qc;
+  if (w[11]) {  // global-ring candidates: run them first next time
+    std::vector<uint32_t> h(std::min<unsigned>(w[11], static_cast<unsigned>(b->n)));
+    CU(cudaMemcpy(h.data(), b->hint.p, 4 * h.size(), cudaMemcpyDeviceToHost));
+    for (uint32_t c : h)
+      if (std::find(b->g3.begin(), b->g3.end(), static_cast<int32_t>(c)) == b->g3.end())
+        b->g3.push_back(static_cast<int32_t>(c));
+  }
   if (b->n_mat == 0 && w[1] == 0) return DPRO_OK;
   std::vector<int32_t> stv(b->n);
   CU(cudaMemcpy(stv.data(), b->O.status, 4 * size_t(b->n), cudaMemcpyDeviceToHost));

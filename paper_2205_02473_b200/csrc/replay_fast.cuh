@@ -42,6 +42,7 @@ __device__ __forceinline__ uint32_t bail_code(uint32_t m) {
 constexpr int kRetry = 9;   // status of a candidate queued for the deep-ring pass
 constexpr int kRetry2 = 11;  // queued for the global-ring pass (pass 3)
 constexpr int kRetryGen = 12;  // handed to the general kernel (replay_batch_kernel)
+constexpr int kRetry3 = 13;    // overlay batches: known deep-queue candidates (pass 4)
 
 // segt: the event-time EPOCH (count of distinct event times so far) of the
 // device's last arrival segment -- a time-independent stand-in for "the
@@ -808,21 +809,28 @@ __global__ void __launch_bounds__(32 * NW) replay_fast_kernel(
 // marked kRetryMat: the host re-runs them through the materialized path.
 constexpr int kRetryMat = 10;
 
+// pass 4: candidates a previous replay of the batch sent to the global-ring
+// pass (status preset to kRetry3), run first on a side stream so they
+// overlap the residency pass instead of trailing it; hint[] records the
+// candidates that reach the global-ring pass (count in work[11]).
 template <int NW, int KD>
 __global__ void __launch_bounds__(32 * NW) replay_ov_kernel(
     const Cand* __restrict__ cands, const OvCand* __restrict__ ovc, int n_cands, OvBase base,
-    Scratch S, Outs O, uint8_t* gcnt, FastCfg F, int want_schedule, unsigned* work, int pass) {
+    Scratch S, Outs O, uint8_t* gcnt, FastCfg F, int want_schedule, unsigned* work, int pass,
+    unsigned* hint) {
   extern __shared__ __align__(16) unsigned char fsm[];
   __shared__ int s_cid;
-  unsigned* counter = work + (pass == 1 ? 2 : pass == 3 ? 4 : 0);
+  unsigned* counter = work + (pass == 1 ? 2 : pass == 3 ? 4 : pass == 4 ? 10 : 0);
   for (;;) {
     if (threadIdx.x == 0) s_cid = static_cast<int>(atomicAdd(counter, 1u));
     __syncthreads();
     const int cid = s_cid;
     __syncthreads();
     if (cid >= n_cands) break;
+    if (pass == 0 && O.status[cid] == kRetry3) continue;
     if (pass == 1 && O.status[cid] != kRetry) continue;
     if (pass == 3 && O.status[cid] != kRetry2) continue;
+    if (pass == 4 && O.status[cid] != kRetry3) continue;
     const Cand c = cands[cid];
     const OvCand oc = ovc[cid];
     if (oc.pad) continue;  // materialized path (host)
@@ -849,6 +857,7 @@ __global__ void __launch_bounds__(32 * NW) replay_ov_kernel(
         O.status[cid] = pass == 0 ? kRetry : kRetry2;
         atomicAdd(work + 3, 1u);
         atomicAdd(work + (rc == kBailRing ? 5 : 6) + (pass == 1 ? 2 : 0), 1u);
+        if (pass == 1) hint[atomicAdd(work + 11, 1u)] = static_cast<unsigned>(cid);
       } else if (rc != kDone) {
         O.status[cid] = kRetryMat;
         atomicAdd(work + 1, 1u);
