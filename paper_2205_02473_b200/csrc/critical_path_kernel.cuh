@@ -43,6 +43,20 @@ __device__ __forceinline__ uint32_t tl_next(uint32_t v, const Cand& c,
   return q + 1 < dhead[c.dev[v]] ? qbuf[q + 1] : kNone;
 }
 
+// qpos (an op's position in its device timeline) from the timelines in qbuf,
+// for the candidates K3 walks: the fast replay kernels write only qbuf.
+__global__ void __launch_bounds__(256) qpos_scatter_kernel(const Cand* __restrict__ cands,
+                                                           int n_cands, Scratch S, Outs O) {
+  for (int cid = blockIdx.x; cid < n_cands; cid += gridDim.x) {
+    if (O.status[cid] != kOk) continue;
+    const Cand c = cands[cid];
+    const uint32_t* qbuf = S.qbuf + c.op_off;
+    uint32_t* qpos = S.qpos + c.op_off;
+    const uint32_t total = S.devoff[c.dof_off + c.d];  // every non-virtual op ran
+    for (uint32_t p = threadIdx.x; p < total; p += blockDim.x) qpos[qbuf[p]] = p;
+  }
+}
+
 __global__ void __launch_bounds__(128) critical_path_kernel(
     const Cand* __restrict__ cands, int n_cands, Scratch S, Outs O,
     CpScratch P, uint32_t* paths, long long* path_len) {

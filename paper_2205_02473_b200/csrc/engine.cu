@@ -297,6 +297,7 @@ struct dpro_batch {
   std::vector<dpro_k::PackInfo> info;  // host copy (read once after pack)
   bool replayed = false;
   bool with_schedule = false;
+  bool qpos_ready = false;  // qpos derived from qbuf since the last replay
   // overlay batches: candidates replayed on the resident base + overlays
   bool overlay = false;
   std::vector<dpro_ov::OverlayHost> ovh;
@@ -1306,6 +1307,22 @@ int build_overlay_batch(dpro_ctx* ctx, dpro_batch* b, dpro_resident* r,
     b->info[i].first_missing = b->ovh[i].first_missing;
     b->info[i].not_fast = b->ovh[i].fast ? 0u : 1u;
   }
+  // whole-graph rewrites (recompute / grad-accum variants: >1% of the ops
+  // new) are the long candidates of a batch: start them first, on the side
+  // stream with global rings, so they overlap everything else
+  b->g3.clear();
+  {
+    std::vector<size_t> sz;
+    for (int32_t i = 0; i < n; ++i)
+      if (b->ovh[i].fast) sz.push_back(b->ovh[i].fin.size());
+    if (!sz.empty()) {
+      std::nth_element(sz.begin(), sz.begin() + sz.size() / 2, sz.end());
+      const size_t med = sz[sz.size() / 2];
+      for (int32_t i = 0; i < n; ++i)
+        if (b->ovh[i].fast && b->ovh[i].fin.size() > std::max<size_t>(100 * med, r->n / 100))
+          b->g3.push_back(i);
+    }
+  }
   b->replayed = b->with_schedule = false;
   tr.mark("overlay batch staged + uploaded", ctx->stream, true);
   return DPRO_OK;
@@ -1886,6 +1903,7 @@ int dpro_cuda_batch_replay(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) 
   if (st != DPRO_OK) return st;
   b->replayed = true;
   b->with_schedule = want_schedule != 0;
+  b->qpos_ready = false;
   return DPRO_OK;
 }
 
@@ -2037,6 +2055,10 @@ int dpro_cuda_batch_critical_paths(dpro_ctx* ctx, dpro_batch* b,
   long long* d_len = b->cp.as<long long>(o); o += s_len;
   CU(cudaMemcpyAsync(P.e_off, e_off.data(), n * 8, cudaMemcpyHostToDevice, ctx->stream));
   CU(cudaMemcpyAsync(P.po_off, po_off.data(), n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  if (!b->qpos_ready)
+    dpro_k::qpos_scatter_kernel<<<std::max<int>(1, std::min<int>(n, ctx->sm_count * 8)), 256, 0,
+                                  ctx->stream>>>(b->desc.as<Cand>(), b->n, b->S, b->O);
+  b->qpos_ready = true;
   const int threads = 128;
   const int grid = std::max<int>(1, std::min<int>((n * 32 + threads - 1) / threads, ctx->sm_count * 8));
   dpro_k::critical_path_kernel<<<grid, threads, 0, ctx->stream>>>(
@@ -2155,6 +2177,7 @@ int dpro_cuda_critical_path(dpro_ctx* ctx, const dpro_csr* graph,
     CU(cudaMemcpyAsync(b->O.status, &ok, 4, cudaMemcpyHostToDevice, ctx->stream));
     b->replayed = true;
     b->with_schedule = true;
+    b->qpos_ready = true;  // no timelines: the exec graph's edges stand for them
     return dpro_cuda_batch_critical_paths(ctx, b, path, path_len);
   };
   st = run();

@@ -472,10 +472,9 @@ struct FastWarp {
       while (head < tail) {
         const uint4 x = r[head & m];
         const unsigned long long en = t + x.y;
-        if (want) {
+        if (want) {  // (qpos is derived from qbuf only when K3 needs it)
           start[x.x] = t;
           end[x.x] = en;
-          qpos[x.x] = base + head;
         }
         qbuf[base + head] = x.x;
         ++head;
