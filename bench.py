@@ -6,15 +6,17 @@
 Workload (default: BASELINE configs[3], the largest single-GPU config):
 GPT-2 medium 64-worker ring-all-reduce DFG (292 tensors, 4.80M ops, 6.0M
 edges, 128 devices) and its per-round candidate mix:
-the recompute candidate, the grad-accum candidate and 146 single-worker
-adjacent op-fusion pairs -- 148 candidates per GPU, one per SM. Candidates
-are deltas of one resident base graph (include/dpro_cuda.h dpro_delta). One
-step = the device-side merge of every delta (K0) + pack + one exact replay
+the recompute candidate, the grad-accum candidate and 738 single-worker
+adjacent op-fusion pairs -- 740 candidates per GPU (5 resident per SM).
+Candidates are deltas of one resident base graph (include/dpro_cuda.h
+dpro_delta), replayed on the base's packed layout plus per-candidate
+overlays (csrc/overlay.h). One step = the overlay upload + one exact replay
 of every candidate (K1: per-op start/end + makespan) + the per-round
 best-cost exchange (argmin; two NCCL MIN all-reduces across ranks when
-N > 1), with the inputs (base graph + deltas) resident in HBM. The step's
-working set (~60 GB of merged CSRs, packed records and schedules) is far
-larger than L2: no flush needed.
+N > 1), with the inputs (base graph + overlays) resident in HBM. The step's
+working set (~85 GB of schedules and timelines) is far larger than L2: no
+flush needed. Smaller configs (--config 1-3) use per-candidate merged
+copies (delta merge K0 + pack) instead of overlays.
 
 Multi-GPU: one process per GPU (torchrun), each rank replays its own batch
 (weak scaling); time is the max over ranks of CUDA-event time.
@@ -286,6 +288,10 @@ def run_ours(args) -> None:
     stream = torch.cuda.current_stream()
     eng = Engine(local)
     eng.set_stream(stream.cuda_stream)
+    # multi-million-op graphs: replay on the resident base + per-candidate
+    # overlays (csrc/overlay.h) instead of a merged copy per candidate
+    overlay = w.spec["layers"] * w.spec["workers"] * w.spec["workers"] > 1_000_000
+    eng.set_option("overlay", 1 if overlay else 0)
     resident = eng.resident(base.graph().csr)  # base graph: uploaded once, stays in HBM
     batch = eng.delta_batch(resident, deltas)   # deltas uploaded once: inputs in HBM
     algo_bytes = batch.algorithmic_bytes()
@@ -330,6 +336,10 @@ def run_ours(args) -> None:
     ok = int((st == 0).sum())
     assert ok == B, f"{B - ok} candidates failed"
     kstats = batch.stats()
+    kdiag = batch.diag()
+    n_ops_mean = float(batch.n_ops.mean())
+    n_edges_mean = float(batch.n_edges.mean())
+    batch.close()  # the e2e call below allocates its own batch
 
     # e2e through the C ABI with HOST buffers: the search's call
     # (dpro_cuda_replay_delta_batch: H2D of the deltas, merge, pack, replay,
@@ -378,7 +388,7 @@ def run_ours(args) -> None:
                                         os.cpu_count() or 1, args.cpu_seconds)
     traffic = _ncu_traffic(args.config)
     clocks = clk.summary()
-    n_ops = float(batch.n_ops.mean())
+    n_ops = n_ops_mean
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
@@ -388,15 +398,22 @@ def run_ours(args) -> None:
         "details": {
             "candidates": {k: sum(1 for d in descs if d[0] == k)
                            for k in sorted({d[0] for d in descs})},
-            "n_ops_mean": n_ops, "n_edges_mean": float(batch.n_edges.mean()),
-            "step": "delta merge (K0) + pack + replay (K1, per-op start/end) + best-cost "
-                    "exchange, inputs (base graph + deltas) resident in HBM",
+            "n_ops_mean": n_ops, "n_edges_mean": n_edges_mean,
+            "engine": "overlay batches (resident base + per-candidate overlays)" if overlay
+                      else "delta merge + pack per candidate",
+            "pass_ms_last_step": kdiag["pass_ms"],
+            "step": ("overlay upload + replay (K1 on base + overlays, per-op start/end) + "
+                     "best-cost exchange, inputs (base graph + overlays) resident in HBM"
+                     if overlay else
+                     "delta merge (K0) + pack + replay (K1, per-op start/end) + best-cost "
+                     "exchange, inputs (base graph + deltas) resident in HBM"),
             "node_updates_per_s": value * n_ops,
             "prepare_ms_mean": float(np.mean(prep_ms)),
             "replay_ms_mean": kmean * 1e3,
             "replay_only_per_s": world * B / kmean,
             "build_s": round(t_build, 2), "status_ok": ok,
-            "kernel": "replay_fast_kernel (general-path fallbacks: %d)" % kstats["fallbacks"],
+            "kernel": "%s (general/materialized hand-offs: %d)" % (
+                "replay_ov_kernel" if overlay else "replay_fast_kernel", kstats["fallbacks"]),
             "fast_smem_bytes_per_candidate": kstats["fast_smem_bytes"],
             "fast_candidates_per_sm": kstats["fast_blocks_per_sm"],
             "deep_ring_candidates": kstats["deep_ring_retries"]},
@@ -404,7 +421,7 @@ def run_ours(args) -> None:
                      "frac": achieved / peak,
                      "traffic": traffic["dram_bytes_per_launch"] if traffic else None,
                      "traffic_source": traffic.get("source") if traffic else None,
-                     "kernel": "replay_fast_kernel",
+                     "kernel": "replay_ov_kernel" if overlay else "replay_fast_kernel",
                      "algorithmic_bytes_per_launch": algo_bytes,
                      "algorithmic_bytes": "32 V + 4 E per candidate (BASELINE.md section 2)",
                      "peak_source": peak_src, "kernel_ms_mean": kmean * 1e3},
@@ -415,9 +432,11 @@ def run_ours(args) -> None:
                 "d2h_bytes_per_step": d2h,
                 "note": "dpro_cuda_replay_delta_batch with host deltas (H2D + merge + pack + "
                         "replay, makespan-only) per step"},
-        # per step: delta_merge_kernel, pack_kernel, replay_fast_kernel x2
-        # (residency pass + deep-ring pass; profiles/r02_c4_launches.csv)
-        "gpu_launches": 4 * args.steps,
+        # per step -- overlay: replay_ov_kernel x4 (global-ring side pass,
+        # residency pass, deep-ring pass, global-ring pass); merged: delta
+        # merge, pack, replay_fast_kernel x3 + the general hand-off
+        # (profiles/r02_*launches.csv)
+        "gpu_launches": (4 if overlay else 6) * args.steps,
         "clocks": clocks,
     }
     print(json.dumps(line))

@@ -25,12 +25,12 @@ def main():
     print(f"deltas {time.perf_counter() - t:.2f} s", flush=True)
     eng = Engine(0)
     import os
-    for key in ("ring", "warps"):
+    for key in ("ring", "warps", "deep_first"):
         if os.environ.get("DPRO_" + key.upper()):
             eng.set_option(key, int(os.environ["DPRO_" + key.upper()]))
     res = eng.resident(base.graph().csr)
     out = {}
-    for ov in (1, 0):
+    for ov in ((1, 0) if not os.environ.get("MAT_ONLY") else (0,)):
         if ov == 0 and (B > 296 or os.environ.get('OV_ONLY')):
             continue
         eng.set_option("overlay", ov)
