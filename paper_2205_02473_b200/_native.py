@@ -145,6 +145,8 @@ def _load() -> C.CDLL:
             "or __graft_entry__.build(); there is no CPU fallback")
     lib = C.CDLL(str(LIB_PATH))
     for name, (res, args) in SIGNATURES.items():
+        if "DPRO_LIB" in os.environ and not hasattr(lib, name):
+            continue  # A/B experiments against an older build of the library
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

@@ -428,10 +428,16 @@ class LayeredBase:
         members = np.ascontiguousarray(members, np.int32)
         ks = np.ascontiguousarray(ks, np.int32)
         out = C.c_void_p()
-        rc = N.lib.dpro_base_delta_batch_ex(self.handle, n, N.ptr(n_groups), N.ptr(spec_off),
-                                            N.ptr(group_off), N.ptr(members), N.ptr(ks),
-                                            N.ptr(fj), N.ptr(bj), N.ptr(jw), threads,
-                                            C.byref(out))
+        if jw is None and not hasattr(N.lib, "dpro_base_delta_batch_ex"):  # older builds
+            rc = N.lib.dpro_base_delta_batch_ops(self.handle, n, N.ptr(n_groups),
+                                                 N.ptr(spec_off), N.ptr(group_off),
+                                                 N.ptr(members), N.ptr(ks), N.ptr(fj),
+                                                 N.ptr(bj), threads, C.byref(out))
+        else:
+            rc = N.lib.dpro_base_delta_batch_ex(self.handle, n, N.ptr(n_groups),
+                                                N.ptr(spec_off), N.ptr(group_off),
+                                                N.ptr(members), N.ptr(ks), N.ptr(fj), N.ptr(bj),
+                                                N.ptr(jw), threads, C.byref(out))
         if rc != N.DPRO_OK:
             raise Error(N.lib.dpro_graph_last_error().decode())
         return DeltaSet(out.value, self)
