@@ -314,6 +314,7 @@ struct dpro_batch {
   uint32_t ring_hint = 0;       // residency-pass ring capacity learned from the last replay
   std::vector<int32_t> g3;      // candidates that needed global rings (run first next time)
   DevBuf hint;                  // device list of this replay's global-ring candidates
+  DevBuf order;                 // candidate order of the residency pass: long ones first
   // pass timing of the last fast / overlay replay (dpro_cuda_batch_diag):
   // events before pass 0, after pass 0, 1, 3 and the general hand-off
   cudaEvent_t pev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -1267,11 +1268,10 @@ int build_overlay_batch(dpro_ctx* ctx, dpro_batch* b, dpro_resident* r,
   const size_t s_u32 = align16(so * 4 + 4), s_dof = align16(sdo * 4 + 4),
                s_busy = align16(sd * 8 + 8), s_dh = align16(sd * 4 + 4),
                s_u8 = align16(so + 1);
-  CU(b->scratch.ensure(2 * s_u32 + s_dof + s_busy + s_dh + s_u8));
+  CU(b->scratch.ensure(s_u32 + s_dof + s_busy + s_dh + s_u8));
   size_t o = 0;
-  b->S = Scratch{};
+  b->S = Scratch{};  // no qpos: K3 does not run on overlay batches
   b->S.qbuf = b->scratch.as<uint32_t>(o); o += s_u32;
-  b->S.qpos = b->scratch.as<uint32_t>(o); o += s_u32;
   b->S.devoff = b->scratch.as<uint32_t>(o); o += s_dof;
   b->S.busy = b->scratch.as<long long>(o); o += s_busy;
   b->S.dhead = b->scratch.as<uint32_t>(o); o += s_dh;
@@ -1307,21 +1307,29 @@ int build_overlay_batch(dpro_ctx* ctx, dpro_batch* b, dpro_resident* r,
     b->info[i].first_missing = b->ovh[i].first_missing;
     b->info[i].not_fast = b->ovh[i].fast ? 0u : 1u;
   }
-  // whole-graph rewrites (recompute / grad-accum variants: >1% of the ops
-  // new) are the long candidates of a batch: start them first, on the side
-  // stream with global rings, so they overlap everything else
+  // whole-graph rewrites (recompute / grad-accum variants: 100x the median
+  // overlay) are the long candidates of a batch (twice the event rounds of
+  // an op fusion): the residency pass hands them out first so they overlap
+  // everything else instead of trailing it
   b->g3.clear();
   {
     std::vector<size_t> sz;
     for (int32_t i = 0; i < n; ++i)
       if (b->ovh[i].fast) sz.push_back(b->ovh[i].fin.size());
+    size_t cut = SIZE_MAX;
     if (!sz.empty()) {
       std::nth_element(sz.begin(), sz.begin() + sz.size() / 2, sz.end());
-      const size_t med = sz[sz.size() / 2];
-      for (int32_t i = 0; i < n; ++i)
-        if (b->ovh[i].fast && b->ovh[i].fin.size() > std::max<size_t>(100 * med, r->n / 100))
-          b->g3.push_back(i);
+      cut = std::max<size_t>(100 * sz[sz.size() / 2], r->n / 100);
     }
+    std::vector<uint32_t> ord;
+    for (int32_t i = 0; i < n; ++i)
+      if (b->ovh[i].fast && b->ovh[i].fin.size() > cut) ord.push_back(i);
+    for (int32_t i = 0; i < n; ++i)
+      if (!(b->ovh[i].fast && b->ovh[i].fin.size() > cut)) ord.push_back(i);
+    CU(b->order.ensure(4 * (size_t(n) + 1)));
+    if (n) CU(cudaMemcpyAsync(b->order.p, ord.data(), 4 * size_t(n), cudaMemcpyHostToDevice,
+                              ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));  // ord is a local
   }
   b->replayed = b->with_schedule = false;
   tr.mark("overlay batch staged + uploaded", ctx->stream, true);
@@ -1746,24 +1754,28 @@ int launch_ov_kd(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule, FastCfg F)
     const int g4 = std::max(1, std::min<int>(ctx->sm_count, static_cast<int>(b->g3.size())));
     kern<<<g4, 32 * NW, G.warp_bytes, ctx->side_stream>>>(
         b->desc.as<Cand>(), b->ovdesc.as<dpro_k::OvCand>(), b->n, r->ob, b->S, b->O,
-        b->ovgcnt.as<uint8_t>(), G, want_schedule ? 1 : 0, b->work.as<unsigned>(), 4, hint);
+        b->ovgcnt.as<uint8_t>(), G, want_schedule ? 1 : 0, b->work.as<unsigned>(), 4, hint,
+        b->order.as<unsigned>());
     CU(cudaGetLastError());
     CU(cudaEventRecord(ctx->side_ev[1], ctx->side_stream));
   }
   kern<<<grid, 32 * NW, F.warp_bytes, ctx->stream>>>(
       b->desc.as<Cand>(), b->ovdesc.as<dpro_k::OvCand>(), b->n, r->ob, b->S, b->O,
-      b->ovgcnt.as<uint8_t>(), F, want_schedule ? 1 : 0, b->work.as<unsigned>(), 0, hint);
+      b->ovgcnt.as<uint8_t>(), F, want_schedule ? 1 : 0, b->work.as<unsigned>(), 0, hint,
+      b->order.as<unsigned>());
   CU(cudaGetLastError());
   b->mark(1, ctx->stream);
   kern<<<ctx->sm_count, 32 * NW, D.warp_bytes, ctx->stream>>>(
       b->desc.as<Cand>(), b->ovdesc.as<dpro_k::OvCand>(), b->n, r->ob, b->S, b->O,
-      b->ovgcnt.as<uint8_t>(), D, want_schedule ? 1 : 0, b->work.as<unsigned>(), 1, hint);
+      b->ovgcnt.as<uint8_t>(), D, want_schedule ? 1 : 0, b->work.as<unsigned>(), 1, hint,
+      b->order.as<unsigned>());
   CU(cudaGetLastError());
   b->mark(2, ctx->stream);
   if (g3ok) {
     kern<<<ctx->sm_count, 32 * NW, G.warp_bytes, ctx->stream>>>(
         b->desc.as<Cand>(), b->ovdesc.as<dpro_k::OvCand>(), b->n, r->ob, b->S, b->O,
-        b->ovgcnt.as<uint8_t>(), G, want_schedule ? 1 : 0, b->work.as<unsigned>(), 3, hint);
+        b->ovgcnt.as<uint8_t>(), G, want_schedule ? 1 : 0, b->work.as<unsigned>(), 3, hint,
+        b->order.as<unsigned>());
     CU(cudaGetLastError());
   }
   if (side) CU(cudaStreamWaitEvent(ctx->stream, ctx->side_ev[1], 0));
@@ -1861,7 +1873,6 @@ int finish_overlay_mat(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
       CU(cp(b->O.end + p.op_off, sub.O.end + q.op_off, 8 * size_t(p.n)));
     }
     CU(cp(b->S.qbuf + p.op_off, sub.S.qbuf + q.op_off, 4 * size_t(p.n)));
-    CU(cp(b->S.qpos + p.op_off, sub.S.qpos + q.op_off, 4 * size_t(p.n)));
     CU(cp(b->S.sched + p.op_off, sub.S.sched + q.op_off, size_t(p.n)));
     CU(cp(b->S.devoff + p.dof_off, sub.S.devoff + q.dof_off, 4 * (size_t(p.d) + 1)));
     CU(cp(b->S.busy + p.dev_off, sub.S.busy + q.dev_off, 8 * size_t(p.d)));

@@ -816,12 +816,16 @@ template <int NW, int KD>
 __global__ void __launch_bounds__(32 * NW) replay_ov_kernel(
     const Cand* __restrict__ cands, const OvCand* __restrict__ ovc, int n_cands, OvBase base,
     Scratch S, Outs O, uint8_t* gcnt, FastCfg F, int want_schedule, unsigned* work, int pass,
-    unsigned* hint) {
+    unsigned* hint, const unsigned* order) {
   extern __shared__ __align__(16) unsigned char fsm[];
   __shared__ int s_cid;
   unsigned* counter = work + (pass == 1 ? 2 : pass == 3 ? 4 : pass == 4 ? 10 : 0);
   for (;;) {
-    if (threadIdx.x == 0) s_cid = static_cast<int>(atomicAdd(counter, 1u));
+    if (threadIdx.x == 0) {
+      // order: the batch's long candidates first, so they overlap the rest
+      const unsigned k = atomicAdd(counter, 1u);
+      s_cid = k < static_cast<unsigned>(n_cands) ? static_cast<int>(order[k]) : n_cands;
+    }
     __syncthreads();
     const int cid = s_cid;
     __syncthreads();

@@ -197,7 +197,8 @@ class Workload:
     def op_fusion_mix(self, n: int, rank: int = 0) -> list[tuple]:
         return op_fusion_mix(self.seed, len(self.cluster.workers()), self.layers, n, rank)
 
-    def candidate_deltas(self, base, n: int, rank: int = 0, threads: int = 8):
+    def candidate_deltas(self, base, n: int, rank: int = 0, threads: int = 8,
+                         variants: bool = True):
         """The workload's candidate batch as deltas against `base` (a
         LayeredBase of this workload) -> (deltas, descriptions). Config 4:
         op_fusion_mix(); the others: candidate_partitions()."""
@@ -208,6 +209,8 @@ class Workload:
             specs = [([[i] for i in range(L)], pk[c].tolist()) for c in range(n)]
             return base.deltas(specs, threads=threads), [("partition", tuple(r)) for r in pk.tolist()]
         descs = self.op_fusion_mix(n, rank)
+        if not variants:  # op-fusion candidates only (measurements)
+            descs = [d for d in self.op_fusion_mix(n + 2, rank) if d[0] == "opf"][:n]
         opf = [d for d in descs if d[0] == "opf"]
         fj = np.zeros((len(opf), L - 1), np.uint8)
         bj = np.zeros((len(opf), L - 1), np.uint8)

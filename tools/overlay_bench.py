@@ -2,6 +2,7 @@
 
     python tools/overlay_bench.py CONFIG B [iters]
 """
+import os
 import sys
 import time
 from pathlib import Path
@@ -21,7 +22,8 @@ def main():
     w = workload(cfg)
     base = LayeredBase(w.model, w.cluster)
     t = time.perf_counter()
-    deltas, descs = w.candidate_deltas(base, B, threads=16)
+    deltas, descs = w.candidate_deltas(base, B, threads=16,
+                                       variants=not os.environ.get("NO_VARIANTS"))
     print(f"deltas {time.perf_counter() - t:.2f} s", flush=True)
     eng = Engine(0)
     import os
