@@ -356,7 +356,8 @@ def run_ours(args) -> None:
             if dist is not None:
                 dist.barrier()
             t0 = time.perf_counter()
-            assert fn() == 0
+            rc = fn()
+            assert rc == 0, f"e2e call failed ({rc}): {N.lib.dpro_cuda_last_error(eng.ctx)}"
             el = time.perf_counter() - t0
             if i > 0:
                 out.append(el)

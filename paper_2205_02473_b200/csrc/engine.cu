@@ -1497,7 +1497,7 @@ void dpro_cuda_batch_destroy(dpro_ctx* ctx, dpro_batch* b) {
   if (!b) return;
   if (ctx) {
     cudaStreamSynchronize(ctx->stream);
-    if (!ctx->spare) {
+    if (!ctx->spare && !b->overlay) {  // overlay batches are big: never kept
       ctx->spare = b;
       return;
     }
