@@ -432,8 +432,10 @@ def run_ours(args) -> None:
                                                      "sample": why},
         "e2e": {"value": world * B / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
-                "note": "dpro_cuda_replay_delta_batch with host deltas (H2D + merge + pack + "
-                        "replay, makespan-only) per step"},
+                "note": ("dpro_cuda_replay_delta_batch with host deltas per step: overlay build on "
+                         "host threads + H2D + replay (makespan only) + D2H" if overlay else
+                         "dpro_cuda_replay_delta_batch with host deltas per step: H2D + merge + "
+                         "pack + replay (makespan only) + D2H")},
         # per step -- overlay: replay_ov_kernel x4 (global-ring side pass,
         # residency pass, deep-ring pass, global-ring pass); merged: delta
         # merge, pack, replay_fast_kernel x3 + the general hand-off

@@ -15,10 +15,18 @@ from paper_2205_02473_b200.workloads import workload  # noqa: E402
 cfg = int(os.environ.get("CFG", "2"))
 nb = int(os.environ.get("NB", "1024"))
 w = workload(cfg)
-graphs = layered_graphs(w.model, w.cluster, w.candidate_partitions(nb), threads=16)
 eng = Engine(0)
 eng.set_option("warps", int(os.environ.get("DPRO_WARPS", "4")))
-b = eng.batch([g.csr for g in graphs])
+if os.environ.get("OVERLAY"):  # the bench's candidate mix on overlay batches
+    from paper_2205_02473_b200.ingest import LayeredBase
+    base = LayeredBase(w.model, w.cluster)
+    deltas, _ = w.candidate_deltas(base, nb, threads=16, variants=False)
+    eng.set_option("overlay", 1)
+    res = eng.resident(base.graph().csr)
+    b = eng.delta_batch(res, deltas)
+else:
+    graphs = layered_graphs(w.model, w.cluster, w.candidate_partitions(nb), threads=16)
+    b = eng.batch([g.csr for g in graphs])
 fn = N.lib.dpro_debug_prof
 fn.argtypes = [C.c_void_p]
 buf = np.zeros(16, np.uint64)
