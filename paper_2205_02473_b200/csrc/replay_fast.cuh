@@ -433,25 +433,13 @@ struct FastWarp {
     }
   }
 
-  // First record of the list starting at sbf (kOv: the overlay's lists).
-  __device__ __forceinline__ uint4 first_rec(uint32_t sbf) const {
-    if (OV && (sbf & kOvF)) return __ldg(ov.erec + (sbf & ~kOvF));
-    return __ldg(erec + sbf);
-  }
-
   // Owner-lane dispatch(t) for device d (replay.cpp:74-90) after merging
   // this round's arrivals into the (ready, index)-ordered tail segment.
   // Returns the in-flight op's end - t (kT32Inf: idle); sets *zero when
   // zero-duration ops ran (they complete next round). epoch: number of
   // distinct event times so far.
-  // frec / zrec (overlay kernels; the materialized kernel keeps the
-  // registers for occupancy): the first out-edge record of the new in-flight
-  // op and of the first zero-duration op dispatched, loaded now and consumed
-  // when they complete (a later round), so the owner applies it without
-  // waiting and single-record lists skip the cooperative expand.
   __device__ __forceinline__ uint32_t dispatch_dev(uint32_t d, unsigned long long t,
-                                                   uint32_t epoch, uint32_t iend, bool* zero,
-                                                   uint4& frec, uint4& zrec, bool* zrec_ok) {
+                                                   uint32_t epoch, uint32_t iend, bool* zero) {
     DevF& s = dv[d];
     uint4* r = ring(d);
     const uint32_t tail = *reinterpret_cast<volatile uint32_t*>(&s.tail);
@@ -496,14 +484,9 @@ struct FastWarp {
         if (x.y > 0) {
           s.isb = x.z;
           s.ise = x.w;
-          if (OV && x.w > (x.z & ~kOvF)) frec = first_rec(x.z);
           iend = x.y;
           infl = true;
           break;
-        }
-        if (OV && head - 1 == zlo && x.w > (x.z & ~kOvF)) {  // first zero-duration op
-          zrec = first_rec(x.z);
-          *zrec_ok = true;
         }
       }
       const unsigned long long bz =
@@ -637,18 +620,15 @@ __device__ uint32_t replay_fast(const Cand& c, int cid, const uint4* rec, const 
 
   // ---- dispatch(0) + event loop (replay.cpp:95-106) ----
   uint32_t iend[KD];  // in-flight end - t per owned device (kT32Inf: idle)
-  uint4 frec[KD], zrec[KD];  // first out-edge records, loaded at dispatch
-  uint32_t zmask = 0, zrmask = 0, epoch = 0;
+  uint32_t zmask = 0, epoch = 0;
 #pragma unroll
   for (int j = 0; j < KD; ++j) {
     iend[j] = kT32Inf;
-    frec[j] = zrec[j] = make_uint4(0, 0, 0, 0);
     const uint32_t d = tid + NT * j;
     if (d < D) {
-      bool z = false, zr = false;
-      iend[j] = W.dispatch_dev(d, 0ull, 0u, kT32Inf, &z, frec[j], zrec[j], &zr);
+      bool z = false;
+      iend[j] = W.dispatch_dev(d, 0ull, 0u, kT32Inf, &z);
       if (z) zmask |= 1u << j;
-      if (zr) zrmask |= 1u << j;
     }
   }
   misc[4 + tid] = 0;  // all devices were just visited
@@ -677,31 +657,22 @@ __device__ uint32_t replay_fast(const Cand& c, int cid, const uint4* rec, const 
     if (tid == 0) misc[2 * ((rpar + 1) & 1u)] = 0;
     ++rpar;
     if (zero_round) {
-      // zero-duration ops dispatched last round complete now (same t); the
-      // owner applies the first op's first record itself (loaded at
-      // dispatch), the rest of the lists go to the cooperative expand
-#pragma unroll
-      for (int j = 0; j < KD; ++j) {
-        if (!(zmask & (1u << j))) continue;
+      // zero-duration ops dispatched last round complete now (same t)
+      uint32_t zm = zmask;
+      while (zm) {
+        const int j = __ffs(zm) - 1;
+        zm &= zm - 1;
         DevF& s = dv[tid + NT * j];
         const uint4* r = W.ring(tid + NT * j);
-        const uint32_t zl = s.zlo, zh = s.zhi;
-        for (uint32_t p = zl; p < zh; ++p) {
+        const uint32_t zh = s.zhi;
+        for (uint32_t p = s.zlo; p < zh; ++p) {
           const uint4 e = r[p & (F.qc - 1)];
           const uint32_t eb = e.z & ~kOvF;
-          if (e.w <= eb) continue;
-          if (OV && p == zl && (zrmask & (1u << j))) {
-            W.edge(zrec[j], t);
-            if (e.w > eb + 1) W.push_range(e.z + 1, e.w - eb - 1);
-          } else {
-            W.push_range(e.z, e.w - eb);
-          }
+          if (e.w > eb) W.push_range(e.z, e.w - eb);
         }
-        __threadfence_block();  // entries read before the slots are released
         *reinterpret_cast<volatile uint32_t*>(&s.zlo) = zh;
       }
       zmask = 0;
-      zrmask = 0;
     } else {
 #pragma unroll
       for (int j = 0; j < KD; ++j) {
@@ -711,14 +682,7 @@ __device__ uint32_t replay_fast(const Cand& c, int cid, const uint4* rec, const 
           const DevF& sd = dv[tid + NT * j];
           const uint32_t ez = sd.isb, ew = sd.ise;
           const uint32_t eb = ez & ~kOvF;
-          if (ew > eb) {
-            if (OV) {  // first record applied by the owner (loaded at dispatch)
-              W.edge(frec[j], t);
-              if (ew > eb + 1) W.push_range(ez + 1, ew - eb - 1);
-            } else {
-              W.push_range(ez, ew - eb);
-            }
-          }
+          if (ew > eb) W.push_range(ez, ew - eb);
         }
       }
     }
@@ -734,10 +698,9 @@ __device__ uint32_t replay_fast(const Cand& c, int cid, const uint4* rec, const 
 #pragma unroll
     for (int j = 0; j < KD; ++j) {
       if (todo & (1u << j)) {
-        bool z = false, zr = false;
-        iend[j] = W.dispatch_dev(tid + NT * j, t, epoch, iend[j], &z, frec[j], zrec[j], &zr);
+        bool z = false;
+        iend[j] = W.dispatch_dev(tid + NT * j, t, epoch, iend[j], &z);
         if (z) zmask |= 1u << j;
-        if (zr) zrmask |= 1u << j;
       }
     }
 #ifdef DPRO_PROFILE
