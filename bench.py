@@ -383,7 +383,8 @@ def run_ours(args) -> None:
     kmean = float(np.mean(kern_ms)) / 1e3
     achieved = algo_bytes / kmean / 1e9
     value = world * B * args.steps / (total_ms / 1e3)
-    cpu, why = (None, "skipped (--cpu-seconds 0)")
+    cpu, why = (None, "skipped (--cpu-seconds 0)" if world == 1 else
+                "measured at N=1 only (rank 0 of a single-GPU run)")
     if args.cpu_seconds > 0 and world == 1:
         S = _specs_module()
         cpu, why = cpu_reference_sample(S, S.workload_spec(args.config), descs, ms,

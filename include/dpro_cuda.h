@@ -96,8 +96,10 @@ int dpro_cuda_set_stream(dpro_ctx* ctx, void* stream);
  * the fast path; 0 = by device count, the default), "gcnt" (1: fast-path
  * counters always in global scratch), "deep_first" (-1 auto, 0 never, 1
  * always start in the deep-ring pass), "host_threads" (host pool size for
- * delta batches; 0 = all hardware threads). Returns DPRO_EINVAL for unknown
- * keys or values. */
+ * delta batches; 0 = all hardware threads), "overlay" (1: delta batches
+ * replay on the resident base + per-candidate overlays), "tsync_host" (1:
+ * t_sync graphs built on host threads instead of on the GPU). Returns
+ * DPRO_EINVAL for unknown keys or values. */
 int dpro_cuda_set_option(dpro_ctx* ctx, const char* key, int64_t value);
 const char* dpro_cuda_last_error(dpro_ctx* ctx);
 
@@ -256,6 +258,12 @@ int dpro_cuda_replay_delta_batch(dpro_ctx* ctx, const dpro_resident* r,
 int dpro_cuda_tsync_grid(dpro_ctx* ctx, const dpro_cluster_desc* cluster,
                          const int64_t* bytes, const int32_t* k, int32_t n,
                          int64_t* out, int32_t* status);
+/* The comm-only graphs of the same grid as a batch (K2: generated on the GPU
+ * straight into CSR, in the reference's index order -- no host graph, no
+ * upload): replay / results / timelines / critical paths as for any batch.
+ * NULL with dpro_cuda_last_error set for k < 1 or a degenerate cluster. */
+dpro_batch* dpro_cuda_batch_create_tsync(dpro_ctx* ctx, const dpro_cluster_desc* cluster,
+                                         const int64_t* bytes, const int32_t* k, int32_t n);
 
 /* ------------------------------------------------------------------------
  * Host-side CSR graph construction (candidate generation; no GPU needed).

@@ -115,6 +115,7 @@ SIGNATURES = {
     "dpro_delta_set_device_str": (C.c_char_p, [_P, _I32, _U32]),
     "dpro_delta_set_free": (None, [_P]),
     "dpro_base_graph": (_P, [_P]),
+    "dpro_cuda_batch_create_tsync": (_P, [_P, C.POINTER(DproClusterDesc), _P, _P, _I32]),
     "dpro_cuda_tsync_grid": (C.c_int, [_P, C.POINTER(DproClusterDesc), _P, _P, _I32, _P, _P]),
     "dpro_graph_layered": (_P, [C.POINTER(DproLayeredModel), C.POINTER(DproClusterDesc), _P, _P]),
     "dpro_graph_layered_variant": (_P, [C.POINTER(DproLayeredModel), C.POINTER(DproClusterDesc), _P, _I32, C.c_double, _P]),

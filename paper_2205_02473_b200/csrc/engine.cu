@@ -11,6 +11,7 @@
 #include <functional>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -27,6 +28,7 @@
 #include "pack_kernel.cuh"
 #include "replay_fast.cuh"
 #include "replay_kernel.cuh"
+#include "tsync_kernel.cuh"
 
 struct dpro_graph;
 dpro_graph* dpro_internal_tsync_graph(const dpro_cluster_desc* cluster,
@@ -214,6 +216,7 @@ struct dpro_ctx {
   int gcnt = 0;       // option "gcnt": 1 = fast-path counters always in global scratch
   int deep_first = -1;  // option "deep_first": -1 auto (mean V > 1M), 0 never, 1 always
   int overlay = 0;      // option "overlay": 1 = delta batches replay on the base + overlays
+  int tsync_host = 0;   // option "tsync_host": 1 = t_sync graphs built on host threads (A/B)
   DevBuf gring;         // pass 3 of the fast kernels: device rings in global memory
   dpro_batch* spare = nullptr;  // recycled arenas for repeated small calls
 };
@@ -1521,6 +1524,10 @@ int dpro_cuda_set_option(dpro_ctx* ctx, const char* key, int64_t value) {
     ctx->host_threads = static_cast<int>(value);
     return DPRO_OK;
   }
+  if (k == "tsync_host" && (value == 0 || value == 1)) {
+    ctx->tsync_host = static_cast<int>(value);
+    return DPRO_OK;
+  }
   if (k == "overlay" && (value == 0 || value == 1)) {
     ctx->overlay = static_cast<int>(value);
     return DPRO_OK;
@@ -2210,10 +2217,342 @@ int dpro_cuda_replay_batch(dpro_ctx* ctx, const dpro_csr* cands,
   return st;
 }
 
+}  // extern "C"
+
+namespace {
+
+// K2 host side: tables of the index order / devices / link parameters of
+// the comm-only graphs, then tsync_*_kernel writes every graph's CSR into
+// the batch arena and the batch is packed like any device-memspace batch.
+uint64_t tsync_fnv1a(const std::string& x) {  // graph.cpp:57-64
+  uint64_t h = 1469598103934665603ULL;
+  for (unsigned char c : x) {
+    h ^= c;
+    h *= 1099511628211ULL;
+  }
+  return h;
+}
+
+// rank of each decimal string of 0..X-1 in byte order, and its inverse
+void decimal_ranks(int X, std::vector<int>& rank, std::vector<int>& inv) {
+  inv.resize(X);
+  for (int x = 0; x < X; ++x) inv[x] = x;
+  std::sort(inv.begin(), inv.end(),
+            [](int a, int b) { return std::to_string(a) < std::to_string(b); });
+  rank.resize(X);
+  for (int r = 0; r < X; ++r) rank[inv[r]] = r;
+}
+
+// Appends v to the host staging image (device offset off, image offset
+// off - base) and sets dptr to where it lands in buf.
+template <typename T>
+void upload_table(DevBuf& buf, size_t base, size_t& off, const std::vector<T>& v, const T*& dptr,
+                  std::vector<char>& stage) {
+  const size_t bytes = v.size() * sizeof(T);
+  if (stage.size() < off - base + align16(bytes)) stage.resize(off - base + align16(bytes));
+  if (bytes) std::memcpy(stage.data() + (off - base), v.data(), bytes);
+  dptr = reinterpret_cast<const T*>(static_cast<char*>(buf.p) + off);
+  off += align16(bytes);
+}
+
+int build_tsync_batch(dpro_ctx* ctx, dpro_batch* b, const dpro_cluster_desc& cd,
+                      const std::vector<int64_t>& bytes, const std::vector<int32_t>& ks) {
+  Tracer tr;
+  const int32_t n = static_cast<int32_t>(bytes.size());
+  std::vector<std::string> names(cd.n_nodes);
+  for (int i = 0; i < cd.n_nodes; ++i) names[i] = cd.node_ids[i];
+  std::map<std::pair<int, int>, std::pair<double, double>> link;  // first wins
+  for (int l = 0; l < cd.n_links; ++l)
+    link.emplace(std::make_pair(cd.link_src[l], cd.link_dst[l]),
+                 std::make_pair(cd.link_bw[l], cd.link_lat[l]));
+  auto bwlat = [&](int a, int z) {
+    auto it = link.find({a, z});
+    return it == link.end() ? std::make_pair(1.0, 0.0) : it->second;
+  };
+  std::vector<int> workers, ps;
+  for (int i = 0; i < cd.n_nodes; ++i) {
+    if (cd.node_role[i] == 0) workers.push_back(i);
+    if (cd.node_role[i] == 1) ps.push_back(i);
+  }
+  auto by_name = [&](int a, int z) { return names[a] < names[z]; };
+  std::sort(workers.begin(), workers.end(), by_name);
+  std::sort(ps.begin(), ps.end(), by_name);
+  int kmax = 1;
+  for (int32_t x : ks) kmax = std::max(kmax, x);
+  std::vector<int> inv_p, inv_p_off(kmax + 2, 0);
+  for (int kk = 1; kk <= kmax; ++kk) {
+    std::vector<int> r, inv;
+    decimal_ranks(kk, r, inv);
+    inv_p_off[kk] = static_cast<int>(inv_p.size());
+    inv_p.insert(inv_p.end(), inv.begin(), inv.end());
+  }
+  std::vector<dpro_k::TsyncDesc> desc(n);
+  std::vector<uint32_t> n_dev(n);
+  std::vector<char> stage;
+  size_t toff = 0;
+  dpro_k::TsyncRing R{};
+  dpro_k::TsyncPs P{};
+  // host vectors kept alive until the upload
+  std::vector<int> rank_c, inv_c, rank_s, inv_s, server_of, srv_off, pull_w, push_w, dev_off;
+  std::vector<uint16_t> link_dev, dev_push, dev_pull;
+  std::vector<double> lbw, llat, bw_push, lat_push, bw_pull, lat_pull;
+  if (cd.scheme == 0) {
+    std::vector<int> ring;
+    if (cd.n_ring > 0) ring.assign(cd.ring_order, cd.ring_order + cd.n_ring);
+    else ring = workers;
+    const int N = static_cast<int>(ring.size());
+    if (N < 2) return set_err(ctx, DPRO_EINVAL, "degenerate ring: allreduce needs at least 2 workers");
+    const int C = cd.chunks_per_tensor > 0 ? cd.chunks_per_tensor : N, S = 2 * (N - 1);
+    decimal_ranks(C, rank_c, inv_c);
+    decimal_ranks(S, rank_s, inv_s);
+    std::vector<std::pair<std::string, std::string>> lk(N);
+    for (int i = 0; i < N; ++i) lk[i] = {names[ring[i]], names[ring[(i + 1) % N]]};
+    std::vector<std::pair<std::string, std::string>> sorted_lk(lk);
+    std::sort(sorted_lk.begin(), sorted_lk.end());
+    sorted_lk.erase(std::unique(sorted_lk.begin(), sorted_lk.end()), sorted_lk.end());
+    link_dev.resize(N);
+    lbw.resize(N);
+    llat.resize(N);
+    for (int i = 0; i < N; ++i) {
+      link_dev[i] = static_cast<uint16_t>(
+          std::lower_bound(sorted_lk.begin(), sorted_lk.end(), lk[i]) - sorted_lk.begin());
+      const auto bl = bwlat(ring[i], ring[(i + 1) % N]);
+      lbw[i] = bl.first;
+      llat[i] = bl.second;
+    }
+    R.n_workers = N;
+    R.chunks = C;
+    R.steps = S;
+    unsigned long long oo = 0, eo = 0;
+    for (int32_t i = 0; i < n; ++i) {
+      const uint64_t kcs = uint64_t(ks[i]) * C * S;
+      if (2 * kcs >= (1ull << 31)) return set_err(ctx, DPRO_EINVAL, "t_sync graph too large");
+      desc[i] = {bytes[i], ks[i], static_cast<uint32_t>(2 * kcs),
+                 static_cast<uint32_t>(2 * kcs - uint64_t(ks[i]) * C), oo, eo};
+      n_dev[i] = static_cast<uint32_t>(sorted_lk.size());
+      oo += desc[i].n;
+      eo += desc[i].e;
+    }
+  } else {
+    if (ps.empty()) return set_err(ctx, DPRO_EINVAL, "parameter-server scheme requires at least one ps node");
+    if (workers.empty()) return set_err(ctx, DPRO_EINVAL, "parameter-server scheme requires at least one worker");
+    const int W = static_cast<int>(workers.size()), NS = static_cast<int>(ps.size());
+    // worker order of the pull ids ("...#pull#<server>#<w>") and the push
+    // ids ("...#push#<w>#<server>") per server
+    pull_w.resize(size_t(NS) * W);
+    push_w.resize(size_t(NS) * W);
+    for (int sv = 0; sv < NS; ++sv) {
+      std::vector<int> o(W);
+      for (int w = 0; w < W; ++w) o[w] = w;
+      std::sort(o.begin(), o.end(), [&](int a, int z) { return names[workers[a]] < names[workers[z]]; });
+      std::copy(o.begin(), o.end(), pull_w.begin() + size_t(sv) * W);
+      const std::string& sn = names[ps[sv]];
+      std::sort(o.begin(), o.end(), [&](int a, int z) {
+        return names[workers[a]] + "#" + sn < names[workers[z]] + "#" + sn;
+      });
+      std::copy(o.begin(), o.end(), push_w.begin() + size_t(sv) * W);
+    }
+    bw_push.resize(size_t(NS) * W);
+    lat_push.resize(size_t(NS) * W);
+    bw_pull.resize(size_t(NS) * W);
+    lat_pull.resize(size_t(NS) * W);
+    for (int sv = 0; sv < NS; ++sv)
+      for (int w = 0; w < W; ++w) {
+        const auto a = bwlat(workers[w], ps[sv]), z = bwlat(ps[sv], workers[w]);
+        bw_push[size_t(sv) * W + w] = a.first;
+        lat_push[size_t(sv) * W + w] = a.second;
+        bw_pull[size_t(sv) * W + w] = z.first;
+        lat_pull[size_t(sv) * W + w] = z.second;
+      }
+    // per k: the server of each partition (by rank) and the dense device ids
+    // over the links those servers use
+    srv_off.assign(kmax + 2, 0);
+    dev_off.assign(kmax + 2, 0);
+    std::vector<uint32_t> ndev_k(kmax + 1, 0);
+    for (int kk = 1; kk <= kmax; ++kk) {
+      srv_off[kk] = static_cast<int>(server_of.size());
+      std::vector<char> used(NS, 0);
+      for (int pr = 0; pr < kk; ++pr) {
+        const int p = inv_p[inv_p_off[kk] + pr];
+        const std::string unit = kk == 1 ? "tsync" : "tsync#p" + std::to_string(p);
+        const int sv = static_cast<int>(tsync_fnv1a(unit) % static_cast<uint64_t>(NS));
+        server_of.push_back(sv);
+        used[sv] = 1;
+      }
+      std::vector<std::pair<std::string, std::string>> lk;
+      for (int sv = 0; sv < NS; ++sv)
+        if (used[sv])
+          for (int w = 0; w < W; ++w) {
+            lk.push_back({names[workers[w]], names[ps[sv]]});
+            lk.push_back({names[ps[sv]], names[workers[w]]});
+          }
+      std::sort(lk.begin(), lk.end());
+      lk.erase(std::unique(lk.begin(), lk.end()), lk.end());
+      dev_off[kk] = static_cast<int>(dev_push.size());
+      dev_push.resize(dev_push.size() + size_t(NS) * W, 0);
+      dev_pull.resize(dev_pull.size() + size_t(NS) * W, 0);
+      for (int sv = 0; sv < NS; ++sv)
+        if (used[sv])
+          for (int w = 0; w < W; ++w) {
+            const std::pair<std::string, std::string> a{names[workers[w]], names[ps[sv]]},
+                z{names[ps[sv]], names[workers[w]]};
+            dev_push[dev_off[kk] + size_t(sv) * W + w] =
+                static_cast<uint16_t>(std::lower_bound(lk.begin(), lk.end(), a) - lk.begin());
+            dev_pull[dev_off[kk] + size_t(sv) * W + w] =
+                static_cast<uint16_t>(std::lower_bound(lk.begin(), lk.end(), z) - lk.begin());
+          }
+      ndev_k[kk] = static_cast<uint32_t>(lk.size());
+    }
+    P.n_workers = W;
+    unsigned long long oo = 0, eo = 0;
+    for (int32_t i = 0; i < n; ++i) {
+      const uint64_t kk = ks[i];
+      if (4 * kk * W + kk * W * W >= (1ull << 31))
+        return set_err(ctx, DPRO_EINVAL, "t_sync graph too large");
+      desc[i] = {bytes[i], ks[i], static_cast<uint32_t>(4 * kk * W),
+                 static_cast<uint32_t>(kk * W * W + 2 * kk * W), oo, eo};
+      n_dev[i] = ndev_k[ks[i]];
+      oo += desc[i].n;
+      eo += desc[i].e;
+    }
+  }
+  // device arena: CSR arrays + tables
+  unsigned long long so = 0, se = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    so += desc[i].n;
+    se += desc[i].e;
+  }
+  const size_t a_dur = align16(so * 8 + 8), a_dev = align16(so * 2 + 2), a_fl = align16(so + 1),
+               a_so = align16((so + n) * 4 + 4), a_su = align16(se * 4 + 4), a_in = align16(so * 4 + 4);
+  const size_t csr_bytes = a_dur + a_dev + a_fl + a_so + a_su + a_in;
+  // tables after the CSR arrays
+  CU(b->arena.ensure(csr_bytes + (1u << 20) + 64 * (dev_push.size() + pull_w.size() + inv_p.size() +
+                                                      rank_c.size() + rank_s.size() + 16 * link_dev.size() + 64)));
+  size_t off = csr_bytes;
+  const size_t t0 = off;
+  if (cd.scheme == 0) {
+    upload_table(b->arena, t0, off, rank_c, R.rank_c, stage);
+    upload_table(b->arena, t0, off, inv_c, R.inv_c, stage);
+    upload_table(b->arena, t0, off, rank_s, R.rank_s, stage);
+    upload_table(b->arena, t0, off, inv_s, R.inv_s, stage);
+    upload_table(b->arena, t0, off, inv_p, R.inv_p, stage);
+    upload_table(b->arena, t0, off, inv_p_off, R.inv_p_off, stage);
+    upload_table(b->arena, t0, off, link_dev, R.link_dev, stage);
+    upload_table(b->arena, t0, off, lbw, R.link_bw, stage);
+    upload_table(b->arena, t0, off, llat, R.link_lat, stage);
+  } else {
+    upload_table(b->arena, t0, off, inv_p, P.inv_p, stage);
+    upload_table(b->arena, t0, off, inv_p_off, P.inv_p_off, stage);
+    upload_table(b->arena, t0, off, server_of, P.server_of, stage);
+    upload_table(b->arena, t0, off, srv_off, P.srv_off, stage);
+    upload_table(b->arena, t0, off, pull_w, P.pull_w, stage);
+    upload_table(b->arena, t0, off, push_w, P.push_w, stage);
+    upload_table(b->arena, t0, off, dev_off, P.dev_off, stage);
+    upload_table(b->arena, t0, off, dev_push, P.dev_push, stage);
+    upload_table(b->arena, t0, off, dev_pull, P.dev_pull, stage);
+    upload_table(b->arena, t0, off, bw_push, P.bw_push, stage);
+    upload_table(b->arena, t0, off, lat_push, P.lat_push, stage);
+    upload_table(b->arena, t0, off, bw_pull, P.bw_pull, stage);
+    upload_table(b->arena, t0, off, lat_pull, P.lat_pull, stage);
+  }
+  {
+    std::vector<dpro_k::TsyncDesc> dd(desc);
+    const dpro_k::TsyncDesc* dptr = nullptr;
+    upload_table(b->arena, t0, off, dd, dptr, stage);
+    if (off > b->arena.cap) return set_err(ctx, DPRO_ENOMEM, "t_sync tables");
+    CU(cudaMemcpyAsync(b->arena.as<char>(t0), stage.data(), off - t0, cudaMemcpyHostToDevice,
+                       ctx->stream));
+    dpro_k::TsyncOut O;
+    size_t o = 0;
+    O.dur = b->arena.as<long long>(o); o += a_dur;
+    O.dev = b->arena.as<uint16_t>(o); o += a_dev;
+    O.flags = b->arena.as<uint8_t>(o); o += a_fl;
+    O.succ_off = b->arena.as<uint32_t>(o); o += a_so;
+    O.succ = b->arena.as<uint32_t>(o); o += a_su;
+    O.indeg = b->arena.as<uint32_t>(o); o += a_in;
+    const int grid = std::max(1, std::min<int>(n, ctx->sm_count * 8));
+    if (n > 0) {
+      if (cd.scheme == 0)
+        dpro_k::tsync_ring_kernel<<<grid, 256, 0, ctx->stream>>>(dptr, n, R, O);
+      else
+        dpro_k::tsync_ps_kernel<<<grid, 256, 0, ctx->stream>>>(dptr, n, P, O);
+      CU(cudaGetLastError());
+    }
+    CU(cudaStreamSynchronize(ctx->stream));  // stage is a local
+    // the batch: device CSRs in the arena, packed like any device batch
+    std::vector<dpro_csr> csrs(n);
+    for (int32_t i = 0; i < n; ++i) {
+      const auto& c = desc[i];
+      csrs[i] = {c.n, c.e, n_dev[i], 64, O.dur + c.op_off, O.dev + c.op_off, O.flags + c.op_off,
+                 O.succ_off + c.op_off + i, O.succ + c.e_off, O.indeg + c.op_off};
+    }
+    b->memspace = DPRO_DEVICE;
+    tr.mark("t_sync graphs generated (K2)");
+    return build_batch(ctx, b, csrs.data());
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+dpro_batch* dpro_cuda_batch_create_tsync(dpro_ctx* ctx, const dpro_cluster_desc* cluster,
+                                         const int64_t* bytes, const int32_t* k, int32_t n) {
+  if (!ctx || !cluster || n < 0 || (n > 0 && (!bytes || !k))) return nullptr;
+  for (int32_t i = 0; i < n; ++i)
+    if (k[i] < 1) {
+      ctx->err = "sync_makespan: partition count must be >= 1, got " + std::to_string(k[i]);
+      return nullptr;
+    }
+  cudaSetDevice(ctx->device);
+  auto* b = new dpro_batch;
+  b->n = n;
+  b->memspace = DPRO_DEVICE;
+  if (build_tsync_batch(ctx, b, *cluster, std::vector<int64_t>(bytes, bytes + n),
+                        std::vector<int32_t>(k, k + n)) != DPRO_OK) {
+    delete b;
+    return nullptr;
+  }
+  return b;
+}
+
 int dpro_cuda_tsync_grid(dpro_ctx* ctx, const dpro_cluster_desc* cluster,
                          const int64_t* bytes, const int32_t* k, int32_t n,
                          int64_t* out, int32_t* status) {
   if (!ctx || !cluster || n < 0) return DPRO_EINVAL;
+  if (!ctx->tsync_host) {  // K2: graphs generated on the device
+    std::vector<int64_t> bb;
+    std::vector<int32_t> kk;
+    std::vector<int> idx;
+    int st = DPRO_OK;
+    for (int32_t i = 0; i < n; ++i) {
+      if (k[i] >= 1) {
+        bb.push_back(bytes[i]);
+        kk.push_back(k[i]);
+        idx.push_back(i);
+      } else {
+        if (status) status[i] = DPRO_EINVAL;
+        out[i] = 0;
+        ctx->err = "sync_makespan: partition count must be >= 1, got " + std::to_string(k[i]);
+      }
+    }
+    if (idx.empty()) return DPRO_OK;
+    cudaSetDevice(ctx->device);
+    dpro_batch b;
+    b.n = static_cast<int32_t>(idx.size());
+    st = build_tsync_batch(ctx, &b, *cluster, bb, kk);
+    if (st == DPRO_OK) st = dpro_cuda_batch_replay(ctx, &b, 0);
+    std::vector<int64_t> ms(idx.size()), er(idx.size());
+    std::vector<int32_t> ss(idx.size());
+    if (st == DPRO_OK)
+      st = dpro_cuda_batch_results(ctx, &b, ms.data(), ss.data(), er.data(), nullptr, nullptr);
+    for (size_t j = 0; j < idx.size(); ++j) {
+      out[idx[j]] = st == DPRO_OK ? ms[j] : 0;
+      if (status) status[idx[j]] = st == DPRO_OK ? ss[j] : st;
+    }
+    cudaStreamSynchronize(ctx->stream);
+    return st;
+  }
   std::vector<dpro_graph*> graphs(n, nullptr);
   std::vector<std::string> errs(n);
   std::vector<int> idx;

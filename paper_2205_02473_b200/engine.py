@@ -105,6 +105,18 @@ class Engine:
         DeltaSet or a ctypes array of N.DproDelta): merged on the GPU."""
         return Batch(self, deltas, N.DPRO_DEVICE, resident=resident)
 
+    def tsync_batch(self, cluster, bytes_: Sequence[int], ks: Sequence[int]) -> "Batch":
+        """The comm-only graphs of sync_makespan over a (bytes, k) grid as a
+        batch, generated on the GPU (dpro_cuda_batch_create_tsync, K2)."""
+        holder = N.ClusterDescHolder(cluster)
+        b = np.ascontiguousarray(bytes_, dtype=np.int64)
+        k = np.ascontiguousarray(ks, dtype=np.int32)
+        h = N.lib.dpro_cuda_batch_create_tsync(self.ctx, C.byref(holder.desc), N.ptr(b), N.ptr(k),
+                                               len(b))
+        if not h:
+            _check(self.ctx, N.DPRO_EINVAL, "batch_create_tsync")
+        return Batch.from_handle(self, h, len(b))
+
     def tsync_grid(self, cluster, bytes_: Sequence[int], ks: Sequence[int]):
         """dpro_cuda_tsync_grid: (makespans, statuses)."""
         holder = N.ClusterDescHolder(cluster)
@@ -176,6 +188,24 @@ class Batch:
                 _check(engine.ctx, N.DPRO_EINVAL, "batch_create")
         self.op_off = np.zeros(self.n + 1, np.int64)
         self.op_off[1:] = np.cumsum(self.n_ops)
+
+    @classmethod
+    def from_handle(cls, engine: Engine, handle: int, n: int) -> "Batch":
+        """A batch the engine built itself (e.g. t_sync graphs on the GPU)."""
+        self = cls.__new__(cls)
+        self.engine, self._keep, self._resident = engine, None, None
+        self.with_schedule = False
+        self.handle, self.n = handle, n
+        no = np.zeros(max(1, n), np.uint32)
+        ne = np.zeros(max(1, n), np.uint32)
+        nd = np.zeros(max(1, n), np.uint32)
+        N.lib.dpro_cuda_batch_sizes(handle, N.ptr(no), N.ptr(ne), N.ptr(nd))
+        self.n_ops = no[:n].astype(np.int64)
+        self.n_edges = ne[:n].astype(np.int64)
+        self.n_devices = nd[:n].astype(np.int64)
+        self.op_off = np.zeros(n + 1, np.int64)
+        self.op_off[1:] = np.cumsum(self.n_ops)
+        return self
 
     def close(self) -> None:
         if self.handle:

@@ -82,3 +82,39 @@ def test_ingest_built_graphs_on_gpu(engine, fast):
     if fast:
         assert batch.stats()["fallbacks"] <= len(vs)  # ring queues > 4 deep fall back
     engine.set_option("fast", 1)
+
+
+@pytest.mark.parametrize("scheme,W,S,bw,lat,ks", [
+    ("ring", 12, 0, 1.0, 0.0, [1, 2, 10, 11, 12]),
+    ("ring", 4, 0, 33.0, 2.5, [1, 3, 16]),
+    ("ps", 3, 2, 1.0, 0.5, [1, 2, 11, 12]),
+    ("ps", 16, 4, 12500.0, 5.0, [1, 4, 7]),
+    ("ps", 1, 1, 1.0, 0.0, [1, 2, 3, 4])])
+def test_device_generated_tsync_graphs_match_host(engine, port, scheme, W, S, bw, lat, ks):
+    """K2: the graphs generated on the GPU (dpro_cuda_batch_create_tsync)
+    replay to the same schedule, position by position (so the same index
+    order, devices and durations), as the host generator's graphs replayed
+    by the C oracle; the grid API agrees with the host-built path."""
+    from paper_2205_02473_b200.graph import synth_cluster
+    from paper_2205_02473_b200.ingest import tsync_graph
+    c = synth_cluster(scheme, W, S, bw, lat)
+    grid = [(b, k) for b in (1, 100, 4096, 123457) for k in ks]
+    b = engine.tsync_batch(c, [x for x, _ in grid], [k for _, k in grid])
+    b.replay(want_schedule=True)
+    ms, st, _, start, end = b.results(schedule=True)
+    for i, (by, k) in enumerate(grid):
+        g = tsync_graph(c, by, k)
+        o = port.port_replay(g.csr)
+        a, z = int(b.op_off[i]), int(b.op_off[i + 1])
+        assert st[i] == 0 and ms[i] == o["T"], (by, k)
+        assert z - a == g.n_ops and int(b.n_edges[i]) == g.n_edges
+        assert np.array_equal(start[a:z], o["start"]) and np.array_equal(end[a:z], o["end"])
+        order, dev_off, busy = b.timelines(i)
+        assert int(b.n_devices[i]) == g.csr.n_devices
+    engine.set_option("tsync_host", 1)
+    try:
+        host, _ = engine.tsync_grid(c, [x for x, _ in grid], [k for _, k in grid])
+    finally:
+        engine.set_option("tsync_host", 0)
+    dev, _ = engine.tsync_grid(c, [x for x, _ in grid], [k for _, k in grid])
+    assert np.array_equal(host, dev) and np.array_equal(dev, ms)
