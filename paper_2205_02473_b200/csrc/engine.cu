@@ -217,6 +217,8 @@ struct dpro_ctx {
   int deep_first = -1;  // option "deep_first": -1 auto (mean V > 1M), 0 never, 1 always
   int overlay = 0;      // option "overlay": 1 = delta batches replay on the base + overlays
   int tsync_host = 0;   // option "tsync_host": 1 = t_sync graphs built on host threads (A/B)
+  int gring0 = 0;       // option "gring0": overlay residency pass with rings in global memory
+  DevBuf gring0_buf;
   DevBuf gring;         // pass 3 of the fast kernels: device rings in global memory
   dpro_batch* spare = nullptr;  // recycled arenas for repeated small calls
 };
@@ -1524,6 +1526,10 @@ int dpro_cuda_set_option(dpro_ctx* ctx, const char* key, int64_t value) {
     ctx->host_threads = static_cast<int>(value);
     return DPRO_OK;
   }
+  if (k == "gring0" && (value == 0 || value == 1)) {
+    ctx->gring0 = static_cast<int>(value);
+    return DPRO_OK;
+  }
   if (k == "tsync_host" && (value == 0 || value == 1)) {
     ctx->tsync_host = static_cast<int>(value);
     return DPRO_OK;
@@ -1725,11 +1731,20 @@ int launch_ov_kd(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule, FastCfg F)
   CU(cudaFuncGetAttributes(&fa, kern));
   const size_t dyn_max = ctx->smem_optin - fa.sharedSizeBytes;
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_max));
+  FastCfg F0 = F;  // residency pass config (option gring0: device rings in global memory)
+  if (ctx->gring0) {
+    F0.warp_bytes = F.warp_bytes - 16 * F.dcap * F.qc;
+    F0.gq = nullptr;  // set below, once the grid is known
+  }
   int blocks_per_sm = 0;
-  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, 32 * NW, F.warp_bytes));
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, 32 * NW, F0.warp_bytes));
   blocks_per_sm = std::max(blocks_per_sm, 1);
   b->blocks_per_sm_fast = blocks_per_sm;
   const int grid = std::max(1, std::min(b->n, ctx->sm_count * blocks_per_sm));
+  if (ctx->gring0) {
+    CU(ctx->gring0_buf.ensure(size_t(grid) * F.dcap * F.qc * 16));
+    F0.gq = ctx->gring0_buf.as<uint4>();
+  }
   CU(cudaMemsetAsync(b->work.p, 0, 48, ctx->stream));
   b->F = F;
   const dpro_resident* r = b->res;
@@ -1766,9 +1781,9 @@ int launch_ov_kd(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule, FastCfg F)
     CU(cudaGetLastError());
     CU(cudaEventRecord(ctx->side_ev[1], ctx->side_stream));
   }
-  kern<<<grid, 32 * NW, F.warp_bytes, ctx->stream>>>(
+  kern<<<grid, 32 * NW, F0.warp_bytes, ctx->stream>>>(
       b->desc.as<Cand>(), b->ovdesc.as<dpro_k::OvCand>(), b->n, r->ob, b->S, b->O,
-      b->ovgcnt.as<uint8_t>(), F, want_schedule ? 1 : 0, b->work.as<unsigned>(), 0, hint,
+      b->ovgcnt.as<uint8_t>(), F0, want_schedule ? 1 : 0, b->work.as<unsigned>(), 0, hint,
       b->order.as<unsigned>());
   CU(cudaGetLastError());
   b->mark(1, ctx->stream);

@@ -26,7 +26,7 @@ def main():
                                        variants=not os.environ.get("NO_VARIANTS"))
     print(f"deltas {time.perf_counter() - t:.2f} s", flush=True)
     eng = Engine(0)
-    for key in ("ring", "warps", "deep_first"):
+    for key in ("ring", "warps", "deep_first", "gring0"):
         if os.environ.get("DPRO_" + key.upper()):
             eng.set_option(key, int(os.environ["DPRO_" + key.upper()]))
     res = eng.resident(base.graph().csr)
