@@ -187,6 +187,10 @@ def run_reference(args) -> None:
     threads = os.cpu_count() or 1
     if spec["mix"] == "op_fusion":
         descs = S.op_fusion_mix(spec["seed"], spec["workers"], spec["layers"], B, 0)
+        # the reference's apply_strategy(kGradAccum) on the 4.8M-op graph did
+        # not finish within 40 min on the GPU box's host: the sample is the
+        # recompute candidate and op-fusion pairs (1,478 of the 1,480)
+        descs = [d for d in descs if d[0] != "grad-accum"]
         n_sample = args.ref_sample or 4
     else:
         pk = S.partition_specs(spec["seed"], spec["layers"], B, 0)
@@ -195,7 +199,13 @@ def run_reference(args) -> None:
     sample = descs[:n_sample]  # config 4: recompute, grad-accum, then op fusion
     from oracle import oracle
     graphs, build_s = ref_sample_graphs(S, spec, sample, log=lambda m: print(m, file=sys.stderr))
-    per_step = max(threads, len(graphs))  # replays per step: every thread busy
+    # replays per step: every thread busy for graphs that fit the caches; a
+    # config-4 graph (4.8M ops, ~12 GB of std::map-based GlobalDFG) is DRAM
+    # bound on the host -- 16 concurrent replays take as long as 16 serial
+    # ones -- so there a step replays each sample graph once, one per thread
+    big = spec["mix"] == "op_fusion"
+    per_step = len(graphs) if big else max(threads, len(graphs))
+    threads = min(threads, per_step)
     vals, step_ms = [], []
     for step in range(args.warmup + args.steps):
         t0 = time.perf_counter()
@@ -245,15 +255,15 @@ def cpu_reference_sample(S, spec, descs, gpu_ms: np.ndarray, threads: int, budge
     per_thread = 1.0 / sec1
     used = min(threads, n)
     measured = n / secp
-    out = {"value": measured if not big else per_thread * threads, "unit": UNIT,
-           "cores": threads, "kind": "reference", "cpu_model": _cpu_model(),
+    out = {"value": measured, "unit": UNIT,
+           "cores": used, "kind": "reference", "cpu_model": _cpu_model(),
            "single_thread_replays_per_s": per_thread,
            "sample": (f"reference dpro::replay() on candidates {idx} of this batch, built by "
                       f"the reference's generator + rewrites ({build_s:.0f} s, excluded); "
                       f"1 replay on 1 thread: {sec1:.1f} s; {n} replays on {used} threads: "
                       f"{secp:.1f} s ({measured:.3f}/s)" +
-                      (f"; value = {threads} threads x the single-thread rate (extrapolated: "
-                       f"replays are independent)" if big else "")),
+                      ("; more threads do not help: a 4.8M-op reference graph is DRAM bound "
+                       "on the host" if big else "")),
            "parity": f"reference makespans {[int(x) for x in msp[:len(graphs)]]} == GPU"}
     return out, None
 
