@@ -217,7 +217,8 @@ struct dpro_ctx {
   int deep_first = -1;  // option "deep_first": -1 auto (mean V > 1M), 0 never, 1 always
   int overlay = 0;      // option "overlay": 1 = delta batches replay on the base + overlays
   int tsync_host = 0;   // option "tsync_host": 1 = t_sync graphs built on host threads (A/B)
-  int gring0 = 0;       // option "gring0": overlay residency pass with rings in global memory
+  int gring0 = -1;      // option "gring0": overlay residency pass with device rings in global
+                        // memory (-1 auto: multi-million-op graphs, 1 on, 0 off)
   DevBuf gring0_buf;
   DevBuf gring;         // pass 3 of the fast kernels: device rings in global memory
   dpro_batch* spare = nullptr;  // recycled arenas for repeated small calls
@@ -1526,7 +1527,7 @@ int dpro_cuda_set_option(dpro_ctx* ctx, const char* key, int64_t value) {
     ctx->host_threads = static_cast<int>(value);
     return DPRO_OK;
   }
-  if (k == "gring0" && (value == 0 || value == 1)) {
+  if (k == "gring0" && value >= -1 && value <= 1) {
     ctx->gring0 = static_cast<int>(value);
     return DPRO_OK;
   }
@@ -1731,8 +1732,14 @@ int launch_ov_kd(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule, FastCfg F)
   CU(cudaFuncGetAttributes(&fa, kern));
   const size_t dyn_max = ctx->smem_optin - fa.sharedSizeBytes;
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_max));
-  FastCfg F0 = F;  // residency pass config (option gring0: device rings in global memory)
-  if (ctx->gring0) {
+  // residency pass: for multi-million-op graphs the 16-entry device rings
+  // (32 KB of 44 KB per CTA) cap residency at 5 CTAs per SM; in global
+  // memory (L2) they cost latency per access but 8 CTAs per SM fit
+  // (register bound): +31 % replays/s on config 4 (profiles/r02_*)
+  const bool gring0 = ctx->gring0 == 1 ||
+                      (ctx->gring0 < 0 && b->n > 0 && b->sum_n / b->n > 1000000ull);
+  FastCfg F0 = F;
+  if (gring0) {
     F0.warp_bytes = F.warp_bytes - 16 * F.dcap * F.qc;
     F0.gq = nullptr;  // set below, once the grid is known
   }
@@ -1741,7 +1748,7 @@ int launch_ov_kd(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule, FastCfg F)
   blocks_per_sm = std::max(blocks_per_sm, 1);
   b->blocks_per_sm_fast = blocks_per_sm;
   const int grid = std::max(1, std::min(b->n, ctx->sm_count * blocks_per_sm));
-  if (ctx->gring0) {
+  if (gring0) {
     CU(ctx->gring0_buf.ensure(size_t(grid) * F.dcap * F.qc * 16));
     F0.gq = ctx->gring0_buf.as<uint4>();
   }
