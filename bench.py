@@ -6,18 +6,18 @@
 Workload (default: BASELINE configs[3], the largest single-GPU config):
 GPT-2 medium 64-worker ring-all-reduce DFG (292 tensors, 4.80M ops, 6.0M
 edges, 128 devices) and its per-round candidate mix:
-the recompute candidate, the grad-accum candidate and 1478 single-worker
-adjacent op-fusion pairs -- 1480 candidates per GPU (two waves of 5
-resident candidates per SM; ~140 GB of schedules and timelines).
+the recompute candidate, the grad-accum candidate and 1182 single-worker
+adjacent op-fusion pairs -- 1184 candidates per GPU, one wave of 8
+resident candidates per SM (~115 GB of schedules and timelines).
 Candidates are deltas of one resident base graph (include/dpro_cuda.h
 dpro_delta), replayed on the base's packed layout plus per-candidate
 overlays (csrc/overlay.h). One step = the overlay upload + one exact replay
 of every candidate (K1: per-op start/end + makespan) + the per-round
 best-cost exchange (argmin; two NCCL MIN all-reduces across ranks when
 N > 1), with the inputs (base graph + overlays) resident in HBM. The step's
-working set (~85 GB of schedules and timelines) is far larger than L2: no
-flush needed. Smaller configs (--config 1-3) use per-candidate merged
-copies (delta merge K0 + pack) instead of overlays.
+working set is far larger than L2: no flush needed. Smaller configs
+(--config 1-3) use per-candidate merged copies (delta merge K0 + pack)
+instead of overlays.
 
 Multi-GPU: one process per GPU (torchrun), each rank replays its own batch
 (weak scaling); time is the max over ranks of CUDA-event time.

@@ -1753,7 +1753,7 @@ int launch_ov_kd(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule, FastCfg F)
     F0.gq = ctx->gring0_buf.as<uint4>();
   }
   CU(cudaMemsetAsync(b->work.p, 0, 48, ctx->stream));
-  b->F = F;
+  b->F = F0;
   const dpro_resident* r = b->res;
   CU(b->hint.ensure(4 * (size_t(b->n) + 1)));
   unsigned* hint = b->hint.as<unsigned>();
