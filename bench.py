@@ -6,9 +6,9 @@
 Workload (default: BASELINE configs[3], the largest single-GPU config):
 GPT-2 medium 64-worker ring-all-reduce DFG (292 tensors, 4.80M ops, 6.0M
 edges, 128 devices) and its per-round candidate mix:
-the recompute candidate, the grad-accum candidate and 1182 single-worker
-adjacent op-fusion pairs -- 1184 candidates per GPU, one wave of 8
-resident candidates per SM (~115 GB of schedules and timelines).
+the recompute candidate, the grad-accum candidate and 1774 single-worker
+adjacent op-fusion pairs -- 1776 candidates per GPU, all resident at once
+(12 per SM, 2-warp CTAs; ~170 GB of schedules and timelines).
 Candidates are deltas of one resident base graph (include/dpro_cuda.h
 dpro_delta), replayed on the base's packed layout plus per-candidate
 overlays (csrc/overlay.h). One step = the overlay upload + one exact replay

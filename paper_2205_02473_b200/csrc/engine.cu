@@ -1914,6 +1914,12 @@ int finish_overlay_mat(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
 int launch_overlay(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
   int nw = ctx->warps;
   if (nw == 0) nw = b->max_d <= 32 ? 1 : b->max_d <= 64 ? 2 : 4;
+  // global-ring residency pass (multi-million-op graphs): registers, not
+  // shared memory, bound the CTAs per SM, so 2-warp CTAs (16 per SM) keep
+  // twice the candidates in flight of 4-warp ones (config 4: +16 %)
+  if (ctx->warps == 0 && ctx->gring0 != 0 && b->max_d <= 128 && b->n > 0 &&
+      b->sum_n / b->n > 1000000ull)
+    nw = 2;
   int st;
   switch (nw) {
     case 1: st = launch_ov_nw<1>(ctx, b, want_schedule); break;

@@ -152,7 +152,7 @@ def workload_spec(config: int) -> dict[str, Any]:
     elif config == 4:
         t = gpt2_medium_tensors()
         fw, bw = _durations(344_000, 594_000, len(t), 4)
-        s = dict(name="gpt2_medium_ring64", scheme="ring", workers=64, ps_count=0, batch=1184,
+        s = dict(name="gpt2_medium_ring64", scheme="ring", workers=64, ps_count=0, batch=1776,
                  seed=4, mix="op_fusion",
                  description="GPT-2 medium 64-worker ring DFG (292 tensors, 4.80M ops), "
                              "op-fusion + recomputation + gradient-accumulation candidates")
