@@ -1314,9 +1314,9 @@ int build_overlay_batch(dpro_ctx* ctx, dpro_batch* b, dpro_resident* r,
     b->info[i].not_fast = b->ovh[i].fast ? 0u : 1u;
   }
   // whole-graph rewrites (recompute / grad-accum variants: 100x the median
-  // overlay) are the long candidates of a batch (twice the event rounds of
-  // an op fusion): the residency pass hands them out first so they overlap
-  // everything else instead of trailing it
+  // overlay) are the long candidates of a batch (the grad-accum variant's
+  // link queues are 230 deep): they start first, on the side stream with
+  // global rings, so they overlap everything else instead of trailing it
   b->g3.clear();
   {
     std::vector<size_t> sz;
@@ -1329,7 +1329,10 @@ int build_overlay_batch(dpro_ctx* ctx, dpro_batch* b, dpro_resident* r,
     }
     std::vector<uint32_t> ord;
     for (int32_t i = 0; i < n; ++i)
-      if (b->ovh[i].fast && b->ovh[i].fin.size() > cut) ord.push_back(i);
+      if (b->ovh[i].fast && b->ovh[i].fin.size() > cut) {
+        ord.push_back(i);
+        b->g3.push_back(i);  // and straight to the side stream (global rings)
+      }
     for (int32_t i = 0; i < n; ++i)
       if (!(b->ovh[i].fast && b->ovh[i].fin.size() > cut)) ord.push_back(i);
     CU(b->order.ensure(4 * (size_t(n) + 1)));
@@ -1762,12 +1765,12 @@ int launch_ov_kd(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule, FastCfg F)
   // first, on the side stream, so they overlap the residency pass
   FastCfg D = F;  // pass 1: ring overflows, one CTA per SM, deepest rings
   D.rl = std::max<uint32_t>(F.rl, 2048);
-  const size_t lim = dyn_max - dpro_k::kOvListBytes;
+  const size_t lim = dyn_max - dpro_k::kOvListBytes - 16 * D.dcap;
   while (D.qc < 4096 && fast_bytes(D.dcap, D.qc * 2, D.rl, D.ccap, NW) <= lim) D.qc *= 2;
   D.warp_bytes = static_cast<uint32_t>(fast_bytes(D.dcap, D.qc, D.rl, D.ccap, NW)) +
-                 dpro_k::kOvListBytes;
+                 dpro_k::kOvListBytes + 16 * D.dcap;
   FastCfg G;
-  const bool g3ok = pass3_cfg(ctx, D, NW, G, dpro_k::kOvListBytes);
+  const bool g3ok = pass3_cfg(ctx, D, NW, G, dpro_k::kOvListBytes + 16 * D.dcap);
   const bool side = g3ok && !b->g3.empty();
   if (side) {
     if (!ctx->side_stream) {
@@ -1839,7 +1842,7 @@ int launch_ov_nw(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule) {
   while (F.qc < 64 && fast_bytes(F.dcap, F.qc * 2, F.rl, F.ccap, NW) <= std::min(target, limit))
     F.qc *= 2;
   F.warp_bytes = static_cast<uint32_t>(fast_bytes(F.dcap, F.qc, F.rl, F.ccap, NW)) +
-                 dpro_k::kOvListBytes;
+                 dpro_k::kOvListBytes + 16 * F.dcap;
   switch (kd) {
     case 1: return launch_ov_kd<NW, 1>(ctx, b, want_schedule, F);
     case 2: return launch_ov_kd<NW, 2>(ctx, b, want_schedule, F);

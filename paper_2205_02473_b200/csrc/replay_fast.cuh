@@ -238,6 +238,7 @@ struct FastWarp {
   uint32_t vcount = 0, dcount = 0;
   unsigned long long tmax = 0;
   bool wide = false;  // u16 counters (some in-degree >= 255)
+  uint4* last = nullptr;        // OV: [dcap] each device's latest arrival (shared memory)
   const uint2* sxs = nullptr;   // OV sparse lists in shared memory
   const uint2* sbps = nullptr;
   uint32_t n_sx = 0, n_sbp = 0, ovmin = 0;
@@ -324,7 +325,9 @@ struct FastWarp {
     if (pos - low >= qc) {
       atomicOr(const_cast<uint32_t*>(&misc[1]), kBailRing);
     } else {
-      ring(d)[pos & (qc - 1)] = make_uint4(s, a.y, sb | fl, se);  // {op, dur, sb, se}
+      const uint4 e = make_uint4(s, a.y, sb | fl, se);  // {op, dur, sb, se}
+      ring(d)[pos & (qc - 1)] = e;
+      if (OV) last[d] = e;  // a lone arrival is dispatched from here (no ring read)
       atomicOr(const_cast<uint32_t*>(&misc[4 + (d % NT)]), 1u << (d / NT));
     }
     if (se > sb) prefetch_l2((OV && fl ? ov.erec : erec) + sb);  // read when s completes
@@ -445,6 +448,12 @@ struct FastWarp {
     const uint32_t tail = *reinterpret_cast<volatile uint32_t*>(&s.tail);
     const uint32_t m = qc - 1;
     uint32_t head = s.head;
+    // OV: with one arrival this round its entry is in last[d] (shared
+    // memory) -- the rings may live in global memory
+    const bool lone = OV && tail == s.tsort + 1;
+    uint4 lone_e = make_uint4(0, 0, 0, 0);
+    uint32_t lone_pos = 0;
+    if (lone) lone_e = last[d];
     if (tail != s.tsort) {
       if (s.segt != epoch) {
         s.segbeg = s.tsort;
@@ -452,7 +461,7 @@ struct FastWarp {
       }
       const uint32_t lo = max(s.segbeg, head);
       for (uint32_t p = s.tsort; p < tail; ++p) {
-        const uint4 x = r[p & m];
+        const uint4 x = lone ? lone_e : r[p & m];
         uint32_t qq = p;
         while (qq > lo) {
           const uint4 y = r[(qq - 1) & m];
@@ -460,7 +469,8 @@ struct FastWarp {
           r[qq & m] = y;
           --qq;
         }
-        r[qq & m] = x;
+        if (!lone || qq != p) r[qq & m] = x;  // (a lone entry in place is already there)
+        lone_pos = qq;
       }
       s.tsort = tail;
     }
@@ -470,7 +480,7 @@ struct FastWarp {
       const uint32_t base = devoff[d];
       bool infl = false;
       while (head < tail) {
-        const uint4 x = r[head & m];
+        const uint4 x = (lone && head == lone_pos) ? lone_e : r[head & m];
         const unsigned long long en = t + x.y;
         if (want) {  // (qpos is derived from qbuf only when K3 needs it)
           start[x.x] = t;
@@ -550,6 +560,8 @@ __device__ uint32_t replay_fast(const Cand& c, int cid, const uint4* rec, const 
     // u16 counters: the base's (u8 or u16), then the overlay's
     W.ov = ovc->v;
     W.wide = true;
+    W.last = reinterpret_cast<uint4*>(reinterpret_cast<char*>(
+                 const_cast<uint32_t*>(misc) + fast_misc_words(NW)) + F.ccap + kOvListBytes);
     if (ovc->sparse) {  // sparse lists after the counter region
       uint2* sl = reinterpret_cast<uint2*>(reinterpret_cast<char*>(
                       const_cast<uint32_t*>(misc) + fast_misc_words(NW)) + F.ccap);
