@@ -27,6 +27,8 @@
 #include "overlay.h"
 #include "pack_kernel.cuh"
 #include "replay_fast.cuh"
+
+static_assert(dpro_ov::kSparseMax == dpro_k::kOvListMax, "sparse overlay list capacity");
 #include "replay_kernel.cuh"
 #include "tsync_kernel.cuh"
 
@@ -320,7 +322,10 @@ struct dpro_batch {
   uint32_t ring_hint = 0;       // residency-pass ring capacity learned from the last replay
   std::vector<int32_t> g3;      // candidates that needed global rings (run first next time)
   DevBuf hint;                  // device list of this replay's global-ring candidates
-  DevBuf order;                 // candidate order of the residency pass: long ones first
+  DevBuf order;                 // candidate order of the residency pass: long ones first,
+                                // then [n] side-stream flags (pass 4 candidates)
+  std::vector<uint32_t> side_h;
+  bool side_any = false;
   // pass timing of the last fast / overlay replay (dpro_cuda_batch_diag):
   // events before pass 0, after pass 0, 1, 3 and the general hand-off
   cudaEvent_t pev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -1335,7 +1340,9 @@ int build_overlay_batch(dpro_ctx* ctx, dpro_batch* b, dpro_resident* r,
       }
     for (int32_t i = 0; i < n; ++i)
       if (!(b->ovh[i].fast && b->ovh[i].fin.size() > cut)) ord.push_back(i);
-    CU(b->order.ensure(4 * (size_t(n) + 1)));
+    CU(b->order.ensure(4 * (2 * size_t(n) + 1)));  // order, then side flags
+    if (n) CU(cudaMemsetAsync(b->order.as<unsigned>() + n, 0, 4 * size_t(n), ctx->stream));
+    b->side_any = false;
     if (n) CU(cudaMemcpyAsync(b->order.p, ord.data(), 4 * size_t(n), cudaMemcpyHostToDevice,
                               ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));  // ord is a local
@@ -1590,8 +1597,8 @@ int launch_general(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule, int filt
 size_t fast_bytes(uint32_t dcap, uint32_t qc, uint32_t rl, uint32_t ccap, int nw);
 
 size_t fast_bytes(uint32_t dcap, uint32_t qc, uint32_t rl, uint32_t ccap, int nw) {
-  return size_t(dcap) * (sizeof(dpro_k::DevF) + 16 * qc) + 8 * size_t(rl) +
-         4 * dpro_k::fast_misc_words(nw) + ccap;
+  return size_t(dcap) * (sizeof(dpro_k::DevF) + 16 * qc + dpro_k::kTailBytesPerDev) +
+         8 * size_t(rl) + 4 * dpro_k::fast_misc_words(nw) + ccap;
 }
 
 // Pass 3 (after the deep-ring pass): candidates whose device queues
@@ -1610,8 +1617,7 @@ bool pass3_cfg(dpro_ctx* ctx, const FastCfg& deep, int nw, FastCfg& G, uint32_t 
     return false;
   }
   G.gq = ctx->gring.as<uint4>();
-  G.warp_bytes = static_cast<uint32_t>(size_t(G.dcap) * sizeof(dpro_k::DevF) + 8 * size_t(G.rl) +
-                                       4 * dpro_k::fast_misc_words(nw) + G.ccap) + extra;
+  G.warp_bytes = static_cast<uint32_t>(fast_bytes(G.dcap, 0, G.rl, G.ccap, nw)) + extra;
   return G.warp_bytes + 1024 <= ctx->smem_optin;
 }
 
@@ -1772,15 +1778,22 @@ int launch_ov_kd(dpro_ctx* ctx, dpro_batch* b, int32_t want_schedule, FastCfg F)
   FastCfg G;
   const bool g3ok = pass3_cfg(ctx, D, NW, G, dpro_k::kOvListBytes + 16 * D.dcap);
   const bool side = g3ok && !b->g3.empty();
+  if (!side && b->side_any) {
+    CU(cudaMemsetAsync(b->order.as<unsigned>() + b->n, 0, 4 * size_t(b->n), ctx->stream));
+  }
+  b->side_any = side;
   if (side) {
     if (!ctx->side_stream) {
       CU(cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking));
       CU(cudaEventCreateWithFlags(&ctx->side_ev[0], cudaEventDisableTiming));
       CU(cudaEventCreateWithFlags(&ctx->side_ev[1], cudaEventDisableTiming));
     }
-    const int32_t k3 = dpro_k::kRetry3;
-    for (int32_t c : b->g3)
-      CU(cudaMemcpyAsync(b->O.status + c, &k3, 4, cudaMemcpyHostToDevice, ctx->stream));
+    // side flags after the order permutation: pass 0 skips these whatever
+    // their status (pass 4 may already have finished one)
+    b->side_h.assign(b->n, 0u);
+    for (int32_t c : b->g3) b->side_h[c] = 1u;
+    CU(cudaMemcpyAsync(b->order.as<unsigned>() + b->n, b->side_h.data(), 4 * size_t(b->n),
+                       cudaMemcpyHostToDevice, ctx->stream));
     CU(cudaEventRecord(ctx->side_ev[0], ctx->stream));
     CU(cudaStreamWaitEvent(ctx->side_stream, ctx->side_ev[0], 0));
     const int g4 = std::max(1, std::min<int>(ctx->sm_count, static_cast<int>(b->g3.size())));

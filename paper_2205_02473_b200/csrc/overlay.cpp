@@ -343,7 +343,6 @@ void build_overlay(const BaseHost& B, const dpro_delta& D, OverlayHost& O) {
   // sparse form: the shift of final(b) = b - #removed<b + #new_pos<=b
   // changes at r + 1 for every removed r (-1) and at every new_pos (+1)
   {
-    constexpr size_t kSparseMax = 64;
     std::vector<std::pair<uint32_t, int32_t>> ch;
     for (uint32_t k = 0; k < D.n_removed && ch.size() <= 2 * kSparseMax; ++k)
       ch.emplace_back(D.removed[k] + 1, -1);

@@ -35,6 +35,9 @@ constexpr uint32_t kBlkOvf = 0x80000000u;    // blk entry: ovf block index follo
 constexpr uint32_t kBlkBias = 0x40000000u;   // clean blk entry: shift + kBlkBias
 constexpr uint32_t kOvfDirty = 0x80000000u;  // ovf entry: dirty, overlay slot follows
 constexpr uint32_t kOvfNone = 0xFFFFFFFFu;   // ovf entry of a removed op
+// sparse form: at most this many dirty ops and shift runs (the kernel keeps
+// both lists in shared memory: replay_fast.cuh kOvListMax)
+constexpr uint32_t kSparseMax = 48;
 
 // The base as the overlay builder needs it (host copies, built once).
 struct BaseHost {

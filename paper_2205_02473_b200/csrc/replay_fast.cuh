@@ -33,6 +33,15 @@
 namespace dpro_k {
 
 constexpr uint32_t kT32Inf = 0xFFFFFFFFu;
+// Register budget of the fast kernels. ptxas picks 56 registers (a few
+// spills to L1-resident local memory); capping at 64 via a minimum CTA count
+// removes the spills but measured 10 % slower on config 4 (1,475 vs 1,645
+// replays/s, profiles/r02_c4_regbudget_ab.log): it stays behind DPRO_MINB.
+#ifdef DPRO_MINB
+#define DPRO_FAST_BOUNDS(NW, KD) __launch_bounds__(32 * NW, (KD <= 5 ? 32 : 16) / NW)
+#else
+#define DPRO_FAST_BOUNDS(NW, KD) __launch_bounds__(32 * NW)
+#endif
 // replay_fast outcomes / bail-out causes
 constexpr uint32_t kDone = 0, kBailRing = 1, kBailOther = 2, kBailRl = 3;
 constexpr uint32_t kMiscRl = 4;  // misc[1] bit: a round's range list overflowed
@@ -42,14 +51,13 @@ __device__ __forceinline__ uint32_t bail_code(uint32_t m) {
 constexpr int kRetry = 9;   // status of a candidate queued for the deep-ring pass
 constexpr int kRetry2 = 11;  // queued for the global-ring pass (pass 3)
 constexpr int kRetryGen = 12;  // handed to the general kernel (replay_batch_kernel)
-constexpr int kRetry3 = 13;    // overlay batches: known deep-queue candidates (pass 4)
 
 // segt: the event-time EPOCH (count of distinct event times so far) of the
 // device's last arrival segment -- a time-independent stand-in for "the
 // arrivals at the current t", exact for any time unit.
 struct __align__(16) DevF {
   uint32_t head, tail, tsort, segbeg;
-  uint32_t zlo, zhi, segt, pad;
+  uint32_t zlo, zhi, segt, qoff;  // qoff: the device's offset in qbuf (devoff)
   uint32_t busy_lo, busy_hi;  // summed dur of the dispatched ops (64-bit)
   uint32_t isb, ise;          // successor range of the in-flight op
 };
@@ -69,10 +77,40 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
+// shared-memory bytes per device after the counters: the successor range of
+// a lone zero-duration op (its completion round reads it instead of the ring).
+// (Copying the in-flight op's records into a 32-byte slot per device with
+// cp.async at dispatch measured 12 % slower on config 4: the larger CTA
+// leaves too few slots per SM -- profiles/r02_c4_prefetch_ab.log.)
+// Per-op outputs (start, end, device-queue order) are written once and not
+// read again by the replay: streaming stores (evict-first in L2), so they do
+// not push the rings, counters and shared base records out of L2.
+#ifdef DPRO_PLAIN_STORES
+template <typename T, typename V>
+__device__ __forceinline__ void st_out(T* p, V v) { *p = static_cast<T>(v); }
+#else
+__device__ __forceinline__ void st_out(long long* p, unsigned long long v) {
+  __stcs(p, static_cast<long long>(v));
+}
+__device__ __forceinline__ void st_out(long long* p, long long v) { __stcs(p, v); }
+__device__ __forceinline__ void st_out(uint32_t* p, uint32_t v) { __stcs(p, v); }
+#endif
+
+#ifdef DPRO_NO_ZR
+constexpr uint32_t kTailBytesPerDev = 0;  // A/B builds: zero rounds read the ring
+#else
+constexpr uint32_t kTailBytesPerDev = 8;
+#endif
+
 #ifndef DPRO_MLP
 #define DPRO_MLP 1
 #endif
 constexpr int kMlp = DPRO_MLP;  // record loads in flight per lane in expand()
+#ifdef DPRO_NO_LANE_EXPAND
+constexpr bool kLaneExpand = false;  // A/B builds: always the scan expansion
+#else
+constexpr bool kLaneExpand = true;
+#endif
 
 // misc words: [0],[2] range counts (double-buffered by round parity),
 // [1] overflow, [4, 4+NT) per-thread dirty masks, then 4*NW words of
@@ -203,9 +241,10 @@ struct OvCand {
   uint32_t n_cnt, n_src, first_missing, pad;
   uint32_t n_sx, n_sbp, ovmin, sparse;
 };
-// shared memory for the sparse lists (64 + 64 pairs)
-constexpr uint32_t kOvListBytes = 1024;
-constexpr uint32_t kOvListMax = 64;
+// shared memory for the sparse lists (48 + 48 pairs: config 4's residency
+// pass fits 15 CTAs per SM)
+constexpr uint32_t kOvListMax = 48;
+constexpr uint32_t kOvListBytes = 2 * 8 * kOvListMax;
 
 // The resident base's packed layout (overlay batches).
 struct OvBase {
@@ -239,6 +278,7 @@ struct FastWarp {
   unsigned long long tmax = 0;
   bool wide = false;  // u16 counters (some in-degree >= 255)
   uint4* last = nullptr;        // OV: [dcap] each device's latest arrival (shared memory)
+  uint2* zr = nullptr;          // [dcap] successor range of a lone zero-duration op
   const uint2* sxs = nullptr;   // OV sparse lists in shared memory
   const uint2* sbps = nullptr;
   uint32_t n_sx = 0, n_sbp = 0, ovmin = 0;
@@ -248,8 +288,12 @@ struct FastWarp {
 
   volatile uint32_t* rlc = nullptr;  // this round's range counter
 
+  // The range counter's high bits count the ranges of more than 2 records:
+  // while there are none, expand() gives every thread its own ranges.
+  static constexpr uint32_t kRlLong = 1u << 20;
   __device__ __forceinline__ void push_range(uint32_t sb, uint32_t n) {
-    const uint32_t p = atomicAdd(const_cast<uint32_t*>(rlc), 1u);
+    const uint32_t p =
+        atomicAdd(const_cast<uint32_t*>(rlc), n > 2u ? 1u + kRlLong : 1u) & (kRlLong - 1u);
     if (p < rlcap)
       rl[p] = make_uint2(sb, n);
     else
@@ -308,8 +352,8 @@ struct FastWarp {
     else se = __ldg(&rec[(a.x & kOpMask) + 1].w);
     if (a.z & kFVirt) {  // multi-predecessor virtual: completes now, cascade
       if (want) {
-        start[s] = t;
-        end[s] = t;
+        st_out(start + s, t);
+        st_out(end + s, t);
       }
       ++vcount;
       tmax = max(tmax, t);
@@ -338,8 +382,8 @@ struct FastWarp {
     const uint32_t s = resolve(a);
     if ((a.z & (kFVirt | kFMulti)) == kFVirt) {  // spliced single-pred virtual
       if (want) {
-        start[s] = t;
-        end[s] = t;
+        st_out(start + s, t);
+        st_out(end + s, t);
       }
       ++vcount;
       tmax = max(tmax, t);
@@ -360,6 +404,11 @@ struct FastWarp {
     ready(a, t, s);
   }
 
+  __device__ __forceinline__ uint4 record(uint32_t sb, uint32_t k) const {
+    if (OV && (sb & kOvF)) return __ldg(ov.erec + (sb & ~kOvF) + k);
+    return __ldg(erec + sb + k);
+  }
+
   // Expands every range pushed this round (and the virtual cascades they
   // trigger) with all 32 lanes: the round's out-edge records are loaded and
   // applied in parallel instead of one lane walking each list.
@@ -370,10 +419,28 @@ struct FastWarp {
   __device__ __forceinline__ uint32_t expand(unsigned long long t) {
     uint32_t lo = 0;
     for (;;) {
-      const uint32_t hi = *rlc;
+      const uint32_t rc = *rlc;
+      const uint32_t hi = rc & (kRlLong - 1u);
       if (misc[1]) return bail_code(misc[1]);
       if (hi > rlcap) return kBailRl;
       if (lo == hi) return kDone;
+      if (kLaneExpand && rc < kRlLong) {
+        // every range has <= 2 records (config 4: no op has more than 2
+        // successors): each thread loads and applies its own ranges, no scan
+        for (uint32_t r = lo + tid; r < hi; r += NT) {
+          const uint2 mine = rl[r];
+          uint4 a0 = make_uint4(0, 0, 0, 0), a1 = a0;
+          if (mine.y) a0 = record(mine.x, 0);
+          if (mine.y > 1u) a1 = record(mine.x, 1);
+          if (mine.y) edge(a0, t);
+          if (mine.y > 1u) edge(a1, t);
+          // (only if the long-range count wrapped: still exact)
+          for (uint32_t k = 2; k < mine.y; ++k) edge(record(mine.x, k), t);
+        }
+        gsync<NW>();
+        lo = hi;
+        continue;
+      }
       for (uint32_t g = lo; g < hi; g += 32) {
         const uint32_t r = g + lane;
         uint2 mine = make_uint2(0u, 0u);
@@ -477,16 +544,18 @@ struct FastWarp {
     if (iend == kT32Inf && head < tail) {
       const uint32_t zlo = head;
       unsigned long long busy = 0;
-      const uint32_t base = devoff[d];
+      const uint32_t base = s.qoff;
       bool infl = false;
+      uint2 z0 = make_uint2(0u, 0u);  // range of the first dispatched op
       while (head < tail) {
         const uint4 x = (lone && head == lone_pos) ? lone_e : r[head & m];
+        if (head == zlo) z0 = make_uint2(x.z, x.w);
         const unsigned long long en = t + x.y;
         if (want) {  // (qpos is derived from qbuf only when K3 needs it)
-          start[x.x] = t;
-          end[x.x] = en;
+          st_out(start + x.x, t);
+          st_out(end + x.x, en);
         }
-        qbuf[base + head] = x.x;
+        st_out(qbuf + base + head, x.x);
         ++head;
         ++dcount;
         busy += x.y;
@@ -508,6 +577,7 @@ struct FastWarp {
       const uint32_t zhi = infl ? head - 1 : head;
       s.zhi = zhi;
       if (zlo < zhi) *zero = true;
+      if (kTailBytesPerDev && zhi - zlo == 1u) zr[d] = z0;  // a lone zero op: its range without a ring read
     }
     return iend;
   }
@@ -527,7 +597,7 @@ __device__ unsigned long long g_prof[16];
 // Returns kDone, kBailRing (a device queue outgrew its ring or a round its
 // range list: retry with deeper ones) or kBailOther (take the general path).
 template <int NW, int KD, bool OV = false>
-__device__ uint32_t replay_fast(const Cand& c, int cid, const uint4* rec, const uint4* erec,
+__device__ __forceinline__ uint32_t replay_fast(const Cand& c, int cid, const uint4* rec, const uint4* erec,
                             const uint8_t* cnt0, const uint32_t* srcs, const PackInfo& info,
                             unsigned char* wsm, const FastCfg& F, const Scratch& S,
                             const Outs& O, bool want_schedule, uint32_t* gcw,
@@ -554,6 +624,9 @@ __device__ uint32_t replay_fast(const Cand& c, int cid, const uint4* rec, const 
                      want_schedule ? O.start + oo : nullptr,
                      want_schedule ? O.end + oo : nullptr, want_schedule, lane, tid};
   W.wide = info.wide != 0;
+  W.zr = reinterpret_cast<uint2*>(reinterpret_cast<unsigned char*>(
+                                      const_cast<uint32_t*>(misc) + fast_misc_words(NW)) +
+                                  F.ccap + (OV ? kOvListBytes + 16 * F.dcap : 0u));
 
   // ---- state init ----
   if constexpr (OV) {
@@ -589,7 +662,8 @@ __device__ uint32_t replay_fast(const Cand& c, int cid, const uint4* rec, const 
   for (uint32_t d = tid; d < D; d += NT) {
     DevF z;
     z.head = z.tail = z.tsort = z.segbeg = 0;
-    z.zlo = z.zhi = z.segt = z.pad = 0;
+    z.zlo = z.zhi = z.segt = 0;
+    z.qoff = __ldg(W.devoff + d);
     z.busy_lo = z.busy_hi = z.isb = z.ise = 0;
     dv[d] = z;
   }
@@ -677,10 +751,16 @@ __device__ uint32_t replay_fast(const Cand& c, int cid, const uint4* rec, const 
         DevF& s = dv[tid + NT * j];
         const uint4* r = W.ring(tid + NT * j);
         const uint32_t zh = s.zhi;
-        for (uint32_t p = s.zlo; p < zh; ++p) {
-          const uint4 e = r[p & (F.qc - 1)];
-          const uint32_t eb = e.z & ~kOvF;
-          if (e.w > eb) W.push_range(e.z, e.w - eb);
+        if (kTailBytesPerDev && zh - s.zlo == 1u) {
+          const uint2 e = W.zr[tid + NT * j];
+          const uint32_t eb = e.x & ~kOvF;
+          if (e.y > eb) W.push_range(e.x, e.y - eb);
+        } else {
+          for (uint32_t p = s.zlo; p < zh; ++p) {
+            const uint4 e = r[p & (F.qc - 1)];
+            const uint32_t eb = e.z & ~kOvF;
+            if (e.w > eb) W.push_range(e.z, e.w - eb);
+          }
         }
         *reinterpret_cast<volatile uint32_t*>(&s.zlo) = zh;
       }
@@ -701,7 +781,7 @@ __device__ uint32_t replay_fast(const Cand& c, int cid, const uint4* rec, const 
     gsync<NW>();
     PROF_T(p2);
 #ifdef DPRO_PROFILE
-    const uint32_t nranges = *W.rlc;
+    const uint32_t nranges = *W.rlc & (W.kRlLong - 1u);
 #endif
     if (const uint32_t bail = W.expand(t)) return bail;
     PROF_T(p3);
@@ -757,7 +837,7 @@ __device__ uint32_t replay_fast(const Cand& c, int cid, const uint4* rec, const 
 // work: [0] pass-0 counter, [1] general fallbacks, [2] pass-1 counter,
 // [3] deep-ring retries.
 template <int NW, int KD>
-__global__ void __launch_bounds__(32 * NW) replay_fast_kernel(
+__global__ void DPRO_FAST_BOUNDS(NW, KD) replay_fast_kernel(
     const Cand* __restrict__ cands, int n_cands, Scratch S, Outs O, PackOut P,
     FastCfg F, int want_schedule, unsigned* work, int pass) {
   extern __shared__ __align__(16) unsigned char fsm[];
@@ -820,12 +900,13 @@ __global__ void __launch_bounds__(32 * NW) replay_fast_kernel(
 // marked kRetryMat: the host re-runs them through the materialized path.
 constexpr int kRetryMat = 10;
 
-// pass 4: candidates a previous replay of the batch sent to the global-ring
-// pass (status preset to kRetry3), run first on a side stream so they
+// pass 4: candidates flagged in order[n_cands + cid] (whole-graph rewrites,
+// or sent to the global-ring pass by a previous replay), run first on a side
+// stream with global rings so they
 // overlap the residency pass instead of trailing it; hint[] records the
 // candidates that reach the global-ring pass (count in work[11]).
 template <int NW, int KD>
-__global__ void __launch_bounds__(32 * NW) replay_ov_kernel(
+__global__ void DPRO_FAST_BOUNDS(NW, KD) replay_ov_kernel(
     const Cand* __restrict__ cands, const OvCand* __restrict__ ovc, int n_cands, OvBase base,
     Scratch S, Outs O, uint8_t* gcnt, FastCfg F, int want_schedule, unsigned* work, int pass,
     unsigned* hint, const unsigned* order) {
@@ -842,10 +923,11 @@ __global__ void __launch_bounds__(32 * NW) replay_ov_kernel(
     const int cid = s_cid;
     __syncthreads();
     if (cid >= n_cands) break;
-    if (pass == 0 && O.status[cid] == kRetry3) continue;
+    const bool side = order[n_cands + cid] != 0u;
+    if (pass == 0 && side) continue;
     if (pass == 1 && O.status[cid] != kRetry) continue;
     if (pass == 3 && O.status[cid] != kRetry2) continue;
-    if (pass == 4 && O.status[cid] != kRetry3) continue;
+    if (pass == 4 && !side) continue;
     const Cand c = cands[cid];
     const OvCand oc = ovc[cid];
     if (oc.pad) continue;  // materialized path (host)
