@@ -2549,9 +2549,7 @@ dpro_batch* dpro_cuda_batch_create_tsync(dpro_ctx* ctx, const dpro_cluster_desc*
       return nullptr;
     }
   cudaSetDevice(ctx->device);
-  auto* b = new dpro_batch;
-  b->n = n;
-  b->memspace = DPRO_DEVICE;
+  dpro_batch* b = acquire_batch(ctx, n, DPRO_DEVICE);
   if (build_tsync_batch(ctx, b, *cluster, std::vector<int64_t>(bytes, bytes + n),
                         std::vector<int32_t>(k, k + n)) != DPRO_OK) {
     delete b;
@@ -2582,19 +2580,20 @@ int dpro_cuda_tsync_grid(dpro_ctx* ctx, const dpro_cluster_desc* cluster,
     }
     if (idx.empty()) return DPRO_OK;
     cudaSetDevice(ctx->device);
-    dpro_batch b;
-    b.n = static_cast<int32_t>(idx.size());
-    st = build_tsync_batch(ctx, &b, *cluster, bb, kk);
-    if (st == DPRO_OK) st = dpro_cuda_batch_replay(ctx, &b, 0);
+    // a recycled batch (ctx->spare): repeated small grids (the greedy
+    // search's opt_part_num) reuse its device buffers instead of allocating
+    dpro_batch* b = acquire_batch(ctx, static_cast<int32_t>(idx.size()), DPRO_DEVICE);
+    st = build_tsync_batch(ctx, b, *cluster, bb, kk);
+    if (st == DPRO_OK) st = dpro_cuda_batch_replay(ctx, b, 0);
     std::vector<int64_t> ms(idx.size()), er(idx.size());
     std::vector<int32_t> ss(idx.size());
     if (st == DPRO_OK)
-      st = dpro_cuda_batch_results(ctx, &b, ms.data(), ss.data(), er.data(), nullptr, nullptr);
+      st = dpro_cuda_batch_results(ctx, b, ms.data(), ss.data(), er.data(), nullptr, nullptr);
     for (size_t j = 0; j < idx.size(); ++j) {
       out[idx[j]] = st == DPRO_OK ? ms[j] : 0;
       if (status) status[idx[j]] = st == DPRO_OK ? ss[j] : st;
     }
-    cudaStreamSynchronize(ctx->stream);
+    dpro_cuda_batch_destroy(ctx, b);  // synchronizes; keeps it as the spare
     return st;
   }
   std::vector<dpro_graph*> graphs(n, nullptr);

@@ -5,6 +5,7 @@ consumes. GlobalDFG keeps ops in byte-lexicographic id order
 the CSR the C ABI takes (include/dpro_cuda.h: dpro_csr)."""
 from __future__ import annotations
 
+import bisect
 import enum
 import math
 from dataclasses import dataclass, field
@@ -211,6 +212,10 @@ def base_of_unit_name(name: str) -> str:
 # --------------------------------------------------------------------------
 # GlobalDFG / GraphBuilder (graph.hpp:106-202)
 # --------------------------------------------------------------------------
+def _op_id(op: "Op") -> str:
+    return op.id
+
+
 class _CsrLists:
     """Per-op index lists held as one CSR (flat, off): list i is sliced out
     on access, so building a graph creates no per-op lists."""
@@ -251,11 +256,23 @@ class GlobalDFG:
     def _preds(self) -> list[list[int]]:
         # ascending: successors are visited in index order
         if self._preds_cache is None:
-            preds: list[list[int]] = [[] for _ in self._ops]
-            for a, ss in enumerate(self._succs):
-                for b in ss:
-                    preds[b].append(a)
-            self._preds_cache = preds
+            sc = self._succs
+            if isinstance(sc, _CsrLists):
+                # the transpose of the successor CSR: a stable sort of the
+                # heads keeps each predecessor list ascending
+                n = len(self._ops)
+                flat = np.asarray(sc.flat_np, np.int64)
+                tails = np.repeat(np.arange(n, dtype=np.int64), np.diff(sc.off_np))
+                order = np.argsort(flat, kind="stable")
+                off = np.zeros(n + 1, np.int64)
+                np.cumsum(np.bincount(flat, minlength=n), out=off[1:])
+                self._preds_cache = _CsrLists(tails[order], off)
+            else:
+                preds: list[list[int]] = [[] for _ in self._ops]
+                for a, ss in enumerate(sc):
+                    for b in ss:
+                        preds[b].append(a)
+                self._preds_cache = preds
         return self._preds_cache
 
     def size(self) -> int:
@@ -336,6 +353,56 @@ class GlobalDFG:
         if not units:
             raise LookupError_(f"no tensor '{base}' in graph")
         return sum(u.bytes for u in units)
+
+    def fused(self, a: int, b: int, op: Op) -> "GlobalDFG":
+        """The graph with ops a and b (indices) replaced by op, which takes
+        their predecessors and successors (other than a and b): what
+        GraphBuilder(g).remove_ops([a, b]); add_op(op); add_edge(...)
+        builds for op fusion (optimize.cpp:245-317), computed on the index
+        arrays instead of string-keyed edge sets. op must be on the device
+        of a (fusion joins two ops of one device)."""
+        ops, n = self._ops, len(self._ops)
+        lo, hi = (a, b) if a < b else (b, a)
+        keep = ops[:lo] + ops[lo + 1:hi] + ops[hi + 1:]
+        pos = bisect.bisect_left(keep, op.id, key=_op_id)
+        new_ops = keep[:pos] + [op] + keep[pos:]
+        m = np.arange(n, dtype=np.int64)
+        m -= (m > lo).astype(np.int64) + (m > hi)
+        m += m >= pos
+        sc = self._succs
+        if isinstance(sc, _CsrLists):
+            heads = np.asarray(sc.flat_np, np.int64)
+            tails = np.repeat(np.arange(n, dtype=np.int64), np.diff(sc.off_np))
+        else:
+            heads = np.fromiter((x for ss in sc for x in ss), np.int64, self._edge_count)
+            tails = np.repeat(np.arange(n, dtype=np.int64), [len(ss) for ss in sc])
+        gone = (tails == a) | (tails == b)
+        into = (heads == a) | (heads == b)
+        preds = np.unique(tails[into & ~gone])
+        succs = np.unique(heads[gone & ~into])
+        keep_e = ~(gone | into)
+        n2 = n - 1
+        key = np.concatenate([m[tails[keep_e]] * n2 + m[heads[keep_e]],
+                              m[preds] * n2 + pos, pos * n2 + m[succs]])
+        key.sort()
+        off = np.zeros(n2 + 1, np.int64)
+        np.cumsum(np.bincount(key // n2, minlength=n2), out=off[1:])
+        g = GlobalDFG(new_ops, _CsrLists(key % n2, off), self._tensors, self._cluster,
+                      {o.id: i for i, o in enumerate(new_ops)}, int(key.size))
+        if self._csr is not None:
+            c = self._csr
+            dindex = {d: i for i, d in enumerate(c["devices"])}
+            if op.device in dindex:
+                fl = (1 if is_virtual(op.kind) else 0) | (2 if is_communication(op.kind) else 0)
+                succ = (key % n2).astype(np.uint32)
+                g._csr = {"dur": np.insert(np.delete(c["dur"], [lo, hi]), pos, op.dur),
+                          "dev": np.insert(np.delete(c["dev"], [lo, hi]), pos,
+                                           dindex[op.device]),
+                          "flags": np.insert(np.delete(c["flags"], [lo, hi]), pos, fl),
+                          "succ_off": off.astype(np.uint32), "succ": succ,
+                          "indeg": np.bincount(succ, minlength=n2).astype(np.uint32),
+                          "devices": c["devices"], "n_devices": c["n_devices"]}
+        return g
 
     # ---- CSR for the engine -------------------------------------------
     def devices(self) -> list[DeviceId]:

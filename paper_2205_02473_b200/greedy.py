@@ -25,7 +25,8 @@ from dataclasses import dataclass, field
 from .errors import Error
 from .graph import GlobalDFG, OpKind, is_computation
 from .memory import ModelMeta
-from .replay import critical_path, execution_graph, replay, replay_times, sync_makespan
+from .replay import (critical_path, execution_graph, replay, replay_times,
+                     sync_makespan_grid)
 from .rewrite import (CostModel, Strategy, StrategyKind, apply_op_fusion, apply_strategy,
                       apply_tensor_fusion, apply_tensor_partition, fused_op_id, local_part,
                       memory_pass, topo_order)
@@ -152,7 +153,15 @@ class _Ctx:
     def sync(self, nbytes: int, k: int) -> int:
         key = (int(nbytes), int(k))
         if key not in self.cache:
-            self.cache[key] = sync_makespan(self.cluster, key[0], key[1])
+            # t_sync is a pure function of (bytes, k): a miss fills the
+            # whole row k = 1..kmax (what opt_part_num asks next) in one
+            # K2 grid launch instead of one launch per k
+            ks = sorted({key[1]} | set(range(1, max(1, min(int(self.opt.kmax), key[0])) + 1)))
+            ks = [x for x in ks if (key[0], x) not in self.cache]
+            if key[1] < 1:
+                ks = [key[1]]  # the reference's error, raised by the grid
+            vals = sync_makespan_grid(self.cluster, [key[0]] * len(ks), ks)
+            self.cache.update({(key[0], x): v for x, v in zip(ks, vals)})
         return self.cache[key]
 
 

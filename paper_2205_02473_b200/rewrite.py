@@ -150,26 +150,30 @@ def apply_op_fusion(g: GlobalDFG, a: str, b: str, cost: CostModel | None = None,
         raise TransformError(f"ops {a} and {b} run on different devices")
     if not g.has_edge(a, b):
         raise TransformError(f"op fusion requires a direct edge {a} -> {b}")
-    parent: dict[str, str] = {}
+    # second path a -> ... -> b: breadth-first over successor indices
+    # (ascending index == id order, so the witness is the id-order BFS's)
+    ia, ib = g.index_of(a), g.index_of(b)
+    parent: dict[int, int] = {}
     frontier = deque()
-    for s in g.succs(a):
-        if s == b:
+    for s in g.succ_indices(ia):
+        if s == ib:
             continue
         if s not in parent:
-            parent[s] = a
+            parent[s] = ia
         frontier.append(s)
     while frontier:
         cur = frontier.popleft()
-        if cur == b:
-            witness = [b]
-            x = parent[b]
-            while x != a:
+        if cur == ib:
+            witness = [ib]
+            x = parent[ib]
+            while x != ia:
                 witness.append(x)
                 x = parent[x]
-            witness.append(a)
+            witness.append(ia)
             witness.reverse()
-            raise CycleError(f"fusing {a} and {b} would create a cycle", witness)
-        for s in g.succs(cur):
+            raise CycleError(f"fusing {a} and {b} would create a cycle",
+                             [g.op_at(i).id for i in witness])
+        for s in g.succ_indices(cur):
             if s not in parent:
                 parent[s] = cur
                 frontier.append(s)
@@ -177,16 +181,9 @@ def apply_op_fusion(g: GlobalDFG, a: str, b: str, cost: CostModel | None = None,
     fused.id = fused_op_id(a, b)
     fused.dur = dur_us_override if dur_us_override >= 0 else round_us(cost.fused_dur_us(oa, ob))
     fused.produces = list(oa.produces) + list(ob.produces)
-    preds = (set(g.preds(a)) | set(g.preds(b))) - {a, b}
-    succs = (set(g.succs(a)) | set(g.succs(b))) - {a, b}
-    bld = GraphBuilder(g)
-    bld.remove_ops([a, b])
-    bld.add_op(fused)
-    for p in preds:
-        bld.add_edge(p, fused.id)
-    for t in succs:
-        bld.add_edge(fused.id, t)
-    return bld.build()
+    if g.has_op(fused.id) and fused.id not in (a, b):
+        raise TransformError(f"duplicate op id '{fused.id}'")
+    return g.fused(ia, ib, fused)
 
 
 def splice_topology(bld: GraphBuilder, topo: CommTopology, base: str, part_index: int,
