@@ -82,6 +82,43 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
 // (Copying the in-flight op's records into a 32-byte slot per device with
 // cp.async at dispatch measured 12 % slower on config 4: the larger CTA
 // leaves too few slots per SM -- profiles/r02_c4_prefetch_ab.log.)
+// 1-D bulk copies global -> shared memory on the TMA engine (no tensor map:
+// cp.async.bulk), completing on an mbarrier: the candidate's contiguous
+// counter image and sparse overlay lists at candidate start. One thread arms
+// the barrier with the byte count and issues the copies; every thread waits
+// on the barrier's phase. Addresses and sizes are multiples of 16 bytes.
+struct BulkBar {
+  uint64_t* bar;   // shared-memory mbarrier (arrival count 1)
+  uint32_t phase;  // parity of the next completion
+};
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void bulk_bar_init(uint64_t* bar) {
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+}
+// thread 0 only: arm with the total bytes of the copies that follow
+__device__ __forceinline__ void bulk_arm(BulkBar& b, uint32_t bytes) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // after generic smem use
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b.bar)),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, BulkBar& b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(b.bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_wait(BulkBar& b) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(b.bar)), "r"(b.phase) : "memory");
+  b.phase ^= 1u;
+}
+
 // Per-op outputs (start, end, device-queue order) are written once and not
 // read again by the replay: streaming stores (evict-first in L2), so they do
 // not push the rings, counters and shared base records out of L2.
@@ -601,7 +638,8 @@ __device__ __forceinline__ uint32_t replay_fast(const Cand& c, int cid, const ui
                             const uint8_t* cnt0, const uint32_t* srcs, const PackInfo& info,
                             unsigned char* wsm, const FastCfg& F, const Scratch& S,
                             const Outs& O, bool want_schedule, uint32_t* gcw,
-                            const OvCand* ovc = nullptr, const OvBase* ob = nullptr) {
+                            const OvCand* ovc = nullptr, const OvBase* ob = nullptr,
+                            BulkBar* bb = nullptr) {
   constexpr uint32_t NT = 32u * NW;
   const int lane = threadIdx.x & 31;
   const int tid = threadIdx.x;
@@ -635,11 +673,21 @@ __device__ __forceinline__ uint32_t replay_fast(const Cand& c, int cid, const ui
     W.wide = true;
     W.last = reinterpret_cast<uint4*>(reinterpret_cast<char*>(
                  const_cast<uint32_t*>(misc) + fast_misc_words(NW)) + F.ccap + kOvListBytes);
-    if (ovc->sparse) {  // sparse lists after the counter region
+    if (ovc->sparse) {  // sparse lists after the counter region (bulk copies)
       uint2* sl = reinterpret_cast<uint2*>(reinterpret_cast<char*>(
                       const_cast<uint32_t*>(misc) + fast_misc_words(NW)) + F.ccap);
-      for (uint32_t i = tid; i < ovc->n_sx; i += NT) sl[i] = __ldg(ovc->sx + i);
-      for (uint32_t i = tid; i < ovc->n_sbp; i += NT) sl[kOvListMax + i] = __ldg(ovc->sbp + i);
+      const uint32_t bx = (8u * ovc->n_sx + 15u) & ~15u, bp = (8u * ovc->n_sbp + 15u) & ~15u;
+      if (!bb) {
+        for (uint32_t i = tid; i < ovc->n_sx; i += NT) sl[i] = __ldg(ovc->sx + i);
+        for (uint32_t i = tid; i < ovc->n_sbp; i += NT) sl[kOvListMax + i] = __ldg(ovc->sbp + i);
+      } else if (bx + bp) {
+        if (tid == 0) {
+          bulk_arm(*bb, bx + bp);
+          if (bx) bulk_g2s(sl, ovc->sx, bx, *bb);
+          if (bp) bulk_g2s(sl + kOvListMax, ovc->sbp, bp, *bb);
+        }
+        bulk_wait(*bb);
+      }
       W.sxs = sl;
       W.sbps = sl + kOvListMax;
       W.n_sx = ovc->n_sx;
@@ -657,7 +705,15 @@ __device__ __forceinline__ uint32_t replay_fast(const Cand& c, int cid, const ui
     const uint32_t nv = ((info.wide ? 2u : 1u) * info.n_cnt + 15) / 16;
     const uint4* src = reinterpret_cast<const uint4*>(cnt0);
     uint4* dst = reinterpret_cast<uint4*>(cw);
-    for (uint32_t i = tid; i < nv; i += NT) dst[i] = __ldg(src + i);
+    if (gcw || !bb) {  // global counter slice: a plain copy
+      for (uint32_t i = tid; i < nv; i += NT) dst[i] = __ldg(src + i);
+    } else if (nv) {  // the counter image into shared memory: one bulk copy
+      if (tid == 0) {
+        bulk_arm(*bb, 16u * nv);
+        bulk_g2s(dst, src, 16u * nv, *bb);
+      }
+      bulk_wait(*bb);
+    }
   }
   for (uint32_t d = tid; d < D; d += NT) {
     DevF z;
@@ -842,6 +898,9 @@ __global__ void DPRO_FAST_BOUNDS(NW, KD) replay_fast_kernel(
     FastCfg F, int want_schedule, unsigned* work, int pass) {
   extern __shared__ __align__(16) unsigned char fsm[];
   __shared__ int s_cid;
+  __shared__ uint64_t s_bar;
+  bulk_bar_init(&s_bar);
+  BulkBar bb{&s_bar, 0u};
   // counters: [0] passes 0 and 2, [2] pass 1, [4] pass 3
   unsigned* counter = work + (pass == 1 ? 2 : pass == 3 ? 4 : 0);
   for (;;) {
@@ -876,7 +935,8 @@ __global__ void DPRO_FAST_BOUNDS(NW, KD) replay_fast_kernel(
           P.srcs + c.op_off, info, fsm, F, S, O, want_schedule != 0,
           (info.wide ? 2u : 1u) * info.n_cnt <= F.ccap
               ? nullptr
-              : reinterpret_cast<uint32_t*>(P.gcnt + P.c_off[cid]));
+              : reinterpret_cast<uint32_t*>(P.gcnt + P.c_off[cid]),
+          nullptr, nullptr, &bb);
     __syncthreads();
     if ((rc == kBailRing || rc == kBailRl) && (pass == 0 || pass == 1)) {
       if (threadIdx.x == 0) {
@@ -912,6 +972,9 @@ __global__ void DPRO_FAST_BOUNDS(NW, KD) replay_ov_kernel(
     unsigned* hint, const unsigned* order) {
   extern __shared__ __align__(16) unsigned char fsm[];
   __shared__ int s_cid;
+  __shared__ uint64_t s_bar;
+  bulk_bar_init(&s_bar);
+  BulkBar bb{&s_bar, 0u};
   unsigned* counter = work + (pass == 1 ? 2 : pass == 3 ? 4 : pass == 4 ? 10 : 0);
   for (;;) {
     if (threadIdx.x == 0) {
@@ -947,7 +1010,8 @@ __global__ void DPRO_FAST_BOUNDS(NW, KD) replay_ov_kernel(
       rc = replay_fast<NW, KD, true>(
           c, cid, base.rec, base.erec, nullptr, nullptr, info, fsm, F, S, O,
           want_schedule != 0,
-          nc2 <= F.ccap ? nullptr : reinterpret_cast<uint32_t*>(gcnt + oc.gcnt_off), &oc, &base);
+          nc2 <= F.ccap ? nullptr : reinterpret_cast<uint32_t*>(gcnt + oc.gcnt_off), &oc, &base,
+          &bb);
     __syncthreads();
     if (threadIdx.x == 0) {
       if ((rc == kBailRing || rc == kBailRl) && (pass == 0 || pass == 1)) {
