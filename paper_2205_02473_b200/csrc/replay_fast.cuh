@@ -42,6 +42,12 @@ constexpr uint32_t kT32Inf = 0xFFFFFFFFu;
 #else
 #define DPRO_FAST_BOUNDS(NW, KD) __launch_bounds__(32 * NW)
 #endif
+// The overlay kernel holds the in-flight ops' records in registers
+// (kRegPrefetch): a bound of 12 CTAs of 2 warps per SM (85 registers) keeps
+// them out of local memory -- 1,780-1,798 vs 1,647-1,676 replays/s unbounded
+// (72 registers + spills) and 1,704-1,742 without the prefetch
+// (profiles/r02_c4_regprefetch_ab.log).
+#define DPRO_OV_BOUNDS(NW, KD) __launch_bounds__(32 * NW, (KD <= 5 ? 24 : 16) / NW)
 // replay_fast outcomes / bail-out causes
 constexpr uint32_t kDone = 0, kBailRing = 1, kBailOther = 2, kBailRl = 3;
 constexpr uint32_t kMiscRl = 4;  // misc[1] bit: a round's range list overflowed
@@ -143,6 +149,13 @@ constexpr uint32_t kTailBytesPerDev = 8;
 #define DPRO_MLP 1
 #endif
 constexpr int kMlp = DPRO_MLP;  // record loads in flight per lane in expand()
+#ifdef DPRO_NO_REG_PREFETCH
+constexpr bool kRegPrefetch = false;  // A/B builds: completions push ranges
+#else
+constexpr bool kRegPrefetch = true;
+#endif
+constexpr uint32_t kNoPre = 0xFFu;
+
 #ifdef DPRO_NO_LANE_EXPAND
 constexpr bool kLaneExpand = false;  // A/B builds: always the scan expansion
 #else
@@ -546,7 +559,8 @@ struct FastWarp {
   // zero-duration ops ran (they complete next round). epoch: number of
   // distinct event times so far.
   __device__ __forceinline__ uint32_t dispatch_dev(uint32_t d, unsigned long long t,
-                                                   uint32_t epoch, uint32_t iend, bool* zero) {
+                                                   uint32_t epoch, uint32_t iend, bool* zero,
+                                                   uint4& p0, uint4& p1, uint32_t& pn) {
     DevF& s = dv[d];
     uint4* r = ring(d);
     const uint32_t tail = *reinterpret_cast<volatile uint32_t*>(&s.tail);
@@ -602,6 +616,19 @@ struct FastWarp {
           s.ise = x.w;
           iend = x.y;
           infl = true;
+          if (kRegPrefetch && OV) {
+            // the in-flight op's out-edge records (<= 2) are loaded into the
+            // owner's registers now and applied by the owner when it
+            // completes (a later round): no record load on that round's path
+            const uint32_t ne = x.w - (x.z & ~kOvF);
+            if (ne <= 2u) {
+              if (ne) p0 = record(x.z, 0);
+              if (ne == 2u) p1 = record(x.z, 1);
+              pn = ne;
+            } else {
+              pn = kNoPre;
+            }
+          }
           break;
         }
       }
@@ -762,14 +789,18 @@ __device__ __forceinline__ uint32_t replay_fast(const Cand& c, int cid, const ui
 
   // ---- dispatch(0) + event loop (replay.cpp:95-106) ----
   uint32_t iend[KD];  // in-flight end - t per owned device (kT32Inf: idle)
+  uint4 pr0[KD], pr1[KD];  // the in-flight op's out-edge records (kRegPrefetch)
+  uint32_t prn[KD];        // their count, kNoPre: push the range instead
   uint32_t zmask = 0, epoch = 0;
 #pragma unroll
   for (int j = 0; j < KD; ++j) {
     iend[j] = kT32Inf;
+    prn[j] = kNoPre;
+    pr0[j] = pr1[j] = make_uint4(0, 0, 0, 0);
     const uint32_t d = tid + NT * j;
     if (d < D) {
       bool z = false;
-      iend[j] = W.dispatch_dev(d, 0ull, 0u, kT32Inf, &z);
+      iend[j] = W.dispatch_dev(d, 0ull, 0u, kT32Inf, &z, pr0[j], pr1[j], prn[j]);
       if (z) zmask |= 1u << j;
     }
   }
@@ -827,10 +858,15 @@ __device__ __forceinline__ uint32_t replay_fast(const Cand& c, int cid, const ui
         if (iend[j] == 0u) {
           iend[j] = kT32Inf;
           freed |= 1u << j;
-          const DevF& sd = dv[tid + NT * j];
-          const uint32_t ez = sd.isb, ew = sd.ise;
-          const uint32_t eb = ez & ~kOvF;
-          if (ew > eb) W.push_range(ez, ew - eb);
+          if (kRegPrefetch && OV && prn[j] != kNoPre) {  // records already in registers
+            if (prn[j]) W.edge(pr0[j], t);
+            if (prn[j] == 2u) W.edge(pr1[j], t);
+          } else {
+            const DevF& sd = dv[tid + NT * j];
+            const uint32_t ez = sd.isb, ew = sd.ise;
+            const uint32_t eb = ez & ~kOvF;
+            if (ew > eb) W.push_range(ez, ew - eb);
+          }
         }
       }
     }
@@ -847,7 +883,7 @@ __device__ __forceinline__ uint32_t replay_fast(const Cand& c, int cid, const ui
     for (int j = 0; j < KD; ++j) {
       if (todo & (1u << j)) {
         bool z = false;
-        iend[j] = W.dispatch_dev(tid + NT * j, t, epoch, iend[j], &z);
+        iend[j] = W.dispatch_dev(tid + NT * j, t, epoch, iend[j], &z, pr0[j], pr1[j], prn[j]);
         if (z) zmask |= 1u << j;
       }
     }
@@ -966,7 +1002,7 @@ constexpr int kRetryMat = 10;
 // overlap the residency pass instead of trailing it; hint[] records the
 // candidates that reach the global-ring pass (count in work[11]).
 template <int NW, int KD>
-__global__ void DPRO_FAST_BOUNDS(NW, KD) replay_ov_kernel(
+__global__ void DPRO_OV_BOUNDS(NW, KD) replay_ov_kernel(
     const Cand* __restrict__ cands, const OvCand* __restrict__ ovc, int n_cands, OvBase base,
     Scratch S, Outs O, uint8_t* gcnt, FastCfg F, int want_schedule, unsigned* work, int pass,
     unsigned* hint, const unsigned* order) {
