@@ -170,6 +170,15 @@ __host__ __device__ constexpr size_t fast_misc_words(int nw) {
   return (4 + 32 * nw + 4 * nw + 3) & ~size_t(3);
 }
 
+// threadIdx.x read once per candidate through an opaque move: ptxas otherwise
+// re-reads the special register (S2R) and rebuilds every tid-derived
+// address in the round loop when registers are tight (profiles/r02_c4_*).
+__device__ __forceinline__ uint32_t tid_once() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%tid.x;" : "=r"(r));
+  return r;
+}
+
 // Group-wide collectives for one candidate replayed by NW warps (one CTA).
 template <int NW>
 __device__ __forceinline__ void gsync() {
@@ -184,12 +193,13 @@ __device__ __forceinline__ bool gany(bool p) {
   return __syncthreads_or(p) != 0;
 }
 template <int NW>
-__device__ __forceinline__ uint32_t gmin(uint32_t v, volatile uint32_t* red, uint32_t& par) {
+__device__ __forceinline__ uint32_t gmin(uint32_t v, volatile uint32_t* red, uint32_t& par,
+                                         uint32_t tid) {
   v = __reduce_min_sync(kFull, v);
   if (NW == 1) return v;
   volatile uint32_t* r = red + (par & 1u) * 2 * NW;  // same buffers as round_head
   ++par;
-  if ((threadIdx.x & 31) == 0) r[threadIdx.x >> 5] = v;
+  if ((tid & 31) == 0) r[tid >> 5] = v;
   __syncthreads();
   uint32_t m = r[0];
 #pragma unroll
@@ -200,7 +210,8 @@ __device__ __forceinline__ uint32_t gmin(uint32_t v, volatile uint32_t* red, uin
 // event time) in ONE barrier. red holds 2 x NW words per parity buffer.
 template <int NW>
 __device__ __forceinline__ void round_head(bool zero, uint32_t lmin, volatile uint32_t* red,
-                                           uint32_t& par, bool& any_zero, uint32_t& tmin) {
+                                           uint32_t& par, bool& any_zero, uint32_t& tmin,
+                                           uint32_t tid) {
   const bool wz = __any_sync(kFull, zero);
   const uint32_t wm = __reduce_min_sync(kFull, lmin);
   if (NW == 1) {
@@ -210,9 +221,9 @@ __device__ __forceinline__ void round_head(bool zero, uint32_t lmin, volatile ui
   }
   volatile uint32_t* r = red + (par & 1u) * 2 * NW;
   ++par;
-  if ((threadIdx.x & 31) == 0) {
-    r[threadIdx.x >> 5] = wz ? 1u : 0u;
-    r[NW + (threadIdx.x >> 5)] = wm;
+  if ((tid & 31) == 0) {
+    r[tid >> 5] = wz ? 1u : 0u;
+    r[NW + (tid >> 5)] = wm;
   }
   __syncthreads();
   bool z = false;
@@ -227,12 +238,13 @@ __device__ __forceinline__ void round_head(bool zero, uint32_t lmin, volatile ui
 }
 
 template <int NW>
-__device__ __forceinline__ uint32_t gsum(uint32_t v, volatile uint32_t* red, uint32_t& par) {
+__device__ __forceinline__ uint32_t gsum(uint32_t v, volatile uint32_t* red, uint32_t& par,
+                                         uint32_t tid) {
   v = __reduce_add_sync(kFull, v);
   if (NW == 1) return v;
   volatile uint32_t* r = red + (par & 1u) * 2 * NW;  // same buffers as round_head
   ++par;
-  if ((threadIdx.x & 31) == 0) r[threadIdx.x >> 5] = v;
+  if ((tid & 31) == 0) r[tid >> 5] = v;
   __syncthreads();
   uint32_t m = 0;
 #pragma unroll
@@ -240,12 +252,13 @@ __device__ __forceinline__ uint32_t gsum(uint32_t v, volatile uint32_t* red, uin
   return m;
 }
 template <int NW>
-__device__ __forceinline__ uint32_t gmax(uint32_t v, volatile uint32_t* red, uint32_t& par) {
+__device__ __forceinline__ uint32_t gmax(uint32_t v, volatile uint32_t* red, uint32_t& par,
+                                         uint32_t tid) {
   v = __reduce_max_sync(kFull, v);
   if (NW == 1) return v;
   volatile uint32_t* r = red + (par & 1u) * 2 * NW;  // same buffers as round_head
   ++par;
-  if ((threadIdx.x & 31) == 0) r[threadIdx.x >> 5] = v;
+  if ((tid & 31) == 0) r[tid >> 5] = v;
   __syncthreads();
   uint32_t m = 0;
 #pragma unroll
@@ -255,9 +268,9 @@ __device__ __forceinline__ uint32_t gmax(uint32_t v, volatile uint32_t* red, uin
 
 template <int NW>
 __device__ __forceinline__ unsigned long long gmax64(unsigned long long v, volatile uint32_t* red,
-                                                     uint32_t& par) {
-  const uint32_t hi = gmax<NW>(static_cast<uint32_t>(v >> 32), red, par);
-  const uint32_t lo = gmax<NW>((v >> 32) == hi ? static_cast<uint32_t>(v) : 0u, red, par);
+                                                     uint32_t& par, uint32_t tid) {
+  const uint32_t hi = gmax<NW>(static_cast<uint32_t>(v >> 32), red, par, tid);
+  const uint32_t lo = gmax<NW>((v >> 32) == hi ? static_cast<uint32_t>(v) : 0u, red, par, tid);
   return (static_cast<unsigned long long>(hi) << 32) | lo;
 }
 
@@ -668,8 +681,8 @@ __device__ __forceinline__ uint32_t replay_fast(const Cand& c, int cid, const ui
                             const OvCand* ovc = nullptr, const OvBase* ob = nullptr,
                             BulkBar* bb = nullptr) {
   constexpr uint32_t NT = 32u * NW;
-  const int lane = threadIdx.x & 31;
-  const int tid = threadIdx.x;
+  const int tid = static_cast<int>(tid_once());
+  const int lane = tid & 31;
   const uint32_t n = c.n, D = c.d;
   DevF* dv = reinterpret_cast<DevF*>(wsm);
   uint4* q = F.gq ? F.gq + size_t(blockIdx.x) * F.dcap * F.qc
@@ -814,7 +827,7 @@ __device__ __forceinline__ uint32_t replay_fast(const Cand& c, int cid, const ui
     for (int j = 0; j < KD; ++j) lmin = min(lmin, iend[j]);
     bool zero_round;
     uint32_t dt;
-    round_head<NW>(zmask != 0, lmin, red, par, zero_round, dt);
+    round_head<NW>(zmask != 0, lmin, red, par, zero_round, dt, tid);
     uint32_t freed = 0;
     if (!zero_round) {
       if (dt == kT32Inf) break;
@@ -897,15 +910,15 @@ __device__ __forceinline__ uint32_t replay_fast(const Cand& c, int cid, const ui
     PROF_ADD(4, p3 - p2);
     PROF_ADD(5, p4 - p3);
     PROF_ADD(6, nranges);
-    const uint32_t ndisp = gsum<NW>(todo != 0 ? 1u : 0u, red, par);
+    const uint32_t ndisp = gsum<NW>(todo != 0 ? 1u : 0u, red, par, tid);
     PROF_ADD(7, ndisp);
 #endif
   }
 
-  const uint32_t vc = gsum<NW>(W.vcount, red, par);
-  const uint32_t dc = gsum<NW>(W.dcount, red, par);
+  const uint32_t vc = gsum<NW>(W.vcount, red, par, tid);
+  const uint32_t dc = gsum<NW>(W.dcount, red, par, tid);
   if (vc + dc != n) return kBailOther;  // cycle: the general path reports it exactly
-  const unsigned long long T = gmax64<NW>(W.tmax, red, par);
+  const unsigned long long T = gmax64<NW>(W.tmax, red, par, tid);
   for (uint32_t d = tid; d < D; d += NT) {
     S.busy[c.dev_off + d] =
         static_cast<long long>((static_cast<unsigned long long>(dv[d].busy_hi) << 32) |
